@@ -1,0 +1,137 @@
+"""Generate golden fixtures by running the REFERENCE package (monoiga) here.
+
+Run in the build container (the reference is mounted read-only):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports ``monoiga`` from /root/reference/pkg/src and writes small
+``.npz`` files next to this script.  Nothing on the GPU box reads the
+reference; tests and the oracle only read these committed fixtures.
+"""
+
+import os
+import sys
+
+import numpy as np
+import scipy.sparse as sp
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from monoiga.assembly import (  # noqa: E402
+    KroneckerOperator, UnivariateMatrices, reaction_mass, spatial_operators, time_matrices)
+from monoiga.bspline import SplineSpace, SpaceTimeSpace  # noqa: E402
+from monoiga.geometry import builtin_geometry  # noqa: E402
+from monoiga.linalg import FastDiagPreconditioner, build_time_pencil, generalized_eig, gmres  # noqa: E402
+from monoiga.stabilization import (  # noqa: E402
+    ResidualIndicator, assemble_stabilization, compute_tau, lowrank_factorize)
+from monoiga.tensorops import kron_chain  # noqa: E402
+from monoiga.solver import _Workspace, MonodomainProblem, FixedPointConfig  # noqa: E402
+from monoiga.assembly import SpatialQuadratureData  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
+
+
+def univariate():
+    out = {}
+    for p in (1, 2, 3, 4):
+        for ne in (1, 3, 5):
+            s = SplineSpace.uniform(p, ne)
+            m = UnivariateMatrices(s)
+            key = "p%d_ne%d" % (p, ne)
+            out[key + "_M"] = m.mass.toarray()
+            out[key + "_K"] = m.stiffness.toarray()
+            out[key + "_W"] = m.advection.toarray()
+            out[key + "_grev"] = s.greville()
+            pts = np.linspace(0, 1, 11)
+            for o in range(min(p, 2) + 1):
+                out[key + "_C%d" % o] = s.collocation_matrix(pts, o).toarray()
+    st = SpaceTimeSpace([SplineSpace.uniform(2, 3)], SplineSpace.uniform(2, 4))
+    Wt, Mt = time_matrices(st, 1.5)
+    out["time_Wt"], out["time_Mt"] = Wt.toarray(), Mt.toarray()
+    tau = compute_tau(SplineSpace.uniform(3, 6))
+    out["tau_p3_ne6_pts"] = np.linspace(0, 1, 13)
+    for k in (1, 2, 3):
+        out["tau_p3_ne6_k%d" % k] = tau.evaluate(k, out["tau_p3_ne6_pts"])
+    np.savez_compressed(os.path.join(HERE, "univariate.npz"), **out)
+
+
+def aniso_terms(st, geo, sigma):
+    """Anisotropic K_sigma from reference pieces."""
+    d = st.num_spatial_dims
+    mats = [UnivariateMatrices(s) for s in st.spatial]
+    K = None
+    for a in range(d):
+        fac = [mats[l].stiffness if l == a else mats[l].mass for l in reversed(range(d))]
+        t = sigma[a] * kron_chain(fac)
+        K = t if K is None else K + t
+    return sp.csr_matrix(K)
+
+
+def case(name, d, p, ne, ne_t, T, sigma, seed, su_tol=0.3, theta=None, gm_iters=400, front=False):
+    rng = np.random.default_rng(seed)
+    nes = [ne] * d if np.isscalar(ne) else list(ne)
+    st = SpaceTimeSpace([SplineSpace.uniform(p, n) for n in nes], SplineSpace.uniform(p, ne_t))
+    geo = builtin_geometry({1: "unit_interval", 2: "unit_square", 3: "unit_cube"}[d], final_time=T)
+    N, nt, ns = st.num_dof, st.num_time, st.num_space
+    W_t, M_t = time_matrices(st, T)
+    M_s, K_s = spatial_operators(st.spatial, geo)
+    sig = np.atleast_1d(sigma)
+    if sig.size == 1:
+        sep = [(1.0, W_t, M_s), (float(sig[0]), M_t, K_s)]
+    else:
+        sep = [(1.0, W_t, M_s), (1.0, M_t, aniso_terms(st, geo, sig))]
+    react = RM["a"] * RM["c1"]
+    # SU terms from an indicator
+    if front:
+        g1 = st.spatial[0].greville()
+        gs = np.tile(g1, ns // g1.size)
+        gt = st.time_greville()
+        th = np.clip(np.exp(-(((gs[None, :] - 0.2 - 0.5 * gt[:, None]) / 0.08) ** 2)), 0, 1)
+    else:
+        th = rng.random((nt, ns))
+    ind = ResidualIndicator(th, st.time_greville(), [s.greville() for s in st.spatial], st.spatial_shape)
+    tau = compute_tau(st.time)
+    lr = lowrank_factorize(ind, su_tol)
+    stab = assemble_stabilization(tau, lr, st, geo, 1.0)
+    su = stab.terms()
+    x = rng.uniform(-1, 1, N)
+    u = rng.uniform(0, 1, N)
+    w = rng.uniform(0, 0.1, N)
+    rhs = rng.standard_normal(N)
+    op_a = KroneckerOperator(nt, ns, sep + [(react, M_t, M_s)] + su)
+    MR = reaction_mass(st, geo, RM, u, w)
+    op_b = KroneckerOperator(nt, ns, sep + su, correction=MR)
+    op_sep = KroneckerOperator(nt, ns, sep + [(react, M_t, M_s)])
+    if sig.size == 1:
+        sd = SpatialQuadratureData(st.spatial, geo)
+        P = FastDiagPreconditioner.build(st, T, 1.0, float(sig[0]), react, spatial_data=sd)
+    else:
+        eigs = [generalized_eig(UnivariateMatrices(s).stiffness, UnivariateMatrices(s).mass) for s in st.spatial]
+        grid = np.zeros(st.spatial_shape)
+        for l in range(d):
+            shp = [1] * d
+            shp[d - 1 - l] = eigs[l][1].size
+            grid = grid + sig[l] * eigs[l][1].reshape(shp)
+        P = FastDiagPreconditioner(eigs, grid.ravel(), build_time_pencil(W_t, M_t), 1.0, 1.0, react)
+    out = dict(d=d, p=p, ne=np.array(nes), ne_t=ne_t, T=T, sigma=sig, su_tol=su_tol, theta=th,
+               x=x, u=u, w=w, rhs=rhs, su_rank=lr.rank, su_weights=lr.weights,
+               y_sep=op_sep.matvec(x), y_a=op_a.matvec(x), y_b=op_b.matvec(x),
+               y_mr=MR @ x, z_pc=P.apply(x), z_pc_ya=P.apply(op_a.matvec(x)))
+    sol, it, hist = gmres(op_a, rhs, precond=P, tol=1e-8, max_iter=gm_iters)
+    out.update(gm_a_x=sol, gm_a_it=it, gm_a_hist=np.array(hist))
+    sol, it, hist = gmres(op_b, rhs, precond=P, tol=1e-8, max_iter=gm_iters)
+    out.update(gm_b_x=sol, gm_b_it=it, gm_b_hist=np.array(hist))
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, "N=%d R=%d gmres a/b %d/%d" % (N, lr.rank, out["gm_a_it"], it))
+
+
+if __name__ == "__main__":
+    univariate()
+    case("case_2d_p2", 2, 2, (3, 2), 3, 2.0, 1e-3, seed=11)
+    case("case_3d_p3", 3, 3, 3, 4, 1.0, 1e-3, seed=12)
+    case("case_2d_aniso", 2, 3, (4, 3), 5, 1.0, (1e-3, 4e-4), seed=13)
+    case("case_1d_p1", 1, 1, 6, 5, 1.0, 1e-2, seed=14)
+    case("case_cfg1", 1, 2, 64, 64, 1.0, 1e-3, seed=0, su_tol=0.1, front=True)
+    case("case_3d_p2_front", 3, 2, (6, 4, 3), 8, 1.0, (1e-3, 4e-4, 4e-4), seed=15, su_tol=0.1, front=True)

@@ -1,0 +1,68 @@
+// Microbenchmark: FP64 FMA pipe vs DMMA (mma.sync m8n8k4 f64) throughput on sm_100a.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+__global__ void dmma_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { c[k][0] = 0; c[k][1] = 0; }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main() {
+  int dev = 0; cudaDeviceProp prop; cudaGetDeviceProperties(&prop, dev);
+  printf("device %s SMs %d clock %d kHz\n", prop.name, prop.multiProcessorCount, prop.clockRate);
+  double* out; cudaMalloc(&out, 1 << 26);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int sms = prop.multiProcessorCount;
+  for (int tpb : {256, 512, 1024}) {
+    int blocks = sms * (2048 / tpb);
+    int iters = 2000;
+    dfma_kernel<<<blocks, tpb>>>(out, 10, 1.0000001, 1e-9);
+    cudaEventRecord(e0);
+    dfma_kernel<<<blocks, tpb>>>(out, iters, 1.0000001, 1e-9);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 2.0 * 128 * (double)iters * blocks * tpb;
+    printf("DFMA tpb=%d: %.2f TFLOP/s (%.3f ms)\n", tpb, flops / ms / 1e9, ms);
+  }
+  for (int tpb : {128, 256, 512, 1024}) {
+    int blocks = sms * (2048 / tpb);
+    int iters = 4000;
+    dmma_kernel<<<blocks, tpb>>>(out, 10);
+    cudaEventRecord(e0);
+    dmma_kernel<<<blocks, tpb>>>(out, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double warps = (double)blocks * tpb / 32;
+    double flops = 2.0 * 8 * 8 * 4 * 8 * (double)iters * warps;
+    printf("DMMA tpb=%d: %.2f TFLOP/s (%.3f ms)\n", tpb, flops / ms / 1e9, ms);
+  }
+  cudaError_t err = cudaGetLastError();
+  printf("err: %s\n", cudaGetErrorString(err));
+  return 0;
+}
