@@ -1,0 +1,124 @@
+/*
+ * libmonoiga_b200 -- C ABI of the B200-native preconditioned space-time
+ * Krylov solve (hot path of arxiv 2311.17500 / reference package `monoiga`).
+ *
+ * Plain C: opaque context, raw pointers and sizes, int status codes.  All
+ * vector arguments named x/y/r/z/V/w/h are DEVICE pointers (fp64) in the
+ * reference layout: C-order (N_t, n_d, ..., n_1), direction 1 fastest
+ * (reference tensorops.py:1-7).  Table arguments marked "host" are copied
+ * to the device by the call.  Every call is ordered on the context's
+ * stream; none allocates after the corresponding *_setup call.
+ *
+ * Status: 0 ok; MI_ERR_ARG (bad argument / dimension mismatch, maps to the
+ * reference's ValueError); MI_ERR_CUDA (device failure); MI_ERR_STATE (call
+ * order); the message is in mi_last_error() (thread-local).
+ */
+#ifndef MONOIGA_B200_H
+#define MONOIGA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MI_OK 0
+#define MI_ERR_ARG 1
+#define MI_ERR_CUDA 2
+#define MI_ERR_STATE 3
+
+typedef struct mi_ctx mi_ctx;
+
+/* Library identity and last error of the calling thread. */
+int mi_version(void);
+const char* mi_last_error(void);
+
+/* Context for one space-time tensor shape on one device.
+ * Replaces the dimension bookkeeping of SpaceTimeSpace (bspline.py:311-420):
+ * d spatial directions with n[0..d-1] = n_1..n_d functions, N_t = nt
+ * (first time function removed), spatial degree p, time degree pt. */
+int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx** out);
+int mi_ctx_destroy(mi_ctx* ctx);
+int mi_ctx_set_stream(mi_ctx* ctx, void* cuda_stream);
+
+/* ---------------------------------------------------------------------
+ * Operator A  (replaces KroneckerOperator + two_factor_matvec,
+ * assembly.py:401-444 / tensorops.py:45-56, with the term list of
+ * _Workspace.operator, solver.py:213-236)
+ *
+ * A = sum_c T_c (x) S_c  over nchan channels.  T_c: banded N_t x N_t time
+ * factor, host band (nchan, nt, 2pt+1) with band[c][i][k] = T_c[i, i-pt+k].
+ * S_c: spatial factor, generated on the device as a (2p+1)^d stencil from
+ * either a sum of Kronecker products of banded 1D factors
+ * (mi_op_set_kron_channel: M_s, K_s, K_sigma of assembly.py:222-238) or a
+ * multilinear-theta weighted mass (mi_op_set_su_channel: S^s_r of
+ * stabilization.py:469-488).
+ * ------------------------------------------------------------------- */
+int mi_op_setup(mi_ctx* ctx, int nchan);
+int mi_op_set_time_bands(mi_ctx* ctx, const double* bands /* host nchan*nt*(2pt+1) */);
+/* channel c spatial factor = sum_t coef[t] * kron_l band[t][l]
+ * bands: host (nterms, d, nmax, 2p+1), band[t][l][i][k] = F_{t,l}[i, i-p+k],
+ * nmax = max_l n_l. */
+int mi_op_set_kron_channel(mi_ctx* ctx, int c, int nterms, const double* coef, const double* bands);
+/* channel c spatial factor = sum_k theta[k] prod_l H_l[i_l, j_l-i_l+p, k_l-i_l+ko]
+ * theta: host N_s (flat spatial order); H: host (d, nmax, 2p+1, 2ko+1). */
+int mi_op_set_su_channel(mi_ctx* ctx, int c, const double* theta, const double* H, int ko);
+/* y = A x   (x, y device, length N, must not alias) */
+int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
+
+/* Reaction correction y += M_R x, M_R = int int C_r B_i B_j with the
+ * ionic linearisation C_r = c1 (u - a)(u - 1) + c2 w evaluated at q = p+1
+ * Gauss points per element and direction (assembly.py:287-347).
+ * u, w: device iterate coefficients (length N, copied).  Tables (host):
+ * colt (qt_total, pt+1) time basis values at Gauss points with first index
+ * firstt (qt_total) and weights wt (qt_total, includes T); per direction
+ * cols_l (q_l_total, p+1), firsts_l, ws_l (includes box length). */
+int mi_op_set_reaction(mi_ctx* ctx, const double* u, const double* w, double c1, double a, double c2,
+                       int q, const int* nel /* d spatial element counts */, int nel_t,
+                       const double* colt, const int* firstt, const double* wt,
+                       const double* cols /* (d, qmax_total, p+1) */, const int* firsts /* (d, qmax_total) */,
+                       const double* ws /* (d, qmax_total) */);
+int mi_op_clear_reaction(mi_ctx* ctx);
+
+/* ---------------------------------------------------------------------
+ * Fast-diagonalisation preconditioner  (replaces
+ * FastDiagPreconditioner.apply / _diag_blocks, linalg.py:309-353, built
+ * from FastDiagPreconditioner.build, linalg.py:264-307)
+ *
+ * P^-1 = (Q (x) U_s) (C_m Delta + mu I)^-1 (Q^T (x) U_s^T)
+ * U: host (d, nmax, nmax) per-direction eigenvectors (row-major n_l x n_l);
+ * lam: host (d, nmax) eigenvalues already multiplied by sigma_l;
+ * Q: host nt x nt real time basis; Delta = real block arrowhead given by
+ * diag/off/partner (2x2 blocks) + border g (upper), glow (lower), sigma.
+ * ------------------------------------------------------------------- */
+int mi_pc_setup(mi_ctx* ctx, const double* U, const double* lam, double cm, double react,
+                const double* Q, const double* diag, const double* off, const int* partner,
+                const double* g, const double* glow, double sigma);
+/* z = P^-1 r  (r, z device; may alias) */
+int mi_pc_apply(mi_ctx* ctx, const double* r, double* z);
+
+/* ---------------------------------------------------------------------
+ * Krylov primitives (replace the numpy CGS2 / update steps of gmres,
+ * linalg.py:404-444).  V is a device matrix of k rows of length n with
+ * row stride ldv.  Reductions are deterministic (fixed partition, fixed
+ * order, no atomics): repeated calls are bitwise identical.
+ * ------------------------------------------------------------------- */
+/* h[i] = <V_i, w>, i < k   (h device) */
+int mi_dots(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* w, double* h);
+/* w -= sum_i h[i] V_i   (h device) */
+int mi_sub_combination(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* h, double* w);
+/* out = x0 + sum_i y[i] V_i   (y device; x0 may be NULL for 0) */
+int mi_combination(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* y,
+                   const double* x0, double* out);
+/* out = x * s  with s = 1 / *hnorm read on the device */
+int mi_scale_inv(mi_ctx* ctx, long long n, const double* x, const double* hnorm, double* out);
+/* out = x / sqrt(*nrm2)  (nrm2 device: squared norm from mi_dots) */
+int mi_normalize(mi_ctx* ctx, long long n, const double* x, const double* nrm2, double* out);
+/* fused CGS2 pass: w -= V^T h_in ; h_out = V w ; optional ||w||^2 into *nrm2 */
+int mi_cgs_pass(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* h_in,
+                double* w, double* h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,85 @@
+// Shared definitions for libmonoiga_b200 (sm_100a).
+//
+// Tensor layout everywhere: C-order (N_t, n_3, n_2, n_1) fp64, direction 1
+// fastest (reference tensorops.py:1-7, bspline.py:311-316).  Spatial
+// directions beyond d have extent 1, so every kernel is written for d = 3.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/monoiga_b200.h"
+
+#define MI_MAX_P 4
+#define MI_MAX_CHAN 64
+
+namespace mi {
+
+void set_error(const std::string& msg);
+int fail(const char* what, cudaError_t err);
+
+#define MI_CUDA(call)                                                   \
+  do {                                                                  \
+    cudaError_t _e = (call);                                            \
+    if (_e != cudaSuccess) return ::mi::fail(#call, _e);                \
+  } while (0)
+
+#define MI_CHECK_LAUNCH(name)                                           \
+  do {                                                                  \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) return ::mi::fail(name, _e);                 \
+  } while (0)
+
+#define MI_REQUIRE(cond, code, msg)                                     \
+  do {                                                                  \
+    if (!(cond)) { ::mi::set_error(msg); return (code); }               \
+  } while (0)
+
+struct DeviceBuf {
+  double* p = nullptr;
+  size_t n = 0;
+};
+
+int dalloc(DeviceBuf& b, size_t n);
+void dfree(DeviceBuf& b);
+
+}  // namespace mi
+
+struct mi_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int d = 1, p = 1, pt = 1;     // spatial dims, spatial degree, time degree
+  int n[3] = {1, 1, 1};         // n_1, n_2, n_3 (1 beyond d)
+  int nt = 0;                   // N_t (constrained)
+  long long ns = 0, N = 0;      // N_s, N
+
+  // ---- operator A: channels c = 0..nchan-1, y = sum_c T_c (x)_t (S_c x)
+  int nchan = 0;
+  int nsten = 0;                // (2p+1)^d stencil points
+  mi::DeviceBuf tband;          // nchan x nt x (2pt+1)
+  mi::DeviceBuf stencil;        // nchan x nsten x ns
+  mi::DeviceBuf wbuf;           // nchan x N  (S_c x per channel)
+  bool op_ready = false;
+
+  // ---- reaction correction M_R (variant B)
+  bool reaction_on = false;
+  mi::DeviceBuf u_it, w_it;     // iterate coefficients (N each)
+  double c1 = 0, a = 0, c2 = 0, final_time = 1;
+  mi::DeviceBuf colt;           // time Gauss tables
+  mi::DeviceBuf cols;           // spatial Gauss tables
+  mi::DeviceBuf rq_scratch;
+
+  // ---- preconditioner
+  bool pc_ready = false;
+  mi::DeviceBuf Us[3], UsT[3];  // per direction n_l x n_l (U and U^T)
+  mi::DeviceBuf lam[3];         // per direction eigenvalues (already scaled by sigma_l)
+  mi::DeviceBuf Q, QT;          // time basis nt x nt and transpose
+  mi::DeviceBuf pen_diag, pen_off, pen_g, pen_glow;  // (nt-1)
+  int* pen_partner = nullptr;   // (nt-1)
+  double pen_sigma = 0, pc_cm = 1, pc_react = 0;
+  mi::DeviceBuf pc_t1, pc_t2;   // N each
+
+  // ---- Krylov scratch
+  mi::DeviceBuf partials;       // reduction partials
+};

@@ -1,0 +1,108 @@
+// Context lifetime, error reporting, device allocation.
+#include "common.cuh"
+
+#include <cstdio>
+
+namespace mi {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(const char* what, cudaError_t err) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(err);
+  return MI_ERR_CUDA;
+}
+
+int dalloc(DeviceBuf& b, size_t n) {
+  if (b.p && b.n >= n) return MI_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+  if (n == 0) return MI_OK;
+  cudaError_t e = cudaMalloc(&b.p, n * sizeof(double));
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    char buf[128];
+    snprintf(buf, sizeof(buf), "cudaMalloc(%zu doubles)", n);
+    return fail(buf, e);
+  }
+  b.n = n;
+  return MI_OK;
+}
+
+void dfree(DeviceBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+}
+
+}  // namespace mi
+
+extern "C" {
+
+int mi_version(void) { return 1; }
+
+const char* mi_last_error(void) { return mi::g_last_error.c_str(); }
+
+int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx** out) {
+  MI_REQUIRE(out != nullptr, MI_ERR_ARG, "out is NULL");
+  MI_REQUIRE(d >= 1 && d <= 3, MI_ERR_ARG, "d must be 1, 2 or 3");
+  MI_REQUIRE(p >= 1 && p <= MI_MAX_P, MI_ERR_ARG, "spatial degree must be in [1, 4]");
+  MI_REQUIRE(pt >= 1 && pt <= MI_MAX_P, MI_ERR_ARG, "time degree must be in [1, 4]");
+  MI_REQUIRE(nt >= 2, MI_ERR_ARG, "N_t must be >= 2");
+  MI_CUDA(cudaSetDevice(device));
+  mi_ctx* c = new mi_ctx();
+  c->device = device;
+  c->d = d;
+  c->p = p;
+  c->pt = pt;
+  c->nt = nt;
+  long long ns = 1;
+  for (int l = 0; l < 3; ++l) {
+    c->n[l] = l < d ? n[l] : 1;
+    if (c->n[l] < 1) {
+      delete c;
+      mi::set_error("spatial dimensions must be positive");
+      return MI_ERR_ARG;
+    }
+    ns *= c->n[l];
+  }
+  c->ns = ns;
+  c->N = ns * nt;
+  int s = 1;
+  for (int l = 0; l < d; ++l) s *= 2 * p + 1;
+  c->nsten = s;
+  int rc = mi::dalloc(c->partials, (size_t)1024 * 592);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return MI_OK;
+}
+
+int mi_ctx_destroy(mi_ctx* c) {
+  if (!c) return MI_OK;
+  cudaSetDevice(c->device);
+  mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->u_it, &c->w_it, &c->colt,
+                           &c->cols, &c->rq_scratch, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
+                           &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->partials};
+  for (auto* b : bufs) mi::dfree(*b);
+  for (int l = 0; l < 3; ++l) {
+    mi::dfree(c->Us[l]);
+    mi::dfree(c->UsT[l]);
+    mi::dfree(c->lam[l]);
+  }
+  if (c->pen_partner) cudaFree(c->pen_partner);
+  delete c;
+  return MI_OK;
+}
+
+int mi_ctx_set_stream(mi_ctx* c, void* stream) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  c->stream = static_cast<cudaStream_t>(stream);
+  return MI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) batched GEMM used for the
+// dense eigenvector mode products of the fast-diagonalisation
+// preconditioner (reference: mode_apply inside FastDiagPreconditioner.apply,
+// linalg.py:329-346 / tensorops.py:13-26).
+//
+// C[b] = A[b] * B[b]  (row-major, arbitrary leading dimensions and batch
+// strides; a zero stride broadcasts one matrix over the batch).
+// Tile 64x64x32, 8 warps (each 2x4 DMMA tiles), cp.async double buffering.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mi {
+
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K;
+  long long lda, ldb, ldc;
+  long long sA, sB, sC;  // batch strides (elements)
+};
+
+constexpr int GT_M = 64, GT_N = 64, GT_K = 32;
+constexpr int GA_LD = GT_K + 4;   // 36: conflict-free A fragment reads
+constexpr int GB_LD = GT_N + 4;   // 68: conflict-free B fragment reads
+constexpr int GEMM_SMEM = 2 * (GT_M * GA_LD + GT_K * GB_LD) * 8;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) dgemm_dmma(GemmArgs g) {
+  extern __shared__ double smem[];
+  double* As = smem;                              // [2][64][36]
+  double* Bs = smem + 2 * GT_M * GA_LD;           // [2][32][68]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.y * GT_M, n0 = blockIdx.x * GT_N;
+  const long long b = blockIdx.z;
+  const double* A = g.A + b * g.sA;
+  const double* B = g.B + b * g.sB;
+  double* C = g.C + b * g.sC;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
+  const int gq = lane >> 2, t4 = lane & 3;
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load = [&](int stage, int k0) {
+    double* as = As + stage * GT_M * GA_LD;
+    double* bs = Bs + stage * GT_K * GB_LD;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int idx = tid + 256 * e;
+      int r = idx >> 5, k = idx & 31;
+      bool v = (m0 + r < g.M) && (k0 + k < g.K);
+      const double* src = v ? A + (long long)(m0 + r) * g.lda + k0 + k : A;
+      cp_async8(as + r * GA_LD + k, src, v);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int idx = tid + 256 * e;
+      int k = idx >> 6, n = idx & 63;
+      bool v = (k0 + k < g.K) && (n0 + n < g.N);
+      const double* src = v ? B + (long long)(k0 + k) * g.ldb + n0 + n : B;
+      cp_async8(bs + k * GB_LD + n, src, v);
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (g.K + GT_K - 1) / GT_K;
+  load(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      load((kc + 1) & 1, (kc + 1) * GT_K);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + (kc & 1) * GT_M * GA_LD;
+    const double* bs = Bs + (kc & 1) * GT_K * GB_LD;
+#pragma unroll
+    for (int ks = 0; ks < GT_K / 4; ++ks) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = as[(wm + 8 * i + gq) * GA_LD + ks * 4 + t4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[(ks * 4 + t4) * GB_LD + wn + 8 * j + gq];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    int r = m0 + wm + 8 * i + gq;
+    if (r >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int cidx = n0 + wn + 8 * j + 2 * t4;
+      double* dst = C + (long long)r * g.ldc + cidx;
+      if (cidx < g.N) dst[0] = acc[i][j][0];
+      if (cidx + 1 < g.N) dst[1] = acc[i][j][1];
+    }
+  }
+}
+
+// Launch helper: returns cudaError_t of the launch.
+inline cudaError_t launch_dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dgemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    attr = true;
+  }
+  dim3 grid((g.N + GT_N - 1) / GT_N, (g.M + GT_M - 1) / GT_M, batch);
+  dgemm_dmma<<<grid, 256, GEMM_SMEM, st>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace mi

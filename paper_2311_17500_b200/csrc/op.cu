@@ -1,0 +1,286 @@
+// Operator A = sum_c T_c (x) S_c  (reference: KroneckerOperator.matvec,
+// assembly.py:430-444, with the terms of _Workspace.operator, solver.py:213-236,
+// and the Spline Upwind terms of StabilizationMatrices.terms, stabilization.py:439-445).
+//
+// Every Kronecker term of the reference is one "channel": a banded time
+// factor T_c and a spatial factor S_c.  Spatial factors are (2p+1)^d
+// stencils generated on the device:
+//   * Kronecker channels (M_s, K_s, K_sigma: assembly.py:222-238) from 1D bands,
+//   * Spline Upwind channels (S^s_r: the theta_r-weighted spatial mass,
+//     stabilization.py:469-488) from theta_r and 1D hat triple products.
+// Apply: W_c = S_c x (one stencil sweep per channel group), then
+// y = sum_c T_c W_c along time (banded), plus the reaction correction.
+#include "common.cuh"
+#include "dispatch.cuh"
+
+namespace mi {
+
+struct Dims {
+  int n1, n2, n3, nt;
+  long long ns, N;
+};
+
+static Dims dims_of(const mi_ctx* c) {
+  return Dims{c->n[0], c->n[1], c->n[2], c->nt, c->ns, c->N};
+}
+
+template <int D, int P>
+struct Sten {
+  static constexpr int W = 2 * P + 1;
+  static constexpr int W1 = W;
+  static constexpr int W2 = D >= 2 ? W : 1;
+  static constexpr int W3 = D >= 3 ? W : 1;
+  static constexpr int S = W1 * W2 * W3;
+};
+
+// ---------------------------------------------------------------- build
+template <int D, int P>
+__global__ void build_kron_channel(double* __restrict__ out, const double* __restrict__ coef,
+                                   const double* __restrict__ bands, int nterms, int nmax, Dims g) {
+  using ST = Sten<D, P>;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (i >= g.ns) return;
+  const int a1 = s % ST::W1, a2 = (s / ST::W1) % ST::W2, a3 = s / (ST::W1 * ST::W2);
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2));
+  const int ii[3] = {i1, i2, i3};
+  const int aa[3] = {a1, a2, a3};
+  const int nn[3] = {g.n1, g.n2, g.n3};
+  bool inside = true;
+#pragma unroll
+  for (int l = 0; l < D; ++l) {
+    int j = ii[l] + aa[l] - P;
+    inside = inside && j >= 0 && j < nn[l];
+  }
+  double v = 0.0;
+  if (inside) {
+    const int W = 2 * P + 1;
+    for (int t = 0; t < nterms; ++t) {
+      double prod = coef[t];
+#pragma unroll
+      for (int l = 0; l < D; ++l)
+        prod *= bands[(((long long)t * D + l) * nmax + ii[l]) * W + aa[l]];
+      v += prod;
+    }
+  }
+  out[(long long)s * g.ns + i] = v;
+}
+
+template <int D, int P>
+__global__ void build_su_channel(double* __restrict__ out, const double* __restrict__ theta,
+                                 const double* __restrict__ H, int ko, int nmax, Dims g) {
+  using ST = Sten<D, P>;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (i >= g.ns) return;
+  const int a1 = s % ST::W1, a2 = (s / ST::W1) % ST::W2, a3 = s / (ST::W1 * ST::W2);
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2));
+  const int ii[3] = {i1, i2, i3};
+  const int aa[3] = {a1, a2, a3};
+  const int nn[3] = {g.n1, g.n2, g.n3};
+  const int W = 2 * P + 1;
+  const int KW = 2 * ko + 1;
+  bool inside = true;
+#pragma unroll
+  for (int l = 0; l < D; ++l) {
+    int j = ii[l] + aa[l] - P;
+    inside = inside && j >= 0 && j < nn[l];
+  }
+  double v = 0.0;
+  if (inside) {
+    // H_l row pointers for (i_l, a_l)
+    const double* h[3];
+#pragma unroll
+    for (int l = 0; l < D; ++l) h[l] = H + (((long long)l * nmax + ii[l]) * W + aa[l]) * KW;
+    const int b3n = D >= 3 ? KW : 1, b2n = D >= 2 ? KW : 1;
+    for (int b3 = 0; b3 < b3n; ++b3) {
+      int k3 = D >= 3 ? i3 + b3 - ko : 0;
+      if (k3 < 0 || k3 >= g.n3) continue;
+      double h3 = D >= 3 ? h[2][b3] : 1.0;
+      if (h3 == 0.0) continue;
+      for (int b2 = 0; b2 < b2n; ++b2) {
+        int k2 = D >= 2 ? i2 + b2 - ko : 0;
+        if (k2 < 0 || k2 >= g.n2) continue;
+        double h23 = h3 * (D >= 2 ? h[1][b2] : 1.0);
+        if (h23 == 0.0) continue;
+        const double* th = theta + ((long long)k3 * g.n2 + k2) * g.n1;
+        double acc = 0.0;
+        for (int b1 = 0; b1 < KW; ++b1) {
+          int k1 = i1 + b1 - ko;
+          if (k1 < 0 || k1 >= g.n1) continue;
+          acc += th[k1] * h[0][b1];
+        }
+        v += h23 * acc;
+      }
+    }
+  }
+  out[(long long)s * g.ns + i] = v;
+}
+
+// ---------------------------------------------------------------- apply
+// W_c[t, i] = sum_s S_c[s, i] x[t, i + off(s)], channels in groups of CG,
+// TC time slices per thread.
+template <int D, int P, int CG, int TC>
+__global__ void __launch_bounds__(128) stencil_apply(const double* __restrict__ x,
+                                                     const double* __restrict__ sten,
+                                                     double* __restrict__ wout, int c0, int nc,
+                                                     Dims g) {
+  using ST = Sten<D, P>;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int t0 = blockIdx.y * TC;
+  if (i >= g.ns) return;
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2));
+  double acc[CG][TC];
+#pragma unroll
+  for (int c = 0; c < CG; ++c)
+#pragma unroll
+    for (int t = 0; t < TC; ++t) acc[c][t] = 0.0;
+  const double* xt = x + (long long)t0 * g.ns;
+  int s = 0;
+  for (int a3 = 0; a3 < ST::W3; ++a3) {
+    int j3 = D >= 3 ? min(max(i3 + a3 - P, 0), g.n3 - 1) : 0;
+    for (int a2 = 0; a2 < ST::W2; ++a2) {
+      int j2 = D >= 2 ? min(max(i2 + a2 - P, 0), g.n2 - 1) : 0;
+      const long long row = ((long long)j3 * g.n2 + j2) * g.n1;
+#pragma unroll
+      for (int a1 = 0; a1 < ST::W1; ++a1, ++s) {
+        int j1 = min(max(i1 + a1 - P, 0), g.n1 - 1);
+        const long long j = row + j1;
+        double xv[TC];
+#pragma unroll
+        for (int t = 0; t < TC; ++t) xv[t] = (t0 + t < g.nt) ? __ldg(xt + (long long)t * g.ns + j) : 0.0;
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+          if (c < nc) {
+            double cf = __ldg(sten + ((long long)(c0 + c) * ST::S + s) * g.ns + i);
+#pragma unroll
+            for (int t = 0; t < TC; ++t) acc[c][t] = fma(cf, xv[t], acc[c][t]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CG; ++c) {
+    if (c < nc) {
+#pragma unroll
+      for (int t = 0; t < TC; ++t)
+        if (t0 + t < g.nt) wout[(long long)(c0 + c) * g.N + (long long)(t0 + t) * g.ns + i] = acc[c][t];
+    }
+  }
+}
+
+// y[t, i] = sum_c sum_k band_c[t, k] W_c[t - pt + k, i]
+__global__ void time_filter(const double* __restrict__ w, const double* __restrict__ band,
+                            double* __restrict__ y, int nchan, int pt, Dims g) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  if (i >= g.ns) return;
+  const int W = 2 * pt + 1;
+  double acc = 0.0;
+  for (int c = 0; c < nchan; ++c) {
+    const double* b = band + ((long long)c * g.nt + t) * W;
+    const double* wc = w + (long long)c * g.N;
+    for (int k = 0; k < W; ++k) {
+      int tt = t - pt + k;
+      if (tt < 0 || tt >= g.nt) continue;
+      acc = fma(__ldg(b + k), __ldg(wc + (long long)tt * g.ns + i), acc);
+    }
+  }
+  y[(long long)t * g.ns + i] = acc;
+}
+
+int reaction_apply(mi_ctx* c, const double* x, double* y);  // reaction.cu
+
+}  // namespace mi
+
+using namespace mi;
+
+extern "C" {
+
+int mi_op_setup(mi_ctx* c, int nchan) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  MI_REQUIRE(nchan >= 1 && nchan <= MI_MAX_CHAN, MI_ERR_ARG, "nchan must be in [1, 64]");
+  MI_CUDA(cudaSetDevice(c->device));
+  c->nchan = nchan;
+  int rc;
+  if ((rc = dalloc(c->tband, (size_t)nchan * c->nt * (2 * c->pt + 1)))) return rc;
+  if ((rc = dalloc(c->stencil, (size_t)nchan * c->nsten * c->ns))) return rc;
+  if ((rc = dalloc(c->wbuf, (size_t)nchan * c->N))) return rc;
+  MI_CUDA(cudaMemsetAsync(c->stencil.p, 0, sizeof(double) * nchan * c->nsten * c->ns, c->stream));
+  MI_CUDA(cudaMemsetAsync(c->tband.p, 0, sizeof(double) * nchan * c->nt * (2 * c->pt + 1), c->stream));
+  c->op_ready = true;
+  return MI_OK;
+}
+
+int mi_op_set_time_bands(mi_ctx* c, const double* bands) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_CUDA(cudaMemcpyAsync(c->tband.p, bands, sizeof(double) * c->nchan * c->nt * (2 * c->pt + 1),
+                          cudaMemcpyHostToDevice, c->stream));
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  return MI_OK;
+}
+
+int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* bands) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
+  MI_REQUIRE(nterms >= 1, MI_ERR_ARG, "nterms must be >= 1");
+  const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
+  const size_t nb = (size_t)nterms * c->d * nmax * (2 * c->p + 1);
+  DeviceBuf dc, db;
+  int rc;
+  if ((rc = dalloc(dc, nterms)) || (rc = dalloc(db, nb))) return rc;
+  MI_CUDA(cudaMemcpyAsync(dc.p, coef, sizeof(double) * nterms, cudaMemcpyHostToDevice, c->stream));
+  MI_CUDA(cudaMemcpyAsync(db.p, bands, sizeof(double) * nb, cudaMemcpyHostToDevice, c->stream));
+  Dims g = dims_of(c);
+  dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
+  double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
+  MI_DISPATCH_DP(c->d, c->p, (build_kron_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dc.p, db.p, nterms, nmax, g)));
+  MI_CHECK_LAUNCH("build_kron_channel");
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(dc);
+  dfree(db);
+  return MI_OK;
+}
+
+int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H, int ko) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
+  MI_REQUIRE(ko >= 0 && ko <= 8, MI_ERR_ARG, "ko out of range");
+  const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
+  const size_t nh = (size_t)c->d * nmax * (2 * c->p + 1) * (2 * ko + 1);
+  DeviceBuf dt, dh;
+  int rc;
+  if ((rc = dalloc(dt, c->ns)) || (rc = dalloc(dh, nh))) return rc;
+  MI_CUDA(cudaMemcpyAsync(dt.p, theta, sizeof(double) * c->ns, cudaMemcpyHostToDevice, c->stream));
+  MI_CUDA(cudaMemcpyAsync(dh.p, H, sizeof(double) * nh, cudaMemcpyHostToDevice, c->stream));
+  Dims g = dims_of(c);
+  dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
+  double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
+  MI_DISPATCH_DP(c->d, c->p, (build_su_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dt.p, dh.p, ko, nmax, g)));
+  MI_CHECK_LAUNCH("build_su_channel");
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(dt);
+  dfree(dh);
+  return MI_OK;
+}
+
+int mi_op_apply(mi_ctx* c, const double* x, double* y) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
+  MI_REQUIRE(x != y, MI_ERR_ARG, "x and y must not alias");
+  Dims g = dims_of(c);
+  constexpr int CG = 4, TC = 8;
+  dim3 grid((unsigned)((c->ns + 127) / 128), (c->nt + TC - 1) / TC);
+  for (int c0 = 0; c0 < c->nchan; c0 += CG) {
+    int nc = min(CG, c->nchan - c0);
+    MI_DISPATCH_DP(c->d, c->p, (stencil_apply<D_, P_, CG, TC><<<grid, 128, 0, c->stream>>>(x, c->stencil.p, c->wbuf.p, c0, nc, g)));
+    MI_CHECK_LAUNCH("stencil_apply");
+  }
+  dim3 g2((unsigned)((c->ns + 255) / 256), c->nt);
+  time_filter<<<g2, 256, 0, c->stream>>>(c->wbuf.p, c->tband.p, y, c->nchan, c->pt, g);
+  MI_CHECK_LAUNCH("time_filter");
+  if (c->reaction_on) return reaction_apply(c, x, y);
+  return MI_OK;
+}
+
+}  // extern "C"

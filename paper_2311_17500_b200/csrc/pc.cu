@@ -1,0 +1,166 @@
+// Fast-diagonalisation preconditioner (reference FastDiagPreconditioner.apply,
+// linalg.py:317-353; _diag_blocks, linalg.py:309-315).
+//
+//   z = (Q (x) U_d..U_1) (C_m Delta + mu_s I)^-1 (Q^T (x) U_d^T..U_1^T) r
+//
+// Dense mode products run on the FP64 tensor cores (DMMA, gemm.cuh).  The
+// time basis Q is the REAL 2x2-block form of the reference's complex
+// pencil (factors.RealTimePencil), so the whole apply is real arithmetic.
+// The block-arrowhead core is solved per spatial eigen-index s with
+// mu_s = react + sum_l sigma_l lam_l[i_l] formed on the fly (the
+// reference materialises H_int as an (N_t-1) x N_s complex array).
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace mi {
+
+// Block-arrowhead solve, one thread per spatial column s, in place on Y
+// (nt x ns).  Interior rows i < m = nt-1 carry 2x2 blocks
+// [[a, b], [c, e]] = C_m T_block + mu I; border column C_m g, border row
+// C_m glow, corner C_m sigma + mu.
+__global__ void arrowhead_solve(double* __restrict__ Y, const double* __restrict__ lam1,
+                                const double* __restrict__ lam2, const double* __restrict__ lam3,
+                                const double* __restrict__ diag, const double* __restrict__ off,
+                                const int* __restrict__ partner, const double* __restrict__ gb,
+                                const double* __restrict__ gl, double sigma, double cm, double react,
+                                int n1, int n2, int nt, long long ns) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  const int i1 = (int)(s % n1), i2 = (int)((s / n1) % n2), i3 = (int)(s / ((long long)n1 * n2));
+  const double mu = react + lam1[i1] + lam2[i2] + lam3[i3];
+  const int m = nt - 1;
+  double sy = 0.0, sb = 0.0;
+  for (int i = 0; i < m; ++i) {
+    const int j = partner[i];
+    const double a = fma(cm, diag[i], mu), e = fma(cm, diag[j], mu);
+    const double b = cm * off[i], c = cm * off[j];
+    const double inv = 1.0 / (a * e - b * c);
+    const double yi = Y[(long long)i * ns + s], yj = Y[(long long)j * ns + s];
+    const double dy = (e * yi - b * yj) * inv;
+    const double db = cm * (e * gb[i] - b * gb[j]) * inv;
+    sy = fma(gl[i], dy, sy);
+    sb = fma(gl[i], db, sb);
+  }
+  const double xl = (Y[(long long)m * ns + s] - cm * sy) / (fma(cm, sigma, mu) - cm * sb);
+  // second sweep: x_i = Dinv y - Dinv (C_m g) x_l ; rows of a 2x2 block are
+  // written together (both read before either is overwritten).
+  for (int i = 0; i < m; ++i) {
+    const int j = partner[i];
+    if (j < i) continue;
+    const double a = fma(cm, diag[i], mu), e = fma(cm, diag[j], mu);
+    const double b = cm * off[i], c = cm * off[j];
+    const double inv = 1.0 / (a * e - b * c);
+    const double yi = Y[(long long)i * ns + s], yj = Y[(long long)j * ns + s];
+    const double gi = cm * gb[i] * xl, gj = cm * gb[j] * xl;
+    const double ri = yi - gi, rj = yj - gj;
+    // rows i (own diag a, partner diag e) and j (own diag e, partner diag a)
+    Y[(long long)i * ns + s] = (e * ri - b * rj) * inv;
+    if (j != i) Y[(long long)j * ns + s] = (a * rj - c * ri) * inv;
+  }
+  Y[(long long)m * ns + s] = xl;
+}
+
+static cudaError_t mode_strided(const double* A, const double* in, double* out, int n, long long inner,
+                                long long outer, cudaStream_t st) {
+  // out[o, i, c] = sum_j A[i, j] in[o, j, c]
+  GemmArgs g{A, in, out, n, (int)inner, n, n, inner, inner, 0, (long long)n * inner, (long long)n * inner};
+  return launch_dgemm(g, (int)outer, st);
+}
+
+static cudaError_t mode_contig(const double* Bm, const double* in, double* out, int n, long long rows,
+                               cudaStream_t st) {
+  // out[r, i] = sum_j in[r, j] Bm[j, i]
+  GemmArgs g{in, Bm, out, (int)rows, n, n, n, n, n, 0, 0, 0};
+  return launch_dgemm(g, 1, st);
+}
+
+}  // namespace mi
+
+using namespace mi;
+
+extern "C" {
+
+int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double react, const double* Q,
+                const double* diag, const double* off, const int* partner, const double* g,
+                const double* glow, double sigma) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  MI_CUDA(cudaSetDevice(c->device));
+  const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
+  int rc;
+  for (int l = 0; l < 3; ++l) {
+    const int nl = c->n[l];
+    if ((rc = dalloc(c->Us[l], (size_t)nl * nl)) || (rc = dalloc(c->UsT[l], (size_t)nl * nl)) ||
+        (rc = dalloc(c->lam[l], nl)))
+      return rc;
+    std::vector<double> u(nl * nl), ut(nl * nl), lm(nl, 0.0);
+    if (l < c->d) {
+      for (int i = 0; i < nl; ++i)
+        for (int j = 0; j < nl; ++j) {
+          u[i * nl + j] = U[((size_t)l * nmax + i) * nmax + j];
+          ut[j * nl + i] = u[i * nl + j];
+        }
+      for (int i = 0; i < nl; ++i) lm[i] = lam[(size_t)l * nmax + i];
+    } else {
+      u[0] = ut[0] = 1.0;
+    }
+    MI_CUDA(cudaMemcpy(c->Us[l].p, u.data(), sizeof(double) * nl * nl, cudaMemcpyHostToDevice));
+    MI_CUDA(cudaMemcpy(c->UsT[l].p, ut.data(), sizeof(double) * nl * nl, cudaMemcpyHostToDevice));
+    MI_CUDA(cudaMemcpy(c->lam[l].p, lm.data(), sizeof(double) * nl, cudaMemcpyHostToDevice));
+  }
+  const int nt = c->nt, m = nt - 1;
+  std::vector<double> qt((size_t)nt * nt);
+  for (int i = 0; i < nt; ++i)
+    for (int j = 0; j < nt; ++j) qt[(size_t)j * nt + i] = Q[(size_t)i * nt + j];
+  if ((rc = dalloc(c->Q, (size_t)nt * nt)) || (rc = dalloc(c->QT, (size_t)nt * nt)) ||
+      (rc = dalloc(c->pen_diag, m)) || (rc = dalloc(c->pen_off, m)) || (rc = dalloc(c->pen_g, m)) ||
+      (rc = dalloc(c->pen_glow, m)) || (rc = dalloc(c->pc_t1, c->N)) || (rc = dalloc(c->pc_t2, c->N)))
+    return rc;
+  for (int i = 0; i < m; ++i)
+    MI_REQUIRE(partner[i] >= 0 && partner[i] < m && partner[partner[i]] == i, MI_ERR_ARG,
+               "pencil partner table is not an involution");
+  MI_CUDA(cudaMemcpy(c->Q.p, Q, sizeof(double) * nt * nt, cudaMemcpyHostToDevice));
+  MI_CUDA(cudaMemcpy(c->QT.p, qt.data(), sizeof(double) * nt * nt, cudaMemcpyHostToDevice));
+  MI_CUDA(cudaMemcpy(c->pen_diag.p, diag, sizeof(double) * m, cudaMemcpyHostToDevice));
+  MI_CUDA(cudaMemcpy(c->pen_off.p, off, sizeof(double) * m, cudaMemcpyHostToDevice));
+  MI_CUDA(cudaMemcpy(c->pen_g.p, g, sizeof(double) * m, cudaMemcpyHostToDevice));
+  MI_CUDA(cudaMemcpy(c->pen_glow.p, glow, sizeof(double) * m, cudaMemcpyHostToDevice));
+  if (!c->pen_partner) MI_CUDA(cudaMalloc(&c->pen_partner, sizeof(int) * m));
+  MI_CUDA(cudaMemcpy(c->pen_partner, partner, sizeof(int) * m, cudaMemcpyHostToDevice));
+  c->pen_sigma = sigma;
+  c->pc_cm = cm;
+  c->pc_react = react;
+  c->pc_ready = true;
+  return MI_OK;
+}
+
+int mi_pc_apply(mi_ctx* c, const double* r, double* z) {
+  MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
+  cudaStream_t st = c->stream;
+  const int n1 = c->n[0], n2 = c->n[1], n3 = c->n[2], nt = c->nt;
+  const long long ns = c->ns, N = c->N;
+  double* t1 = c->pc_t1.p;
+  double* t2 = c->pc_t2.p;
+  // forward: U_1^T (x), U_2^T (y), U_3^T (z), Q^T (t)
+  const double* cur = r;
+  double* bufs[2] = {t1, t2};
+  int k = 0;
+  auto next = [&]() { double* b = bufs[k]; k ^= 1; return b; };
+  if (n1 > 1) { double* o = next(); MI_CUDA(mode_contig(c->Us[0].p, cur, o, n1, N / n1, st)); cur = o; }
+  if (n2 > 1) { double* o = next(); MI_CUDA(mode_strided(c->UsT[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
+  if (n3 > 1) { double* o = next(); MI_CUDA(mode_strided(c->UsT[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
+  { double* o = next(); MI_CUDA(mode_strided(c->QT.p, cur, o, nt, ns, 1, st)); cur = o; }
+  arrowhead_solve<<<(unsigned)((ns + 127) / 128), 128, 0, st>>>(
+      const_cast<double*>(cur), c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p,
+      c->pen_partner, c->pen_g.p, c->pen_glow.p, c->pen_sigma, c->pc_cm, c->pc_react, n1, n2, nt, ns);
+  MI_CHECK_LAUNCH("arrowhead_solve");
+  // inverse: Q (t), U_3 (z), U_2 (y), U_1 (x); the last stage writes z
+  const bool more_z = n3 > 1, more_y = n2 > 1, more_x = n1 > 1;
+  auto dst = [&](bool last) { return last ? z : next(); };
+  { double* o = dst(!more_z && !more_y && !more_x); MI_CUDA(mode_strided(c->Q.p, cur, o, nt, ns, 1, st)); cur = o; }
+  if (more_z) { double* o = dst(!more_y && !more_x); MI_CUDA(mode_strided(c->Us[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
+  if (more_y) { double* o = dst(!more_x); MI_CUDA(mode_strided(c->Us[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
+  if (more_x) { double* o = dst(true); MI_CUDA(mode_contig(c->UsT[0].p, cur, o, n1, N / n1, st)); cur = o; }
+  return MI_OK;
+}
+
+}  // extern "C"

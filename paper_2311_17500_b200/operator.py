@@ -1,0 +1,161 @@
+"""Device operator of the potential system (drop-in for the reference's
+``KroneckerOperator`` as built by ``_Workspace.operator``, solver.py:213-236).
+
+A = C_m W_t (x) M_s + M_t (x) (sum_a sigma_a K_a + r M_s)        [Galerkin]
+  + sum_r C_m s_r (sum_k S^t_{r,k}) (x) S^s_r                    [Spline Upwind]
+  + M_R                                   [reaction, when the iterate != 0]
+
+with r = c1 * a at the zero iterate (solver.py:220-223) and M_R the q=p+1
+reaction mass otherwise (assembly.py:287-347).  Each Kronecker term is one
+device "channel" (see csrc/op.cu).
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceContext, dptr, host_ptr
+from .factors import hat_triple, lowrank_factorize, su_time_bands, upwind_weights
+from .spaces import time_factors, to_band, univariate_factors
+
+
+def _is_zero(v):
+    if v is None:
+        return True
+    if isinstance(v, torch.Tensor):
+        return not bool(torch.any(v != 0).item())
+    return not np.any(v)
+
+
+class Stabilization:
+    """Spline Upwind data for the operator (stabilization.py:401-489).
+
+    From the N_t x N_s indicator: upwind weights tau_k, truncated SVD at
+    ``tol`` (rank R), per-rank time bands C_m s_r sum_k S^t_{r,k}, and the
+    spatial factors theta_r with the 1D hat triple products that generate
+    the stencils of S^s_r on the device.
+    """
+
+    def __init__(self, space_time, indicator, tol=0.1, capacitance=1.0, lengths=None):
+        st = space_time
+        self.tau = upwind_weights(st.time)
+        self.lowrank = lowrank_factorize(indicator, tol)
+        self.rank = self.lowrank.rank
+        d = len(st.spatial)
+        L = np.ones(d) if lengths is None else np.asarray(lengths, float)
+        if self.rank:
+            self.time_bands = su_time_bands(st, self.tau, self.lowrank, capacitance)
+            self.theta = np.ascontiguousarray(self.lowrank.space_factors.T)
+            nmax = max(s.dimension for s in st.spatial)
+            tabs = [hat_triple(s, L[l]) for l, s in enumerate(st.spatial)]
+            self.ko = tabs[0][1]
+            p = st.spatial[0].degree
+            H = np.zeros((d, nmax, 2 * p + 1, 2 * self.ko + 1))
+            for l, (h, _) in enumerate(tabs):
+                H[l, :h.shape[0]] = h
+            self.H = H
+        else:
+            self.time_bands = np.zeros((0, st.num_time, 2 * st.time.degree + 1))
+
+
+class KroneckerOperator:
+    """Device operator A (see module docstring).
+
+    ``matvec(x)`` accepts a numpy array (returns numpy; the host<->device
+    copies are part of the call) or a CUDA tensor (returns a CUDA tensor,
+    no host traffic).  Size mismatch raises ValueError like
+    assembly.py:431-436.
+    """
+
+    def __init__(self, space_time, final_time, capacitance=1.0, diffusion=1e-4, constants=None,
+                 u=None, w=None, stabilization=None, lengths=None, device=0, context=None):
+        st = space_time
+        self.ctx = context if context is not None else DeviceContext(st, device)
+        ctx = self.ctx
+        self.space_time = st
+        self.num_time, self.num_space = ctx.nt, ctx.ns
+        consts = dict(c1=0.26, a=0.13, c2=0.1) if constants is None else dict(constants)
+        d, p, pt = ctx.d, ctx.p, ctx.pt
+        L = np.ones(d) if lengths is None else np.asarray(lengths, float)
+        sig = np.atleast_1d(np.asarray(diffusion, float))
+        sig = np.repeat(sig, d) if sig.size == 1 else sig
+        if sig.size != d:
+            raise ValueError("diffusion must be a scalar or one value per direction")
+        zero_iterate = _is_zero(u) and _is_zero(w)
+        react = consts["c1"] * consts["a"] if zero_iterate else 0.0
+        self.zero_iterate = zero_iterate
+        stab = stabilization
+        R = 0 if stab is None else stab.rank
+        nchan = 2 + R
+        self.nchan = nchan
+        ctx.bind_stream()
+        _lib.call("mi_op_setup", ctx.handle, nchan)
+        # time bands: c0 = C_m W_t, c1 = M_t, SU ranks
+        Wt, Mt = time_factors(st, final_time)
+        bands = np.zeros((nchan, ctx.nt, 2 * pt + 1))
+        bands[0] = capacitance * to_band(Wt, pt)
+        bands[1] = to_band(Mt, pt)
+        if R:
+            bands[2:] = stab.time_bands
+        bands = np.ascontiguousarray(bands)
+        _lib.call("mi_op_set_time_bands", ctx.handle, host_ptr(bands))
+        # spatial Kronecker channels
+        nmax = max(ctx.n)
+        Mb, Kb = [], []
+        for l, s in enumerate(st.spatial):
+            M, K, _ = univariate_factors(s)
+            Mb.append(L[l] * to_band(M, p))
+            Kb.append(to_band(K, p) / L[l])
+
+        def pack(rows):
+            out = np.zeros((len(rows), d, nmax, 2 * p + 1))
+            for t, row in enumerate(rows):
+                for l in range(d):
+                    out[t, l, :row[l].shape[0]] = row[l]
+            return np.ascontiguousarray(out)
+
+        c0 = np.array([1.0])
+        b0 = pack([Mb])
+        _lib.call("mi_op_set_kron_channel", ctx.handle, 0, 1, host_ptr(c0), host_ptr(b0))
+        rows, coefs = [], []
+        for a in range(d):
+            rows.append([Kb[l] if l == a else Mb[l] for l in range(d)])
+            coefs.append(sig[a])
+        if react != 0.0:
+            rows.append(list(Mb))
+            coefs.append(react)
+        c1 = np.asarray(coefs, float)
+        b1 = pack(rows)
+        _lib.call("mi_op_set_kron_channel", ctx.handle, 1, len(rows), host_ptr(c1), host_ptr(b1))
+        for r in range(R):
+            th = np.ascontiguousarray(stab.theta[r])
+            H = np.ascontiguousarray(stab.H)
+            _lib.call("mi_op_set_su_channel", ctx.handle, 2 + r, host_ptr(th), host_ptr(H), stab.ko)
+        if not zero_iterate:
+            from .reaction import set_reaction
+            set_reaction(ctx, st, final_time, consts, u, w, L)
+
+    @property
+    def shape(self):
+        n = self.num_time * self.num_space
+        return (n, n)
+
+    def apply_device(self, x, y):
+        """y = A x for contiguous fp64 CUDA tensors of length N (no checks)."""
+        self.ctx.bind_stream()
+        _lib.call("mi_op_apply", self.ctx.handle, dptr(x), dptr(y))
+
+    def matvec(self, x):
+        n = self.shape[0]
+        size = x.numel() if isinstance(x, torch.Tensor) else np.asarray(x).size
+        if size != n:
+            raise ValueError("dimension mismatch: operator of size %d applied to vector of size %d"
+                             % (n, size))
+        xd = self.ctx.to_device(x)
+        yd = self.ctx.empty(n)
+        self.apply_device(xd, yd)
+        if isinstance(x, torch.Tensor):
+            return yd
+        return yd.cpu().numpy()
+
+    __call__ = matvec

@@ -1,0 +1,90 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference-pinned oracle
+and the reference's own golden vectors.
+
+Tolerances (fp64): component applies <= 1e-12 relative; GMRES iteration
+counts equal and solutions <= 1e-10 relative (north_star parity bar).
+"""
+
+import numpy as np
+import pytest
+
+from cases import CASES, load, oracle_objects
+
+pytestmark = pytest.mark.gpu
+
+RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def product_objects(g, with_su=True, u=None, w=None):
+    import paper_2311_17500_b200 as mb
+    p = int(g["p"])
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, int(n)) for n in g["ne"]],
+                           mb.SplineSpace.uniform(p, int(g["ne_t"])))
+    sig = np.atleast_1d(g["sigma"])
+    sig = float(sig[0]) if sig.size == 1 else sig
+    stab = mb.Stabilization(st, g["theta"], float(g["su_tol"]), 1.0) if with_su else None
+    op = mb.KroneckerOperator(st, float(g["T"]), 1.0, sig, RM, u=u, w=w, stabilization=stab)
+    P = mb.FastDiagPreconditioner.build(st, float(g["T"]), 1.0, sig, 0.13 * 0.26, context=op.ctx)
+    return st, op, P
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_separable_operator(name):
+    g = load(name)
+    _, op, _ = product_objects(g, with_su=False)
+    assert rel(op.matvec(g["x"]), g["y_sep"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_full_operator_zero_iterate(name):
+    g = load(name)
+    _, op, _ = product_objects(g)
+    assert rel(op.matvec(g["x"]), g["y_a"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_preconditioner(name):
+    g = load(name)
+    _, op, P = product_objects(g)
+    assert rel(P.apply(g["x"]), g["z_pc"]) < 1e-12
+    assert rel(P.apply(op.matvec(g["x"])), g["z_pc_ya"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gmres_matches_reference(name):
+    import paper_2311_17500_b200 as mb
+    g = load(name)
+    _, op, P = product_objects(g)
+    x, it, hist = mb.gmres(op, g["rhs"], precond=P, tol=1e-8, max_iter=400)
+    assert it == int(g["gm_a_it"])
+    assert rel(x, g["gm_a_x"]) < 1e-10
+    np.testing.assert_allclose(hist, g["gm_a_hist"], rtol=1e-6, atol=1e-14)
+
+
+def test_dimension_mismatch_and_torch_inputs():
+    import torch
+    g = load("case_2d_p2")
+    _, op, P = product_objects(g)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        op.matvec(np.zeros(op.shape[0] + 1))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        P.apply(np.zeros(3))
+    xt = torch.from_numpy(g["x"]).cuda()
+    yt = op.matvec(xt)
+    assert yt.is_cuda and rel(yt.cpu().numpy(), g["y_a"]) < 1e-12
+
+
+def test_gmres_known_answers_device():
+    """tests/test_linalg.py:177-214 semantics on the device path."""
+    import paper_2311_17500_b200 as mb
+    g = load("case_2d_p2")
+    _, op, P = product_objects(g)
+    x, it, hist = mb.gmres(op, np.zeros(op.shape[0]), precond=P)
+    assert it == 0 and hist == [0.0] and not np.any(x)
+    with pytest.raises(mb.NonConvergenceError) as e:
+        mb.gmres(op, g["rhs"], precond=P, tol=1e-14, max_iter=3)
+    assert e.value.iterations == 3 and len(e.value.residuals) == 4
