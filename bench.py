@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark: space-time DoF/s of the operator+preconditioner apply z = P^-1 (A x).
+
+Workload (BASELINE.json configs[3], the apply micro-benchmark): 3D space x
+time, p = 3, 96^3 space elements x 192 time elements (N = 188,238,006 DoFs,
+1.5 GB per fp64 vector), Spline Upwind on (seeded front indicator of SURVEY
+8(d), low-rank tol 0.1), zero-iterate reaction (a*c1 M_t x M_s),
+fast-diagonalisation preconditioner.  One step = one z = P^-1 (A x) on a
+seeded x ~ U[-1, 1].  Inputs/outputs are 1.5 GB each (> 126 MB L2), so no
+L2 flush is needed between steps.
+
+Arms:
+  (default)          this package's CUDA path, device-resident vectors ("value"),
+                     plus "e2e" through the public API from pinned host memory.
+  --impl reference   the reference algorithm on the host CPU: the oracle port
+                     (oracle/, a restatement of the reference pinned against
+                     its golden vectors) at a bounded sample of the workload.
+
+Multi-GPU (torchrun, N > 1): the time-sharded solve is not in this round;
+each rank runs an independent replica of the full workload ("scaling":
+"weak", value = all ranks' DoFs / max-over-ranks time).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time DoF/s of operator+preconditioner apply"
+CFG = dict(name="cfg4_apply_microbench", d=3, p=3, ne=96, ne_t=192, sigma=1e-3, su_tol=0.1)
+SAMPLE = dict(ne=12, ne_t=24)       # bounded CPU sample (same d, p, physics, SU)
+RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ne", type=int, default=CFG["ne"])
+    ap.add_argument("--ne-t", type=int, default=CFG["ne_t"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def front_indicator_np(tg, g1, ns):
+    """SURVEY 8(d) seeded SU indicator, computed without the oracle."""
+    gs = np.tile(g1, ns // g1.size)
+    th = np.exp(-(((gs[None, :] - 0.2 - 0.5 * tg[:, None]) / 0.08) ** 2))
+    return np.clip(th, 0.0, 1.0)
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_sample_rate(steps, warmup, ne, ne_t):
+    """Reference algorithm (oracle port) on the host: DoF/s of P^-1 (A x)."""
+    from oracle import problem as oprob
+    from oracle.splines import make_space_time
+    st = make_space_time(CFG["d"], CFG["p"], ne, ne_t)
+    th = oprob.front_indicator(st)
+    su, lr, _ = oprob.su_from_indicator(st, th, CFG["su_tol"])
+    op = oprob.operator_terms(st, 1.0, 1.0, CFG["sigma"], RM, su_terms=su)
+    pc = oprob.preconditioner(st, 1.0, 1.0, CFG["sigma"], RM)
+    x = np.random.default_rng(0).uniform(-1, 1, st.num_dof)
+    for _ in range(warmup):
+        pc.apply(op.matvec(x))
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        pc.apply(op.matvec(x))
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    sample = ("oracle port of the reference (CSR Kronecker matvec + complex FD apply), d=3 p=3 %d^3 x %d "
+              "elements (N=%d, SU rank %d), %d timed applies" % (ne, ne_t, st.num_dof, lr.rank, steps))
+    return st.num_dof * steps / tot, tot / steps, sample, st.num_dof
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    rate, sec, sample, n = cpu_sample_rate(args.steps, max(args.warmup, 1), SAMPLE["ne"], SAMPLE["ne_t"])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "DoF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+        "config": {"workload": CFG["name"] + " (bounded CPU sample)", "d": 3, "p": 3,
+                   "sample_mesh": [SAMPLE["ne"]] * 3 + [SAMPLE["ne_t"]], "dofs": n},
+        "cpu_baseline": {"value": rate, "unit": "DoF/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+class ClockSampler:
+    def __init__(self, index):
+        self.proc = None
+        self.index = index
+        self.path = os.path.join(ROOT, "gpurun_out", "clocks_bench.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        loaded = sorted(sm)[len(sm) // 4:] if len(sm) > 4 else sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak_tflops(torch, dev):
+    """Measured FP64 tensor-core throughput (cuBLAS DGEMM 4096^3, best of 5)."""
+    n = 4096
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize(dev)
+    best = 1e30
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2311_17500_b200 as mb
+    from paper_2311_17500_b200.spaces import greville
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    d, p = CFG["d"], CFG["p"]
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, args.ne) for _ in range(d)],
+                           mb.SplineSpace.uniform(p, args.ne_t))
+    N = st.num_dof
+    t_setup = time.perf_counter()
+    theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
+    stab = mb.Stabilization(st, theta, CFG["su_tol"], 1.0)
+    del theta
+    op = mb.KroneckerOperator(st, 1.0, 1.0, CFG["sigma"], RM, stabilization=stab, device=local)
+    P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, CFG["sigma"], RM["a"] * RM["c1"], context=op.ctx)
+    t_setup = time.perf_counter() - t_setup
+    ctx = op.ctx
+    x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).to(dev)
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+
+    def step():
+        op.apply_device(x, y)
+        P.apply_device(y, z)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    peak64 = fp64_peak_tflops(torch, dev)
+    ctx.read_profile(reset=True)
+    ctx.profiling(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = ctx.read_profile(reset=True)
+    ctx.profiling(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = N * args.steps * world / (ms_max * 1e-3)
+
+    # ---- e2e through the public API: pinned host x -> device -> A, P^-1 -> pinned host z
+    xh = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).pin_memory()
+    zh = torch.empty(N, dtype=torch.float64).pin_memory()
+    for _ in range(1):
+        zh.copy_(P.apply(op.matvec(xh.to(dev, non_blocking=True))), non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2_steps = max(1, min(args.steps, 5))
+    if world > 1:
+        dist.barrier()
+    e2.record()
+    for _ in range(e2_steps):
+        zh.copy_(P.apply(op.matvec(xh.to(dev, non_blocking=True))), non_blocking=True)
+    e3.record()
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = N * e2_steps * world / (float(te.item()) * 1e-3)
+
+    # ---- roofline of the dominant kernel class (live CUDA events over the timed region)
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms = prof[dom][0] / args.steps
+    nsten = (2 * p + 1) ** d
+    F_dom = {"op_stencil": 2.0 * op.nchan * nsten * N,
+             "pc_spatial": 2.0 * 2 * sum(n for n in ctx.n) * N,
+             "pc_time": 2.0 * 2 * ctx.nt * N,
+             "pc_arrowhead": 20.0 * N}.get(dom)
+    peaks = measured_peaks()
+    roof = {"kernel": dom, "bound": "tensor", "unit": "TFLOP/s", "peak": peak64,
+            "peak_source": "FP64 cuBLAS DGEMM 4096^3 measured live in this run (FP64 DMMA/DFMA pipes)",
+            "achieved": (F_dom / (dom_ms * 1e-3) / 1e12) if F_dom else None,
+            "flops_per_step": F_dom, "ms_per_step": dom_ms, "traffic": None}
+    roof["frac"] = roof["achieved"] / peak64 if roof["achieved"] else None
+    R = stab.rank
+    F_sep = 10 * 2 * (2 * p + 1)
+    F_su = R * (2 * (2 * p + 1) + 2 * nsten)
+    F_pc = 4 * ctx.nt + 4 * sum(ctx.n) + 40
+    B_alg = 16 + R * nsten * st.num_space * 8 / N
+    apply_roof = {"flops_per_dof": F_sep + F_su + F_pc, "bytes_per_dof": B_alg,
+                  "achieved_tflops": (F_sep + F_su + F_pc) * value / world / 1e12,
+                  "frac_of_fp64_peak": (F_sep + F_su + F_pc) * value / world / 1e12 / peak64,
+                  "hbm_floor_ms": B_alg * N / (peaks.get("hbm_gbs", 6550.4) * 1e9) * 1e3,
+                  "note": "SURVEY 8(d) algorithmic counts, real-block time pencil (4 N_t)"}
+    launches = sum(v[1] for v in prof.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded x ~ U[-1,1])",
+        "config": {"workload": CFG["name"], "d": d, "p": p, "mesh": [args.ne] * 3 + [args.ne_t], "dofs": N,
+                   "su_rank": R, "channels": op.nchan, "reaction": "zero-iterate a*c1 M_t x M_s",
+                   "l2": "inputs 1.5 GB > 126 MB L2 (no flush needed)",
+                   "parallelism": "replicas" if world > 1 else "single GPU", "setup_s": t_setup},
+        "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+                "path": "KroneckerOperator.matvec + FastDiagPreconditioner.apply on CUDA tensors from pinned host"},
+        "roofline": roof,
+        "apply_roofline": apply_roof,
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, sec, sample, _ = cpu_sample_rate(3, 1, SAMPLE["ne"], SAMPLE["ne_t"])
+        line["cpu_baseline"] = {"value": rate, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -41,6 +41,14 @@ int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx
 int mi_ctx_destroy(mi_ctx* ctx);
 int mi_ctx_set_stream(mi_ctx* ctx, void* cuda_stream);
 
+/* Per-kernel-class CUDA-event timing (bench/roofline support; no reference
+ * counterpart).  Slots: 0 op stencil, 1 op time filter, 2 op reaction,
+ * 3 pc spatial transforms, 4 pc time transforms, 5 pc arrowhead, 6 krylov,
+ * 7 setup.  mi_prof_read syncs the stream and returns accumulated ms and
+ * launch counts (arrays of 8); reset != 0 clears them. */
+int mi_prof_enable(mi_ctx* ctx, int on);
+int mi_prof_read(mi_ctx* ctx, double* ms, long long* launches, int reset);
+
 /* ---------------------------------------------------------------------
  * Operator A  (replaces KroneckerOperator + two_factor_matvec,
  * assembly.py:401-444 / tensorops.py:45-56, with the term list of

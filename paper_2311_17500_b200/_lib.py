@@ -23,6 +23,8 @@ _SIGS = {
     "mi_ctx_create": ([_c_int, _c_int, _vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
     "mi_ctx_destroy": ([_vp], _c_int),
     "mi_ctx_set_stream": ([_vp, _vp], _c_int),
+    "mi_prof_enable": ([_vp, _c_int], _c_int),
+    "mi_prof_read": ([_vp, _vp, _vp, _c_int], _c_int),
     "mi_op_setup": ([_vp, _c_int], _c_int),
     "mi_op_set_time_bands": ([_vp, _vp], _c_int),
     "mi_op_set_kron_channel": ([_vp, _c_int, _c_int, _vp, _vp], _c_int),
@@ -42,6 +44,9 @@ _SIGS = {
 }
 
 EXPORTED = tuple(_SIGS)
+
+PROF_SLOTS = ("op_stencil", "op_time_filter", "op_reaction", "pc_spatial", "pc_time", "pc_arrowhead",
+              "krylov", "setup")
 
 _lib = None
 

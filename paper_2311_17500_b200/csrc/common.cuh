@@ -36,6 +36,19 @@ int fail(const char* what, cudaError_t err);
     if (!(cond)) { ::mi::set_error(msg); return (code); }               \
   } while (0)
 
+enum ProfSlot { PROF_OP_STENCIL = 0, PROF_OP_TFILTER, PROF_OP_REACTION, PROF_PC_SPATIAL, PROF_PC_TIME,
+                PROF_PC_ARROW, PROF_KRYLOV, PROF_BUILD, PROF_NSLOTS };
+
+// Records a CUDA event pair around the launches of one slot when profiling
+// is on; always counts launches.
+struct ProfScope {
+  mi_ctx* c;
+  int slot;
+  cudaEvent_t e1 = nullptr;
+  ProfScope(mi_ctx* ctx, int s, int nlaunch = 1);
+  ~ProfScope();
+};
+
 struct DeviceBuf {
   double* p = nullptr;
   size_t n = 0;
@@ -79,6 +92,14 @@ struct mi_ctx {
   int* pen_partner = nullptr;   // (nt-1)
   double pen_sigma = 0, pc_cm = 1, pc_react = 0;
   mi::DeviceBuf pc_t1, pc_t2;   // N each
+
+  // ---- profiling: per-slot accumulated ms and launch counts
+  bool prof_on = false;
+  long long launches[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  struct EvRec { int slot; cudaEvent_t a, b; };
+  std::vector<EvRec> prof_events;
+  std::vector<cudaEvent_t> prof_pool;
+  double prof_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   // ---- Krylov scratch
   mi::DeviceBuf partials;       // reduction partials

@@ -37,9 +37,64 @@ void dfree(DeviceBuf& b) {
   b.n = 0;
 }
 
+static cudaEvent_t take_event(mi_ctx* c) {
+  if (!c->prof_pool.empty()) {
+    cudaEvent_t e = c->prof_pool.back();
+    c->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+ProfScope::ProfScope(mi_ctx* ctx, int s, int nlaunch) : c(ctx), slot(s) {
+  c->launches[s] += nlaunch;
+  if (c->prof_on) {
+    e1 = take_event(c);
+    cudaEventRecord(e1, c->stream);
+  }
+}
+
+ProfScope::~ProfScope() {
+  if (e1) {
+    cudaEvent_t e2 = take_event(c);
+    cudaEventRecord(e2, c->stream);
+    c->prof_events.push_back({slot, e1, e2});
+  }
+}
+
 }  // namespace mi
 
 extern "C" {
+
+int mi_prof_enable(mi_ctx* c, int on) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  c->prof_on = on != 0;
+  return MI_OK;
+}
+
+int mi_prof_read(mi_ctx* c, double* ms, long long* launches, int reset) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->prof_events) {
+    float t = 0.f;
+    MI_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    c->prof_ms[r.slot] += t;
+    c->prof_pool.push_back(r.a);
+    c->prof_pool.push_back(r.b);
+  }
+  c->prof_events.clear();
+  for (int s = 0; s < mi::PROF_NSLOTS; ++s) {
+    if (ms) ms[s] = c->prof_ms[s];
+    if (launches) launches[s] = c->launches[s];
+    if (reset) {
+      c->prof_ms[s] = 0;
+      c->launches[s] = 0;
+    }
+  }
+  return MI_OK;
+}
 
 int mi_version(void) { return 1; }
 
@@ -95,6 +150,11 @@ int mi_ctx_destroy(mi_ctx* c) {
     mi::dfree(c->lam[l]);
   }
   if (c->pen_partner) cudaFree(c->pen_partner);
+  for (auto& r : c->prof_events) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->prof_pool) cudaEventDestroy(e);
   delete c;
   return MI_OK;
 }

@@ -104,6 +104,7 @@ int mi_dots(mi_ctx* c, long long n, int k, const double* V, long long ldv, const
   if (k == 0) return MI_OK;
   int rc;
   if ((rc = dalloc(c->partials, (size_t)k * KB))) return rc;
+  ProfScope ps(c, PROF_KRYLOV, (k + KG - 1) / KG + 1);
   for (int k0 = 0; k0 < k; k0 += KG) {
     dots_partial<KG><<<KB, KT, 0, c->stream>>>(V, ldv, w, n, k0, k, c->partials.p);
     MI_CHECK_LAUNCH("dots_partial");
@@ -116,6 +117,7 @@ int mi_dots(mi_ctx* c, long long n, int k, const double* V, long long ldv, const
 int mi_sub_combination(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* h, double* w) {
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_sub_combination");
   if (k == 0) return MI_OK;
+  ProfScope ps(c, PROF_KRYLOV);
   sub_comb<<<grid_for(n), 256, sizeof(double) * k, c->stream>>>(V, ldv, h, k, w, n);
   MI_CHECK_LAUNCH("sub_comb");
   return MI_OK;
@@ -124,6 +126,7 @@ int mi_sub_combination(mi_ctx* c, long long n, int k, const double* V, long long
 int mi_combination(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* y,
                    const double* x0, double* out) {
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_combination");
+  ProfScope ps(c, PROF_KRYLOV);
   comb<<<grid_for(n), 256, sizeof(double) * (k > 0 ? k : 1), c->stream>>>(V, ldv, y, k, x0, out, n);
   MI_CHECK_LAUNCH("comb");
   return MI_OK;
@@ -131,6 +134,7 @@ int mi_combination(mi_ctx* c, long long n, int k, const double* V, long long ldv
 
 int mi_scale_inv(mi_ctx* c, long long n, const double* x, const double* hnorm, double* out) {
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  ProfScope ps(c, PROF_KRYLOV);
   scale_div<<<grid_for(n), 256, 0, c->stream>>>(x, hnorm, out, n, 0);
   MI_CHECK_LAUNCH("scale_div");
   return MI_OK;
@@ -138,6 +142,7 @@ int mi_scale_inv(mi_ctx* c, long long n, const double* x, const double* hnorm, d
 
 int mi_normalize(mi_ctx* c, long long n, const double* x, const double* nrm2, double* out) {
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  ProfScope ps(c, PROF_KRYLOV);
   scale_div<<<grid_for(n), 256, 0, c->stream>>>(x, nrm2, out, n, 1);
   MI_CHECK_LAUNCH("scale_div");
   return MI_OK;

@@ -273,13 +273,20 @@ int mi_op_apply(mi_ctx* c, const double* x, double* y) {
   dim3 grid((unsigned)((c->ns + 127) / 128), (c->nt + TC - 1) / TC);
   for (int c0 = 0; c0 < c->nchan; c0 += CG) {
     int nc = min(CG, c->nchan - c0);
+    ProfScope ps(c, PROF_OP_STENCIL);
     MI_DISPATCH_DP(c->d, c->p, (stencil_apply<D_, P_, CG, TC><<<grid, 128, 0, c->stream>>>(x, c->stencil.p, c->wbuf.p, c0, nc, g)));
     MI_CHECK_LAUNCH("stencil_apply");
   }
+  {
   dim3 g2((unsigned)((c->ns + 255) / 256), c->nt);
+  ProfScope ps(c, PROF_OP_TFILTER);
   time_filter<<<g2, 256, 0, c->stream>>>(c->wbuf.p, c->tband.p, y, c->nchan, c->pt, g);
   MI_CHECK_LAUNCH("time_filter");
-  if (c->reaction_on) return reaction_apply(c, x, y);
+  }
+  if (c->reaction_on) {
+    ProfScope ps(c, PROF_OP_REACTION);
+    return reaction_apply(c, x, y);
+  }
   return MI_OK;
 }
 

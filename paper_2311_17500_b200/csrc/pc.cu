@@ -145,21 +145,24 @@ int mi_pc_apply(mi_ctx* c, const double* r, double* z) {
   double* bufs[2] = {t1, t2};
   int k = 0;
   auto next = [&]() { double* b = bufs[k]; k ^= 1; return b; };
-  if (n1 > 1) { double* o = next(); MI_CUDA(mode_contig(c->Us[0].p, cur, o, n1, N / n1, st)); cur = o; }
-  if (n2 > 1) { double* o = next(); MI_CUDA(mode_strided(c->UsT[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
-  if (n3 > 1) { double* o = next(); MI_CUDA(mode_strided(c->UsT[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
-  { double* o = next(); MI_CUDA(mode_strided(c->QT.p, cur, o, nt, ns, 1, st)); cur = o; }
+  if (n1 > 1) { double* o = next(); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_contig(c->Us[0].p, cur, o, n1, N / n1, st)); cur = o; }
+  if (n2 > 1) { double* o = next(); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->UsT[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
+  if (n3 > 1) { double* o = next(); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->UsT[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
+  { double* o = next(); ProfScope ps(c, PROF_PC_TIME); MI_CUDA(mode_strided(c->QT.p, cur, o, nt, ns, 1, st)); cur = o; }
+  {
+  ProfScope ps(c, PROF_PC_ARROW);
   arrowhead_solve<<<(unsigned)((ns + 127) / 128), 128, 0, st>>>(
       const_cast<double*>(cur), c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p,
       c->pen_partner, c->pen_g.p, c->pen_glow.p, c->pen_sigma, c->pc_cm, c->pc_react, n1, n2, nt, ns);
   MI_CHECK_LAUNCH("arrowhead_solve");
+  }
   // inverse: Q (t), U_3 (z), U_2 (y), U_1 (x); the last stage writes z
   const bool more_z = n3 > 1, more_y = n2 > 1, more_x = n1 > 1;
   auto dst = [&](bool last) { return last ? z : next(); };
-  { double* o = dst(!more_z && !more_y && !more_x); MI_CUDA(mode_strided(c->Q.p, cur, o, nt, ns, 1, st)); cur = o; }
-  if (more_z) { double* o = dst(!more_y && !more_x); MI_CUDA(mode_strided(c->Us[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
-  if (more_y) { double* o = dst(!more_x); MI_CUDA(mode_strided(c->Us[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
-  if (more_x) { double* o = dst(true); MI_CUDA(mode_contig(c->UsT[0].p, cur, o, n1, N / n1, st)); cur = o; }
+  { double* o = dst(!more_z && !more_y && !more_x); ProfScope ps(c, PROF_PC_TIME); MI_CUDA(mode_strided(c->Q.p, cur, o, nt, ns, 1, st)); cur = o; }
+  if (more_z) { double* o = dst(!more_y && !more_x); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->Us[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
+  if (more_y) { double* o = dst(!more_x); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->Us[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
+  if (more_x) { double* o = dst(true); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_contig(c->UsT[0].p, cur, o, n1, N / n1, st)); cur = o; }
   return MI_OK;
 }
 

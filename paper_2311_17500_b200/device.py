@@ -62,6 +62,16 @@ class DeviceContext:
             self._stream = s
         return s
 
+    def profiling(self, on=True):
+        _lib.call("mi_prof_enable", self.handle, 1 if on else 0)
+
+    def read_profile(self, reset=True):
+        """{slot: (ms, launches)} accumulated since the last reset."""
+        ms = np.zeros(8)
+        n = np.zeros(8, dtype=np.int64)
+        _lib.call("mi_prof_read", self.handle, host_ptr(ms), host_ptr(n), 1 if reset else 0)
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(_lib.PROF_SLOTS)}
+
     def close(self):
         if self.handle:
             _lib.load().mi_ctx_destroy(self.handle)
