@@ -72,8 +72,12 @@ struct mi_ctx {
   int nsten = 0;                // (2p+1)^d stencil points
   mi::DeviceBuf tband;          // nchan x nt x (2pt+1)
   mi::DeviceBuf stencil;        // nchan x nsten x ns
-  mi::DeviceBuf wbuf;           // nchan x N  (S_c x per channel)
+  mi::DeviceBuf wbuf;           // nchan x N  (S_c x per channel), fallback path only
+  mi::DeviceBuf frag;           // fragment-major coefficients for the DMMA path
   bool op_ready = false;
+  bool frag_dirty = true;
+  bool use_dmma = false;
+  int C[3] = {1, 1, 1};         // DMMA cube grid
 
   // ---- reaction correction M_R (variant B)
   bool reaction_on = false;

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace mi {
 
 struct GemmArgs {
@@ -25,21 +27,6 @@ constexpr int GT_M = 64, GT_N = 64, GT_K = 32;
 constexpr int GA_LD = GT_K + 4;   // 36: conflict-free A fragment reads
 constexpr int GB_LD = GT_N + 4;   // 68: conflict-free B fragment reads
 constexpr int GEMM_SMEM = 2 * (GT_M * GA_LD + GT_K * GB_LD) * 8;
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int n = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 __global__ void __launch_bounds__(256) dgemm_dmma(GemmArgs g) {
   extern __shared__ double smem[];

@@ -12,6 +12,7 @@
 // y = sum_c T_c W_c along time (banded), plus the reaction correction.
 #include "common.cuh"
 #include "dispatch.cuh"
+#include "stencil_dmma.cuh"
 
 namespace mi {
 
@@ -206,7 +207,9 @@ int mi_op_setup(mi_ctx* c, int nchan) {
   int rc;
   if ((rc = dalloc(c->tband, (size_t)nchan * c->nt * (2 * c->pt + 1)))) return rc;
   if ((rc = dalloc(c->stencil, (size_t)nchan * c->nsten * c->ns))) return rc;
-  if ((rc = dalloc(c->wbuf, (size_t)nchan * c->N))) return rc;
+  c->use_dmma = c->p <= 3;
+  if (!c->use_dmma && (rc = dalloc(c->wbuf, (size_t)nchan * c->N))) return rc;
+  c->frag_dirty = true;
   MI_CUDA(cudaMemsetAsync(c->stencil.p, 0, sizeof(double) * nchan * c->nsten * c->ns, c->stream));
   MI_CUDA(cudaMemsetAsync(c->tband.p, 0, sizeof(double) * nchan * c->nt * (2 * c->pt + 1), c->stream));
   c->op_ready = true;
@@ -237,6 +240,7 @@ int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
   double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
   MI_DISPATCH_DP(c->d, c->p, (build_kron_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dc.p, db.p, nterms, nmax, g)));
   MI_CHECK_LAUNCH("build_kron_channel");
+  c->frag_dirty = true;
   MI_CUDA(cudaStreamSynchronize(c->stream));
   dfree(dc);
   dfree(db);
@@ -259,15 +263,69 @@ int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H
   double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
   MI_DISPATCH_DP(c->d, c->p, (build_su_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dt.p, dh.p, ko, nmax, g)));
   MI_CHECK_LAUNCH("build_su_channel");
+  c->frag_dirty = true;
   MI_CUDA(cudaStreamSynchronize(c->stream));
   dfree(dt);
   dfree(dh);
   return MI_OK;
 }
 
+static int dmma_prepare(mi_ctx* c) {
+  int rc = MI_OK;
+  MI_DISPATCH_DP(c->d, c->p, {
+    using G = DmmaSten<D_, P_>;
+    c->C[0] = (c->n[0] + G::B1 - 1) / G::B1;
+    c->C[1] = (c->n[1] + G::B2 - 1) / G::B2;
+    c->C[2] = (c->n[2] + G::B3 - 1) / G::B3;
+    const long long ncubes = (long long)c->C[0] * c->C[1] * c->C[2];
+    const long long per_group = ncubes * 8 * G::KS * 32;
+    const int ngroups = (c->nchan + 7) / 8;
+    if ((rc = dalloc(c->frag, (size_t)per_group * ngroups))) return rc;
+    for (int gi = 0; gi < ngroups; ++gi) {
+      const int c0 = gi * 8, nc = min(8, c->nchan - c0);
+      repack_frag<D_, P_><<<(unsigned)((per_group + 255) / 256), 256, 0, c->stream>>>(
+          c->stencil.p, c->frag.p + gi * per_group, c0, nc, c->n[0], c->n[1], c->n[2], c->C[0], c->C[1],
+          c->ns, per_group);
+      MI_CHECK_LAUNCH("repack_frag");
+    }
+    MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)G::SMEM));
+  });
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  c->frag_dirty = false;
+  return rc;
+}
+
+static int dmma_apply(mi_ctx* c, const double* x, double* y) {
+  MI_DISPATCH_DP(c->d, c->p, {
+    using G = DmmaSten<D_, P_>;
+    const long long ncubes = (long long)c->C[0] * c->C[1] * c->C[2];
+    const long long per_group = ncubes * 8 * G::KS * 32;
+    const int ngroups = (c->nchan + 7) / 8;
+    for (int gi = 0; gi < ngroups; ++gi) {
+      DmmaArgs a{x, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
+                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, c->C[0], c->C[1], c->C[2], c->ns};
+      ProfScope ps(c, PROF_OP_STENCIL);
+      stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a);
+      MI_CHECK_LAUNCH("stencil_dmma");
+    }
+  });
+  return MI_OK;
+}
+
 int mi_op_apply(mi_ctx* c, const double* x, double* y) {
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
   MI_REQUIRE(x != y, MI_ERR_ARG, "x and y must not alias");
+  if (c->use_dmma) {
+    int rc;
+    if (c->frag_dirty && (rc = dmma_prepare(c))) return rc;
+    if ((rc = dmma_apply(c, x, y))) return rc;
+    if (c->reaction_on) {
+      ProfScope ps(c, PROF_OP_REACTION);
+      return reaction_apply(c, x, y);
+    }
+    return MI_OK;
+  }
   Dims g = dims_of(c);
   constexpr int CG = 4, TC = 8;
   dim3 grid((unsigned)((c->ns + 127) / 128), (c->nt + TC - 1) / TC);
