@@ -34,13 +34,13 @@ struct DmmaSten {
   static constexpr int H3 = D >= 3 ? B3 + 2 * P : 1;
   static constexpr int HS = H1 * H2 * H3;
   static constexpr int TS = HS + ((4 - HS % 16) + 16) % 16;   // row stride = 4 mod 16 doubles
-  static constexpr int TT = 16;                     // time rows per chunk (2 M-tiles)
+  static constexpr int MT = 3;                      // M-tiles (8 time rows each) per chunk
+  static constexpr int TT = 8 * MT;                 // time rows per chunk
   static constexpr int PTMAX = 4;
   static constexpr int RING = TT + 2 * PTMAX;
   static constexpr int THREADS = 512;
   static constexpr size_t SMEM = (size_t)2 * TT * TS * 8      // X halo, double buffered
-                                 + (size_t)8 * 2 * 32 * 2 * 8  // K-split partials
-                                 + (size_t)8 * 8 * RING * 8    // W ring [ch][pt][row]
+                                 + (size_t)8 * 8 * RING * 8    // W ring [pt][ch][row]
                                  + (size_t)KS * 4 * 4;         // stencil offsets
 };
 
@@ -56,13 +56,16 @@ struct DmmaArgs {
   long long ns;
 };
 
+__device__ __forceinline__ void pair_sync(int id) {
+  asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
+}
+
 template <int D, int P>
 __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   using G = DmmaSten<D, P>;
   extern __shared__ double sm[];
   double* Xs = sm;                                   // [2][TT][TS]
-  double* part = Xs + 2 * G::TT * G::TS;             // [8 pt][2 mt][32][2]
-  double* ring = part + 8 * 2 * 32 * 2;              // [8 ch][8 pt][RING]
+  double* ring = Xs + 2 * G::TT * G::TS;             // [8 pt][8 ch][RING]
   int* offs = reinterpret_cast<int*>(ring + 8 * 8 * G::RING);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -79,12 +82,14 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
     }
     offs[s] = v;
   }
-  for (int e = tid; e < 8 * 8 * G::RING; e += G::THREADS) ring[e] = 0.0;
+  double* myring = ring + pt * 8 * G::RING;          // this point's W ring [ch][row]
+  for (int e = (tid & 63); e < 8 * G::RING; e += 64) myring[e] = 0.0;
 
   // this warp's point
   const int l1 = pt % G::B1, l2 = (pt / G::B1) % G::B2, l3 = pt / (G::B1 * G::B2);
   const int p1 = o1 + l1, p2 = o2 + l2, p3 = o3 + l3;
   const bool pvalid = p1 < a.n1 && p2 < a.n2 && p3 < a.n3;
+  const long long pidx = ((long long)p3 * a.n2 + p2) * a.n1 + p1;
   const int base = (l3 * G::H2 + l2) * G::H1 + l1;
 
   // coefficient fragments for this warp's half of K (registers, whole sweep)
@@ -100,97 +105,94 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
 
   const int nchunks = (a.nt + a.pt + G::TT - 1) / G::TT;
   auto load_chunk = [&](int buf, int t0) {
+    if (t0 >= a.nt) return;
     double* dst = Xs + buf * G::TT * G::TS;
-    for (int e = tid; e < G::TT * G::HS; e += G::THREADS) {
+    const int rows = min(G::TT, a.nt - t0);
+    for (int e = tid; e < rows * G::HS; e += G::THREADS) {
       const int t = e / G::HS, h = e - t * G::HS;
       const int h1 = h % G::H1, h2 = (h / G::H1) % G::H2, h3 = h / (G::H1 * G::H2);
       const int g1 = o1 - P + h1;
       const int g2 = D >= 2 ? o2 - P + h2 : 0;
       const int g3 = D >= 3 ? o3 - P + h3 : 0;
-      const bool v = (t0 + t < a.nt) && g1 >= 0 && g1 < a.n1 && g2 >= 0 && g2 < a.n2 && g3 >= 0 && g3 < a.n3;
+      const bool v = g1 >= 0 && g1 < a.n1 && g2 >= 0 && g2 < a.n2 && g3 >= 0 && g3 < a.n3;
       const double* src = v ? a.x + (long long)(t0 + t) * a.ns + ((long long)g3 * a.n2 + g2) * a.n1 + g1 : a.x;
       cp_async8(dst + t * G::TS + h, src, v);
     }
-    cp_async_commit();
   };
 
   load_chunk(0, 0);
+  cp_async_commit();
   const int W2pt = 2 * a.pt + 1;
+  const int bar_id = 1 + pt;
+  // filter work split: 64 threads of the pair = TT rows x (64/TT) channel slices
+  const int ptid = tid & 63;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int t0 = ch * G::TT;
-    if (ch + 1 < nchunks) {
-      load_chunk((ch + 1) & 1, t0 + G::TT);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    cp_async_wait<0>();
+    __syncthreads();                                  // chunk ch visible; buffer (ch+1)&1 free
+    if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
+    cp_async_commit();
     const double* X = Xs + (ch & 1) * G::TT * G::TS;
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    if (t0 < a.nt) {
+    double acc[G::MT][2];
+#pragma unroll
+    for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+    const int mt_live = t0 < a.nt ? min(G::MT, (a.nt - t0 + 7) / 8) : 0;
+    if (mt_live > 0) {
       const double* xa = X + (lane >> 2) * G::TS + base;
 #pragma unroll
       for (int j = 0; j < G::KH; ++j) {
         const int ks = half * G::KH + j;
         if (ks < G::KS) {
           const int o = offs[ks * 4 + (lane & 3)];
-          const double a0 = xa[o];
-          const double a1 = xa[8 * G::TS + o];
-          dmma(acc[0][0], acc[0][1], a0, breg[j]);
-          dmma(acc[1][0], acc[1][1], a1, breg[j]);
+#pragma unroll
+          for (int m = 0; m < G::MT; ++m)
+            if (m < mt_live) dmma(acc[m][0], acc[m][1], xa[m * 8 * G::TS + o], breg[j]);
         }
       }
     }
-    // K-split reduction: half 1 -> smem, half 0 adds and writes the W ring
-    double* pp = part + (pt * 2) * 64 + lane * 2;
+    // K-split reduction in place in the ring rows of this chunk
+    const int mr = lane >> 2, n0 = 2 * (lane & 3);
     if (half == 1) {
-      pp[0] = acc[0][0];
-      pp[1] = acc[0][1];
-      pp[64] = acc[1][0];
-      pp[65] = acc[1][1];
-    }
-    __syncthreads();
-    if (half == 0) {
-      const int m = lane >> 2, n0 = 2 * (lane & 3);
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int row = 2 * G::PTMAX + mt * 8 + m;
-        ring[((n0)*8 + pt) * G::RING + row] = acc[mt][0] + pp[mt * 64];
-        ring[((n0 + 1) * 8 + pt) * G::RING + row] = acc[mt][1] + pp[mt * 64 + 1];
+      for (int m = 0; m < G::MT; ++m) {
+        const int row = 2 * G::PTMAX + m * 8 + mr;
+        myring[n0 * G::RING + row] = acc[m][0];
+        myring[(n0 + 1) * G::RING + row] = acc[m][1];
       }
     }
-    __syncthreads();
-    // time filter: finalize y[t] for t in [t0 - pt, t0 + TT - pt)
-    if (tid < 8 * G::TT) {
-      const int q = tid / G::TT, tl = tid % G::TT;
+    pair_sync(bar_id);
+    if (half == 0) {
+#pragma unroll
+      for (int m = 0; m < G::MT; ++m) {
+        const int row = 2 * G::PTMAX + m * 8 + mr;
+        myring[n0 * G::RING + row] += acc[m][0];
+        myring[(n0 + 1) * G::RING + row] += acc[m][1];
+      }
+    }
+    pair_sync(bar_id);
+    // time filter: y[t] for t in [t0 - pt, t0 + TT - pt), by the warp pair
+    for (int e = ptid; e < G::TT; e += 64) {
+      const int tl = e;
       const int t = t0 - a.pt + tl;
-      const int q1 = q % G::B1, q2 = (q / G::B1) % G::B2, q3 = q / (G::B1 * G::B2);
-      const int i1 = o1 + q1, i2 = o2 + q2, i3 = o3 + q3;
-      if (t >= 0 && t < a.nt && i1 < a.n1 && i2 < a.n2 && i3 < a.n3) {
+      if (t >= 0 && t < a.nt && pvalid) {
         double v = 0.0;
         for (int c = 0; c < a.nc; ++c) {
           const double* bd = a.band + ((long long)(a.c0 + c) * a.nt + t) * W2pt;
-          const double* rw = ring + (c * 8 + q) * G::RING + (2 * G::PTMAX - a.pt) + tl;
-          // ring row of time t' = t - pt + k is (2*PTMAX + (t' - t0)) = (2*PTMAX - pt + tl - pt + k) ...
-          for (int k = 0; k < W2pt; ++k) v = fma(__ldg(bd + k), rw[k - a.pt], v);
+          const double* rw = myring + c * G::RING + 2 * (G::PTMAX - a.pt) + tl;
+          for (int k = 0; k < W2pt; ++k) v = fma(__ldg(bd + k), rw[k], v);
         }
-        double* dst = a.y + (long long)t * a.ns + ((long long)i3 * a.n2 + i2) * a.n1 + i1;
+        double* dst = a.y + (long long)t * a.ns + pidx;
         if (a.accumulate) *dst += v; else *dst = v;
       }
     }
-    __syncthreads();
-    // shift the ring: keep the last 2*PTMAX rows
-    for (int e = tid; e < 64 * 2 * G::PTMAX; e += G::THREADS) {
-      const int r = e % (2 * G::PTMAX), cp = e / (2 * G::PTMAX);
-      ring[cp * G::RING + r] = ring[cp * G::RING + G::TT + r];
+    pair_sync(bar_id);
+    // shift the ring: keep the last 2*PTMAX rows, clear the rest
+    for (int e = ptid; e < 8 * 2 * G::PTMAX; e += 64) {
+      const int r = e % (2 * G::PTMAX), c = e / (2 * G::PTMAX);
+      myring[c * G::RING + r] = myring[c * G::RING + G::TT + r];
     }
-    for (int e = tid; e < 64 * G::TT; e += G::THREADS) {
-      const int r = e % G::TT, cp = e / G::TT;
-      ring[cp * G::RING + 2 * G::PTMAX + r] = 0.0;
-    }
-    __syncthreads();
+    pair_sync(bar_id);
   }
-  (void)pvalid;
 }
 
 // Repack channel stencils [c][s][i] into the fragment-major layout
