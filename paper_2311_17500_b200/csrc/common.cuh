@@ -74,6 +74,7 @@ struct mi_ctx {
   mi::DeviceBuf stencil;        // nchan x nsten x ns
   mi::DeviceBuf wbuf;           // nchan x N  (S_c x per channel), fallback path only
   mi::DeviceBuf frag;           // fragment-major coefficients for the DMMA path
+  mi::DeviceBuf xt;             // time-innermost copy of the operator input
   bool op_ready = false;
   bool frag_dirty = true;
   bool use_dmma = false;

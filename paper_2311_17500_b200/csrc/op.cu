@@ -281,6 +281,8 @@ static int dmma_prepare(mi_ctx* c) {
     const long long per_group = ncubes * 8 * G::KS * 32;
     const int ngroups = (c->nchan + 7) / 8;
     if ((rc = dalloc(c->frag, (size_t)per_group * ngroups))) return rc;
+    const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
+    if ((rc = dalloc(c->xt, (size_t)ntp * c->ns))) return rc;
     for (int gi = 0; gi < ngroups; ++gi) {
       const int c0 = gi * 8, nc = min(8, c->nchan - c0);
       repack_frag<D_, P_><<<(unsigned)((per_group + 255) / 256), 256, 0, c->stream>>>(
@@ -302,9 +304,16 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
     const long long ncubes = (long long)c->C[0] * c->C[1] * c->C[2];
     const long long per_group = ncubes * 8 * G::KS * 32;
     const int ngroups = (c->nchan + 7) / 8;
+    const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
+    {
+      ProfScope ps(c, PROF_OP_STENCIL);
+      dim3 tg((unsigned)((c->ns + 31) / 32), (ntp + 31) / 32);
+      transpose_time_inner<<<tg, dim3(32, 8), 0, c->stream>>>(x, c->xt.p, c->nt, ntp, c->ns);
+      MI_CHECK_LAUNCH("transpose_time_inner");
+    }
     for (int gi = 0; gi < ngroups; ++gi) {
-      DmmaArgs a{x, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
-                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, c->C[0], c->C[1], c->C[2], c->ns};
+      DmmaArgs a{c->xt.p, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
+                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns};
       ProfScope ps(c, PROF_OP_STENCIL);
       stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a);
       MI_CHECK_LAUNCH("stencil_dmma");

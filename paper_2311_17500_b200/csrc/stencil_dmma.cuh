@@ -24,7 +24,12 @@ template <int D, int P>
 struct DmmaSten {
   static constexpr int W = 2 * P + 1;
   static constexpr int S = D == 3 ? W * W * W : (D == 2 ? W * W : W);
-  static constexpr int KS = (S + 3) / 4;            // k-steps per point
+  // K order: x-offset a1 padded to W1P (multiple of 4) so every k-step covers
+  // 4 consecutive x-offsets of one (a2, a3) row (zero coefficients in the pad)
+  static constexpr int W1P = (W + 3) / 4 * 4;
+  static constexpr int QR = W1P / 4;                // k-steps per stencil row
+  static constexpr int NROW = D == 3 ? W * W : (D == 2 ? W : 1);
+  static constexpr int KS = QR * NROW;              // k-steps per point
   static constexpr int KH = (KS + 1) / 2;           // k-steps per warp (2 warps / point)
   static constexpr int B1 = D == 3 ? 2 : (D == 2 ? 4 : 8);
   static constexpr int B2 = D == 3 ? 2 : (D == 2 ? 2 : 1);
@@ -33,40 +38,75 @@ struct DmmaSten {
   static constexpr int H2 = D >= 2 ? B2 + 2 * P : 1;
   static constexpr int H3 = D >= 3 ? B3 + 2 * P : 1;
   static constexpr int HS = H1 * H2 * H3;
-  static constexpr int TS = HS + ((4 - HS % 16) + 16) % 16;   // row stride = 4 mod 16 doubles
-  static constexpr int MT = 3;                      // M-tiles (8 time rows each) per chunk
+  static constexpr int MT = 2;                      // M-tiles (8 time rows each) per chunk
   static constexpr int TT = 8 * MT;                 // time rows per chunk
+  static constexpr int TSTR = TT + 4;               // smem stride per halo point (= 4 mod 16)
   static constexpr int PTMAX = 4;
-  static constexpr int RING = TT + 2 * PTMAX;
+  static constexpr int BW = 2 * PTMAX + 1;
+  static constexpr int WL = 2 * TT + 2 * PTMAX;     // circular W buffer length (rows)
   static constexpr int THREADS = 512;
-  static constexpr size_t SMEM = (size_t)2 * TT * TS * 8      // X halo, double buffered
-                                 + (size_t)8 * 8 * RING * 8    // W ring [pt][ch][row]
-                                 + (size_t)KS * 4 * 4;         // stencil offsets
+  static constexpr size_t SMEM = (size_t)2 * HS * TSTR * 8       // X halo [buf][h][t]
+                                 + (size_t)2 * 8 * 8 * WL * 8;    // W partials [half][pt][ch][row mod WL]
+  // halo offset of lane-k 0 of k-step ks (lane kl adds kl)
+  static constexpr __host__ __device__ int koff(int ks) {
+    return ((D >= 3 ? (ks / QR) / W : 0) * H2 + (D >= 2 ? (ks / QR) % W : 0)) * H1 + 4 * (ks % QR);
+  }
 };
 
 struct DmmaArgs {
-  const double* x;
+  const double* xt;     // time-innermost copy of x: xt[i * ntp + t]
   const double* frag;   // fragment-major coefficients of this channel group
   const double* band;   // time bands (nchan_total, nt, 2pt+1)
   double* y;
   int c0, nc;           // channel group [c0, c0+nc)
   int pt, accumulate;
-  int n1, n2, n3, nt;
+  int n1, n2, n3, nt, ntp;
   int C1, C2, C3;       // cube grid
   long long ns;
 };
 
-__device__ __forceinline__ void pair_sync(int id) {
-  asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
+// x (nt, ns) -> xt (ns, ntp), zero padded in time; 32x32 smem tiles.
+__global__ void transpose_time_inner(const double* __restrict__ x, double* __restrict__ xt, int nt, int ntp,
+                                     long long ns) {
+  __shared__ double tile[32][33];
+  const long long s0 = (long long)blockIdx.x * 32;
+  const int t0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int t = t0 + r;
+    const long long s = s0 + threadIdx.x;
+    tile[r][threadIdx.x] = (t < nt && s < ns) ? x[(long long)t * ns + s] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long s = s0 + r;
+    const int t = t0 + threadIdx.x;
+    if (s < ns && t < ntp) xt[s * ntp + t] = tile[threadIdx.x][r];
+  }
+}
+
+// One warp's K-half of the DMMA sweep over a time chunk: per k-step two
+// immediate-offset LDS.64 (lane kl reads x-offset 4q+kl: conflict-free) and
+// two DMMAs; no per-step address arithmetic, no branches.
+template <class G, int HALF>
+__device__ __forceinline__ void dmma_sweep(const double* X, const double (&breg)[G::KH],
+                                           double (&acc)[G::MT][2]) {
+#pragma unroll
+  for (int j = 0; j < G::KH; ++j) {
+    const int ks = HALF * G::KH + j;
+    if (ks < G::KS) {
+      const double* xa = X + G::koff(ks) * G::TSTR;
+#pragma unroll
+      for (int m = 0; m < G::MT; ++m) dmma(acc[m][0], acc[m][1], xa[m * 8], breg[j]);
+    }
+  }
 }
 
 template <int D, int P>
 __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   using G = DmmaSten<D, P>;
   extern __shared__ double sm[];
-  double* Xs = sm;                                   // [2][TT][TS]
-  double* ring = Xs + 2 * G::TT * G::TS;             // [8 pt][8 ch][RING]
-  int* offs = reinterpret_cast<int*>(ring + 8 * 8 * G::RING);
+  double* Xs = sm;                                   // [2][HS][TSTR]
+  double* Wp = Xs + 2 * G::HS * G::TSTR;             // [2 half][8 pt][8 ch][WL]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pt = warp >> 1, half = warp & 1;
@@ -74,25 +114,8 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   const int c1 = cube % a.C1, c2 = (cube / a.C1) % a.C2, c3 = cube / (a.C1 * a.C2);
   const int o1 = c1 * G::B1, o2 = c2 * G::B2, o3 = c3 * G::B3;
 
-  for (int s = tid; s < G::KS * 4; s += G::THREADS) {
-    int v = 0;
-    if (s < G::S) {
-      const int a1 = s % G::W, a2 = D >= 2 ? (s / G::W) % G::W : 0, a3 = D >= 3 ? s / (G::W * G::W) : 0;
-      v = (a3 * G::H2 + a2) * G::H1 + a1;
-    }
-    offs[s] = v;
-  }
-  double* myring = ring + pt * 8 * G::RING;          // this point's W ring [ch][row]
-  for (int e = (tid & 63); e < 8 * G::RING; e += 64) myring[e] = 0.0;
+  for (int e = tid; e < 2 * 8 * 8 * G::WL; e += G::THREADS) Wp[e] = 0.0;
 
-  // this warp's point
-  const int l1 = pt % G::B1, l2 = (pt / G::B1) % G::B2, l3 = pt / (G::B1 * G::B2);
-  const int p1 = o1 + l1, p2 = o2 + l2, p3 = o3 + l3;
-  const bool pvalid = p1 < a.n1 && p2 < a.n2 && p3 < a.n3;
-  const long long pidx = ((long long)p3 * a.n2 + p2) * a.n1 + p1;
-  const int base = (l3 * G::H2 + l2) * G::H1 + l1;
-
-  // coefficient fragments for this warp's half of K (registers, whole sweep)
   double breg[G::KH];
   {
     const double* f = a.frag + ((long long)cube * 8 + pt) * G::KS * 32 + lane;
@@ -103,95 +126,89 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
     }
   }
 
-  const int nchunks = (a.nt + a.pt + G::TT - 1) / G::TT;
+  const int W2pt = 2 * a.pt + 1;
+  // ---- async loads of chunk t0: halo tile (16 B copies) + band rows of the
+  constexpr int PAIRS = G::TT / 2;
   auto load_chunk = [&](int buf, int t0) {
     if (t0 >= a.nt) return;
-    double* dst = Xs + buf * G::TT * G::TS;
-    const int rows = min(G::TT, a.nt - t0);
-    for (int e = tid; e < rows * G::HS; e += G::THREADS) {
-      const int t = e / G::HS, h = e - t * G::HS;
+    double* dst = Xs + buf * G::HS * G::TSTR;
+    for (int e = tid; e < G::HS * PAIRS; e += G::THREADS) {
+      const int h = e / PAIRS, pr = e - h * PAIRS;
       const int h1 = h % G::H1, h2 = (h / G::H1) % G::H2, h3 = h / (G::H1 * G::H2);
       const int g1 = o1 - P + h1;
       const int g2 = D >= 2 ? o2 - P + h2 : 0;
       const int g3 = D >= 3 ? o3 - P + h3 : 0;
       const bool v = g1 >= 0 && g1 < a.n1 && g2 >= 0 && g2 < a.n2 && g3 >= 0 && g3 < a.n3;
-      const double* src = v ? a.x + (long long)(t0 + t) * a.ns + ((long long)g3 * a.n2 + g2) * a.n1 + g1 : a.x;
-      cp_async8(dst + t * G::TS + h, src, v);
+      const double* src = v ? a.xt + (((long long)g3 * a.n2 + g2) * a.n1 + g1) * a.ntp + t0 + 2 * pr : a.xt;
+      cp_async16(dst + h * G::TSTR + 2 * pr, src, v);
     }
   };
 
+  // filter item of this thread: (point fq, channel fc, rows fr + 8*hh)
+  const int fc = tid & 7, fr = (tid >> 3) & 7, fq = tid >> 6;
+  const int f1 = o1 + fq % G::B1, f2 = o2 + (fq / G::B1) % G::B2, f3 = o3 + fq / (G::B1 * G::B2);
+  const bool fvalid = f1 < a.n1 && f2 < a.n2 && f3 < a.n3;
+  const long long fidx = ((long long)f3 * a.n2 + f2) * a.n1 + f1;
+  const double* w0 = Wp + (fq * 8 + fc) * G::WL;
+  const double* w1 = Wp + ((8 + fq) * 8 + fc) * G::WL;
+
+  const int base = ((pt / (G::B1 * G::B2)) * G::H2 + (pt / G::B1) % G::B2) * G::H1 + pt % G::B1;
+  const int kl = lane & 3, mrow = lane >> 2;
+  double* wmine = Wp + ((half * 8 + pt) * 8 + 2 * kl) * G::WL;   // channels 2kl, 2kl+1
+
+  const int nchunks = (a.nt + a.pt + G::TT - 1) / G::TT + 1;   // +1: filter of the last chunk
   load_chunk(0, 0);
   cp_async_commit();
-  const int W2pt = 2 * a.pt + 1;
-  const int bar_id = 1 + pt;
-  // filter work split: 64 threads of the pair = TT rows x (64/TT) channel slices
-  const int ptid = tid & 63;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int t0 = ch * G::TT;
     cp_async_wait<0>();
-    __syncthreads();                                  // chunk ch visible; buffer (ch+1)&1 free
+    __syncthreads();                  // X(ch), bands(ch) visible; W rows of chunk ch-1 complete
     if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
     cp_async_commit();
-    const double* X = Xs + (ch & 1) * G::TT * G::TS;
-    double acc[G::MT][2];
+    // ---- time filter of chunk ch-1: y[t], t in [t0 - TT - pt, t0 - pt)
+    if (ch > 0) {
+      const int tp0 = t0 - G::TT;
 #pragma unroll
-    for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-    const int mt_live = t0 < a.nt ? min(G::MT, (a.nt - t0 + 7) / 8) : 0;
-    if (mt_live > 0) {
-      const double* xa = X + (lane >> 2) * G::TS + base;
-#pragma unroll
-      for (int j = 0; j < G::KH; ++j) {
-        const int ks = half * G::KH + j;
-        if (ks < G::KS) {
-          const int o = offs[ks * 4 + (lane & 3)];
-#pragma unroll
-          for (int m = 0; m < G::MT; ++m)
-            if (m < mt_live) dmma(acc[m][0], acc[m][1], xa[m * 8 * G::TS + o], breg[j]);
-        }
-      }
-    }
-    // K-split reduction in place in the ring rows of this chunk
-    const int mr = lane >> 2, n0 = 2 * (lane & 3);
-    if (half == 1) {
-#pragma unroll
-      for (int m = 0; m < G::MT; ++m) {
-        const int row = 2 * G::PTMAX + m * 8 + mr;
-        myring[n0 * G::RING + row] = acc[m][0];
-        myring[(n0 + 1) * G::RING + row] = acc[m][1];
-      }
-    }
-    pair_sync(bar_id);
-    if (half == 0) {
-#pragma unroll
-      for (int m = 0; m < G::MT; ++m) {
-        const int row = 2 * G::PTMAX + m * 8 + mr;
-        myring[n0 * G::RING + row] += acc[m][0];
-        myring[(n0 + 1) * G::RING + row] += acc[m][1];
-      }
-    }
-    pair_sync(bar_id);
-    // time filter: y[t] for t in [t0 - pt, t0 + TT - pt), by the warp pair
-    for (int e = ptid; e < G::TT; e += 64) {
-      const int tl = e;
-      const int t = t0 - a.pt + tl;
-      if (t >= 0 && t < a.nt && pvalid) {
+      for (int hh = 0; hh < G::TT / 8; ++hh) {
+        const int tl = fr + 8 * hh;
+        const int t = tp0 - a.pt + tl;
         double v = 0.0;
-        for (int c = 0; c < a.nc; ++c) {
-          const double* bd = a.band + ((long long)(a.c0 + c) * a.nt + t) * W2pt;
-          const double* rw = myring + c * G::RING + 2 * (G::PTMAX - a.pt) + tl;
-          for (int k = 0; k < W2pt; ++k) v = fma(__ldg(bd + k), rw[k], v);
+        if (fc < a.nc && t >= 0 && t < a.nt) {
+          const double* bd = a.band + ((long long)(a.c0 + fc) * a.nt + t) * W2pt;
+          for (int k = 0; k < W2pt; ++k) {
+            int r = t - a.pt + k + 2 * G::PTMAX;           // row of time t-pt+k (shifted >= 0)
+            r = r % G::WL;
+            v = fma(__ldg(bd + k), w0[r] + w1[r], v);
+          }
         }
-        double* dst = a.y + (long long)t * a.ns + pidx;
-        if (a.accumulate) *dst += v; else *dst = v;
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        if (fc == 0 && t >= 0 && t < a.nt && fvalid) {
+          double* dst = a.y + (long long)t * a.ns + fidx;
+          if (a.accumulate) *dst += v; else *dst = v;
+        }
       }
     }
-    pair_sync(bar_id);
-    // shift the ring: keep the last 2*PTMAX rows, clear the rest
-    for (int e = ptid; e < 8 * 2 * G::PTMAX; e += 64) {
-      const int r = e % (2 * G::PTMAX), c = e / (2 * G::PTMAX);
-      myring[c * G::RING + r] = myring[c * G::RING + G::TT + r];
+    // ---- DMMA sweep of chunk ch into this half's W partial rows
+    if (t0 < a.nt + a.pt) {
+      double acc[G::MT][2];
+#pragma unroll
+      for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+      if (t0 < a.nt) {
+        const double* X = Xs + (ch & 1) * G::HS * G::TSTR + (base + kl) * G::TSTR + mrow;
+        if (half == 0)
+          dmma_sweep<G, 0>(X, breg, acc);
+        else
+          dmma_sweep<G, 1>(X, breg, acc);
+      }
+#pragma unroll
+      for (int m = 0; m < G::MT; ++m) {
+        const int r = (t0 + m * 8 + mrow + 2 * G::PTMAX) % G::WL;
+        wmine[r] = acc[m][0];
+        wmine[G::WL + r] = acc[m][1];
+      }
     }
-    pair_sync(bar_id);
   }
 }
 
@@ -212,9 +229,11 @@ __global__ void repack_frag(const double* __restrict__ sten, double* __restrict_
   const int cc1 = (int)(cube % C1), cc2 = (int)((cube / C1) % C2), cc3 = (int)(cube / ((long long)C1 * C2));
   const int i1 = cc1 * G::B1 + pt % G::B1, i2 = cc2 * G::B2 + (pt / G::B1) % G::B2,
             i3 = cc3 * G::B3 + pt / (G::B1 * G::B2);
-  const int ch = lane >> 2, s = ks * 4 + (lane & 3);
+  const int ch = lane >> 2;
+  const int a1 = 4 * (ks % G::QR) + (lane & 3), row = ks / G::QR;
+  const int s = row * G::W + a1;                   // unpadded stencil index
   double v = 0.0;
-  if (ch < nc && s < G::S && i1 < n1 && i2 < n2 && i3 < n3) {
+  if (ch < nc && a1 < G::W && i1 < n1 && i2 < n2 && i3 < n3) {
     const long long i = ((long long)i3 * n2 + i2) * n1 + i1;
     v = sten[((long long)(c0 + ch) * G::S + s) * ns + i];
   }
