@@ -75,6 +75,8 @@ struct mi_ctx {
   mi::DeviceBuf wbuf;           // nchan x N  (S_c x per channel), fallback path only
   mi::DeviceBuf frag;           // fragment-major coefficients for the DMMA path
   mi::DeviceBuf xt;             // time-innermost copy of the operator input
+  mi::DeviceBuf afr;            // time-filter A fragments (DMMA path)
+  int ntau = 0;
   bool op_ready = false;
   bool frag_dirty = true;
   bool use_dmma = false;

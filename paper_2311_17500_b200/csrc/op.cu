@@ -207,7 +207,7 @@ int mi_op_setup(mi_ctx* c, int nchan) {
   int rc;
   if ((rc = dalloc(c->tband, (size_t)nchan * c->nt * (2 * c->pt + 1)))) return rc;
   if ((rc = dalloc(c->stencil, (size_t)nchan * c->nsten * c->ns))) return rc;
-  c->use_dmma = c->p <= 3;
+  c->use_dmma = c->p <= 3 && c->pt <= 4;
   if (!c->use_dmma && (rc = dalloc(c->wbuf, (size_t)nchan * c->N))) return rc;
   c->frag_dirty = true;
   MI_CUDA(cudaMemsetAsync(c->stencil.p, 0, sizeof(double) * nchan * c->nsten * c->ns, c->stream));
@@ -220,6 +220,7 @@ int mi_op_set_time_bands(mi_ctx* c, const double* bands) {
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_CUDA(cudaMemcpyAsync(c->tband.p, bands, sizeof(double) * c->nchan * c->nt * (2 * c->pt + 1),
                           cudaMemcpyHostToDevice, c->stream));
+  c->frag_dirty = true;
   MI_CUDA(cudaStreamSynchronize(c->stream));
   return MI_OK;
 }
@@ -290,6 +291,14 @@ static int dmma_prepare(mi_ctx* c) {
           c->ns, per_group);
       MI_CHECK_LAUNCH("repack_frag");
     }
+    c->ntau = (c->nt + c->pt + 2 * G::TT) / 8 + 2;
+    if ((rc = dalloc(c->afr, (size_t)ngroups * c->ntau * 1024))) return rc;
+    for (int gi = 0; gi < ngroups; ++gi) {
+      build_filter_frag<<<(c->ntau * 1024 + 255) / 256, 256, 0, c->stream>>>(
+          c->afr.p + (size_t)gi * c->ntau * 1024, c->tband.p, gi * 8, min(8, c->nchan - gi * 8), c->nt, c->pt,
+          c->ntau);
+      MI_CHECK_LAUNCH("build_filter_frag");
+    }
     MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)G::SMEM));
   });
@@ -312,7 +321,7 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
       MI_CHECK_LAUNCH("transpose_time_inner");
     }
     for (int gi = 0; gi < ngroups; ++gi) {
-      DmmaArgs a{c->xt.p, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
+      DmmaArgs a{c->xt.p, c->afr.p + (size_t)gi * c->ntau * 1024, c->ntau, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
                  gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns};
       ProfScope ps(c, PROF_OP_STENCIL);
       stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a);

@@ -44,9 +44,12 @@ struct DmmaSten {
   static constexpr int PTMAX = 4;
   static constexpr int BW = 2 * PTMAX + 1;
   static constexpr int WL = 2 * TT + 2 * PTMAX;     // circular W buffer length (rows)
+  static constexpr int PSTR = 8 * WL + 4;           // point stride in the W buffer (= 4 mod 16)
   static constexpr int THREADS = 512;
+  static constexpr int FK = 8 * 16;                 // filter K: 8 channels x 16 time taps
   static constexpr size_t SMEM = (size_t)2 * HS * TSTR * 8       // X halo [buf][h][t]
-                                 + (size_t)2 * 8 * 8 * WL * 8;    // W partials [half][pt][ch][row mod WL]
+                                 + (size_t)2 * 8 * PSTR * 8       // W partials [half][pt][ch*WL + row]
+                                 + (size_t)2 * 2 * 4 * 64 * 8;    // filter partials [buf][mtile][cpair][64]
   // halo offset of lane-k 0 of k-step ks (lane kl adds kl)
   static constexpr __host__ __device__ int koff(int ks) {
     return ((D >= 3 ? (ks / QR) / W : 0) * H2 + (D >= 2 ? (ks / QR) % W : 0)) * H1 + 4 * (ks % QR);
@@ -55,6 +58,8 @@ struct DmmaSten {
 
 struct DmmaArgs {
   const double* xt;     // time-innermost copy of x: xt[i * ntp + t]
+  const double* afr;    // time-filter A fragments [tau][32 ks][32 lanes] of this group
+  int ntau;
   const double* frag;   // fragment-major coefficients of this channel group
   const double* band;   // time bands (nchan_total, nt, 2pt+1)
   double* y;
@@ -106,7 +111,8 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   using G = DmmaSten<D, P>;
   extern __shared__ double sm[];
   double* Xs = sm;                                   // [2][HS][TSTR]
-  double* Wp = Xs + 2 * G::HS * G::TSTR;             // [2 half][8 pt][8 ch][WL]
+  double* Wp = Xs + 2 * G::HS * G::TSTR;             // [2 half][8 pt][PSTR]
+  double* ys = Wp + 2 * 8 * G::PSTR;                 // [2 buf][2 mtile][4 cpair][64]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pt = warp >> 1, half = warp & 1;
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   const int c1 = cube % a.C1, c2 = (cube / a.C1) % a.C2, c3 = cube / (a.C1 * a.C2);
   const int o1 = c1 * G::B1, o2 = c2 * G::B2, o3 = c3 * G::B3;
 
-  for (int e = tid; e < 2 * 8 * 8 * G::WL; e += G::THREADS) Wp[e] = 0.0;
+  for (int e = tid; e < 2 * 8 * G::PSTR; e += G::THREADS) Wp[e] = 0.0;
 
   double breg[G::KH];
   {
@@ -129,34 +135,54 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   const int W2pt = 2 * a.pt + 1;
   // ---- async loads of chunk t0: halo tile (16 B copies) + band rows of the
   constexpr int PAIRS = G::TT / 2;
+  // Fast path: one (h1, h2) column of the halo per thread, h3 = q
+  // (THREADS == H1*H2*PAIRS, e.g. d=3 p=3), so a copy is one add + compare.
+  constexpr bool FAST = G::THREADS == G::H1 * G::H2 * PAIRS;
+  const int fpr = tid % PAIRS, fh12 = tid / PAIRS;
+  const int fg1 = o1 - P + fh12 % G::H1;
+  const int fg2 = D >= 2 ? o2 - P + fh12 / G::H1 : 0;
+  const bool fval12 = fg1 >= 0 && fg1 < a.n1 && fg2 >= 0 && fg2 < a.n2;
+  const long long plane = (long long)a.n1 * a.n2 * a.ntp;
+  const double* fsrc0 = a.xt + (((long long)(o3 - P) * a.n2 + fg2) * a.n1 + fg1) * a.ntp + 2 * fpr;
   auto load_chunk = [&](int buf, int t0) {
     if (t0 >= a.nt) return;
     double* dst = Xs + buf * G::HS * G::TSTR;
-    for (int e = tid; e < G::HS * PAIRS; e += G::THREADS) {
-      const int h = e / PAIRS, pr = e - h * PAIRS;
-      const int h1 = h % G::H1, h2 = (h / G::H1) % G::H2, h3 = h / (G::H1 * G::H2);
-      const int g1 = o1 - P + h1;
-      const int g2 = D >= 2 ? o2 - P + h2 : 0;
-      const int g3 = D >= 3 ? o3 - P + h3 : 0;
-      const bool v = g1 >= 0 && g1 < a.n1 && g2 >= 0 && g2 < a.n2 && g3 >= 0 && g3 < a.n3;
-      const double* src = v ? a.xt + (((long long)g3 * a.n2 + g2) * a.n1 + g1) * a.ntp + t0 + 2 * pr : a.xt;
-      cp_async16(dst + h * G::TSTR + 2 * pr, src, v);
+    if constexpr (FAST) {
+      double* d0 = dst + fh12 * G::TSTR + 2 * fpr;
+#pragma unroll
+      for (int q = 0; q < G::H3; ++q) {
+        const int g3 = o3 - P + q;
+        const bool v = fval12 && g3 >= 0 && g3 < a.n3;
+        cp_async16(d0 + q * G::H1 * G::H2 * G::TSTR, v ? fsrc0 + q * plane + t0 : a.xt, v);
+      }
+    } else {
+      for (int e = tid; e < G::HS * PAIRS; e += G::THREADS) {
+        const int h = e / PAIRS, pr = e - h * PAIRS;
+        const int h1 = h % G::H1, h2 = (h / G::H1) % G::H2, h3 = h / (G::H1 * G::H2);
+        const int g1 = o1 - P + h1;
+        const int g2 = D >= 2 ? o2 - P + h2 : 0;
+        const int g3 = D >= 3 ? o3 - P + h3 : 0;
+        const bool v = g1 >= 0 && g1 < a.n1 && g2 >= 0 && g2 < a.n2 && g3 >= 0 && g3 < a.n3;
+        const double* src = v ? a.xt + (((long long)g3 * a.n2 + g2) * a.n1 + g1) * a.ntp + t0 + 2 * pr : a.xt;
+        cp_async16(dst + h * G::TSTR + 2 * pr, src, v);
+      }
     }
   };
 
-  // filter item of this thread: (point fq, channel fc, rows fr + 8*hh)
-  const int fc = tid & 7, fr = (tid >> 3) & 7, fq = tid >> 6;
-  const int f1 = o1 + fq % G::B1, f2 = o2 + (fq / G::B1) % G::B2, f3 = o3 + fq / (G::B1 * G::B2);
-  const bool fvalid = f1 < a.n1 && f2 < a.n2 && f3 < a.n3;
-  const long long fidx = ((long long)f3 * a.n2 + f2) * a.n1 + f1;
-  const double* w0 = Wp + (fq * 8 + fc) * G::WL;
-  const double* w1 = Wp + ((8 + fq) * 8 + fc) * G::WL;
+  // time filter on the tensor cores: warps 0..7 -> (mtile fm, channel pair fcq)
+  const int fm = warp & 1, fcq = (warp >> 1) & 3;
+  // output write of the previous filter: threads 0..127 -> (mtile, row m, point n)
+  const int om = (tid >> 6) & 1, orow = (tid >> 3) & 7, opt = tid & 7;
+  const int q1 = o1 + opt % G::B1, q2 = o2 + (opt / G::B1) % G::B2, q3 = o3 + opt / (G::B1 * G::B2);
+  const bool ovalid = q1 < a.n1 && q2 < a.n2 && q3 < a.n3;
+  const long long oidx = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
 
   const int base = ((pt / (G::B1 * G::B2)) * G::H2 + (pt / G::B1) % G::B2) * G::H1 + pt % G::B1;
   const int kl = lane & 3, mrow = lane >> 2;
-  double* wmine = Wp + ((half * 8 + pt) * 8 + 2 * kl) * G::WL;   // channels 2kl, 2kl+1
+  double* wmine = Wp + (half * 8 + pt) * G::PSTR + 2 * kl * G::WL;   // channels 2kl, 2kl+1
 
   const int nchunks = (a.nt + a.pt + G::TT - 1) / G::TT + 1;   // +1: filter of the last chunk
+  (void)W2pt;
   load_chunk(0, 0);
   cp_async_commit();
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -165,30 +191,38 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
     __syncthreads();                  // X(ch), bands(ch) visible; W rows of chunk ch-1 complete
     if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
     cp_async_commit();
-    // ---- time filter of chunk ch-1: y[t], t in [t0 - TT - pt, t0 - pt)
-    if (ch > 0) {
-      const int tp0 = t0 - G::TT;
-#pragma unroll
-      for (int hh = 0; hh < G::TT / 8; ++hh) {
-        const int tl = fr + 8 * hh;
-        const int t = tp0 - a.pt + tl;
-        double v = 0.0;
-        if (fc < a.nc && t >= 0 && t < a.nt) {
-          const double* bd = a.band + ((long long)(a.c0 + fc) * a.nt + t) * W2pt;
-          for (int k = 0; k < W2pt; ++k) {
-            int r = t - a.pt + k + 2 * G::PTMAX;           // row of time t-pt+k (shifted >= 0)
-            r = r % G::WL;
-            v = fma(__ldg(bd + k), w0[r] + w1[r], v);
-          }
-        }
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        if (fc == 0 && t >= 0 && t < a.nt && fvalid) {
-          double* dst = a.y + (long long)t * a.ns + fidx;
-          if (a.accumulate) *dst += v; else *dst = v;
-        }
+    // ---- write y of the filter of chunk ch-2 (partials summed over channel pairs)
+    if (ch >= 2 && tid < 128) {
+      const int t = t0 - 2 * G::TT - a.pt + 8 * om + orow;
+      if (t >= 0 && t < a.nt && ovalid) {
+        const double* yp = ys + ((ch & 1) * 2 + om) * 4 * 64 + orow * 8 + opt;
+        const double v = (yp[0] + yp[64]) + (yp[128] + yp[192]);
+        double* dst = a.y + (long long)t * a.ns + oidx;
+        if (a.accumulate) *dst += v; else *dst = v;
       }
+    }
+    // ---- time filter of chunk ch-1 on the tensor cores (warps 0..7)
+    if (ch >= 1 && warp < 8) {
+      const int tau = 2 * (ch - 1) + fm;                   // M-tile rows tb = 8 tau - pt
+      const int tb = 8 * tau - a.pt;
+      const double* af = a.afr + ((long long)tau * 32 + 8 * fcq) * 32 + lane;
+      const int n = lane >> 2;                             // point (B column)
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+      const int r0 = (tb - a.pt + 2 * G::PTMAX) % G::WL;  // row of time tb - pt
+#pragma unroll
+      for (int kq = 0; kq < 8; ++kq) {
+        const int k = 4 * (8 * fcq + kq) + kl;             // K index: channel k/16, tap j = k%16
+        const int c = k >> 4, j = k & 15;
+        int r = r0 + j;
+        r = r >= G::WL ? r - G::WL : r;
+        const double* wp = Wp + n * G::PSTR + c * G::WL + r;
+        const double bv = wp[0] + wp[8 * G::PSTR];
+        const double av = __ldg(af + kq * 32);
+        if (kq & 1) dmma(d0, d1, av, bv); else dmma(c0, c1, av, bv);
+      }
+      double* yp = ys + (((ch + 1) & 1) * 2 + fm) * 4 * 64 + fcq * 64;
+      yp[mrow * 8 + 2 * kl] = c0 + d0;
+      yp[mrow * 8 + 2 * kl + 1] = c1 + d1;
     }
     // ---- DMMA sweep of chunk ch into this half's W partial rows
     if (t0 < a.nt + a.pt) {
@@ -210,6 +244,35 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
       }
     }
   }
+  // flush the last filter's partials (chunk nchunks-2)
+  __syncthreads();
+  if (tid < 128) {
+    const int t = nchunks * G::TT - 2 * G::TT - a.pt + 8 * om + orow;
+    if (t >= 0 && t < a.nt && ovalid) {
+      const double* yp = ys + ((nchunks & 1) * 2 + om) * 4 * 64 + orow * 8 + opt;
+      const double v = (yp[0] + yp[64]) + (yp[128] + yp[192]);
+      double* dst = a.y + (long long)t * a.ns + oidx;
+      if (a.accumulate) *dst += v; else *dst = v;
+    }
+  }
+}
+
+// Time-filter A fragments: afr[tau][ks][lane] = T_{c0+c}[t, t'] with
+// t = 8 tau - pt + lane/4, k = 4 ks + lane%4 = 16 c + j, t' = t - (lane/4) - pt + j
+// (zero outside the band, the channel group or [0, nt)).
+__global__ void build_filter_frag(double* __restrict__ afr, const double* __restrict__ band, int c0, int nc,
+                                  int nt, int pt, int ntau) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ntau * 32 * 32) return;
+  const int lane = e & 31, ks = (e >> 5) & 31, tau = e >> 10;
+  const int m = lane >> 2, k = 4 * ks + (lane & 3);
+  const int c = k >> 4, j = k & 15;
+  const int t = 8 * tau - pt + m;
+  const int tap = j - m;                                  // t' - t + pt
+  double v = 0.0;
+  if (c < nc && t >= 0 && t < nt && tap >= 0 && tap <= 2 * pt)
+    v = band[((long long)(c0 + c) * nt + t) * (2 * pt + 1) + tap];
+  afr[e] = v;
 }
 
 // Repack channel stencils [c][s][i] into the fragment-major layout
