@@ -74,18 +74,20 @@ int mi_op_set_su_channel(mi_ctx* ctx, int c, const double* theta, const double* 
 /* y = A x   (x, y device, length N, must not alias) */
 int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
 
-/* Reaction correction y += M_R x, M_R = int int C_r B_i B_j with the
- * ionic linearisation C_r = c1 (u - a)(u - 1) + c2 w evaluated at q = p+1
- * Gauss points per element and direction (assembly.py:287-347).
- * u, w: device iterate coefficients (length N, copied).  Tables (host):
- * colt (qt_total, pt+1) time basis values at Gauss points with first index
- * firstt (qt_total) and weights wt (qt_total, includes T); per direction
- * cols_l (q_l_total, p+1), firsts_l, ws_l (includes box length). */
+/* Reaction correction y += M_R x (added by every subsequent mi_op_apply),
+ * M_R = int int C_r B_i B_j with the Rogers-McCulloch linearisation
+ * C_r = c1 (u - a)(u - 1) + c2 w evaluated at q = p+1 Gauss points per
+ * element and direction (replaces reaction_mass + the CSR correction of
+ * KroneckerOperator.matvec, assembly.py:287-347 / 442-443).
+ * u, w: DEVICE iterate coefficients (length N, copied).  Host tables per
+ * present direction in the order x, y, ..., t (spatial directions 1..d,
+ * then time): q[l] Gauss points per element, nel[l] elements; B = concat_l
+ * (nel_l, q_l, p_l + 1) values of functions e..e+p_l at the Gauss points of
+ * element e (time: FULL basis incl. the removed first function); Wq = concat_l
+ * (nel_l, q_l) weights (Gauss x half-length x box length, x T in time).
+ * q, nel have d+1 entries. */
 int mi_op_set_reaction(mi_ctx* ctx, const double* u, const double* w, double c1, double a, double c2,
-                       int q, const int* nel /* d spatial element counts */, int nel_t,
-                       const double* colt, const int* firstt, const double* wt,
-                       const double* cols /* (d, qmax_total, p+1) */, const int* firsts /* (d, qmax_total) */,
-                       const double* ws /* (d, qmax_total) */);
+                       const int* q, const int* nel, const double* B, const double* Wq);
 int mi_op_clear_reaction(mi_ctx* ctx);
 
 /* ---------------------------------------------------------------------

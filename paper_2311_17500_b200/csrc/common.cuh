@@ -5,6 +5,7 @@
 // directions beyond d have extent 1, so every kernel is written for d = 3.
 #pragma once
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -85,10 +86,10 @@ struct mi_ctx {
   // ---- reaction correction M_R (variant B)
   bool reaction_on = false;
   mi::DeviceBuf u_it, w_it;     // iterate coefficients (N each)
-  double c1 = 0, a = 0, c2 = 0, final_time = 1;
-  mi::DeviceBuf colt;           // time Gauss tables
-  mi::DeviceBuf cols;           // spatial Gauss tables
-  mi::DeviceBuf rq_scratch;
+  double c1 = 0, a = 0, c2 = 0;
+  mi::DeviceBuf rx_B, rx_W;     // Gauss tables, directions x, y, z, t
+  size_t rx_Boff[4] = {0, 0, 0, 0}, rx_Woff[4] = {0, 0, 0, 0};
+  int rx_q[4] = {1, 1, 1, 1}, rx_p[4] = {0, 0, 0, 0}, rx_nel[4] = {1, 1, 1, 1}, rx_E[4] = {1, 1, 1, 1};
 
   // ---- preconditioner
   bool pc_ready = false;

@@ -140,8 +140,8 @@ int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx
 int mi_ctx_destroy(mi_ctx* c) {
   if (!c) return MI_OK;
   cudaSetDevice(c->device);
-  mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->frag, &c->xt, &c->afr, &c->u_it, &c->w_it, &c->colt,
-                           &c->cols, &c->rq_scratch, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
+  mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->frag, &c->xt, &c->afr, &c->u_it, &c->w_it, &c->rx_B,
+                           &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
                            &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->partials};
   for (auto* b : bufs) mi::dfree(*b);
   for (int l = 0; l < 3; ++l) {

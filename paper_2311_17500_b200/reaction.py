@@ -1,5 +1,49 @@
-"""Reaction correction M_R x on the device (assembly.py:287-347)."""
+"""Host tables for the device reaction correction M_R x (assembly.py:287-347).
+
+The reference evaluates C_r = c1 (u - a)(u - 1) + c2 w at q = p+1 Gauss
+points per element in every spatial direction (SpatialQuadratureData with
+its default rule, assembly.py:146-155) and in time (TimeQuadratureData,
+assembly.py:256-262, physical weights x T); the device kernel uses exactly
+these points.
+"""
+
+import numpy as np
+
+from . import _lib
+from .device import dptr, host_ptr
+from .spaces import basis_table, gauss_rule
+
+
+def element_tables(space, q, scale):
+    """(B, W): B[e, g, a] = value of function e + a at Gauss point g of element e."""
+    bp = space.breakpoints
+    ne = bp.size - 1
+    x, w = gauss_rule(bp, q)
+    T = basis_table(space, x, 0)
+    p = space.degree
+    B = np.zeros((ne, q, p + 1))
+    for e in range(ne):
+        B[e] = T[e * q:(e + 1) * q, e:e + p + 1]
+        # open uniform knots: element e carries functions e..e+p
+        assert np.allclose(T[e * q:(e + 1) * q].sum(axis=1), 1.0)
+    return B, (w * scale).reshape(ne, q)
 
 
 def set_reaction(ctx, st, final_time, consts, u, w, lengths):
-    raise NotImplementedError("reaction correction kernel not built yet")
+    d = len(st.spatial)
+    L = np.ones(d) if lengths is None else np.asarray(lengths, float)
+    Bs, Ws, qs, nels = [], [], [], []
+    for l, s in enumerate(st.spatial):
+        B, W = element_tables(s, s.degree + 1, L[l])
+        Bs.append(B.ravel()); Ws.append(W.ravel()); qs.append(s.degree + 1); nels.append(B.shape[0])
+    B, W = element_tables(st.time, st.time.degree + 1, final_time)
+    Bs.append(B.ravel()); Ws.append(W.ravel()); qs.append(st.time.degree + 1); nels.append(B.shape[0])
+    Bh = np.ascontiguousarray(np.concatenate(Bs))
+    Wh = np.ascontiguousarray(np.concatenate(Ws))
+    qh = np.asarray(qs, dtype=np.int32)
+    nh = np.asarray(nels, dtype=np.int32)
+    ud = ctx.to_device(u)
+    wd = ctx.to_device(w)
+    ctx.bind_stream()
+    _lib.call("mi_op_set_reaction", ctx.handle, dptr(ud), dptr(wd), float(consts["c1"]), float(consts["a"]),
+              float(consts["c2"]), host_ptr(qh), host_ptr(nh), host_ptr(Bh), host_ptr(Wh))

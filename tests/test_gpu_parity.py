@@ -88,3 +88,37 @@ def test_gmres_known_answers_device():
     with pytest.raises(mb.NonConvergenceError) as e:
         mb.gmres(op, g["rhs"], precond=P, tol=1e-14, max_iter=3)
     assert e.value.iterations == 3 and len(e.value.residuals) == 4
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_operator_general_iterate_reaction(name):
+    """Variant B: M_R (q=p+1 Gauss, Rogers-McCulloch linearisation) at u, w != 0."""
+    g = load(name)
+    _, op, _ = product_objects(g, u=g["u"], w=g["w"])
+    assert not op.zero_iterate
+    assert rel(op.matvec(g["x"]), g["y_b"]) < 1e-12
+    # the reaction part alone: A_b x - (A_a x - a c1 M_t M_s x) = M_R x
+    _, op_sep, _ = product_objects(g, with_su=False, u=g["u"], w=g["w"])
+    _, op_sep0, _ = product_objects(g, with_su=False)
+    y_mr = op_sep.matvec(g["x"]) - op_sep0.matvec(g["x"])
+    y_ref = g["y_mr"] - (g["y_sep"] - op_sep0_galerkin(g))
+    assert rel(y_mr, y_ref) < 1e-10
+
+
+def op_sep0_galerkin(g):
+    """Galerkin part without reaction, from the oracle (test helper)."""
+    from oracle import problem
+    from cases import space_of, sigma_of
+    st = space_of(g)
+    op = problem.operator_terms(st, float(g["T"]), 1.0, sigma_of(g), {"c1": 0.0, "a": 0.0, "c2": 0.0})
+    return op.matvec(g["x"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gmres_general_iterate_matches_reference(name):
+    import paper_2311_17500_b200 as mb
+    g = load(name)
+    _, op, P = product_objects(g, u=g["u"], w=g["w"])
+    x, it, hist = mb.gmres(op, g["rhs"], precond=P, tol=1e-8, max_iter=400)
+    assert it == int(g["gm_b_it"])
+    assert rel(x, g["gm_b_x"]) < 1e-10
