@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--ne", type=int, default=CFG["ne"])
     ap.add_argument("--ne-t", type=int, default=CFG["ne_t"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-extras", action="store_true", help="skip variant-B apply and the cfg3 solve")
     return ap.parse_args()
 
 
@@ -185,6 +186,39 @@ def measured_peaks():
         return {}
 
 
+def _lib_clear(ctx):
+    from paper_2311_17500_b200 import _lib
+    _lib.call("mi_op_clear_reaction", ctx.handle)
+
+
+def measure_solve(torch, mb, dev):
+    """Solve time of one preconditioned GMRES solve (tol 1e-8) on BASELINE cfg 3:
+    3D p=2 64^3 x 128 (N=37.1M), anisotropic sigma, SU on (front indicator),
+    zero-iterate reaction, seeded rhs ~ N(0,1) (u0 lifting is not part of the
+    reference).  Device time with CUDA events, 1 GPU."""
+    from paper_2311_17500_b200.spaces import greville
+    d, p, ne, ne_t = 3, 2, 64, 128
+    sigma = (1e-3, 4e-4, 4e-4)
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(d)], mb.SplineSpace.uniform(p, ne_t))
+    theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
+    stab = mb.Stabilization(st, theta, 0.1, 1.0)
+    del theta
+    op = mb.KroneckerOperator(st, 1.0, 1.0, sigma, RM, stabilization=stab, device=dev.index)
+    P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, sigma, RM["a"] * RM["c1"], context=op.ctx)
+    b = torch.from_numpy(np.random.default_rng(2).standard_normal(st.num_dof)).to(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    xs, it, hist = mb.gmres(op, b, precond=P, tol=1e-8, max_iter=200)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    out = {"config": "cfg3 3D p=2 64^3x128 (N=%d), sigma=diag(1e-3,4e-4,4e-4), SU rank %d" % (st.num_dof, stab.rank),
+           "seconds": e0.elapsed_time(e1) * 1e-3, "iterations": it, "final_rel_residual": hist[-1],
+           "n_gpus": 1}
+    op.ctx.close()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -306,6 +340,39 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    # ---- variant B: the same apply at a general iterate (reaction mass M_R with the
+    #      Rogers-McCulloch linearisation at q=p+1 Gauss points), u ~ U[0,1], w ~ U[0,0.1]
+    extras = not args.skip_extras and world == 1
+    if extras:
+        rng = np.random.default_rng(1)
+        u = torch.from_numpy(rng.uniform(0, 1, N)).to(dev)
+        w = torch.from_numpy(rng.uniform(0, 0.1, N)).to(dev)
+        from paper_2311_17500_b200.reaction import set_reaction
+        set_reaction(ctx, st, 1.0, RM, u, w, None)
+        del u, w
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize(dev)
+        ctx.read_profile(reset=True)
+        ctx.profiling(True)
+        e0.record()
+        nb = 3
+        for _ in range(nb):
+            step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        pb = ctx.read_profile(reset=True)
+        ctx.profiling(False)
+        _lib_clear(ctx)
+        line["variant_b"] = {"value": N * nb / (e0.elapsed_time(e1) * 1e-3), "unit": "DoF/s",
+                             "ms_per_step": e0.elapsed_time(e1) / nb,
+                             "kernel_ms_per_step": {k: v[0] / nb for k, v in pb.items() if v[1]},
+                             "note": "A x with M_R at u~U[0,1], w~U[0,0.1] (seed 1), then P^-1"}
+    del op, P, x, y, z, xh, zh
+    ctx.close()
+    torch.cuda.empty_cache()
+    if extras:
+        line["solve"] = measure_solve(torch, mb, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sec, sample, _ = cpu_sample_rate(3, 1, SAMPLE["ne"], SAMPLE["ne_t"])
         line["cpu_baseline"] = {"value": rate, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",

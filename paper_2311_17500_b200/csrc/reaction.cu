@@ -26,171 +26,232 @@ struct RxArgs {
   // B_l[(e * q + g) * (p_l + 1) + a] of function e + a, weights W_l[e * q + g]
   const double* B[4];
   const double* Wq[4];
-  int q[4];            // Gauss points per element per direction (1 for absent dims)
-  int pl[4];           // degree per direction (0 for absent dims)
   int nel[4];          // elements per direction (1 for absent dims)
-  int n[4];            // functions per direction (time: FULL basis incl. removed first)
-  int E[4];            // tile size in elements per direction
-  int ntile[4];        // tiles per direction
-  int color[4];        // colour class of this launch (tile parity)
-  int ncol[4];         // tiles of this colour per direction
-  int ntc;             // constrained time functions (= n[3] - 1)
+  int n[3];            // spatial functions per direction
+  int color[3];        // colour class of this launch (element index mod (p+1))
+  int ncol[3];         // elements of this colour per direction
+  int ntc;             // constrained time functions
   long long ns;
   double c1, a, c2;
 };
 
-// Interpolate along one direction: in[..., L] (coefficients) -> out[..., Q]
-// (Gauss points of the tile's elements).  Layout: pre x dim x post.
-__device__ __forceinline__ void interp_dir(const double* in, double* out, int pre, int L, int Q, int post,
-                                           const double* B, int q, int p, int e0, int k0) {
-  // out[pre][Qi][post] = sum_a B[(e*q+g)*(p+1)+a] in[pre][e - k0 + a][post], Qi = (e - e0)*q + g
-  const int total = pre * Q * post;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int po = idx % post, r = idx / post;
-    const int Qi = r % Q, pr = r / Q;
-    const int e = e0 + Qi / q, g = Qi % q;
-    const double* b = B + ((long long)e * q + g) * (p + 1);
-    const double* src = in + ((long long)pr * L + (e - k0)) * post + po;
-    double v = 0.0;
-    for (int aa = 0; aa <= p; ++aa) v = fma(b[aa], src[aa * post], v);
-    out[idx] = v;
-  }
-}
-
-// Project (transpose of interp_dir): in[pre][Q][post] -> out[pre][L][post]
-__device__ __forceinline__ void project_dir(const double* in, double* out, int pre, int L, int Q, int post,
-                                            const double* B, int q, int p, int e0, int ne, int k0) {
-  const int total = pre * L * post;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int po = idx % post, r = idx / post;
-    const int li = r % L, pr = r / L;
-    const int f = k0 + li;                       // function index
-    double v = 0.0;
-    // elements e in [e0, e0+ne) with f - e in [0, p]
-    const int elo = max(e0, f - p), ehi = min(e0 + ne - 1, f);
-    for (int e = elo; e <= ehi; ++e) {
-      const int aa = f - e;
-      for (int g = 0; g < q; ++g) {
-        const double bv = B[((long long)e * q + g) * (p + 1) + aa];
-        v = fma(bv, in[((long long)pr * Q + (e - e0) * q + g) * post + po], v);
-      }
-    }
-    out[idx] = v;
-  }
-}
-
-__global__ void reaction_tile(RxArgs r) {
+// One warp per spatial element (colour class: elements p+1 apart never
+// share a basis function), sweeping all time elements with a sliding
+// window of p_t+1 coefficient slices and p_t+1 output slices in shared
+// memory.  Sum factorisation per time Gauss point: x, y, z interpolation of
+// u, w, x (LD = p+1 functions -> Q = p+1 points per direction), pointwise
+// C_r(u, w) x W, then z, y, x projection.  q = p+1 is the reference rule.
+template <int D, int P, int PT>
+__global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
+  constexpr int LD = P + 1, Q = P + 1;
+  constexpr int L1 = LD, L2 = D >= 2 ? LD : 1, L3 = D >= 3 ? LD : 1;
+  constexpr int LS = L1 * L2 * L3;                   // local spatial functions (= quad points)
+  constexpr int PW = PT + 1;                         // time window
+  constexpr int QT = PT + 1;                         // time Gauss points
+  constexpr int WARP_SM = 3 * PW * LS + PW * LS + 2 * 3 * LS + 3 * Q * LD;
   extern __shared__ double sm[];
-  // tile coordinates of this colour
-  int b = blockIdx.x;
-  int k[4], e0[4], ne[4], L[4], Q[4];
-  for (int l = 0; l < 4; ++l) {
-    const int m = b % r.ncol[l];
-    b /= r.ncol[l];
-    k[l] = 2 * m + r.color[l];
-    e0[l] = k[l] * r.E[l];
-    ne[l] = min(r.E[l], r.nel[l] - e0[l]);
-    L[l] = ne[l] + r.pl[l];                      // local functions [e0, e0 + L)
-    Q[l] = ne[l] * r.q[l];
-  }
-  const int Ls = L[0] * L[1] * L[2];
-  const int Qs = Q[0] * Q[1] * Q[2];
-  // smem carve-up (sizes from the launch: worst case per block)
-  double* cu = sm;                               // [Lt][Ls] x3 fields
-  double* cw = cu + L[3] * Ls;
-  double* cx = cw + L[3] * Ls;
-  double* outc = cx + L[3] * Ls;                 // [Lt][Ls] output accumulation
-  double* f0 = outc + L[3] * Ls;                 // time-interpolated fields [3][Ls]
-  const int big = max(Qs, max(Q[0] * L[1] * L[2], Q[0] * Q[1] * L[2]));
-  double* s1 = f0 + 3 * Ls;                      // [3][big]
-  double* s2 = s1 + 3 * big;                     // [3][big]
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* base = sm + wib * WARP_SM;
+  double* win = base;                                // [3][PW][LS]
+  double* outw = win + 3 * PW * LS;                  // [PW][LS]
+  double* ta = outw + PW * LS;                       // [3][LS]
+  double* tb = ta + 3 * LS;                          // [3][LS]
+  double* bsp = tb + 3 * LS;                         // [3 dirs][Q][LD] spatial basis of this element
 
-  // load local coefficients (time index in the FULL basis: constrained = f - 1)
-  for (int idx = threadIdx.x; idx < L[3] * Ls; idx += blockDim.x) {
-    const int sl = idx % Ls, tl = idx / Ls;
-    const int i1 = sl % L[0], i2 = (sl / L[0]) % L[1], i3 = sl / (L[0] * L[1]);
-    const int ft = e0[3] + tl, ct = ft - 1;
-    const long long gs = ((long long)(e0[2] + i3) * r.n[1] + (e0[1] + i2)) * r.n[0] + (e0[0] + i1);
-    const bool v = ct >= 0 && ct < r.ntc;
-    const long long gi = (long long)ct * r.ns + gs;
-    cu[idx] = v ? r.u[gi] : 0.0;
-    cw[idx] = v ? r.w[gi] : 0.0;
-    cx[idx] = v ? r.x[gi] : 0.0;
-    outc[idx] = 0.0;
-  }
-  __syncthreads();
-  const int pt = r.pl[3], qt = r.q[3];
-  for (int et = e0[3]; et < e0[3] + ne[3]; ++et) {
-    for (int g = 0; g < qt; ++g) {
-      const double* bt = r.B[3] + ((long long)et * qt + g) * (pt + 1);
-      const double wt = r.Wq[3][et * qt + g];
-      // time interpolation of u, w, x at this Gauss time
-      for (int idx = threadIdx.x; idx < 3 * Ls; idx += blockDim.x) {
-        const int fld = idx / Ls, sl = idx % Ls;
-        const double* c = (fld == 0 ? cu : (fld == 1 ? cw : cx)) + (et - e0[3]) * Ls + sl;
-        double v = 0.0;
-        for (int aa = 0; aa <= pt; ++aa) v = fma(bt[aa], c[aa * Ls], v);
-        f0[idx] = v;
-      }
-      __syncthreads();
-      // spatial interpolation x -> y -> z for the 3 fields
-      for (int fld = 0; fld < 3; ++fld)
-        interp_dir(f0 + fld * Ls, s1 + fld * big, L[2] * L[1], L[0], Q[0], 1, r.B[0], r.q[0], r.pl[0], e0[0], e0[0]);
-      __syncthreads();
-      for (int fld = 0; fld < 3; ++fld)
-        interp_dir(s1 + fld * big, s2 + fld * big, L[2], L[1], Q[1], Q[0], r.B[1], r.q[1], r.pl[1], e0[1], e0[1]);
-      __syncthreads();
-      for (int fld = 0; fld < 3; ++fld)
-        interp_dir(s2 + fld * big, s1 + fld * big, 1, L[2], Q[2], Q[1] * Q[0], r.B[2], r.q[2], r.pl[2], e0[2], e0[2]);
-      __syncthreads();
-      // pointwise ionic linearisation and quadrature weights
-      for (int idx = threadIdx.x; idx < Qs; idx += blockDim.x) {
-        const int g1 = idx % Q[0], g2 = (idx / Q[0]) % Q[1], g3 = idx / (Q[0] * Q[1]);
-        const double w1 = r.Wq[0][e0[0] * r.q[0] + g1];
-        const double w2 = r.Wq[1][e0[1] * r.q[1] + g2];
-        const double w3 = r.Wq[2][e0[2] * r.q[2] + g3];
-        const double uu = s1[idx], ww = s1[big + idx], xx = s1[2 * big + idx];
-        const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
-        s2[idx] = cr * xx * (wt * w1 * w2 * w3);
-      }
-      __syncthreads();
-      // projection z -> y -> x
-      project_dir(s2, s1, 1, L[2], Q[2], Q[1] * Q[0], r.B[2], r.q[2], r.pl[2], e0[2], ne[2], e0[2]);
-      __syncthreads();
-      project_dir(s1, s2, L[2], L[1], Q[1], Q[0], r.B[1], r.q[1], r.pl[1], e0[1], ne[1], e0[1]);
-      __syncthreads();
-      project_dir(s2, s1, L[2] * L[1], L[0], Q[0], 1, r.B[0], r.q[0], r.pl[0], e0[0], ne[0], e0[0]);
-      __syncthreads();
-      // time projection into the output block
-      for (int idx = threadIdx.x; idx < (pt + 1) * Ls; idx += blockDim.x) {
-        const int aa = idx / Ls, sl = idx % Ls;
-        outc[(et - e0[3] + aa) * Ls + sl] += bt[aa] * s1[sl];
-      }
-      __syncthreads();
+  long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long long nw = (long long)r.ncol[0] * r.ncol[1] * r.ncol[2];
+  if (wid >= nw) return;
+  int e[3];
+  {
+    long long t = wid;
+    for (int l = 0; l < 3; ++l) {
+      const int m = (int)(t % r.ncol[l]);
+      t /= r.ncol[l];
+      e[l] = (l < D) ? m * LD + r.color[l] : 0;
     }
   }
-  // add to y (this colour's tiles own disjoint output DoFs)
-  for (int idx = threadIdx.x; idx < L[3] * Ls; idx += blockDim.x) {
-    const int sl = idx % Ls, tl = idx / Ls;
-    const int i1 = sl % L[0], i2 = (sl / L[0]) % L[1], i3 = sl / (L[0] * L[1]);
-    const int ct = e0[3] + tl - 1;
-    if (ct < 0 || ct >= r.ntc) continue;
-    const long long gs = ((long long)(e0[2] + i3) * r.n[1] + (e0[1] + i2)) * r.n[0] + (e0[0] + i1);
-    r.y[(long long)ct * r.ns + gs] += outc[idx];
+  // spatial basis tables of this element and quadrature weights (registers)
+  double wsp[LS > 32 ? (LS + 31) / 32 : 1];
+  for (int l = 0; l < 3; ++l) {
+    for (int i = lane; i < Q * LD; i += 32) {
+      const bool pres = l < D;
+      bsp[l * Q * LD + i] = pres ? r.B[l][(long long)e[l] * Q * LD + i] : (i == 0 ? 1.0 : 0.0);
+    }
   }
+#pragma unroll
+  for (int k = 0; k < (LS + 31) / 32; ++k) {
+    const int s = lane + 32 * k;
+    double wv = 0.0;
+    if (s < LS) {
+      const int g1 = s % L1, g2 = (s / L1) % L2, g3 = s / (L1 * L2);
+      wv = r.Wq[0][e[0] * Q + g1];
+      if (D >= 2) wv *= r.Wq[1][e[1] * Q + g2];
+      if (D >= 3) wv *= r.Wq[2][e[2] * Q + g3];
+    }
+    wsp[k] = wv;
+  }
+  // global index of local function s
+  auto gidx = [&](int s) -> long long {
+    const int j1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
+    return ((long long)(e[2] + j3) * r.n[1] + (e[1] + j2)) * r.n[0] + (e[0] + j1);
+  };
+  auto load_slice = [&](int ft) {                     // full-basis time function ft
+    const int ct = ft - 1, slot = ft % PW;
+    for (int s = lane; s < LS; s += 32) {
+      const bool v = ct >= 0 && ct < r.ntc;
+      const long long gi = (long long)ct * r.ns + gidx(s);
+      win[(0 * PW + slot) * LS + s] = v ? r.u[gi] : 0.0;
+      win[(1 * PW + slot) * LS + s] = v ? r.w[gi] : 0.0;
+      win[(2 * PW + slot) * LS + s] = v ? r.x[gi] : 0.0;
+      outw[slot * LS + s] = 0.0;
+    }
+  };
+  auto flush_slice = [&](int ft) {
+    const int ct = ft - 1, slot = ft % PW;
+    if (ct >= 0 && ct < r.ntc)
+      for (int s = lane; s < LS; s += 32) r.y[(long long)ct * r.ns + gidx(s)] += outw[slot * LS + s];
+  };
+  // interpolation along direction l: in[j] (L per dir) -> out[g] (Q per dir); strides in the
+  // combined (dir1, dir2, dir3) index with extents ext (before) -> ext with dir l replaced.
+  const double* bx = bsp;
+  const double* by = bsp + Q * LD;
+  const double* bz = bsp + 2 * Q * LD;
+  for (int ft = 0; ft < PT; ++ft) load_slice(ft);
+  for (int et = 0; et < r.nel[3]; ++et) {
+    load_slice(et + PT);
+    __syncwarp();
+    for (int g = 0; g < QT; ++g) {
+      const double* bt = r.B[3] + ((long long)et * QT + g) * (PT + 1);
+      const double wt = r.Wq[3][et * QT + g];
+      double btv[PT + 1];
+#pragma unroll
+      for (int aa = 0; aa <= PT; ++aa) btv[aa] = __ldg(bt + aa);
+      // time interpolation -> ta[3][LS]
+      for (int i = lane; i < 3 * LS; i += 32) {
+        const int fld = i / LS, s = i % LS;
+        double v = 0.0;
+#pragma unroll
+        for (int aa = 0; aa <= PT; ++aa) v = fma(btv[aa], win[(fld * PW + (et + aa) % PW) * LS + s], v);
+        ta[i] = v;
+      }
+      __syncwarp();
+      // x: ta -> tb
+      for (int i = lane; i < 3 * LS; i += 32) {
+        const int fld = i / LS, s = i % LS;
+        const int g1 = s % L1, rest = s / L1;
+        const double* src = ta + fld * LS + rest * L1;
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < L1; ++j) v = fma(bx[g1 * LD + j], src[j], v);
+        tb[i] = v;
+      }
+      __syncwarp();
+      if (D >= 2) {  // y: tb -> ta
+        for (int i = lane; i < 3 * LS; i += 32) {
+          const int fld = i / LS, s = i % LS;
+          const int g1 = s % L1, g2 = (s / L1) % L2, g3 = s / (L1 * L2);
+          const double* src = tb + fld * LS + g3 * L1 * L2 + g1;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < L2; ++j) v = fma(by[g2 * LD + j], src[j * L1], v);
+          ta[i] = v;
+        }
+      } else {
+        for (int i = lane; i < 3 * LS; i += 32) ta[i] = tb[i];
+      }
+      __syncwarp();
+      if (D >= 3) {  // z: ta -> tb
+        for (int i = lane; i < 3 * LS; i += 32) {
+          const int fld = i / LS, s = i % LS;
+          const int g12 = s % (L1 * L2), g3 = s / (L1 * L2);
+          const double* src = ta + fld * LS + g12;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < L3; ++j) v = fma(bz[g3 * LD + j], src[j * L1 * L2], v);
+          tb[i] = v;
+        }
+      } else {
+        for (int i = lane; i < 3 * LS; i += 32) tb[i] = ta[i];
+      }
+      __syncwarp();
+      // pointwise: C_r(u, w) * x * weights -> ta[0..LS)
+#pragma unroll
+      for (int k = 0; k < (LS + 31) / 32; ++k) {
+        const int s = lane + 32 * k;
+        if (s < LS) {
+          const double uu = tb[s], ww = tb[LS + s], xx = tb[2 * LS + s];
+          const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
+          ta[s] = cr * xx * (wt * wsp[k]);
+        }
+      }
+      __syncwarp();
+      // projections z, y, x (transposes): ta -> tb -> ta -> tb
+      if (D >= 3) {
+        for (int s = lane; s < LS; s += 32) {
+          const int g12 = s % (L1 * L2), j3 = s / (L1 * L2);
+          double v = 0.0;
+#pragma unroll
+          for (int g3 = 0; g3 < L3; ++g3) v = fma(bz[g3 * LD + j3], ta[g3 * L1 * L2 + g12], v);
+          tb[s] = v;
+        }
+      } else {
+        for (int s = lane; s < LS; s += 32) tb[s] = ta[s];
+      }
+      __syncwarp();
+      if (D >= 2) {
+        for (int s = lane; s < LS; s += 32) {
+          const int g1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
+          double v = 0.0;
+#pragma unroll
+          for (int g2 = 0; g2 < L2; ++g2) v = fma(by[g2 * LD + j2], tb[(j3 * L2 + g2) * L1 + g1], v);
+          ta[s] = v;
+        }
+      } else {
+        for (int s = lane; s < LS; s += 32) ta[s] = tb[s];
+      }
+      __syncwarp();
+      for (int s = lane; s < LS; s += 32) {
+        const int j1 = s % L1, rest = s / L1;
+        double v = 0.0;
+#pragma unroll
+        for (int g1 = 0; g1 < L1; ++g1) v = fma(bx[g1 * LD + j1], ta[rest * L1 + g1], v);
+        // time projection into the output window
+#pragma unroll
+        for (int aa = 0; aa <= PT; ++aa) outw[((et + aa) % PW) * LS + s] += btv[aa] * v;
+      }
+      __syncwarp();
+    }
+    // time function et is complete for this element
+    flush_slice(et);
+    __syncwarp();
+  }
+  for (int ft = r.nel[3]; ft < r.nel[3] + PT; ++ft) flush_slice(ft);
 }
 
-static size_t rx_smem(const mi_ctx* c) {
-  int L[4], Q[4];
-  for (int l = 0; l < 4; ++l) {
-    L[l] = c->rx_E[l] + c->rx_p[l];
-    Q[l] = c->rx_E[l] * c->rx_q[l];
-  }
-  const size_t Ls = (size_t)L[0] * L[1] * L[2];
-  const size_t Qs = (size_t)Q[0] * Q[1] * Q[2];
-  const size_t big = std::max(Qs, std::max((size_t)Q[0] * L[1] * L[2], (size_t)Q[0] * Q[1] * L[2]));
-  return (4 * L[3] * Ls + 3 * Ls + 6 * big) * sizeof(double);
+template <int D, int P, int PT>
+static constexpr size_t rx_warp_smem() {
+  constexpr int LD = P + 1;
+  constexpr int LS = LD * (D >= 2 ? LD : 1) * (D >= 3 ? LD : 1);
+  constexpr int PW = PT + 1;
+  return (size_t)(3 * PW * LS + PW * LS + 2 * 3 * LS + 3 * (P + 1) * LD) * 8;
 }
+
+#define MI_RX_CASE(dv, pv, ptv, ...)                                 \
+  case ((dv) * 8 + (pv)) * 8 + (ptv): {                              \
+    constexpr int D_ = (dv), P_ = (pv), PT_ = (ptv);                 \
+    __VA_ARGS__;                                                     \
+  } break;
+#define MI_RX_DISPATCH(d, p, pt, ...)                                            \
+  switch (((d) * 8 + (p)) * 8 + (pt)) {                                          \
+    MI_RX_CASE(1, 1, 1, __VA_ARGS__) MI_RX_CASE(1, 2, 2, __VA_ARGS__)            \
+    MI_RX_CASE(1, 3, 3, __VA_ARGS__) MI_RX_CASE(2, 1, 1, __VA_ARGS__)            \
+    MI_RX_CASE(2, 2, 2, __VA_ARGS__) MI_RX_CASE(2, 3, 3, __VA_ARGS__)            \
+    MI_RX_CASE(3, 1, 1, __VA_ARGS__) MI_RX_CASE(3, 2, 2, __VA_ARGS__)            \
+    MI_RX_CASE(3, 3, 3, __VA_ARGS__)                                             \
+    default:                                                                     \
+      ::mi::set_error("reaction: unsupported (d, p, p_t) (need p = p_t <= 3)");  \
+      return MI_ERR_ARG;                                                         \
+  }
 
 int reaction_apply(mi_ctx* c, const double* x, double* y) {
   RxArgs r{};
@@ -201,35 +262,45 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   for (int l = 0; l < 4; ++l) {
     r.B[l] = c->rx_B.p + c->rx_Boff[l];
     r.Wq[l] = c->rx_W.p + c->rx_Woff[l];
-    r.q[l] = c->rx_q[l];
-    r.pl[l] = c->rx_p[l];
     r.nel[l] = c->rx_nel[l];
-    r.E[l] = c->rx_E[l];
-    r.ntile[l] = (c->rx_nel[l] + c->rx_E[l] - 1) / c->rx_E[l];
   }
   r.n[0] = c->n[0];
   r.n[1] = c->n[1];
   r.n[2] = c->n[2];
-  r.n[3] = c->nt + 1;
   r.ntc = c->nt;
   r.ns = c->ns;
   r.c1 = c->c1;
   r.a = c->a;
   r.c2 = c->c2;
-  const size_t smem = rx_smem(c);
-  for (int col = 0; col < 16; ++col) {
-    long long nb = 1;
-    bool empty = false;
-    for (int l = 0; l < 4; ++l) {
-      r.color[l] = (col >> l) & 1;
-      r.ncol[l] = (r.ntile[l] - r.color[l] + 1) / 2;
-      if (r.ncol[l] <= 0) empty = true;
-      nb *= r.ncol[l];
+  const int LD = c->p + 1;
+  const int ncolors = LD * (c->d >= 2 ? LD : 1) * (c->d >= 3 ? LD : 1);
+  MI_RX_DISPATCH(c->d, c->p, c->pt, {
+    constexpr size_t smem = rx_warp_smem<D_, P_, PT_>() * 4;
+    static bool attr = false;
+    if (!attr) {
+      MI_CUDA(cudaFuncSetAttribute(reaction_warp<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr = true;
     }
-    if (empty) continue;
-    reaction_tile<<<(unsigned)nb, 256, smem, c->stream>>>(r);
-    MI_CHECK_LAUNCH("reaction_tile");
-  }
+    for (int col = 0; col < ncolors; ++col) {
+      int cc = col;
+      long long nw = 1;
+      for (int l = 0; l < 3; ++l) {
+        if (l < c->d) {
+          r.color[l] = cc % LD;
+          cc /= LD;
+          r.ncol[l] = (c->rx_nel[l] - r.color[l] + LD - 1) / LD;
+        } else {
+          r.color[l] = 0;
+          r.ncol[l] = 1;
+        }
+        nw *= r.ncol[l] > 0 ? r.ncol[l] : 0;
+      }
+      if (nw == 0) continue;
+      reaction_warp<D_, P_, PT_><<<(unsigned)((nw + 3) / 4), 128, smem, c->stream>>>(r);
+      MI_CHECK_LAUNCH("reaction_warp");
+    }
+  });
   return MI_OK;
 }
 
@@ -280,9 +351,9 @@ int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, d
   c->c1 = c1;
   c->a = a;
   c->c2 = c2;
-  const size_t smem = rx_smem(c);
-  MI_REQUIRE(smem <= 227 * 1024, MI_ERR_ARG, "reaction tile does not fit in shared memory");
-  MI_CUDA(cudaFuncSetAttribute(reaction_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MI_REQUIRE(c->p == c->pt && c->p <= 3, MI_ERR_ARG, "reaction: need p = p_t <= 3");
+  for (int l = 0; l < 4; ++l)
+    MI_REQUIRE(c->rx_q[l] == ((l == 3 || l < c->d) ? c->p + 1 : 1), MI_ERR_ARG, "reaction: need q = p + 1");
   c->reaction_on = true;
   return MI_OK;
 }
