@@ -313,6 +313,14 @@ def run_ours(args):
             "achieved": (F_dom / (dom_ms * 1e-3) / 1e12) if F_dom else None,
             "flops_per_step": F_dom, "ms_per_step": dom_ms, "traffic": None}
     roof["frac"] = roof["achieved"] / peak64 if roof["achieved"] else None
+    try:  # DRAM traffic of the same kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01_stencil_ncu.json")) as fh:
+            cap = json.load(fh)
+        if dom == "op_stencil" and str(N) in cap["command"].replace(",", ""):
+            roof["traffic"] = cap["traffic_bytes"]
+            roof["traffic_source"] = "profiles/r01_stencil_ncu.json (dram__bytes_read.sum + dram__bytes_write.sum)"
+    except Exception:
+        pass
     R = stab.rank
     F_sep = 10 * 2 * (2 * p + 1)
     F_su = R * (2 * (2 * p + 1) + 2 * nsten)
