@@ -89,6 +89,9 @@ int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
 int mi_op_set_reaction(mi_ctx* ctx, const double* u, const double* w, double c1, double a, double c2,
                        const int* q, const int* nel, const double* B, const double* Wq);
 int mi_op_clear_reaction(mi_ctx* ctx);
+/* Time-sharded slabs: the reaction tables cover local time elements whose
+ * full-basis function ft maps to local row ft + row_offset (default -1). */
+int mi_op_set_reaction_rows(mi_ctx* ctx, int row_offset);
 
 /* ---------------------------------------------------------------------
  * Fast-diagonalisation preconditioner  (replaces
@@ -106,6 +109,13 @@ int mi_pc_setup(mi_ctx* ctx, const double* U, const double* lam, double cm, doub
                 const double* g, const double* glow, double sigma);
 /* z = P^-1 r  (r, z device; may alias) */
 int mi_pc_apply(mi_ctx* ctx, const double* r, double* z);
+/* Stages for the time-sharded preconditioner: spatial transforms
+ * of nrows local time rows (inverse=0: U^T, inverse=1: U), and the time
+ * stage (Q^T, block-arrowhead solve, Q) in place on a time-major (N_t x
+ * ncols) block of spatial eigen-columns [col0, col0+ncols) after the
+ * all-to-all transpose. */
+int mi_pc_apply_spatial(mi_ctx* ctx, const double* in, double* out, long long nrows, int inverse);
+int mi_pc_apply_time(mi_ctx* ctx, double* y, long long ncols, long long col0);
 
 /* ---------------------------------------------------------------------
  * Krylov primitives (replace the numpy CGS2 / update steps of gmres,

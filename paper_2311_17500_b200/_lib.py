@@ -32,8 +32,11 @@ _SIGS = {
     "mi_op_apply": ([_vp, _vp, _vp], _c_int),
     "mi_op_set_reaction": ([_vp, _vp, _vp, _c_dbl, _c_dbl, _c_dbl, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_clear_reaction": ([_vp], _c_int),
+    "mi_op_set_reaction_rows": ([_vp, _c_int], _c_int),
     "mi_pc_setup": ([_vp, _vp, _vp, _c_dbl, _c_dbl, _vp, _vp, _vp, _vp, _vp, _vp, _c_dbl], _c_int),
     "mi_pc_apply": ([_vp, _vp, _vp], _c_int),
+    "mi_pc_apply_spatial": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),
+    "mi_pc_apply_time": ([_vp, _vp, _c_ll, _c_ll], _c_int),
     "mi_dots": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp], _c_int),
     "mi_sub_combination": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp], _c_int),
     "mi_combination": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp, _vp], _c_int),

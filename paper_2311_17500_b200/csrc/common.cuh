@@ -89,6 +89,7 @@ struct mi_ctx {
   double c1 = 0, a = 0, c2 = 0;
   mi::DeviceBuf rx_B, rx_W;     // Gauss tables, directions x, y, z, t
   size_t rx_Boff[4] = {0, 0, 0, 0}, rx_Woff[4] = {0, 0, 0, 0};
+  int rx_rowoff = -1;          // constrained row of full time function ft = ft + rx_rowoff
   int rx_q[4] = {1, 1, 1, 1}, rx_p[4] = {0, 0, 0, 0}, rx_nel[4] = {1, 1, 1, 1}, rx_E[4] = {1, 1, 1, 1};
 
   // ---- preconditioner
@@ -99,7 +100,7 @@ struct mi_ctx {
   mi::DeviceBuf pen_diag, pen_off, pen_g, pen_glow;  // (nt-1)
   int* pen_partner = nullptr;   // (nt-1)
   double pen_sigma = 0, pc_cm = 1, pc_react = 0;
-  mi::DeviceBuf pc_t1, pc_t2;   // N each
+  mi::DeviceBuf pc_t1, pc_t2, pc_t3;   // N each
 
   // ---- profiling: per-slot accumulated ms and launch counts
   bool prof_on = false;

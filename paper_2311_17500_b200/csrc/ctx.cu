@@ -142,7 +142,7 @@ int mi_ctx_destroy(mi_ctx* c) {
   cudaSetDevice(c->device);
   mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->frag, &c->xt, &c->afr, &c->u_it, &c->w_it, &c->rx_B,
                            &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
-                           &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->partials};
+                           &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->partials};
   for (auto* b : bufs) mi::dfree(*b);
   for (int l = 0; l < 3; ++l) {
     mi::dfree(c->Us[l]);

@@ -23,10 +23,13 @@ __global__ void arrowhead_solve(double* __restrict__ Y, const double* __restrict
                                 const double* __restrict__ diag, const double* __restrict__ off,
                                 const int* __restrict__ partner, const double* __restrict__ gb,
                                 const double* __restrict__ gl, double sigma, double cm, double react,
-                                int n1, int n2, int nt, long long ns) {
+                                int n1, int n2, int nt, long long ns, long long col0) {
+  // Y is (nt x ns) with ns = number of columns handled; column j is global
+  // spatial eigen-index col0 + j (time-sharded runs handle a column range).
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= ns) return;
-  const int i1 = (int)(s % n1), i2 = (int)((s / n1) % n2), i3 = (int)(s / ((long long)n1 * n2));
+  const long long sg = s + col0;
+  const int i1 = (int)(sg % n1), i2 = (int)((sg / n1) % n2), i3 = (int)(sg / ((long long)n1 * n2));
   const double mu = react + lam1[i1] + lam2[i2] + lam3[i3];
   const int m = nt - 1;
   double sy = 0.0, sb = 0.0;
@@ -113,7 +116,8 @@ int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double
     for (int j = 0; j < nt; ++j) qt[(size_t)j * nt + i] = Q[(size_t)i * nt + j];
   if ((rc = dalloc(c->Q, (size_t)nt * nt)) || (rc = dalloc(c->QT, (size_t)nt * nt)) ||
       (rc = dalloc(c->pen_diag, m)) || (rc = dalloc(c->pen_off, m)) || (rc = dalloc(c->pen_g, m)) ||
-      (rc = dalloc(c->pen_glow, m)) || (rc = dalloc(c->pc_t1, c->N)) || (rc = dalloc(c->pc_t2, c->N)))
+      (rc = dalloc(c->pen_glow, m)) || (rc = dalloc(c->pc_t1, c->N)) || (rc = dalloc(c->pc_t2, c->N)) ||
+      (rc = dalloc(c->pc_t3, c->N)))
     return rc;
   for (int i = 0; i < m; ++i)
     MI_REQUIRE(partner[i] >= 0 && partner[i] < m && partner[partner[i]] == i, MI_ERR_ARG,
@@ -133,37 +137,97 @@ int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double
   return MI_OK;
 }
 
+}  // extern "C"
+
+namespace mi {
+
+// spatial transforms of nrows time rows: forward U_1^T, U_2^T, U_3^T or inverse U_3, U_2, U_1.
+// The result is written to out; scratch t1/t2 (>= nrows * ns each).
+static int pc_spatial(mi_ctx* c, const double* in, double* out, long long nrows, bool inverse) {
+  cudaStream_t st = c->stream;
+  const int n1 = c->n[0], n2 = c->n[1], n3 = c->n[2];
+  const long long ns = c->ns, N = nrows * ns;
+  const bool has[3] = {n1 > 1, n2 > 1, n3 > 1};
+  int nstage = has[0] + has[1] + has[2];
+  if (nstage == 0) {
+    if (out != in) MI_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    return MI_OK;
+  }
+  double* cand[3] = {c->pc_t1.p, c->pc_t2.p, c->pc_t3.p};
+  double* bufs[2];
+  int nb = 0;
+  for (int i = 0; i < 3 && nb < 2; ++i)
+    if (cand[i] != in && cand[i] != out) bufs[nb++] = cand[i];
+  int k = 0, done = 0;
+  const double* cur = in;
+  auto dst = [&]() { ++done; if (done == nstage) return out; double* b = bufs[k]; k ^= 1; return b; };
+  for (int step = 0; step < 3; ++step) {
+    const int l = inverse ? 2 - step : step;
+    if (!has[l]) continue;
+    double* o = dst();
+    ProfScope ps(c, PROF_PC_SPATIAL);
+    if (l == 0) {
+      MI_CUDA(mode_contig(inverse ? c->UsT[0].p : c->Us[0].p, cur, o, n1, N / n1, st));
+    } else if (l == 1) {
+      MI_CUDA(mode_strided(inverse ? c->Us[1].p : c->UsT[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st));
+    } else {
+      MI_CUDA(mode_strided(inverse ? c->Us[2].p : c->UsT[2].p, cur, o, n3, (long long)n1 * n2, nrows, st));
+    }
+    cur = o;
+  }
+  return MI_OK;
+}
+
+// time stage on a (nt x ncols) column block (time-major): Q^T, arrowhead, Q.  In place.
+static int pc_time(mi_ctx* c, double* y, long long ncols, long long col0) {
+  cudaStream_t st = c->stream;
+  const int nt = c->nt;
+  double* t = c->pc_t2.p;
+  {
+    ProfScope ps(c, PROF_PC_TIME);
+    MI_CUDA(mode_strided(c->QT.p, y, t, nt, ncols, 1, st));
+  }
+  {
+    ProfScope ps(c, PROF_PC_ARROW);
+    arrowhead_solve<<<(unsigned)((ncols + 127) / 128), 128, 0, st>>>(
+        t, c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p, c->pen_partner, c->pen_g.p,
+        c->pen_glow.p, c->pen_sigma, c->pc_cm, c->pc_react, c->n[0], c->n[1], nt, ncols, col0);
+    MI_CHECK_LAUNCH("arrowhead_solve");
+  }
+  {
+    ProfScope ps(c, PROF_PC_TIME);
+    MI_CUDA(mode_strided(c->Q.p, t, y, nt, ncols, 1, st));
+  }
+  return MI_OK;
+}
+
+}  // namespace mi
+
+using namespace mi;
+
+extern "C" {
+
 int mi_pc_apply(mi_ctx* c, const double* r, double* z) {
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
-  cudaStream_t st = c->stream;
-  const int n1 = c->n[0], n2 = c->n[1], n3 = c->n[2], nt = c->nt;
-  const long long ns = c->ns, N = c->N;
-  double* t1 = c->pc_t1.p;
-  double* t2 = c->pc_t2.p;
-  // forward: U_1^T (x), U_2^T (y), U_3^T (z), Q^T (t)
-  const double* cur = r;
-  double* bufs[2] = {t1, t2};
-  int k = 0;
-  auto next = [&]() { double* b = bufs[k]; k ^= 1; return b; };
-  if (n1 > 1) { double* o = next(); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_contig(c->Us[0].p, cur, o, n1, N / n1, st)); cur = o; }
-  if (n2 > 1) { double* o = next(); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->UsT[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
-  if (n3 > 1) { double* o = next(); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->UsT[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
-  { double* o = next(); ProfScope ps(c, PROF_PC_TIME); MI_CUDA(mode_strided(c->QT.p, cur, o, nt, ns, 1, st)); cur = o; }
-  {
-  ProfScope ps(c, PROF_PC_ARROW);
-  arrowhead_solve<<<(unsigned)((ns + 127) / 128), 128, 0, st>>>(
-      const_cast<double*>(cur), c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p,
-      c->pen_partner, c->pen_g.p, c->pen_glow.p, c->pen_sigma, c->pc_cm, c->pc_react, n1, n2, nt, ns);
-  MI_CHECK_LAUNCH("arrowhead_solve");
-  }
-  // inverse: Q (t), U_3 (z), U_2 (y), U_1 (x); the last stage writes z
-  const bool more_z = n3 > 1, more_y = n2 > 1, more_x = n1 > 1;
-  auto dst = [&](bool last) { return last ? z : next(); };
-  { double* o = dst(!more_z && !more_y && !more_x); ProfScope ps(c, PROF_PC_TIME); MI_CUDA(mode_strided(c->Q.p, cur, o, nt, ns, 1, st)); cur = o; }
-  if (more_z) { double* o = dst(!more_y && !more_x); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->Us[2].p, cur, o, n3, (long long)n1 * n2, nt, st)); cur = o; }
-  if (more_y) { double* o = dst(!more_x); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_strided(c->Us[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st)); cur = o; }
-  if (more_x) { double* o = dst(true); ProfScope ps(c, PROF_PC_SPATIAL); MI_CUDA(mode_contig(c->UsT[0].p, cur, o, n1, N / n1, st)); cur = o; }
-  return MI_OK;
+  int rc;
+  // forward spatial into pc_t1 (scratch t2 used internally), time stage in place, inverse into z
+  double* y = c->pc_t1.p;
+  if ((rc = pc_spatial(c, r, y, c->nt, false))) return rc;
+  if ((rc = pc_time(c, y, c->ns, 0))) return rc;
+  return pc_spatial(c, y, z, c->nt, true);
+}
+
+int mi_pc_apply_spatial(mi_ctx* c, const double* in, double* out, long long nrows, int inverse) {
+  MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
+  MI_REQUIRE(nrows >= 1 && nrows <= c->nt, MI_ERR_ARG, "nrows out of range");
+  MI_REQUIRE(in != out, MI_ERR_ARG, "in and out must not alias");
+  return pc_spatial(c, in, out, nrows, inverse != 0);
+}
+
+int mi_pc_apply_time(mi_ctx* c, double* y, long long ncols, long long col0) {
+  MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
+  MI_REQUIRE(ncols >= 1 && col0 >= 0 && col0 + ncols <= c->ns, MI_ERR_ARG, "column range out of range");
+  return pc_time(c, y, ncols, col0);
 }
 
 }  // extern "C"

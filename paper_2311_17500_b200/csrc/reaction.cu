@@ -30,7 +30,8 @@ struct RxArgs {
   int n[3];            // spatial functions per direction
   int color[3];        // colour class of this launch (element index mod (p+1))
   int ncol[3];         // elements of this colour per direction
-  int ntc;             // constrained time functions
+  int ntc;             // constrained time functions (rows of this context)
+  int rowoff;          // row of full time function ft is ft + rowoff (-1 unsharded)
   long long ns;
   double c1, a, c2;
 };
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
     return ((long long)(e[2] + j3) * r.n[1] + (e[1] + j2)) * r.n[0] + (e[0] + j1);
   };
   auto load_slice = [&](int ft) {                     // full-basis time function ft
-    const int ct = ft - 1, slot = ft % PW;
+    const int ct = ft + r.rowoff, slot = ft % PW;
     for (int s = lane; s < LS; s += 32) {
       const bool v = ct >= 0 && ct < r.ntc;
       const long long gi = (long long)ct * r.ns + gidx(s);
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
     }
   };
   auto flush_slice = [&](int ft) {
-    const int ct = ft - 1, slot = ft % PW;
+    const int ct = ft + r.rowoff, slot = ft % PW;
     if (ct >= 0 && ct < r.ntc)
       for (int s = lane; s < LS; s += 32) r.y[(long long)ct * r.ns + gidx(s)] += outw[slot * LS + s];
   };
@@ -268,6 +269,7 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   r.n[1] = c->n[1];
   r.n[2] = c->n[2];
   r.ntc = c->nt;
+  r.rowoff = c->rx_rowoff;
   r.ns = c->ns;
   r.c1 = c->c1;
   r.a = c->a;
@@ -355,6 +357,12 @@ int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, d
   for (int l = 0; l < 4; ++l)
     MI_REQUIRE(c->rx_q[l] == ((l == 3 || l < c->d) ? c->p + 1 : 1), MI_ERR_ARG, "reaction: need q = p + 1");
   c->reaction_on = true;
+  return MI_OK;
+}
+
+int mi_op_set_reaction_rows(mi_ctx* c, int row_offset) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  c->rx_rowoff = row_offset;
   return MI_OK;
 }
 

@@ -32,7 +32,7 @@ def dptr(t):
 class DeviceContext:
     """Owns the C context for one space-time shape on one GPU."""
 
-    def __init__(self, space_time, device=0):
+    def __init__(self, space_time, device=0, nt=None):
         self.device = _require_cuda(device)
         st = space_time
         self.space_time = st
@@ -42,7 +42,7 @@ class DeviceContext:
             raise ValueError("all spatial directions must share one degree")
         self.pt = int(st.time.degree)
         self.n = [int(s.dimension) for s in st.spatial]
-        self.nt = int(st.time.dimension) - 1
+        self.nt = int(st.time.dimension) - 1 if nt is None else int(nt)
         self.ns = int(np.prod(self.n))
         self.N = self.ns * self.nt
         _lib.load()

@@ -7,6 +7,11 @@ vector vanishes.  The Krylov basis lives in HBM; all length-N work runs in
 libmonoiga_b200 kernels (deterministic reductions).  Only the (j+1)-long
 Hessenberg column and the Givens rotations are handled on the host (one
 small device->host copy per iteration, needed for the stopping test).
+
+The core loop (:func:`gmres_core`) is written against a small vector-ops
+interface plus an optional ``allreduce`` hook, so the time-sharded solve
+(sharded.py) runs the identical recurrence on local slabs with NCCL
+allreduces of the dot products.
 """
 
 import ctypes
@@ -27,86 +32,85 @@ def _write_log(path, history):
             fh.write("%d,%.17g\n" % (i, r))
 
 
-def default_max_iter(n, ctx, reserve_vectors=8, fraction=0.6):
-    """Unrestarted GMRES keeps max_iter+1 basis vectors; the reference's
-    default max_iter = n (linalg.py:381-382) is replaced by the HBM bound."""
-    free, _ = torch.cuda.mem_get_info(ctx.device)
-    cap = int(fraction * free // (8 * n)) - reserve_vectors
-    return max(1, min(n, cap, 1000))
+class DeviceVecOps:
+    """Krylov vector kernels of libmonoiga_b200 on one context's stream."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.h = ctx.handle
+
+    def dots(self, V, k, w, out):
+        """out[:k] = V[:k] @ w (local partial sums)."""
+        n = w.numel()
+        _lib.call("mi_dots", self.h, n, k, ctypes.c_void_p(V.data_ptr()), V.stride(0), dptr(w), dptr(out))
+
+    def sub_comb(self, V, k, hvec, w):
+        n = w.numel()
+        _lib.call("mi_sub_combination", self.h, n, k, ctypes.c_void_p(V.data_ptr()), V.stride(0), dptr(hvec),
+                  dptr(w))
+
+    def normalize(self, src, nrm2, dst):
+        _lib.call("mi_normalize", self.h, src.numel(), dptr(src), dptr(nrm2), dptr(dst))
+
+    def comb(self, V, k, y, x0, out):
+        n = out.numel()
+        _lib.call("mi_combination", self.h, n, k, ctypes.c_void_p(V.data_ptr()), V.stride(0), dptr(y),
+                  dptr(x0) if x0 is not None else ctypes.c_void_p(0), dptr(out))
 
 
-def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None):
-    """Returns ``(x, iterations, residual_history)`` like linalg.py:367-447.
+def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=None, n_global=None):
+    """CGS2 GMRES on (local) vectors; see module docstring.
 
-    ``op`` / ``precond`` are device objects of this package (they expose
-    ``apply_device``).  ``rhs`` / ``x0`` may be numpy arrays (then ``x`` is
-    returned as numpy) or CUDA tensors.
+    apply_A(src, dst), apply_P(src, dst): device applies on local vectors.
+    allreduce(t): in-place sum over ranks of a small tensor (None = 1 rank).
+    Returns (x_local, iterations, history).
     """
-    if not hasattr(op, "apply_device"):
-        raise TypeError("device gmres needs a device operator (KroneckerOperator of this package)")
-    if precond is not None and not hasattr(precond, "apply_device"):
-        raise TypeError("device gmres needs a device preconditioner")
-    ctx = op.ctx
-    ctx.bind_stream()
-    h = ctx.handle
-    as_numpy = not isinstance(rhs, torch.Tensor)
-    b = ctx.to_device(rhs)
+    dev = b.device
     n = b.numel()
-    if n != op.shape[0]:
-        raise ValueError("dimension mismatch: operator of size %d applied to vector of size %d"
-                         % (op.shape[0], n))
-    m = default_max_iter(n, ctx) if max_iter is None else int(max_iter)
-    dev = ctx.device
-
-    def out(t):
-        return t.cpu().numpy() if as_numpy else t
-
-    def P(src, dst):
-        if precond is None:
-            dst.copy_(src)
-        else:
-            precond.apply_device(src, dst)
-
-    tmp = ctx.empty(n)
-    scal = torch.empty(4 * (m + 2) + 8, dtype=torch.float64, device=dev)
+    red = allreduce if allreduce is not None else (lambda t: None)
+    tmp = torch.empty_like(b)
+    scal = torch.zeros(8 + 2 * (m + 1), dtype=torch.float64, device=dev)
     nrm = scal[0:1]
+    h1 = scal[8:8 + m + 1]
+    h2 = scal[8 + m + 1:8 + 2 * (m + 1)]
     if x0 is None:
-        xs = torch.zeros(n, dtype=torch.float64, device=dev)
+        xs = torch.zeros_like(b)
         r = b
     else:
-        xs = ctx.to_device(x0).clone()
-        op.apply_device(xs, tmp)
+        xs = x0.clone()
+        apply_A(xs, tmp)
         minus = torch.full((1,), -1.0, dtype=torch.float64, device=dev)
-        r = ctx.empty(n)
-        _lib.call("mi_combination", h, n, 1, dptr(tmp), n, dptr(minus), dptr(b), dptr(r))
+        r = torch.empty_like(b)
+        ops.comb(tmp.view(1, -1), 1, minus, b, r)
     V = torch.empty((m + 1, n), dtype=torch.float64, device=dev)
-    P(r, V[0])
-    _lib.call("mi_dots", h, n, 1, dptr(V[0]), n, dptr(V[0]), dptr(nrm))
+    apply_P(r, V[0])
+    ops.dots(V[0].view(1, -1), 1, V[0], nrm)
+    red(nrm)
     beta = float(np.sqrt(nrm.item()))
     if beta == 0.0:
         if log_path is not None:
             _write_log(log_path, [0.0])
-        return out(xs), 0, [0.0]
-    _lib.call("mi_normalize", h, n, dptr(V[0]), dptr(nrm), dptr(V[0]))
+        return xs, 0, [0.0]
+    ops.normalize(V[0], nrm, V[0])
     H = np.zeros((m + 1, m))
     cs, sn, gv = np.zeros(m), np.zeros(m), np.zeros(m + 1)
     gv[0] = beta
     history = [1.0]
     k_done = None
-    w = ctx.empty(n)
-    h1 = scal[8:8 + m + 1]
-    h2 = scal[8 + m + 1:8 + 2 * (m + 1)]
-    Vp = V.data_ptr()
+    w = torch.empty_like(b)
     for j in range(m):
-        op.apply_device(V[j], tmp)
-        P(tmp, w)
+        apply_A(V[j], tmp)
+        apply_P(tmp, w)
         k = j + 1
-        _lib.call("mi_dots", h, n, k, ctypes.c_void_p(Vp), n, dptr(w), dptr(h1))
-        _lib.call("mi_sub_combination", h, n, k, ctypes.c_void_p(Vp), n, dptr(h1), dptr(w))
-        _lib.call("mi_dots", h, n, k, ctypes.c_void_p(Vp), n, dptr(w), dptr(h2))
-        _lib.call("mi_sub_combination", h, n, k, ctypes.c_void_p(Vp), n, dptr(h2), dptr(w))
-        _lib.call("mi_dots", h, n, 1, dptr(w), n, dptr(w), dptr(nrm))
-        host = scal[:8 + 2 * (m + 1)].cpu().numpy()
+        ops.dots(V, k, w, h1)
+        red(h1[:k])
+        ops.sub_comb(V, k, h1, w)
+        ops.dots(V, k, w, h2)
+        red(h2[:k])
+        ops.sub_comb(V, k, h2, w)
+        ops.dots(w.view(1, -1), 1, w, nrm)
+        red(nrm)
+        host = scal.cpu().numpy()
         hv = host[8:8 + k] + host[8 + m + 1:8 + m + 1 + k]
         hnorm = float(np.sqrt(host[0]))
         H[:k, j] = hv
@@ -129,7 +133,7 @@ def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None
         if rel <= tol or hnorm == 0.0:
             k_done = j + 1
             break
-        _lib.call("mi_normalize", h, n, dptr(w), dptr(nrm), dptr(V[j + 1]))
+        ops.normalize(w, nrm, V[j + 1])
     if k_done is None:
         if log_path is not None:
             _write_log(log_path, history)
@@ -137,8 +141,48 @@ def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None
                                   iterations=m, residuals=history)
     y = sla.solve_triangular(H[:k_done, :k_done], gv[:k_done])
     yd = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
-    xout = ctx.empty(n)
-    _lib.call("mi_combination", h, n, k_done, ctypes.c_void_p(Vp), n, dptr(yd), dptr(xs), dptr(xout))
+    xout = torch.empty_like(b)
+    ops.comb(V, k_done, yd, xs, xout)
     if log_path is not None:
         _write_log(log_path, history)
-    return out(xout), k_done, history
+    return xout, k_done, history
+
+
+def default_max_iter(n, device, reserve_vectors=8, fraction=0.6):
+    """Unrestarted GMRES keeps max_iter+1 basis vectors; the reference's
+    default max_iter = n (linalg.py:381-382) is replaced by the HBM bound."""
+    free, _ = torch.cuda.mem_get_info(device)
+    cap = int(fraction * free // (8 * n)) - reserve_vectors
+    return max(1, min(n, cap, 1000))
+
+
+def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None):
+    """Returns ``(x, iterations, residual_history)`` like linalg.py:367-447.
+
+    ``op`` / ``precond`` are device objects of this package (they expose
+    ``apply_device``).  ``rhs`` / ``x0`` may be numpy arrays (then ``x`` is
+    returned as numpy) or CUDA tensors.
+    """
+    if not hasattr(op, "apply_device"):
+        raise TypeError("device gmres needs a device operator (KroneckerOperator of this package)")
+    if precond is not None and not hasattr(precond, "apply_device"):
+        raise TypeError("device gmres needs a device preconditioner")
+    ctx = op.ctx
+    ctx.bind_stream()
+    as_numpy = not isinstance(rhs, torch.Tensor)
+    b = ctx.to_device(rhs)
+    n = b.numel()
+    if n != op.shape[0]:
+        raise ValueError("dimension mismatch: operator of size %d applied to vector of size %d"
+                         % (op.shape[0], n))
+    m = default_max_iter(n, ctx.device) if max_iter is None else int(max_iter)
+
+    def P(src, dst):
+        if precond is None:
+            dst.copy_(src)
+        else:
+            precond.apply_device(src, dst)
+
+    x0d = None if x0 is None else ctx.to_device(x0)
+    x, it, hist = gmres_core(op.apply_device, P, DeviceVecOps(ctx), b, x0d, tol, m, log_path=log_path)
+    return (x.cpu().numpy() if as_numpy else x), it, hist

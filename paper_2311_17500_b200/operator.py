@@ -68,9 +68,15 @@ class KroneckerOperator:
     """
 
     def __init__(self, space_time, final_time, capacitance=1.0, diffusion=1e-4, constants=None,
-                 u=None, w=None, stabilization=None, lengths=None, device=0, context=None):
+                 u=None, w=None, stabilization=None, lengths=None, device=0, context=None, time_rows=None):
+        """``time_rows=(e_lo, e_hi)`` builds the operator restricted to a slab of
+        constrained time rows (time-sharded runs, sharded.py): the time bands
+        are the global rows e_lo..e_hi, and u, w (if given) are slab vectors."""
         st = space_time
-        self.ctx = context if context is not None else DeviceContext(st, device)
+        nt_glob = st.time.dimension - 1
+        self.time_rows = (0, nt_glob) if time_rows is None else tuple(int(v) for v in time_rows)
+        r0, r1 = self.time_rows
+        self.ctx = context if context is not None else DeviceContext(st, device, nt=r1 - r0)
         ctx = self.ctx
         self.space_time = st
         self.num_time, self.num_space = ctx.nt, ctx.ns
@@ -92,12 +98,14 @@ class KroneckerOperator:
         _lib.call("mi_op_setup", ctx.handle, nchan)
         # time bands: c0 = C_m W_t, c1 = M_t, SU ranks
         Wt, Mt = time_factors(st, final_time)
-        bands = np.zeros((nchan, ctx.nt, 2 * pt + 1))
+        bands = np.zeros((nchan, nt_glob, 2 * pt + 1))
         bands[0] = capacitance * to_band(Wt, pt)
         bands[1] = to_band(Mt, pt)
         if R:
             bands[2:] = stab.time_bands
-        bands = np.ascontiguousarray(bands)
+        # slab rows: band entries reaching outside the slab multiply halo rows
+        # whose results are discarded by the caller
+        bands = np.ascontiguousarray(bands[:, r0:r1])
         _lib.call("mi_op_set_time_bands", ctx.handle, host_ptr(bands))
         # spatial Kronecker channels
         nmax = max(ctx.n)
@@ -133,7 +141,7 @@ class KroneckerOperator:
             _lib.call("mi_op_set_su_channel", ctx.handle, 2 + r, host_ptr(th), host_ptr(H), stab.ko)
         if not zero_iterate:
             from .reaction import set_reaction
-            set_reaction(ctx, st, final_time, consts, u, w, L)
+            set_reaction(ctx, st, final_time, consts, u, w, L, time_rows=self.time_rows)
 
     @property
     def shape(self):

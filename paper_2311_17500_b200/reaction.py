@@ -29,7 +29,7 @@ def element_tables(space, q, scale):
     return B, (w * scale).reshape(ne, q)
 
 
-def set_reaction(ctx, st, final_time, consts, u, w, lengths):
+def set_reaction(ctx, st, final_time, consts, u, w, lengths, time_rows=None):
     d = len(st.spatial)
     L = np.ones(d) if lengths is None else np.asarray(lengths, float)
     Bs, Ws, qs, nels = [], [], [], []
@@ -37,7 +37,16 @@ def set_reaction(ctx, st, final_time, consts, u, w, lengths):
         B, W = element_tables(s, s.degree + 1, L[l])
         Bs.append(B.ravel()); Ws.append(W.ravel()); qs.append(s.degree + 1); nels.append(B.shape[0])
     B, W = element_tables(st.time, st.time.degree + 1, final_time)
-    Bs.append(B.ravel()); Ws.append(W.ravel()); qs.append(st.time.degree + 1); nels.append(B.shape[0])
+    pt = st.time.degree
+    nt_glob = st.time.dimension - 1
+    r0, r1 = (0, nt_glob) if time_rows is None else time_rows
+    # elements whose functions (full index e..e+pt, constrained row = full - 1)
+    # touch the slab rows [r0, r1); local row of full function ft_local is
+    # ft_local + (el0 - 1 - r0)
+    el0 = max(0, r0 + 1 - pt)
+    el1 = min(B.shape[0], r1 + 1)
+    B, W = B[el0:el1], W[el0:el1]
+    Bs.append(B.ravel()); Ws.append(W.ravel()); qs.append(pt + 1); nels.append(B.shape[0])
     Bh = np.ascontiguousarray(np.concatenate(Bs))
     Wh = np.ascontiguousarray(np.concatenate(Ws))
     qh = np.asarray(qs, dtype=np.int32)
@@ -47,3 +56,4 @@ def set_reaction(ctx, st, final_time, consts, u, w, lengths):
     ctx.bind_stream()
     _lib.call("mi_op_set_reaction", ctx.handle, dptr(ud), dptr(wd), float(consts["c1"]), float(consts["a"]),
               float(consts["c2"]), host_ptr(qh), host_ptr(nh), host_ptr(Bh), host_ptr(Wh))
+    _lib.call("mi_op_set_reaction_rows", ctx.handle, int(el0 - 1 - r0))
