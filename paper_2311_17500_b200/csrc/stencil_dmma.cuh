@@ -138,16 +138,17 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   // Fast path: one (h1, h2) column of the halo per thread, h3 = q
   // (THREADS == H1*H2*PAIRS, e.g. d=3 p=3), so a copy is one add + compare.
   constexpr bool FAST = G::THREADS == G::H1 * G::H2 * PAIRS;
-  const int fpr = tid % PAIRS, fh12 = tid / PAIRS;
-  const int fg1 = o1 - P + fh12 % G::H1;
-  const int fg2 = D >= 2 ? o2 - P + fh12 / G::H1 : 0;
-  const bool fval12 = fg1 >= 0 && fg1 < a.n1 && fg2 >= 0 && fg2 < a.n2;
-  const long long plane = (long long)a.n1 * a.n2 * a.ntp;
-  const double* fsrc0 = a.xt + (((long long)(o3 - P) * a.n2 + fg2) * a.n1 + fg1) * a.ntp + 2 * fpr;
   auto load_chunk = [&](int buf, int t0) {
     if (t0 >= a.nt) return;
     double* dst = Xs + buf * G::HS * G::TSTR;
     if constexpr (FAST) {
+      // recomputed per chunk (cheap) rather than kept live across the sweep
+      const int fpr = tid % PAIRS, fh12 = tid / PAIRS;
+      const int fg1 = o1 - P + fh12 % G::H1;
+      const int fg2 = D >= 2 ? o2 - P + fh12 / G::H1 : 0;
+      const bool fval12 = fg1 >= 0 && fg1 < a.n1 && fg2 >= 0 && fg2 < a.n2;
+      const long long plane = (long long)a.n1 * a.n2 * a.ntp;
+      const double* fsrc0 = a.xt + (((long long)(o3 - P) * a.n2 + fg2) * a.n1 + fg1) * a.ntp + 2 * fpr;
       double* d0 = dst + fh12 * G::TSTR + 2 * fpr;
 #pragma unroll
       for (int q = 0; q < G::H3; ++q) {
@@ -171,11 +172,20 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
 
   // time filter on the tensor cores: warps 0..7 -> (mtile fm, channel pair fcq)
   const int fm = warp & 1, fcq = (warp >> 1) & 3;
-  // output write of the previous filter: threads 0..127 -> (mtile, row m, point n)
-  const int om = (tid >> 6) & 1, orow = (tid >> 3) & 7, opt = tid & 7;
-  const int q1 = o1 + opt % G::B1, q2 = o2 + (opt / G::B1) % G::B2, q3 = o3 + opt / (G::B1 * G::B2);
-  const bool ovalid = q1 < a.n1 && q2 < a.n2 && q3 < a.n3;
-  const long long oidx = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
+  // output write of the previous filter: warps 8..11 (tid 256..383) -> (mtile, row m, point n);
+  // warps 0..7 run the tensor-core filter, so the extra work is spread over 12 warps
+  auto write_y = [&](int ch_buf, int tbase) {
+    const int wt_ = tid - 256;
+    const int om = (wt_ >> 6) & 1, orow = (wt_ >> 3) & 7, opt = wt_ & 7;
+    const int q1 = o1 + opt % G::B1, q2 = o2 + (opt / G::B1) % G::B2, q3 = o3 + opt / (G::B1 * G::B2);
+    const int t = tbase + 8 * om + orow;
+    if (t >= 0 && t < a.nt && q1 < a.n1 && q2 < a.n2 && q3 < a.n3) {
+      const double* yp = ys + (ch_buf * 2 + om) * 4 * 64 + orow * 8 + opt;
+      const double v = (yp[0] + yp[64]) + (yp[128] + yp[192]);
+      double* dst = a.y + (long long)t * a.ns + ((long long)q3 * a.n2 + q2) * a.n1 + q1;
+      if (a.accumulate) *dst += v; else *dst = v;
+    }
+  };
 
   const int base = ((pt / (G::B1 * G::B2)) * G::H2 + (pt / G::B1) % G::B2) * G::H1 + pt % G::B1;
   const int kl = lane & 3, mrow = lane >> 2;
@@ -192,15 +202,7 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
     if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
     cp_async_commit();
     // ---- write y of the filter of chunk ch-2 (partials summed over channel pairs)
-    if (ch >= 2 && tid < 128) {
-      const int t = t0 - 2 * G::TT - a.pt + 8 * om + orow;
-      if (t >= 0 && t < a.nt && ovalid) {
-        const double* yp = ys + ((ch & 1) * 2 + om) * 4 * 64 + orow * 8 + opt;
-        const double v = (yp[0] + yp[64]) + (yp[128] + yp[192]);
-        double* dst = a.y + (long long)t * a.ns + oidx;
-        if (a.accumulate) *dst += v; else *dst = v;
-      }
-    }
+    if (ch >= 2 && tid >= 256 && tid < 384) write_y(ch & 1, t0 - 2 * G::TT - a.pt);
     // ---- time filter of chunk ch-1 on the tensor cores (warps 0..7)
     if (ch >= 1 && warp < 8) {
       const int tau = 2 * (ch - 1) + fm;                   // M-tile rows tb = 8 tau - pt
@@ -246,15 +248,7 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   }
   // flush the last filter's partials (chunk nchunks-2)
   __syncthreads();
-  if (tid < 128) {
-    const int t = nchunks * G::TT - 2 * G::TT - a.pt + 8 * om + orow;
-    if (t >= 0 && t < a.nt && ovalid) {
-      const double* yp = ys + ((nchunks & 1) * 2 + om) * 4 * 64 + orow * 8 + opt;
-      const double v = (yp[0] + yp[64]) + (yp[128] + yp[192]);
-      double* dst = a.y + (long long)t * a.ns + oidx;
-      if (a.accumulate) *dst += v; else *dst = v;
-    }
-  }
+  if (tid >= 256 && tid < 384) write_y(nchunks & 1, nchunks * G::TT - 2 * G::TT - a.pt);
 }
 
 // Time-filter A fragments: afr[tau][ks][lane] = T_{c0+c}[t, t'] with
