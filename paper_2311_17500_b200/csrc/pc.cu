@@ -67,14 +67,14 @@ static cudaError_t mode_strided(const double* A, const double* in, double* out, 
                                 long long outer, cudaStream_t st) {
   // out[o, i, c] = sum_j A[i, j] in[o, j, c]
   GemmArgs g{A, in, out, n, (int)inner, n, n, inner, inner, 0, (long long)n * inner, (long long)n * inner};
-  return launch_dgemm(g, (int)outer, st);
+  return launch_panel_n<true>(g, n, (int)outer, st);
 }
 
 static cudaError_t mode_contig(const double* Bm, const double* in, double* out, int n, long long rows,
                                cudaStream_t st) {
   // out[r, i] = sum_j in[r, j] Bm[j, i]
   GemmArgs g{in, Bm, out, (int)rows, n, n, n, n, n, 0, 0, 0};
-  return launch_dgemm(g, 1, st);
+  return launch_panel_n<false>(g, n, 1, st);
 }
 
 }  // namespace mi
