@@ -39,16 +39,19 @@ struct RxArgs {
 // One warp per spatial element (colour class: elements p+1 apart never
 // share a basis function), sweeping all time elements with a sliding
 // window of p_t+1 coefficient slices and p_t+1 output slices in shared
-// memory.  Sum factorisation per time Gauss point: x, y, z interpolation of
-// u, w, x (LD = p+1 functions -> Q = p+1 points per direction), pointwise
-// C_r(u, w) x W, then z, y, x projection.  q = p+1 is the reference rule.
+// memory.  Sum factorisation per time Gauss point as LINE operations: a lane
+// takes one line of LD coefficients along a direction and produces its Q
+// Gauss values with the element's 1D basis matrix held in registers
+// (LD loads -> LD*Q FMAs -> Q stores), then C_r(u, w) x W pointwise and the
+// transposed line operations back.  q = p+1 is the reference rule.
 template <int D, int P, int PT>
-__global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
+__global__ void __launch_bounds__(128, 8) reaction_warp(RxArgs r) {
   constexpr int LD = P + 1, Q = P + 1;
   constexpr int L1 = LD, L2 = D >= 2 ? LD : 1, L3 = D >= 3 ? LD : 1;
   constexpr int LS = L1 * L2 * L3;                   // local spatial functions (= quad points)
   constexpr int PW = PT + 1;                         // time window
   constexpr int QT = PT + 1;                         // time Gauss points
+  constexpr int NL = LS / LD;                        // lines per field along a direction
   constexpr int WARP_SM = 3 * PW * LS + PW * LS + 2 * 3 * LS + 3 * Q * LD;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -57,7 +60,7 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
   double* outw = win + 3 * PW * LS;                  // [PW][LS]
   double* ta = outw + PW * LS;                       // [3][LS]
   double* tb = ta + 3 * LS;                          // [3][LS]
-  double* bsp = tb + 3 * LS;                         // [3 dirs][Q][LD] spatial basis of this element
+  double* bsm = tb + 3 * LS;                         // [3 dirs][Q][LD] basis of this element
 
   long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nw = (long long)r.ncol[0] * r.ncol[1] * r.ncol[2];
@@ -71,14 +74,16 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
       e[l] = (l < D) ? m * LD + r.color[l] : 0;
     }
   }
-  // spatial basis tables of this element and quadrature weights (registers)
-  double wsp[LS > 32 ? (LS + 31) / 32 : 1];
-  for (int l = 0; l < 3; ++l) {
-    for (int i = lane; i < Q * LD; i += 32) {
-      const bool pres = l < D;
-      bsp[l * Q * LD + i] = pres ? r.B[l][(long long)e[l] * Q * LD + i] : (i == 0 ? 1.0 : 0.0);
-    }
+  // the element's 1D basis matrices B_l[g][j] (shared by the warp's lanes: broadcast loads)
+  for (int i = lane; i < 3 * Q * LD; i += 32) {
+    const int l = i / (Q * LD), gj = i % (Q * LD);
+    bsm[i] = l < D ? __ldg(r.B[l] + (long long)e[l] * Q * LD + gj) : 0.0;
   }
+  __syncwarp();
+  const double* bx = bsm;
+  const double* by = bsm + Q * LD;
+  const double* bz = bsm + 2 * Q * LD;
+  double wsp[(LS + 31) / 32];
 #pragma unroll
   for (int k = 0; k < (LS + 31) / 32; ++k) {
     const int s = lane + 32 * k;
@@ -91,15 +96,14 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
     }
     wsp[k] = wv;
   }
-  // global index of local function s
   auto gidx = [&](int s) -> long long {
     const int j1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
     return ((long long)(e[2] + j3) * r.n[1] + (e[1] + j2)) * r.n[0] + (e[0] + j1);
   };
   auto load_slice = [&](int ft) {                     // full-basis time function ft
     const int ct = ft + r.rowoff, slot = ft % PW;
+    const bool v = ct >= 0 && ct < r.ntc;
     for (int s = lane; s < LS; s += 32) {
-      const bool v = ct >= 0 && ct < r.ntc;
       const long long gi = (long long)ct * r.ns + gidx(s);
       win[(0 * PW + slot) * LS + s] = v ? r.u[gi] : 0.0;
       win[(1 * PW + slot) * LS + s] = v ? r.w[gi] : 0.0;
@@ -112,11 +116,38 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
     if (ct >= 0 && ct < r.ntc)
       for (int s = lane; s < LS; s += 32) r.y[(long long)ct * r.ns + gidx(s)] += outw[slot * LS + s];
   };
-  // interpolation along direction l: in[j] (L per dir) -> out[g] (Q per dir); strides in the
-  // combined (dir1, dir2, dir3) index with extents ext (before) -> ext with dir l replaced.
-  const double* bx = bsp;
-  const double* by = bsp + Q * LD;
-  const double* bz = bsp + 2 * Q * LD;
+  // line op along a direction with stride `st` (1, L1, L1*L2): in[line base + j*st] -> out[.. + g*st]
+  auto line_fwd = [&](const double* in, double* out, const double* bm, int lb, int st) {
+    double v[LD];
+#pragma unroll
+    for (int j = 0; j < LD; ++j) v[j] = in[lb + j * st];
+#pragma unroll
+    for (int g = 0; g < Q; ++g) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < LD; ++j) acc = fma(bm[g * LD + j], v[j], acc);
+      out[lb + g * st] = acc;
+    }
+  };
+  auto line_bwd = [&](const double* in, double* out, const double* bm, int lb, int st) {
+    double v[Q];
+#pragma unroll
+    for (int g = 0; g < Q; ++g) v[g] = in[lb + g * st];
+#pragma unroll
+    for (int j = 0; j < LD; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int g = 0; g < Q; ++g) acc = fma(bm[g * LD + j], v[g], acc);
+      out[lb + j * st] = acc;
+    }
+  };
+  // line base index of line `li` (0..NL) along direction dir
+  auto line_base = [&](int dir, int li) -> int {
+    if (dir == 0) return li * L1;                                // (j2, j3) -> rows of L1
+    if (dir == 1) return (li / L1) * (L1 * L2) + (li % L1);      // (g1, j3)
+    return li;                                                   // (g1, g2)
+  };
+
   for (int ft = 0; ft < PT; ++ft) load_slice(ft);
   for (int et = 0; et < r.nel[3]; ++et) {
     load_slice(et + PT);
@@ -136,41 +167,17 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
         ta[i] = v;
       }
       __syncwarp();
-      // x: ta -> tb
-      for (int i = lane; i < 3 * LS; i += 32) {
-        const int fld = i / LS, s = i % LS;
-        const int g1 = s % L1, rest = s / L1;
-        const double* src = ta + fld * LS + rest * L1;
-        double v = 0.0;
-#pragma unroll
-        for (int j = 0; j < L1; ++j) v = fma(bx[g1 * LD + j], src[j], v);
-        tb[i] = v;
-      }
+      // x, y, z interpolation as line ops: ta -> tb -> ta -> tb
+      for (int i = lane; i < 3 * NL; i += 32) line_fwd(ta + (i / NL) * LS, tb + (i / NL) * LS, bx, line_base(0, i % NL), 1);
       __syncwarp();
-      if (D >= 2) {  // y: tb -> ta
-        for (int i = lane; i < 3 * LS; i += 32) {
-          const int fld = i / LS, s = i % LS;
-          const int g1 = s % L1, g2 = (s / L1) % L2, g3 = s / (L1 * L2);
-          const double* src = tb + fld * LS + g3 * L1 * L2 + g1;
-          double v = 0.0;
-#pragma unroll
-          for (int j = 0; j < L2; ++j) v = fma(by[g2 * LD + j], src[j * L1], v);
-          ta[i] = v;
-        }
+      if (D >= 2) {
+        for (int i = lane; i < 3 * NL; i += 32) line_fwd(tb + (i / NL) * LS, ta + (i / NL) * LS, by, line_base(1, i % NL), L1);
       } else {
         for (int i = lane; i < 3 * LS; i += 32) ta[i] = tb[i];
       }
       __syncwarp();
-      if (D >= 3) {  // z: ta -> tb
-        for (int i = lane; i < 3 * LS; i += 32) {
-          const int fld = i / LS, s = i % LS;
-          const int g12 = s % (L1 * L2), g3 = s / (L1 * L2);
-          const double* src = ta + fld * LS + g12;
-          double v = 0.0;
-#pragma unroll
-          for (int j = 0; j < L3; ++j) v = fma(bz[g3 * LD + j], src[j * L1 * L2], v);
-          tb[i] = v;
-        }
+      if (D >= 3) {
+        for (int i = lane; i < 3 * NL; i += 32) line_fwd(ta + (i / NL) * LS, tb + (i / NL) * LS, bz, line_base(2, i % NL), L1 * L2);
       } else {
         for (int i = lane; i < 3 * LS; i += 32) tb[i] = ta[i];
       }
@@ -186,43 +193,29 @@ __global__ void __launch_bounds__(128) reaction_warp(RxArgs r) {
         }
       }
       __syncwarp();
-      // projections z, y, x (transposes): ta -> tb -> ta -> tb
+      // projections z, y, x: ta -> tb -> ta -> tb
       if (D >= 3) {
-        for (int s = lane; s < LS; s += 32) {
-          const int g12 = s % (L1 * L2), j3 = s / (L1 * L2);
-          double v = 0.0;
-#pragma unroll
-          for (int g3 = 0; g3 < L3; ++g3) v = fma(bz[g3 * LD + j3], ta[g3 * L1 * L2 + g12], v);
-          tb[s] = v;
-        }
+        for (int i = lane; i < NL; i += 32) line_bwd(ta, tb, bz, line_base(2, i), L1 * L2);
       } else {
-        for (int s = lane; s < LS; s += 32) tb[s] = ta[s];
+        for (int i = lane; i < LS; i += 32) tb[i] = ta[i];
       }
       __syncwarp();
       if (D >= 2) {
-        for (int s = lane; s < LS; s += 32) {
-          const int g1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
-          double v = 0.0;
-#pragma unroll
-          for (int g2 = 0; g2 < L2; ++g2) v = fma(by[g2 * LD + j2], tb[(j3 * L2 + g2) * L1 + g1], v);
-          ta[s] = v;
-        }
+        for (int i = lane; i < NL; i += 32) line_bwd(tb, ta, by, line_base(1, i), L1);
       } else {
-        for (int s = lane; s < LS; s += 32) ta[s] = tb[s];
+        for (int i = lane; i < LS; i += 32) ta[i] = tb[i];
       }
       __syncwarp();
+      for (int i = lane; i < NL; i += 32) line_bwd(ta, tb, bx, line_base(0, i), 1);
+      __syncwarp();
+      // time projection into the output window
       for (int s = lane; s < LS; s += 32) {
-        const int j1 = s % L1, rest = s / L1;
-        double v = 0.0;
-#pragma unroll
-        for (int g1 = 0; g1 < L1; ++g1) v = fma(bx[g1 * LD + j1], ta[rest * L1 + g1], v);
-        // time projection into the output window
+        const double v = tb[s];
 #pragma unroll
         for (int aa = 0; aa <= PT; ++aa) outw[((et + aa) % PW) * LS + s] += btv[aa] * v;
       }
       __syncwarp();
     }
-    // time function et is complete for this element
     flush_slice(et);
     __syncwarp();
   }

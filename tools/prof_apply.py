@@ -17,11 +17,17 @@ ap.add_argument("--p", type=int, default=3)
 ap.add_argument("--ne", type=int, default=96)
 ap.add_argument("--ne-t", type=int, default=192)
 ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--reaction", action="store_true")
 a = ap.parse_args()
 st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(a.p, a.ne) for _ in range(a.d)], mb.SplineSpace.uniform(a.p, a.ne_t))
 theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
 stab = mb.Stabilization(st, theta, 0.1, 1.0)
-op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, stabilization=stab)
+u = w = None
+if a.reaction:
+    rng = np.random.default_rng(1)
+    u = rng.uniform(0, 1, st.num_dof)
+    w = rng.uniform(0, 0.1, st.num_dof)
+op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, stabilization=stab, u=u, w=w)
 P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1e-3, RM["a"] * RM["c1"], context=op.ctx)
 x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, st.num_dof)).cuda()
 y = torch.empty_like(x)
