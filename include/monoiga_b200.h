@@ -118,6 +118,22 @@ int mi_pc_apply_spatial(mi_ctx* ctx, const double* in, double* out, long long nr
 int mi_pc_apply_time(mi_ctx* ctx, double* y, long long ncols, long long col0);
 
 /* ---------------------------------------------------------------------
+ * Recovery-variable solve ((W_t + b d_e M_t) (x) M_s) w = g  (replaces
+ * solve_w_system + pcg + KroneckerMassPreconditioner, linalg.py:176-203,
+ * 450-547).  Host tables: Kinv (nt x nt) = (W_t + b d_e M_t)^{-1};
+ * M, Minv (d, nmax, nmax): spatial mass factors (incl. box length) and the
+ * preconditioner's inverse univariate masses.  The PCG over time rows is
+ * driven by the caller with the row-batched primitives below.
+ * ------------------------------------------------------------------- */
+int mi_ws_setup(mi_ctx* ctx, const double* Kinv, const double* M, const double* Minv);
+int mi_ws_time(mi_ctx* ctx, const double* in, double* out);
+int mi_ws_mass(mi_ctx* ctx, const double* in, double* out, long long nrows, int inverse);
+int mi_rowdots(mi_ctx* ctx, long long nrows, long long ncols, const double* a, const double* b, double* out);
+int mi_row_axpy(mi_ctx* ctx, long long nrows, long long ncols, const double* alpha, double sign,
+                const double* x, double* y);
+int mi_row_xpby(mi_ctx* ctx, long long nrows, long long ncols, const double* beta, const double* z, double* p);
+
+/* ---------------------------------------------------------------------
  * Krylov primitives (replace the numpy CGS2 / update steps of gmres,
  * linalg.py:404-444).  V is a device matrix of k rows of length n with
  * row stride ldv.  Reductions are deterministic (fixed partition, fixed

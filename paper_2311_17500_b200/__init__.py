@@ -10,7 +10,13 @@ entry points:
 * :func:`gmres` -- same signature, return value and exceptions
   (linalg.py:367-447);
 * :class:`Stabilization` -- Spline Upwind terms from an indicator
-  (stabilization.py:401-489).
+  (stabilization.py:401-489);
+* :class:`RecoverySolver` -- the recovery-variable solve (solve_w_system,
+  linalg.py:502-547) with row-batched device PCG;
+* :func:`fixed_point_solve` with :class:`MonodomainProblem`,
+  :class:`FixedPointConfig`, :class:`SolveResult`, :class:`FixedPointDiverged`
+  (solver.py:58-386) for box geometries; :func:`compute_theta`
+  (stabilization.py:235-339) on the host.
 
 All (d+1)-way tensor work runs in ``lib/libmonoiga_b200.so`` (C ABI in
 ``include/monoiga_b200.h``); there is no CPU fallback.
@@ -18,6 +24,8 @@ All (d+1)-way tensor work runs in ``lib/libmonoiga_b200.so`` (C ABI in
 
 from .errors import (ConsistencyError, DecompositionError, ExtensionError, NonConvergenceError,
                      StabilizationError)
+from .problem import (BoxGeometry, FixedPointConfig, FixedPointDiverged, MonodomainProblem, ResidualIndicator,
+                      SolveResult, compute_theta)
 from .spaces import SpaceTimeSpace, SplineSpace
 
 __version__ = "0.1.0"
@@ -25,7 +33,9 @@ __version__ = "0.1.0"
 __all__ = [
     "SplineSpace", "SpaceTimeSpace", "KroneckerOperator", "FastDiagPreconditioner", "Stabilization",
     "gmres", "DeviceContext", "ConsistencyError", "DecompositionError", "ExtensionError",
-    "NonConvergenceError", "StabilizationError",
+    "NonConvergenceError", "StabilizationError", "BoxGeometry", "FixedPointConfig", "FixedPointDiverged",
+    "MonodomainProblem", "ResidualIndicator", "SolveResult", "compute_theta", "fixed_point_solve",
+    "RecoverySolver",
 ]
 
 
@@ -40,6 +50,12 @@ def __getattr__(name):
     if name == "gmres":
         from .krylov import gmres
         return gmres
+    if name == "fixed_point_solve":
+        from .fixed_point import fixed_point_solve
+        return fixed_point_solve
+    if name == "RecoverySolver":
+        from .wsolve import RecoverySolver
+        return RecoverySolver
     if name == "DeviceContext":
         from .device import DeviceContext
         return DeviceContext

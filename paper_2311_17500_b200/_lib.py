@@ -37,6 +37,12 @@ _SIGS = {
     "mi_pc_apply": ([_vp, _vp, _vp], _c_int),
     "mi_pc_apply_spatial": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),
     "mi_pc_apply_time": ([_vp, _vp, _c_ll, _c_ll], _c_int),
+    "mi_ws_setup": ([_vp, _vp, _vp, _vp], _c_int),
+    "mi_ws_time": ([_vp, _vp, _vp], _c_int),
+    "mi_ws_mass": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),
+    "mi_rowdots": ([_vp, _c_ll, _c_ll, _vp, _vp, _vp], _c_int),
+    "mi_row_axpy": ([_vp, _c_ll, _c_ll, _vp, _c_dbl, _vp, _vp], _c_int),
+    "mi_row_xpby": ([_vp, _c_ll, _c_ll, _vp, _vp, _vp], _c_int),
     "mi_dots": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp], _c_int),
     "mi_sub_combination": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp], _c_int),
     "mi_combination": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp, _vp], _c_int),

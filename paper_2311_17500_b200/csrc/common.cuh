@@ -102,6 +102,12 @@ struct mi_ctx {
   double pen_sigma = 0, pc_cm = 1, pc_react = 0;
   mi::DeviceBuf pc_t1, pc_t2, pc_t3;   // N each
 
+  // ---- recovery-variable solve (w-solve)
+  bool ws_ready = false;
+  mi::DeviceBuf ws_Kinv;        // (W_t + b d_e M_t)^{-1}, nt x nt
+  mi::DeviceBuf ws_M[3], ws_Mi[3], ws_MT0, ws_MiT0;   // spatial mass factors, inverses (+ transposes, dir 1)
+  mi::DeviceBuf ws_t1, ws_t2, ws_t3;
+
   // ---- profiling: per-slot accumulated ms and launch counts
   bool prof_on = false;
   long long launches[8] = {0, 0, 0, 0, 0, 0, 0, 0};

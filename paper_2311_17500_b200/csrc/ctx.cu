@@ -144,7 +144,11 @@ int mi_ctx_destroy(mi_ctx* c) {
                            &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
                            &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->partials};
   for (auto* b : bufs) mi::dfree(*b);
+  mi::DeviceBuf* wbufs[] = {&c->ws_Kinv, &c->ws_MT0, &c->ws_MiT0, &c->ws_t1, &c->ws_t2, &c->ws_t3};
+  for (auto* b : wbufs) mi::dfree(*b);
   for (int l = 0; l < 3; ++l) {
+    mi::dfree(c->ws_M[l]);
+    mi::dfree(c->ws_Mi[l]);
     mi::dfree(c->Us[l]);
     mi::dfree(c->UsT[l]);
     mi::dfree(c->lam[l]);

@@ -28,7 +28,7 @@ constexpr int GA_LD = GT_K + 4;   // 36: conflict-free A fragment reads
 constexpr int GB_LD = GT_N + 4;   // 68: conflict-free B fragment reads
 constexpr int GEMM_SMEM = 2 * (GT_M * GA_LD + GT_K * GB_LD) * 8;
 
-__global__ void __launch_bounds__(256) dgemm_dmma(GemmArgs g) {
+static __global__ void __launch_bounds__(256) dgemm_dmma(GemmArgs g) {
   extern __shared__ double smem[];
   double* As = smem;                              // [2][64][36]
   double* Bs = smem + 2 * GT_M * GA_LD;           // [2][32][68]
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) dgemm_dmma(GemmArgs g) {
 }
 
 // Launch helper: returns cudaError_t of the launch.
-inline cudaError_t launch_dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
+static inline cudaError_t launch_dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dgemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);

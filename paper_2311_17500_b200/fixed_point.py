@@ -1,0 +1,134 @@
+"""Relaxed fixed-point driver on the device (drop-in for the reference's
+``fixed_point_solve``, solver.py:239-386).
+
+Each sweep freezes the Rogers-McCulloch reaction at the previous iterate,
+solves the potential system with the device GMRES + fast-diagonalisation
+preconditioner (the hot path), solves the recovery system with the device
+w-solve, relaxes both, and stops when max |u_new - u| <= tolerance.
+Spline Upwind: the indicator is recomputed (compute_theta, host) and
+relaxed/frozen exactly as solver.py:291-324 does, then factorised and turned
+into device stencil channels.
+"""
+
+import time as _time
+
+import numpy as np
+import torch
+
+from .device import DeviceContext
+from .krylov import gmres
+from .operator import KroneckerOperator, Stabilization
+from .precond import FastDiagPreconditioner
+from .problem import (FixedPointConfig, FixedPointDiverged, GaussGrid, SolveResult, box_of, compute_theta,
+                      load_vector)
+from .wsolve import RecoverySolver
+
+
+class _Workspace:
+    """solver.py:163-211 (box geometry, device objects)."""
+
+    def __init__(self, problem, config, device=0):
+        st = problem.space
+        if config.linear_solver == "direct":
+            raise NotImplementedError("the direct (host LU) linear solver is not part of the device path")
+        self.L, _ = box_of(problem.geometry)
+        self.device = device
+        self.grid = GaussGrid(st, problem.geometry)
+        self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid)
+        self.pc_ctx = DeviceContext(st, device)
+        self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.D,
+                                                    problem.a * problem.c1, lengths=self.L, context=self.pc_ctx)
+        # M_t (x) M_s for g = b (M_t (x) M_s) u  (C_m = D = 0, unit reaction: channel c1 = M_t (x) M_s)
+        self.mass_op = KroneckerOperator(st, problem.final_time, 0.0, 0.0, {"c1": 1.0, "a": 1.0, "c2": 0.0},
+                                         lengths=self.L, device=device)
+        self.wsolver = RecoverySolver(st, problem.final_time, problem.b, problem.d_e, config.linear_tol,
+                                      lengths=self.L, device=device)
+
+    def operator(self, problem, u_k, w_k, stab):
+        return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
+                                 problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
+                                 lengths=self.L, device=self.device)
+
+
+def _indicator_values(ind):
+    return np.asarray(getattr(ind, "values", ind), float)
+
+
+def fixed_point_solve(problem, config=None, device=0):
+    """solver.py:239-386 on the device; returns SolveResult (numpy u, w)."""
+    if config is None:
+        config = FixedPointConfig()
+    st = problem.space
+    t0 = _time.perf_counter()
+
+    frozen_stab = None
+    galerkin_sweeps = 0
+    frozen_indicator = None
+    if config.stabilization == "spline_upwind" and config.indicator_update == "frozen":
+        from dataclasses import replace
+        pre = fixed_point_solve(problem, replace(config, stabilization="off"), device)
+        galerkin_sweeps = pre.iterations
+        if config.indicator_override is not None:
+            frozen_indicator = config.indicator_override(problem, pre.u, pre.w)
+        else:
+            frozen_indicator = compute_theta(problem, pre.u, pre.w)
+        frozen_stab = Stabilization(st, _indicator_values(frozen_indicator), config.lowrank_tol, problem.C_m,
+                                    lengths=box_of(problem.geometry)[0])
+
+    ws = _Workspace(problem, config, device)
+    u = np.zeros(st.num_dof)
+    w = np.zeros(st.num_dof)
+    increments, gmres_iters, pcg_iters = [], [], []
+    indicator = frozen_indicator
+    alpha = config.relaxation
+    freeze_now = False
+
+    for k in range(galerkin_sweeps + 1, galerkin_sweeps + config.max_iterations + 1):
+        stab = None
+        if config.stabilization == "spline_upwind":
+            if frozen_stab is not None:
+                stab = frozen_stab
+            else:
+                if config.indicator_override is not None:
+                    fresh = config.indicator_override(problem, u, w)
+                else:
+                    fresh = compute_theta(problem, u, w, grid=ws.grid)
+                if indicator is not None and alpha < 1.0:
+                    prev = _indicator_values(indicator)
+                    fv = _indicator_values(fresh)
+                    drift = float(np.max(np.abs(fv - prev)))
+                    fresh.values = alpha * fv + (1.0 - alpha) * prev
+                    if (config.indicator_freeze_tol > 0.0 and k > galerkin_sweeps + 1
+                            and drift * alpha <= config.indicator_freeze_tol):
+                        freeze_now = True
+                indicator = fresh
+                stab = Stabilization(st, _indicator_values(indicator), config.lowrank_tol, problem.C_m,
+                                     lengths=ws.L)
+                if freeze_now:
+                    frozen_stab = stab
+        op = ws.operator(problem, u, w, stab)
+        u_tilde, nit, _ = gmres(op, ws.f_vec, precond=ws.precond, tol=config.linear_tol)
+        gmres_iters.append(nit)
+        op.ctx.close()
+
+        if config.evolve_recovery:
+            g_vec = problem.b * ws.mass_op.matvec(u)
+            w_tilde, w_its = ws.wsolver.solve(g_vec)
+            pcg_iters.extend(w_its)
+        else:
+            w_tilde = w
+
+        u_new = alpha * u_tilde + (1.0 - alpha) * u
+        w_new = alpha * w_tilde + (1.0 - alpha) * w
+        inc = float(np.max(np.abs(u_new - u)))
+        increments.append(inc)
+        if config.verbose:
+            print("  sweep %3d: increment %.3e" % (k, inc))
+        u, w = u_new, w_new
+        if inc <= config.tolerance:
+            return SolveResult(u, w, k, increments, True, gmres_iters, pcg_iters,
+                               _time.perf_counter() - t0, indicator)
+    result = SolveResult(u, w, galerkin_sweeps + config.max_iterations, increments, False, gmres_iters,
+                         pcg_iters, _time.perf_counter() - t0, indicator)
+    raise FixedPointDiverged("fixed point did not reach %.2e in %d iterations"
+                             % (config.tolerance, config.max_iterations), result)

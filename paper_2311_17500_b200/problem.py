@@ -1,0 +1,285 @@
+"""Problem description and per-sweep host setup of the fixed-point driver.
+
+Mirrors the reference's ``MonodomainProblem`` / ``FixedPointConfig`` /
+``SolveResult`` / ``FixedPointDiverged`` (solver.py:58-160) and the two
+per-sweep host computations the driver needs on box geometries:
+
+* ``load_vector``: the source load vector of rhs_vectors (assembly.py:350-398);
+* ``compute_theta``: the Spline Upwind residual indicator
+  (stabilization.py:235-339) -- strong residual with the Rogers-McCulloch
+  ionic current at the Gauss points, element maxima, support-extension
+  window maxima, clamped ratio.
+
+Both are host numpy (sum factorised); the (d+1)-way solve they feed runs on
+the device.  Geometry: axis-aligned boxes (the reference's affine maps).
+"""
+
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .spaces import basis_table, gauss_rule, greville
+
+
+class FixedPointDiverged(RuntimeError):
+    """Fixed-point iteration exhausted its budget; carries the last state."""
+
+    def __init__(self, message, result):
+        super().__init__(message)
+        self.result = result
+
+
+class BoxGeometry:
+    """Axis-aligned box prod_l (o_l, o_l + L_l) x (0, T) (geometry.py:217-234)."""
+
+    def __init__(self, lengths, final_time=1.0, offsets=None):
+        self.lengths = np.atleast_1d(np.asarray(lengths, float))
+        self.dim = self.lengths.size
+        self.offsets = np.zeros(self.dim) if offsets is None else np.atleast_1d(np.asarray(offsets, float))
+        if final_time <= 0:
+            raise ValueError("final_time must be positive")
+        self.final_time = float(final_time)
+        self.affine_scales = (self.lengths, self.offsets)
+
+
+def box_of(geometry):
+    """(lengths, offsets) of a box geometry (ours or the reference's GeometryMap)."""
+    aff = getattr(geometry, "affine_scales", None)
+    if aff is None:
+        raise NotImplementedError("mapped (non-affine) geometries are not supported on the device path")
+    L, off = aff
+    return np.asarray(L, float), np.asarray(off, float)
+
+
+@dataclass
+class MonodomainProblem:
+    """solver.py:66-101 (same fields, defaults and validation)."""
+
+    geometry: object
+    space: object
+    source: object = None
+    C_m: float = 1.0
+    D: float = 1e-4
+    a: float = 0.13
+    b: float = 0.013
+    c1: float = 0.26
+    c2: float = 0.1
+    d_e: float = 1.0
+
+    def __post_init__(self):
+        for name in ("C_m", "D", "a", "b", "c1", "c2", "d_e"):
+            if getattr(self, name) < 0:
+                raise ValueError("%s must be nonnegative" % name)
+        if self.geometry.final_time <= 0:
+            raise ValueError("final time must be positive")
+        if self.geometry.dim != len(self.space.spatial):
+            raise ValueError("geometry and space dimensions differ")
+
+    @property
+    def final_time(self):
+        return self.geometry.final_time
+
+    def reaction_constants(self):
+        return {"c1": self.c1, "a": self.a, "c2": self.c2}
+
+
+@dataclass
+class FixedPointConfig:
+    """solver.py:104-137.  ``linear_solver`` "auto" selects the device GMRES
+    (the reference's direct LU for N <= 20000 is host-only and out of scope);
+    "direct" is rejected."""
+
+    relaxation: float = 0.5
+    tolerance: float = 1e-4
+    max_iterations: int = 100
+    stabilization: str = "off"
+    lowrank_tol: float = 0.1
+    indicator_update: str = "every_sweep"
+    indicator_freeze_tol: float = 0.02
+    linear_solver: str = "auto"
+    linear_tol: float = 1e-8
+    evolve_recovery: bool = True
+    indicator_override: object = None
+    verbose: bool = False
+
+    def __post_init__(self):
+        if not 0.0 < self.relaxation <= 1.0:
+            raise ValueError("relaxation must lie in (0, 1]")
+        if self.tolerance <= 0:
+            raise ValueError("tolerance must be positive")
+        if self.stabilization not in ("off", "spline_upwind"):
+            raise ValueError("unknown stabilization %r" % self.stabilization)
+        if self.indicator_update not in ("every_sweep", "frozen"):
+            raise ValueError("unknown indicator update %r" % self.indicator_update)
+        if self.linear_solver not in ("auto", "direct", "iterative"):
+            raise ValueError("unknown linear solver %r" % self.linear_solver)
+
+
+@dataclass
+class SolveResult:
+    """solver.py:140-160."""
+
+    u: np.ndarray
+    w: np.ndarray
+    iterations: int
+    increments: list = field(default_factory=list)
+    converged: bool = True
+    gmres_iterations: list = field(default_factory=list)
+    pcg_iterations: list = field(default_factory=list)
+    wall_time: float = 0.0
+    indicator: object = None
+
+    @property
+    def avg_gmres(self):
+        return float(np.mean(self.gmres_iterations)) if self.gmres_iterations else 0.0
+
+    @property
+    def avg_pcg(self):
+        return float(np.mean(self.pcg_iterations)) if self.pcg_iterations else 0.0
+
+
+class ResidualIndicator:
+    """N_t x N_s indicator values with the Greville grids (stabilization.py:177-193)."""
+
+    def __init__(self, values, time_greville, spatial_grevilles, spatial_shape):
+        self.values = np.asarray(values, float)
+        self.time_greville = np.asarray(time_greville, float)
+        self.spatial_grevilles = [np.asarray(g, float) for g in spatial_grevilles]
+        self.spatial_shape = tuple(spatial_shape)
+
+    @property
+    def max(self):
+        return float(self.values.max(initial=0.0))
+
+
+# --------------------------------------------------------------------------
+# Gauss-grid helpers (default q = p+1 rules on the breakpoints)
+# --------------------------------------------------------------------------
+
+def _mode(A, X, axis):
+    t = np.moveaxis(X, axis, 0)
+    out = (A @ t.reshape(t.shape[0], -1)).reshape((A.shape[0],) + t.shape[1:])
+    return np.moveaxis(out, 0, axis)
+
+
+class GaussGrid:
+    """Default Gauss rules (q = p+1) of every direction with basis tables."""
+
+    def __init__(self, st, geometry):
+        self.st = st
+        self.L, self.off = box_of(geometry)
+        self.T = geometry.final_time
+        self.d = len(st.spatial)
+        self.sx, self.sw, self.sB = [], [], []
+        for s in st.spatial:
+            x, w = gauss_rule(s.breakpoints, s.degree + 1)
+            self.sx.append(x)
+            self.sw.append(w)
+            self.sB.append([basis_table(s, x, o) for o in range(min(2, s.degree) + 1)])
+        tx, tw = gauss_rule(st.time.breakpoints, st.time.degree + 1)
+        self.tx, self.tw = tx, tw
+        self.tB = [basis_table(st.time, tx, o)[:, 1:] for o in range(2)]   # constrained time basis
+
+    def field(self, coeffs, space_orders, time_order):
+        """Values on the grid (Q_t, Q_d, ..., Q_1) of a coefficient vector."""
+        st, d = self.st, self.d
+        U = np.asarray(coeffs, float).reshape(st.coeff_shape)
+        out = _mode(self.tB[time_order], U, 0)
+        for l in range(d):
+            out = _mode(self.sB[l][space_orders[l]], out, 1 + (d - 1 - l))
+        return out
+
+    def physical_points(self):
+        d = self.d
+        mesh = np.meshgrid(*[self.off[l] + self.L[l] * self.sx[l] for l in reversed(range(d))], indexing="ij")
+        return np.stack([mesh[d - 1 - l].ravel() for l in range(d)], axis=-1)
+
+    def source_values(self, source):
+        xq = self.physical_points()
+        qs = xq.shape[0]
+        tq = self.tx * self.T
+        fv = np.empty((tq.size, qs))
+        for i, t in enumerate(tq):
+            fv[i] = np.asarray(source(xq, np.full(qs, t)), float).reshape(qs)
+        return fv.reshape((tq.size,) + tuple(x.size for x in reversed(self.sx)))
+
+
+def load_vector(st, geometry, source, grid=None):
+    """f_vec[i] = int int f B_i (assembly.py:350-398, box geometry)."""
+    if source is None:
+        return np.zeros(st.num_dof)
+    g = grid if grid is not None else GaussGrid(st, geometry)
+    d = g.d
+    ws = np.asarray(g.sw[d - 1] * g.L[d - 1])
+    for l in reversed(range(d - 1)):
+        ws = np.multiply.outer(ws, g.sw[l] * g.L[l])
+    vals = g.source_values(source) * ws[None] * (g.tw * g.T).reshape((-1,) + (1,) * d)
+    out = _mode(g.tB[0].T, vals, 0)
+    for l in range(d):
+        out = _mode(g.sB[l][0].T, out, 1 + (d - 1 - l))
+    return out.ravel()
+
+
+def window_elements(space, i):
+    """bspline.py:270-277."""
+    p = space.degree
+    k = np.asarray(space.knots, float)
+    bp = space.breakpoints
+    lo, hi = k[max(i - p, 0)], k[min(i + p + 1, k.size - 1)]
+    first = max(int(np.searchsorted(bp, lo, side="right")) - 1, 0)
+    last = int(np.searchsorted(bp, hi, side="left")) - 1
+    last = min(max(last, first), bp.size - 2)
+    return first, last + 1
+
+
+def compute_theta(problem, u, w, grid=None):
+    """Residual indicator (stabilization.py:235-339) on a box geometry."""
+    st = problem.space
+    g = grid if grid is not None else GaussGrid(st, problem.geometry)
+    d, T = g.d, g.T
+    zero = [0] * d
+    u_val = g.field(u, zero, 0)
+    u_dtau = g.field(u, zero, 1)
+    w_val = g.field(w, zero, 0)
+    lap = np.zeros_like(u_val)
+    for a in range(d):
+        if st.spatial[a].degree < 2:
+            continue
+        orders = [0] * d
+        orders[a] = 2
+        lap += g.field(u, orders, 0) / g.L[a] ** 2       # affine: metric = diag(1/L^2), no Hessian term
+    res = (problem.C_m * (u_dtau / T) - problem.D * lap
+           + problem.c1 * u_val * (u_val - problem.a) * (u_val - 1.0) + problem.c2 * u_val * w_val)
+    if problem.source is not None:
+        res = res - g.source_values(problem.source)
+    absres = np.abs(res)
+    denom = problem.C_m * (np.max(np.abs(u_val), initial=0.0) / T + np.max(np.abs(u_dtau), initial=0.0) / T)
+    qt = st.time.degree + 1
+    shape = [st.time.breakpoints.size - 1, qt]
+    for l in reversed(range(d)):
+        s = st.spatial[l]
+        shape += [s.breakpoints.size - 1, s.degree + 1]
+    emax = absres.reshape(shape)
+    for ax in reversed(range(1, 2 * (d + 1), 2)):
+        emax = emax.max(axis=ax)
+    # windows: the reference uses full-basis time functions 0..N_t-1 (stabilization.py:307)
+    out = np.stack([emax[a:b].max(axis=0) for a, b in (window_elements(st.time, c) for c in range(st.num_time))])
+    for l in reversed(range(d)):
+        axis = 1 + (d - 1 - l)
+        s = st.spatial[l]
+        moved = np.moveaxis(out, axis, 0)
+        moved = np.stack([moved[a:b].max(axis=0) for a, b in (window_elements(s, i) for i in range(s.dimension))])
+        out = np.moveaxis(moved, 0, axis)
+    numer = out.reshape(st.num_time, st.num_space)
+    if denom > 0.0:
+        theta = np.minimum(numer / denom, 1.0)
+    else:
+        theta = np.zeros_like(numer)
+        hot = numer > 1e-12 * numer.max(initial=0.0)
+        if np.any(hot) and numer.max(initial=0.0) > 0.0:
+            warnings.warn("residual indicator denominator vanished with a nonzero residual; "
+                          "activating the stabilizer fully there", RuntimeWarning, stacklevel=2)
+            theta[hot] = 1.0
+    return ResidualIndicator(theta, greville(st.time)[1:], [greville(s) for s in st.spatial],
+                             tuple(s.dimension for s in reversed(st.spatial)))

@@ -127,7 +127,7 @@ def case(name, d, p, ne, ne_t, T, sigma, seed, su_tol=0.3, theta=None, gm_iters=
     print(name, "N=%d R=%d gmres a/b %d/%d" % (N, lr.rank, out["gm_a_it"], it))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     univariate()
     case("case_2d_p2", 2, 2, (3, 2), 3, 2.0, 1e-3, seed=11)
     case("case_3d_p3", 3, 3, 3, 4, 1.0, 1e-3, seed=12)
@@ -135,3 +135,45 @@ if __name__ == "__main__":
     case("case_1d_p1", 1, 1, 6, 5, 1.0, 1e-2, seed=14)
     case("case_cfg1", 1, 2, 64, 64, 1.0, 1e-3, seed=0, su_tol=0.1, front=True)
     case("case_3d_p2_front", 3, 2, (6, 4, 3), 8, 1.0, (1e-3, 4e-4, 4e-4), seed=15, su_tol=0.1, front=True)
+
+
+def pulse_source(x, t):
+    """Stimulus stand-in (the reference cannot take u0 != 0)."""
+    return 1.0 * (x[:, 0] < 0.1) * (t < 0.05)
+
+
+def fixed_point_cases():
+    from monoiga.solver import fixed_point_solve
+    from monoiga.stabilization import compute_theta
+    out = {}
+    cases = [("fp_1d_off", 1, 2, 12, 12, "off"), ("fp_1d_su", 1, 2, 12, 12, "spline_upwind"),
+             ("fp_2d_su", 2, 2, (6, 5), 8, "spline_upwind")]
+    for name, d, p, ne, ne_t, stab in cases:
+        nes = [ne] * d if np.isscalar(ne) else list(ne)
+        st = SpaceTimeSpace([SplineSpace.uniform(p, n) for n in nes], SplineSpace.uniform(p, ne_t))
+        geo = builtin_geometry({1: "unit_interval", 2: "unit_square"}[d], final_time=1.0)
+        prob = MonodomainProblem(geo, st, source=pulse_source, D=1e-3)
+        cfg = FixedPointConfig(stabilization=stab, linear_solver="iterative")
+        res = fixed_point_solve(prob, cfg)
+        from monoiga.assembly import rhs_vectors
+        fv, _ = rhs_vectors(st, geo, pulse_source, np.zeros(st.num_dof), prob.b)
+        out[name + "_f"] = fv
+        out.update({name + "_u": res.u, name + "_w": res.w, name + "_it": res.iterations,
+                    name + "_inc": np.array(res.increments), name + "_gm": np.array(res.gmres_iterations),
+                    name + "_pcg": np.array(res.pcg_iterations), name + "_d": d, name + "_p": p,
+                    name + "_ne": np.array(nes), name + "_ne_t": ne_t})
+        print(name, "sweeps", res.iterations, "gmres", res.gmres_iterations[:5])
+    # compute_theta at a random state (2D)
+    rng = np.random.default_rng(21)
+    st = SpaceTimeSpace([SplineSpace.uniform(2, 5), SplineSpace.uniform(3, 4)], SplineSpace.uniform(2, 6))
+    geo = builtin_geometry("unit_square", final_time=2.0)
+    prob = MonodomainProblem(geo, st, source=pulse_source, D=1e-2)
+    u = rng.uniform(0, 1, st.num_dof)
+    w = rng.uniform(0, 0.1, st.num_dof)
+    th = compute_theta(prob, u, w)
+    out.update(theta_u=u, theta_w=w, theta_values=th.values)
+    np.savez_compressed(os.path.join(HERE, "fixed_point.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fixed_point":
+    fixed_point_cases()

@@ -1,0 +1,61 @@
+"""Fixed-point driver pieces: host indicator / load vector (CPU) and the full
+device driver vs the reference's fixed_point_solve (GPU)."""
+
+import numpy as np
+import pytest
+
+from cases import load
+
+SWEEPS = ["fp_1d_off", "fp_1d_su", "fp_2d_su"]
+
+
+def pulse_source(x, t):
+    return 1.0 * (x[:, 0] < 0.1) * (t < 0.05)
+
+
+def problem_for(g, name, D=1e-3):
+    import paper_2311_17500_b200.spaces as sp
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem
+    d, p = int(g[name + "_d"]), int(g[name + "_p"])
+    st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(p, int(n)) for n in g[name + "_ne"]],
+                           sp.SplineSpace.uniform(p, int(g[name + "_ne_t"])))
+    return MonodomainProblem(BoxGeometry([1.0] * d, 1.0), st, source=pulse_source, D=D)
+
+
+def test_compute_theta_matches_reference():
+    import paper_2311_17500_b200.spaces as sp
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, compute_theta
+    g = load("fixed_point")
+    st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(2, 5), sp.SplineSpace.uniform(3, 4)], sp.SplineSpace.uniform(2, 6))
+    prob = MonodomainProblem(BoxGeometry([1.0, 1.0], 2.0), st, source=pulse_source, D=1e-2)
+    th = compute_theta(prob, g["theta_u"], g["theta_w"])
+    np.testing.assert_allclose(th.values, g["theta_values"], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("name", SWEEPS)
+def test_load_vector_matches_reference(name):
+    from paper_2311_17500_b200.problem import load_vector
+    g = load("fixed_point")
+    prob = problem_for(g, name)
+    f = load_vector(prob.space, prob.geometry, prob.source)
+    ref = g[name + "_f"]
+    assert np.linalg.norm(f - ref) / np.linalg.norm(ref) < 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SWEEPS)
+def test_fixed_point_solve_matches_reference(name):
+    from paper_2311_17500_b200.fixed_point import fixed_point_solve
+    from paper_2311_17500_b200.problem import FixedPointConfig
+    g = load("fixed_point")
+    prob = problem_for(g, name)
+    stab = "off" if name.endswith("off") else "spline_upwind"
+    res = fixed_point_solve(prob, FixedPointConfig(stabilization=stab, linear_solver="iterative"))
+    assert res.iterations == int(g[name + "_it"])
+    assert res.gmres_iterations == [int(v) for v in g[name + "_gm"]]
+    assert res.pcg_iterations == [int(v) for v in g[name + "_pcg"]]
+    for key in ("u", "w"):
+        ref = g[name + "_" + key]
+        got = getattr(res, key)
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-10, key
+    np.testing.assert_allclose(res.increments, g[name + "_inc"], rtol=1e-8)
