@@ -4,6 +4,7 @@
 // fastest (reference tensorops.py:1-7, bspline.py:311-316).  Spatial
 // directions beyond d have extent 1, so every kernel is written for d = 3.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -76,6 +77,7 @@ struct mi_ctx {
   mi::DeviceBuf wbuf;           // nchan x N  (S_c x per channel), fallback path only
   mi::DeviceBuf frag;           // fragment-major coefficients for the DMMA path
   mi::DeviceBuf xt;             // time-innermost copy of the operator input
+  CUtensorMap tmap_xt;          // TMA descriptor of xt (DMMA path)
   mi::DeviceBuf afr;            // time-filter A fragments (DMMA path)
   int ntau = 0;
   bool op_ready = false;

@@ -14,6 +14,11 @@
 #include "dispatch.cuh"
 #include "stencil_dmma.cuh"
 
+typedef CUresult (*mi_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                       CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                       CUtensorMapFloatOOBfill);
+
 namespace mi {
 
 struct Dims {
@@ -284,6 +289,22 @@ static int dmma_prepare(mi_ctx* c) {
     if ((rc = dalloc(c->frag, (size_t)per_group * ngroups))) return rc;
     const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
     if ((rc = dalloc(c->xt, (size_t)ntp * c->ns))) return rc;
+    {
+      // TMA descriptor of the time-innermost copy: dims (ntp, n1, n2, n3), box (TSTR, H1, H2, H3)
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      MI_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      MI_REQUIRE(fn != nullptr && q == cudaDriverEntryPointSuccess, MI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      cuuint64_t dims[4] = {(cuuint64_t)ntp, (cuuint64_t)c->n[0], (cuuint64_t)c->n[1], (cuuint64_t)c->n[2]};
+      cuuint64_t strides[3] = {(cuuint64_t)ntp * 8, (cuuint64_t)ntp * c->n[0] * 8,
+                               (cuuint64_t)ntp * c->n[0] * c->n[1] * 8};
+      cuuint32_t box[4] = {(cuuint32_t)G::TSTR, (cuuint32_t)G::H1, (cuuint32_t)G::H2, (cuuint32_t)G::H3};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      CUresult r = ((mi_encode_tiled_fn)fn)(&c->tmap_xt, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->xt.p, dims, strides,
+                                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      MI_REQUIRE(r == CUDA_SUCCESS, MI_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    }
     for (int gi = 0; gi < ngroups; ++gi) {
       const int c0 = gi * 8, nc = min(8, c->nchan - c0);
       repack_frag<D_, P_><<<(unsigned)((per_group + 255) / 256), 256, 0, c->stream>>>(
@@ -324,7 +345,7 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
       DmmaArgs a{c->xt.p, c->afr.p + (size_t)gi * c->ntau * 1024, c->ntau, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
                  gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns};
       ProfScope ps(c, PROF_OP_STENCIL);
-      stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a);
+      stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");
     }
   });

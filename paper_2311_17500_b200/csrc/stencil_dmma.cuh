@@ -17,6 +17,7 @@
 #pragma once
 #include "common.cuh"
 #include "ptx.cuh"
+#include <cuda.h>
 
 namespace mi {
 
@@ -49,7 +50,8 @@ struct DmmaSten {
   static constexpr int FK = 8 * 16;                 // filter K: 8 channels x 16 time taps
   static constexpr size_t SMEM = (size_t)2 * HS * TSTR * 8       // X halo [buf][h][t]
                                  + (size_t)2 * 8 * PSTR * 8       // W partials [half][pt][ch*WL + row]
-                                 + (size_t)2 * 2 * 4 * 64 * 8;    // filter partials [buf][mtile][cpair][64]
+                                 + (size_t)2 * 2 * 4 * 64 * 8     // filter partials [buf][mtile][cpair][64]
+                                 + 16;                            // TMA mbarriers
   // halo offset of lane-k 0 of k-step ks (lane kl adds kl)
   static constexpr __host__ __device__ int koff(int ks) {
     return ((D >= 3 ? (ks / QR) / W : 0) * H2 + (D >= 2 ? (ks / QR) % W : 0)) * H1 + 4 * (ks % QR);
@@ -107,12 +109,13 @@ __device__ __forceinline__ void dmma_sweep(const double* X, const double (&breg)
 }
 
 template <int D, int P>
-__global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
+__global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_constant__ CUtensorMap tmap) {
   using G = DmmaSten<D, P>;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   double* Xs = sm;                                   // [2][HS][TSTR]
   double* Wp = Xs + 2 * G::HS * G::TSTR;             // [2 half][8 pt][PSTR]
   double* ys = Wp + 2 * 8 * G::PSTR;                 // [2 buf][2 mtile][4 cpair][64]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ys + 2 * 2 * 4 * 64);   // 2 mbarriers
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pt = warp >> 1, half = warp & 1;
@@ -134,39 +137,20 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
 
   const int W2pt = 2 * a.pt + 1;
   // ---- async loads of chunk t0: halo tile (16 B copies) + band rows of the
-  constexpr int PAIRS = G::TT / 2;
-  // Fast path: one (h1, h2) column of the halo per thread, h3 = q
-  // (THREADS == H1*H2*PAIRS, e.g. d=3 p=3), so a copy is one add + compare.
-  constexpr bool FAST = G::THREADS == G::H1 * G::H2 * PAIRS;
+  // halo tile of chunk t0 by ONE TMA bulk-tensor copy: box (TSTR time rows, H1, H2, H3) of the
+  // time-innermost copy; out-of-range halo coordinates (incl. negative) are zero-filled by TMA
+  constexpr unsigned TILE_BYTES = (unsigned)(G::TSTR * G::HS * 8);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   auto load_chunk = [&](int buf, int t0) {
-    if (t0 >= a.nt) return;
-    double* dst = Xs + buf * G::HS * G::TSTR;
-    if constexpr (FAST) {
-      // recomputed per chunk (cheap) rather than kept live across the sweep
-      const int fpr = tid % PAIRS, fh12 = tid / PAIRS;
-      const int fg1 = o1 - P + fh12 % G::H1;
-      const int fg2 = D >= 2 ? o2 - P + fh12 / G::H1 : 0;
-      const bool fval12 = fg1 >= 0 && fg1 < a.n1 && fg2 >= 0 && fg2 < a.n2;
-      const long long plane = (long long)a.n1 * a.n2 * a.ntp;
-      const double* fsrc0 = a.xt + (((long long)(o3 - P) * a.n2 + fg2) * a.n1 + fg1) * a.ntp + 2 * fpr;
-      double* d0 = dst + fh12 * G::TSTR + 2 * fpr;
-#pragma unroll
-      for (int q = 0; q < G::H3; ++q) {
-        const int g3 = o3 - P + q;
-        const bool v = fval12 && g3 >= 0 && g3 < a.n3;
-        cp_async16(d0 + q * G::H1 * G::H2 * G::TSTR, v ? fsrc0 + q * plane + t0 : a.xt, v);
-      }
-    } else {
-      for (int e = tid; e < G::HS * PAIRS; e += G::THREADS) {
-        const int h = e / PAIRS, pr = e - h * PAIRS;
-        const int h1 = h % G::H1, h2 = (h / G::H1) % G::H2, h3 = h / (G::H1 * G::H2);
-        const int g1 = o1 - P + h1;
-        const int g2 = D >= 2 ? o2 - P + h2 : 0;
-        const int g3 = D >= 3 ? o3 - P + h3 : 0;
-        const bool v = g1 >= 0 && g1 < a.n1 && g2 >= 0 && g2 < a.n2 && g3 >= 0 && g3 < a.n3;
-        const double* src = v ? a.xt + (((long long)g3 * a.n2 + g2) * a.n1 + g1) * a.ntp + t0 + 2 * pr : a.xt;
-        cp_async16(dst + h * G::TSTR + 2 * pr, src, v);
-      }
+    if (tid == 0 && t0 < a.nt) {
+      mbar_expect_tx(&bars[buf], TILE_BYTES);
+      tma_load_4d(Xs + buf * G::HS * G::TSTR, &tmap, &bars[buf], t0, o1 - P, D >= 2 ? o2 - P : 0,
+                  D >= 3 ? o3 - P : 0);
     }
   };
 
@@ -194,17 +178,21 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a) {
   const int nchunks = (a.nt + a.pt + G::TT - 1) / G::TT + 1;   // +1: filter of the last chunk
   (void)W2pt;
   load_chunk(0, 0);
-  cp_async_commit();
   for (int ch = 0; ch < nchunks; ++ch) {
     const int t0 = ch * G::TT;
-    cp_async_wait<0>();
-    __syncthreads();                  // X(ch), bands(ch) visible; W rows of chunk ch-1 complete
+    if (t0 < a.nt) mbar_wait(&bars[ch & 1], (ch >> 1) & 1);   // X(ch) landed (k-th use of buffer -> parity k&1)
+    __syncthreads();                  // other buffer free; W rows of chunk ch-1 complete
     if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
-    cp_async_commit();
     // ---- write y of the filter of chunk ch-2 (partials summed over channel pairs)
+#ifndef MI_EXP_NOFILTER
     if (ch >= 2 && tid >= 256 && tid < 384) write_y(ch & 1, t0 - 2 * G::TT - a.pt);
+#endif
     // ---- time filter of chunk ch-1 on the tensor cores (warps 0..7)
+#ifdef MI_EXP_NOFILTER
+    if (false) {
+#else
     if (ch >= 1 && warp < 8) {
+#endif
       const int tau = 2 * (ch - 1) + fm;                   // M-tile rows tb = 8 tau - pt
       const int tb = 8 * tau - a.pt;
       const double* af = a.afr + ((long long)tau * 32 + 8 * fcq) * 32 + lane;

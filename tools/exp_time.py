@@ -1,0 +1,22 @@
+"""Time the operator apply with an alternative build of the library (ablations)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import sys, os, shutil
+lib = sys.argv[1]
+import paper_2311_17500_b200._lib as L
+L.LIB_PATH = os.path.abspath(lib)
+import numpy as np, torch
+sys.argv = [sys.argv[0]]
+import paper_2311_17500_b200 as mb
+from bench import RM, front_indicator_np
+from paper_2311_17500_b200.spaces import greville
+st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(3, 96) for _ in range(3)], mb.SplineSpace.uniform(3, 192))
+theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
+stab = mb.Stabilization(st, theta, 0.1, 1.0)
+op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, stabilization=stab)
+x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, st.num_dof)).cuda(); y = torch.empty_like(x)
+for _ in range(3): op.apply_device(x, y)
+torch.cuda.synchronize(); e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5): op.apply_device(x, y)
+e1.record(); torch.cuda.synchronize(); print(lib, "apply A ms", e0.elapsed_time(e1) / 5)
