@@ -312,14 +312,7 @@ static int dmma_prepare(mi_ctx* c) {
           c->ns, per_group);
       MI_CHECK_LAUNCH("repack_frag");
     }
-    c->ntau = (c->nt + c->pt + 2 * G::TT) / 8 + 2;
-    if ((rc = dalloc(c->afr, (size_t)ngroups * c->ntau * 1024))) return rc;
-    for (int gi = 0; gi < ngroups; ++gi) {
-      build_filter_frag<<<(c->ntau * 1024 + 255) / 256, 256, 0, c->stream>>>(
-          c->afr.p + (size_t)gi * c->ntau * 1024, c->tband.p, gi * 8, min(8, c->nchan - gi * 8), c->nt, c->pt,
-          c->ntau);
-      MI_CHECK_LAUNCH("build_filter_frag");
-    }
+    if ((rc = dalloc(c->wbuf, (size_t)c->nchan * c->N))) return rc;
     MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)G::SMEM));
   });
@@ -342,11 +335,17 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
       MI_CHECK_LAUNCH("transpose_time_inner");
     }
     for (int gi = 0; gi < ngroups; ++gi) {
-      DmmaArgs a{c->xt.p, c->afr.p + (size_t)gi * c->ntau * 1024, c->ntau, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
+      DmmaArgs a{c->xt.p, c->wbuf.p, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
                  gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns};
       ProfScope ps(c, PROF_OP_STENCIL);
       stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");
+    }
+    {
+      ProfScope ps(c, PROF_OP_TFILTER);
+      dim3 fg((unsigned)((c->ns + 127) / 128), (c->nt + 15) / 16);
+      time_filter_tiled<<<fg, 128, 0, c->stream>>>(c->wbuf.p, c->tband.p, y, c->nchan, c->pt, c->nt, c->ns, 0);
+      MI_CHECK_LAUNCH("time_filter_tiled");
     }
   });
   return MI_OK;

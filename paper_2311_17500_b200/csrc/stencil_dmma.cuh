@@ -44,13 +44,12 @@ struct DmmaSten {
   static constexpr int TSTR = TT + 4;               // smem stride per halo point (= 4 mod 16)
   static constexpr int PTMAX = 4;
   static constexpr int BW = 2 * PTMAX + 1;
-  static constexpr int WL = 2 * TT + 2 * PTMAX;     // circular W buffer length (rows)
+  static constexpr int WL = 2 * TT;                 // W partial rows: this chunk + the previous one
   static constexpr int PSTR = 8 * WL + 4;           // point stride in the W buffer (= 4 mod 16)
   static constexpr int THREADS = 512;
   static constexpr int FK = 8 * 16;                 // filter K: 8 channels x 16 time taps
   static constexpr size_t SMEM = (size_t)2 * HS * TSTR * 8       // X halo [buf][h][t]
                                  + (size_t)2 * 8 * PSTR * 8       // W partials [half][pt][ch*WL + row]
-                                 + (size_t)2 * 2 * 4 * 64 * 8     // filter partials [buf][mtile][cpair][64]
                                  + 16;                            // TMA mbarriers
   // halo offset of lane-k 0 of k-step ks (lane kl adds kl)
   static constexpr __host__ __device__ int koff(int ks) {
@@ -60,8 +59,7 @@ struct DmmaSten {
 
 struct DmmaArgs {
   const double* xt;     // time-innermost copy of x: xt[i * ntp + t]
-  const double* afr;    // time-filter A fragments [tau][32 ks][32 lanes] of this group
-  int ntau;
+  double* wout;         // W_c[t, i] of all channels (nchan, nt, ns): the time filter is a separate kernel
   const double* frag;   // fragment-major coefficients of this channel group
   const double* band;   // time bands (nchan_total, nt, 2pt+1)
   double* y;
@@ -114,8 +112,7 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
   extern __shared__ __align__(128) double sm[];
   double* Xs = sm;                                   // [2][HS][TSTR]
   double* Wp = Xs + 2 * G::HS * G::TSTR;             // [2 half][8 pt][PSTR]
-  double* ys = Wp + 2 * 8 * G::PSTR;                 // [2 buf][2 mtile][4 cpair][64]
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ys + 2 * 2 * 4 * 64);   // 2 mbarriers
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Wp + 2 * 8 * G::PSTR);   // 2 mbarriers
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pt = warp >> 1, half = warp & 1;
@@ -154,20 +151,21 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
     }
   };
 
-  // time filter on the tensor cores: warps 0..7 -> (mtile fm, channel pair fcq)
-  const int fm = warp & 1, fcq = (warp >> 1) & 3;
-  // output write of the previous filter: warps 8..11 (tid 256..383) -> (mtile, row m, point n);
-  // warps 0..7 run the tensor-core filter, so the extra work is spread over 12 warps
-  auto write_y = [&](int ch_buf, int tbase) {
-    const int wt_ = tid - 256;
-    const int om = (wt_ >> 6) & 1, orow = (wt_ >> 3) & 7, opt = wt_ & 7;
-    const int q1 = o1 + opt % G::B1, q2 = o2 + (opt / G::B1) % G::B2, q3 = o3 + opt / (G::B1 * G::B2);
-    const int t = tbase + 8 * om + orow;
-    if (t >= 0 && t < a.nt && q1 < a.n1 && q2 < a.n2 && q3 < a.n3) {
-      const double* yp = ys + (ch_buf * 2 + om) * 4 * 64 + orow * 8 + opt;
-      const double v = (yp[0] + yp[64]) + (yp[128] + yp[192]);
-      double* dst = a.y + (long long)t * a.ns + ((long long)q3 * a.n2 + q2) * a.n1 + q1;
-      if (a.accumulate) *dst += v; else *dst = v;
+  // write-out of W of a finished chunk (both K-halves summed): thread -> (point, channel, row pair)
+  auto write_w = [&](int tc0) {
+    const int q = tid & 7, c = (tid >> 3) & 7, rp = tid >> 6;
+    const int q1 = o1 + q % G::B1, q2 = o2 + (q / G::B1) % G::B2, q3 = o3 + q / (G::B1 * G::B2);
+    if (c >= a.nc || q1 >= a.n1 || q2 >= a.n2 || q3 >= a.n3) return;
+    const long long gi = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
+    const double* w0 = Wp + q * G::PSTR + c * G::WL;
+    const double* w1 = w0 + 8 * G::PSTR;
+#pragma unroll
+    for (int h = 0; h < G::TT / 8; ++h) {
+      const int t = tc0 + rp + 8 * h;
+      if (t < a.nt) {
+        const int r = t % G::WL;
+        a.wout[((long long)(a.c0 + c) * a.nt + t) * a.ns + gi] = w0[r] + w1[r];
+      }
     }
   };
 
@@ -175,47 +173,17 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
   const int kl = lane & 3, mrow = lane >> 2;
   double* wmine = Wp + (half * 8 + pt) * G::PSTR + 2 * kl * G::WL;   // channels 2kl, 2kl+1
 
-  const int nchunks = (a.nt + a.pt + G::TT - 1) / G::TT + 1;   // +1: filter of the last chunk
-  (void)W2pt;
+  const int nchunks = (a.nt + G::TT - 1) / G::TT;
   load_chunk(0, 0);
   for (int ch = 0; ch < nchunks; ++ch) {
     const int t0 = ch * G::TT;
     if (t0 < a.nt) mbar_wait(&bars[ch & 1], (ch >> 1) & 1);   // X(ch) landed (k-th use of buffer -> parity k&1)
     __syncthreads();                  // other buffer free; W rows of chunk ch-1 complete
     if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
-    // ---- write y of the filter of chunk ch-2 (partials summed over channel pairs)
-#ifndef MI_EXP_NOFILTER
-    if (ch >= 2 && tid >= 256 && tid < 384) write_y(ch & 1, t0 - 2 * G::TT - a.pt);
-#endif
-    // ---- time filter of chunk ch-1 on the tensor cores (warps 0..7)
-#ifdef MI_EXP_NOFILTER
-    if (false) {
-#else
-    if (ch >= 1 && warp < 8) {
-#endif
-      const int tau = 2 * (ch - 1) + fm;                   // M-tile rows tb = 8 tau - pt
-      const int tb = 8 * tau - a.pt;
-      const double* af = a.afr + ((long long)tau * 32 + 8 * fcq) * 32 + lane;
-      const int n = lane >> 2;                             // point (B column)
-      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-      const int r0 = (tb - a.pt + 2 * G::PTMAX) % G::WL;  // row of time tb - pt
-#pragma unroll
-      for (int kq = 0; kq < 8; ++kq) {
-        const int k = 4 * (8 * fcq + kq) + kl;             // K index: channel k/16, tap j = k%16
-        const int c = k >> 4, j = k & 15;
-        int r = r0 + j;
-        r = r >= G::WL ? r - G::WL : r;
-        const double* wp = Wp + n * G::PSTR + c * G::WL + r;
-        const double bv = wp[0] + wp[8 * G::PSTR];
-        const double av = __ldg(af + kq * 32);
-        if (kq & 1) dmma(d0, d1, av, bv); else dmma(c0, c1, av, bv);
-      }
-      double* yp = ys + (((ch + 1) & 1) * 2 + fm) * 4 * 64 + fcq * 64;
-      yp[mrow * 8 + 2 * kl] = c0 + d0;
-      yp[mrow * 8 + 2 * kl + 1] = c1 + d1;
-    }
+    // ---- W of chunk ch-1 to HBM (its partials were completed before the barrier)
+    if (ch >= 1) write_w(t0 - G::TT);
     // ---- DMMA sweep of chunk ch into this half's W partial rows
-    if (t0 < a.nt + a.pt) {
+    {
       double acc[G::MT][2];
 #pragma unroll
       for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
@@ -228,15 +196,57 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
       }
 #pragma unroll
       for (int m = 0; m < G::MT; ++m) {
-        const int r = (t0 + m * 8 + mrow + 2 * G::PTMAX) % G::WL;
+        const int r = (t0 + m * 8 + mrow) % G::WL;
         wmine[r] = acc[m][0];
         wmine[G::WL + r] = acc[m][1];
       }
     }
   }
-  // flush the last filter's partials (chunk nchunks-2)
+  // W of the last chunk
   __syncthreads();
-  if (tid >= 256 && tid < 384) write_y(nchunks & 1, nchunks * G::TT - 2 * G::TT - a.pt);
+  write_w((nchunks - 1) * G::TT);
+}
+
+// y[t, i] (+)= sum_c sum_k band_c[t, k] W_c[t - pt + k, i]: block = 128 spatial points x 16
+// time rows; per channel the (16 + 2 pt) x 128 W tile is staged in smem (coalesced rows),
+// each thread accumulates its 16 outputs in registers.  HBM-bound (W read ~once).
+__global__ void __launch_bounds__(128) time_filter_tiled(const double* __restrict__ w, const double* __restrict__ band,
+                                                         double* __restrict__ y, int nchan, int pt, int nt,
+                                                         long long ns, int accumulate) {
+  constexpr int TR = 16, PX = 4;
+  __shared__ double tile[TR + 2 * PX][128];
+  const long long i = blockIdx.x * 128LL + threadIdx.x;
+  const int t0 = blockIdx.y * TR;
+  const int W = 2 * pt + 1;
+  double acc[TR];
+#pragma unroll
+  for (int r = 0; r < TR; ++r) acc[r] = 0.0;
+  for (int c = 0; c < nchan; ++c) {
+    __syncthreads();
+    for (int r = 0; r < TR + 2 * pt; ++r) {
+      const int t = t0 - pt + r;
+      tile[r][threadIdx.x] = (t >= 0 && t < nt && i < ns) ? __ldg(w + ((long long)c * nt + t) * ns + i) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int t = t0 + r;
+      if (t < nt) {
+        const double* bd = band + ((long long)c * nt + t) * W;
+        for (int k = 0; k < W; ++k) acc[r] = fma(__ldg(bd + k), tile[r + k][threadIdx.x], acc[r]);
+      }
+    }
+  }
+  if (i < ns) {
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int t = t0 + r;
+      if (t < nt) {
+        double* dst = y + (long long)t * ns + i;
+        if (accumulate) *dst += acc[r]; else *dst = acc[r];
+      }
+    }
+  }
 }
 
 // Time-filter A fragments: afr[tau][ks][lane] = T_{c0+c}[t, t'] with
