@@ -312,13 +312,39 @@ static int dmma_prepare(mi_ctx* c) {
           c->ns, per_group);
       MI_CHECK_LAUNCH("repack_frag");
     }
-    if ((rc = dalloc(c->wbuf, (size_t)c->nchan * c->N))) return rc;
+    if ((rc = dalloc(c->wbuf, (size_t)c->nchan * c->ns * ntp))) return rc;
+    MI_CUDA(cudaMemsetAsync(c->wbuf.p, 0, sizeof(double) * c->nchan * c->ns * ntp, c->stream));
     MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)G::SMEM));
   });
   MI_CUDA(cudaStreamSynchronize(c->stream));
   c->frag_dirty = false;
   return rc;
+}
+
+// y = sum_c T_c (x) along time of the time-innermost W buffer (HBM-bound)
+static int launch_time_filter(mi_ctx* c, double* y) {
+  MI_REQUIRE(c->nchan <= 64, MI_ERR_ARG, "too many channels for the time filter");
+  dim3 fg((unsigned)((c->ns + 127) / 128), (c->nt + 15) / 16);
+  const int ntp = ((c->nt + 15) / 16) * 16;
+  const size_t fsm = (size_t)c->nchan * 16 * (2 * c->pt + 1) * sizeof(double);
+#define MI_TF(PTV)                                                                                       \
+  case PTV:                                                                                              \
+    if (fsm > 48 * 1024)                                                                                 \
+      MI_CUDA(cudaFuncSetAttribute(time_filter_ti<16, PTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)fsm));                                                           \
+    time_filter_ti<16, PTV><<<fg, 128, fsm, c->stream>>>(c->wbuf.p, c->tband.p, y, c->nchan, c->nt, ntp, \
+                                                         c->ns, 0);                                      \
+    break;
+  switch (c->pt) {
+    MI_TF(1) MI_TF(2) MI_TF(3) MI_TF(4)
+    default:
+      set_error("time degree > 4");
+      return MI_ERR_ARG;
+  }
+#undef MI_TF
+  MI_CHECK_LAUNCH("time_filter_ti");
+  return MI_OK;
 }
 
 static int dmma_apply(mi_ctx* c, const double* x, double* y) {
@@ -343,9 +369,9 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
     }
     {
       ProfScope ps(c, PROF_OP_TFILTER);
-      dim3 fg((unsigned)((c->ns + 127) / 128), (c->nt + 15) / 16);
-      time_filter_tiled<<<fg, 128, 0, c->stream>>>(c->wbuf.p, c->tband.p, y, c->nchan, c->pt, c->nt, c->ns, 0);
-      MI_CHECK_LAUNCH("time_filter_tiled");
+      int frc = launch_time_filter(c, y);
+      if (frc) return frc;
+      MI_CHECK_LAUNCH("time_filter_ti");
     }
   });
   return MI_OK;

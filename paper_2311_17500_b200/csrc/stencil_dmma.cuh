@@ -59,7 +59,7 @@ struct DmmaSten {
 
 struct DmmaArgs {
   const double* xt;     // time-innermost copy of x: xt[i * ntp + t]
-  double* wout;         // W_c[t, i] of all channels (nchan, nt, ns): the time filter is a separate kernel
+  double* wout;         // W_c of all channels, time-innermost (nchan, ns, ntp): the time filter is a separate kernel
   const double* frag;   // fragment-major coefficients of this channel group
   const double* band;   // time bands (nchan_total, nt, 2pt+1)
   double* y;
@@ -151,22 +151,21 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
     }
   };
 
-  // write-out of W of a finished chunk (both K-halves summed): thread -> (point, channel, row pair)
+  // write-out of W of a finished chunk (both K-halves summed) to the time-innermost layout:
+  // thread -> (row pair rp, point q, channel c); 8 consecutive threads write 16 consecutive rows (128 B)
   auto write_w = [&](int tc0) {
-    const int q = tid & 7, c = (tid >> 3) & 7, rp = tid >> 6;
+    const int rp = tid & 7, q = (tid >> 3) & 7, c = tid >> 6;
     const int q1 = o1 + q % G::B1, q2 = o2 + (q / G::B1) % G::B2, q3 = o3 + q / (G::B1 * G::B2);
     if (c >= a.nc || q1 >= a.n1 || q2 >= a.n2 || q3 >= a.n3) return;
     const long long gi = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
     const double* w0 = Wp + q * G::PSTR + c * G::WL;
     const double* w1 = w0 + 8 * G::PSTR;
-#pragma unroll
-    for (int h = 0; h < G::TT / 8; ++h) {
-      const int t = tc0 + rp + 8 * h;
-      if (t < a.nt) {
-        const int r = t % G::WL;
-        a.wout[((long long)(a.c0 + c) * a.nt + t) * a.ns + gi] = w0[r] + w1[r];
-      }
-    }
+    const int t = tc0 + 2 * rp;                      // tc0 is a multiple of TT; ntp a multiple of TT
+    const int r = t % G::WL;
+    double2 v;
+    v.x = w0[r] + w1[r];
+    v.y = w0[r + 1] + w1[r + 1];
+    *reinterpret_cast<double2*>(a.wout + ((long long)(a.c0 + c) * a.ns + gi) * a.ntp + t) = v;
   };
 
   const int base = ((pt / (G::B1 * G::B2)) * G::H2 + (pt / G::B1) % G::B2) * G::H1 + pt % G::B1;
@@ -207,44 +206,57 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
   write_w((nchunks - 1) * G::TT);
 }
 
-// y[t, i] (+)= sum_c sum_k band_c[t, k] W_c[t - pt + k, i]: block = 128 spatial points x 16
-// time rows; per channel the (16 + 2 pt) x 128 W tile is staged in smem (coalesced rows),
-// each thread accumulates its 16 outputs in registers.  HBM-bound (W read ~once).
-__global__ void __launch_bounds__(128) time_filter_tiled(const double* __restrict__ w, const double* __restrict__ band,
-                                                         double* __restrict__ y, int nchan, int pt, int nt,
-                                                         long long ns, int accumulate) {
-  constexpr int TR = 16, PX = 4;
-  __shared__ double tile[TR + 2 * PX][128];
+// y[t, i] (+)= sum_c sum_k band_c[t, k] W_c[t - pt + k, i] with W time-innermost
+// (nchan, ns, ntp): thread = one spatial point x TR time rows; per channel it reads
+// TR + 2 pt contiguous values (16-byte loads), the band rows of the block's TR rows
+// are staged in smem (shared by all points).  Writes y coalesced along i.
+template <int TR, int PT>
+__global__ void __launch_bounds__(128) time_filter_ti(const double* __restrict__ w, const double* __restrict__ band,
+                                                      double* __restrict__ y, int nchan, int nt, int ntp,
+                                                      long long ns, int accumulate) {
+  constexpr int PX = PT + (PT & 1), BWX = 2 * PT + 1;   // PX even: 16-byte aligned pairs
+  constexpr int pt = PT;
+  extern __shared__ double bs[];                     // [nchan][TR][BWX]
   const long long i = blockIdx.x * 128LL + threadIdx.x;
   const int t0 = blockIdx.y * TR;
-  const int W = 2 * pt + 1;
+  constexpr int W = 2 * PT + 1;
+  for (int e = threadIdx.x; e < nchan * TR * W; e += blockDim.x) {
+    const int k = e % W, r = (e / W) % TR, c = e / (W * TR);
+    const int t = t0 + r;
+    bs[(c * TR + r) * BWX + k] = t < nt ? band[((long long)c * nt + t) * W + k] : 0.0;
+  }
+  __syncthreads();
+  if (i >= ns) return;
   double acc[TR];
 #pragma unroll
   for (int r = 0; r < TR; ++r) acc[r] = 0.0;
   for (int c = 0; c < nchan; ++c) {
-    __syncthreads();
-    for (int r = 0; r < TR + 2 * pt; ++r) {
-      const int t = t0 - pt + r;
-      tile[r][threadIdx.x] = (t >= 0 && t < nt && i < ns) ? __ldg(w + ((long long)c * nt + t) * ns + i) : 0.0;
-    }
-    __syncthreads();
+    const double* wc = w + ((long long)c * ns + i) * ntp;
+    double v[TR + 2 * PX];
 #pragma unroll
-    for (int r = 0; r < TR; ++r) {
-      const int t = t0 + r;
-      if (t < nt) {
-        const double* bd = band + ((long long)c * nt + t) * W;
-        for (int k = 0; k < W; ++k) acc[r] = fma(__ldg(bd + k), tile[r + k][threadIdx.x], acc[r]);
+    for (int r = 0; r < TR + 2 * PX; r += 2) {
+      const int t = t0 - PX + r;                     // even: t0, PX even -> 16-byte aligned pairs
+      if (t >= 0 && t + 1 < ntp) {
+        const double2 q = __ldg(reinterpret_cast<const double2*>(wc + t));
+        v[r] = q.x;
+        v[r + 1] = q.y;
+      } else {
+        v[r] = (t >= 0 && t < ntp) ? __ldg(wc + t) : 0.0;
+        v[r + 1] = (t + 1 >= 0 && t + 1 < ntp) ? __ldg(wc + t + 1) : 0.0;
       }
     }
+    const double* bc = bs + c * TR * BWX;
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[r] = fma(bc[r * BWX + k], v[r + PX - PT + k], acc[r]);
   }
-  if (i < ns) {
 #pragma unroll
-    for (int r = 0; r < TR; ++r) {
-      const int t = t0 + r;
-      if (t < nt) {
-        double* dst = y + (long long)t * ns + i;
-        if (accumulate) *dst += acc[r]; else *dst = acc[r];
-      }
+  for (int r = 0; r < TR; ++r) {
+    const int t = t0 + r;
+    if (t < nt) {
+      double* dst = y + (long long)t * ns + i;
+      if (accumulate) *dst += acc[r]; else *dst = acc[r];
     }
   }
 }
