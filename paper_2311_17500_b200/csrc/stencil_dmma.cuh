@@ -25,12 +25,9 @@ template <int D, int P>
 struct DmmaSten {
   static constexpr int W = 2 * P + 1;
   static constexpr int S = D == 3 ? W * W * W : (D == 2 ? W * W : W);
-  // K order: x-offset a1 padded to W1P (multiple of 4) so every k-step covers
-  // 4 consecutive x-offsets of one (a2, a3) row (zero coefficients in the pad)
-  static constexpr int W1P = (W + 3) / 4 * 4;
-  static constexpr int QR = W1P / 4;                // k-steps per stencil row
-  static constexpr int NROW = D == 3 ? W * W : (D == 2 ? W : 1);
-  static constexpr int KS = QR * NROW;              // k-steps per point
+  // K order: the S stencil points in (a3, a2, a1) order, 4 per k-step (unpadded);
+  // a k-step's 4 points span at most one stencil-row boundary (W >= 4 for p >= 2)
+  static constexpr int KS = (S + 3) / 4;            // k-steps per point
   static constexpr int KH = (KS + 1) / 2;           // k-steps per warp (2 warps / point)
   static constexpr int B1 = D == 3 ? 2 : (D == 2 ? 4 : 8);
   static constexpr int B2 = D == 3 ? 2 : (D == 2 ? 2 : 1);
@@ -51,9 +48,18 @@ struct DmmaSten {
   static constexpr size_t SMEM = (size_t)2 * HS * TSTR * 8       // X halo [buf][h][t]
                                  + (size_t)2 * 8 * PSTR * 8       // W partials [half][pt][ch*WL + row]
                                  + 16;                            // TMA mbarriers
-  // halo offset of lane-k 0 of k-step ks (lane kl adds kl)
-  static constexpr __host__ __device__ int koff(int ks) {
-    return ((D >= 3 ? (ks / QR) / W : 0) * H2 + (D >= 2 ? (ks / QR) % W : 0)) * H1 + 4 * (ks % QR);
+  // halo offset of stencil point s (0 beyond S)
+  static constexpr __host__ __device__ int offs(int s) {
+    return s >= S ? 0 : ((D >= 3 ? s / (W * W) : 0) * H2 + (D >= 2 ? (s / W) % W : 0)) * H1 + s % W;
+  }
+  // lane kl of k-step ks reads offs(4 ks) + kl + (kl >= cut(ks) ? jump(ks) : 0)
+  static constexpr __host__ __device__ int cut(int ks) {
+    return (4 * ks + 1 < S && offs(4 * ks + 1) != offs(4 * ks) + 1) ? 1
+         : (4 * ks + 2 < S && offs(4 * ks + 2) != offs(4 * ks) + 2) ? 2
+         : (4 * ks + 3 < S && offs(4 * ks + 3) != offs(4 * ks) + 3) ? 3 : 4;
+  }
+  static constexpr __host__ __device__ int jump(int ks) {
+    return cut(ks) < 4 ? offs(4 * ks + cut(ks)) - offs(4 * ks) - cut(ks) : 0;
   }
 };
 
@@ -93,13 +99,18 @@ __global__ void transpose_time_inner(const double* __restrict__ x, double* __res
 // immediate-offset LDS.64 (lane kl reads x-offset 4q+kl: conflict-free) and
 // two DMMAs; no per-step address arithmetic, no branches.
 template <class G, int HALF>
-__device__ __forceinline__ void dmma_sweep(const double* X, const double (&breg)[G::KH],
+__device__ __forceinline__ void dmma_sweep(const double* X, int kl, const double (&breg)[G::KH],
                                            double (&acc)[G::MT][2]) {
+  const bool ge1 = kl >= 1, ge2 = kl >= 2, ge3 = kl >= 3;
 #pragma unroll
   for (int j = 0; j < G::KH; ++j) {
     const int ks = HALF * G::KH + j;
     if (ks < G::KS) {
-      const double* xa = X + G::koff(ks) * G::TSTR;
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int ct = G::cut(ks);
+      const bool past = ct == 1 ? ge1 : (ct == 2 ? ge2 : (ct == 3 ? ge3 : false));
+      const double* xa = X + (G::offs(4 * ks) + (past ? G::jump(ks) : 0)) * G::TSTR;
 #pragma unroll
       for (int m = 0; m < G::MT; ++m) dmma(acc[m][0], acc[m][1], xa[m * 8], breg[j]);
     }
@@ -189,9 +200,9 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
       if (t0 < a.nt) {
         const double* X = Xs + (ch & 1) * G::HS * G::TSTR + (base + kl) * G::TSTR + mrow;
         if (half == 0)
-          dmma_sweep<G, 0>(X, breg, acc);
+          dmma_sweep<G, 0>(X, kl, breg, acc);
         else
-          dmma_sweep<G, 1>(X, breg, acc);
+          dmma_sweep<G, 1>(X, kl, breg, acc);
       }
 #pragma unroll
       for (int m = 0; m < G::MT; ++m) {
@@ -297,10 +308,9 @@ __global__ void repack_frag(const double* __restrict__ sten, double* __restrict_
   const int i1 = cc1 * G::B1 + pt % G::B1, i2 = cc2 * G::B2 + (pt / G::B1) % G::B2,
             i3 = cc3 * G::B3 + pt / (G::B1 * G::B2);
   const int ch = lane >> 2;
-  const int a1 = 4 * (ks % G::QR) + (lane & 3), row = ks / G::QR;
-  const int s = row * G::W + a1;                   // unpadded stencil index
+  const int s = ks * 4 + (lane & 3);              // stencil index (unpadded K order)
   double v = 0.0;
-  if (ch < nc && a1 < G::W && i1 < n1 && i2 < n2 && i3 < n3) {
+  if (ch < nc && s < G::S && i1 < n1 && i2 < n2 && i3 < n3) {
     const long long i = ((long long)i3 * n2 + i2) * n1 + i1;
     v = sten[((long long)(c0 + ch) * G::S + s) * ns + i];
   }
