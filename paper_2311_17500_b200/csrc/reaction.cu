@@ -222,6 +222,223 @@ __global__ void __launch_bounds__(128, 8) reaction_warp(RxArgs r) {
   for (int ft = r.nel[3]; ft < r.nel[3] + PT; ++ft) flush_slice(ft);
 }
 
+// R3: one block per tile of E x E x E spatial elements (E = 2), sweeping all
+// time elements with sliding windows.  Stages per time Gauss point run over
+// the whole tile (x, y, z interpolation of u, w, x; pointwise C_r * x * W;
+// z, y, x projection; time projection), so neighbouring elements share the
+// interpolation work.  Tiles are coloured by (tile index mod RC) per
+// direction, RC = ceil((E + p) / E): same-colour tiles never share a basis
+// function.  Deterministic, no atomics.
+template <int D, int P, int PT>
+struct RxTile {
+  static constexpr int E = 2;
+  static constexpr int LD = P + 1, Q = P + 1;
+  static constexpr int E1 = E, E2 = D >= 2 ? E : 1, E3 = D >= 3 ? E : 1;
+  static constexpr int L1 = E1 + P, L2 = D >= 2 ? E2 + P : 1, L3 = D >= 3 ? E3 + P : 1;   // local functions
+  static constexpr int Q1 = E1 * Q, Q2 = D >= 2 ? E2 * Q : 1, Q3 = D >= 3 ? E3 * Q : 1;   // Gauss points
+  static constexpr int LS = L1 * L2 * L3, QS = Q1 * Q2 * Q3;
+  static constexpr int PW = PT + 1, QT = PT + 1;
+  static constexpr int RC = (E + P + E - 1) / E;          // colours per direction
+  static constexpr int S1 = Q1 * L2 * L3, S2 = Q1 * Q2 * L3;   // intermediate sizes
+  static constexpr int BIG = QS > S2 ? (QS > S1 ? QS : S1) : (S2 > S1 ? S2 : S1);
+  static constexpr int THREADS = 256;
+  // smem: coefficient window [3][PW][LS], output window [PW][LS], f0 [3][LS],
+  // two work buffers [3][BIG], basis tables [3 dirs][E][Q][LD], weights [3][E*Q]
+  static constexpr size_t SMEM = (size_t)(3 * PW * LS + PW * LS + 3 * LS + 6 * BIG + 3 * E * Q * LD + 3 * E * Q) * 8;
+};
+
+template <int D, int P, int PT>
+__global__ void __launch_bounds__(256) reaction_tile3(RxArgs r) {
+  using G = RxTile<D, P, PT>;
+  constexpr int E = G::E, LD = G::LD, Q = G::Q, PW = G::PW, QT = G::QT;
+  constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2, Q3 = G::Q3;
+  constexpr int LS = G::LS, QS = G::QS, BIG = G::BIG;
+  extern __shared__ double sm[];
+  double* win = sm;                               // [3][PW][LS]
+  double* outw = win + 3 * PW * LS;               // [PW][LS]
+  double* f0 = outw + PW * LS;                    // [3][LS]
+  double* s1 = f0 + 3 * LS;                       // [3][BIG]
+  double* s2 = s1 + 3 * BIG;                      // [3][BIG]
+  double* bt = s2 + 3 * BIG;                      // [3][E][Q][LD]
+  double* wq = bt + 3 * E * Q * LD;               // [3][E*Q]
+  const int tid = threadIdx.x;
+  // tile of this block (colour class)
+  int b = blockIdx.x, k[3], ne[3];
+  for (int l = 0; l < 3; ++l) {
+    const int m = b % r.ncol[l];
+    b /= r.ncol[l];
+    k[l] = l < D ? (m * G::RC + r.color[l]) * E : 0;     // first element of the tile
+    ne[l] = l < D ? min(E, r.nel[l] - k[l]) : 1;
+  }
+  // basis tables / weights of the tile's elements (zero for elements beyond the mesh)
+  for (int i = tid; i < 3 * E * Q * LD; i += G::THREADS) {
+    const int l = i / (E * Q * LD), rem = i % (E * Q * LD), le = rem / (Q * LD);
+    const bool ok = l < D && le < ne[l];
+    bt[i] = ok ? __ldg(r.B[l] + (long long)(k[l] + le) * Q * LD + rem % (Q * LD)) : (l >= D && le == 0 && rem % (Q * LD) == 0 ? 1.0 : 0.0);
+  }
+  for (int i = tid; i < 3 * E * Q; i += G::THREADS) {
+    const int l = i / (E * Q), rem = i % (E * Q), le = rem / Q;
+    wq[i] = (l < D && le < ne[l]) ? __ldg(r.Wq[l] + (long long)(k[l] + le) * Q + rem % Q) : (l >= D ? 1.0 : 0.0);
+  }
+  auto gfun = [&](int s, int& g1, int& g2, int& g3) {
+    const int j1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
+    g1 = k[0] + j1;
+    g2 = k[1] + j2;
+    g3 = k[2] + j3;
+  };
+  auto load_slice = [&](int ft) {
+    const int ct = ft + r.rowoff, slot = ft % PW;
+    const bool vt = ct >= 0 && ct < r.ntc;
+    for (int s = tid; s < LS; s += G::THREADS) {
+      int g1, g2, g3;
+      gfun(s, g1, g2, g3);
+      const bool v = vt && g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
+      const long long gi = (long long)ct * r.ns + ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+      win[(0 * PW + slot) * LS + s] = v ? r.u[gi] : 0.0;
+      win[(1 * PW + slot) * LS + s] = v ? r.w[gi] : 0.0;
+      win[(2 * PW + slot) * LS + s] = v ? r.x[gi] : 0.0;
+      outw[slot * LS + s] = 0.0;
+    }
+  };
+  auto flush_slice = [&](int ft) {
+    const int ct = ft + r.rowoff, slot = ft % PW;
+    if (ct < 0 || ct >= r.ntc) return;
+    for (int s = tid; s < LS; s += G::THREADS) {
+      int g1, g2, g3;
+      gfun(s, g1, g2, g3);
+      if (g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2])
+        r.y[(long long)ct * r.ns + ((long long)g3 * r.n[1] + g2) * r.n[0] + g1] += outw[slot * LS + s];
+    }
+  };
+  const double* bx = bt;
+  const double* by = bt + E * Q * LD;
+  const double* bz = bt + 2 * E * Q * LD;
+  for (int ft = 0; ft < PT; ++ft) load_slice(ft);
+  for (int et = 0; et < r.nel[3]; ++et) {
+    load_slice(et + PT);
+    __syncthreads();
+    for (int g = 0; g < QT; ++g) {
+      const double* btt = r.B[3] + ((long long)et * QT + g) * (PT + 1);
+      const double wt = __ldg(r.Wq[3] + et * QT + g);
+      double btv[PT + 1];
+#pragma unroll
+      for (int aa = 0; aa <= PT; ++aa) btv[aa] = __ldg(btt + aa);
+      // time interpolation -> f0[3][LS]
+      for (int i = tid; i < 3 * LS; i += G::THREADS) {
+        const int fld = i / LS, s = i % LS;
+        double v = 0.0;
+#pragma unroll
+        for (int aa = 0; aa <= PT; ++aa) v = fma(btv[aa], win[(fld * PW + (et + aa) % PW) * LS + s], v);
+        f0[i] = v;
+      }
+      __syncthreads();
+      // x: f0 [3][L3][L2][L1] -> s1 [3][L3][L2][Q1]
+      for (int i = tid; i < 3 * L3 * L2 * Q1; i += G::THREADS) {
+        const int q1 = i % Q1, rest = i / Q1;       // rest = (fld, j3, j2)
+        const int le = q1 / Q, gq = q1 % Q;
+        const double* src = f0 + rest * L1 + le;
+        const double* bb = bx + (le * Q + gq) * LD;
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < LD; ++j) v = fma(bb[j], src[j], v);
+        s1[(rest / (L3 * L2)) * BIG + (rest % (L3 * L2)) * Q1 + q1] = v;
+      }
+      __syncthreads();
+      // y: s1 [3][L3][L2][Q1] -> s2 [3][L3][Q2][Q1]
+      if (D >= 2) {
+        for (int i = tid; i < 3 * L3 * Q2 * Q1; i += G::THREADS) {
+          const int q1 = i % Q1, q2 = (i / Q1) % Q2, j3 = (i / (Q1 * Q2)) % L3, fld = i / (Q1 * Q2 * L3);
+          const int le = q2 / Q, gq = q2 % Q;
+          const double* src = s1 + fld * BIG + (j3 * L2 + le) * Q1 + q1;
+          const double* bb = by + (le * Q + gq) * LD;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < LD; ++j) v = fma(bb[j], src[j * Q1], v);
+          s2[fld * BIG + (j3 * Q2 + q2) * Q1 + q1] = v;
+        }
+      } else {
+        for (int i = tid; i < 3 * BIG; i += G::THREADS) s2[i] = s1[i];
+      }
+      __syncthreads();
+      // z: s2 [3][L3][Q2][Q1] -> s1 [3][Q3][Q2][Q1]
+      if (D >= 3) {
+        for (int i = tid; i < 3 * QS; i += G::THREADS) {
+          const int q12 = i % (Q1 * Q2), q3 = (i / (Q1 * Q2)) % Q3, fld = i / QS;
+          const int le = q3 / Q, gq = q3 % Q;
+          const double* src = s2 + fld * BIG + le * Q2 * Q1 + q12;
+          const double* bb = bz + (le * Q + gq) * LD;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < LD; ++j) v = fma(bb[j], src[j * Q1 * Q2], v);
+          s1[fld * BIG + q3 * Q1 * Q2 + q12] = v;
+        }
+      } else {
+        for (int i = tid; i < 3 * BIG; i += G::THREADS) s1[i] = s2[i];
+      }
+      __syncthreads();
+      // pointwise: C_r(u, w) * x * weights -> s2[0..QS)
+      for (int i = tid; i < QS; i += G::THREADS) {
+        const int q1 = i % Q1, q2 = (i / Q1) % Q2, q3 = i / (Q1 * Q2);
+        const double uu = s1[i], ww = s1[BIG + i], xx = s1[2 * BIG + i];
+        const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
+        s2[i] = cr * xx * (wt * wq[q1] * wq[E * Q + q2] * wq[2 * E * Q + q3]);
+      }
+      __syncthreads();
+      // z projection: s2 [Q3][Q2][Q1] -> s1 [L3][Q2][Q1]
+      if (D >= 3) {
+        for (int i = tid; i < L3 * Q2 * Q1; i += G::THREADS) {
+          const int q12 = i % (Q1 * Q2), j3 = i / (Q1 * Q2);
+          double v = 0.0;
+          for (int le = 0; le < E; ++le) {
+            const int aa = j3 - le;
+            if (aa < 0 || aa > P) continue;
+#pragma unroll
+            for (int gq = 0; gq < Q; ++gq) v = fma(bz[(le * Q + gq) * LD + aa], s2[(le * Q + gq) * Q1 * Q2 + q12], v);
+          }
+          s1[i] = v;
+        }
+      } else {
+        for (int i = tid; i < QS; i += G::THREADS) s1[i] = s2[i];
+      }
+      __syncthreads();
+      // y projection: s1 [L3][Q2][Q1] -> s2 [L3][L2][Q1]
+      if (D >= 2) {
+        for (int i = tid; i < L3 * L2 * Q1; i += G::THREADS) {
+          const int q1 = i % Q1, j2 = (i / Q1) % L2, j3 = i / (Q1 * L2);
+          double v = 0.0;
+          for (int le = 0; le < E; ++le) {
+            const int aa = j2 - le;
+            if (aa < 0 || aa > P) continue;
+#pragma unroll
+            for (int gq = 0; gq < Q; ++gq) v = fma(by[(le * Q + gq) * LD + aa], s1[(j3 * Q2 + le * Q + gq) * Q1 + q1], v);
+          }
+          s2[i] = v;
+        }
+      } else {
+        for (int i = tid; i < L3 * L2 * Q1; i += G::THREADS) s2[i] = s1[i];
+      }
+      __syncthreads();
+      // x projection + time projection into the output window
+      for (int i = tid; i < LS; i += G::THREADS) {
+        const int j1 = i % L1, rest = i / L1;
+        double v = 0.0;
+        for (int le = 0; le < E; ++le) {
+          const int aa = j1 - le;
+          if (aa < 0 || aa > P) continue;
+#pragma unroll
+          for (int gq = 0; gq < Q; ++gq) v = fma(bx[(le * Q + gq) * LD + aa], s2[rest * Q1 + le * Q + gq], v);
+        }
+#pragma unroll
+        for (int aa = 0; aa <= PT; ++aa) outw[((et + aa) % PW) * LS + i] += btv[aa] * v;
+      }
+      __syncthreads();
+    }
+    flush_slice(et);
+    __syncthreads();
+  }
+  for (int ft = r.nel[3]; ft < r.nel[3] + PT; ++ft) flush_slice(ft);
+}
+
 template <int D, int P, int PT>
 static constexpr size_t rx_warp_smem() {
   constexpr int LD = P + 1;
@@ -267,33 +484,35 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   r.c1 = c->c1;
   r.a = c->a;
   r.c2 = c->c2;
-  const int LD = c->p + 1;
-  const int ncolors = LD * (c->d >= 2 ? LD : 1) * (c->d >= 3 ? LD : 1);
   MI_RX_DISPATCH(c->d, c->p, c->pt, {
-    constexpr size_t smem = rx_warp_smem<D_, P_, PT_>() * 4;
+    using G = RxTile<D_, P_, PT_>;
+    constexpr size_t smem = G::SMEM;
     static bool attr = false;
     if (!attr) {
-      MI_CUDA(cudaFuncSetAttribute(reaction_warp<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      MI_CUDA(cudaFuncSetAttribute(reaction_tile3<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       attr = true;
     }
+    const int RC = G::RC;
+    const int ncolors = RC * (c->d >= 2 ? RC : 1) * (c->d >= 3 ? RC : 1);
     for (int col = 0; col < ncolors; ++col) {
       int cc = col;
-      long long nw = 1;
+      long long nb = 1;
       for (int l = 0; l < 3; ++l) {
         if (l < c->d) {
-          r.color[l] = cc % LD;
-          cc /= LD;
-          r.ncol[l] = (c->rx_nel[l] - r.color[l] + LD - 1) / LD;
+          r.color[l] = cc % RC;
+          cc /= RC;
+          const int ntile = (c->rx_nel[l] + G::E - 1) / G::E;
+          r.ncol[l] = (ntile - r.color[l] + RC - 1) / RC;
         } else {
           r.color[l] = 0;
           r.ncol[l] = 1;
         }
-        nw *= r.ncol[l] > 0 ? r.ncol[l] : 0;
+        nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
       }
-      if (nw == 0) continue;
-      reaction_warp<D_, P_, PT_><<<(unsigned)((nw + 3) / 4), 128, smem, c->stream>>>(r);
-      MI_CHECK_LAUNCH("reaction_warp");
+      if (nb == 0) continue;
+      reaction_tile3<D_, P_, PT_><<<(unsigned)nb, G::THREADS, smem, c->stream>>>(r);
+      MI_CHECK_LAUNCH("reaction_tile3");
     }
   });
   return MI_OK;
