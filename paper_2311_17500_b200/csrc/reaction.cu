@@ -14,6 +14,7 @@
 // touch the same output DoF: no atomics, bitwise deterministic.
 #include "common.cuh"
 #include "dispatch.cuh"
+#include "ptx.cuh"
 
 namespace mi {
 
@@ -439,6 +440,271 @@ __global__ void __launch_bounds__(256) reaction_tile3(RxArgs r) {
   for (int ft = r.nel[3]; ft < r.nel[3] + PT; ++ft) flush_slice(ft);
 }
 
+// R4: the R3 tile sweep with every sum-factorisation stage on the FP64
+// tensor cores.  Per direction the tile's 2 elements give a dense
+// (L = 2 + p functions) x (Q = 2 (p+1) Gauss points) basis block; a stage is
+// C[lines, Q] = A[lines, L] B_l[L, Q] (interpolation) or C[lines, L] =
+// A[lines, Q] B_l^T (projection), with M = 8 lines, N = Q or L <= 8, K = L or
+// Q (<= 8, 1-2 k-steps).  The B fragments of all six stage matrices live in
+// registers for the whole sweep; each DMMA needs one shared load.
+template <int D, int P>
+struct RxT4 {
+  static constexpr int E = 2, LD = P + 1, QE = P + 1;
+  static constexpr int L = E + P, Q = E * QE;                    // per present direction
+  static constexpr int L1 = L, L2 = D >= 2 ? L : 1, L3 = D >= 3 ? L : 1;
+  static constexpr int Q1 = Q, Q2 = D >= 2 ? Q : 1, Q3 = D >= 3 ? Q : 1;
+  static constexpr int LS = L1 * L2 * L3, QS = Q1 * Q2 * Q3;
+  static constexpr int KI = (L + 3) / 4, KP = (Q + 3) / 4;      // k-steps interp / proj
+  static constexpr int RC = (E + P + E - 1) / E;
+};
+
+template <int D, int P, int PT>
+__global__ void __launch_bounds__(256) reaction_tile4(RxArgs r) {
+  using G = RxT4<D, P>;
+  constexpr int E = G::E, LD = G::LD, QE = G::QE, L = G::L, Q = G::Q;
+  constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2, Q3 = G::Q3;
+  constexpr int LS = G::LS, QS = G::QS, KI = G::KI, KP = G::KP;
+  constexpr int PW = PT + 1, QT = PT + 1;
+  // stage buffer sizes (3 fields for the interpolation stages)
+  constexpr int SX = 3 * L3 * L2 * Q1, SY = 3 * L3 * Q2 * Q1, SZ = 3 * QS;
+  constexpr int BUF = (SX > SY ? (SX > SZ ? SX : SZ) : (SY > SZ ? SY : SZ));
+  extern __shared__ double sm[];
+  double* win = sm;                               // [3][PW][LS]
+  double* outw = win + 3 * PW * LS;               // [PW][LS]
+  double* f0 = outw + PW * LS;                    // [3][LS]
+  double* sa = f0 + 3 * LS;                       // [BUF]
+  double* sb = sa + BUF;                          // [BUF]
+  double* wq = sb + BUF;                          // [3][Q]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;        // fragment row / col
+  int b = blockIdx.x, k[3], ne[3];
+  for (int l = 0; l < 3; ++l) {
+    const int m = b % r.ncol[l];
+    b /= r.ncol[l];
+    k[l] = l < D ? (m * G::RC + r.color[l]) * E : 0;
+    ne[l] = l < D ? min(E, r.nel[l] - k[l]) : 1;
+  }
+  // basis value of local function j at tile Gauss point q (direction l)
+  auto basis = [&](int l, int j, int q) -> double {
+    if (q >= Q || j >= L) return 0.0;
+    const int le = q / QE, gq = q % QE, aa = j - le;
+    if (le >= ne[l] || aa < 0 || aa > P) return 0.0;
+    return __ldg(r.B[l] + ((long long)(k[l] + le) * QE + gq) * LD + aa);
+  };
+  // B fragments: interpolation (K = j, N = q) and projection (K = q, N = j), per direction
+  double bI[3][2], bP[3][2];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const bool pres = l < D;
+      bI[l][ks] = pres ? basis(l, 4 * ks + fk, fr) : 0.0;
+      bP[l][ks] = pres ? basis(l, fr, 4 * ks + fk) : 0.0;
+    }
+  for (int i = tid; i < 3 * Q; i += 256) {
+    const int l = i / Q, q = i % Q, le = q / QE;
+    wq[i] = (l < D) ? ((le < ne[l]) ? __ldg(r.Wq[l] + (long long)(k[l] + le) * QE + q % QE) : 0.0) : (q == 0 ? 1.0 : 0.0);
+  }
+  auto gidx = [&](int s, bool& ok) -> long long {
+    const int j1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
+    const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
+    ok = g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
+    return ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+  };
+  auto load_slice = [&](int ft) {
+    const int ct = ft + r.rowoff, slot = ft % PW;
+    const bool vt = ct >= 0 && ct < r.ntc;
+    for (int s = tid; s < LS; s += 256) {
+      bool ok;
+      const long long gs = gidx(s, ok);
+      const bool v = vt && ok;
+      const long long gi = (long long)ct * r.ns + gs;
+      win[(0 * PW + slot) * LS + s] = v ? r.u[gi] : 0.0;
+      win[(1 * PW + slot) * LS + s] = v ? r.w[gi] : 0.0;
+      win[(2 * PW + slot) * LS + s] = v ? r.x[gi] : 0.0;
+      outw[slot * LS + s] = 0.0;
+    }
+  };
+  auto flush_slice = [&](int ft) {
+    const int ct = ft + r.rowoff, slot = ft % PW;
+    if (ct < 0 || ct >= r.ntc) return;
+    for (int s = tid; s < LS; s += 256) {
+      bool ok;
+      const long long gs = gidx(s, ok);
+      if (ok) r.y[(long long)ct * r.ns + gs] += outw[slot * LS + s];
+    }
+  };
+  const int nL13 = L3 * L2, lines_x = 3 * nL13, lines_y = 3 * L3 * Q1, lines_z = 3 * Q2 * Q1;
+  for (int ft = 0; ft < PT; ++ft) load_slice(ft);
+  for (int et = 0; et < r.nel[3]; ++et) {
+    load_slice(et + PT);
+    __syncthreads();
+    for (int g = 0; g < QT; ++g) {
+      const double* btt = r.B[3] + ((long long)et * QT + g) * (PT + 1);
+      const double wt = __ldg(r.Wq[3] + et * QT + g);
+      double btv[PT + 1];
+#pragma unroll
+      for (int aa = 0; aa <= PT; ++aa) btv[aa] = __ldg(btt + aa);
+      // time interpolation -> f0[3][LS] (layout [fld][j3][j2][j1])
+      for (int i = tid; i < 3 * LS; i += 256) {
+        const int fld = i / LS, s = i % LS;
+        double v = 0.0;
+#pragma unroll
+        for (int aa = 0; aa <= PT; ++aa) v = fma(btv[aa], win[(fld * PW + (et + aa) % PW) * LS + s], v);
+        f0[i] = v;
+      }
+      __syncthreads();
+      // x interpolation: lines (fld, j3, j2), K = j1, N = q1 -> sa [fld][j3][j2][q1]
+      for (int mt = warp; mt < (lines_x + 7) / 8; mt += 8) {
+        const int line = mt * 8 + fr;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KI; ++ks) {
+          const int j = 4 * ks + fk;
+          const double av = (line < lines_x && j < L1) ? f0[line * L1 + j] : 0.0;
+          dmma(c0, c1, av, bI[0][ks]);
+        }
+        const int lo = mt * 8 + fr, n0 = 2 * fk;
+        if (lo < lines_x) {
+          if (n0 < Q1) sa[lo * Q1 + n0] = c0;
+          if (n0 + 1 < Q1) sa[lo * Q1 + n0 + 1] = c1;
+        }
+      }
+      __syncthreads();
+      // y interpolation: lines (fld, j3, q1), K = j2, N = q2 -> sb [fld][j3][q2][q1]
+      if (D >= 2) {
+        for (int mt = warp; mt < (lines_y + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          const int q1 = line % Q1, fj3 = line / Q1;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KI; ++ks) {
+            const int j = 4 * ks + fk;
+            const double av = (line < lines_y && j < L2) ? sa[(fj3 * L2 + j) * Q1 + q1] : 0.0;
+            dmma(c0, c1, av, bI[1][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < lines_y) {
+            if (n0 < Q2) sb[(fj3 * Q2 + n0) * Q1 + q1] = c0;
+            if (n0 + 1 < Q2) sb[(fj3 * Q2 + n0 + 1) * Q1 + q1] = c1;
+          }
+        }
+        // note: stores are per (line, n) with line = this lane's row
+      } else {
+        for (int i = tid; i < SX; i += 256) sb[i] = sa[i];
+      }
+      __syncthreads();
+      // z interpolation: lines (fld, q2, q1), K = j3, N = q3 -> sa [fld][q3][q2][q1]
+      if (D >= 3) {
+        for (int mt = warp; mt < (lines_z + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          const int q12 = line % (Q1 * Q2), fld = line / (Q1 * Q2);
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KI; ++ks) {
+            const int j = 4 * ks + fk;
+            const double av = (line < lines_z && j < L3) ? sb[(fld * L3 + j) * Q1 * Q2 + q12] : 0.0;
+            dmma(c0, c1, av, bI[2][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < lines_z) {
+            if (n0 < Q3) sa[(fld * Q3 + n0) * Q1 * Q2 + q12] = c0;
+            if (n0 + 1 < Q3) sa[(fld * Q3 + n0 + 1) * Q1 * Q2 + q12] = c1;
+          }
+        }
+      } else {
+        for (int i = tid; i < SY; i += 256) sa[i] = sb[i];
+      }
+      __syncthreads();
+      // pointwise: C_r(u, w) * x * weights -> sb[0..QS)
+      for (int i = tid; i < QS; i += 256) {
+        const int q1 = i % Q1, q2 = (i / Q1) % Q2, q3 = i / (Q1 * Q2);
+        const double uu = sa[i], ww = sa[QS + i], xx = sa[2 * QS + i];
+        const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
+        sb[i] = cr * xx * (wt * wq[q1] * wq[Q + q2] * wq[2 * Q + q3]);
+      }
+      __syncthreads();
+      // z projection: lines (q2, q1), K = q3, N = j3 -> sa [j3][q2][q1]
+      if (D >= 3) {
+        for (int mt = warp; mt < (Q1 * Q2 + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks) {
+            const int q = 4 * ks + fk;
+            const double av = (line < Q1 * Q2 && q < Q3) ? sb[q * Q1 * Q2 + line] : 0.0;
+            dmma(c0, c1, av, bP[2][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < Q1 * Q2) {
+            if (n0 < L3) sa[n0 * Q1 * Q2 + line] = c0;
+            if (n0 + 1 < L3) sa[(n0 + 1) * Q1 * Q2 + line] = c1;
+          }
+        }
+      } else {
+        for (int i = tid; i < QS; i += 256) sa[i] = sb[i];
+      }
+      __syncthreads();
+      // y projection: lines (j3, q1), K = q2, N = j2 -> sb [j3][j2][q1]
+      if (D >= 2) {
+        for (int mt = warp; mt < (L3 * Q1 + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          const int q1 = line % Q1, j3 = line / Q1;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks) {
+            const int q = 4 * ks + fk;
+            const double av = (line < L3 * Q1 && q < Q2) ? sa[(j3 * Q2 + q) * Q1 + q1] : 0.0;
+            dmma(c0, c1, av, bP[1][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < L3 * Q1) {
+            if (n0 < L2) sb[(j3 * L2 + n0) * Q1 + q1] = c0;
+            if (n0 + 1 < L2) sb[(j3 * L2 + n0 + 1) * Q1 + q1] = c1;
+          }
+        }
+      } else {
+        for (int i = tid; i < L3 * Q1; i += 256) sb[i] = sa[i];
+      }
+      __syncthreads();
+      // x projection: lines (j3, j2), K = q1, N = j1 -> f0 [j3][j2][j1]  (then time projection)
+      for (int mt = warp; mt < (L3 * L2 + 7) / 8; mt += 8) {
+        const int line = mt * 8 + fr;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KP; ++ks) {
+          const int q = 4 * ks + fk;
+          const double av = (line < L3 * L2 && q < Q1) ? sb[line * Q1 + q] : 0.0;
+          dmma(c0, c1, av, bP[0][ks]);
+        }
+        const int n0 = 2 * fk;
+        if (line < L3 * L2) {
+          if (n0 < L1) f0[line * L1 + n0] = c0;
+          if (n0 + 1 < L1) f0[line * L1 + n0 + 1] = c1;
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < LS; i += 256) {
+        const double v = f0[i];
+#pragma unroll
+        for (int aa = 0; aa <= PT; ++aa) outw[((et + aa) % PW) * LS + i] += btv[aa] * v;
+      }
+      __syncthreads();
+    }
+    flush_slice(et);
+    __syncthreads();
+  }
+  for (int ft = r.nel[3]; ft < r.nel[3] + PT; ++ft) flush_slice(ft);
+}
+
+template <int D, int P, int PT>
+static constexpr size_t rx4_smem() {
+  using G = RxT4<D, P>;
+  constexpr int SX = 3 * G::L3 * G::L2 * G::Q1, SY = 3 * G::L3 * G::Q2 * G::Q1, SZ = 3 * G::QS;
+  constexpr int BUF = (SX > SY ? (SX > SZ ? SX : SZ) : (SY > SZ ? SY : SZ));
+  return (size_t)(3 * (PT + 1) * G::LS + (PT + 1) * G::LS + 3 * G::LS + 2 * BUF + 3 * G::Q) * 8;
+}
+
 template <int D, int P, int PT>
 static constexpr size_t rx_warp_smem() {
   constexpr int LD = P + 1;
@@ -485,11 +751,11 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   r.a = c->a;
   r.c2 = c->c2;
   MI_RX_DISPATCH(c->d, c->p, c->pt, {
-    using G = RxTile<D_, P_, PT_>;
-    constexpr size_t smem = G::SMEM;
+    using G = RxT4<D_, P_>;
+    constexpr size_t smem = rx4_smem<D_, P_, PT_>();
     static bool attr = false;
     if (!attr) {
-      MI_CUDA(cudaFuncSetAttribute(reaction_tile3<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      MI_CUDA(cudaFuncSetAttribute(reaction_tile4<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       attr = true;
     }
@@ -511,8 +777,8 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
         nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
       }
       if (nb == 0) continue;
-      reaction_tile3<D_, P_, PT_><<<(unsigned)nb, G::THREADS, smem, c->stream>>>(r);
-      MI_CHECK_LAUNCH("reaction_tile3");
+      reaction_tile4<D_, P_, PT_><<<(unsigned)nb, 256, smem, c->stream>>>(r);
+      MI_CHECK_LAUNCH("reaction_tile4");
     }
   });
   return MI_OK;
