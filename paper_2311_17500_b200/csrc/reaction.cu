@@ -447,6 +447,9 @@ __global__ void __launch_bounds__(256) reaction_tile3(RxArgs r) {
 // A[lines, Q] B_l^T (projection), with M = 8 lines, N = Q or L <= 8, K = L or
 // Q (<= 8, 1-2 k-steps).  The B fragments of all six stage matrices live in
 // registers for the whole sweep; each DMMA needs one shared load.
+#ifndef RX4_GB
+#define RX4_GB 1   // time Gauss points per pass (2 halves the barriers but costs occupancy: 653 vs 615 ms at cfg4)
+#endif
 template <int D, int P>
 struct RxT4 {
   static constexpr int E = 2, LD = P + 1, QE = P + 1;
@@ -465,14 +468,16 @@ __global__ void __launch_bounds__(256) reaction_tile4(RxArgs r) {
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2, Q3 = G::Q3;
   constexpr int LS = G::LS, QS = G::QS, KI = G::KI, KP = G::KP;
   constexpr int PW = PT + 1, QT = PT + 1;
-  // stage buffer sizes (3 fields for the interpolation stages)
-  constexpr int SX = 3 * L3 * L2 * Q1, SY = 3 * L3 * Q2 * Q1, SZ = 3 * QS;
+  constexpr int GB = RX4_GB;                        // time Gauss points per pass
+  constexpr int F = 3 * GB;                       // (g, field) pairs per pass
+  // stage buffer sizes
+  constexpr int SX = F * L3 * L2 * Q1, SY = F * L3 * Q2 * Q1, SZ = F * QS;
   constexpr int BUF = (SX > SY ? (SX > SZ ? SX : SZ) : (SY > SZ ? SY : SZ));
   extern __shared__ double sm[];
   double* win = sm;                               // [3][PW][LS]
   double* outw = win + 3 * PW * LS;               // [PW][LS]
-  double* f0 = outw + PW * LS;                    // [3][LS]
-  double* sa = f0 + 3 * LS;                       // [BUF]
+  double* f0 = outw + PW * LS;                    // [GB][3][LS]
+  double* sa = f0 + F * LS;                       // [BUF]
   double* sb = sa + BUF;                          // [BUF]
   double* wq = sb + BUF;                          // [3][Q]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -534,23 +539,20 @@ __global__ void __launch_bounds__(256) reaction_tile4(RxArgs r) {
       if (ok) r.y[(long long)ct * r.ns + gs] += outw[slot * LS + s];
     }
   };
-  const int nL13 = L3 * L2, lines_x = 3 * nL13, lines_y = 3 * L3 * Q1, lines_z = 3 * Q2 * Q1;
+  const int nL13 = L3 * L2, lines_x = F * nL13, lines_y = F * L3 * Q1, lines_z = F * Q2 * Q1;
   for (int ft = 0; ft < PT; ++ft) load_slice(ft);
   for (int et = 0; et < r.nel[3]; ++et) {
     load_slice(et + PT);
     __syncthreads();
-    for (int g = 0; g < QT; ++g) {
-      const double* btt = r.B[3] + ((long long)et * QT + g) * (PT + 1);
-      const double wt = __ldg(r.Wq[3] + et * QT + g);
-      double btv[PT + 1];
-#pragma unroll
-      for (int aa = 0; aa <= PT; ++aa) btv[aa] = __ldg(btt + aa);
-      // time interpolation -> f0[3][LS] (layout [fld][j3][j2][j1])
-      for (int i = tid; i < 3 * LS; i += 256) {
-        const int fld = i / LS, s = i % LS;
+    static_assert(QT % GB == 0, "GB must divide the time Gauss count");
+    for (int g0 = 0; g0 < QT; g0 += GB) {
+      // time interpolation of GB Gauss points -> f0[(gb, fld)][LS] (layout [gb][fld][j3][j2][j1])
+      for (int i = tid; i < F * LS; i += 256) {
+        const int gf = i / LS, s = i % LS, gb = gf / 3, fld = gf % 3;
+        const double* btt = r.B[3] + ((long long)et * QT + g0 + gb) * (PT + 1);
         double v = 0.0;
 #pragma unroll
-        for (int aa = 0; aa <= PT; ++aa) v = fma(btv[aa], win[(fld * PW + (et + aa) % PW) * LS + s], v);
+        for (int aa = 0; aa <= PT; ++aa) v = fma(__ldg(btt + aa), win[(fld * PW + (et + aa) % PW) * LS + s], v);
         f0[i] = v;
       }
       __syncthreads();
@@ -616,78 +618,91 @@ __global__ void __launch_bounds__(256) reaction_tile4(RxArgs r) {
         for (int i = tid; i < SY; i += 256) sa[i] = sb[i];
       }
       __syncthreads();
-      // pointwise: C_r(u, w) * x * weights -> sb[0..QS)
-      for (int i = tid; i < QS; i += 256) {
-        const int q1 = i % Q1, q2 = (i / Q1) % Q2, q3 = i / (Q1 * Q2);
-        const double uu = sa[i], ww = sa[QS + i], xx = sa[2 * QS + i];
+      // pointwise: C_r(u, w) * x * weights -> sb[gb][QS]
+      for (int i = tid; i < GB * QS; i += 256) {
+        const int gb = i / QS, qi = i % QS;
+        const int q1 = qi % Q1, q2 = (qi / Q1) % Q2, q3 = qi / (Q1 * Q2);
+        const double wt = __ldg(r.Wq[3] + et * QT + g0 + gb);
+        const double* src = sa + gb * 3 * QS + qi;
+        const double uu = src[0], ww = src[QS], xx = src[2 * QS];
         const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
         sb[i] = cr * xx * (wt * wq[q1] * wq[Q + q2] * wq[2 * Q + q3]);
       }
       __syncthreads();
-      // z projection: lines (q2, q1), K = q3, N = j3 -> sa [j3][q2][q1]
+      // z projection: lines (gb, q2, q1), K = q3, N = j3 -> sa [gb][j3][q2][q1]
       if (D >= 3) {
-        for (int mt = warp; mt < (Q1 * Q2 + 7) / 8; mt += 8) {
+        constexpr int NL = GB * Q1 * Q2;
+        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
           const int line = mt * 8 + fr;
+          const int gb = line / (Q1 * Q2), q12 = line % (Q1 * Q2);
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KP; ++ks) {
             const int q = 4 * ks + fk;
-            const double av = (line < Q1 * Q2 && q < Q3) ? sb[q * Q1 * Q2 + line] : 0.0;
+            const double av = (line < NL && q < Q3) ? sb[gb * QS + q * Q1 * Q2 + q12] : 0.0;
             dmma(c0, c1, av, bP[2][ks]);
           }
           const int n0 = 2 * fk;
-          if (line < Q1 * Q2) {
-            if (n0 < L3) sa[n0 * Q1 * Q2 + line] = c0;
-            if (n0 + 1 < L3) sa[(n0 + 1) * Q1 * Q2 + line] = c1;
+          if (line < NL) {
+            if (n0 < L3) sa[(gb * L3 + n0) * Q1 * Q2 + q12] = c0;
+            if (n0 + 1 < L3) sa[(gb * L3 + n0 + 1) * Q1 * Q2 + q12] = c1;
           }
         }
       } else {
-        for (int i = tid; i < QS; i += 256) sa[i] = sb[i];
+        for (int i = tid; i < GB * QS; i += 256) sa[i] = sb[i];
       }
       __syncthreads();
-      // y projection: lines (j3, q1), K = q2, N = j2 -> sb [j3][j2][q1]
+      // y projection: lines (gb, j3, q1), K = q2, N = j2 -> sb [gb][j3][j2][q1]
       if (D >= 2) {
-        for (int mt = warp; mt < (L3 * Q1 + 7) / 8; mt += 8) {
+        constexpr int NL = GB * L3 * Q1;
+        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
           const int line = mt * 8 + fr;
-          const int q1 = line % Q1, j3 = line / Q1;
+          const int q1 = line % Q1, gj3 = line / Q1;    // gj3 = gb * L3 + j3
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KP; ++ks) {
             const int q = 4 * ks + fk;
-            const double av = (line < L3 * Q1 && q < Q2) ? sa[(j3 * Q2 + q) * Q1 + q1] : 0.0;
+            const double av = (line < NL && q < Q2) ? sa[(gj3 * Q2 + q) * Q1 + q1] : 0.0;
             dmma(c0, c1, av, bP[1][ks]);
           }
           const int n0 = 2 * fk;
-          if (line < L3 * Q1) {
-            if (n0 < L2) sb[(j3 * L2 + n0) * Q1 + q1] = c0;
-            if (n0 + 1 < L2) sb[(j3 * L2 + n0 + 1) * Q1 + q1] = c1;
+          if (line < NL) {
+            if (n0 < L2) sb[(gj3 * L2 + n0) * Q1 + q1] = c0;
+            if (n0 + 1 < L2) sb[(gj3 * L2 + n0 + 1) * Q1 + q1] = c1;
           }
         }
       } else {
-        for (int i = tid; i < L3 * Q1; i += 256) sb[i] = sa[i];
+        for (int i = tid; i < GB * L3 * Q1; i += 256) sb[i] = sa[i];
       }
       __syncthreads();
-      // x projection: lines (j3, j2), K = q1, N = j1 -> f0 [j3][j2][j1]  (then time projection)
-      for (int mt = warp; mt < (L3 * L2 + 7) / 8; mt += 8) {
-        const int line = mt * 8 + fr;
-        double c0 = 0.0, c1 = 0.0;
+      // x projection: lines (gb, j3, j2), K = q1, N = j1 -> f0 [gb][j3][j2][j1]  (then time projection)
+      {
+        constexpr int NL = GB * L3 * L2;
+        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KP; ++ks) {
-          const int q = 4 * ks + fk;
-          const double av = (line < L3 * L2 && q < Q1) ? sb[line * Q1 + q] : 0.0;
-          dmma(c0, c1, av, bP[0][ks]);
-        }
-        const int n0 = 2 * fk;
-        if (line < L3 * L2) {
-          if (n0 < L1) f0[line * L1 + n0] = c0;
-          if (n0 + 1 < L1) f0[line * L1 + n0 + 1] = c1;
+          for (int ks = 0; ks < KP; ++ks) {
+            const int q = 4 * ks + fk;
+            const double av = (line < NL && q < Q1) ? sb[line * Q1 + q] : 0.0;
+            dmma(c0, c1, av, bP[0][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < NL) {
+            if (n0 < L1) f0[line * L1 + n0] = c0;
+            if (n0 + 1 < L1) f0[line * L1 + n0 + 1] = c1;
+          }
         }
       }
       __syncthreads();
       for (int i = tid; i < LS; i += 256) {
-        const double v = f0[i];
 #pragma unroll
-        for (int aa = 0; aa <= PT; ++aa) outw[((et + aa) % PW) * LS + i] += btv[aa] * v;
+        for (int gb = 0; gb < GB; ++gb) {
+          const double v = f0[gb * LS + i];
+          const double* btt = r.B[3] + ((long long)et * QT + g0 + gb) * (PT + 1);
+#pragma unroll
+          for (int aa = 0; aa <= PT; ++aa) outw[((et + aa) % PW) * LS + i] += __ldg(btt + aa) * v;
+        }
       }
       __syncthreads();
     }
@@ -697,12 +712,333 @@ __global__ void __launch_bounds__(256) reaction_tile4(RxArgs r) {
   for (int ft = r.nel[3]; ft < r.nel[3] + PT; ++ft) flush_slice(ft);
 }
 
+// R5: time-streamed sum factorisation.  The block still owns a 2^d tile of
+// spatial elements and sweeps all time elements, but the spatial stages now
+// run once per TIME FUNCTION instead of once per time Gauss point:
+//   * each time slice entering the window is interpolated to the tile's
+//     spatial Gauss grid (x, y on the tensor cores through shared memory;
+//     the last direction's DMMA accumulators stay in registers, which fixes
+//     the Gauss points every thread owns);
+//   * per time element the thread does the time interpolation, the
+//     Rogers-McCulloch linearisation and the time projection on its own
+//     points in registers (a rotating window of p_t+1 slices, no barriers);
+//   * the slice leaving the window is projected back (last direction from
+//     registers via quad shuffles into the A fragments, then y, x) and added
+//     straight into y.
+// 5 block barriers per time element (R4: 9 per time Gauss point).
+template <int D, int P>
+struct RxT5 : RxT4<D, P> {
+  using B4 = RxT4<D, P>;
+  static constexpr int QL = D == 3 ? B4::Q1 * B4::Q2 : (D == 2 ? B4::Q1 : 1);  // lines of the last stage
+  static constexpr int NT = (QL + 7) / 8;                                          // its M tiles
+  static constexpr int MT = (NT + 7) / 8;                                          // tiles per warp
+  static constexpr int SIN = 3 * B4::LS;
+  static constexpr int SA = D >= 2 ? 3 * B4::L3 * B4::L2 * B4::Q1 : 1;
+  static constexpr int SB = D >= 3 ? 3 * B4::L3 * B4::Q2 * B4::Q1 : 1;
+  static constexpr int SC = D >= 2 ? B4::L * QL : 1;
+  static constexpr int SD = D >= 3 ? B4::L3 * B4::L2 * B4::Q1 : 1;
+  static constexpr int NPRE = (SIN + 255) / 256;
+  static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD) * 8;
+};
+
+template <int D, int P, int PT>
+__global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
+  using G = RxT5<D, P>;
+  constexpr int E = G::E, QE = G::QE, L = G::L, Q = G::Q;
+  constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
+  constexpr int LS = G::LS, KI = G::KI, KP = G::KP, QL = G::QL, NT = G::NT, MT = G::MT;
+  constexpr int PW = PT + 1, QT = PT + 1;
+  extern __shared__ double sm[];
+  double* sIn = sm;                // [fld][j3][j2][j1]
+  double* sA = sIn + G::SIN;       // x-interp out [fld][j3][j2][q1]
+  double* sB = sA + G::SA;         // y-interp out [fld][j3][q2][q1]
+  double* sC = sB + G::SB;         // last-direction projection out [j_last][QL]
+  double* sD = sC + G::SC;         // y-projection out [j3][j2][q1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  int b = blockIdx.x, k[3], ne[3];
+  for (int l = 0; l < 3; ++l) {
+    const int m = b % r.ncol[l];
+    b /= r.ncol[l];
+    k[l] = l < D ? (m * G::RC + r.color[l]) * E : 0;
+    ne[l] = l < D ? min(E, r.nel[l] - k[l]) : 1;
+  }
+  auto basis = [&](int l, int j, int q) -> double {
+    if (l >= D || q >= Q || j >= L) return 0.0;
+    const int le = q / QE, gq = q % QE, aa = j - le;
+    if (le >= ne[l] || aa < 0 || aa > P) return 0.0;
+    return __ldg(r.B[l] + ((long long)(k[l] + le) * QE + gq) * (P + 1) + aa);
+  };
+  auto wgt = [&](int l, int q) -> double {
+    const int le = q / QE;
+    return (q < Q && le < ne[l]) ? __ldg(r.Wq[l] + (long long)(k[l] + le) * QE + q % QE) : 0.0;
+  };
+  double bI[D][KI], bP[D][KP];
+#pragma unroll
+  for (int l = 0; l < D; ++l) {
+#pragma unroll
+    for (int ks = 0; ks < KI; ++ks) bI[l][ks] = basis(l, 4 * ks + fk, fr);
+#pragma unroll
+    for (int ks = 0; ks < KP; ++ks) bP[l][ks] = basis(l, fr, 4 * ks + fk);
+  }
+  // the thread's Gauss points: (line = 8 t + fr, q_last = 2 fk + e), t = warp + 8 mi
+  double wsp[MT][2];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int line = 8 * (warp + 8 * mi) + fr, ql = 2 * fk + e;
+      double v = 0.0;
+      if (line < QL && ql < Q) {
+        v = wgt(D - 1, ql);
+        if (D == 3) v *= wgt(0, line % Q1) * wgt(1, line / Q1);
+        if (D == 2) v *= wgt(0, line);
+      }
+      wsp[mi][e] = v;
+    }
+  // input slice items of this thread: (fld, s) -> global spatial index
+  long long gsp[G::NPRE];
+  int fldp[G::NPRE];
+#pragma unroll
+  for (int m = 0; m < G::NPRE; ++m) {
+    const int i = tid + 256 * m;
+    const int fld = i / LS, s = i % LS;
+    const int j1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
+    const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
+    const bool ok = i < G::SIN && g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
+    gsp[m] = ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+    fldp[m] = ok ? fld : -1;
+  }
+  double pre[G::NPRE];
+  auto prefetch = [&](int ft) {
+    const int ct = ft + r.rowoff;
+    const bool vt = ct >= 0 && ct < r.ntc;
+#pragma unroll
+    for (int m = 0; m < G::NPRE; ++m) {
+      const int f = fldp[m];
+      const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
+      pre[m] = (vt && f >= 0) ? __ldg(src + (long long)ct * r.ns + gsp[m]) : 0.0;
+    }
+  };
+  // global add of one output function value (j3, j2, j1) of time function ft
+  auto gadd = [&](int ft, int j3, int j2, int j1, double v) {
+    const int ct = ft + r.rowoff;
+    const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
+    if (ct >= 0 && ct < r.ntc && j1 < L1 && g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2]) {
+      double* dst = r.y + (long long)ct * r.ns + ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+      *dst += v;
+    }
+  };
+  double X[MT][PW][3][2], Y[MT][PW][2];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int a = 0; a < PW; ++a) {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) X[mi][a][f][0] = X[mi][a][f][1] = 0.0;
+      Y[mi][a][0] = Y[mi][a][1] = 0.0;
+    }
+
+  // project Y[.][0] (time function ft, complete) back to the tile's functions and add into y
+  auto project = [&](int ft) {
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+      const int t = warp + 8 * mi;
+      if (t < NT) {                                  // warp-uniform
+        const int line = 8 * t + fr;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KP; ++ks) {
+          const int c = 4 * ks + fk, src = (lane & ~3) | (c >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, Y[mi][0][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, Y[mi][0][1], src);
+          dmma(c0, c1, (c & 1) ? v1 : v0, bP[D - 1][ks]);
+        }
+        const int n0 = 2 * fk;
+        if (line < QL) {
+          if constexpr (D == 1) {
+            gadd(ft, 0, 0, n0, c0);
+            gadd(ft, 0, 0, n0 + 1, c1);
+          } else {
+            if (n0 < L) sC[n0 * QL + line] = c0;
+            if (n0 + 1 < L) sC[(n0 + 1) * QL + line] = c1;
+          }
+        }
+      }
+    }
+    if constexpr (D >= 2) {
+      __syncthreads();
+      const double* xb = sC;
+      if constexpr (D == 3) {
+        // y projection: lines (j3, q1), K = q2, N = j2 -> sD [j3][j2][q1]
+        constexpr int NL = L3 * Q1;
+        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          const int q1 = line % Q1, j3 = line / Q1;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks) {
+            const int q = 4 * ks + fk;
+            const double av = (line < NL && q < Q2) ? sC[(j3 * Q2 + q) * Q1 + q1] : 0.0;
+            dmma(c0, c1, av, bP[1][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < NL) {
+            if (n0 < L2) sD[(j3 * L2 + n0) * Q1 + q1] = c0;
+            if (n0 + 1 < L2) sD[(j3 * L2 + n0 + 1) * Q1 + q1] = c1;
+          }
+        }
+        __syncthreads();
+        xb = sD;
+      }
+      // x projection: lines (j3, j2), K = q1, N = j1 -> y
+      constexpr int NL = L3 * L2;
+      for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+        const int line = mt * 8 + fr;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KP; ++ks) {
+          const int q = 4 * ks + fk;
+          const double av = (line < NL && q < Q1) ? xb[line * Q1 + q] : 0.0;
+          dmma(c0, c1, av, bP[0][ks]);
+        }
+        if (line < NL) {
+          const int j2 = line % L2, j3 = line / L2;
+          gadd(ft, j3, j2, 2 * fk, c0);
+          gadd(ft, j3, j2, 2 * fk + 1, c1);
+        }
+      }
+    }
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+#pragma unroll
+      for (int a = 0; a < PW - 1; ++a) {
+        Y[mi][a][0] = Y[mi][a + 1][0];
+        Y[mi][a][1] = Y[mi][a + 1][1];
+      }
+      Y[mi][PW - 1][0] = Y[mi][PW - 1][1] = 0.0;
+    }
+  };
+
+  const int nfull = r.nel[3] + PT;                   // full-basis time functions
+  prefetch(0);
+  for (int j = 0; j < nfull; ++j) {
+    if constexpr (D == 1) __syncthreads();           // sIn is read by the last stage directly
+#pragma unroll
+    for (int m = 0; m < G::NPRE; ++m)
+      if (tid + 256 * m < G::SIN) sIn[tid + 256 * m] = pre[m];
+    __syncthreads();
+    if (j + 1 < nfull) prefetch(j + 1);
+    const double* fin = sIn;
+    if constexpr (D >= 2) {
+      // x interpolation: lines (fld, j3, j2), K = j1, N = q1 -> sA [fld][j3][j2][q1]
+      constexpr int NL = 3 * L3 * L2;
+      for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+        const int line = mt * 8 + fr;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KI; ++ks) {
+          const int jj = 4 * ks + fk;
+          const double av = (line < NL && jj < L1) ? sIn[line * L1 + jj] : 0.0;
+          dmma(c0, c1, av, bI[0][ks]);
+        }
+        const int n0 = 2 * fk;
+        if (line < NL) {
+          if (n0 < Q1) sA[line * Q1 + n0] = c0;
+          if (n0 + 1 < Q1) sA[line * Q1 + n0 + 1] = c1;
+        }
+      }
+      __syncthreads();
+      fin = sA;
+    }
+    if constexpr (D == 3) {
+      // y interpolation: lines (fld, j3, q1), K = j2, N = q2 -> sB [fld][j3][q2][q1]
+      constexpr int NL = 3 * L3 * Q1;
+      for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+        const int line = mt * 8 + fr;
+        const int q1 = line % Q1, fj3 = line / Q1;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KI; ++ks) {
+          const int jj = 4 * ks + fk;
+          const double av = (line < NL && jj < L2) ? sA[(fj3 * L2 + jj) * Q1 + q1] : 0.0;
+          dmma(c0, c1, av, bI[1][ks]);
+        }
+        const int n0 = 2 * fk;
+        if (line < NL) {
+          if (n0 < Q2) sB[(fj3 * Q2 + n0) * Q1 + q1] = c0;
+          if (n0 + 1 < Q2) sB[(fj3 * Q2 + n0 + 1) * Q1 + q1] = c1;
+        }
+      }
+      __syncthreads();
+      fin = sB;
+    }
+    // last direction: lines = lower Gauss points, K = j_last, N = q_last -> registers; rotate the window
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+#pragma unroll
+      for (int a = 0; a < PW - 1; ++a)
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          X[mi][a][f][0] = X[mi][a + 1][f][0];
+          X[mi][a][f][1] = X[mi][a + 1][f][1];
+        }
+      const int t = warp + 8 * mi;
+      if (t < NT) {
+        const int line = 8 * t + fr;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KI; ++ks) {
+            const int jj = 4 * ks + fk;
+            const double av = (line < QL && jj < L) ? fin[(f * L + jj) * QL + line] : 0.0;
+            dmma(c0, c1, av, bI[D - 1][ks]);
+          }
+          X[mi][PW - 1][f][0] = c0;
+          X[mi][PW - 1][f][1] = c1;
+        }
+      }
+    }
+    if (j < PT) continue;
+    // time element et = j - PT: window slots 0..PT hold functions et..et+PT
+    const int et = j - PT;
+    const double* btb = r.B[3] + (long long)et * QT * PW;
+#pragma unroll
+    for (int g = 0; g < QT; ++g) {
+      double bt[PW];
+#pragma unroll
+      for (int a = 0; a < PW; ++a) bt[a] = __ldg(btb + g * PW + a);
+      const double wt = __ldg(r.Wq[3] + (long long)et * QT + g);
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double uu = 0.0, ww = 0.0, xx = 0.0;
+#pragma unroll
+          for (int a = 0; a < PW; ++a) {
+            uu = fma(bt[a], X[mi][a][0][e], uu);
+            ww = fma(bt[a], X[mi][a][1][e], ww);
+            xx = fma(bt[a], X[mi][a][2][e], xx);
+          }
+          const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
+          const double v = cr * xx * (wt * wsp[mi][e]);
+#pragma unroll
+          for (int a = 0; a < PW; ++a) Y[mi][a][e] = fma(bt[a], v, Y[mi][a][e]);
+        }
+    }
+    project(et);
+  }
+  for (int ft = r.nel[3]; ft < nfull; ++ft) project(ft);
+}
+
 template <int D, int P, int PT>
 static constexpr size_t rx4_smem() {
   using G = RxT4<D, P>;
-  constexpr int SX = 3 * G::L3 * G::L2 * G::Q1, SY = 3 * G::L3 * G::Q2 * G::Q1, SZ = 3 * G::QS;
+  constexpr int GB = RX4_GB, F = 3 * GB;
+  constexpr int SX = F * G::L3 * G::L2 * G::Q1, SY = F * G::L3 * G::Q2 * G::Q1, SZ = F * G::QS;
   constexpr int BUF = (SX > SY ? (SX > SZ ? SX : SZ) : (SY > SZ ? SY : SZ));
-  return (size_t)(3 * (PT + 1) * G::LS + (PT + 1) * G::LS + 3 * G::LS + 2 * BUF + 3 * G::Q) * 8;
+  return (size_t)(3 * (PT + 1) * G::LS + (PT + 1) * G::LS + F * G::LS + 2 * BUF + 3 * G::Q) * 8;
 }
 
 template <int D, int P, int PT>
@@ -751,11 +1087,11 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   r.a = c->a;
   r.c2 = c->c2;
   MI_RX_DISPATCH(c->d, c->p, c->pt, {
-    using G = RxT4<D_, P_>;
-    constexpr size_t smem = rx4_smem<D_, P_, PT_>();
+    using G = RxT5<D_, P_>;
+    constexpr size_t smem = G::SMEM;
     static bool attr = false;
     if (!attr) {
-      MI_CUDA(cudaFuncSetAttribute(reaction_tile4<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      MI_CUDA(cudaFuncSetAttribute(reaction_tile5<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       attr = true;
     }
@@ -777,8 +1113,8 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
         nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
       }
       if (nb == 0) continue;
-      reaction_tile4<D_, P_, PT_><<<(unsigned)nb, 256, smem, c->stream>>>(r);
-      MI_CHECK_LAUNCH("reaction_tile4");
+      reaction_tile5<D_, P_, PT_><<<(unsigned)nb, 256, smem, c->stream>>>(r);
+      MI_CHECK_LAUNCH("reaction_tile5");
     }
   });
   return MI_OK;
