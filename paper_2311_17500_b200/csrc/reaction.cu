@@ -738,7 +738,7 @@ struct RxT5 : RxT4<D, P> {
   static constexpr int SC = D >= 2 ? B4::L * QL : 1;
   static constexpr int SD = D >= 3 ? B4::L3 * B4::L2 * B4::Q1 : 1;
   static constexpr int NPRE = (SIN + 255) / 256;
-  static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD) * 8;
+  static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD + 64) * 8;
 };
 
 template <int D, int P, int PT>
@@ -748,12 +748,16 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
   constexpr int LS = G::LS, KI = G::KI, KP = G::KP, QL = G::QL, NT = G::NT, MT = G::MT;
   constexpr int PW = PT + 1, QT = PT + 1;
+  constexpr int NBT = QT * PW + QT;                 // time basis + weights of one element
+  constexpr int NLX = L3 * L2;                      // x-projection lines (j3, j2)
+  static_assert(NBT <= 32 && (NLX + 7) / 8 <= 8, "reaction tile too large");
   extern __shared__ double sm[];
   double* sIn = sm;                // [fld][j3][j2][j1]
   double* sA = sIn + G::SIN;       // x-interp out [fld][j3][j2][q1]
   double* sB = sA + G::SA;         // y-interp out [fld][j3][q2][q1]
   double* sC = sB + G::SB;         // last-direction projection out [j_last][QL]
   double* sD = sC + G::SC;         // y-projection out [j3][j2][q1]
+  double* sBt = sD + G::SD;        // [2][32] time tables (double-buffered by iteration parity)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   int b = blockIdx.x, k[3], ne[3];
@@ -796,18 +800,21 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
       }
       wsp[mi][e] = v;
     }
-  // input slice items of this thread: (fld, s) -> global spatial index
+  const long long ns = r.ns;
+  auto spatial = [&](int j3, int j2, int j1, bool& ok) -> long long {
+    const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
+    ok = j1 < L1 && g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
+    return ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+  };
+  // input slice items of this thread: (fld, s) -> global spatial index (-1: padding)
   long long gsp[G::NPRE];
-  int fldp[G::NPRE];
 #pragma unroll
   for (int m = 0; m < G::NPRE; ++m) {
     const int i = tid + 256 * m;
-    const int fld = i / LS, s = i % LS;
-    const int j1 = s % L1, j2 = (s / L1) % L2, j3 = s / (L1 * L2);
-    const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
-    const bool ok = i < G::SIN && g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
-    gsp[m] = ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
-    fldp[m] = ok ? fld : -1;
+    const int s = i % LS;
+    bool ok;
+    const long long gs = spatial(s / (L1 * L2), (s / L1) % L2, s % L1, ok);
+    gsp[m] = (i < G::SIN && ok) ? gs : -1;
   }
   double pre[G::NPRE];
   auto prefetch = [&](int ft) {
@@ -815,20 +822,33 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     const bool vt = ct >= 0 && ct < r.ntc;
 #pragma unroll
     for (int m = 0; m < G::NPRE; ++m) {
-      const int f = fldp[m];
+      const int f = (tid + 256 * m) / LS;
       const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
-      pre[m] = (vt && f >= 0) ? __ldg(src + (long long)ct * r.ns + gsp[m]) : 0.0;
+      pre[m] = (vt && gsp[m] >= 0) ? __ldg(src + (long long)ct * ns + gsp[m]) : 0.0;
     }
   };
-  // global add of one output function value (j3, j2, j1) of time function ft
-  auto gadd = [&](int ft, int j3, int j2, int j1, double v) {
+  double btp = 0.0;
+  auto prefetch_bt = [&](int et) {
+    if (tid < NBT && et >= 0 && et < r.nel[3])
+      btp = tid < QT * PW ? __ldg(r.B[3] + (long long)et * QT * PW + tid)
+                          : __ldg(r.Wq[3] + (long long)et * QT + (tid - QT * PW));
+  };
+  // x-projection outputs of this thread: line 8 warp + fr, j1 = 2 fk + e (old y prefetched a phase early)
+  const int xline = 8 * warp + fr;
+  long long yidx[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    bool ok = false;
+    long long gs = 0;
+    if (xline < NLX) gs = spatial(D >= 2 ? xline / L2 : 0, D >= 2 ? xline % L2 : 0, 2 * fk + e, ok);
+    yidx[e] = ok ? gs : -1;
+  }
+  double yold[2] = {0.0, 0.0};
+  auto yrow = [&](int ft) -> long long {           // row offset of time function ft, -1 if constrained / foreign
     const int ct = ft + r.rowoff;
-    const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
-    if (ct >= 0 && ct < r.ntc && j1 < L1 && g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2]) {
-      double* dst = r.y + (long long)ct * r.ns + ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
-      *dst += v;
-    }
+    return (ct >= 0 && ct < r.ntc) ? (long long)ct * ns : -1;
   };
+
   double X[MT][PW][3][2], Y[MT][PW][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
@@ -839,8 +859,178 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
       Y[mi][a][0] = Y[mi][a][1] = 0.0;
     }
 
-  // project Y[.][0] (time function ft, complete) back to the tile's functions and add into y
-  auto project = [&](int ft) {
+  // x projection of function ft: lines (j3, j2), K = q1, N = j1 -> y (from sC for D = 2, sD for D = 3)
+  auto xproj = [&](int ft, const double* xb) {
+    if (warp < (NLX + 7) / 8) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KP; ++ks) {
+        const int q = 4 * ks + fk;
+        const double av = (xline < NLX && q < Q1) ? xb[xline * Q1 + q] : 0.0;
+        dmma(c0, c1, av, bP[0][ks]);
+      }
+      const long long row = yrow(ft);
+      if (row >= 0) {
+        if (yidx[0] >= 0) r.y[row + yidx[0]] = yold[0] + c0;
+        if (yidx[1] >= 0) r.y[row + yidx[1]] = yold[1] + c1;
+      }
+    }
+  };
+
+  const int nfull = r.nel[3] + PT;                   // full-basis time functions
+  prefetch(0);
+  for (int j = 0; j <= nfull + PT; ++j) {
+    const int et = j - PT;                           // time element (0 <= et < nel_t); z-projection of function et
+    const int fp = j - PT - 1;                       // function whose y / x projections run in this iteration
+    const bool has_in = j < nfull, has_fp = fp >= 0 && fp < nfull;
+    if constexpr (D == 1) __syncthreads();           // sIn is read by the last stage directly
+    if (has_in) {
+#pragma unroll
+      for (int m = 0; m < G::NPRE; ++m)
+        if (tid + 256 * m < G::SIN) sIn[tid + 256 * m] = pre[m];
+    }
+    if (tid < NBT) sBt[(j & 1) * 32 + tid] = btp;
+    if constexpr (D >= 2) {
+      if (has_fp) {
+        const long long row = yrow(fp);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) yold[e] = (row >= 0 && yidx[e] >= 0) ? r.y[row + yidx[e]] : 0.0;
+      }
+    }
+    __syncthreads();                                 // B1
+    if (j + 1 < nfull) prefetch(j + 1);
+    prefetch_bt(et + 1);
+    const double* fin = sIn;
+    if constexpr (D >= 2) {
+      // phase 2: x interpolation of slice j: lines (fld, j3, j2), K = j1, N = q1 -> sA [fld][j3][j2][q1]
+      if (has_in) {
+        constexpr int NL = 3 * L3 * L2;
+        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KI; ++ks) {
+            const int jj = 4 * ks + fk;
+            const double av = (line < NL && jj < L1) ? sIn[line * L1 + jj] : 0.0;
+            dmma(c0, c1, av, bI[0][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < NL) {
+            if (n0 < Q1) sA[line * Q1 + n0] = c0;
+            if (n0 + 1 < Q1) sA[line * Q1 + n0 + 1] = c1;
+          }
+        }
+      }
+      // ... and the y projection of function fp: lines (j3, q1), K = q2, N = j2 -> sD [j3][j2][q1]
+      if (has_fp) {
+        if constexpr (D == 3) {
+          constexpr int NL = L3 * Q1;
+          for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+            const int line = mt * 8 + fr;
+            const int q1 = line % Q1, j3 = line / Q1;
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KP; ++ks) {
+              const int q = 4 * ks + fk;
+              const double av = (line < NL && q < Q2) ? sC[(j3 * Q2 + q) * Q1 + q1] : 0.0;
+              dmma(c0, c1, av, bP[1][ks]);
+            }
+            const int n0 = 2 * fk;
+            if (line < NL) {
+              if (n0 < L2) sD[(j3 * L2 + n0) * Q1 + q1] = c0;
+              if (n0 + 1 < L2) sD[(j3 * L2 + n0 + 1) * Q1 + q1] = c1;
+            }
+          }
+        } else {
+          xproj(fp, sC);
+        }
+      }
+      __syncthreads();                               // B2
+      fin = sA;
+    }
+    if constexpr (D == 3) {
+      // phase 3: y interpolation of slice j: lines (fld, j3, q1), K = j2, N = q2 -> sB [fld][j3][q2][q1]
+      if (has_in) {
+        constexpr int NL = 3 * L3 * Q1;
+        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+          const int line = mt * 8 + fr;
+          const int q1 = line % Q1, fj3 = line / Q1;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KI; ++ks) {
+            const int jj = 4 * ks + fk;
+            const double av = (line < NL && jj < L2) ? sA[(fj3 * L2 + jj) * Q1 + q1] : 0.0;
+            dmma(c0, c1, av, bI[1][ks]);
+          }
+          const int n0 = 2 * fk;
+          if (line < NL) {
+            if (n0 < Q2) sB[(fj3 * Q2 + n0) * Q1 + q1] = c0;
+            if (n0 + 1 < Q2) sB[(fj3 * Q2 + n0 + 1) * Q1 + q1] = c1;
+          }
+        }
+      }
+      // ... and the x projection of function fp (from sD) -> y
+      if (has_fp) xproj(fp, sD);
+      __syncthreads();                               // B3
+      fin = sB;
+    }
+    // phase 4: last-direction interpolation of slice j -> registers (window rotates) ...
+    if (has_in) {
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) {
+#pragma unroll
+        for (int a = 0; a < PW - 1; ++a)
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            X[mi][a][f][0] = X[mi][a + 1][f][0];
+            X[mi][a][f][1] = X[mi][a + 1][f][1];
+          }
+        const int t = warp + 8 * mi;
+        if (t < NT) {
+          const int line = 8 * t + fr;
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KI; ++ks) {
+              const int jj = 4 * ks + fk;
+              const double av = (line < QL && jj < L) ? fin[(f * L + jj) * QL + line] : 0.0;
+              dmma(c0, c1, av, bI[D - 1][ks]);
+            }
+            X[mi][PW - 1][f][0] = c0;
+            X[mi][PW - 1][f][1] = c1;
+          }
+        }
+      }
+    }
+    if (et < 0 || et >= nfull) continue;
+    // ... time element et (window slots 0..PT = functions et..et+PT): interpolate in time, linearise,
+    // project in time, all on the thread's own points ...
+    if (et < r.nel[3]) {
+      const double* bt = sBt + (j & 1) * 32;
+#pragma unroll
+      for (int g = 0; g < QT; ++g) {
+        const double wt = bt[QT * PW + g];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double uu = 0.0, ww = 0.0, xx = 0.0;
+#pragma unroll
+            for (int a = 0; a < PW; ++a) {
+              const double ba = bt[g * PW + a];
+              uu = fma(ba, X[mi][a][0][e], uu);
+              ww = fma(ba, X[mi][a][1][e], ww);
+              xx = fma(ba, X[mi][a][2][e], xx);
+            }
+            const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
+            const double v = cr * xx * (wt * wsp[mi][e]);
+#pragma unroll
+            for (int a = 0; a < PW; ++a) Y[mi][a][e] = fma(bt[g * PW + a], v, Y[mi][a][e]);
+          }
+      }
+    }
+    // ... and the last-direction projection of the completed function et (quad shuffles -> A fragments)
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi) {
       const int t = warp + 8 * mi;
@@ -857,60 +1047,17 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
         const int n0 = 2 * fk;
         if (line < QL) {
           if constexpr (D == 1) {
-            gadd(ft, 0, 0, n0, c0);
-            gadd(ft, 0, 0, n0 + 1, c1);
+            const long long row = yrow(et);
+            if (row >= 0) {
+              if (yidx[0] >= 0) r.y[row + yidx[0]] += c0;
+              if (yidx[1] >= 0) r.y[row + yidx[1]] += c1;
+            }
           } else {
             if (n0 < L) sC[n0 * QL + line] = c0;
             if (n0 + 1 < L) sC[(n0 + 1) * QL + line] = c1;
           }
         }
       }
-    }
-    if constexpr (D >= 2) {
-      __syncthreads();
-      const double* xb = sC;
-      if constexpr (D == 3) {
-        // y projection: lines (j3, q1), K = q2, N = j2 -> sD [j3][j2][q1]
-        constexpr int NL = L3 * Q1;
-        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
-          const int line = mt * 8 + fr;
-          const int q1 = line % Q1, j3 = line / Q1;
-          double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < KP; ++ks) {
-            const int q = 4 * ks + fk;
-            const double av = (line < NL && q < Q2) ? sC[(j3 * Q2 + q) * Q1 + q1] : 0.0;
-            dmma(c0, c1, av, bP[1][ks]);
-          }
-          const int n0 = 2 * fk;
-          if (line < NL) {
-            if (n0 < L2) sD[(j3 * L2 + n0) * Q1 + q1] = c0;
-            if (n0 + 1 < L2) sD[(j3 * L2 + n0 + 1) * Q1 + q1] = c1;
-          }
-        }
-        __syncthreads();
-        xb = sD;
-      }
-      // x projection: lines (j3, j2), K = q1, N = j1 -> y
-      constexpr int NL = L3 * L2;
-      for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
-        const int line = mt * 8 + fr;
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KP; ++ks) {
-          const int q = 4 * ks + fk;
-          const double av = (line < NL && q < Q1) ? xb[line * Q1 + q] : 0.0;
-          dmma(c0, c1, av, bP[0][ks]);
-        }
-        if (line < NL) {
-          const int j2 = line % L2, j3 = line / L2;
-          gadd(ft, j3, j2, 2 * fk, c0);
-          gadd(ft, j3, j2, 2 * fk + 1, c1);
-        }
-      }
-    }
-#pragma unroll
-    for (int mi = 0; mi < MT; ++mi) {
 #pragma unroll
       for (int a = 0; a < PW - 1; ++a) {
         Y[mi][a][0] = Y[mi][a + 1][0];
@@ -918,118 +1065,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
       }
       Y[mi][PW - 1][0] = Y[mi][PW - 1][1] = 0.0;
     }
-  };
-
-  const int nfull = r.nel[3] + PT;                   // full-basis time functions
-  prefetch(0);
-  for (int j = 0; j < nfull; ++j) {
-    if constexpr (D == 1) __syncthreads();           // sIn is read by the last stage directly
-#pragma unroll
-    for (int m = 0; m < G::NPRE; ++m)
-      if (tid + 256 * m < G::SIN) sIn[tid + 256 * m] = pre[m];
-    __syncthreads();
-    if (j + 1 < nfull) prefetch(j + 1);
-    const double* fin = sIn;
-    if constexpr (D >= 2) {
-      // x interpolation: lines (fld, j3, j2), K = j1, N = q1 -> sA [fld][j3][j2][q1]
-      constexpr int NL = 3 * L3 * L2;
-      for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
-        const int line = mt * 8 + fr;
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KI; ++ks) {
-          const int jj = 4 * ks + fk;
-          const double av = (line < NL && jj < L1) ? sIn[line * L1 + jj] : 0.0;
-          dmma(c0, c1, av, bI[0][ks]);
-        }
-        const int n0 = 2 * fk;
-        if (line < NL) {
-          if (n0 < Q1) sA[line * Q1 + n0] = c0;
-          if (n0 + 1 < Q1) sA[line * Q1 + n0 + 1] = c1;
-        }
-      }
-      __syncthreads();
-      fin = sA;
-    }
-    if constexpr (D == 3) {
-      // y interpolation: lines (fld, j3, q1), K = j2, N = q2 -> sB [fld][j3][q2][q1]
-      constexpr int NL = 3 * L3 * Q1;
-      for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
-        const int line = mt * 8 + fr;
-        const int q1 = line % Q1, fj3 = line / Q1;
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KI; ++ks) {
-          const int jj = 4 * ks + fk;
-          const double av = (line < NL && jj < L2) ? sA[(fj3 * L2 + jj) * Q1 + q1] : 0.0;
-          dmma(c0, c1, av, bI[1][ks]);
-        }
-        const int n0 = 2 * fk;
-        if (line < NL) {
-          if (n0 < Q2) sB[(fj3 * Q2 + n0) * Q1 + q1] = c0;
-          if (n0 + 1 < Q2) sB[(fj3 * Q2 + n0 + 1) * Q1 + q1] = c1;
-        }
-      }
-      __syncthreads();
-      fin = sB;
-    }
-    // last direction: lines = lower Gauss points, K = j_last, N = q_last -> registers; rotate the window
-#pragma unroll
-    for (int mi = 0; mi < MT; ++mi) {
-#pragma unroll
-      for (int a = 0; a < PW - 1; ++a)
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          X[mi][a][f][0] = X[mi][a + 1][f][0];
-          X[mi][a][f][1] = X[mi][a + 1][f][1];
-        }
-      const int t = warp + 8 * mi;
-      if (t < NT) {
-        const int line = 8 * t + fr;
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < KI; ++ks) {
-            const int jj = 4 * ks + fk;
-            const double av = (line < QL && jj < L) ? fin[(f * L + jj) * QL + line] : 0.0;
-            dmma(c0, c1, av, bI[D - 1][ks]);
-          }
-          X[mi][PW - 1][f][0] = c0;
-          X[mi][PW - 1][f][1] = c1;
-        }
-      }
-    }
-    if (j < PT) continue;
-    // time element et = j - PT: window slots 0..PT hold functions et..et+PT
-    const int et = j - PT;
-    const double* btb = r.B[3] + (long long)et * QT * PW;
-#pragma unroll
-    for (int g = 0; g < QT; ++g) {
-      double bt[PW];
-#pragma unroll
-      for (int a = 0; a < PW; ++a) bt[a] = __ldg(btb + g * PW + a);
-      const double wt = __ldg(r.Wq[3] + (long long)et * QT + g);
-#pragma unroll
-      for (int mi = 0; mi < MT; ++mi)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double uu = 0.0, ww = 0.0, xx = 0.0;
-#pragma unroll
-          for (int a = 0; a < PW; ++a) {
-            uu = fma(bt[a], X[mi][a][0][e], uu);
-            ww = fma(bt[a], X[mi][a][1][e], ww);
-            xx = fma(bt[a], X[mi][a][2][e], xx);
-          }
-          const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
-          const double v = cr * xx * (wt * wsp[mi][e]);
-#pragma unroll
-          for (int a = 0; a < PW; ++a) Y[mi][a][e] = fma(bt[a], v, Y[mi][a][e]);
-        }
-    }
-    project(et);
   }
-  for (int ft = r.nel[3]; ft < nfull; ++ft) project(ft);
 }
 
 template <int D, int P, int PT>
