@@ -16,7 +16,9 @@ entry points:
 * :func:`fixed_point_solve` with :class:`MonodomainProblem`,
   :class:`FixedPointConfig`, :class:`SolveResult`, :class:`FixedPointDiverged`
   (solver.py:58-386) for box geometries; :func:`compute_theta`
-  (stabilization.py:235-339) on the host.
+  (stabilization.py:235-339) on the host;
+* :class:`ApplyStream` -- pipelined P^{-1} A over a queue of host vectors
+  (copy-in / apply / copy-out overlapped on three CUDA streams).
 
 All (d+1)-way tensor work runs in ``lib/libmonoiga_b200.so`` (C ABI in
 ``include/monoiga_b200.h``); there is no CPU fallback.
@@ -35,7 +37,7 @@ __all__ = [
     "gmres", "DeviceContext", "ConsistencyError", "DecompositionError", "ExtensionError",
     "NonConvergenceError", "StabilizationError", "BoxGeometry", "FixedPointConfig", "FixedPointDiverged",
     "MonodomainProblem", "ResidualIndicator", "SolveResult", "compute_theta", "fixed_point_solve",
-    "RecoverySolver",
+    "RecoverySolver", "ApplyStream",
 ]
 
 
@@ -56,6 +58,9 @@ def __getattr__(name):
     if name == "RecoverySolver":
         from .wsolve import RecoverySolver
         return RecoverySolver
+    if name == "ApplyStream":
+        from .stream import ApplyStream
+        return ApplyStream
     if name == "DeviceContext":
         from .device import DeviceContext
         return DeviceContext

@@ -16,6 +16,12 @@
 #include "dispatch.cuh"
 #include "ptx.cuh"
 
+#include <type_traits>
+
+#ifndef RX_UNROLL
+#define RX_UNROLL 0   // unroll the slice loop by p_t+1 (no window rotation; more registers / code)
+#endif
+
 namespace mi {
 
 struct RxArgs {
@@ -35,6 +41,9 @@ struct RxArgs {
   int rowoff;          // row of full time function ft is ft + rowoff (-1 unsharded)
   long long ns;
   double c1, a, c2;
+#ifdef RX_ABL_CBT
+  double btc[32];
+#endif
 };
 
 // One warp per spatial element (colour class: elements p+1 apart never
@@ -732,13 +741,15 @@ struct RxT5 : RxT4<D, P> {
   static constexpr int QL = D == 3 ? B4::Q1 * B4::Q2 : (D == 2 ? B4::Q1 : 1);  // lines of the last stage
   static constexpr int NT = (QL + 7) / 8;                                          // its M tiles
   static constexpr int MT = (NT + 7) / 8;                                          // tiles per warp
-  static constexpr int SIN = 3 * B4::LS;
-  static constexpr int SA = D >= 2 ? 3 * B4::L3 * B4::L2 * B4::Q1 : 1;
-  static constexpr int SB = D >= 3 ? 3 * B4::L3 * B4::Q2 * B4::Q1 : 1;
-  static constexpr int SC = D >= 2 ? B4::L * QL : 1;
-  static constexpr int SD = D >= 3 ? B4::L3 * B4::L2 * B4::Q1 : 1;
-  static constexpr int NPRE = (SIN + 255) / 256;
-  static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD + 64) * 8;
+  static constexpr int ev(int n) { return (n + 1) & ~1; }                        // 16-byte aligned buffers
+  static constexpr int SIN = ev(3 * B4::LS);
+  static constexpr int SA = D >= 2 ? ev(3 * B4::L3 * B4::L2 * B4::Q1) : 2;
+  static constexpr int SB = D >= 3 ? ev(3 * B4::L3 * B4::Q2 * B4::Q1) : 2;
+  static constexpr int SC = D >= 2 ? ev(B4::L * QL) : 2;
+  static constexpr int SD = D >= 3 ? ev(B4::L3 * B4::L2 * B4::Q1) : 2;
+  static constexpr int NIN = 3 * B4::LS;                                          // input items per slice
+  static constexpr int NPRE = (NIN + 255) / 256;
+  static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD + 64 + 256) * 8;   // + time tables + read pad
 };
 
 template <int D, int P, int PT>
@@ -748,9 +759,10 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
   constexpr int LS = G::LS, KI = G::KI, KP = G::KP, QL = G::QL, NT = G::NT, MT = G::MT;
   constexpr int PW = PT + 1, QT = PT + 1;
-  constexpr int NBT = QT * PW + QT;                 // time basis + weights of one element
+  constexpr int NBT = 2 * QT * PW;                  // time basis (interpolation) + weighted (projection)
   constexpr int NLX = L3 * L2;                      // x-projection lines (j3, j2)
   static_assert(NBT <= 32 && (NLX + 7) / 8 <= 8, "reaction tile too large");
+  static_assert(Q1 % 2 == 0, "paired stores need an even Gauss count");
   extern __shared__ double sm[];
   double* sIn = sm;                // [fld][j3][j2][j1]
   double* sA = sIn + G::SIN;       // x-interp out [fld][j3][j2][q1]
@@ -760,6 +772,9 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
   double* sBt = sD + G::SD;        // [2][32] time tables (double-buffered by iteration parity)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
+  // A-fragment loads run unpredicated over padded rows / k columns: whatever they read is finite
+  // (the buffers start zeroed) and meets a zero B entry or lands in a discarded output row
+  for (int i = tid; i < (int)(G::SMEM / 8); i += 256) sm[i] = 0.0;
   int b = blockIdx.x, k[3], ne[3];
   for (int l = 0; l < 3; ++l) {
     const int m = b % r.ncol[l];
@@ -785,7 +800,8 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
 #pragma unroll
     for (int ks = 0; ks < KP; ++ks) bP[l][ks] = basis(l, fr, 4 * ks + fk);
   }
-  // the thread's Gauss points: (line = 8 t + fr, q_last = 2 fk + e), t = warp + 8 mi
+  // the thread's Gauss points: (line = 8 t + fr, q_last = 2 fk + e), t = warp + 8 mi.  The spatial
+  // weight is folded into the x field and c2 into the w field as the slice enters the window.
   double wsp[MT][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
@@ -814,7 +830,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     const int s = i % LS;
     bool ok;
     const long long gs = spatial(s / (L1 * L2), (s / L1) % L2, s % L1, ok);
-    gsp[m] = (i < G::SIN && ok) ? gs : -1;
+    gsp[m] = (i < G::NIN && ok) ? gs : -1;
   }
   double pre[G::NPRE];
   auto prefetch = [&](int ft) {
@@ -829,9 +845,11 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
   };
   double btp = 0.0;
   auto prefetch_bt = [&](int et) {
-    if (tid < NBT && et >= 0 && et < r.nel[3])
-      btp = tid < QT * PW ? __ldg(r.B[3] + (long long)et * QT * PW + tid)
-                          : __ldg(r.Wq[3] + (long long)et * QT + (tid - QT * PW));
+    if (tid < NBT && et >= 0 && et < r.nel[3]) {
+      const int ga = tid % (QT * PW);
+      const double bv = __ldg(r.B[3] + (long long)et * QT * PW + ga);
+      btp = tid < QT * PW ? bv : bv * __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
+    }
   };
   // x-projection outputs of this thread: line 8 warp + fr, j1 = 2 fk + e (old y prefetched a phase early)
   const int xline = 8 * warp + fr;
@@ -848,7 +866,9 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     const int ct = ft + r.rowoff;
     return (ct >= 0 && ct < r.ntc) ? (long long)ct * ns : -1;
   };
+  const double rc1 = r.c1, rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;
 
+  // window slot of time function f is f % PW (compile-time below: the slice loop is unrolled by PW)
   double X[MT][PW][3][2], Y[MT][PW][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
@@ -864,11 +884,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     if (warp < (NLX + 7) / 8) {
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KP; ++ks) {
-        const int q = 4 * ks + fk;
-        const double av = (xline < NLX && q < Q1) ? xb[xline * Q1 + q] : 0.0;
-        dmma(c0, c1, av, bP[0][ks]);
-      }
+      for (int ks = 0; ks < KP; ++ks) dmma(c0, c1, xb[xline * Q1 + 4 * ks + fk], bP[0][ks]);
       const long long row = yrow(ft);
       if (row >= 0) {
         if (yidx[0] >= 0) r.y[row + yidx[0]] = yold[0] + c0;
@@ -878,8 +894,9 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
   };
 
   const int nfull = r.nel[3] + PT;                   // full-basis time functions
-  prefetch(0);
-  for (int j = 0; j <= nfull + PT; ++j) {
+  const int jmax = nfull + PT;
+  auto step = [&](auto phc, int j) {
+    constexpr int PH = decltype(phc)::value;         // j % PW: slot of the entering slice
     const int et = j - PT;                           // time element (0 <= et < nel_t); z-projection of function et
     const int fp = j - PT - 1;                       // function whose y / x projections run in this iteration
     const bool has_in = j < nfull, has_fp = fp >= 0 && fp < nfull;
@@ -887,7 +904,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     if (has_in) {
 #pragma unroll
       for (int m = 0; m < G::NPRE; ++m)
-        if (tid + 256 * m < G::SIN) sIn[tid + 256 * m] = pre[m];
+        if (tid + 256 * m < G::NIN) sIn[tid + 256 * m] = pre[m];
     }
     if (tid < NBT) sBt[(j & 1) * 32 + tid] = btp;
     if constexpr (D >= 2) {
@@ -903,22 +920,19 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     const double* fin = sIn;
     if constexpr (D >= 2) {
       // phase 2: x interpolation of slice j: lines (fld, j3, j2), K = j1, N = q1 -> sA [fld][j3][j2][q1]
+#ifdef RX_ABL_NOXY
+      if (false) {
+#else
       if (has_in) {
+#endif
         constexpr int NL = 3 * L3 * L2;
         for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
           const int line = mt * 8 + fr;
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < KI; ++ks) {
-            const int jj = 4 * ks + fk;
-            const double av = (line < NL && jj < L1) ? sIn[line * L1 + jj] : 0.0;
-            dmma(c0, c1, av, bI[0][ks]);
-          }
+          for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, sIn[line * L1 + 4 * ks + fk], bI[0][ks]);
           const int n0 = 2 * fk;
-          if (line < NL) {
-            if (n0 < Q1) sA[line * Q1 + n0] = c0;
-            if (n0 + 1 < Q1) sA[line * Q1 + n0 + 1] = c1;
-          }
+          if (line < NL && n0 < Q1) *reinterpret_cast<double2*>(sA + line * Q1 + n0) = make_double2(c0, c1);
         }
       }
       // ... and the y projection of function fp: lines (j3, q1), K = q2, N = j2 -> sD [j3][j2][q1]
@@ -930,11 +944,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
             const int q1 = line % Q1, j3 = line / Q1;
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < KP; ++ks) {
-              const int q = 4 * ks + fk;
-              const double av = (line < NL && q < Q2) ? sC[(j3 * Q2 + q) * Q1 + q1] : 0.0;
-              dmma(c0, c1, av, bP[1][ks]);
-            }
+            for (int ks = 0; ks < KP; ++ks) dmma(c0, c1, sC[(j3 * Q2 + 4 * ks + fk) * Q1 + q1], bP[1][ks]);
             const int n0 = 2 * fk;
             if (line < NL) {
               if (n0 < L2) sD[(j3 * L2 + n0) * Q1 + q1] = c0;
@@ -950,18 +960,18 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
     }
     if constexpr (D == 3) {
       // phase 3: y interpolation of slice j: lines (fld, j3, q1), K = j2, N = q2 -> sB [fld][j3][q2][q1]
+#ifdef RX_ABL_NOXY
+      if (false) {
+#else
       if (has_in) {
+#endif
         constexpr int NL = 3 * L3 * Q1;
         for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
           const int line = mt * 8 + fr;
           const int q1 = line % Q1, fj3 = line / Q1;
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < KI; ++ks) {
-            const int jj = 4 * ks + fk;
-            const double av = (line < NL && jj < L2) ? sA[(fj3 * L2 + jj) * Q1 + q1] : 0.0;
-            dmma(c0, c1, av, bI[1][ks]);
-          }
+          for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, sA[(fj3 * L2 + 4 * ks + fk) * Q1 + q1], bI[1][ks]);
           const int n0 = 2 * fk;
           if (line < NL) {
             if (n0 < Q2) sB[(fj3 * Q2 + n0) * Q1 + q1] = c0;
@@ -974,17 +984,10 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
       __syncthreads();                               // B3
       fin = sB;
     }
-    // phase 4: last-direction interpolation of slice j -> registers (window rotates) ...
+    // phase 4: last-direction interpolation of slice j -> window slot PH ...
     if (has_in) {
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi) {
-#pragma unroll
-        for (int a = 0; a < PW - 1; ++a)
-#pragma unroll
-          for (int f = 0; f < 3; ++f) {
-            X[mi][a][f][0] = X[mi][a + 1][f][0];
-            X[mi][a][f][1] = X[mi][a + 1][f][1];
-          }
         const int t = warp + 8 * mi;
         if (t < NT) {
           const int line = 8 * t + fr;
@@ -992,25 +995,31 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
           for (int f = 0; f < 3; ++f) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < KI; ++ks) {
-              const int jj = 4 * ks + fk;
-              const double av = (line < QL && jj < L) ? fin[(f * L + jj) * QL + line] : 0.0;
-              dmma(c0, c1, av, bI[D - 1][ks]);
-            }
-            X[mi][PW - 1][f][0] = c0;
-            X[mi][PW - 1][f][1] = c1;
+            for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, fin[(f * L + 4 * ks + fk) * QL + line], bI[D - 1][ks]);
+            const double sc0 = f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]);
+            const double sc1 = f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]);
+            X[mi][PH][f][0] = f == 0 ? c0 : c0 * sc0;
+            X[mi][PH][f][1] = f == 0 ? c1 : c1 * sc1;
           }
         }
       }
     }
-    if (et < 0 || et >= nfull) continue;
-    // ... time element et (window slots 0..PT = functions et..et+PT): interpolate in time, linearise,
-    // project in time, all on the thread's own points ...
+    if (et < 0 || et >= nfull) return;
+    constexpr int S0 = (PH + 1) % PW;                // slot of function et
+    // ... time element et (slots S0 + a = functions et + a): interpolate in time, linearise, project
+    // in time, all on the thread's own points ...
+#ifndef RX_ABL_NOTIME
     if (et < r.nel[3]) {
+#else
+    if (et < 0) {
+#endif
+#ifdef RX_ABL_CBT
+      const double* bt = r.btc;          // timing experiment: one table for every element (wrong results)
+#else
       const double* bt = sBt + (j & 1) * 32;
+#endif
 #pragma unroll
       for (int g = 0; g < QT; ++g) {
-        const double wt = bt[QT * PW + g];
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
@@ -1019,14 +1028,16 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
 #pragma unroll
             for (int a = 0; a < PW; ++a) {
               const double ba = bt[g * PW + a];
-              uu = fma(ba, X[mi][a][0][e], uu);
-              ww = fma(ba, X[mi][a][1][e], ww);
-              xx = fma(ba, X[mi][a][2][e], xx);
+              uu = fma(ba, X[mi][(S0 + a) % PW][0][e], uu);
+              ww = fma(ba, X[mi][(S0 + a) % PW][1][e], ww);
+              xx = fma(ba, X[mi][(S0 + a) % PW][2][e], xx);
             }
-            const double cr = r.c1 * (uu - r.a) * (uu - 1.0) + r.c2 * ww;
-            const double v = cr * xx * (wt * wsp[mi][e]);
+            // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
+            const double cr = fma(uu, fma(rc1, uu, rk1), ww + rk0);
+            const double v = cr * xx;
 #pragma unroll
-            for (int a = 0; a < PW; ++a) Y[mi][a][e] = fma(bt[g * PW + a], v, Y[mi][a][e]);
+            for (int a = 0; a < PW; ++a)
+              Y[mi][(S0 + a) % PW][e] = fma(bt[QT * PW + g * PW + a], v, Y[mi][(S0 + a) % PW][e]);
           }
       }
     }
@@ -1040,8 +1051,8 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
 #pragma unroll
         for (int ks = 0; ks < KP; ++ks) {
           const int c = 4 * ks + fk, src = (lane & ~3) | (c >> 1);
-          const double v0 = __shfl_sync(0xffffffffu, Y[mi][0][0], src);
-          const double v1 = __shfl_sync(0xffffffffu, Y[mi][0][1], src);
+          const double v0 = __shfl_sync(0xffffffffu, Y[mi][S0][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, Y[mi][S0][1], src);
           dmma(c0, c1, (c & 1) ? v1 : v0, bP[D - 1][ks]);
         }
         const int n0 = 2 * fk;
@@ -1058,14 +1069,40 @@ __global__ void __launch_bounds__(256, 2) reaction_tile5(RxArgs r) {
           }
         }
       }
+      Y[mi][S0][0] = Y[mi][S0][1] = 0.0;
+    }
+  };
+  prefetch(0);
+#if RX_UNROLL
+  for (int j0 = 0; j0 <= jmax; j0 += PW) {
+    step(std::integral_constant<int, 0>{}, j0);
+    if (j0 + 1 <= jmax) step(std::integral_constant<int, 1 % PW>{}, j0 + 1);
+    if constexpr (PW > 2) if (j0 + 2 <= jmax) step(std::integral_constant<int, 2 % PW>{}, j0 + 2);
+    if constexpr (PW > 3) if (j0 + 3 <= jmax) step(std::integral_constant<int, 3 % PW>{}, j0 + 3);
+  }
+#else
+  // one copy of the step with fixed slots (entering slice -> slot PT, function et -> slot 0) and a
+  // cyclic rotation of both windows after it (fewer registers and instruction bytes than unrolling)
+  for (int j = 0; j <= jmax; ++j) {
+    step(std::integral_constant<int, PT>{}, j);
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+      double xs[3][2], ys[2];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) xs[f][0] = X[mi][0][f][0], xs[f][1] = X[mi][0][f][1];
+      ys[0] = Y[mi][0][0], ys[1] = Y[mi][0][1];
 #pragma unroll
       for (int a = 0; a < PW - 1; ++a) {
-        Y[mi][a][0] = Y[mi][a + 1][0];
-        Y[mi][a][1] = Y[mi][a + 1][1];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) X[mi][a][f][0] = X[mi][a + 1][f][0], X[mi][a][f][1] = X[mi][a + 1][f][1];
+        Y[mi][a][0] = Y[mi][a + 1][0], Y[mi][a][1] = Y[mi][a + 1][1];
       }
-      Y[mi][PW - 1][0] = Y[mi][PW - 1][1] = 0.0;
+#pragma unroll
+      for (int f = 0; f < 3; ++f) X[mi][PW - 1][f][0] = xs[f][0], X[mi][PW - 1][f][1] = xs[f][1];
+      Y[mi][PW - 1][0] = ys[0], Y[mi][PW - 1][1] = ys[1];
     }
   }
+#endif
 }
 
 template <int D, int P, int PT>

@@ -122,3 +122,27 @@ def test_gmres_general_iterate_matches_reference(name):
     x, it, hist = mb.gmres(op, g["rhs"], precond=P, tol=1e-8, max_iter=400)
     assert it == int(g["gm_b_it"])
     assert rel(x, g["gm_b_x"]) < 1e-10
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_apply_stream_matches_serial(depth):
+    """ApplyStream (copy-in / apply / copy-out on three streams) is bitwise the serial path."""
+    import torch
+    import paper_2311_17500_b200 as mb
+    g = load("case_3d_p3")
+    _, op, P = product_objects(g)
+    n = op.shape[0]
+    rng = np.random.default_rng(7)
+    xs = [torch.from_numpy(rng.uniform(-1, 1, n)).pin_memory() for _ in range(5)]
+    zs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    ys = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    mb.ApplyStream(op, P, depth=depth).run(xs, zs)
+    mb.ApplyStream(op, None, depth=depth).run(xs, ys)
+    torch.cuda.synchronize()
+    for x, z, y in zip(xs, zs, ys):
+        ref_y = op.matvec(x.numpy())
+        ref_z = P.apply(ref_y)
+        assert np.array_equal(y.numpy(), ref_y)
+        assert np.array_equal(z.numpy(), ref_z)
+    with pytest.raises(ValueError):
+        mb.ApplyStream(op, P).run(xs[:1], [torch.empty(3, dtype=torch.float64)])
