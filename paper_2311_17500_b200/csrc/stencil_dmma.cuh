@@ -143,7 +143,6 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
     }
   }
 
-  const int W2pt = 2 * a.pt + 1;
   // ---- async loads of chunk t0: halo tile (16 B copies) + band rows of the
   // halo tile of chunk t0 by ONE TMA bulk-tensor copy: box (TSTR time rows, H1, H2, H3) of the
   // time-innermost copy; out-of-range halo coordinates (incl. negative) are zero-filled by TMA
@@ -226,7 +225,6 @@ __global__ void __launch_bounds__(128) time_filter_ti(const double* __restrict__
                                                       double* __restrict__ y, int nchan, int nt, int ntp,
                                                       long long ns, int accumulate) {
   constexpr int PX = PT + (PT & 1), BWX = 2 * PT + 1;   // PX even: 16-byte aligned pairs
-  constexpr int pt = PT;
   extern __shared__ double bs[];                     // [nchan][TR][BWX]
   const long long i = blockIdx.x * 128LL + threadIdx.x;
   const int t0 = blockIdx.y * TR;
