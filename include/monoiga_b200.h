@@ -154,6 +154,30 @@ int mi_normalize(mi_ctx* ctx, long long n, const double* x, const double* nrm2, 
 int mi_cgs_pass(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* h_in,
                 double* w, double* h_out);
 
+/* ---------------------------------------------------------------------
+ * Spline Upwind residual indicator (replaces compute_theta's grid work,
+ * stabilization.py:235-339, with the strong residual of 148-174 and the
+ * ionic current c1 u (u-a)(u-1) + c2 u w at the q = p+1 Gauss points).
+ * ------------------------------------------------------------------- */
+/* Element tables per present direction x, y, z (d of them) then t, each
+   [nel][q][p+1] (value of function e + a at Gauss point g of element e):
+   B0 values; B1 second parametric derivatives (space) / first (time).
+   lengths: box edge lengths (lap u = sum_l d2u/dx_l^2 / L_l^2). */
+int mi_theta_setup(mi_ctx* ctx, const int* nel, const double* B0, const double* B1, const double* lengths,
+                   double final_time, double C_m, double D, double c1, double a, double c2);
+/* Element maxima of |res| for time elements [et0, et1) into emax (device,
+   [nel_t][nel_3][nel_2][nel_1]) and running maxima of |u|, |u_t| into
+   maxes (device double[2], zeroed by the caller before the first call).
+   src: NULL, or the source at the Gauss points of those elements,
+   [(et - et0) * q_t + g][spatial Gauss index] (device). */
+int mi_theta_elements(mi_ctx* ctx, const double* u, const double* w, const double* src, int et0, int et1,
+                      double* emax, double* maxes);
+/* out[o][i][r] = max over e in [w0[i], w1[i]) of in[o][e][r]   (w0, w1 host) */
+int mi_window_max(mi_ctx* ctx, const double* in, double* out, long long outer, int n_in, int n_out,
+                  long long inner, const int* w0, const int* w1);
+/* theta = min(numer / denom, 1)   (denom > 0) */
+int mi_theta_ratio(mi_ctx* ctx, const double* numer, double* theta, long long n, double denom);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,16 @@ struct mi_ctx {
   mi::DeviceBuf ws_M[3], ws_Mi[3], ws_MT0, ws_MiT0;   // spatial mass factors, inverses (+ transposes, dir 1)
   mi::DeviceBuf ws_t1, ws_t2, ws_t3;
 
+  // ---- SU residual indicator (compute_theta)
+  bool th_ready = false;
+  mi::DeviceBuf th_B0, th_B1;   // element tables, directions x, y, z, t (values; 2nd / 1st derivatives)
+  size_t th_off[4] = {0, 0, 0, 0};
+  int th_nel[4] = {1, 1, 1, 1};
+  double th_il2[3] = {0, 0, 0};
+  double th_cmT = 0, th_D = 0, th_c1 = 0, th_a = 0, th_c2 = 0;
+  int* th_win = nullptr;        // window tables of mi_window_max
+  int th_nwin = 0;
+
   // ---- profiling: per-slot accumulated ms and launch counts
   bool prof_on = false;
   long long launches[8] = {0, 0, 0, 0, 0, 0, 0, 0};

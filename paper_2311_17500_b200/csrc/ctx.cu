@@ -144,7 +144,8 @@ int mi_ctx_destroy(mi_ctx* c) {
                            &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
                            &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->partials};
   for (auto* b : bufs) mi::dfree(*b);
-  mi::DeviceBuf* wbufs[] = {&c->ws_Kinv, &c->ws_MT0, &c->ws_MiT0, &c->ws_t1, &c->ws_t2, &c->ws_t3};
+  mi::DeviceBuf* wbufs[] = {&c->ws_Kinv, &c->ws_MT0, &c->ws_MiT0, &c->ws_t1, &c->ws_t2, &c->ws_t3,
+                            &c->th_B0, &c->th_B1};
   for (auto* b : wbufs) mi::dfree(*b);
   for (int l = 0; l < 3; ++l) {
     mi::dfree(c->ws_M[l]);
@@ -154,6 +155,7 @@ int mi_ctx_destroy(mi_ctx* c) {
     mi::dfree(c->lam[l]);
   }
   if (c->pen_partner) cudaFree(c->pen_partner);
+  if (c->th_win) cudaFree(c->th_win);
   for (auto& r : c->prof_events) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

@@ -5,9 +5,10 @@ Each sweep freezes the Rogers-McCulloch reaction at the previous iterate,
 solves the potential system with the device GMRES + fast-diagonalisation
 preconditioner (the hot path), solves the recovery system with the device
 w-solve, relaxes both, and stops when max |u_new - u| <= tolerance.
-Spline Upwind: the indicator is recomputed (compute_theta, host) and
-relaxed/frozen exactly as solver.py:291-324 does, then factorised and turned
-into device stencil channels.
+Spline Upwind: the indicator is recomputed on the device (DeviceIndicator,
+the reference compute_theta) and relaxed/frozen exactly as
+solver.py:291-324 does, then factorised and turned into device stencil
+channels.
 """
 
 import time as _time
@@ -19,8 +20,8 @@ from .device import DeviceContext
 from .krylov import gmres
 from .operator import KroneckerOperator, Stabilization
 from .precond import FastDiagPreconditioner
-from .problem import (FixedPointConfig, FixedPointDiverged, GaussGrid, SolveResult, box_of, compute_theta,
-                      load_vector)
+from .problem import FixedPointConfig, FixedPointDiverged, GaussGrid, SolveResult, box_of, load_vector
+from .theta import DeviceIndicator
 from .wsolve import RecoverySolver
 
 
@@ -43,6 +44,7 @@ class _Workspace:
                                          lengths=self.L, device=device)
         self.wsolver = RecoverySolver(st, problem.final_time, problem.b, problem.d_e, config.linear_tol,
                                       lengths=self.L, device=device)
+        self.indicator = DeviceIndicator(problem, device) if config.stabilization == "spline_upwind" else None
 
     def operator(self, problem, u_k, w_k, stab):
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
@@ -71,7 +73,7 @@ def fixed_point_solve(problem, config=None, device=0):
         if config.indicator_override is not None:
             frozen_indicator = config.indicator_override(problem, pre.u, pre.w)
         else:
-            frozen_indicator = compute_theta(problem, pre.u, pre.w)
+            frozen_indicator = DeviceIndicator(problem, device).compute(pre.u, pre.w)
         frozen_stab = Stabilization(st, _indicator_values(frozen_indicator), config.lowrank_tol, problem.C_m,
                                     lengths=box_of(problem.geometry)[0])
 
@@ -92,7 +94,7 @@ def fixed_point_solve(problem, config=None, device=0):
                 if config.indicator_override is not None:
                     fresh = config.indicator_override(problem, u, w)
                 else:
-                    fresh = compute_theta(problem, u, w, grid=ws.grid)
+                    fresh = ws.indicator.compute(u, w)
                 if indicator is not None and alpha < 1.0:
                     prev = _indicator_values(indicator)
                     fv = _indicator_values(fresh)

@@ -196,17 +196,25 @@ class GaussGrid:
         return np.stack([mesh[d - 1 - l].ravel() for l in range(d)], axis=-1)
 
     def source_values(self, source):
-        xq = self.physical_points()
+        return self.source_rows(source, 0, self.tx.size)
+
+    def source_rows(self, source, i0, i1):
+        """Source at time Gauss points i0..i1-1 x all spatial Gauss points, (i1-i0, Q_d, ..., Q_1)."""
+        if getattr(self, "_xq", None) is None:
+            self._xq = self.physical_points()
+        xq = self._xq
         qs = xq.shape[0]
-        tq = self.tx * self.T
+        tq = self.tx[i0:i1] * self.T
         fv = np.empty((tq.size, qs))
         for i, t in enumerate(tq):
             fv[i] = np.asarray(source(xq, np.full(qs, t)), float).reshape(qs)
         return fv.reshape((tq.size,) + tuple(x.size for x in reversed(self.sx)))
 
 
-def load_vector(st, geometry, source, grid=None):
-    """f_vec[i] = int int f B_i (assembly.py:350-398, box geometry)."""
+def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24):
+    """f_vec[i] = int int f B_i (assembly.py:350-398, box geometry).  The Gauss grid is visited in
+    chunks of time points (spatial projection per chunk, then the time projection accumulates),
+    so the full space-time grid is never held at once."""
     if source is None:
         return np.zeros(st.num_dof)
     g = grid if grid is not None else GaussGrid(st, geometry)
@@ -214,11 +222,16 @@ def load_vector(st, geometry, source, grid=None):
     ws = np.asarray(g.sw[d - 1] * g.L[d - 1])
     for l in reversed(range(d - 1)):
         ws = np.multiply.outer(ws, g.sw[l] * g.L[l])
-    vals = g.source_values(source) * ws[None] * (g.tw * g.T).reshape((-1,) + (1,) * d)
-    out = _mode(g.tB[0].T, vals, 0)
-    for l in range(d):
-        out = _mode(g.sB[l][0].T, out, 1 + (d - 1 - l))
-    return out.ravel()
+    nq = g.tx.size
+    step = max(1, chunk_points // max(1, ws.size))
+    acc = np.zeros((g.tB[0].shape[1],) + tuple(s.dimension for s in reversed(st.spatial)))
+    for i0 in range(0, nq, step):
+        i1 = min(nq, i0 + step)
+        vals = g.source_rows(source, i0, i1) * ws[None] * (g.tw[i0:i1] * g.T).reshape((-1,) + (1,) * d)
+        for l in range(d):
+            vals = _mode(g.sB[l][0].T, vals, 1 + (d - 1 - l))
+        acc += _mode(g.tB[0][i0:i1].T, vals, 0)
+    return acc.ravel()
 
 
 def window_elements(space, i):

@@ -1,0 +1,155 @@
+"""Spline Upwind residual indicator on the device (reference compute_theta,
+stabilization.py:235-339).
+
+``DeviceIndicator(problem).compute(u, w)`` returns the same
+``ResidualIndicator`` as the reference: the strong residual
+
+    res = C_m u_t / T - D lap u + c1 u (u - a)(u - 1) + c2 u w - f
+
+at the q = p+1 Gauss points of every space-time element (kernel
+``theta_elements``, csrc/theta.cu), element maxima of |res|, the window
+maxima over each basis function's support (the reference's full-basis time
+windows 0..N_t-1 included, stabilization.py:307), and
+theta = min(numer / denom, 1) with denom = C_m (max|u| + max|u_t|) / T.
+
+The source is a Python callable, as in the reference; it is evaluated on the
+host one chunk of time elements at a time and streamed to the device, so the
+full space-time Gauss grid is never materialised.
+"""
+
+import warnings
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceContext, dptr, host_ptr
+from .problem import GaussGrid, ResidualIndicator, box_of, window_elements
+from .spaces import basis_table, gauss_rule, greville
+
+
+def element_tables(space, order):
+    """B[e, g, a] = order-th parametric derivative of function e + a at Gauss point g (q = p+1) of
+    element e (open uniform knots: element e carries functions e..e+p)."""
+    bp = space.breakpoints
+    ne = bp.size - 1
+    p = space.degree
+    q = p + 1
+    x, _ = gauss_rule(bp, q)
+    T = basis_table(space, x, order)
+    B = np.zeros((ne, q, p + 1))
+    for e in range(ne):
+        B[e] = T[e * q:(e + 1) * q, e:e + p + 1]
+    return B
+
+
+class DeviceIndicator:
+    """Per-problem device state for compute_theta (tables uploaded once)."""
+
+    def __init__(self, problem, device=0, context=None, chunk_points=1 << 26):
+        st = problem.space
+        self.problem = problem
+        self.st = st
+        self.d = len(st.spatial)
+        self.ctx = context if context is not None else DeviceContext(st, device)
+        ctx = self.ctx
+        p = ctx.p
+        if ctx.pt != p or p > 3:
+            raise ValueError("device residual indicator needs p = p_t <= 3")
+        self.L, _ = box_of(problem.geometry)
+        self.T = float(problem.final_time)
+        B0, B1, nel = [], [], []
+        for s in st.spatial:
+            B0.append(element_tables(s, 0).ravel())
+            B1.append(element_tables(s, 2).ravel())
+            nel.append(s.breakpoints.size - 1)
+        B0.append(element_tables(st.time, 0).ravel())
+        B1.append(element_tables(st.time, 1).ravel())
+        nel.append(st.time.breakpoints.size - 1)
+        self.nel = [int(v) for v in nel]
+        b0 = np.ascontiguousarray(np.concatenate(B0))
+        b1 = np.ascontiguousarray(np.concatenate(B1))
+        nh = np.asarray(self.nel, dtype=np.int32)
+        Lh = np.ascontiguousarray(np.asarray(self.L, float))
+        _lib.call("mi_theta_setup", ctx.handle, host_ptr(nh), host_ptr(b0), host_ptr(b1), host_ptr(Lh),
+                  self.T, float(problem.C_m), float(problem.D), float(problem.c1), float(problem.a),
+                  float(problem.c2))
+        self.chunk_points = int(chunk_points)
+        self._grid = None
+        # support windows (element ranges) of every function, time windows over the full basis
+        self.win_t = [window_elements(st.time, c) for c in range(st.num_time)]
+        self.win_s = [[window_elements(s, i) for i in range(s.dimension)] for s in st.spatial]
+
+    def _window(self, src, dst, outer, n_in, wins, inner):
+        w0 = np.ascontiguousarray([a for a, _ in wins], dtype=np.int32)
+        w1 = np.ascontiguousarray([b for _, b in wins], dtype=np.int32)
+        _lib.call("mi_window_max", self.ctx.handle, dptr(src), dptr(dst), int(outer), int(n_in), len(wins),
+                  int(inner), host_ptr(w0), host_ptr(w1))
+
+    def compute(self, u, w):
+        """ResidualIndicator for the state (u, w) (numpy or device tensors of length N)."""
+        ctx, st, d = self.ctx, self.st, self.d
+        ctx.bind_stream()
+        ud = ctx.to_device(u)
+        wd = ctx.to_device(w)
+        if ud.numel() != ctx.N or wd.numel() != ctx.N:
+            raise ValueError("dimension mismatch: state of size %d for a space of size %d" % (ud.numel(), ctx.N))
+        nel_t = self.nel[d]
+        nes = int(np.prod(self.nel[:d]))
+        emax = ctx.empty(nel_t * nes)
+        maxes = torch.zeros(2, dtype=torch.float64, device=ctx.device)
+        source = self.problem.source
+        if source is None:
+            _lib.call("mi_theta_elements", ctx.handle, dptr(ud), dptr(wd), None, 0, nel_t, dptr(emax),
+                      dptr(maxes))
+        else:
+            if self._grid is None:
+                self._grid = GaussGrid(st, self.problem.geometry)
+            grid = self._grid
+            qt = st.time.degree + 1
+            per_el = qt * int(np.prod([x.size for x in grid.sx]))
+            step = max(1, self.chunk_points // per_el)
+            for et0 in range(0, nel_t, step):
+                et1 = min(nel_t, et0 + step)
+                fv = grid.source_rows(source, et0 * qt, et1 * qt)
+                fd = torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(ctx.device)
+                _lib.call("mi_theta_elements", ctx.handle, dptr(ud), dptr(wd), dptr(fd), et0, et1, dptr(emax),
+                          dptr(maxes))
+                del fd
+        umax, utmax = (float(v) for v in maxes.cpu().numpy())
+        denom = float(self.problem.C_m) * (umax / self.T + utmax / self.T)
+        # window maxima: time (over elements -> functions), then x, y, z
+        nt = st.num_time
+        cur = ctx.empty(nt * nes)
+        self._window(emax, cur, 1, nel_t, self.win_t, nes)
+        del emax
+        shape = [nt] + [self.nel[l] for l in reversed(range(d))]    # (nt, E_d, ..., E_1)
+        for l in range(d):
+            axis = d - l                                 # position of direction l in `shape`
+            outer = int(np.prod(shape[:axis]))
+            inner = int(np.prod(shape[axis + 1:]))
+            n_out = st.spatial[l].dimension
+            nxt = ctx.empty(outer * n_out * inner)
+            self._window(cur, nxt, outer, shape[axis], self.win_s[l], inner)
+            shape[axis] = n_out
+            cur = nxt
+        numer = cur
+        if denom > 0.0:
+            theta = ctx.empty(numer.numel())
+            _lib.call("mi_theta_ratio", ctx.handle, dptr(numer), dptr(theta), int(numer.numel()), denom)
+            values = theta.cpu().numpy().reshape(nt, st.num_space)
+        else:
+            # stabilization.py:317-333 (zero denominator)
+            nh = numer.cpu().numpy().reshape(nt, st.num_space)
+            values = np.zeros_like(nh)
+            top = nh.max(initial=0.0)
+            hot = nh > 1e-12 * top
+            if np.any(hot) and top > 0.0:
+                warnings.warn("residual indicator denominator vanished with a nonzero residual; "
+                              "activating the stabilizer fully there", RuntimeWarning, stacklevel=2)
+                values[hot] = 1.0
+        return ResidualIndicator(values, greville(st.time)[1:], [greville(s) for s in st.spatial],
+                                 tuple(s.dimension for s in reversed(st.spatial)))
+
+    def close(self):
+        self.ctx.close()

@@ -175,5 +175,30 @@ def fixed_point_cases():
     np.savez_compressed(os.path.join(HERE, "fixed_point.npz"), **out)
 
 
+def theta_cases():
+    """compute_theta at random states on equal-degree spaces (the device path's domain)."""
+    from monoiga.geometry import box_geometry
+    from monoiga.stabilization import compute_theta
+    out = {}
+    rng = np.random.default_rng(33)
+    cases = [("th3d", 2, (4, 3, 5), 6, (1.0, 0.5, 2.0), 2.0, True, 1e-2),
+             ("th1d", 3, (9,), 7, (1.5,), 1.0, False, 1e-3)]
+    for name, p, nes, ne_t, L, T, with_src, D in cases:
+        st = SpaceTimeSpace([SplineSpace.uniform(p, n) for n in nes], SplineSpace.uniform(p, ne_t))
+        geo = box_geometry(list(L), final_time=T)
+        prob = MonodomainProblem(geo, st, source=pulse_source if with_src else None, D=D)
+        u = rng.uniform(0, 1, st.num_dof)
+        w = rng.uniform(0, 0.1, st.num_dof)
+        th = compute_theta(prob, u, w)
+        out.update({name + "_u": u, name + "_w": w, name + "_values": th.values, name + "_p": p,
+                    name + "_ne": np.array(nes), name + "_ne_t": ne_t, name + "_L": np.array(L), name + "_T": T,
+                    name + "_src": int(with_src), name + "_D": D})
+        print(name, th.values.shape, float(th.values.max()))
+    np.savez_compressed(os.path.join(HERE, "theta.npz"), **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fixed_point":
     fixed_point_cases()
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "theta":
+    theta_cases()
