@@ -35,6 +35,19 @@ class UpwindWeights:
 
 
 def upwind_weights(tspace):
+    """Cached per time space (knots, degree); see _upwind_weights."""
+    key = (tuple(np.asarray(tspace.knots, float).tolist()), int(tspace.degree))
+    hit = _TAU_CACHE.get(key)
+    if hit is None:
+        hit = _upwind_weights(tspace)
+        _TAU_CACHE[key] = hit
+    return hit
+
+
+_TAU_CACHE = {}
+
+
+def _upwind_weights(tspace):
     """Solve the orthogonality conditions of stabilization.py:84-145.
 
     For every near-diagonal pair (i, i+l), l = 1..p, of the full time basis,
@@ -113,26 +126,39 @@ def hat_values(nodes, x):
     return H
 
 
+def _shifted(A, lo, hi):
+    """Column-shifted view helper: S[:, s - lo, i] = A[:, i + s] (0 outside), s in [lo, hi]."""
+    nq, n = A.shape
+    P = np.zeros((nq, n + hi - lo))
+    P[:, -lo:-lo + n] = A
+    return [P[:, s - lo:s - lo + n] for s in range(lo, hi + 1)]
+
+
 def su_time_bands(st, tau, lowrank, capacitance):
     """Per rank r: band of C_m s_r sum_k int tau_k prof_r b_i^(k) b_j^(k) dt.
 
     Parametric time integrals, p+2 Gauss points on cells split at the
     constrained time Greville abscissae (stabilization.py:461-486).  The
     k-sum is a legal reassociation (one spatial factor per rank,
-    stabilization.py:439-445).  Returns (R, N_t, 2p+1).
+    stabilization.py:439-445).  Only the 2p+1 diagonals are formed.
+    Returns (R, N_t, 2p+1).
     """
     p = st.time.degree
     tg = st.time_greville()
     x, w = gauss_rule(cells_with(st.time, tg), p + 2)
     prof = hat_values(tg, x) @ lowrank.time_factors          # (nq, R)
-    mats = np.zeros((lowrank.rank, st.num_time, st.num_time))
+    nt = st.num_time
+    bands = np.zeros((lowrank.rank, nt, 2 * p + 1))
     for k in range(1, p + 1):
         Bk = basis_table(st.time, x, k)[:, 1:]
         tk = tau.evaluate(k, x)
-        for r in range(lowrank.rank):
-            mats[r] += (Bk * (w * tk * prof[:, r])[:, None]).T @ Bk
+        shifts = _shifted(Bk, -p, p)                          # Bk[:, i + dj - p]
+        wk = (w * tk)[:, None] * prof                         # (nq, R)
+        for dj in range(2 * p + 1):
+            prod = Bk * shifts[dj]                            # (nq, nt): b_i b_{i+dj-p}
+            bands[:, :, dj] += wk.T @ prod
     coef = capacitance * lowrank.weights
-    return np.stack([coef[r] * to_band(mats[r], p) for r in range(lowrank.rank)])
+    return bands * coef[:, None, None]
 
 
 def hat_triple(space, length=1.0):
@@ -142,9 +168,22 @@ def hat_triple(space, length=1.0):
     theta_r multilinear on the Greville grid (stabilization.py:469-488), i.e.
     S^s_r[i, j] = sum_k theta_r[k] prod_l H_l[i_l, j_l - i_l + p, k_l - i_l + KO].
     Computed with p+2 Gauss points on cells split at the Greville abscissae
-    (exact: the integrand is a polynomial of degree 2p+1 per cell).
-    Returns (H, KO) with H of shape (n, 2p+1, 2*KO+1).
+    (exact: the integrand is a polynomial of degree 2p+1 per cell), band by
+    band.  Returns (H, KO) with H of shape (n, 2p+1, 2*KO+1); cached per
+    (knots, degree, length) because it depends on the space only.
     """
+    key = (tuple(np.asarray(space.knots, float).tolist()), int(space.degree), float(length))
+    hit = _HAT_CACHE.get(key)
+    if hit is None:
+        hit = _hat_triple(space, length)
+        _HAT_CACHE[key] = hit
+    return hit[0].copy(), hit[1]
+
+
+_HAT_CACHE = {}
+
+
+def _hat_triple(space, length):
     p = space.degree
     n = space.dimension
     g = greville(space)
@@ -154,19 +193,19 @@ def hat_triple(space, length=1.0):
     Hat = hat_values(g, x)
     KO = p + 1
     H = np.zeros((n, 2 * p + 1, 2 * KO + 1))
-    full = np.einsum("q,qi,qj,qk->ijk", w, B, B, Hat, optimize=True)
-    for i in range(n):
-        for dj in range(2 * p + 1):
-            j = i + dj - p
-            if not 0 <= j < n:
-                continue
-            for dk in range(2 * KO + 1):
-                k = i + dk - KO
-                if 0 <= k < n:
-                    H[i, dj, dk] = full[i, j, k]
-    # every nonzero triple product must fall inside the stored window
-    check = np.abs(full).sum() - np.abs(H).sum()
-    if check > 1e-12 * max(np.abs(full).sum(), 1e-300):
+    Bs = _shifted(B, -p, p)
+    Hs = _shifted(Hat, -KO, KO)
+    WB = w[:, None] * B
+    inside = 0.0
+    for dj in range(2 * p + 1):
+        WBB = WB * Bs[dj]
+        for dk in range(2 * KO + 1):
+            H[:, dj, dk] = (WBB * Hs[dk]).sum(axis=0)
+            inside += (np.abs(WBB) * np.abs(Hs[dk])).sum()
+    # every nonzero triple product must fall inside the stored window: the windowed sum of
+    # |w b_i b_j hat_k| must equal the unrestricted one, sum_q |w| (sum_i |b|)^2 (sum_k |hat|)
+    total = float((np.abs(w) * np.abs(B).sum(axis=1) ** 2 * np.abs(Hat).sum(axis=1)).sum())
+    if total - inside > 1e-12 * max(total, 1e-300):
         raise StabilizationError("hat triple-product window too small")
     return H, KO
 

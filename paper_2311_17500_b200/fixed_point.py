@@ -56,12 +56,29 @@ def _indicator_values(ind):
     return np.asarray(getattr(ind, "values", ind), float)
 
 
+class _Phases:
+    """Wall time per driver phase (synchronised, so GPU work is attributed to its phase)."""
+
+    def __init__(self):
+        self.sec = {}
+        self._t = None
+
+    def start(self):
+        torch.cuda.synchronize()
+        self._t = _time.perf_counter()
+
+    def stop(self, name):
+        torch.cuda.synchronize()
+        self.sec[name] = self.sec.get(name, 0.0) + _time.perf_counter() - self._t
+
+
 def fixed_point_solve(problem, config=None, device=0):
     """solver.py:239-386 on the device; returns SolveResult (numpy u, w)."""
     if config is None:
         config = FixedPointConfig()
     st = problem.space
     t0 = _time.perf_counter()
+    ph = _Phases()
 
     frozen_stab = None
     galerkin_sweeps = 0
@@ -77,7 +94,9 @@ def fixed_point_solve(problem, config=None, device=0):
         frozen_stab = Stabilization(st, _indicator_values(frozen_indicator), config.lowrank_tol, problem.C_m,
                                     lengths=box_of(problem.geometry)[0])
 
+    ph.start()
     ws = _Workspace(problem, config, device)
+    ph.stop("setup")
     u = np.zeros(st.num_dof)
     w = np.zeros(st.num_dof)
     increments, gmres_iters, pcg_iters = [], [], []
@@ -91,10 +110,12 @@ def fixed_point_solve(problem, config=None, device=0):
             if frozen_stab is not None:
                 stab = frozen_stab
             else:
+                ph.start()
                 if config.indicator_override is not None:
                     fresh = config.indicator_override(problem, u, w)
                 else:
                     fresh = ws.indicator.compute(u, w)
+                ph.stop("indicator")
                 if indicator is not None and alpha < 1.0:
                     prev = _indicator_values(indicator)
                     fv = _indicator_values(fresh)
@@ -104,21 +125,29 @@ def fixed_point_solve(problem, config=None, device=0):
                             and drift * alpha <= config.indicator_freeze_tol):
                         freeze_now = True
                 indicator = fresh
+                ph.start()
                 stab = Stabilization(st, _indicator_values(indicator), config.lowrank_tol, problem.C_m,
                                      lengths=ws.L)
+                ph.stop("stabilization")
                 if freeze_now:
                     frozen_stab = stab
+        ph.start()
         op = ws.operator(problem, u, w, stab)
+        ph.stop("operator_setup")
+        ph.start()
         u_tilde, nit, _ = gmres(op, ws.f_vec, precond=ws.precond, tol=config.linear_tol)
+        ph.stop("gmres")
         gmres_iters.append(nit)
         op.ctx.close()
 
+        ph.start()
         if config.evolve_recovery:
             g_vec = problem.b * ws.mass_op.matvec(u)
             w_tilde, w_its = ws.wsolver.solve(g_vec)
             pcg_iters.extend(w_its)
         else:
             w_tilde = w
+        ph.stop("w_solve")
 
         u_new = alpha * u_tilde + (1.0 - alpha) * u
         w_new = alpha * w_tilde + (1.0 - alpha) * w
@@ -129,8 +158,8 @@ def fixed_point_solve(problem, config=None, device=0):
         u, w = u_new, w_new
         if inc <= config.tolerance:
             return SolveResult(u, w, k, increments, True, gmres_iters, pcg_iters,
-                               _time.perf_counter() - t0, indicator)
+                               _time.perf_counter() - t0, indicator, ph.sec)
     result = SolveResult(u, w, galerkin_sweeps + config.max_iterations, increments, False, gmres_iters,
-                         pcg_iters, _time.perf_counter() - t0, indicator)
+                         pcg_iters, _time.perf_counter() - t0, indicator, ph.sec)
     raise FixedPointDiverged("fixed point did not reach %.2e in %d iterations"
                              % (config.tolerance, config.max_iterations), result)

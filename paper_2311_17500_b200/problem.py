@@ -129,6 +129,7 @@ class SolveResult:
     pcg_iterations: list = field(default_factory=list)
     wall_time: float = 0.0
     indicator: object = None
+    phase_seconds: dict = field(default_factory=dict)   # device driver only: wall time per phase
 
     @property
     def avg_gmres(self):

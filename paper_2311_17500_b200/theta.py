@@ -46,7 +46,7 @@ def element_tables(space, order):
 class DeviceIndicator:
     """Per-problem device state for compute_theta (tables uploaded once)."""
 
-    def __init__(self, problem, device=0, context=None, chunk_points=1 << 26):
+    def __init__(self, problem, device=0, context=None, chunk_points=1 << 26, cache_bytes=4 << 30):
         st = problem.space
         self.problem = problem
         self.st = st
@@ -75,10 +75,34 @@ class DeviceIndicator:
                   self.T, float(problem.C_m), float(problem.D), float(problem.c1), float(problem.a),
                   float(problem.c2))
         self.chunk_points = int(chunk_points)
+        self.cache_bytes = int(cache_bytes)
         self._grid = None
+        self._src_cache = None        # [(et0, et1, device tensor)] when the source fits cache_bytes
         # support windows (element ranges) of every function, time windows over the full basis
         self.win_t = [window_elements(st.time, c) for c in range(st.num_time)]
         self.win_s = [[window_elements(s, i) for i in range(s.dimension)] for s in st.spatial]
+
+    def _source_chunks(self, source, nel_t):
+        if self._src_cache is not None:
+            yield from self._src_cache
+            return
+        if self._grid is None:
+            self._grid = GaussGrid(self.st, self.problem.geometry)
+        grid = self._grid
+        qt = self.st.time.degree + 1
+        per_el = qt * int(np.prod([x.size for x in grid.sx]))
+        keep = per_el * nel_t * 8 <= self.cache_bytes
+        step = max(1, self.chunk_points // per_el)
+        chunks = []
+        for et0 in range(0, nel_t, step):
+            et1 = min(nel_t, et0 + step)
+            fv = grid.source_rows(source, et0 * qt, et1 * qt)
+            fd = torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device)
+            if keep:
+                chunks.append((et0, et1, fd))
+            yield et0, et1, fd
+        if keep:
+            self._src_cache = chunks
 
     def _window(self, src, dst, outer, n_in, wins, inner):
         w0 = np.ascontiguousarray([a for a, _ in wins], dtype=np.int32)
@@ -103,19 +127,11 @@ class DeviceIndicator:
             _lib.call("mi_theta_elements", ctx.handle, dptr(ud), dptr(wd), None, 0, nel_t, dptr(emax),
                       dptr(maxes))
         else:
-            if self._grid is None:
-                self._grid = GaussGrid(st, self.problem.geometry)
-            grid = self._grid
-            qt = st.time.degree + 1
-            per_el = qt * int(np.prod([x.size for x in grid.sx]))
-            step = max(1, self.chunk_points // per_el)
-            for et0 in range(0, nel_t, step):
-                et1 = min(nel_t, et0 + step)
-                fv = grid.source_rows(source, et0 * qt, et1 * qt)
-                fd = torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(ctx.device)
+            # the source does not change between sweeps: its Gauss values stay on the device when
+            # they fit cache_bytes, otherwise they are re-evaluated and streamed chunk by chunk
+            for et0, et1, fd in self._source_chunks(source, nel_t):
                 _lib.call("mi_theta_elements", ctx.handle, dptr(ud), dptr(wd), dptr(fd), et0, et1, dptr(emax),
                           dptr(maxes))
-                del fd
         umax, utmax = (float(v) for v in maxes.cpu().numpy())
         denom = float(self.problem.C_m) * (umax / self.T + utmax / self.T)
         # window maxima: time (over elements -> functions), then x, y, z
