@@ -162,9 +162,10 @@ int mi_cgs_pass(mi_ctx* ctx, long long n, int k, const double* V, long long ldv,
 /* Element tables per present direction x, y, z (d of them) then t, each
    [nel][q][p+1] (value of function e + a at Gauss point g of element e):
    B0 values; B1 second parametric derivatives (space) / first (time).
-   lengths: box edge lengths (lap u = sum_l d2u/dx_l^2 / L_l^2). */
+   lengths: box edge lengths; diffusion: D_l per direction (the reference's
+   scalar D repeated), so the diffusion term is sum_l D_l d2u/dx_l^2 / L_l^2. */
 int mi_theta_setup(mi_ctx* ctx, const int* nel, const double* B0, const double* B1, const double* lengths,
-                   double final_time, double C_m, double D, double c1, double a, double c2);
+                   const double* diffusion, double final_time, double C_m, double c1, double a, double c2);
 /* Element maxima of |res| for time elements [et0, et1) into emax (device,
    [nel_t][nel_3][nel_2][nel_1]) and running maxima of |u|, |u_t| into
    maxes (device double[2], zeroed by the caller before the first call).

@@ -116,7 +116,7 @@ struct mi_ctx {
   size_t th_off[4] = {0, 0, 0, 0};
   int th_nel[4] = {1, 1, 1, 1};
   double th_il2[3] = {0, 0, 0};
-  double th_cmT = 0, th_D = 0, th_c1 = 0, th_a = 0, th_c2 = 0;
+  double th_cmT = 0, th_c1 = 0, th_a = 0, th_c2 = 0;
   int* th_win = nullptr;        // window tables of mi_window_max
   int th_nwin = 0;
 

@@ -1,8 +1,9 @@
 // Spline Upwind residual indicator on the device (reference compute_theta,
 // stabilization.py:235-339; strong residual stabilization.py:148-174):
 //
-//   res = C_m u_t / T - D lap u + c1 u (u - a)(u - 1) + c2 u w - f
+//   res = C_m u_t / T - sum_l D_l d2u/dx_l^2 + c1 u (u - a)(u - 1) + c2 u w - f
 //
+// (D scalar in the reference; one value per direction here)
 // at the q = p+1 Gauss points of every space-time element, reduced to
 // per-element maxima of |res|, plus the global maxima max|u|, max|u_t| of
 // the denominator.  The per-function window maxima (separable along t, x, y,
@@ -38,8 +39,8 @@ struct ThArgs {
   long long ns, gs;               // spatial DoFs; spatial Gauss points (src row length)
   int G[3];                       // spatial Gauss points per direction
   int et0, et1;
-  double il2[3];                  // 1 / L_l^2
-  double cmT, D, c1, a, c2;       // C_m / T, D, Rogers-McCulloch constants
+  double il2[3];                  // D_l / L_l^2
+  double cmT, c1, a, c2;          // C_m / T, Rogers-McCulloch constants
 };
 
 template <int D, int P>
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(256, 2) theta_elements(ThArgs r) {
 #pragma unroll
       for (int f = 0; f < 3; ++f) X[mi][a][f][0] = X[mi][a][f][1] = 0.0;
   double umax = 0.0, utmax = 0.0;
-  const double cmT = r.cmT, Dd = r.D, rc1 = r.c1, ra = r.a, rc2 = r.c2;
+  const double cmT = r.cmT, rc1 = r.c1, ra = r.a, rc2 = r.c2;
 
   const int nsl = r.et1 - r.et0 + PT;              // slices: full time functions et0 .. et1 + PT - 1
   prefetch(r.et0);
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(256, 2) theta_elements(ThArgs r) {
             lp = fma(b0t, X[mi][a][1][e], lp);
             ww = fma(b0t, X[mi][a][2][e], ww);
           }
-          double res = cmT * ut - Dd * lp + rc1 * uu * (uu - ra) * (uu - 1.0) + rc2 * uu * ww;
+          double res = cmT * ut - lp + rc1 * uu * (uu - ra) * (uu - 1.0) + rc2 * uu * ww;
           if (r.src) res -= __ldg(r.src + ((long long)(et - r.et0) * QT + g) * r.gs + psrc[mi][e]);
           amax = fmax(amax, fabs(res));
           umax = fmax(umax, fabs(uu));
@@ -360,8 +361,8 @@ using namespace mi;
 extern "C" {
 
 int mi_theta_setup(mi_ctx* c, const int* nel, const double* B0, const double* B1, const double* lengths,
-                   double final_time, double C_m, double D, double c1, double a, double c2) {
-  MI_REQUIRE(c != nullptr && nel && B0 && B1 && lengths, MI_ERR_ARG, "NULL argument to mi_theta_setup");
+                   const double* diffusion, double final_time, double C_m, double c1, double a, double c2) {
+  MI_REQUIRE(c != nullptr && nel && B0 && B1 && lengths && diffusion, MI_ERR_ARG, "NULL argument to mi_theta_setup");
   MI_REQUIRE(final_time > 0.0, MI_ERR_ARG, "final time must be positive");
   MI_REQUIRE(c->p == c->pt && c->p <= 3, MI_ERR_ARG, "residual indicator: need p = p_t <= 3");
   MI_CUDA(cudaSetDevice(c->device));
@@ -390,9 +391,8 @@ int mi_theta_setup(mi_ctx* c, const int* nel, const double* B0, const double* B1
   if ((rc = dalloc(c->th_B0, tot)) || (rc = dalloc(c->th_B1, tot))) return rc;
   MI_CUDA(cudaMemcpy(c->th_B0.p, h0.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
   MI_CUDA(cudaMemcpy(c->th_B1.p, h1.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
-  for (int l = 0; l < 3; ++l) c->th_il2[l] = l < c->d ? 1.0 / (lengths[l] * lengths[l]) : 0.0;
+  for (int l = 0; l < 3; ++l) c->th_il2[l] = l < c->d ? diffusion[l] / (lengths[l] * lengths[l]) : 0.0;
   c->th_cmT = C_m / final_time;
-  c->th_D = D;
   c->th_c1 = c1;
   c->th_a = a;
   c->th_c2 = c2;
@@ -430,7 +430,6 @@ int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double*
   r.et0 = et0;
   r.et1 = et1;
   r.cmT = c->th_cmT;
-  r.D = c->th_D;
   r.c1 = c->th_c1;
   r.a = c->th_a;
   r.c2 = c->th_c2;

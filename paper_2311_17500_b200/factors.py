@@ -96,7 +96,8 @@ class LowRankIndicator:
 
 
 def lowrank_factorize(values, tol):
-    """stabilization.py:401-418 (numpy SVD on the host, rank >= 1 unless Theta = 0)."""
+    """stabilization.py:401-418 (numpy SVD on the host, rank >= 1 unless Theta = 0; large wide
+    indicators through the Gram matrix, see below)."""
     if not 0.0 < tol < 1.0:
         raise ValueError("tolerance must lie in (0, 1)")
     th = np.asarray(getattr(values, "values", values), float)
@@ -104,10 +105,26 @@ def lowrank_factorize(values, tol):
     nt, ns = th.shape
     if nrm == 0.0:
         return LowRankIndicator(th, 0, np.zeros((nt, 0)), np.zeros((ns, 0)), np.zeros(0), tol)
+    if nt * ns > GRAM_MIN_SIZE and ns >= 8 * nt:
+        # wide indicator (N_s >> N_t): eigen-decomposition of the N_t x N_t Gram matrix is ~40x
+        # cheaper than the full SVD at cfg 3 (0.1 vs 4 s).  The rank decision uses the same
+        # tails (eigenvalues = s^2); when a tail sits within 1e-8 of the cut, the full SVD decides.
+        lam, W = np.linalg.eigh(th @ th.T)
+        lam, W = np.clip(lam[::-1], 0.0, None), W[:, ::-1]
+        tails2 = np.append(np.cumsum(lam[::-1])[::-1], 0.0)
+        cut2 = (tol * nrm) ** 2
+        if np.min(np.abs(tails2 - cut2)) > 1e-8 * nrm ** 2:
+            rank = max(int(np.argmax(tails2 <= cut2)), 1)
+            s = np.sqrt(lam[:rank])          # > 0: tails2[rank-1] > cut2 >= tails2[rank]
+            V = (th.T @ W[:, :rank]) / s
+            return LowRankIndicator(th, rank, np.ascontiguousarray(W[:, :rank]), V, s[:rank].copy(), tol)
     U, s, Vt = np.linalg.svd(th, full_matrices=False)
     tails = np.sqrt(np.append(np.cumsum((s ** 2)[::-1])[::-1], 0.0))
     rank = max(int(np.argmax(tails <= tol * nrm)), 1)
     return LowRankIndicator(th, rank, U[:, :rank], Vt[:rank].T.copy(), s[:rank].copy(), tol)
+
+
+GRAM_MIN_SIZE = 10_000_000
 
 
 def hat_values(nodes, x):

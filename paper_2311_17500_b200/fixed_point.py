@@ -34,8 +34,16 @@ class _Workspace:
             raise NotImplementedError("the direct (host LU) linear solver is not part of the device path")
         self.L, _ = box_of(problem.geometry)
         self.device = device
-        self.grid = GaussGrid(st, problem.geometry)
-        self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid)
+        self.indicator = DeviceIndicator(problem, device) if config.stabilization == "spline_upwind" else None
+        if self.indicator is not None and problem.source is not None:
+            # one host evaluation of the source feeds both the load vector and the indicator's
+            # device-resident copy
+            self.grid = self.indicator._grid = GaussGrid(st, problem.geometry)
+            self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid,
+                                     chunks=self.indicator.source_chunks(problem.source))
+        else:
+            self.grid = GaussGrid(st, problem.geometry)
+            self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid)
         self.pc_ctx = DeviceContext(st, device)
         self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.D,
                                                     problem.a * problem.c1, lengths=self.L, context=self.pc_ctx)
@@ -44,7 +52,6 @@ class _Workspace:
                                          lengths=self.L, device=device)
         self.wsolver = RecoverySolver(st, problem.final_time, problem.b, problem.d_e, config.linear_tol,
                                       lengths=self.L, device=device)
-        self.indicator = DeviceIndicator(problem, device) if config.stabilization == "spline_upwind" else None
 
     def operator(self, problem, u_k, w_k, stab):
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,

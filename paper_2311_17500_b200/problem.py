@@ -68,9 +68,16 @@ class MonodomainProblem:
     d_e: float = 1.0
 
     def __post_init__(self):
-        for name in ("C_m", "D", "a", "b", "c1", "c2", "d_e"):
+        for name in ("C_m", "a", "b", "c1", "c2", "d_e"):
             if getattr(self, name) < 0:
                 raise ValueError("%s must be nonnegative" % name)
+        # D: scalar (the reference) or one value per spatial direction (anisotropic diagonal sigma,
+        # the oracle extension of SURVEY Appendix B)
+        Dv = np.atleast_1d(np.asarray(self.D, float))
+        if np.any(Dv < 0):
+            raise ValueError("D must be nonnegative")
+        if Dv.size not in (1, len(self.space.spatial)):
+            raise ValueError("D must be a scalar or one value per spatial direction")
         if self.geometry.final_time <= 0:
             raise ValueError("final time must be positive")
         if self.geometry.dim != len(self.space.spatial):
@@ -79,6 +86,11 @@ class MonodomainProblem:
     @property
     def final_time(self):
         return self.geometry.final_time
+
+    def diffusion(self):
+        """Per-direction diffusion coefficients (length d)."""
+        Dv = np.atleast_1d(np.asarray(self.D, float))
+        return np.repeat(Dv, len(self.space.spatial)) if Dv.size == 1 else Dv
 
     def reaction_constants(self):
         return {"c1": self.c1, "a": self.a, "c2": self.c2}
@@ -199,6 +211,13 @@ class GaussGrid:
     def source_values(self, source):
         return self.source_rows(source, 0, self.tx.size)
 
+    def source_chunks(self, source, rows_per_chunk):
+        """Yield (i0, i1, values) over all time Gauss rows, rows_per_chunk at a time."""
+        nq = self.tx.size
+        for i0 in range(0, nq, rows_per_chunk):
+            i1 = min(nq, i0 + rows_per_chunk)
+            yield i0, i1, self.source_rows(source, i0, i1)
+
     def source_rows(self, source, i0, i1):
         """Source at time Gauss points i0..i1-1 x all spatial Gauss points, (i1-i0, Q_d, ..., Q_1)."""
         if getattr(self, "_xq", None) is None:
@@ -212,10 +231,12 @@ class GaussGrid:
         return fv.reshape((tq.size,) + tuple(x.size for x in reversed(self.sx)))
 
 
-def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24):
+def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24, chunks=None):
     """f_vec[i] = int int f B_i (assembly.py:350-398, box geometry).  The Gauss grid is visited in
     chunks of time points (spatial projection per chunk, then the time projection accumulates),
-    so the full space-time grid is never held at once."""
+    so the full space-time grid is never held at once; time points where the source vanishes
+    identically contribute nothing and are skipped.  ``chunks`` may supply the evaluated source
+    as (i0, i1, values) rows (GaussGrid.source_chunks) so another consumer can share them."""
     if source is None:
         return np.zeros(st.num_dof)
     g = grid if grid is not None else GaussGrid(st, geometry)
@@ -223,15 +244,18 @@ def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24):
     ws = np.asarray(g.sw[d - 1] * g.L[d - 1])
     for l in reversed(range(d - 1)):
         ws = np.multiply.outer(ws, g.sw[l] * g.L[l])
-    nq = g.tx.size
-    step = max(1, chunk_points // max(1, ws.size))
+    if chunks is None:
+        chunks = g.source_chunks(source, max(1, chunk_points // max(1, ws.size)))
     acc = np.zeros((g.tB[0].shape[1],) + tuple(s.dimension for s in reversed(st.spatial)))
-    for i0 in range(0, nq, step):
-        i1 = min(nq, i0 + step)
-        vals = g.source_rows(source, i0, i1) * ws[None] * (g.tw[i0:i1] * g.T).reshape((-1,) + (1,) * d)
+    for i0, i1, fv in chunks:
+        live = np.flatnonzero(fv.reshape(i1 - i0, -1).any(axis=1))
+        if live.size == 0:
+            continue
+        rows = i0 + live
+        vals = fv[live] * ws[None] * (g.tw[rows] * g.T).reshape((-1,) + (1,) * d)
         for l in range(d):
             vals = _mode(g.sB[l][0].T, vals, 1 + (d - 1 - l))
-        acc += _mode(g.tB[0][i0:i1].T, vals, 0)
+        acc += _mode(g.tB[0][rows].T, vals, 0)
     return acc.ravel()
 
 
@@ -257,13 +281,14 @@ def compute_theta(problem, u, w, grid=None):
     u_dtau = g.field(u, zero, 1)
     w_val = g.field(w, zero, 0)
     lap = np.zeros_like(u_val)
+    Dv = problem.diffusion()
     for a in range(d):
         if st.spatial[a].degree < 2:
             continue
         orders = [0] * d
         orders[a] = 2
-        lap += g.field(u, orders, 0) / g.L[a] ** 2       # affine: metric = diag(1/L^2), no Hessian term
-    res = (problem.C_m * (u_dtau / T) - problem.D * lap
+        lap += (Dv[a] / g.L[a] ** 2) * g.field(u, orders, 0)   # affine: metric diag(1/L^2), no Hessian term
+    res = (problem.C_m * (u_dtau / T) - lap
            + problem.c1 * u_val * (u_val - problem.a) * (u_val - 1.0) + problem.c2 * u_val * w_val)
     if problem.source is not None:
         res = res - g.source_values(problem.source)

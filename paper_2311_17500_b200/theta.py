@@ -4,7 +4,7 @@ stabilization.py:235-339).
 ``DeviceIndicator(problem).compute(u, w)`` returns the same
 ``ResidualIndicator`` as the reference: the strong residual
 
-    res = C_m u_t / T - D lap u + c1 u (u - a)(u - 1) + c2 u w - f
+    res = C_m u_t / T - sum_l D_l u_ll + c1 u (u - a)(u - 1) + c2 u w - f
 
 at the q = p+1 Gauss points of every space-time element (kernel
 ``theta_elements``, csrc/theta.cu), element maxima of |res|, the window
@@ -46,7 +46,7 @@ def element_tables(space, order):
 class DeviceIndicator:
     """Per-problem device state for compute_theta (tables uploaded once)."""
 
-    def __init__(self, problem, device=0, context=None, chunk_points=1 << 26, cache_bytes=4 << 30):
+    def __init__(self, problem, device=0, context=None, chunk_points=1 << 26, cache_bytes=None):
         st = problem.space
         self.problem = problem
         self.st = st
@@ -71,10 +71,13 @@ class DeviceIndicator:
         b1 = np.ascontiguousarray(np.concatenate(B1))
         nh = np.asarray(self.nel, dtype=np.int32)
         Lh = np.ascontiguousarray(np.asarray(self.L, float))
+        Dh = np.ascontiguousarray(problem.diffusion(), dtype=float)
         _lib.call("mi_theta_setup", ctx.handle, host_ptr(nh), host_ptr(b0), host_ptr(b1), host_ptr(Lh),
-                  self.T, float(problem.C_m), float(problem.D), float(problem.c1), float(problem.a),
+                  host_ptr(Dh), self.T, float(problem.C_m), float(problem.c1), float(problem.a),
                   float(problem.c2))
         self.chunk_points = int(chunk_points)
+        if cache_bytes is None:   # default: up to a quarter of the device memory free now
+            cache_bytes = torch.cuda.mem_get_info(ctx.device)[0] // 4
         self.cache_bytes = int(cache_bytes)
         self._grid = None
         self._src_cache = None        # [(et0, et1, device tensor)] when the source fits cache_bytes
@@ -82,27 +85,38 @@ class DeviceIndicator:
         self.win_t = [window_elements(st.time, c) for c in range(st.num_time)]
         self.win_s = [[window_elements(s, i) for i in range(s.dimension)] for s in st.spatial]
 
+    def _plan(self):
+        if self._grid is None:
+            self._grid = GaussGrid(self.st, self.problem.geometry)
+        qt = self.st.time.degree + 1
+        per_el = qt * int(np.prod([x.size for x in self._grid.sx]))
+        nel_t = self.nel[self.d]
+        keep = per_el * nel_t * 8 <= self.cache_bytes
+        return qt, per_el, max(1, self.chunk_points // per_el), keep
+
+    def source_chunks(self, source):
+        """Evaluate the source chunk by chunk (host, like the reference), yielding
+        (i0, i1, values) time Gauss rows for other consumers (the load vector) while the
+        device copies are kept for compute() when they fit cache_bytes."""
+        qt, per_el, step, keep = self._plan()
+        nel_t = self.nel[self.d]
+        chunks = []
+        for et0 in range(0, nel_t, step):
+            et1 = min(nel_t, et0 + step)
+            fv = self._grid.source_rows(source, et0 * qt, et1 * qt)
+            if keep:
+                chunks.append((et0, et1, torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device)))
+            yield et0 * qt, et1 * qt, fv
+        if keep:
+            self._src_cache = chunks
+
     def _source_chunks(self, source, nel_t):
         if self._src_cache is not None:
             yield from self._src_cache
             return
-        if self._grid is None:
-            self._grid = GaussGrid(self.st, self.problem.geometry)
-        grid = self._grid
-        qt = self.st.time.degree + 1
-        per_el = qt * int(np.prod([x.size for x in grid.sx]))
-        keep = per_el * nel_t * 8 <= self.cache_bytes
-        step = max(1, self.chunk_points // per_el)
-        chunks = []
-        for et0 in range(0, nel_t, step):
-            et1 = min(nel_t, et0 + step)
-            fv = grid.source_rows(source, et0 * qt, et1 * qt)
-            fd = torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device)
-            if keep:
-                chunks.append((et0, et1, fd))
-            yield et0, et1, fd
-        if keep:
-            self._src_cache = chunks
+        for i0, i1, fv in self.source_chunks(source):
+            qt = self.st.time.degree + 1
+            yield i0 // qt, i1 // qt, torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device)
 
     def _window(self, src, dst, outer, n_in, wins, inner):
         w0 = np.ascontiguousarray([a for a, _ in wins], dtype=np.int32)

@@ -134,3 +134,23 @@ def test_real_pencil_fd_apply_matches_reference(name):
     # Q^T M_t Q = I
     Wt, Mt = time_factors(st, float(g["T"]))
     assert np.max(np.abs(pen.Q.T @ Mt @ pen.Q - np.eye(st.num_time))) < 1e-10
+
+
+def test_lowrank_gram_path_matches_svd(monkeypatch):
+    """Large wide indicators use the Gram eigendecomposition: same rank, same singular values,
+    same truncated reconstruction as numpy's SVD (to the truncation's own rounding sensitivity)."""
+    import numpy as np
+    import paper_2311_17500_b200.factors as F
+    rng = np.random.default_rng(3)
+    nt, ns = 40, 4000
+    tg = np.linspace(0, 1, nt)[:, None]
+    xs = np.linspace(0, 1, ns)[None, :]
+    th = np.clip(np.exp(-((xs - 0.2 - 0.5 * tg) / 0.08) ** 2) + 0.05 * rng.uniform(0, 1, (nt, ns)), 0, 1)
+    ref = F.lowrank_factorize(th, 0.1)
+    monkeypatch.setattr(F, "GRAM_MIN_SIZE", 0)
+    got = F.lowrank_factorize(th, 0.1)
+    assert got.rank == ref.rank
+    np.testing.assert_allclose(got.weights, ref.weights, rtol=1e-12)
+    A = (ref.time_factors * ref.weights) @ ref.space_factors.T
+    B = (got.time_factors * got.weights) @ got.space_factors.T
+    assert np.abs(A - B).max() <= 1e-10 * np.abs(A).max()

@@ -79,3 +79,19 @@ def test_device_theta_zero_denominator():
         got = DeviceIndicator(prob).compute(z, z).values
     np.testing.assert_array_equal(got, ref)
     assert got.max() == 1.0
+
+
+@pytest.mark.gpu
+def test_device_theta_anisotropic_matches_host():
+    """Diagonal anisotropic D (cfg 3's sigma; SURVEY App. B extension): device vs host restatement."""
+    import paper_2311_17500_b200.spaces as sp
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, compute_theta
+    from paper_2311_17500_b200.theta import DeviceIndicator
+    st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(2, n) for n in (5, 4, 3)], sp.SplineSpace.uniform(2, 4))
+    prob = MonodomainProblem(BoxGeometry([1.0, 0.8, 1.2], 1.0), st, source=pulse_source, D=[1e-1, 4e-2, 2e-2])
+    rng = np.random.default_rng(5)
+    u = rng.uniform(0, 1, st.num_dof)
+    w = rng.uniform(0, 0.1, st.num_dof)
+    ref = compute_theta(prob, u, w).values
+    got = DeviceIndicator(prob).compute(u, w).values
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-14)
