@@ -547,6 +547,18 @@ def run_ours(args):
     if extras:
         line["solve"] = measure_solve(torch, mb, dev)
         line["fixed_point_cfg1"] = measure_fixed_point_cfg1(torch, mb, dev)
+        # full relaxed fixed-point solves (SU every sweep, GMRES rtol 1e-8) on BASELINE cfgs 2 and 3:
+        # BASELINE's "solve time" at 1 GPU (source-pulse stimulus stand-ins)
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("solve_cfg", os.path.join(ROOT, "tools", "solve_cfg.py"))
+        solve_cfg = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(solve_cfg)
+        for c in (2, 3):
+            try:
+                line["fixed_point_cfg%d" % c] = solve_cfg.run(c, device=dev.index)
+            except Exception as exc:   # keep the headline line even if an extra fails
+                line["fixed_point_cfg%d" % c] = {"error": repr(exc)[:300]}
+            torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sec, sample, _ = cpu_sample_rate(3, 1, SAMPLE["ne"], SAMPLE["ne_t"])
         line["cpu_baseline"] = {"value": rate, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",

@@ -124,7 +124,7 @@ def lowrank_factorize(values, tol):
     return LowRankIndicator(th, rank, U[:, :rank], Vt[:rank].T.copy(), s[:rank].copy(), tol)
 
 
-GRAM_MIN_SIZE = 10_000_000
+GRAM_MIN_SIZE = 2_000_000
 
 
 def hat_values(nodes, x):

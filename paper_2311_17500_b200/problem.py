@@ -14,12 +14,17 @@ Both are host numpy (sum factorised); the (d+1)-way solve they feed runs on
 the device.  Geometry: axis-aligned boxes (the reference's affine maps).
 """
 
+import os
 import warnings
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from .spaces import basis_table, gauss_rule, greville
+
+
+SOURCE_THREADS = max(1, min(32, os.cpu_count() or 1))   # host threads for source evaluation
 
 
 class FixedPointDiverged(RuntimeError):
@@ -226,8 +231,19 @@ class GaussGrid:
         qs = xq.shape[0]
         tq = self.tx[i0:i1] * self.T
         fv = np.empty((tq.size, qs))
-        for i, t in enumerate(tq):
-            fv[i] = np.asarray(source(xq, np.full(qs, t)), float).reshape(qs)
+
+        def row(i):
+            fv[i] = np.asarray(source(xq, np.full(qs, tq[i])), float).reshape(qs)
+
+        # one call per time point like the reference (assembly.py:380-388); numpy releases the GIL,
+        # so large grids evaluate on a thread pool (the source must be a pure function of (x, t))
+        workers = min(SOURCE_THREADS, tq.size) if qs * tq.size >= (1 << 22) else 1
+        if workers > 1:
+            with ThreadPoolExecutor(max_workers=workers) as pool:
+                list(pool.map(row, range(tq.size)))
+        else:
+            for i in range(tq.size):
+                row(i)
         return fv.reshape((tq.size,) + tuple(x.size for x in reversed(self.sx)))
 
 
