@@ -103,9 +103,12 @@ def fixed_point_solve(problem, config=None, device=0):
 
     ph.start()
     ws = _Workspace(problem, config, device)
+    # the iterate stays on the device between sweeps; only the result comes back to the host
+    dev = ws.pc_ctx.device
+    f_dev = torch.from_numpy(np.ascontiguousarray(ws.f_vec)).to(dev)
     ph.stop("setup")
-    u = np.zeros(st.num_dof)
-    w = np.zeros(st.num_dof)
+    u = torch.zeros(st.num_dof, dtype=torch.float64, device=dev)
+    w = torch.zeros_like(u)
     increments, gmres_iters, pcg_iters = [], [], []
     indicator = frozen_indicator
     alpha = config.relaxation
@@ -119,7 +122,7 @@ def fixed_point_solve(problem, config=None, device=0):
             else:
                 ph.start()
                 if config.indicator_override is not None:
-                    fresh = config.indicator_override(problem, u, w)
+                    fresh = config.indicator_override(problem, u.cpu().numpy(), w.cpu().numpy())
                 else:
                     fresh = ws.indicator.compute(u, w)
                 ph.stop("indicator")
@@ -142,7 +145,7 @@ def fixed_point_solve(problem, config=None, device=0):
         op = ws.operator(problem, u, w, stab)
         ph.stop("operator_setup")
         ph.start()
-        u_tilde, nit, _ = gmres(op, ws.f_vec, precond=ws.precond, tol=config.linear_tol)
+        u_tilde, nit, _ = gmres(op, f_dev, precond=ws.precond, tol=config.linear_tol)
         ph.stop("gmres")
         gmres_iters.append(nit)
         op.ctx.close()
@@ -158,15 +161,15 @@ def fixed_point_solve(problem, config=None, device=0):
 
         u_new = alpha * u_tilde + (1.0 - alpha) * u
         w_new = alpha * w_tilde + (1.0 - alpha) * w
-        inc = float(np.max(np.abs(u_new - u)))
+        inc = float((u_new - u).abs().max().item())
         increments.append(inc)
         if config.verbose:
             print("  sweep %3d: increment %.3e" % (k, inc))
         u, w = u_new, w_new
         if inc <= config.tolerance:
-            return SolveResult(u, w, k, increments, True, gmres_iters, pcg_iters,
+            return SolveResult(u.cpu().numpy(), w.cpu().numpy(), k, increments, True, gmres_iters, pcg_iters,
                                _time.perf_counter() - t0, indicator, ph.sec)
-    result = SolveResult(u, w, galerkin_sweeps + config.max_iterations, increments, False, gmres_iters,
-                         pcg_iters, _time.perf_counter() - t0, indicator, ph.sec)
+    result = SolveResult(u.cpu().numpy(), w.cpu().numpy(), galerkin_sweeps + config.max_iterations, increments,
+                         False, gmres_iters, pcg_iters, _time.perf_counter() - t0, indicator, ph.sec)
     raise FixedPointDiverged("fixed point did not reach %.2e in %d iterations"
                              % (config.tolerance, config.max_iterations), result)
