@@ -54,9 +54,13 @@ class _Workspace:
                                       lengths=self.L, device=device)
 
     def operator(self, problem, u_k, w_k, stab):
+        # one operator context for all sweeps: its buffers are reused (dalloc keeps large-enough
+        # allocations), so a sweep rebuilds tables, not allocations
+        if getattr(self, "op_ctx", None) is None:
+            self.op_ctx = DeviceContext(problem.space, self.device)
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
                                  problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
-                                 lengths=self.L, device=self.device)
+                                 lengths=self.L, device=self.device, context=self.op_ctx)
 
 
 def _indicator_values(ind):
@@ -148,7 +152,6 @@ def fixed_point_solve(problem, config=None, device=0):
         u_tilde, nit, _ = gmres(op, f_dev, precond=ws.precond, tol=config.linear_tol)
         ph.stop("gmres")
         gmres_iters.append(nit)
-        op.ctx.close()
 
         ph.start()
         if config.evolve_recovery:

@@ -142,6 +142,8 @@ class KroneckerOperator:
         if not zero_iterate:
             from .reaction import set_reaction
             set_reaction(ctx, st, final_time, consts, u, w, L, time_rows=self.time_rows)
+        else:
+            _lib.call("mi_op_clear_reaction", ctx.handle)    # a reused context may carry one
 
     @property
     def shape(self):
