@@ -67,7 +67,9 @@ struct RxTile {
   using B4 = RxTile;
   static constexpr int QL = D == 3 ? B4::Q1 * B4::Q2 : (D == 2 ? B4::Q1 : 1);  // lines of the last stage
   static constexpr int NT = (QL + 7) / 8;                                          // its M tiles
-  static constexpr int MT = (NT + 7) / 8;                                          // tiles per warp
+  static constexpr int NW = NT < 8 ? NT : 8;                                       // warps: one last-stage tile each
+  static constexpr int NTH = 32 * NW;
+  static constexpr int MT = (NT + NW - 1) / NW;                                    // last-stage tiles per warp
   static constexpr int ev(int n) { return (n + 1) & ~1; }                        // 16-byte aligned buffers
   static constexpr int SIN = ev(3 * B4::LS);
   static constexpr int SA = D >= 2 ? ev(3 * B4::L3 * B4::L2 * B4::Q1) : 2;
@@ -75,20 +77,21 @@ struct RxTile {
   static constexpr int SC = D >= 2 ? ev(B4::L * QL) : 2;
   static constexpr int SD = D >= 3 ? ev(B4::L3 * B4::L2 * B4::Q1) : 2;
   static constexpr int NIN = 3 * B4::LS;                                          // input items per slice
-  static constexpr int NPRE = (NIN + 255) / 256;
+  static constexpr int NPRE = (NIN + NTH - 1) / NTH;
   static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD + 64 + 256) * 8;   // + time tables + read pad
 };
 
 template <int D, int P, int PT>
-__global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
+__global__ void __launch_bounds__(RxTile<D, P>::NTH, 512 / RxTile<D, P>::NTH) reaction_tile(RxArgs r) {
   using G = RxTile<D, P>;
   constexpr int E = G::E, QE = G::QE, L = G::L, Q = G::Q;
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
   constexpr int LS = G::LS, KI = G::KI, KP = G::KP, QL = G::QL, NT = G::NT, MT = G::MT;
+  constexpr int NW = G::NW, NTH = G::NTH;
   constexpr int PW = PT + 1, QT = PT + 1;
   constexpr int NBT = 2 * QT * PW;                  // time basis (interpolation) + weighted (projection)
   constexpr int NLX = L3 * L2;                      // x-projection lines (j3, j2)
-  static_assert(NBT <= 32 && (NLX + 7) / 8 <= 8, "reaction tile too large");
+  static_assert(NBT <= 32 && (NLX + 7) / 8 <= NW, "reaction tile too large");
   static_assert(Q1 % 2 == 0, "paired stores need an even Gauss count");
   extern __shared__ double sm[];
   double* sIn = sm;                // [fld][j3][j2][j1]
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
   const int fr = lane >> 2, fk = lane & 3;
   // A-fragment loads run unpredicated over padded rows / k columns: whatever they read is finite
   // (the buffers start zeroed) and meets a zero B entry or lands in a discarded output row
-  for (int i = tid; i < (int)(G::SMEM / 8); i += 256) sm[i] = 0.0;
+  for (int i = tid; i < (int)(G::SMEM / 8); i += NTH) sm[i] = 0.0;
   int b = blockIdx.x, k[3], ne[3];
   for (int l = 0; l < 3; ++l) {
     const int m = b % r.ncol[l];
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
   for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int line = 8 * (warp + 8 * mi) + fr, ql = 2 * fk + e;
+      const int line = 8 * (warp + NW * mi) + fr, ql = 2 * fk + e;
       double v = 0.0;
       if (line < QL && ql < Q) {
         v = wgt(D - 1, ql);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
   long long gsp[G::NPRE];
 #pragma unroll
   for (int m = 0; m < G::NPRE; ++m) {
-    const int i = tid + 256 * m;
+    const int i = tid + NTH * m;
     const int s = i % LS;
     bool ok;
     const long long gs = spatial(s / (L1 * L2), (s / L1) % L2, s % L1, ok);
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
     const bool vt = ct >= 0 && ct < r.ntc;
 #pragma unroll
     for (int m = 0; m < G::NPRE; ++m) {
-      const int f = (tid + 256 * m) / LS;
+      const int f = (tid + NTH * m) / LS;
       const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
       pre[m] = (vt && gsp[m] >= 0) ? __ldg(src + (long long)ct * ns + gsp[m]) : 0.0;
     }
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
     if (has_in) {
 #pragma unroll
       for (int m = 0; m < G::NPRE; ++m)
-        if (tid + 256 * m < G::NIN) sIn[tid + 256 * m] = pre[m];
+        if (tid + NTH * m < G::NIN) sIn[tid + NTH * m] = pre[m];
     }
     if (tid < NBT) sBt[(j & 1) * 32 + tid] = btp;
     if constexpr (D >= 2) {
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
       // phase 2: x interpolation of slice j: lines (fld, j3, j2), K = j1, N = q1 -> sA [fld][j3][j2][q1]
       if (has_in) {
         constexpr int NL = 3 * L3 * L2;
-        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+        for (int mt = warp; mt < (NL + 7) / 8; mt += NW) {
           const int line = mt * 8 + fr;
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
       if (has_fp) {
         if constexpr (D == 3) {
           constexpr int NL = L3 * Q1;
-          for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+          for (int mt = warp; mt < (NL + 7) / 8; mt += NW) {
             const int line = mt * 8 + fr;
             const int q1 = line % Q1, j3 = line / Q1;
             double c0 = 0.0, c1 = 0.0;
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
       // phase 3: y interpolation of slice j: lines (fld, j3, q1), K = j2, N = q2 -> sB [fld][j3][q2][q1]
       if (has_in) {
         constexpr int NL = 3 * L3 * Q1;
-        for (int mt = warp; mt < (NL + 7) / 8; mt += 8) {
+        for (int mt = warp; mt < (NL + 7) / 8; mt += NW) {
           const int line = mt * 8 + fr;
           const int q1 = line % Q1, fj3 = line / Q1;
           double c0 = 0.0, c1 = 0.0;
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
     if (has_in) {
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi) {
-        const int t = warp + 8 * mi;
+        const int t = warp + NW * mi;
         if (t < NT) {
           const int line = 8 * t + fr;
 #pragma unroll
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(256, 2) reaction_tile(RxArgs r) {
     // ... and the last-direction projection of the completed function et (quad shuffles -> A fragments)
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi) {
-      const int t = warp + 8 * mi;
+      const int t = warp + NW * mi;
       if (t < NT) {                                  // warp-uniform
         const int line = 8 * t + fr;
         double c0 = 0.0, c1 = 0.0;
@@ -472,7 +475,7 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
         nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
       }
       if (nb == 0) continue;
-      reaction_tile<D_, P_, PT_><<<(unsigned)nb, 256, smem, c->stream>>>(r);
+      reaction_tile<D_, P_, PT_><<<(unsigned)nb, G::NTH, smem, c->stream>>>(r);
       MI_CHECK_LAUNCH("reaction_tile");
     }
   });
