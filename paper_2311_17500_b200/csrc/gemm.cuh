@@ -231,7 +231,8 @@ inline cudaError_t launch_panel_n(const GemmArgs& g, int n, int batch, cudaStrea
   if (t <= 9) return launch_panel<9, ALONG_N>(g, batch, st);
   if (t <= 13) return launch_panel<13, ALONG_N>(g, batch, st);
   if (t <= 17) return launch_panel<17, ALONG_N>(g, batch, st);
-  return launch_dgemm(g, batch, st);   // larger n (the time transforms): generic 64x64 tiles measured faster
+  if (t <= 26) return launch_panel<13, ALONG_N>(g, batch, st);   // two row (column) blocks of 104
+  return launch_dgemm(g, batch, st);
 }
 
 }  // namespace mi
