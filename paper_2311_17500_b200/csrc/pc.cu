@@ -11,6 +11,7 @@
 // reference materialises H_int as an (N_t-1) x N_s complex array).
 #include "common.cuh"
 #include "gemm.cuh"
+#include "mode_resident.cuh"
 
 namespace mi {
 
@@ -63,9 +64,22 @@ __global__ void arrowhead_solve(double* __restrict__ Y, const double* __restrict
   Y[(long long)m * ns + s] = xl;
 }
 
+static int num_sms() {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  return nsm;
+}
+
 static cudaError_t mode_strided(const double* A, const double* in, double* out, int n, long long inner,
                                 long long outer, cudaStream_t st) {
   // out[o, i, c] = sum_j A[i, j] in[o, j, c]
+  cudaError_t err;
+  if (launch_mode_resident<false>(A, in, out, n, inner, outer, num_sms(), st, &err)) return err;
   GemmArgs g{A, in, out, n, (int)inner, n, n, inner, inner, 0, (long long)n * inner, (long long)n * inner};
   return launch_panel_n<true>(g, n, (int)outer, st);
 }
@@ -73,6 +87,8 @@ static cudaError_t mode_strided(const double* A, const double* in, double* out, 
 static cudaError_t mode_contig(const double* Bm, const double* in, double* out, int n, long long rows,
                                cudaStream_t st) {
   // out[r, i] = sum_j in[r, j] Bm[j, i]
+  cudaError_t err;
+  if (launch_mode_resident<true>(Bm, in, out, n, 0, rows, num_sms(), st, &err)) return err;
   GemmArgs g{in, Bm, out, (int)rows, n, n, n, n, n, 0, 0, 0};
   return launch_panel_n<false>(g, n, 1, st);
 }
