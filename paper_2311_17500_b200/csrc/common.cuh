@@ -78,6 +78,7 @@ struct mi_ctx {
   mi::DeviceBuf frag;           // fragment-major coefficients for the DMMA path
   mi::DeviceBuf xt;             // time-innermost copy of the operator input
   CUtensorMap tmap_xt;          // TMA descriptor of xt (DMMA path)
+  CUtensorMap tmap_w;           // TMA descriptor of wbuf as (nchan*ns) rows x ntp times (time filter)
   mi::DeviceBuf afr;            // time-filter A fragments (DMMA path)
   int ntau = 0;
   bool op_ready = false;

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "dispatch.cuh"
 #include "stencil_dmma.cuh"
+#include "tfilter.cuh"
 
 typedef CUresult (*mi_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -314,6 +315,22 @@ static int dmma_prepare(mi_ctx* c) {
     }
     if ((rc = dalloc(c->wbuf, (size_t)c->nchan * c->ns * ntp))) return rc;
     MI_CUDA(cudaMemsetAsync(c->wbuf.p, 0, sizeof(double) * c->nchan * c->ns * ntp, c->stream));
+    {
+      // TMA descriptor of W for the tensor-core time filter: 2D (ntp times, nchan*ns rows), box 16 x 64,
+      // 128-byte swizzle (conflict-free B-fragment reads)
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      MI_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      MI_REQUIRE(fn != nullptr && q == cudaDriverEntryPointSuccess, MI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      cuuint64_t dims[2] = {(cuuint64_t)ntp, (cuuint64_t)c->nchan * c->ns};
+      cuuint64_t strides[1] = {(cuuint64_t)ntp * 8};
+      cuuint32_t box[2] = {16, (cuuint32_t)TFilterCfg::NP};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = ((mi_encode_tiled_fn)fn)(&c->tmap_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->wbuf.p, dims, strides,
+                                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      MI_REQUIRE(r == CUDA_SUCCESS, MI_ERR_CUDA, "cuTensorMapEncodeTiled (W) failed");
+    }
     MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)G::SMEM));
   });
@@ -325,6 +342,37 @@ static int dmma_prepare(mi_ctx* c) {
 // y = sum_c T_c (x) along time of the time-innermost W buffer (HBM-bound)
 static int launch_time_filter(mi_ctx* c, double* y) {
   MI_REQUIRE(c->nchan <= 64, MI_ERR_ARG, "too many channels for the time filter");
+  if (TFilterCfg::smem(c->pt, c->nchan) <= 232448 && c->pt <= TFilterCfg::PX) {
+    // tensor-core filter: persistent blocks, one time block of 56 rows each
+    static int nsm = 0;
+    if (nsm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      if (nsm <= 0) nsm = 148;
+    }
+    const int ntb = (c->nt + TFilterCfg::TR - 1) / TFilterCfg::TR;
+    const int grid = ntb * std::max(1, nsm / ntb);
+    const size_t sm = TFilterCfg::smem(c->pt, c->nchan);
+#define MI_TFD(PTV)                                                                                            \
+  case PTV: {                                                                                                  \
+    static bool attr = false;                                                                                  \
+    if (!attr) {                                                                                               \
+      MI_CUDA(cudaFuncSetAttribute(time_filter_dmma<PTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448)); \
+      attr = true;                                                                                             \
+    }                                                                                                          \
+    time_filter_dmma<PTV><<<grid, 256, sm, c->stream>>>(c->tmap_w, c->tband.p, y, c->nchan, c->nt, c->ns, ntb, 0); \
+  } break;
+    switch (c->pt) {
+      MI_TFD(1) MI_TFD(2) MI_TFD(3) MI_TFD(4)
+      default:
+        set_error("time degree > 4");
+        return MI_ERR_ARG;
+    }
+#undef MI_TFD
+    MI_CHECK_LAUNCH("time_filter_dmma");
+    return MI_OK;
+  }
   dim3 fg((unsigned)((c->ns + 127) / 128), (c->nt + 15) / 16);
   const int ntp = ((c->nt + 15) / 16) * 16;
   const size_t fsm = (size_t)c->nchan * 16 * (2 * c->pt + 1) * sizeof(double);

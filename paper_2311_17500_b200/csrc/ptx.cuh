@@ -55,4 +55,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, void* b
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, void* bar, int c0, int c1) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(d),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(b)
+      : "memory");
+}
+
 }  // namespace mi
