@@ -34,6 +34,10 @@ __device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(void* bar) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(s) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
   unsigned s = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(

@@ -24,7 +24,7 @@ struct TFilterCfg {
   static constexpr int NP = 64;                      // points per tile
   static constexpr int NST = 6;                      // pipeline stages
   static constexpr int STAGE = NP * TW;              // doubles per stage (4 boxes of 16 x 64)
-  static size_t smem(int pt, int nchan) { return 1024 + (size_t)NST * STAGE * 8 + (size_t)nchan * TR * (2 * pt + 1) * 8 + 64; }
+  static size_t smem(int pt, int nchan) { return 1024 + (size_t)NST * STAGE * 8 + (size_t)nchan * TR * (2 * pt + 1) * 8 + 128; }
 };
 
 template <int PT>
@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(256, 1) time_filter_dmma(const __grid_constant
   // 1024-byte aligned stage buffers (128-byte swizzle atoms)
   double* stages = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   double* bands = stages + F::NST * F::STAGE;                      // [nchan][TR][BW]
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bands + nchan * F::TR * BW);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bands + nchan * F::TR * BW);   // full[NST]
+  unsigned long long* empty = bars + F::NST;                                                        // empty[NST]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, fk = lane & 3;
   const int tb = blockIdx.x % ntb;
@@ -52,7 +53,10 @@ __global__ void __launch_bounds__(256, 1) time_filter_dmma(const __grid_constant
     bands[e] = t < nt ? band[((long long)c * nt + t) * BW + k] : 0.0;
   }
   if (tid == 0) {
-    for (int s = 0; s < F::NST; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < F::NST; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&empty[s], 8);                       // one arrival per warp when it is done with the stage
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -88,9 +92,14 @@ __global__ void __launch_bounds__(256, 1) time_filter_dmma(const __grid_constant
   double acc[F::MT][2];
 #pragma unroll
   for (int m = 0; m < F::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+  const bool pair = (ns & 1) == 0;                      // y rows 16-byte aligned at even points
   for (long long s = 0; s < nsteps; ++s) {
-    __syncthreads();                                    // stage (s - 1) % NST is free again
-    if (tid == 0 && s + F::NST - 1 < nsteps) issue(s + F::NST - 1);
+    if (tid == 0 && s + F::NST - 1 < nsteps) {
+      // refill the stage step s - 1 used, once all 8 warps have released it
+      const long long f = s + F::NST - 1;
+      if (f >= F::NST) mbar_wait(&empty[f % F::NST], (unsigned)(((f / F::NST) - 1) & 1));
+      issue(f);
+    }
     mbar_wait(&bars[s % F::NST], (unsigned)((s / F::NST) & 1));
     const int c = (int)(s % nchan);
     const unsigned char* st = reinterpret_cast<const unsigned char*>(stages + (s % F::NST) * F::STAGE);
@@ -106,6 +115,8 @@ __global__ void __launch_bounds__(256, 1) time_filter_dmma(const __grid_constant
         dmma(acc[m][0], acc[m][1], av, bv);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s % F::NST]);
     if (c == nchan - 1) {
       const long long p = p_first + (s / nchan) * p_step;
       const long long i0 = p * F::NP + 8 * warp + 2 * fk;
@@ -113,12 +124,15 @@ __global__ void __launch_bounds__(256, 1) time_filter_dmma(const __grid_constant
       for (int m = 0; m < F::MT; ++m) {
         const int t = t0 + 8 * m + gq;
         if (t < nt) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            if (i0 + e < ns) {
-              double* dst = y + (long long)t * ns + i0 + e;
-              *dst = accumulate ? *dst + acc[m][e] : acc[m][e];
-            }
+          double* dst = y + (long long)t * ns + i0;
+          if (accumulate) {
+            if (i0 < ns) dst[0] += acc[m][0];
+            if (i0 + 1 < ns) dst[1] += acc[m][1];
+          } else if (pair && i0 + 1 < ns) {
+            *reinterpret_cast<double2*>(dst) = make_double2(acc[m][0], acc[m][1]);
+          } else {
+            if (i0 < ns) dst[0] = acc[m][0];
+            if (i0 + 1 < ns) dst[1] = acc[m][1];
           }
         }
         acc[m][0] = acc[m][1] = 0.0;
