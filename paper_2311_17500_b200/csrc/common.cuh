@@ -104,6 +104,8 @@ struct mi_ctx {
   int* pen_partner = nullptr;   // (nt-1)
   double pen_sigma = 0, pc_cm = 1, pc_react = 0;
   mi::DeviceBuf pc_t1, pc_t2, pc_t3;   // N each
+  mi::DeviceBuf tq_frag;        // fused time stage: Q^T and Q as fragment-major DMMA A operands
+  int tq_mb = 0, tq_ksp = 0;    // row blocks (8 rows) and padded k-steps of the fused time stage (0 = unfused)
 
   // ---- recovery-variable solve (w-solve)
   bool ws_ready = false;

@@ -12,6 +12,11 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "mode_resident.cuh"
+#include "tstage.cuh"
+
+#ifndef MI_TSTAGE
+#define MI_TSTAGE 1   // fused time stage (tstage.cuh); 0 = separate Q^T / arrowhead / Q passes
+#endif
 
 namespace mi {
 
@@ -146,6 +151,14 @@ int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double
   MI_CUDA(cudaMemcpy(c->pen_glow.p, glow, sizeof(double) * m, cudaMemcpyHostToDevice));
   if (!c->pen_partner) MI_CUDA(cudaMalloc(&c->pen_partner, sizeof(int) * m));
   MI_CUDA(cudaMemcpy(c->pen_partner, partner, sizeof(int) * m, cudaMemcpyHostToDevice));
+  c->tq_mb = MI_TSTAGE ? tstage_mb(nt) : 0;
+  if (c->tq_mb > 0) {
+    c->tq_ksp = 2 * (((nt + 3) / 4 + 1) / 2);
+    std::vector<double> f;
+    build_tstage_frags(Q, nt, c->tq_mb, c->tq_ksp, f);
+    if ((rc = dalloc(c->tq_frag, f.size()))) return rc;
+    MI_CUDA(cudaMemcpy(c->tq_frag.p, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice));
+  }
   c->pen_sigma = sigma;
   c->pc_cm = cm;
   c->pc_react = react;
@@ -198,6 +211,14 @@ static int pc_spatial(mi_ctx* c, const double* in, double* out, long long nrows,
 static int pc_time(mi_ctx* c, double* y, long long ncols, long long col0) {
   cudaStream_t st = c->stream;
   const int nt = c->nt;
+  if (c->tq_mb > 0) {
+    ProfScope ps(c, PROF_PC_TIME);
+    TStageArgs a{y, c->tq_frag.p, c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p,
+                 c->pen_g.p, c->pen_glow.p, c->pen_partner, c->pen_sigma, c->pc_cm, c->pc_react, c->n[0], c->n[1],
+                 nt, c->tq_ksp, ncols, col0};
+    MI_CUDA(launch_tstage(c->tq_mb, a, st));
+    return MI_OK;
+  }
   double* t = c->pc_t2.p;
   {
     ProfScope ps(c, PROF_PC_TIME);

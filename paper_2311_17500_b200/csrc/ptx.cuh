@@ -68,4 +68,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, void* b
       : "memory");
 }
 
+// 1D bulk copy global -> shared (TMA engine), completion via mbarrier transaction bytes
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+// arrive on an mbarrier when all of this thread's prior cp.async copies have landed (count not incremented)
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(void* bar) {
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(b) : "memory");
+}
+
 }  // namespace mi

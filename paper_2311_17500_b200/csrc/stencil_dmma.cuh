@@ -98,7 +98,7 @@ __global__ void transpose_time_inner(const double* __restrict__ x, double* __res
 // One warp's K-half of the DMMA sweep over a time chunk: per k-step two
 // immediate-offset LDS.64 (lane kl reads x-offset 4q+kl: conflict-free) and
 // two DMMAs; no per-step address arithmetic, no branches.
-template <class G, int HALF>
+template <class G, int HALF, int MTV>
 __device__ __forceinline__ void dmma_sweep(const double* X, int kl, const double (&breg)[G::KH],
                                            double (&acc)[G::MT][2]) {
   const bool ge1 = kl >= 1, ge2 = kl >= 2, ge3 = kl >= 3;
@@ -112,7 +112,7 @@ __device__ __forceinline__ void dmma_sweep(const double* X, int kl, const double
       const bool past = ct == 1 ? ge1 : (ct == 2 ? ge2 : (ct == 3 ? ge3 : false));
       const double* xa = X + (G::offs(4 * ks) + (past ? G::jump(ks) : 0)) * G::TSTR;
 #pragma unroll
-      for (int m = 0; m < G::MT; ++m) dmma(acc[m][0], acc[m][1], xa[m * 8], breg[j]);
+      for (int m = 0; m < MTV; ++m) dmma(acc[m][0], acc[m][1], xa[m * 8], breg[j]);
     }
   }
 }
@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
     *reinterpret_cast<double2*>(a.wout + ((long long)(a.c0 + c) * a.ns + gi) * a.ntp + t) = v;
   };
 
+
   const int base = ((pt / (G::B1 * G::B2)) * G::H2 + (pt / G::B1) % G::B2) * G::H1 + pt % G::B1;
   const int kl = lane & 3, mrow = lane >> 2;
   double* wmine = Wp + (half * 8 + pt) * G::PSTR + 2 * kl * G::WL;   // channels 2kl, 2kl+1
@@ -198,10 +199,18 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
       for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
       if (t0 < a.nt) {
         const double* X = Xs + (ch & 1) * G::HS * G::TSTR + (base + kl) * G::TSTR + mrow;
-        if (half == 0)
-          dmma_sweep<G, 0>(X, kl, breg, acc);
-        else
-          dmma_sweep<G, 1>(X, kl, breg, acc);
+        // the last chunk skips M-tiles that lie wholly past nt (warp-uniform)
+        if (t0 + 8 * (G::MT - 1) < a.nt) {
+          if (half == 0)
+            dmma_sweep<G, 0, G::MT>(X, kl, breg, acc);
+          else
+            dmma_sweep<G, 1, G::MT>(X, kl, breg, acc);
+        } else {
+          if (half == 0)
+            dmma_sweep<G, 0, 1>(X, kl, breg, acc);
+          else
+            dmma_sweep<G, 1, 1>(X, kl, breg, acc);
+        }
       }
 #pragma unroll
       for (int m = 0; m < G::MT; ++m) {

@@ -20,3 +20,15 @@ torch.cuda.synchronize(); e0, e1 = torch.cuda.Event(enable_timing=True), torch.c
 e0.record()
 for _ in range(5): op.apply_device(x, y)
 e1.record(); torch.cuda.synchronize(); print(lib, "apply A ms", e0.elapsed_time(e1) / 5)
+P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1e-3, RM["a"] * RM["c1"], context=op.ctx)
+z = torch.empty_like(x)
+for _ in range(3): P.apply_device(y, z)
+torch.cuda.synchronize(); e0.record()
+for _ in range(5): P.apply_device(y, z)
+e1.record(); torch.cuda.synchronize(); print(lib, "P^-1 ms", e0.elapsed_time(e1) / 5, "checksum", float(z.double().norm()))
+op.ctx.read_profile(reset=True); op.ctx.profiling(True)
+for _ in range(5):
+    op.apply_device(x, y); P.apply_device(y, z)
+torch.cuda.synchronize()
+prof = op.ctx.read_profile(reset=True); op.ctx.profiling(False)
+print(lib, "kernels ms/apply", {k: round(v[0] / 5, 3) for k, v in prof.items() if v[1]})
