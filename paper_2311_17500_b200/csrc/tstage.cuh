@@ -27,6 +27,10 @@
 
 #include "ptx.cuh"
 
+#ifndef MI_TS_WM
+#define MI_TS_WM 4
+#endif
+
 namespace mi {
 
 struct TStageArgs {
@@ -40,30 +44,31 @@ struct TStageArgs {
   long long ncols, col0;
 };
 
-template <int MB, int NC>
+template <int MB, int NC, int WM>
 struct TStage {
   static constexpr int KC = 2;                      // k-steps per ring stage (= 8 tile rows)
   static constexpr int NST = 4;                     // ring stages
   static constexpr int NP = NC / 16;                // column pairs of 8-column blocks
-  static constexpr int MH = (MB + 1) / 2;           // row blocks per warp (rows split in two halves)
-  static constexpr int WARPS = 2 * NP;
-  static constexpr int THREADS = 32 * WARPS;        // = 4 NC: the arrowhead uses 4 row groups x NC columns
+  static constexpr int MH = (MB + WM - 1) / WM;     // row blocks per warp (rows split in WM groups)
+  static constexpr int WARPS = WM * NP;
+  static constexpr int THREADS = 32 * WARPS;        // = 2 WM NC: the arrowhead uses 2 WM row groups x NC columns
+  static constexpr int RG = 2 * WM;
   static constexpr int LD = NC + 4;                 // = 4 (mod 16) doubles: conflict-free B fragment reads
   static constexpr int ROWS = 8 * MB;
   static constexpr int RCH = MB;                    // 8-row load chunks
   static constexpr int STAGE = KC * MB * 32;        // doubles per ring stage
-  static constexpr size_t SMEM = ((size_t)ROWS * LD + (size_t)NST * STAGE + 8 * NC) * 8 +
+  static constexpr size_t SMEM = ((size_t)ROWS * LD + (size_t)NST * STAGE + 2 * RG * NC) * 8 +
                                  (size_t)(2 * NST + RCH) * 8;
 };
 
-template <int MB, int NC>
-__global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(TStageArgs a) {
-  using G = TStage<MB, NC>;
+template <int MB, int NC, int WM>
+__global__ void __launch_bounds__(TStage<MB, NC, WM>::THREADS, 1) time_stage_fused(TStageArgs a) {
+  using G = TStage<MB, NC, WM>;
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                                 // [NST][KC][MB][32]   (16-byte aligned for the bulk copies)
   double* Ys = ring + G::NST * G::STAGE;             // [ROWS][LD]
-  double* red = Ys + G::ROWS * G::LD;                // [2][4][NC] border-sum partials
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(red + 8 * NC);
+  double* red = Ys + G::ROWS * G::LD;                // [2][RG][NC] border-sum partials
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(red + 2 * G::RG * NC);
   unsigned long long* empty = full + G::NST;
   unsigned long long* ybar = empty + G::NST;         // [RCH]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(T
   }
 
   const int h = warp / G::NP, q = warp % G::NP;
-  const bool full_h = h == 0 || 2 * G::MH == MB;     // the second half has MH-1 row blocks when MB is odd
+  const int nmine = min(G::MH, MB - h * G::MH);     // row blocks of this warp's group (the last may be short)
   double acc[G::MH][2][2];
 
   // one product: acc = A * Ys over ring chunks [f0, f0 + nchk)
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(T
         const double b0 = bp[row * G::LD], b1 = bp[row * G::LD + 8];
 #pragma unroll
         for (int i = 0; i < G::MH; ++i) {
-          if (i < G::MH - 1 || full_h) {
+          if (i < nmine) {
             const double av = st[(kk * MB + i) * 32];
             dmma(acc[i][0][0], acc[i][0][1], av, b0);
             dmma(acc[i][1][0], acc[i][1][1], av, b1);
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(T
   __syncthreads();                                   // every warp has finished reading Ys
 #pragma unroll
   for (int i = 0; i < G::MH; ++i) {
-    if (i < G::MH - 1 || full_h) {
+    if (i < nmine) {
       double* d = Ys + (8 * (h * G::MH + i) + gq) * G::LD + 16 * q + 2 * t4;
       d[0] = acc[i][0][0];
       d[1] = acc[i][0][1];
@@ -156,14 +161,14 @@ __global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(T
   // interior 2x2 blocks [[a, b], [c, e]] = C_m T_block + mu I, border column C_m g,
   // border row C_m glow, corner C_m sigma + mu.  Thread = (column c, row group rg).
   {
-    const int c = tid % NC, rg = tid / NC;           // 4 row groups
+    const int c = tid % NC, rg = tid / NC;           // RG row groups
     const long long sg = a.col0 + c0 + c;
     const int i1 = (int)(sg % a.n1), i2 = (int)((sg / a.n1) % a.n2), i3 = (int)(sg / ((long long)a.n1 * a.n2));
     const double mu = a.react + __ldg(a.lam1 + i1) + __ldg(a.lam2 + i2) + __ldg(a.lam3 + i3);
     const double cm = a.cm;
     const int m = nt - 1;
     double sy = 0.0, sb = 0.0;
-    for (int i = rg; i < m; i += 4) {
+    for (int i = rg; i < m; i += G::RG) {
       const int j = __ldg(a.partner + i);
       const double di = fma(cm, __ldg(a.diag + i), mu), dj = fma(cm, __ldg(a.diag + j), mu);
       const double b = cm * __ldg(a.off + i), cc = cm * __ldg(a.off + j);
@@ -174,14 +179,18 @@ __global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(T
       sb = fma(gli, cm * (dj * __ldg(a.gb + i) - b * __ldg(a.gb + j)) * inv, sb);
     }
     red[rg * NC + c] = sy;
-    red[(4 + rg) * NC + c] = sb;
+    red[(G::RG + rg) * NC + c] = sb;
     __syncthreads();
-    const double syt = red[c] + red[NC + c] + red[2 * NC + c] + red[3 * NC + c];
-    const double sbt = red[4 * NC + c] + red[5 * NC + c] + red[6 * NC + c] + red[7 * NC + c];
+    double syt = 0.0, sbt = 0.0;
+#pragma unroll
+    for (int g = 0; g < G::RG; ++g) {
+      syt += red[g * NC + c];
+      sbt += red[(G::RG + g) * NC + c];
+    }
     const double xl = (Ys[m * G::LD + c] - cm * syt) / (fma(cm, a.sigma, mu) - cm * sbt);
     __syncthreads();                                 // all reads of the pre-solve row m are done
     // second sweep: rows of a 2x2 block are written together by the thread of the smaller index
-    for (int i = rg; i < m; i += 4) {
+    for (int i = rg; i < m; i += G::RG) {
       const int j = __ldg(a.partner + i);
       if (j < i) continue;
       const double di = fma(cm, __ldg(a.diag + i), mu), dj = fma(cm, __ldg(a.diag + j), mu);
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(TStage<MB, NC>::THREADS, 1) time_stage_fused(T
 #pragma unroll
   for (int i = 0; i < G::MH; ++i) {
     const int r = 8 * (h * G::MH + i) + gq;
-    if ((i < G::MH - 1 || full_h) && r < nt) {
+    if (i < nmine && r < nt) {
 #pragma unroll
       for (int n = 0; n < 2; ++n) {
         const long long col = c0 + 16 * q + 8 * n + 2 * t4;
@@ -236,33 +245,33 @@ inline int tstage_mb(int nt) {
   return 0;
 }
 
-template <int MB, int NC>
+template <int MB, int NC, int WM>
 inline cudaError_t launch_tstage_t(const TStageArgs& a, cudaStream_t st) {
-  using G = TStage<MB, NC>;
+  using G = TStage<MB, NC, WM>;
   static_assert(G::SMEM <= 232448, "tile does not fit in shared memory");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(time_stage_fused<MB, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(time_stage_fused<MB, NC, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)G::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const long long nb = (a.ncols + NC - 1) / NC;
-  time_stage_fused<MB, NC><<<(unsigned)nb, G::THREADS, G::SMEM, st>>>(a);
+  time_stage_fused<MB, NC, WM><<<(unsigned)nb, G::THREADS, G::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
 // Column-tile width per MB: the widest multiple of 16 whose tile + ring fit in shared memory.
 inline cudaError_t launch_tstage(int mb, const TStageArgs& a, cudaStream_t st) {
   switch (mb) {
-    case 4: return launch_tstage_t<4, 160>(a, st);
-    case 8: return launch_tstage_t<8, 160>(a, st);
-    case 13: return launch_tstage_t<13, 160>(a, st);
-    case 17: return launch_tstage_t<17, 160>(a, st);
-    case 25: return launch_tstage_t<25, 96>(a, st);
-    case 33: return launch_tstage_t<33, 64>(a, st);
-    case 41: return launch_tstage_t<41, 48>(a, st);
-    case 49: return launch_tstage_t<49, 32>(a, st);
+    case 4: return launch_tstage_t<4, 160, 2>(a, st);
+    case 8: return launch_tstage_t<8, 160, 2>(a, st);
+    case 13: return launch_tstage_t<13, 160, 2>(a, st);
+    case 17: return launch_tstage_t<17, 160, 2>(a, st);
+    case 25: return launch_tstage_t<25, 96, MI_TS_WM>(a, st);
+    case 33: return launch_tstage_t<33, 64, 2>(a, st);
+    case 41: return launch_tstage_t<41, 48, 2>(a, st);
+    case 49: return launch_tstage_t<49, 32, 2>(a, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -10,7 +10,9 @@ sys.argv = [sys.argv[0]]
 import paper_2311_17500_b200 as mb
 from bench import RM, front_indicator_np
 from paper_2311_17500_b200.spaces import greville
-st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(3, 96) for _ in range(3)], mb.SplineSpace.uniform(3, 192))
+NE, NET = int(os.environ.get('NE', 96)), int(os.environ.get('NET', 192))
+DD, PP = int(os.environ.get('D', 3)), int(os.environ.get('P', 3))
+st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(PP, NE) for _ in range(DD)], mb.SplineSpace.uniform(PP, NET))
 theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
 stab = mb.Stabilization(st, theta, 0.1, 1.0)
 op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, stabilization=stab)
