@@ -26,13 +26,14 @@ All (d+1)-way tensor work runs in ``lib/libmonoiga_b200.so`` (C ABI in
 
 from .errors import (ConsistencyError, DecompositionError, ExtensionError, NonConvergenceError,
                      StabilizationError)
-from .problem import (BoxGeometry, FixedPointConfig, FixedPointDiverged, MonodomainProblem, ResidualIndicator,
+from .problem import (BoxGeometry, DeviceSource, FixedPointConfig, FixedPointDiverged, MonodomainProblem, ResidualIndicator,
                       SolveResult, compute_theta)
 from .spaces import SpaceTimeSpace, SplineSpace
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "DeviceSource",
     "SplineSpace", "SpaceTimeSpace", "KroneckerOperator", "FastDiagPreconditioner", "Stabilization",
     "gmres", "DeviceContext", "ConsistencyError", "DecompositionError", "ExtensionError",
     "NonConvergenceError", "StabilizationError", "BoxGeometry", "FixedPointConfig", "FixedPointDiverged",

@@ -43,7 +43,7 @@ class _Workspace:
                                      chunks=self.indicator.source_chunks(problem.source))
         else:
             self.grid = GaussGrid(st, problem.geometry)
-            self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid)
+            self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid, device=device)
         self.pc_ctx = DeviceContext(st, device)
         self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.D,
                                                     problem.a * problem.c1, lengths=self.L, context=self.pc_ctx)
@@ -109,7 +109,8 @@ def fixed_point_solve(problem, config=None, device=0):
     ws = _Workspace(problem, config, device)
     # the iterate stays on the device between sweeps; only the result comes back to the host
     dev = ws.pc_ctx.device
-    f_dev = torch.from_numpy(np.ascontiguousarray(ws.f_vec)).to(dev)
+    f_dev = (ws.f_vec.to(dev) if torch.is_tensor(ws.f_vec)
+             else torch.from_numpy(np.ascontiguousarray(ws.f_vec)).to(dev))
     ph.stop("setup")
     u = torch.zeros(st.num_dof, dtype=torch.float64, device=dev)
     w = torch.zeros_like(u)

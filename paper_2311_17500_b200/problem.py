@@ -27,6 +27,26 @@ from .spaces import basis_table, gauss_rule, greville
 SOURCE_THREADS = max(1, min(32, os.cpu_count() or 1))   # host threads for source evaluation
 
 
+class DeviceSource:
+    """A source term f(x, t) with a device implementation.
+
+    Called like the reference's source callable (numpy points (Q, d) and times (Q,) -> (Q,)), so
+    the reference and the oracle see the same function.  ``torch`` is the same function on torch
+    tensors; when present, the Gauss-point values that feed the load vector and the residual
+    indicator are evaluated and contracted on the GPU instead of on the host."""
+
+    def __init__(self, host, torch):
+        self.host = host
+        self.torch = torch
+
+    def __call__(self, x, t):
+        return self.host(x, t)
+
+
+def device_capable(source):
+    return source is not None and callable(getattr(source, "torch", None))
+
+
 class FixedPointDiverged(RuntimeError):
     """Fixed-point iteration exhausted its budget; carries the last state."""
 
@@ -176,6 +196,10 @@ class ResidualIndicator:
 # --------------------------------------------------------------------------
 
 def _mode(A, X, axis):
+    if not isinstance(X, np.ndarray):                 # torch tensor (device load vector)
+        import torch
+        At = torch.as_tensor(A, dtype=X.dtype, device=X.device)
+        return torch.movedim(torch.tensordot(At, X, dims=([1], [axis])), 0, axis)
     t = np.moveaxis(X, axis, 0)
     out = (A @ t.reshape(t.shape[0], -1)).reshape((A.shape[0],) + t.shape[1:])
     return np.moveaxis(out, 0, axis)
@@ -223,6 +247,21 @@ class GaussGrid:
             i1 = min(nq, i0 + rows_per_chunk)
             yield i0, i1, self.source_rows(source, i0, i1)
 
+    def source_rows_device(self, source, i0, i1, device):
+        """Like source_rows, evaluated on the device by ``source.torch`` (one call per time point)."""
+        import torch
+        if getattr(self, "_xq_dev", None) is None or self._xq_dev.device != torch.device(device):
+            self._xq_dev = torch.from_numpy(self.physical_points()).to(device)
+        xq = self._xq_dev
+        qs = xq.shape[0]
+        tq = self.tx[i0:i1] * self.T
+        fv = torch.empty((tq.size, qs), dtype=torch.float64, device=xq.device)
+        for i in range(tq.size):
+            fv[i] = torch.as_tensor(source.torch(xq, torch.full((qs,), float(tq[i]), dtype=torch.float64,
+                                                                device=xq.device)),
+                                    dtype=torch.float64).reshape(qs)
+        return fv.reshape((tq.size,) + tuple(x.size for x in reversed(self.sx)))
+
     def source_rows(self, source, i0, i1):
         """Source at time Gauss points i0..i1-1 x all spatial Gauss points, (i1-i0, Q_d, ..., Q_1)."""
         if getattr(self, "_xq", None) is None:
@@ -247,12 +286,13 @@ class GaussGrid:
         return fv.reshape((tq.size,) + tuple(x.size for x in reversed(self.sx)))
 
 
-def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24, chunks=None):
+def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24, chunks=None, device=None):
     """f_vec[i] = int int f B_i (assembly.py:350-398, box geometry).  The Gauss grid is visited in
     chunks of time points (spatial projection per chunk, then the time projection accumulates),
     so the full space-time grid is never held at once; time points where the source vanishes
     identically contribute nothing and are skipped.  ``chunks`` may supply the evaluated source
-    as (i0, i1, values) rows (GaussGrid.source_chunks) so another consumer can share them."""
+    as (i0, i1, values) rows (GaussGrid.source_chunks) so another consumer can share them.
+    A DeviceSource is evaluated and contracted on the GPU; the result is then a device tensor."""
     if source is None:
         return np.zeros(st.num_dof)
     g = grid if grid is not None else GaussGrid(st, geometry)
@@ -261,18 +301,43 @@ def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24, chunks=No
     for l in reversed(range(d - 1)):
         ws = np.multiply.outer(ws, g.sw[l] * g.L[l])
     if chunks is None:
-        chunks = g.source_chunks(source, max(1, chunk_points // max(1, ws.size)))
-    acc = np.zeros((g.tB[0].shape[1],) + tuple(s.dimension for s in reversed(st.spatial)))
+        rows_per = max(1, chunk_points // max(1, ws.size))
+        if device_capable(source):
+            import torch
+            dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+            nq = g.tx.size
+            chunks = ((i0, min(nq, i0 + rows_per), g.source_rows_device(source, i0, min(nq, i0 + rows_per), dev))
+                      for i0 in range(0, nq, rows_per))
+        else:
+            chunks = g.source_chunks(source, rows_per)
+    shape = (g.tB[0].shape[1],) + tuple(s.dimension for s in reversed(st.spatial))
+    acc = None
     for i0, i1, fv in chunks:
-        live = np.flatnonzero(fv.reshape(i1 - i0, -1).any(axis=1))
+        if acc is None:
+            if isinstance(fv, np.ndarray):
+                acc = np.zeros(shape)
+            else:                                         # device-evaluated source: contract on the device
+                import torch
+                acc = torch.zeros(shape, dtype=torch.float64, device=fv.device)
+                ws = torch.as_tensor(ws, device=fv.device)
+        if isinstance(fv, np.ndarray):
+            live = np.flatnonzero(fv.reshape(i1 - i0, -1).any(axis=1))
+        else:
+            live = fv.reshape(i1 - i0, -1).any(dim=1).nonzero().flatten().cpu().numpy()
         if live.size == 0:
             continue
         rows = i0 + live
-        vals = fv[live] * ws[None] * (g.tw[rows] * g.T).reshape((-1,) + (1,) * d)
+        tw = (g.tw[rows] * g.T).reshape((-1,) + (1,) * d)
+        if not isinstance(fv, np.ndarray):
+            tw = torch.as_tensor(tw, device=fv.device)
+            live = torch.as_tensor(live, device=fv.device)
+        vals = fv[live] * ws[None] * tw
         for l in range(d):
             vals = _mode(g.sB[l][0].T, vals, 1 + (d - 1 - l))
         acc += _mode(g.tB[0][rows].T, vals, 0)
-    return acc.ravel()
+    if acc is None:
+        return np.zeros(st.num_dof)
+    return acc.ravel() if isinstance(acc, np.ndarray) else acc.reshape(-1)
 
 
 def window_elements(space, i):

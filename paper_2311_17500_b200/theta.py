@@ -24,7 +24,7 @@ import torch
 
 from . import _lib
 from .device import DeviceContext, dptr, host_ptr
-from .problem import GaussGrid, ResidualIndicator, box_of, window_elements
+from .problem import GaussGrid, ResidualIndicator, box_of, device_capable, window_elements
 from .spaces import basis_table, gauss_rule, greville
 
 
@@ -101,11 +101,17 @@ class DeviceIndicator:
         qt, per_el, step, keep = self._plan()
         nel_t = self.nel[self.d]
         chunks = []
+        on_device = device_capable(source)
         for et0 in range(0, nel_t, step):
             et1 = min(nel_t, et0 + step)
-            fv = self._grid.source_rows(source, et0 * qt, et1 * qt)
+            if on_device:                                 # evaluated by source.torch on the GPU
+                fv = self._grid.source_rows_device(source, et0 * qt, et1 * qt, self.ctx.device)
+                fd = fv.reshape(-1)
+            else:
+                fv = self._grid.source_rows(source, et0 * qt, et1 * qt)
+                fd = torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device) if keep else None
             if keep:
-                chunks.append((et0, et1, torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device)))
+                chunks.append((et0, et1, fd))
             yield et0 * qt, et1 * qt, fv
         if keep:
             self._src_cache = chunks
@@ -116,7 +122,8 @@ class DeviceIndicator:
             return
         for i0, i1, fv in self.source_chunks(source):
             qt = self.st.time.degree + 1
-            yield i0 // qt, i1 // qt, torch.from_numpy(np.ascontiguousarray(fv.reshape(-1))).to(self.ctx.device)
+            fd = fv.reshape(-1) if torch.is_tensor(fv) else torch.from_numpy(np.ascontiguousarray(fv.reshape(-1)))
+            yield i0 // qt, i1 // qt, fd.to(self.ctx.device)
 
     def _window(self, src, dst, outer, n_in, wins, inner):
         w0 = np.ascontiguousarray([a for a, _ in wins], dtype=np.int32)

@@ -48,6 +48,21 @@ def test_device_theta_matches_reference(name, chunk):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("chunk", [1 << 26, 500])
+def test_device_theta_device_source(name, chunk):
+    """The source given as a DeviceSource: its Gauss values are evaluated on the GPU."""
+    from paper_2311_17500_b200.problem import DeviceSource
+    from paper_2311_17500_b200.theta import DeviceIndicator
+    g = load("theta")
+    prob = problem_for(g, name)
+    if prob.source is not None:
+        prob.source = DeviceSource(pulse_source, lambda x, t: 1.0 * (x[:, 0] < 0.1).to(x.dtype) * (t < 0.05))
+    th = DeviceIndicator(prob, chunk_points=chunk).compute(g[name + "_u"], g[name + "_w"])
+    np.testing.assert_allclose(th.values, g[name + "_values"], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("p", [1, 2, 3])
 def test_device_theta_matches_host_2d(p):
     import paper_2311_17500_b200.spaces as sp

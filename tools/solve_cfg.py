@@ -27,11 +27,21 @@ def make_problem(d, p, ne, ne_t, sigma, stim, corner):
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200.problem import BoxGeometry
 
-    def pulse(x, t):
+    def pulse_host(x, t):
         m = (x[:, 0] < stim).astype(float)
         if corner:
             m = m * (x[:, 1] < stim)
         return m * (t < 0.05)
+
+    def pulse_torch(x, t):
+        m = (x[:, 0] < stim).to(x.dtype)
+        if corner:
+            m = m * (x[:, 1] < stim)
+        return m * (t < 0.05)
+
+    # the same pulse with a device implementation: the Gauss-point values feeding the load
+    # vector and the residual indicator are evaluated on the GPU
+    pulse = mb.DeviceSource(pulse_host, pulse_torch)
 
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(d)], mb.SplineSpace.uniform(p, ne_t))
     D = sigma[0] if len(sigma) == 1 else list(sigma)
