@@ -16,11 +16,11 @@ Arms:
                      (oracle/, a restatement of the reference pinned against
                      its golden vectors) at a bounded sample of the workload.
 
-Multi-GPU (torchrun, N > 1): the time-sharded apply of the SAME workload
-(strong scaling): each rank owns N_t/G time rows; a step is the halo
-exchange + local operator kernel + P^-1 with two NCCL all-to-all
-transposes (paper_2311_17500_b200/sharded.py); value = N * steps / max
-over ranks of the device time.
+Multi-GPU (torchrun, N > 1): the space-sharded apply of the SAME workload
+(strong scaling): each rank owns n_3/G z planes for all time rows; a step is
+the p-plane halo exchange + the local z-slab operator + P^-1 with two NCCL
+all-to-all transposes to y-slabs (paper_2311_17500_b200/sharded.py);
+value = N * steps / max over ranks of the device time.
 """
 
 import argparse
@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--ne-t", type=int, default=CFG["ne_t"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-extras", action="store_true", help="skip variant-B apply and the cfg3 solve")
-    ap.add_argument("--force-sharded", action="store_true", help="run the time-sharded path even on 1 rank")
+    ap.add_argument("--force-sharded", action="store_true", help="run the space-sharded path even on 1 rank")
     return ap.parse_args()
 
 
@@ -223,10 +223,10 @@ def measure_solve(torch, mb, dev):
 
 
 def run_sharded(args):
-    """N > 1: the time-sharded apply (strong scaling of the same cfg-4 workload).
+    """N > 1: the space-sharded apply (strong scaling of the same cfg-4 workload).
 
-    Each rank owns N_t/G time rows; one step = halo exchange + local operator
-    kernel + P^-1 with two NCCL all-to-all transposes.  value = N * steps /
+    Each rank owns n_3/G z planes (all time rows); one step = p-plane halo exchange
+    + local z-slab operator + P^-1 with two NCCL all-to-all transposes.  value = N * steps /
     (max over ranks of the device time)."""
     import torch
     import torch.distributed as dist
@@ -249,13 +249,13 @@ def run_sharded(args):
     theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), ns)
     stab = mb.Stabilization(st, theta, CFG["su_tol"], 1.0)
     del theta
-    L = sh.SlabLayout(nt, ns, p, rank, world)
+    L = sh.ZSlabLayout(nt, [s.dimension for s in st.spatial], p, rank, world)
     be = sh.DeviceSlabBackend(L, st, 1.0, 1.0, CFG["sigma"], RM, stabilization=stab, device=local)
     sop, spc = sh.ShardedOperator(L, be), sh.ShardedPreconditioner(L, be)
     t_setup = time.perf_counter() - t_setup
     rng = np.random.default_rng(0)
     xg = rng.uniform(-1, 1, N)
-    x = torch.from_numpy(xg[L.t_lo * ns:L.t_hi * ns].copy()).to(dev)
+    x = torch.from_numpy(np.ascontiguousarray(L.own_slice(xg))).to(dev)
     del xg
     y = torch.empty_like(x)
     z = torch.empty_like(x)
@@ -308,7 +308,7 @@ def run_sharded(args):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     dom = max(prof, key=lambda k: prof[k][0])
     nsten = (2 * p + 1) ** d
-    F_dom = 2.0 * sop.backend.op.nchan * nsten * L.next_ * ns if dom == "op_stencil" else None
+    F_dom = 2.0 * sop.backend.op.nchan * nsten * L.n_own if dom == "op_stencil" else None
     peak64 = fp64_peak_tflops(torch, dev)
     roof = {"kernel": dom, "bound": "tensor", "unit": "TFLOP/s", "peak": peak64,
             "peak_source": "FP64 cuBLAS DGEMM 4096^3 measured live (rank %d)" % rank,
@@ -320,8 +320,9 @@ def run_sharded(args):
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded x ~ U[-1,1])",
         "config": {"workload": CFG["name"], "d": d, "p": p, "mesh": [args.ne] * 3 + [args.ne_t], "dofs": N,
-                   "su_rank": stab.rank, "parallelism": "time-sharded x%d (halo + 2 all-to-all per step)" % world,
-                   "rows_per_rank": L.nown, "setup_s": t_setup,
+                   "su_rank": stab.rank,
+                   "parallelism": "z-sharded x%d (p-plane halo + 2 all-to-all per step)" % world,
+                   "planes_per_rank": L.nz, "setup_s": t_setup,
                    "l2": "inputs > 126 MB L2 per rank (no flush needed)"},
         "e2e": {"value": N * e2s / (float(te.item()) * 1e-3), "unit": "DoF/s",
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,

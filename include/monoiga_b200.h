@@ -40,6 +40,15 @@ const char* mi_last_error(void);
 int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx** out);
 int mi_ctx_destroy(mi_ctx* ctx);
 int mi_ctx_set_stream(mi_ctx* ctx, void* cuda_stream);
+/* z-slab context for the space-sharded solve (no reference
+ * counterpart: the reference is single-process).  d = 3 only; call before
+ * mi_op_setup.  The context's n[2] planes are the global planes
+ * [z_lo, z_lo + n[2]) of n3g; mi_op_apply then takes x (and the reaction
+ * iterate u, w) on the INPUT slab = hz_lo halo planes + the owned planes +
+ * hz_hi halo planes (hz <= p), and writes y on the owned planes only.
+ * Channel tables stay global: band / H tables have max(n_1, n_2, n3g) rows,
+ * theta has n_1 n_2 n3g entries. */
+int mi_ctx_set_zslab(mi_ctx* ctx, int z_lo, int n3g, int hz_lo, int hz_hi);
 
 /* Per-kernel-class CUDA-event timing (bench/roofline support; no reference
  * counterpart).  Slots: 0 op stencil, 1 op time filter, 2 op reaction,
@@ -116,6 +125,14 @@ int mi_pc_apply(mi_ctx* ctx, const double* r, double* z);
  * all-to-all transpose. */
 int mi_pc_apply_spatial(mi_ctx* ctx, const double* in, double* out, long long nrows, int inverse);
 int mi_pc_apply_time(mi_ctx* ctx, double* y, long long ncols, long long col0);
+/* Stages for the z-sharded preconditioner (sharded.py; the reference's
+ * mode_apply, tensorops.py:13-26, one direction at a time): out = the
+ * direction-l mode product of in viewed as (outer, n_l, inner), with U_l^T
+ * (inverse=0) or U_l (inverse=1); and the time stage on a y-slab
+ * (N_t, n_3, y_hi - y_lo, n_1) holding spatial eigen-indices with
+ * i_2 in [y_lo, y_hi). */
+int mi_pc_mode(mi_ctx* ctx, int l, int inverse, const double* in, double* out, long long outer, long long inner);
+int mi_pc_apply_time_yslab(mi_ctx* ctx, double* y, int y_lo, int y_hi);
 
 /* ---------------------------------------------------------------------
  * Recovery-variable solve ((W_t + b d_e M_t) (x) M_s) w = g  (replaces

@@ -23,6 +23,7 @@ _SIGS = {
     "mi_ctx_create": ([_c_int, _c_int, _vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
     "mi_ctx_destroy": ([_vp], _c_int),
     "mi_ctx_set_stream": ([_vp, _vp], _c_int),
+    "mi_ctx_set_zslab": ([_vp, _c_int, _c_int, _c_int, _c_int], _c_int),
     "mi_prof_enable": ([_vp, _c_int], _c_int),
     "mi_prof_read": ([_vp, _vp, _vp, _c_int], _c_int),
     "mi_op_setup": ([_vp, _c_int], _c_int),
@@ -37,6 +38,8 @@ _SIGS = {
     "mi_pc_apply": ([_vp, _vp, _vp], _c_int),
     "mi_pc_apply_spatial": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),
     "mi_pc_apply_time": ([_vp, _vp, _c_ll, _c_ll], _c_int),
+    "mi_pc_apply_time_yslab": ([_vp, _vp, _c_int, _c_int], _c_int),
+    "mi_pc_mode": ([_vp, _c_int, _c_int, _vp, _vp, _c_ll, _c_ll], _c_int),
     "mi_ws_setup": ([_vp, _vp, _vp, _vp], _c_int),
     "mi_ws_time": ([_vp, _vp, _vp], _c_int),
     "mi_ws_mass": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),

@@ -68,6 +68,11 @@ struct mi_ctx {
   int n[3] = {1, 1, 1};         // n_1, n_2, n_3 (1 beyond d)
   int nt = 0;                   // N_t (constrained)
   long long ns = 0, N = 0;      // N_s, N
+  // z-slab (space-sharded runs, sharded.py): the points are the global planes [z_lo, z_lo + n[2]) of
+  // n3g; operator inputs carry hz_lo / hz_hi halo planes before / after them.  Unsharded: z_lo = 0,
+  // n3g = n[2], no halo, ns_in = ns.
+  int z_lo = 0, n3g = 1, hz_lo = 0, hz_hi = 0;
+  long long ns_in = 0, N_in = 0;  // operator input slab (owned + halo planes)
 
   // ---- operator A: channels c = 0..nchan-1, y = sum_c T_c (x)_t (S_c x)
   int nchan = 0;
@@ -88,7 +93,8 @@ struct mi_ctx {
 
   // ---- reaction correction M_R (variant B)
   bool reaction_on = false;
-  mi::DeviceBuf u_it, w_it;     // iterate coefficients (N each)
+  mi::DeviceBuf u_it, w_it;     // iterate coefficients (N_in each: input slab)
+  mi::DeviceBuf y_in;           // reaction output on the input slab (z-slab contexts with a halo)
   double c1 = 0, a = 0, c2 = 0;
   mi::DeviceBuf rx_B, rx_W;     // Gauss tables, directions x, y, z, t
   size_t rx_Boff[4] = {0, 0, 0, 0}, rx_Woff[4] = {0, 0, 0, 0};

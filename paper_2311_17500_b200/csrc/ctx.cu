@@ -125,6 +125,9 @@ int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx
   }
   c->ns = ns;
   c->N = ns * nt;
+  c->n3g = c->n[2];
+  c->ns_in = ns;
+  c->N_in = c->N;
   int s = 1;
   for (int l = 0; l < d; ++l) s *= 2 * p + 1;
   c->nsten = s;
@@ -137,12 +140,28 @@ int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx
   return MI_OK;
 }
 
+int mi_ctx_set_zslab(mi_ctx* c, int z_lo, int n3g, int hz_lo, int hz_hi) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  MI_REQUIRE(!c->op_ready, MI_ERR_STATE, "mi_ctx_set_zslab must precede mi_op_setup");
+  MI_REQUIRE(c->d == 3, MI_ERR_ARG, "z-slab contexts need d = 3");
+  MI_REQUIRE(z_lo >= 0 && z_lo + c->n[2] <= n3g, MI_ERR_ARG, "slab planes outside [0, n3g)");
+  MI_REQUIRE(hz_lo >= 0 && hz_hi >= 0 && hz_lo <= c->p && hz_hi <= c->p, MI_ERR_ARG, "halo must be in [0, p]");
+  MI_REQUIRE(z_lo - hz_lo >= 0 && z_lo + c->n[2] + hz_hi <= n3g, MI_ERR_ARG, "halo planes outside [0, n3g)");
+  c->z_lo = z_lo;
+  c->n3g = n3g;
+  c->hz_lo = hz_lo;
+  c->hz_hi = hz_hi;
+  c->ns_in = (long long)c->n[0] * c->n[1] * (c->n[2] + hz_lo + hz_hi);
+  c->N_in = c->ns_in * c->nt;
+  return MI_OK;
+}
+
 int mi_ctx_destroy(mi_ctx* c) {
   if (!c) return MI_OK;
   cudaSetDevice(c->device);
   mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->frag, &c->xt, &c->afr, &c->u_it, &c->w_it, &c->rx_B,
                            &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
-                           &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->tq_frag,
+                           &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->tq_frag, &c->y_in,
                            &c->partials};
   for (auto* b : bufs) mi::dfree(*b);
   mi::DeviceBuf* wbufs[] = {&c->ws_Kinv, &c->ws_MT0, &c->ws_MiT0, &c->ws_t1, &c->ws_t2, &c->ws_t3,

@@ -25,11 +25,15 @@ namespace mi {
 struct Dims {
   int n1, n2, n3, nt;
   long long ns, N;
+  int z_lo, n3g;        // global plane of local z = 0, global n_3 (z-slab contexts)
 };
 
 static Dims dims_of(const mi_ctx* c) {
-  return Dims{c->n[0], c->n[1], c->n[2], c->nt, c->ns, c->N};
+  return Dims{c->n[0], c->n[1], c->n[2], c->nt, c->ns, c->N, c->z_lo, c->n3g};
 }
+
+// rows of the host 1D tables (bands, hat triple products): global in every direction
+static int table_rows(const mi_ctx* c) { return std::max(c->n[0], std::max(c->n[1], c->n3g)); }
 
 template <int D, int P>
 struct Sten {
@@ -49,10 +53,11 @@ __global__ void build_kron_channel(double* __restrict__ out, const double* __res
   const int s = blockIdx.y;
   if (i >= g.ns) return;
   const int a1 = s % ST::W1, a2 = (s / ST::W1) % ST::W2, a3 = s / (ST::W1 * ST::W2);
-  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2));
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2),
+            i3 = (int)(i / ((long long)g.n1 * g.n2)) + g.z_lo;     // global plane
   const int ii[3] = {i1, i2, i3};
   const int aa[3] = {a1, a2, a3};
-  const int nn[3] = {g.n1, g.n2, g.n3};
+  const int nn[3] = {g.n1, g.n2, g.n3g};
   bool inside = true;
 #pragma unroll
   for (int l = 0; l < D; ++l) {
@@ -81,10 +86,11 @@ __global__ void build_su_channel(double* __restrict__ out, const double* __restr
   const int s = blockIdx.y;
   if (i >= g.ns) return;
   const int a1 = s % ST::W1, a2 = (s / ST::W1) % ST::W2, a3 = s / (ST::W1 * ST::W2);
-  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2));
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2),
+            i3 = (int)(i / ((long long)g.n1 * g.n2)) + g.z_lo;     // global plane (theta, H are global)
   const int ii[3] = {i1, i2, i3};
   const int aa[3] = {a1, a2, a3};
-  const int nn[3] = {g.n1, g.n2, g.n3};
+  const int nn[3] = {g.n1, g.n2, g.n3g};
   const int W = 2 * P + 1;
   const int KW = 2 * ko + 1;
   bool inside = true;
@@ -102,7 +108,7 @@ __global__ void build_su_channel(double* __restrict__ out, const double* __restr
     const int b3n = D >= 3 ? KW : 1, b2n = D >= 2 ? KW : 1;
     for (int b3 = 0; b3 < b3n; ++b3) {
       int k3 = D >= 3 ? i3 + b3 - ko : 0;
-      if (k3 < 0 || k3 >= g.n3) continue;
+      if (k3 < 0 || k3 >= g.n3g) continue;
       double h3 = D >= 3 ? h[2][b3] : 1.0;
       if (h3 == 0.0) continue;
       for (int b2 = 0; b2 < b2n; ++b2) {
@@ -214,6 +220,8 @@ int mi_op_setup(mi_ctx* c, int nchan) {
   if ((rc = dalloc(c->tband, (size_t)nchan * c->nt * (2 * c->pt + 1)))) return rc;
   if ((rc = dalloc(c->stencil, (size_t)nchan * c->nsten * c->ns))) return rc;
   c->use_dmma = c->p <= 3 && c->pt <= 4;
+  MI_REQUIRE(c->use_dmma || (c->n3g == c->n[2] && c->ns_in == c->ns), MI_ERR_ARG,
+             "z-slab contexts need the tensor-core operator (p <= 3)");
   if (!c->use_dmma && (rc = dalloc(c->wbuf, (size_t)nchan * c->N))) return rc;
   c->frag_dirty = true;
   MI_CUDA(cudaMemsetAsync(c->stencil.p, 0, sizeof(double) * nchan * c->nsten * c->ns, c->stream));
@@ -235,7 +243,7 @@ int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(nterms >= 1, MI_ERR_ARG, "nterms must be >= 1");
-  const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
+  const int nmax = table_rows(c);
   const size_t nb = (size_t)nterms * c->d * nmax * (2 * c->p + 1);
   DeviceBuf dc, db;
   int rc;
@@ -258,12 +266,13 @@ int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(ko >= 0 && ko <= 8, MI_ERR_ARG, "ko out of range");
-  const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
+  const int nmax = table_rows(c);
   const size_t nh = (size_t)c->d * nmax * (2 * c->p + 1) * (2 * ko + 1);
+  const size_t nth = (size_t)c->n[0] * c->n[1] * c->n3g;      // theta on the global spatial grid
   DeviceBuf dt, dh;
   int rc;
-  if ((rc = dalloc(dt, c->ns)) || (rc = dalloc(dh, nh))) return rc;
-  MI_CUDA(cudaMemcpyAsync(dt.p, theta, sizeof(double) * c->ns, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = dalloc(dt, nth)) || (rc = dalloc(dh, nh))) return rc;
+  MI_CUDA(cudaMemcpyAsync(dt.p, theta, sizeof(double) * nth, cudaMemcpyHostToDevice, c->stream));
   MI_CUDA(cudaMemcpyAsync(dh.p, H, sizeof(double) * nh, cudaMemcpyHostToDevice, c->stream));
   Dims g = dims_of(c);
   dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
@@ -289,14 +298,16 @@ static int dmma_prepare(mi_ctx* c) {
     const int ngroups = (c->nchan + 7) / 8;
     if ((rc = dalloc(c->frag, (size_t)per_group * ngroups))) return rc;
     const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
-    if ((rc = dalloc(c->xt, (size_t)ntp * c->ns))) return rc;
+    if ((rc = dalloc(c->xt, (size_t)ntp * c->ns_in))) return rc;
     {
       // TMA descriptor of the time-innermost copy: dims (ntp, n1, n2, n3), box (TSTR, H1, H2, H3)
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q;
       MI_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
       MI_REQUIRE(fn != nullptr && q == cudaDriverEntryPointSuccess, MI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-      cuuint64_t dims[4] = {(cuuint64_t)ntp, (cuuint64_t)c->n[0], (cuuint64_t)c->n[1], (cuuint64_t)c->n[2]};
+      // (the input slab: owned planes plus the z halo)
+      cuuint64_t dims[4] = {(cuuint64_t)ntp, (cuuint64_t)c->n[0], (cuuint64_t)c->n[1],
+                            (cuuint64_t)(c->n[2] + c->hz_lo + c->hz_hi)};
       cuuint64_t strides[3] = {(cuuint64_t)ntp * 8, (cuuint64_t)ntp * c->n[0] * 8,
                                (cuuint64_t)ntp * c->n[0] * c->n[1] * 8};
       cuuint32_t box[4] = {(cuuint32_t)G::TSTR, (cuuint32_t)G::H1, (cuuint32_t)G::H2, (cuuint32_t)G::H3};
@@ -404,13 +415,13 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
     const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
     {
       ProfScope ps(c, PROF_OP_STENCIL);
-      dim3 tg((unsigned)((c->ns + 31) / 32), (ntp + 31) / 32);
-      transpose_time_inner<<<tg, dim3(32, 8), 0, c->stream>>>(x, c->xt.p, c->nt, ntp, c->ns);
+      dim3 tg((unsigned)((c->ns_in + 31) / 32), (ntp + 31) / 32);
+      transpose_time_inner<<<tg, dim3(32, 8), 0, c->stream>>>(x, c->xt.p, c->nt, ntp, c->ns_in);
       MI_CHECK_LAUNCH("transpose_time_inner");
     }
     for (int gi = 0; gi < ngroups; ++gi) {
       DmmaArgs a{c->xt.p, c->wbuf.p, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
-                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns};
+                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns, c->hz_lo};
       ProfScope ps(c, PROF_OP_STENCIL);
       stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");

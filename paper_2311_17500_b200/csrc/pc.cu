@@ -207,14 +207,18 @@ static int pc_spatial(mi_ctx* c, const double* in, double* out, long long nrows,
   return MI_OK;
 }
 
-// time stage on a (nt x ncols) column block (time-major): Q^T, arrowhead, Q.  In place.
-static int pc_time(mi_ctx* c, double* y, long long ncols, long long col0) {
+// time stage on a (nt x ncols) column block (time-major): Q^T, arrowhead, Q.  In place.  Column j is
+// the spatial eigen-index col0 + j of the grid (n1, n2c, *) whose direction-2 indices start at y_lo
+// (unsharded and time-sharded: n2c = n_2, y_lo = 0; z-sharded y-slabs: n2c = owned y range).
+static int pc_time(mi_ctx* c, double* y, long long ncols, long long col0, int y_lo = 0, int n2c = -1) {
   cudaStream_t st = c->stream;
   const int nt = c->nt;
+  if (n2c < 0) n2c = c->n[1];
+  const double* lam2 = c->lam[1].p + y_lo;
   if (c->tq_mb > 0) {
     ProfScope ps(c, PROF_PC_TIME);
-    TStageArgs a{y, c->tq_frag.p, c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p,
-                 c->pen_g.p, c->pen_glow.p, c->pen_partner, c->pen_sigma, c->pc_cm, c->pc_react, c->n[0], c->n[1],
+    TStageArgs a{y, c->tq_frag.p, c->lam[0].p, lam2, c->lam[2].p, c->pen_diag.p, c->pen_off.p,
+                 c->pen_g.p, c->pen_glow.p, c->pen_partner, c->pen_sigma, c->pc_cm, c->pc_react, c->n[0], n2c,
                  nt, c->tq_ksp, ncols, col0};
     MI_CUDA(launch_tstage(c->tq_mb, a, st));
     return MI_OK;
@@ -227,8 +231,8 @@ static int pc_time(mi_ctx* c, double* y, long long ncols, long long col0) {
   {
     ProfScope ps(c, PROF_PC_ARROW);
     arrowhead_solve<<<(unsigned)((ncols + 127) / 128), 128, 0, st>>>(
-        t, c->lam[0].p, c->lam[1].p, c->lam[2].p, c->pen_diag.p, c->pen_off.p, c->pen_partner, c->pen_g.p,
-        c->pen_glow.p, c->pen_sigma, c->pc_cm, c->pc_react, c->n[0], c->n[1], nt, ncols, col0);
+        t, c->lam[0].p, lam2, c->lam[2].p, c->pen_diag.p, c->pen_off.p, c->pen_partner, c->pen_g.p,
+        c->pen_glow.p, c->pen_sigma, c->pc_cm, c->pc_react, c->n[0], n2c, nt, ncols, col0);
     MI_CHECK_LAUNCH("arrowhead_solve");
   }
   {
@@ -265,6 +269,28 @@ int mi_pc_apply_time(mi_ctx* c, double* y, long long ncols, long long col0) {
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   MI_REQUIRE(ncols >= 1 && col0 >= 0 && col0 + ncols <= c->ns, MI_ERR_ARG, "column range out of range");
   return pc_time(c, y, ncols, col0);
+}
+
+int mi_pc_apply_time_yslab(mi_ctx* c, double* y, int y_lo, int y_hi) {
+  MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
+  MI_REQUIRE(c->d == 3 && 0 <= y_lo && y_lo < y_hi && y_hi <= c->n[1], MI_ERR_ARG, "y range out of range");
+  const long long ncols = (long long)c->n[0] * (y_hi - y_lo) * c->n[2];
+  return pc_time(c, y, ncols, 0, y_lo, y_hi - y_lo);
+}
+
+int mi_pc_mode(mi_ctx* c, int l, int inverse, const double* in, double* out, long long outer, long long inner) {
+  MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
+  MI_REQUIRE(l >= 0 && l < c->d, MI_ERR_ARG, "direction out of range");
+  MI_REQUIRE(outer >= 1 && inner >= 1 && in != out, MI_ERR_ARG, "bad mode-product shape or aliasing");
+  const int n = c->n[l];
+  ProfScope ps(c, PROF_PC_SPATIAL);
+  // forward applies U_l^T, inverse U_l (pc_spatial's convention)
+  if (inner == 1) {
+    MI_CUDA(mode_contig(inverse ? c->UsT[l].p : c->Us[l].p, in, out, n, outer, c->stream));
+  } else {
+    MI_CUDA(mode_strided(inverse ? c->Us[l].p : c->UsT[l].p, in, out, n, inner, outer, c->stream));
+  }
+  return MI_OK;
 }
 
 }  // extern "C"

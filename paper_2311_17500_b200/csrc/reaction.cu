@@ -428,12 +428,28 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, 512 / RxTile<D, P>::NTH) re
       return MI_ERR_ARG;                                                         \
   }
 
+// y[t, owned planes] += y_in[t, same planes of the input slab] (z-slab contexts)
+__global__ void add_owned_planes(double* __restrict__ y, const double* __restrict__ yin, long long ns,
+                                 long long ns_in, long long off, int nt) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  if (i < ns && t < nt) y[(long long)t * ns + i] += yin[(long long)t * ns_in + off + i];
+}
+
 int reaction_apply(mi_ctx* c, const double* x, double* y) {
+  // the reaction runs on the input frame (owned + halo planes): element contributions to the owned
+  // planes need the iterate and x on every function of the elements touching them
+  const bool slab = c->ns_in != c->ns;
+  if (slab) {
+    int rc;
+    if ((rc = dalloc(c->y_in, (size_t)c->N_in))) return rc;
+    MI_CUDA(cudaMemsetAsync(c->y_in.p, 0, sizeof(double) * c->N_in, c->stream));
+  }
   RxArgs r{};
   r.u = c->u_it.p;
   r.w = c->w_it.p;
   r.x = x;
-  r.y = y;
+  r.y = slab ? c->y_in.p : y;
   for (int l = 0; l < 4; ++l) {
     r.B[l] = c->rx_B.p + c->rx_Boff[l];
     r.Wq[l] = c->rx_W.p + c->rx_Woff[l];
@@ -441,10 +457,10 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   }
   r.n[0] = c->n[0];
   r.n[1] = c->n[1];
-  r.n[2] = c->n[2];
+  r.n[2] = c->n[2] + c->hz_lo + c->hz_hi;
   r.ntc = c->nt;
   r.rowoff = c->rx_rowoff;
-  r.ns = c->ns;
+  r.ns = c->ns_in;
   r.c1 = c->c1;
   r.a = c->a;
   r.c2 = c->c2;
@@ -479,6 +495,12 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
       MI_CHECK_LAUNCH("reaction_tile");
     }
   });
+  if (slab) {
+    dim3 g((unsigned)((c->ns + 255) / 256), c->nt);
+    add_owned_planes<<<g, 256, 0, c->stream>>>(y, c->y_in.p, c->ns, c->ns_in,
+                                               (long long)c->hz_lo * c->n[0] * c->n[1], c->nt);
+    MI_CHECK_LAUNCH("add_owned_planes");
+  }
   return MI_OK;
 }
 
@@ -493,9 +515,10 @@ int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, d
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(u && w && q && nel && B && Wq, MI_ERR_ARG, "NULL argument to mi_op_set_reaction");
   int rc;
-  if ((rc = dalloc(c->u_it, c->N)) || (rc = dalloc(c->w_it, c->N))) return rc;
-  MI_CUDA(cudaMemcpyAsync(c->u_it.p, u, sizeof(double) * c->N, cudaMemcpyDeviceToDevice, c->stream));
-  MI_CUDA(cudaMemcpyAsync(c->w_it.p, w, sizeof(double) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  // u, w on the input slab (owned planes plus the z halo; = N unsharded)
+  if ((rc = dalloc(c->u_it, c->N_in)) || (rc = dalloc(c->w_it, c->N_in))) return rc;
+  MI_CUDA(cudaMemcpyAsync(c->u_it.p, u, sizeof(double) * c->N_in, cudaMemcpyDeviceToDevice, c->stream));
+  MI_CUDA(cudaMemcpyAsync(c->w_it.p, w, sizeof(double) * c->N_in, cudaMemcpyDeviceToDevice, c->stream));
   // per direction tables, direction order x, y, z, t; absent spatial dims get q=1, p=0
   size_t nb = 0, nw = 0;
   for (int l = 0; l < 4; ++l) {

@@ -74,6 +74,7 @@ struct DmmaArgs {
   int n1, n2, n3, nt, ntp;
   int C1, C2, C3;       // cube grid
   long long ns;
+  int zoff;             // halo planes below the owned ones in xt (z-slab contexts; 0 unsharded)
 };
 
 // x (nt, ns) -> xt (ns, ntp), zero padded in time; 32x32 smem tiles.
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(512, 1) stencil_dmma(DmmaArgs a, const __grid_
     if (tid == 0 && t0 < a.nt) {
       mbar_expect_tx(&bars[buf], TILE_BYTES);
       tma_load_4d(Xs + buf * G::HS * G::TSTR, &tmap, &bars[buf], t0, o1 - P, D >= 2 ? o2 - P : 0,
-                  D >= 3 ? o3 - P : 0);
+                  D >= 3 ? o3 - P + a.zoff : 0);
     }
   };
 

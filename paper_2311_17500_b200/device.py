@@ -32,7 +32,9 @@ def dptr(t):
 class DeviceContext:
     """Owns the C context for one space-time shape on one GPU."""
 
-    def __init__(self, space_time, device=0, nt=None):
+    def __init__(self, space_time, device=0, nt=None, zslab=None):
+        """``zslab=(z_lo, z_hi, hz_lo, hz_hi)``: a z-slab context (space-sharded runs) owning the
+        global planes [z_lo, z_hi) with hz_lo / hz_hi halo planes on the operator input."""
         self.device = _require_cuda(device)
         st = space_time
         self.space_time = st
@@ -42,9 +44,18 @@ class DeviceContext:
             raise ValueError("all spatial directions must share one degree")
         self.pt = int(st.time.degree)
         self.n = [int(s.dimension) for s in st.spatial]
+        self.n3g = self.n[-1]
+        self.zslab = None if zslab is None else tuple(int(v) for v in zslab)
+        if self.zslab is not None:
+            if self.d != 3:
+                raise ValueError("z-slab contexts need d = 3")
+            self.n[2] = self.zslab[1] - self.zslab[0]
         self.nt = int(st.time.dimension) - 1 if nt is None else int(nt)
         self.ns = int(np.prod(self.n))
         self.N = self.ns * self.nt
+        hz = (0, 0) if self.zslab is None else self.zslab[2:]
+        self.ns_in = self.ns // self.n[-1] * (self.n[-1] + hz[0] + hz[1])
+        self.N_in = self.ns_in * self.nt
         _lib.load()
         h = ctypes.c_void_p()
         dims = np.asarray(self.n, dtype=np.int32)
@@ -52,6 +63,9 @@ class DeviceContext:
             _lib.call("mi_ctx_create", self.device.index, self.d, host_ptr(dims), self.nt, self.p, self.pt,
                       ctypes.byref(h))
         self.handle = h
+        if self.zslab is not None:
+            z_lo, _, h_lo, h_hi = self.zslab
+            _lib.call("mi_ctx_set_zslab", h, z_lo, self.n3g, h_lo, h_hi)
         self._stream = None
 
     def bind_stream(self):

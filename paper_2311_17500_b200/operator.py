@@ -68,15 +68,24 @@ class KroneckerOperator:
     """
 
     def __init__(self, space_time, final_time, capacitance=1.0, diffusion=1e-4, constants=None,
-                 u=None, w=None, stabilization=None, lengths=None, device=0, context=None, time_rows=None):
+                 u=None, w=None, stabilization=None, lengths=None, device=0, context=None, time_rows=None,
+                 z_planes=None):
         """``time_rows=(e_lo, e_hi)`` builds the operator restricted to a slab of
-        constrained time rows (time-sharded runs, sharded.py): the time bands
-        are the global rows e_lo..e_hi, and u, w (if given) are slab vectors."""
+        constrained time rows: the time bands are the global rows e_lo..e_hi, and
+        u, w (if given) are slab vectors.  ``z_planes=(z_lo, z_hi)`` (d = 3) builds
+        the z-slab operator of the space-sharded solve (sharded.py): it maps an input
+        slab (the owned planes plus up to p halo planes on each side, all time rows)
+        to the owned planes of A x; u, w (if given) are input-slab vectors."""
         st = space_time
         nt_glob = st.time.dimension - 1
         self.time_rows = (0, nt_glob) if time_rows is None else tuple(int(v) for v in time_rows)
         r0, r1 = self.time_rows
-        self.ctx = context if context is not None else DeviceContext(st, device, nt=r1 - r0)
+        zslab = None
+        if z_planes is not None:
+            n3, p_s = st.spatial[-1].dimension, st.spatial[-1].degree
+            z_lo, z_hi = (int(v) for v in z_planes)
+            zslab = (z_lo, z_hi, min(p_s, z_lo), min(p_s, n3 - z_hi))
+        self.ctx = context if context is not None else DeviceContext(st, device, nt=r1 - r0, zslab=zslab)
         ctx = self.ctx
         self.space_time = st
         self.num_time, self.num_space = ctx.nt, ctx.ns
@@ -107,8 +116,8 @@ class KroneckerOperator:
         # whose results are discarded by the caller
         bands = np.ascontiguousarray(bands[:, r0:r1])
         _lib.call("mi_op_set_time_bands", ctx.handle, host_ptr(bands))
-        # spatial Kronecker channels
-        nmax = max(ctx.n)
+        # spatial Kronecker channels (1D tables are global in every direction)
+        nmax = max(ctx.n[:-1] + [ctx.n3g])
         Mb, Kb = [], []
         for l, s in enumerate(st.spatial):
             M, K, _ = univariate_factors(s)
@@ -141,14 +150,14 @@ class KroneckerOperator:
             _lib.call("mi_op_set_su_channel", ctx.handle, 2 + r, host_ptr(th), host_ptr(H), stab.ko)
         if not zero_iterate:
             from .reaction import set_reaction
-            set_reaction(ctx, st, final_time, consts, u, w, L, time_rows=self.time_rows)
+            set_reaction(ctx, st, final_time, consts, u, w, L, time_rows=self.time_rows, zslab=ctx.zslab)
         else:
             _lib.call("mi_op_clear_reaction", ctx.handle)    # a reused context may carry one
 
     @property
     def shape(self):
-        n = self.num_time * self.num_space
-        return (n, n)
+        """(owned outputs, inputs): square unless this is a z-slab operator."""
+        return (self.num_time * self.num_space, self.ctx.N_in)
 
     def apply_device(self, x, y):
         """y = A x for contiguous fp64 CUDA tensors of length N (no checks)."""
@@ -156,11 +165,11 @@ class KroneckerOperator:
         _lib.call("mi_op_apply", self.ctx.handle, dptr(x), dptr(y))
 
     def matvec(self, x):
-        n = self.shape[0]
+        n, n_in = self.shape
         size = x.numel() if isinstance(x, torch.Tensor) else np.asarray(x).size
-        if size != n:
+        if size != n_in:
             raise ValueError("dimension mismatch: operator of size %d applied to vector of size %d"
-                             % (n, size))
+                             % (n_in, size))
         xd = self.ctx.to_device(x)
         yd = self.ctx.empty(n)
         self.apply_device(xd, yd)

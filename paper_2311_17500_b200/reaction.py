@@ -29,12 +29,18 @@ def element_tables(space, q, scale):
     return B, (w * scale).reshape(ne, q)
 
 
-def set_reaction(ctx, st, final_time, consts, u, w, lengths, time_rows=None):
+def set_reaction(ctx, st, final_time, consts, u, w, lengths, time_rows=None, zslab=None):
+    """``zslab=(z_lo, z_hi, hz_lo, hz_hi)``: the kernel runs on the input slab (global planes
+    [z_lo - hz_lo, z_hi + hz_hi)); its z elements are those whose functions all lie there."""
     d = len(st.spatial)
     L = np.ones(d) if lengths is None else np.asarray(lengths, float)
     Bs, Ws, qs, nels = [], [], [], []
     for l, s in enumerate(st.spatial):
         B, W = element_tables(s, s.degree + 1, L[l])
+        if zslab is not None and l == d - 1:
+            f0 = zslab[0] - zslab[2]
+            f1 = zslab[1] + zslab[3]
+            B, W = B[f0:f1 - s.degree], W[f0:f1 - s.degree]   # element e carries functions e..e+p
         Bs.append(B.ravel()); Ws.append(W.ravel()); qs.append(s.degree + 1); nels.append(B.shape[0])
     B, W = element_tables(st.time, st.time.degree + 1, final_time)
     pt = st.time.degree

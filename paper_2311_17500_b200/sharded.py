@@ -1,17 +1,22 @@
-"""Time-sharded solve over torch.distributed: one process per GPU.
+"""Space-sharded solve over torch.distributed: one process per GPU.
 
-Each rank owns a contiguous slab of time rows [t_lo, t_hi) of every
-(N_t, N_s) vector.  The exchanges are exactly the ones the path needs:
+Each rank owns a contiguous slab of planes [z_lo, z_hi) of the slowest spatial
+direction (direction 3) for ALL time rows: a vector slab is the C-order
+(N_t, z_hi - z_lo, n_2, n_1) block.  Sharding space instead of time keeps every
+rank's operator sweep over the full time axis, where the tensor-core stencil
+amortises its per-block start-up (a time slab of N_t/G rows would spend most
+of each block on start-up and halo rows).  The exchanges are exactly the ones
+the path needs:
 
-* operator A: a p_t-row halo of x from each time neighbour (send/recv), then
-  the local stencil + time-filter kernel on the extended slab; only the
-  owned rows of the result are kept.  (The reaction's time elements reach
-  p_t rows as well, so the same halo covers it; u, w halos are exchanged
+* operator A: a p-plane halo of x from each z neighbour (send/recv, all time
+  rows), then the local z-slab operator (stencil, time filter, reaction on
+  the input slab) writes the owned planes directly.  (u, w halos are exchanged
   once when the operator is built.)
-* preconditioner P^-1: spatial transforms on the owned rows, an all-to-all
-  transpose to spatial-column slabs (every rank then holds all N_t rows of
-  N_s/G eigen-columns), the time stage (Q^T, arrowhead, Q) locally, the
-  inverse all-to-all, inverse spatial transforms.
+* preconditioner P^-1: the direction-1 and -2 eigenvector transforms on the
+  owned slab, an all-to-all transpose to y-slabs (every rank then holds all
+  z planes and all time rows of n_2/G y-columns), the direction-3 transform
+  and the time stage (Q^T, arrowhead, Q) locally, the inverse direction-3
+  transform, the inverse all-to-all, the inverse direction-2/1 transforms.
 * GMRES: the CGS2 dot products and norms are summed with all_reduce; the
   Hessenberg recurrence is replicated on every rank (krylov.gmres_core).
 
@@ -20,7 +25,6 @@ kernels of libmonoiga_b200 (NCCL on the GPU box); the CPU tests plug in a
 reference backend with the gloo process group (tests/test_sharded_cpu.py).
 """
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -36,71 +40,95 @@ def split(n, parts):
     return bounds
 
 
-class SlabLayout:
-    """Row / column ownership of one rank."""
+class ZSlabLayout:
+    """Ownership of one rank: z planes [z_lo, z_hi) (vectors, A) and y columns [y_lo, y_hi)
+    (the transposed layout inside P^-1).  ``n = (n_1, n_2, n_3)``, ``halo`` = spatial degree p."""
 
-    def __init__(self, nt, ns, halo, rank, world):
-        if nt < world * max(halo, 1):
-            raise ValueError("too few time rows (%d) for %d ranks with halo %d" % (nt, world, halo))
-        self.nt, self.ns, self.halo, self.rank, self.world = nt, ns, halo, rank, world
-        self.rows = split(nt, world)
-        self.cols = split(ns, world)
-        self.t_lo, self.t_hi = self.rows[rank], self.rows[rank + 1]
-        self.e_lo = max(0, self.t_lo - halo)
-        self.e_hi = min(nt, self.t_hi + halo)
-        self.s_lo, self.s_hi = self.cols[rank], self.cols[rank + 1]
-
-    @property
-    def nown(self):
-        return self.t_hi - self.t_lo
-
-    @property
-    def next_(self):
-        return self.e_hi - self.e_lo
+    def __init__(self, nt, n, halo, rank, world):
+        n1, n2, n3 = (int(v) for v in n)
+        if n3 < world * max(halo, 1):
+            raise ValueError("too few z planes (%d) for %d ranks with halo %d" % (n3, world, halo))
+        if n2 < world:
+            raise ValueError("too few y columns (%d) for %d ranks" % (n2, world))
+        self.nt, self.n1, self.n2, self.n3 = int(nt), n1, n2, n3
+        self.halo, self.rank, self.world = int(halo), rank, world
+        self.zs = split(n3, world)
+        self.ys = split(n2, world)
+        self.z_lo, self.z_hi = self.zs[rank], self.zs[rank + 1]
+        self.y_lo, self.y_hi = self.ys[rank], self.ys[rank + 1]
+        self.h_lo = min(self.halo, self.z_lo)
+        self.h_hi = min(self.halo, n3 - self.z_hi)
 
     @property
-    def ncols(self):
-        return self.s_hi - self.s_lo
+    def nz(self):
+        return self.z_hi - self.z_lo
+
+    @property
+    def nz_in(self):
+        return self.nz + self.h_lo + self.h_hi
+
+    @property
+    def ny(self):
+        return self.y_hi - self.y_lo
+
+    @property
+    def plane(self):
+        return self.n1 * self.n2
+
+    @property
+    def n_own(self):
+        return self.nt * self.nz * self.plane
+
+    @property
+    def n_in(self):
+        return self.nt * self.nz_in * self.plane
+
+    @property
+    def n_blk(self):
+        return self.nt * self.n3 * self.ny * self.n1
+
+    def own_slice(self, x_global):
+        """This rank's slab of a global (N_t, n_3, n_2, n_1) vector (any array type)."""
+        return x_global.reshape(self.nt, self.n3, self.plane)[:, self.z_lo:self.z_hi].reshape(-1)
 
 
-def exchange_halo(layout, x_own, x_ext, group=None):
-    """x_ext[rows e_lo..e_hi) <- own rows + halos from the time neighbours."""
-    L, ns = layout, layout.ns
-    off = (L.t_lo - L.e_lo) * ns
-    x_ext[off:off + L.nown * ns].copy_(x_own)
-    ops = []
-    left, right = L.rank - 1, L.rank + 1
-    hl = L.t_lo - L.e_lo                      # rows received from the left neighbour
-    hr = L.e_hi - L.t_hi                      # rows received from the right neighbour
-    nsend = min(L.halo, L.nown)
-    if left >= 0:
-        # my first rows are the left neighbour's right halo; its last rows are my left halo
-        ops.append(dist.P2POp(dist.isend, x_ext[off:off + nsend * ns], left, group))
-        ops.append(dist.P2POp(dist.irecv, x_ext[:hl * ns], left, group))
-    if right < L.world:
-        ops.append(dist.P2POp(dist.isend, x_ext[off + (L.nown - nsend) * ns:off + L.nown * ns], right, group))
-        ops.append(dist.P2POp(dist.irecv, x_ext[off + L.nown * ns:off + (L.nown + hr) * ns], right, group))
-    if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-    return x_ext
+def exchange_halo(L, x_own, x_in, group=None):
+    """x_in = [h_lo planes from the left | owned planes | h_hi planes from the right], all time rows."""
+    nt, P = L.nt, L.plane
+    xo = x_own.view(nt, L.nz, P)
+    xi = x_in.view(nt, L.nz_in, P)
+    xi[:, L.h_lo:L.h_lo + L.nz].copy_(xo)
+    if L.world == 1:
+        return x_in
+    ops, recv = [], []
+    h = L.halo
+    if L.rank > 0:
+        snd = xo[:, :h].contiguous()                   # my first planes = the left neighbour's upper halo
+        rcv = torch.empty(nt, L.h_lo, P, dtype=x_own.dtype, device=x_own.device)
+        ops += [dist.P2POp(dist.isend, snd, L.rank - 1, group), dist.P2POp(dist.irecv, rcv, L.rank - 1, group)]
+        recv.append((rcv, 0))
+    if L.rank < L.world - 1:
+        snd_r = xo[:, L.nz - h:].contiguous()
+        rcv_r = torch.empty(nt, L.h_hi, P, dtype=x_own.dtype, device=x_own.device)
+        ops += [dist.P2POp(dist.isend, snd_r, L.rank + 1, group), dist.P2POp(dist.irecv, rcv_r, L.rank + 1, group)]
+        recv.append((rcv_r, L.h_lo + L.nz))
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    for buf, at in recv:
+        xi[:, at:at + buf.shape[1]].copy_(buf)
+    return x_in
 
 
 class ShardedOperator:
-    """y_own = (A x)_own with a p_t-row halo exchange (``apply_device``)."""
+    """y_own = (A x)_own: p-plane halo exchange + the local z-slab operator (``apply_device``)."""
 
     def __init__(self, layout, backend, group=None):
         self.layout, self.backend, self.group = layout, backend, group
-        n = layout.next_ * layout.ns
-        self.x_ext = backend.empty(n)
-        self.y_ext = backend.empty(n)
+        self.x_in = backend.empty(layout.n_in)
 
     def apply_device(self, x_own, y_own):
-        L = self.layout
-        exchange_halo(L, x_own, self.x_ext, self.group)
-        self.backend.apply_ext(self.x_ext, self.y_ext)
-        off = (L.t_lo - L.e_lo) * L.ns
-        y_own.copy_(self.y_ext[off:off + L.nown * L.ns])
+        exchange_halo(self.layout, x_own, self.x_in, self.group)
+        self.backend.apply_in(self.x_in, y_own)
 
 
 class ShardedPreconditioner:
@@ -109,38 +137,72 @@ class ShardedPreconditioner:
     def __init__(self, layout, backend, group=None):
         self.layout, self.backend, self.group = layout, backend, group
         L = layout
-        self.s_own = backend.empty(L.nown * L.ns)
-        self.send = backend.empty(L.nown * L.ns)
-        self.blk = backend.empty(L.nt * L.ncols)
-        self.in_splits = [L.nown * (L.cols[r + 1] - L.cols[r]) for r in range(L.world)]
-        self.out_splits = [(L.rows[r + 1] - L.rows[r]) * L.ncols for r in range(L.world)]
+        self.t1 = backend.empty(L.n_own)
+        self.t2 = backend.empty(L.n_own)
+        self.send = backend.empty(L.n_own)
+        self.blk = backend.empty(L.n_blk)
+        self.blk2 = backend.empty(L.n_blk)
+        # all-to-all splits: to rank q go my planes x its y columns; from rank r come its planes x my columns
+        self.split_own = [L.nt * L.nz * (L.ys[q + 1] - L.ys[q]) * L.n1 for q in range(L.world)]
+        self.split_blk = [L.nt * (L.zs[r + 1] - L.zs[r]) * L.ny * L.n1 for r in range(L.world)]
+
+    def _to_blk(self, s_own):
+        """(N_t, nz, n_2, n_1) owned slab -> (N_t, n_3, ny, n_1) y-slab via all-to-all."""
+        L = self.layout
+        S = s_own.view(L.nt, L.nz, L.n2, L.n1)
+        off = 0
+        for q in range(L.world):
+            y0, y1 = L.ys[q], L.ys[q + 1]
+            n = L.nt * L.nz * (y1 - y0) * L.n1
+            self.send[off:off + n].view(L.nt, L.nz, y1 - y0, L.n1).copy_(S[:, :, y0:y1])
+            off += n
+        if L.world > 1:
+            dist.all_to_all_single(self.blk2, self.send, self.split_blk, self.split_own, group=self.group)
+        else:
+            self.blk2.copy_(self.send)
+        B = self.blk.view(L.nt, L.n3, L.ny, L.n1)
+        off = 0
+        for r in range(L.world):
+            z0, z1 = L.zs[r], L.zs[r + 1]
+            n = L.nt * (z1 - z0) * L.ny * L.n1
+            B[:, z0:z1].copy_(self.blk2[off:off + n].view(L.nt, z1 - z0, L.ny, L.n1))
+            off += n
+        return self.blk
+
+    def _from_blk(self, blk, s_own):
+        L = self.layout
+        B = blk.view(L.nt, L.n3, L.ny, L.n1)
+        off = 0
+        for r in range(L.world):
+            z0, z1 = L.zs[r], L.zs[r + 1]
+            n = L.nt * (z1 - z0) * L.ny * L.n1
+            self.blk2[off:off + n].view(L.nt, z1 - z0, L.ny, L.n1).copy_(B[:, z0:z1])
+            off += n
+        if L.world > 1:
+            dist.all_to_all_single(self.send, self.blk2, self.split_own, self.split_blk, group=self.group)
+        else:
+            self.send.copy_(self.blk2)
+        S = s_own.view(L.nt, L.nz, L.n2, L.n1)
+        off = 0
+        for q in range(L.world):
+            y0, y1 = L.ys[q], L.ys[q + 1]
+            n = L.nt * L.nz * (y1 - y0) * L.n1
+            S[:, :, y0:y1].copy_(self.send[off:off + n].view(L.nt, L.nz, y1 - y0, L.n1))
+            off += n
 
     def apply_device(self, r_own, z_own):
         L, be = self.layout, self.backend
-        be.pc_spatial(r_own, self.s_own, L.nown, inverse=False)
-        # pack: for each destination rank, (own rows x its columns), contiguous
-        S = self.s_own.view(L.nown, L.ns)
-        off = 0
-        for q in range(L.world):
-            c0, c1 = L.cols[q], L.cols[q + 1]
-            self.send[off:off + L.nown * (c1 - c0)].view(L.nown, c1 - c0).copy_(S[:, c0:c1])
-            off += L.nown * (c1 - c0)
-        if L.world > 1:
-            dist.all_to_all_single(self.blk, self.send, self.out_splits, self.in_splits, group=self.group)
-        else:
-            self.blk.copy_(self.send)
-        # blk is the time-major (N_t x ncols) block of my eigen-columns
-        be.pc_time(self.blk, L.ncols, L.s_lo)
-        if L.world > 1:
-            dist.all_to_all_single(self.send, self.blk, self.in_splits, self.out_splits, group=self.group)
-        else:
-            self.send.copy_(self.blk)
-        off = 0
-        for q in range(L.world):
-            c0, c1 = L.cols[q], L.cols[q + 1]
-            S[:, c0:c1].copy_(self.send[off:off + L.nown * (c1 - c0)].view(L.nown, c1 - c0))
-            off += L.nown * (c1 - c0)
-        be.pc_spatial(self.s_own, z_own, L.nown, inverse=True)
+        # forward: U_1^T (contiguous), U_2^T (stride n_1) on the owned planes
+        be.pc_mode(0, False, r_own, self.t1, L.nt * L.nz * L.n2, 1)
+        be.pc_mode(1, False, self.t1, self.t2, L.nt * L.nz, L.n1)
+        blk = self._to_blk(self.t2)
+        # y-slab: U_3^T (stride ny n_1), time stage in place, U_3
+        be.pc_mode(2, False, blk, self.blk2, L.nt, L.ny * L.n1)
+        be.pc_time_yslab(self.blk2, L.y_lo, L.y_hi)
+        be.pc_mode(2, True, self.blk2, blk, L.nt, L.ny * L.n1)
+        self._from_blk(blk, self.t2)
+        be.pc_mode(1, True, self.t2, self.t1, L.nt * L.nz, L.n1)
+        be.pc_mode(0, True, self.t1, z_own, L.nt * L.nz * L.n2, 1)
 
 
 def allreduce_sum(group=None):
@@ -160,20 +222,21 @@ def sharded_gmres(op, pc, ops, b_own, tol=1e-8, max_iter=200, group=None, log_pa
 # --------------------------------------------------------------------------
 
 class DeviceSlabBackend:
-    """Local CUDA contexts of one rank: the extended-slab operator and the
-    preconditioner stages (libmonoiga_b200)."""
+    """Local CUDA contexts of one rank: the z-slab operator and the preconditioner stages
+    (libmonoiga_b200).  ``u``, ``w`` (variant B) are input-slab vectors."""
 
     def __init__(self, layout, space_time, final_time, capacitance, diffusion, constants,
                  stabilization=None, u=None, w=None, device=0):
         from . import _lib
-        from .device import DeviceContext
         from .operator import KroneckerOperator
         from .precond import FastDiagPreconditioner
+        if len(space_time.spatial) != 3:
+            raise ValueError("the space-sharded solve needs d = 3")
         self._lib = _lib
         L = layout
         self.op = KroneckerOperator(space_time, final_time, capacitance, diffusion, constants,
                                     u=u, w=w, stabilization=stabilization, device=device,
-                                    time_rows=(L.e_lo, L.e_hi))
+                                    z_planes=(L.z_lo, L.z_hi))
         self.pc = FastDiagPreconditioner.build(space_time, final_time, capacitance, diffusion,
                                                constants["a"] * constants["c1"], device=device)
         self.device = self.op.ctx.device
@@ -182,16 +245,16 @@ class DeviceSlabBackend:
     def empty(self, n):
         return torch.empty(n, dtype=torch.float64, device=self.device)
 
-    def apply_ext(self, x_ext, y_ext):
-        self.op.apply_device(x_ext, y_ext)
+    def apply_in(self, x_in, y_own):
+        self.op.apply_device(x_in, y_own)
 
-    def pc_spatial(self, src, dst, nrows, inverse):
+    def pc_mode(self, l, inverse, src, dst, outer, inner):
         from .device import dptr
         self.pc.ctx.bind_stream()
-        self._lib.call("mi_pc_apply_spatial", self.pc.ctx.handle, dptr(src), dptr(dst), nrows,
-                       1 if inverse else 0)
+        self._lib.call("mi_pc_mode", self.pc.ctx.handle, l, 1 if inverse else 0, dptr(src), dptr(dst),
+                       int(outer), int(inner))
 
-    def pc_time(self, blk, ncols, col0):
+    def pc_time_yslab(self, blk, y_lo, y_hi):
         from .device import dptr
         self.pc.ctx.bind_stream()
-        self._lib.call("mi_pc_apply_time", self.pc.ctx.handle, dptr(blk), ncols, col0)
+        self._lib.call("mi_pc_apply_time_yslab", self.pc.ctx.handle, dptr(blk), int(y_lo), int(y_hi))

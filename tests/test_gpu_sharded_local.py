@@ -1,15 +1,17 @@
-"""GPU: the per-rank slab operations of the time-sharded solve (CUDA backend)
-match the numpy reference backend, for every rank of simulated 2/3-rank
+"""GPU: the per-rank slab operations of the space-sharded solve (CUDA backend)
+match the numpy reference backend, for every rank of simulated 2-4-rank
 layouts (no collectives needed: each rank's local math is checked in one
-process).  Covers time-row slicing of the operator bands, the reaction's
-slab row offset, and the column-offset time stage of P^-1."""
+process).  Covers the z-slab operator (owned planes from an input slab with
+p halo planes: global channel tables, TMA halo offset, the reaction on the
+input frame) and the per-direction mode products and the y-slab time stage
+of P^-1."""
 
 import numpy as np
 import pytest
 import torch
 
-from cases import RM, load, oracle_objects
-from test_sharded_cpu import NumpySlabBackend
+from cases import RM, load
+from test_sharded_cpu import NumpySlabBackend, layout_for, synthetic_case
 
 pytestmark = pytest.mark.gpu
 
@@ -18,14 +20,17 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("name,world", [("case_2d_aniso", 2), ("case_3d_p2_front", 3), ("case_cfg1", 3)])
+def input_slab(L, v):
+    return np.ascontiguousarray(v.reshape(L.nt, L.n3, L.plane)[:, L.z_lo - L.h_lo:L.z_hi + L.h_hi]).ravel()
+
+
+@pytest.mark.parametrize("name,world", [("case_3d_p2_front", 2), ("case_3d_p3", 2), ("synthetic", 3),
+                                        ("synthetic", 4)])
 @pytest.mark.parametrize("variant", ["a", "b"])
 def test_slab_backend_matches_reference(name, world, variant):
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200 import sharded as sh
-    g = load(name)
-    st_o, op_a, op_b, _, _, _ = oracle_objects(g)
-    nt, ns = st_o.num_time, st_o.num_space
+    g = synthetic_case() if name == "synthetic" else load(name)
     p = int(g["p"])
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, int(n)) for n in g["ne"]], mb.SplineSpace.uniform(p, int(g["ne_t"])))
     sig = np.atleast_1d(g["sigma"])
@@ -33,46 +38,44 @@ def test_slab_backend_matches_reference(name, world, variant):
     stab = mb.Stabilization(st, g["theta"], float(g["su_tol"]), 1.0)
     rng = np.random.default_rng(5)
     for rank in range(world):
-        L = sh.SlabLayout(nt, ns, p, rank, world)
+        L = layout_for(g, rank, world)
         u = w = None
         if variant == "b":
-            u = g["u"][L.e_lo * ns:L.e_hi * ns]
-            w = g["w"][L.e_lo * ns:L.e_hi * ns]
+            u, w = input_slab(L, g["u"]), input_slab(L, g["w"])
         dev = sh.DeviceSlabBackend(L, st, float(g["T"]), 1.0, sig, RM, stabilization=stab, u=u, w=w)
-        ref = NumpySlabBackend(L, g)
-        if variant == "b":
-            ref.op_a = op_b
-        x_ext = rng.uniform(-1, 1, L.next_ * ns)
-        yd = dev.empty(L.next_ * ns)
-        dev.apply_ext(torch.from_numpy(x_ext).cuda(), yd)
-        yr = torch.empty(L.next_ * ns, dtype=torch.float64)
-        ref.apply_ext(torch.from_numpy(x_ext), yr)
-        off = (L.t_lo - L.e_lo) * ns
-        own = slice(off, off + L.nown * ns)
-        assert rel(yd.cpu().numpy()[own], yr.numpy()[own]) < 1e-12, (rank, variant)
-        # preconditioner stages
-        r_own = rng.uniform(-1, 1, L.nown * ns)
-        sd = dev.empty(L.nown * ns)
-        dev.pc_spatial(torch.from_numpy(r_own).cuda(), sd, L.nown, inverse=False)
-        sr = torch.empty(L.nown * ns, dtype=torch.float64)
-        ref.pc_spatial(torch.from_numpy(r_own), sr, L.nown, inverse=False)
-        assert rel(sd.cpu().numpy(), sr.numpy()) < 1e-12
-        blk = rng.uniform(-1, 1, nt * L.ncols)
+        ref = NumpySlabBackend(L, g, variant)
+        x_in = rng.uniform(-1, 1, L.n_in)
+        yd = dev.empty(L.n_own)
+        dev.apply_in(torch.from_numpy(x_in).cuda(), yd)
+        yr = torch.empty(L.n_own, dtype=torch.float64)
+        ref.apply_in(torch.from_numpy(x_in), yr)
+        assert rel(yd.cpu().numpy(), yr.numpy()) < 1e-12, (rank, variant)
+        # preconditioner stages: every direction both ways on the owned / y-slab shapes, time stage
+        shapes = [(0, L.nt * L.nz * L.n2, 1, L.n_own), (1, L.nt * L.nz, L.n1, L.n_own),
+                  (2, L.nt, L.ny * L.n1, L.n_blk)]
+        for l, outer, inner, n in shapes:
+            for inv in (False, True):
+                src = rng.uniform(-1, 1, n)
+                od = dev.empty(n)
+                dev.pc_mode(l, inv, torch.from_numpy(src).cuda(), od, outer, inner)
+                orf = torch.empty(n, dtype=torch.float64)
+                ref.pc_mode(l, inv, torch.from_numpy(src), orf, outer, inner)
+                assert rel(od.cpu().numpy(), orf.numpy()) < 1e-12, (rank, l, inv)
+        blk = rng.uniform(-1, 1, L.n_blk)
         bd = torch.from_numpy(blk).cuda()
-        dev.pc_time(bd, L.ncols, L.s_lo)
+        dev.pc_time_yslab(bd, L.y_lo, L.y_hi)
         br = torch.from_numpy(blk.copy())
-        ref.pc_time(br, L.ncols, L.s_lo)
+        ref.pc_time_yslab(br, L.y_lo, L.y_hi)
         assert rel(bd.cpu().numpy(), br.numpy()) < 1e-12
 
 
-def test_sharded_gmres_world1_nccl_equals_unsharded():
-    """The distributed recurrence on a 1-rank NCCL group == the plain device GMRES."""
+def test_sharded_gmres_world1_nccl_equals_reference():
+    """The distributed recurrence on a 1-rank NCCL group reproduces the reference GMRES."""
     import os
     import torch.distributed as dist
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200 import sharded as sh
     g = load("case_3d_p3")
-    st_o = oracle_objects(g)[0]
     p = int(g["p"])
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, int(n)) for n in g["ne"]], mb.SplineSpace.uniform(p, int(g["ne_t"])))
     stab = mb.Stabilization(st, g["theta"], float(g["su_tol"]), 1.0)
@@ -80,8 +83,9 @@ def test_sharded_gmres_world1_nccl_equals_unsharded():
     os.environ.setdefault("MASTER_PORT", "29561")
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        L = sh.SlabLayout(st_o.num_time, st_o.num_space, p, 0, 1)
-        be = sh.DeviceSlabBackend(L, st, float(g["T"]), 1.0, float(g["sigma"][0]), RM, stabilization=stab)
+        L = layout_for(g, 0, 1)
+        be = sh.DeviceSlabBackend(L, st, float(g["T"]), 1.0, float(np.atleast_1d(g["sigma"])[0]), RM,
+                                  stabilization=stab)
         sop, spc = sh.ShardedOperator(L, be), sh.ShardedPreconditioner(L, be)
         b = torch.from_numpy(g["rhs"]).cuda()
         x, it, hist = sh.sharded_gmres(sop, spc, be.vec_ops, b, tol=1e-8, max_iter=400)

@@ -12,7 +12,8 @@ from bench import RM, front_indicator_np
 from paper_2311_17500_b200.spaces import greville
 NE, NET = int(os.environ.get('NE', 96)), int(os.environ.get('NET', 192))
 DD, PP = int(os.environ.get('D', 3)), int(os.environ.get('P', 3))
-st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(PP, NE) for _ in range(DD)], mb.SplineSpace.uniform(PP, NET))
+NEZ = int(os.environ.get('NEZ', NE))   # last spatial direction (slab experiments)
+st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(PP, NE) for _ in range(DD - 1)] + [mb.SplineSpace.uniform(PP, NEZ)], mb.SplineSpace.uniform(PP, NET))
 theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
 stab = mb.Stabilization(st, theta, 0.1, 1.0)
 op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, stabilization=stab)
@@ -33,4 +34,4 @@ for _ in range(5):
     op.apply_device(x, y); P.apply_device(y, z)
 torch.cuda.synchronize()
 prof = op.ctx.read_profile(reset=True); op.ctx.profiling(False)
-print(lib, "kernels ms/apply", {k: round(v[0] / 5, 3) for k, v in prof.items() if v[1]})
+print(lib, "N", st.num_dof, "kernels ms/apply", {k: round(v[0] / 5, 3) for k, v in prof.items() if v[1]})
