@@ -127,6 +127,9 @@ class ShardedOperator:
         self.x_in = backend.empty(layout.n_in)
 
     def apply_device(self, x_own, y_own):
+        if self.layout.world == 1:                   # no halo: the owned slab is the input slab
+            self.backend.apply_in(x_own, y_own)
+            return
         exchange_halo(self.layout, x_own, self.x_in, self.group)
         self.backend.apply_in(self.x_in, y_own)
 
@@ -195,12 +198,14 @@ class ShardedPreconditioner:
         # forward: U_1^T (contiguous), U_2^T (stride n_1) on the owned planes
         be.pc_mode(0, False, r_own, self.t1, L.nt * L.nz * L.n2, 1)
         be.pc_mode(1, False, self.t1, self.t2, L.nt * L.nz, L.n1)
-        blk = self._to_blk(self.t2)
+        # one rank: the owned slab already is the y-slab (no transposes)
+        blk = self.t2 if L.world == 1 else self._to_blk(self.t2)
         # y-slab: U_3^T (stride ny n_1), time stage in place, U_3
         be.pc_mode(2, False, blk, self.blk2, L.nt, L.ny * L.n1)
         be.pc_time_yslab(self.blk2, L.y_lo, L.y_hi)
         be.pc_mode(2, True, self.blk2, blk, L.nt, L.ny * L.n1)
-        self._from_blk(blk, self.t2)
+        if L.world > 1:
+            self._from_blk(blk, self.t2)
         be.pc_mode(1, True, self.t2, self.t1, L.nt * L.nz, L.n1)
         be.pc_mode(0, True, self.t1, z_own, L.nt * L.nz * L.n2, 1)
 
