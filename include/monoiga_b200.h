@@ -80,6 +80,16 @@ int mi_op_set_kron_channel(mi_ctx* ctx, int c, int nterms, const double* coef, c
 /* channel c spatial factor = sum_k theta[k] prod_l H_l[i_l, j_l-i_l+p, k_l-i_l+ko]
  * theta: host N_s (flat spatial order); H: host (d, nmax, 2p+1, 2ko+1). */
 int mi_op_set_su_channel(mi_ctx* ctx, int c, const double* theta, const double* H, int ko);
+/* Mapped (non-affine) geometry: channel c spatial factor assembled by
+ * tensor Gauss quadrature (replaces SpatialQuadratureData.mass/stiffness,
+ * assembly.py:197-219):
+ *   S[i, j] = sum_t coef[t] sum_k theta[t][k] prod_l T[t][l][i_l][j_l-i_l+p][k_l-(i_l-p) q_l]
+ * theta: host nterms x (Q_d ... Q_1) Gauss-grid weights (w |det J|, times the
+ * metric (J^-1 J^-T)_ab for stiffness terms); T: host nterms x d x nmax x
+ * (2p+1) x kw products of basis values / derivatives, kw = max_l (p+1) q_l;
+ * q[l] Gauss points per element, Q[l] in total (direction 1 first). */
+int mi_op_set_quad_channel(mi_ctx* ctx, int c, int nterms, const double* coef, const double* theta,
+                           const double* T, const int* q, const int* Q);
 /* y = A x   (x, y device, length N, must not alias) */
 int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
 
@@ -98,6 +108,11 @@ int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
 int mi_op_set_reaction(mi_ctx* ctx, const double* u, const double* w, double c1, double a, double c2,
                        const int* q, const int* nel, const double* B, const double* Wq);
 int mi_op_clear_reaction(mi_ctx* ctx);
+/* Mapped geometry: |det J| at the spatial Gauss points (host, C order
+ * Q_d ... Q_1) multiplies the reaction's quadrature weights
+ * (reaction_mass with spatial_data, assembly.py:320-326); NULL = box.
+ * Call after mi_op_set_reaction. */
+int mi_op_set_reaction_weight(mi_ctx* ctx, const double* jw);
 /* Time-sharded slabs: the reaction tables cover local time elements whose
  * full-basis function ft maps to local row ft + row_offset (default -1). */
 int mi_op_set_reaction_rows(mi_ctx* ctx, int row_offset);

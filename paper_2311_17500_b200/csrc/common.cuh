@@ -100,6 +100,8 @@ struct mi_ctx {
   size_t rx_Boff[4] = {0, 0, 0, 0}, rx_Woff[4] = {0, 0, 0, 0};
   int rx_rowoff = -1;          // constrained row of full time function ft = ft + rx_rowoff
   int rx_q[4] = {1, 1, 1, 1}, rx_p[4] = {0, 0, 0, 0}, rx_nel[4] = {1, 1, 1, 1}, rx_E[4] = {1, 1, 1, 1};
+  mi::DeviceBuf rx_jw;          // mapped geometry: |det J| on the spatial Gauss grid (Q_d .. Q_1); empty = box
+  bool rx_mapped = false;
 
   // ---- preconditioner
   bool pc_ready = false;

@@ -130,6 +130,74 @@ __global__ void build_su_channel(double* __restrict__ out, const double* __restr
   out[(long long)s * g.ns + i] = v;
 }
 
+// Mapped-geometry spatial factors (SpatialQuadratureData.mass / .stiffness, assembly.py:197-219):
+//   S[i, j] = sum_t coef_t sum_k theta_t[k] prod_l T_{t,l}[i_l, j_l - i_l + p, k_l - (i_l - p) q_l]
+// over the tensor Gauss grid k (q_l points per element, Q_l in total).  theta_t = w |det J| (mass) or
+// w |det J| (J^-1 J^-T)_ab (stiffness term a, b); T_{t,l}[i, a, b] = B^(o)_i(x_k) B^(o')_j(x_k) with the
+// derivative orders of the term.  Function i's support covers the Gauss points
+// [(i - p) q_l, (i + 1) q_l): KW_l = (p + 1) q_l window entries.
+struct QuadSpec {
+  int q[3], Q[3];       // Gauss points per element / in total, per direction (1 beyond d)
+  int kw;               // window length (max over directions) = row stride of the T tables
+  long long nq;         // Q_1 Q_2 Q_3
+};
+
+template <int D, int P>
+__global__ void build_quad_channel(double* __restrict__ out, const double* __restrict__ coef,
+                                   const double* __restrict__ theta, const double* __restrict__ T, int nterms,
+                                   int nmax, QuadSpec qs, Dims g) {
+  using ST = Sten<D, P>;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (i >= g.ns) return;
+  const int a1 = s % ST::W1, a2 = (s / ST::W1) % ST::W2, a3 = s / (ST::W1 * ST::W2);
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2)) + g.z_lo;
+  const int ii[3] = {i1, i2, i3};
+  const int aa[3] = {a1, a2, a3};
+  const int nn[3] = {g.n1, g.n2, g.n3g};
+  const int W = 2 * P + 1;
+  bool inside = true;
+#pragma unroll
+  for (int l = 0; l < D; ++l) {
+    int j = ii[l] + aa[l] - P;
+    inside = inside && j >= 0 && j < nn[l];
+  }
+  double v = 0.0;
+  if (inside) {
+    const int kw1 = (P + 1) * qs.q[0];
+    const int kw2 = D >= 2 ? (P + 1) * qs.q[1] : 1, kw3 = D >= 3 ? (P + 1) * qs.q[2] : 1;
+    for (int t = 0; t < nterms; ++t) {
+      const double* th = theta + (long long)t * qs.nq;
+      const double* h[3];
+#pragma unroll
+      for (int l = 0; l < D; ++l) h[l] = T + ((((long long)t * D + l) * nmax + ii[l]) * W + aa[l]) * qs.kw;
+      double vt = 0.0;
+      for (int b3 = 0; b3 < kw3; ++b3) {
+        const int k3 = D >= 3 ? (i3 - P) * qs.q[2] + b3 : 0;
+        if (k3 < 0 || k3 >= qs.Q[2]) continue;
+        const double h3 = D >= 3 ? h[2][b3] : 1.0;
+        if (h3 == 0.0) continue;
+        for (int b2 = 0; b2 < kw2; ++b2) {
+          const int k2 = D >= 2 ? (i2 - P) * qs.q[1] + b2 : 0;
+          if (k2 < 0 || k2 >= qs.Q[1]) continue;
+          const double h23 = h3 * (D >= 2 ? h[1][b2] : 1.0);
+          if (h23 == 0.0) continue;
+          const double* tr = th + ((long long)k3 * qs.Q[1] + k2) * qs.Q[0];
+          double acc = 0.0;
+          for (int b1 = 0; b1 < kw1; ++b1) {
+            const int k1 = (i1 - P) * qs.q[0] + b1;
+            if (k1 < 0 || k1 >= qs.Q[0]) continue;
+            acc += tr[k1] * h[0][b1];
+          }
+          vt += h23 * acc;
+        }
+      }
+      v += coef[t] * vt;
+    }
+  }
+  out[(long long)s * g.ns + i] = v;
+}
+
 // ---------------------------------------------------------------- apply
 // W_c[t, i] = sum_s S_c[s, i] x[t, i + off(s)], channels in groups of CG,
 // TC time slices per thread.
@@ -283,6 +351,44 @@ int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H
   MI_CUDA(cudaStreamSynchronize(c->stream));
   dfree(dt);
   dfree(dh);
+  return MI_OK;
+}
+
+int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta,
+                           const double* T, const int* q, const int* Q) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
+  MI_REQUIRE(nterms >= 1 && coef && theta && T && q && Q, MI_ERR_ARG, "bad quadrature channel arguments");
+  QuadSpec qs{};
+  qs.nq = 1;
+  int kw = 1;
+  for (int l = 0; l < 3; ++l) {
+    qs.q[l] = l < c->d ? q[l] : 1;
+    qs.Q[l] = l < c->d ? Q[l] : 1;
+    MI_REQUIRE(qs.q[l] >= 1 && qs.Q[l] >= 1, MI_ERR_ARG, "quadrature sizes must be positive");
+    if (l < c->d) kw = max(kw, (c->p + 1) * qs.q[l]);
+    qs.nq *= qs.Q[l];
+  }
+  qs.kw = kw;
+  const int nmax = table_rows(c);
+  const size_t nT = (size_t)nterms * c->d * nmax * (2 * c->p + 1) * kw;
+  DeviceBuf dc, dth, dT;
+  int rc;
+  if ((rc = dalloc(dc, nterms)) || (rc = dalloc(dth, (size_t)nterms * qs.nq)) || (rc = dalloc(dT, nT))) return rc;
+  MI_CUDA(cudaMemcpyAsync(dc.p, coef, sizeof(double) * nterms, cudaMemcpyHostToDevice, c->stream));
+  MI_CUDA(cudaMemcpyAsync(dth.p, theta, sizeof(double) * nterms * qs.nq, cudaMemcpyHostToDevice, c->stream));
+  MI_CUDA(cudaMemcpyAsync(dT.p, T, sizeof(double) * nT, cudaMemcpyHostToDevice, c->stream));
+  Dims g = dims_of(c);
+  dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
+  double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
+  MI_DISPATCH_DP(c->d, c->p, (build_quad_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dc.p, dth.p, dT.p, nterms,
+                                                                                      nmax, qs, g)));
+  MI_CHECK_LAUNCH("build_quad_channel");
+  c->frag_dirty = true;
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  dfree(dc);
+  dfree(dth);
+  dfree(dT);
   return MI_OK;
 }
 

@@ -39,6 +39,7 @@ struct RxArgs {
   int rowoff;          // row of full time function ft is ft + rowoff (-1 unsharded)
   long long ns;
   double c1, a, c2;
+  const double* jw;    // mapped geometry: |det J| at the spatial Gauss points, C order (Q_3, Q_2, Q_1); null: box
 };
 
 // R5: time-streamed sum factorisation.  The block still owns a 2^d tile of
@@ -143,6 +144,15 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, 512 / RxTile<D, P>::NTH) re
         v = wgt(D - 1, ql);
         if (D == 3) v *= wgt(0, line % Q1) * wgt(1, line / Q1);
         if (D == 2) v *= wgt(0, line);
+        if (r.jw != nullptr && v != 0.0) {
+          // global Gauss index of this point: element k[l] + local element, QE points per element
+          int gq[3] = {0, 0, 0};
+          if (D == 3) { gq[0] = k[0] * QE + line % Q1; gq[1] = k[1] * QE + line / Q1; gq[2] = k[2] * QE + ql; }
+          if (D == 2) { gq[0] = k[0] * QE + line; gq[1] = k[1] * QE + ql; }
+          if (D == 1) { gq[0] = k[0] * QE + ql; }
+          const long long G1 = (long long)r.nel[0] * QE, G2 = D >= 2 ? (long long)r.nel[1] * QE : 1;
+          v *= __ldg(r.jw + ((long long)gq[2] * G2 + gq[1]) * G1 + gq[0]);
+        }
       }
       wsp[mi][e] = v;
     }
@@ -464,6 +474,7 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   r.c1 = c->c1;
   r.a = c->a;
   r.c2 = c->c2;
+  r.jw = c->rx_mapped ? c->rx_jw.p : nullptr;
   MI_RX_DISPATCH(c->d, c->p, c->pt, {
     using G = RxTile<D_, P_>;
     constexpr size_t smem = G::SMEM;
@@ -512,6 +523,7 @@ extern "C" {
 
 int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, double a, double c2,
                        const int* q, const int* nel, const double* B, const double* Wq) {
+  if (c) c->rx_mapped = false;    // a mapped weight is re-attached by mi_op_set_reaction_weight
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(u && w && q && nel && B && Wq, MI_ERR_ARG, "NULL argument to mi_op_set_reaction");
   int rc;
@@ -556,6 +568,22 @@ int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, d
   for (int l = 0; l < 4; ++l)
     MI_REQUIRE(c->rx_q[l] == ((l == 3 || l < c->d) ? c->p + 1 : 1), MI_ERR_ARG, "reaction: need q = p + 1");
   c->reaction_on = true;
+  return MI_OK;
+}
+
+int mi_op_set_reaction_weight(mi_ctx* c, const double* jw) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  if (jw == nullptr) {
+    c->rx_mapped = false;
+    return MI_OK;
+  }
+  MI_REQUIRE(c->ns_in == c->ns, MI_ERR_ARG, "mapped reaction weights are not supported on z-slab contexts");
+  size_t nq = 1;
+  for (int l = 0; l < c->d; ++l) nq *= (size_t)c->rx_nel[l] * c->rx_q[l];
+  int rc;
+  if ((rc = dalloc(c->rx_jw, nq))) return rc;
+  MI_CUDA(cudaMemcpy(c->rx_jw.p, jw, sizeof(double) * nq, cudaMemcpyHostToDevice));
+  c->rx_mapped = true;
   return MI_OK;
 }
 

@@ -253,6 +253,26 @@ def spatial_eigs(st, lengths=None):
     return out
 
 
+def mapped_spatial_eigs(sd):
+    """linalg.py:286-297 on a mapped geometry: eigh(K_l, M_l) of the univariate factors weighted by
+    the separable surrogates of the pulled-back measures (geometry.separable_weights), on the
+    q = p+1 Gauss rule of the mesh (the rule of SpatialQuadratureData)."""
+    from .geometry import separable_weights
+    from .spaces import gram
+    w_mass, w_stiff = separable_weights(sd)
+    out = []
+    for l, s in enumerate(sd.spaces):
+        x, w = sd.rules[l]
+        M = gram(s, 0, 0, x, w * w_mass[l])
+        K = gram(s, 1, 1, x, w * w_stiff[l])
+        try:
+            lam, U = sla.eigh(K, M)
+        except sla.LinAlgError as exc:
+            raise DecompositionError("generalized eigendecomposition failed: %s" % exc) from exc
+        out.append((U, lam))
+    return out
+
+
 class RealTimePencil:
     """Bordered time pencil in real 2x2-block form.
 

@@ -1,0 +1,228 @@
+"""Mapped (non-affine) spatial geometries.
+
+``GeometryMap`` restates the reference's tensor-product spline map
+(geometry.py:31-206): control net in colexicographic order (direction 1
+fastest), values and Jacobians on tensor grids of parametric points.
+``load_geometry`` / ``save_geometry`` read and write the reference's plain-text
+control-point format (geometry.py:309-344), so a geometry built with the
+reference (e.g. its ellipse annulus) is used unchanged here.
+
+``MappedSpatialData`` is the host side of the reference's
+SpatialQuadratureData (assembly.py:137-219) as the device path needs it:
+q = p+1 Gauss rules on the solution mesh, per-direction basis tables, and
+at every tensor quadrature point the weight w |det J| and the pulled-back
+metric J^-1 J^-T.  The spatial mass / stiffness stencils, the reaction
+weight and the load vector are generated from these on the device; the
+reference assembles N_s x N_s CSR matrices instead.
+"""
+
+import numpy as np
+
+from .spaces import SplineSpace, basis_table, gauss_rule
+
+SINGULAR_REL_TOL = 1e-12
+
+
+class GeometryError(RuntimeError):
+    """Singular or invalid geometry map (geometry.py:27-28)."""
+
+
+class GeometryMap:
+    """Tensor-product spline map from [0, 1]^d to the physical domain (geometry.py:31-66)."""
+
+    def __init__(self, spaces, control_points, final_time=1.0, affine_scales=None):
+        self.spaces = tuple(spaces)
+        self.dim = len(self.spaces)
+        n = int(np.prod([s.dimension for s in self.spaces]))
+        cp = np.asarray(control_points, dtype=float)
+        if cp.shape != (n, self.dim):
+            raise ValueError("control_points must have shape (%d, %d)" % (n, self.dim))
+        if final_time <= 0:
+            raise ValueError("final_time must be positive")
+        self.control_points = cp
+        self.final_time = float(final_time)
+        self.affine_scales = affine_scales
+        self._grid = cp.reshape(tuple(s.dimension for s in reversed(self.spaces)) + (self.dim,))
+
+    def grid_data(self, axes, order=1):
+        """x (grid + (d,)) and, for order >= 1, jac (grid + (d, d)) with jac[..., c, a] = dF_c/deta_a;
+        grid axes in C order (direction d first), like geometry.py:135-186."""
+        if order > 1:
+            raise NotImplementedError("Hessians are not needed on the device path")
+        d = self.dim
+        tabs = [[basis_table(s, np.asarray(ax, float), o) for o in range(order + 1)]
+                for s, ax in zip(self.spaces, axes)]
+
+        def tabulate(orders):
+            val = self._grid
+            for l in range(d):
+                ax = d - 1 - l
+                val = np.moveaxis(np.tensordot(tabs[l][orders[l]], val, axes=(1, ax)), 0, ax)
+            return val
+
+        out = {"x": tabulate([0] * d)}
+        if order >= 1:
+            jac = np.empty(out["x"].shape[:-1] + (d, d))
+            for a in range(d):
+                orders = [0] * d
+                orders[a] = 1
+                jac[..., a] = tabulate(orders)
+            out["jac"] = jac
+        return out
+
+
+def jacobian_inverse_and_det(jac):
+    """geometry.py:207-214."""
+    det = np.linalg.det(jac)
+    scale = np.prod(np.linalg.norm(jac, axis=-2), axis=-1)
+    if np.any(np.abs(det) < SINGULAR_REL_TOL * np.maximum(scale, 1e-300)):
+        raise GeometryError("singular Jacobian encountered during pull-back")
+    return np.linalg.inv(jac), det
+
+
+def save_geometry(geo, path):
+    """geometry.py:309-323: dimension; degrees; knot counts; knot lines; control points."""
+    lines = [str(geo.dim), " ".join(str(s.degree) for s in geo.spaces),
+             " ".join(str(s.knots.size) for s in geo.spaces)]
+    for s in geo.spaces:
+        lines.append(" ".join("%.17g" % k for k in s.knots))
+    for row in geo.control_points:
+        lines.append(" ".join("%.17g" % v for v in row))
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def load_geometry(path, final_time=1.0):
+    """geometry.py:326-344."""
+    with open(path) as fh:
+        tokens = [ln.split() for ln in fh if ln.strip() and not ln.startswith("#")]
+    d = int(tokens[0][0])
+    degrees = [int(v) for v in tokens[1][:d]]
+    counts = [int(v) for v in tokens[2][:d]]
+    spaces = [SplineSpace(np.array([float(v) for v in tokens[3 + l][:counts[l]]]), degrees[l]) for l in range(d)]
+    n = int(np.prod([s.dimension for s in spaces]))
+    rows = tokens[3 + d:3 + d + n]
+    if len(rows) != n:
+        raise ValueError("geometry file has %d control rows, expected %d" % (len(rows), n))
+    return GeometryMap(spaces, np.array([[float(v) for v in r[:d]] for r in rows]), final_time=final_time)
+
+
+def is_mapped(geometry):
+    return isinstance(geometry, GeometryMap) and geometry.affine_scales is None
+
+
+class MappedSpatialData:
+    """Quadrature data of a mapped geometry on the solution mesh (assembly.py:137-219)."""
+
+    def __init__(self, spatial_spaces, geometry):
+        self.spaces = tuple(spatial_spaces)
+        d = len(self.spaces)
+        if geometry.dim != d:
+            raise ValueError("geometry dimension %d != number of spatial directions %d" % (geometry.dim, d))
+        self.geo = geometry
+        self.q = [s.degree + 1 for s in self.spaces]
+        self.rules = [gauss_rule(s.breakpoints, s.degree + 1) for s in self.spaces]   # (points, weights)
+        data = geometry.grid_data([r[0] for r in self.rules], order=1)
+        self.xgrid = data["x"]
+        self.jinv, self.detj = jacobian_inverse_and_det(data["jac"])
+        w = np.ones(())
+        for l in reversed(range(d)):
+            w = np.multiply.outer(w, self.rules[l][1])
+        self.wgrid = w                                        # (Q_d, ..., Q_1)
+        self.grid_shape = self.wgrid.shape
+
+    def measure(self):
+        """w |det J| on the grid."""
+        return self.wgrid * np.abs(self.detj)
+
+    def metric(self, a, b):
+        """(J^-1 J^-T)_{ab} on the grid."""
+        return np.einsum("...k,...k->...", self.jinv[..., a, :], self.jinv[..., b, :])
+
+    def metric_diag(self, direction):
+        return self.metric(direction, direction)
+
+    def physical_points(self):
+        return self.xgrid.reshape(-1, len(self.spaces))
+
+    def tables(self, l, order):
+        """(Q_l, n_l) basis table of direction l (collocation_matrix, assembly.py:157-160)."""
+        return basis_table(self.spaces[l], self.rules[l][0], order)
+
+
+def quad_tables(sd, orders, p, nmax):
+    """Basis-product tables of the quadrature channel generator (mi_op_set_quad_channel):
+    T[t, l, i, a, b] = B^(o)_i(x_k) B^(o')_j(x_k), j = i + a - p, k = (i - p) q_l + b, for the
+    derivative orders ``orders[t][l] = (o, o')`` of term t."""
+    d = len(sd.spaces)
+    kw = max((p + 1) * q for q in sd.q)
+    T = np.zeros((len(orders), d, nmax, 2 * p + 1, kw))
+    for l in range(d):
+        n, q = sd.spaces[l].dimension, sd.q[l]
+        Q = sd.rules[l][0].size
+        i = np.arange(n)[:, None, None]
+        a = np.arange(2 * p + 1)[None, :, None]
+        b = np.arange((p + 1) * q)[None, None, :]
+        j = i + a - p
+        k = (i - p) * q + b
+        ok = (j >= 0) & (j < n) & (k >= 0) & (k < Q)
+        jj, kk = np.where(ok, j, 0), np.where(ok, k, 0)
+        ii = np.broadcast_to(i, ok.shape)
+        tabs = {}
+        for t, ords in enumerate(orders):
+            oi, oj = ords[l]
+            for o in (oi, oj):
+                if o not in tabs:
+                    tabs[o] = sd.tables(l, o)
+            T[t, l, :n, :, :(p + 1) * q] = np.where(ok, tabs[oi][kk, ii] * tabs[oj][kk, jj], 0.0)
+    return np.ascontiguousarray(T)
+
+
+def mass_terms(sd):
+    """(coef, theta, orders) of M_s = C^T diag(w |det J|) C (assembly.py:197-203)."""
+    d = len(sd.spaces)
+    return [(1.0, sd.measure(), [(0, 0)] * d)]
+
+
+def stiffness_terms(sd, coef=1.0):
+    """K_s = sum_ab C_a^T diag(w |det J| (J^-1 J^-T)_ab) C_b (assembly.py:205-219): the test function
+    carries the derivative in direction a, the trial function the one in direction b."""
+    d = len(sd.spaces)
+    base = sd.measure()
+    terms = []
+    for a in range(d):
+        for b in range(d):
+            orders = [(1 if l == a else 0, 1 if l == b else 0) for l in range(d)]
+            terms.append((coef, base * sd.metric(a, b), orders))
+    return terms
+
+
+def separable_weights(sd):
+    """Rank-one per-direction surrogates of the pulled-back measures (FastDiagPreconditioner.
+    _separable_weights, linalg.py:228-262): mass[l] approximates |det J| multiplicatively, stiff[l]
+    the metric coefficient (J^-1 J^-T)_ll |det J| relative to the other directions' mass weights."""
+    d = len(sd.spaces)
+    detj = np.abs(sd.detj)
+    log_detj = np.log(detj)
+    grand = log_detj.mean()
+    mass = []
+    for l in range(d):
+        axis = d - 1 - l
+        other = tuple(x for x in range(d) if x != axis)
+        main = log_detj.mean(axis=other) if other else log_detj
+        mass.append(np.exp(main - grand + grand / d))
+    stiff = []
+    for l in range(d):
+        axis = d - 1 - l
+        coeff = detj * sd.metric_diag(l)
+        denom = np.ones_like(coeff)
+        for m in range(d):
+            if m == l:
+                continue
+            shape = [1] * d
+            shape[d - 1 - m] = mass[m].size
+            denom = denom * mass[m].reshape(shape)
+        ratio = coeff / denom
+        other = tuple(x for x in range(d) if x != axis)
+        stiff.append(ratio.mean(axis=other) if other else ratio)
+    return mass, stiff

@@ -69,13 +69,24 @@ class KroneckerOperator:
 
     def __init__(self, space_time, final_time, capacitance=1.0, diffusion=1e-4, constants=None,
                  u=None, w=None, stabilization=None, lengths=None, device=0, context=None, time_rows=None,
-                 z_planes=None):
+                 z_planes=None, spatial_data=None):
         """``time_rows=(e_lo, e_hi)`` builds the operator restricted to a slab of
         constrained time rows: the time bands are the global rows e_lo..e_hi, and
         u, w (if given) are slab vectors.  ``z_planes=(z_lo, z_hi)`` (d = 3) builds
         the z-slab operator of the space-sharded solve (sharded.py): it maps an input
         slab (the owned planes plus up to p halo planes on each side, all time rows)
-        to the owned planes of A x; u, w (if given) are input-slab vectors."""
+        to the owned planes of A x; u, w (if given) are input-slab vectors.
+        ``spatial_data`` (a geometry.MappedSpatialData) selects a mapped geometry: M_s and K_s are
+        then assembled by Gauss quadrature on the device (SpatialQuadratureData.mass/stiffness,
+        assembly.py:197-219) and the reaction carries |det J| (assembly.py:320-326)."""
+        sd = spatial_data
+        if sd is not None:
+            if z_planes is not None or time_rows is not None:
+                raise NotImplementedError("mapped geometries are not sharded")
+            if stabilization is not None and stabilization.rank:
+                raise NotImplementedError("Spline Upwind on mapped geometries is not built")
+            if np.atleast_1d(np.asarray(diffusion, float)).size != 1:
+                raise ValueError("mapped geometries take a scalar diffusion (the reference's D)")
         st = space_time
         nt_glob = st.time.dimension - 1
         self.time_rows = (0, nt_glob) if time_rows is None else tuple(int(v) for v in time_rows)
@@ -131,26 +142,49 @@ class KroneckerOperator:
                     out[t, l, :row[l].shape[0]] = row[l]
             return np.ascontiguousarray(out)
 
-        c0 = np.array([1.0])
-        b0 = pack([Mb])
-        _lib.call("mi_op_set_kron_channel", ctx.handle, 0, 1, host_ptr(c0), host_ptr(b0))
-        rows, coefs = [], []
-        for a in range(d):
-            rows.append([Kb[l] if l == a else Mb[l] for l in range(d)])
-            coefs.append(sig[a])
-        if react != 0.0:
-            rows.append(list(Mb))
-            coefs.append(react)
-        c1 = np.asarray(coefs, float)
-        b1 = pack(rows)
-        _lib.call("mi_op_set_kron_channel", ctx.handle, 1, len(rows), host_ptr(c1), host_ptr(b1))
+        if sd is not None:
+            # c0 = M_s, c1 = D K_s (+ a c1 M_s at the zero iterate), by quadrature on the device
+            from .geometry import mass_terms, quad_tables, stiffness_terms
+            qh = np.asarray(sd.q, dtype=np.int32)
+            Qh = np.asarray([r[0].size for r in sd.rules], dtype=np.int32)
+
+            def quad(ch, terms):
+                coef = np.asarray([t[0] for t in terms], float)
+                theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
+                T = quad_tables(sd, [t[2] for t in terms], p, nmax)
+                _lib.call("mi_op_set_quad_channel", ctx.handle, ch, len(terms), host_ptr(coef), host_ptr(theta),
+                          host_ptr(T), host_ptr(qh), host_ptr(Qh))
+
+            quad(0, mass_terms(sd))
+            t1 = stiffness_terms(sd, float(sig[0]))
+            if react != 0.0:
+                t1 += [(react, sd.measure(), [(0, 0)] * d)]
+            quad(1, t1)
+        else:
+            c0 = np.array([1.0])
+            b0 = pack([Mb])
+            _lib.call("mi_op_set_kron_channel", ctx.handle, 0, 1, host_ptr(c0), host_ptr(b0))
+            rows, coefs = [], []
+            for a in range(d):
+                rows.append([Kb[l] if l == a else Mb[l] for l in range(d)])
+                coefs.append(sig[a])
+            if react != 0.0:
+                rows.append(list(Mb))
+                coefs.append(react)
+            c1 = np.asarray(coefs, float)
+            b1 = pack(rows)
+            _lib.call("mi_op_set_kron_channel", ctx.handle, 1, len(rows), host_ptr(c1), host_ptr(b1))
         for r in range(R):
             th = np.ascontiguousarray(stab.theta[r])
             H = np.ascontiguousarray(stab.H)
             _lib.call("mi_op_set_su_channel", ctx.handle, 2 + r, host_ptr(th), host_ptr(H), stab.ko)
         if not zero_iterate:
             from .reaction import set_reaction
-            set_reaction(ctx, st, final_time, consts, u, w, L, time_rows=self.time_rows, zslab=ctx.zslab)
+            set_reaction(ctx, st, final_time, consts, u, w, None if sd is not None else L,
+                         time_rows=self.time_rows, zslab=ctx.zslab)
+            if sd is not None:
+                jw = np.ascontiguousarray(np.abs(sd.detj))
+                _lib.call("mi_op_set_reaction_weight", ctx.handle, host_ptr(jw))
         else:
             _lib.call("mi_op_clear_reaction", ctx.handle)    # a reused context may carry one
 

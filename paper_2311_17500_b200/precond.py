@@ -12,7 +12,7 @@ import torch
 
 from . import _lib
 from .device import DeviceContext, dptr, host_ptr
-from .factors import spatial_eigs, time_pencil
+from .factors import mapped_spatial_eigs, spatial_eigs, time_pencil
 
 
 class FastDiagPreconditioner:
@@ -54,10 +54,15 @@ class FastDiagPreconditioner:
     @classmethod
     def build(cls, space_time, final_time, capacitance, diffusion, reaction, spatial_data=None,
               lengths=None, device=0, context=None):
-        """linalg.py:264-307 for box geometries (spatial_data is accepted for
-        signature compatibility; on boxes its separable weights are the
-        constants applied by factors.spatial_eigs)."""
-        eigs = spatial_eigs(space_time, lengths)
+        """linalg.py:264-307.  Boxes: the separable weights are the constants applied by
+        factors.spatial_eigs (``spatial_data`` may be omitted).  Mapped geometries: pass a
+        geometry.MappedSpatialData; the per-direction factors are weighted by the rank-one
+        surrogates of |det J| and of the metric (linalg.py:228-262, 286-296)."""
+        from .geometry import MappedSpatialData
+        if isinstance(spatial_data, MappedSpatialData):
+            eigs = mapped_spatial_eigs(spatial_data)
+        else:
+            eigs = spatial_eigs(space_time, lengths)
         pen = time_pencil(space_time, final_time)
         return cls(space_time, eigs, pen, capacitance, diffusion, reaction, device, context)
 

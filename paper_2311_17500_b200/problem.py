@@ -209,8 +209,14 @@ class GaussGrid:
     """Default Gauss rules (q = p+1) of every direction with basis tables."""
 
     def __init__(self, st, geometry):
+        from .geometry import MappedSpatialData, is_mapped
         self.st = st
-        self.L, self.off = box_of(geometry)
+        # mapped geometries: parametric rules, physical points and |det J| from the map
+        self.mapped = MappedSpatialData(st.spatial, geometry) if is_mapped(geometry) else None
+        if self.mapped is None:
+            self.L, self.off = box_of(geometry)
+        else:
+            self.L, self.off = np.ones(len(st.spatial)), np.zeros(len(st.spatial))
         self.T = geometry.final_time
         self.d = len(st.spatial)
         self.sx, self.sw, self.sB = [], [], []
@@ -233,6 +239,8 @@ class GaussGrid:
         return out
 
     def physical_points(self):
+        if self.mapped is not None:
+            return self.mapped.physical_points()
         d = self.d
         mesh = np.meshgrid(*[self.off[l] + self.L[l] * self.sx[l] for l in reversed(range(d))], indexing="ij")
         return np.stack([mesh[d - 1 - l].ravel() for l in range(d)], axis=-1)
@@ -297,9 +305,12 @@ def load_vector(st, geometry, source, grid=None, chunk_points=1 << 24, chunks=No
         return np.zeros(st.num_dof)
     g = grid if grid is not None else GaussGrid(st, geometry)
     d = g.d
-    ws = np.asarray(g.sw[d - 1] * g.L[d - 1])
-    for l in reversed(range(d - 1)):
-        ws = np.multiply.outer(ws, g.sw[l] * g.L[l])
+    if g.mapped is not None:
+        ws = g.mapped.measure()                        # w |det J| (rhs_vectors, assembly.py:385-387)
+    else:
+        ws = np.asarray(g.sw[d - 1] * g.L[d - 1])
+        for l in reversed(range(d - 1)):
+            ws = np.multiply.outer(ws, g.sw[l] * g.L[l])
     if chunks is None:
         rows_per = max(1, chunk_points // max(1, ws.size))
         if device_capable(source):
@@ -356,6 +367,8 @@ def compute_theta(problem, u, w, grid=None):
     """Residual indicator (stabilization.py:235-339) on a box geometry."""
     st = problem.space
     g = grid if grid is not None else GaussGrid(st, problem.geometry)
+    if g.mapped is not None:
+        raise NotImplementedError("the residual indicator on mapped geometries (map Hessians) is not built")
     d, T = g.d, g.T
     zero = [0] * d
     u_val = g.field(u, zero, 0)

@@ -202,3 +202,70 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fixed_point"
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "theta":
     theta_cases()
+
+
+def warped_cube_geometry(final_time=1.0):
+    """A curved 3D map: degree-2 tensor spline whose control net is the Greville grid of the unit
+    cube pushed through a smooth bijection (det J > 0)."""
+    from monoiga.geometry import GeometryMap
+    spaces = [SplineSpace.uniform(2, 2) for _ in range(3)]
+    g = [s.greville() for s in spaces]
+    Z, Y, X = np.meshgrid(g[2], g[1], g[0], indexing="ij")
+    x = X + 0.08 * np.sin(np.pi * Y) * (1.0 + Z)
+    y = Y * (1.0 + 0.25 * X) + 0.05 * Z
+    z = Z * (1.0 + 0.2 * X * Y) - 0.06 * np.sin(np.pi * X)
+    ctrl = np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1)
+    return GeometryMap(spaces, ctrl, final_time=final_time)
+
+
+def smooth_source(x, t):
+    return np.exp(-((x[:, 0] - 0.3) ** 2 + (x[:, 1] - 0.2) ** 2) / 0.05) * (t < 0.4)
+
+
+def mapped_cases():
+    """Mapped (non-affine) geometries: SpatialQuadratureData mass/stiffness, the reaction mass, the
+    separable-weight preconditioner, GMRES and the load vector."""
+    from monoiga.assembly import rhs_vectors
+    from monoiga.geometry import builtin_geometry, save_geometry
+    out = {}
+    geos = {"annulus": builtin_geometry("ellipse_annulus", final_time=1.0), "warped": warped_cube_geometry()}
+    for key, geo in geos.items():
+        save_geometry(geo, os.path.join(HERE, "geo_%s.txt" % key))
+    cases = [("m2d", "annulus", 2, (8, 3), 4, 1e-3, 41), ("m3d_p2", "warped", 2, (3, 3, 4), 3, 1e-2, 42),
+             ("m3d_p3", "warped", 3, (2, 2, 3), 3, 1e-2, 43)]
+    for name, gkey, p, nes, ne_t, D, seed in cases:
+        rng = np.random.default_rng(seed)
+        geo = geos[gkey]
+        T = 1.0
+        st = SpaceTimeSpace([SplineSpace.uniform(p, n) for n in nes], SplineSpace.uniform(p, ne_t))
+        N, nt, ns = st.num_dof, st.num_time, st.num_space
+        sd = SpatialQuadratureData(st.spatial, geo)
+        M_s, K_s = sd.mass(), sd.stiffness()
+        W_t, M_t = time_matrices(st, T)
+        react = RM["a"] * RM["c1"]
+        x = rng.uniform(-1, 1, N)
+        u = rng.uniform(0, 1, N)
+        w = rng.uniform(0, 0.1, N)
+        rhs = rng.standard_normal(N)
+        op_a = KroneckerOperator(nt, ns, [(1.0, W_t, M_s), (D, M_t, K_s), (react, M_t, M_s)])
+        MR = reaction_mass(st, geo, RM, u, w, spatial_data=sd)
+        op_b = KroneckerOperator(nt, ns, [(1.0, W_t, M_s), (D, M_t, K_s)], correction=MR)
+        P = FastDiagPreconditioner.build(st, T, 1.0, D, react, spatial_data=sd)
+        wm, wk = FastDiagPreconditioner._separable_weights(sd)
+        f, _ = rhs_vectors(st, geo, smooth_source, np.zeros(N), 0.013, spatial_data=sd)
+        rec = {"geo": gkey, "p": p, "ne": np.array(nes), "ne_t": ne_t, "D": D, "x": x, "u": u, "w": w,
+               "rhs": rhs, "M_s": M_s.toarray(), "K_s": K_s.toarray(), "y_a": op_a.matvec(x), "y_b": op_b.matvec(x),
+               "y_mr": MR @ x, "z_pc": P.apply(x), "f": f, "detj": sd.detj, "xq": sd.xgrid}
+        for l in range(len(nes)):
+            rec["wmass%d" % l], rec["wstiff%d" % l] = wm[l], wk[l]
+        sol, it, hist = gmres(op_a, rhs, precond=P, tol=1e-8, max_iter=400)
+        rec.update(gm_a_x=sol, gm_a_it=it, gm_a_hist=np.array(hist))
+        sol, it, hist = gmres(op_b, rhs, precond=P, tol=1e-8, max_iter=400)
+        rec.update(gm_b_x=sol, gm_b_it=it, gm_b_hist=np.array(hist))
+        out.update({name + "_" + k: v for k, v in rec.items()})
+        print(name, "N=%d gmres a/b %d/%d" % (N, rec["gm_a_it"], it), "detJ in [%.3f, %.3f]" % (sd.detj.min(), sd.detj.max()))
+    np.savez_compressed(os.path.join(HERE, "mapped.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "mapped":
+    mapped_cases()
