@@ -29,10 +29,16 @@ class _Workspace:
     """solver.py:163-211 (box geometry, device objects)."""
 
     def __init__(self, problem, config, device=0):
+        from .geometry import MappedSpatialData, is_mapped
         st = problem.space
         if config.linear_solver == "direct":
             raise NotImplementedError("the direct (host LU) linear solver is not part of the device path")
-        self.L, _ = box_of(problem.geometry)
+        # mapped geometries: quadrature M_s / K_s, |det J| reaction, separable-weight P^-1 (solver.py:167-202)
+        self.sd = MappedSpatialData(st.spatial, problem.geometry) if is_mapped(problem.geometry) else None
+        if self.sd is not None and config.stabilization == "spline_upwind":
+            raise NotImplementedError("Spline Upwind on mapped geometries is not built (the residual indicator "
+                                      "needs the map's Hessians)")
+        self.L = None if self.sd is not None else box_of(problem.geometry)[0]
         self.device = device
         self.indicator = DeviceIndicator(problem, device) if config.stabilization == "spline_upwind" else None
         if self.indicator is not None and problem.source is not None:
@@ -46,12 +52,13 @@ class _Workspace:
             self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid, device=device)
         self.pc_ctx = DeviceContext(st, device)
         self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.D,
-                                                    problem.a * problem.c1, lengths=self.L, context=self.pc_ctx)
+                                                    problem.a * problem.c1, lengths=self.L, context=self.pc_ctx,
+                                                    spatial_data=self.sd)
         # M_t (x) M_s for g = b (M_t (x) M_s) u  (C_m = D = 0, unit reaction: channel c1 = M_t (x) M_s)
         self.mass_op = KroneckerOperator(st, problem.final_time, 0.0, 0.0, {"c1": 1.0, "a": 1.0, "c2": 0.0},
-                                         lengths=self.L, device=device)
+                                         lengths=self.L, device=device, spatial_data=self.sd)
         self.wsolver = RecoverySolver(st, problem.final_time, problem.b, problem.d_e, config.linear_tol,
-                                      lengths=self.L, device=device)
+                                      lengths=self.L, device=device, spatial_data=self.sd)
 
     def operator(self, problem, u_k, w_k, stab):
         # one operator context for all sweeps: its buffers are reused (dalloc keeps large-enough
@@ -60,7 +67,7 @@ class _Workspace:
             self.op_ctx = DeviceContext(problem.space, self.device)
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
                                  problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
-                                 lengths=self.L, device=self.device, context=self.op_ctx)
+                                 lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd)
 
 
 def _indicator_values(ind):

@@ -212,3 +212,35 @@ class KroneckerOperator:
         return yd.cpu().numpy()
 
     __call__ = matvec
+
+
+class SpatialMassOperator:
+    """(I_t (x) M_s) x on the device for a mapped geometry: one channel, identity time band, M_s
+    assembled by quadrature (the PCG operator of solve_w_system, linalg.py:502-547, whose M_s is
+    SpatialQuadratureData.mass on mapped geometries, solver.py:173-175)."""
+
+    def __init__(self, space_time, spatial_data, device=0, context=None):
+        from .geometry import mass_terms, quad_tables
+        st, sd = space_time, spatial_data
+        self.ctx = context if context is not None else DeviceContext(st, device)
+        ctx = self.ctx
+        p, pt = ctx.p, ctx.pt
+        ctx.bind_stream()
+        _lib.call("mi_op_setup", ctx.handle, 1)
+        bands = np.zeros((1, ctx.nt, 2 * pt + 1))
+        bands[0, :, pt] = 1.0
+        _lib.call("mi_op_set_time_bands", ctx.handle, host_ptr(np.ascontiguousarray(bands)))
+        terms = mass_terms(sd)
+        coef = np.asarray([t[0] for t in terms], float)
+        theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
+        T = quad_tables(sd, [t[2] for t in terms], p, max(ctx.n))
+        qh = np.asarray(sd.q, dtype=np.int32)
+        Qh = np.asarray([r[0].size for r in sd.rules], dtype=np.int32)
+        _lib.call("mi_op_set_quad_channel", ctx.handle, 0, 1, host_ptr(coef), host_ptr(theta), host_ptr(T),
+                  host_ptr(qh), host_ptr(Qh))
+        _lib.call("mi_op_clear_reaction", ctx.handle)
+
+    def apply_device(self, x, y):
+        self.ctx.bind_stream()
+        _lib.call("mi_op_apply", self.ctx.handle, dptr(x), dptr(y))
+

@@ -22,7 +22,10 @@ from .spaces import time_factors, univariate_factors
 
 class RecoverySolver:
     def __init__(self, space_time, final_time, recovery_rate, equilibrium_rate, tol=1e-8, lengths=None,
-                 device=0, context=None):
+                 device=0, context=None, spatial_data=None):
+        """``spatial_data`` (geometry.MappedSpatialData): a mapped geometry, whose M_s (the PCG
+        operator) is assembled by quadrature; the preconditioner stays the parametric Kronecker mass
+        inverse (KroneckerMassPreconditioner(st.spatial), solver.py:202), as in the reference."""
         st = space_time
         self.ctx = context if context is not None else DeviceContext(st, device)
         ctx = self.ctx
@@ -48,6 +51,18 @@ class RecoverySolver:
         ctx.bind_stream()
         _lib.call("mi_ws_setup", ctx.handle, host_ptr(Kinv), host_ptr(M), host_ptr(Minv))
         self.nt, self.ns = ctx.nt, ctx.ns
+        self.mass = None
+        if spatial_data is not None:
+            from .operator import SpatialMassOperator
+            self.mass = SpatialMassOperator(st, spatial_data, device=ctx.device.index)
+
+    def _mass_apply(self, src, dst):
+        """Ap = (I (x) M_s) p for every time row."""
+        if self.mass is not None:
+            self.mass.apply_device(src, dst)
+            self.ctx.bind_stream()
+        else:
+            _lib.call("mi_ws_mass", self.ctx.handle, dptr(src), dptr(dst), self.nt, 0)
 
     def _rowdots(self, a, b, out):
         _lib.call("mi_rowdots", self.ctx.handle, self.nt, self.ns, dptr(a), dptr(b), dptr(out))
@@ -86,7 +101,7 @@ class RecoverySolver:
         for it in range(1, max_iter + 1):
             if not active.any():
                 break
-            _lib.call("mi_ws_mass", h, dptr(p), dptr(Ap), nt, 0)
+            self._mass_apply(p, Ap)
             self._rowdots(p, Ap, curv)
             rz_h, curv_h = rz.cpu().numpy(), curv.cpu().numpy()
             if np.any(curv_h[active] <= 0.0):

@@ -264,6 +264,14 @@ def mapped_cases():
         rec.update(gm_b_x=sol, gm_b_it=it, gm_b_hist=np.array(hist))
         out.update({name + "_" + k: v for k, v in rec.items()})
         print(name, "N=%d gmres a/b %d/%d" % (N, rec["gm_a_it"], it), "detJ in [%.3f, %.3f]" % (sd.detj.min(), sd.detj.max()))
+    # full fixed-point solve on the annulus (Galerkin: the residual indicator needs map Hessians)
+    from monoiga.solver import fixed_point_solve
+    st = SpaceTimeSpace([SplineSpace.uniform(2, 8), SplineSpace.uniform(2, 3)], SplineSpace.uniform(2, 8))
+    prob = MonodomainProblem(geos["annulus"], st, source=smooth_source, D=1e-3)
+    res = fixed_point_solve(prob, FixedPointConfig(stabilization="off", linear_solver="iterative"))
+    out.update(fp_u=res.u, fp_w=res.w, fp_it=res.iterations, fp_gm=np.array(res.gmres_iterations),
+               fp_pcg=np.array(res.pcg_iterations), fp_inc=np.array(res.increments))
+    print("fp annulus sweeps", res.iterations, "gmres", res.gmres_iterations, "pcg", res.pcg_iterations[:6])
     np.savez_compressed(os.path.join(HERE, "mapped.npz"), **out)
 
 
