@@ -80,10 +80,14 @@ struct RxTile {
   static constexpr int NIN = 3 * B4::LS;                                          // input items per slice
   static constexpr int NPRE = (NIN + NTH - 1) / NTH;
   static constexpr size_t SMEM = (size_t)(SIN + SA + SB + SC + SD + 64 + 256) * 8;   // + time tables + read pad
+  // resident blocks per SM the register budget is sized for: the kernel is latency-bound, and at
+  // d = 3, p = 2 a fourth 160-thread block (96 registers, a 100-byte spill) beats three (126
+  // registers): 24.1 -> 20.6 ms at cfg 3; five or six blocks spill more and lose
+  static constexpr int MINB = (D == 3 && P == 2) ? 640 / NTH : 512 / NTH;
 };
 
 template <int D, int P, int PT>
-__global__ void __launch_bounds__(RxTile<D, P>::NTH, 512 / RxTile<D, P>::NTH) reaction_tile(RxArgs r) {
+__global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reaction_tile(RxArgs r) {
   using G = RxTile<D, P>;
   constexpr int E = G::E, QE = G::QE, L = G::L, Q = G::Q;
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
