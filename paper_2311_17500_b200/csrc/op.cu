@@ -400,7 +400,7 @@ static int dmma_prepare(mi_ctx* c) {
     c->C[1] = (c->n[1] + G::B2 - 1) / G::B2;
     c->C[2] = (c->n[2] + G::B3 - 1) / G::B3;
     const long long ncubes = (long long)c->C[0] * c->C[1] * c->C[2];
-    const long long per_group = ncubes * 8 * G::KS * 32;
+    const long long per_group = ncubes * G::PPB * G::KS * 32;
     const int ngroups = (c->nchan + 7) / 8;
     if ((rc = dalloc(c->frag, (size_t)per_group * ngroups))) return rc;
     const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
@@ -516,7 +516,7 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
   MI_DISPATCH_DP(c->d, c->p, {
     using G = DmmaSten<D_, P_>;
     const long long ncubes = (long long)c->C[0] * c->C[1] * c->C[2];
-    const long long per_group = ncubes * 8 * G::KS * 32;
+    const long long per_group = ncubes * G::PPB * G::KS * 32;
     const int ngroups = (c->nchan + 7) / 8;
     const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
     {
