@@ -90,6 +90,12 @@ int mi_op_set_su_channel(mi_ctx* ctx, int c, const double* theta, const double* 
  * q[l] Gauss points per element, Q[l] in total (direction 1 first). */
 int mi_op_set_quad_channel(mi_ctx* ctx, int c, int nterms, const double* coef, const double* theta,
                            const double* T, const int* q, const int* Q);
+/* Device-to-device copy of channel c's stencil ((2p+1)^d x N_s, point
+ * fastest) in / out: a caller reuses generated spatial factors across
+ * operator rebuilds (the reference keeps M_s, K_s in its _Workspace,
+ * solver.py:167-175). */
+int mi_op_set_channel_stencil(mi_ctx* ctx, int c, const double* stencil);
+int mi_op_get_channel_stencil(mi_ctx* ctx, int c, double* stencil);
 /* y = A x   (x, y device, length N, must not alias) */
 int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
 

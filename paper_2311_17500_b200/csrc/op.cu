@@ -392,6 +392,23 @@ int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
   return MI_OK;
 }
 
+int mi_op_set_channel_stencil(mi_ctx* c, int ch, const double* sten) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(ch >= 0 && ch < c->nchan && sten != nullptr, MI_ERR_ARG, "channel out of range");
+  MI_CUDA(cudaMemcpyAsync(c->stencil.p + (size_t)ch * c->nsten * c->ns, sten, sizeof(double) * c->nsten * c->ns,
+                          cudaMemcpyDeviceToDevice, c->stream));
+  c->frag_dirty = true;
+  return MI_OK;
+}
+
+int mi_op_get_channel_stencil(mi_ctx* c, int ch, double* sten) {
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(ch >= 0 && ch < c->nchan && sten != nullptr, MI_ERR_ARG, "channel out of range");
+  MI_CUDA(cudaMemcpyAsync(sten, c->stencil.p + (size_t)ch * c->nsten * c->ns, sizeof(double) * c->nsten * c->ns,
+                          cudaMemcpyDeviceToDevice, c->stream));
+  return MI_OK;
+}
+
 static int dmma_prepare(mi_ctx* c) {
   int rc = MI_OK;
   MI_DISPATCH_DP(c->d, c->p, {

@@ -226,3 +226,42 @@ def separable_weights(sd):
         other = tuple(x for x in range(d) if x != axis)
         stiff.append(ratio.mean(axis=other) if other else ratio)
     return mass, stiff
+
+
+def interpolate_map(spaces, fn):
+    """Tensor-product spline map interpolating fn: (m, d) parametric -> (m, d) physical at the Greville
+    points (collocation solve per direction)."""
+    from .spaces import greville
+    d = len(spaces)
+    g = [greville(s) for s in spaces]
+    mesh = np.meshgrid(*[g[l] for l in reversed(range(d))], indexing="ij")
+    pts = np.stack([mesh[d - 1 - l].ravel() for l in range(d)], axis=-1)
+    X = np.asarray(fn(pts), float).reshape(tuple(s.dimension for s in reversed(spaces)) + (d,))
+    for l in range(d):
+        C = basis_table(spaces[l], g[l], 0)
+        ax = d - 1 - l
+        X = np.moveaxis(np.tensordot(np.linalg.inv(C), X, axes=(1, ax)), 0, ax)
+    return GeometryMap(spaces, X.reshape(-1, d))
+
+
+def prolate_shell_geometry(final_time=1.0, radii=(1.0, 1.0, 2.0), thickness=0.2, polar=(np.pi / 6, 5 * np.pi / 6),
+                           degree=3, elements=8):
+    """BASELINE cfg 5 geometry (absent from the reference): a thick slab of a
+    prolate-ellipsoid shell, quarter sector in azimuth, as a degree-3 tensor-product spline map
+    interpolating the exact shell at the Greville points.  Direction 1: azimuth phi in [0, pi/2],
+    direction 2: polar angle theta in ``polar``, direction 3: through the wall, rho in
+    [1 - thickness, 1] (x = rho (a sin(theta) cos(phi), b sin(theta) sin(phi), c cos(theta)))."""
+    a, b, c = radii
+    t0, t1 = polar
+
+    def shell(p):
+        phi = 0.5 * np.pi * p[:, 0]
+        th = t1 - (t1 - t0) * p[:, 1]                 # decreasing theta keeps det J > 0
+        rho = 1.0 - thickness + thickness * p[:, 2]
+        return np.stack([rho * a * np.sin(th) * np.cos(phi), rho * b * np.sin(th) * np.sin(phi),
+                         rho * c * np.cos(th)], axis=1)
+
+    spaces = [SplineSpace.uniform(degree, elements) for _ in range(3)]
+    geo = interpolate_map(spaces, shell)
+    geo.final_time = float(final_time)
+    return geo

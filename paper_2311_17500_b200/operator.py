@@ -143,23 +143,15 @@ class KroneckerOperator:
             return np.ascontiguousarray(out)
 
         if sd is not None:
-            # c0 = M_s, c1 = D K_s (+ a c1 M_s at the zero iterate), by quadrature on the device
-            from .geometry import mass_terms, quad_tables, stiffness_terms
-            qh = np.asarray(sd.q, dtype=np.int32)
-            Qh = np.asarray([r[0].size for r in sd.rules], dtype=np.int32)
-
-            def quad(ch, terms):
-                coef = np.asarray([t[0] for t in terms], float)
-                theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
-                T = quad_tables(sd, [t[2] for t in terms], p, nmax)
-                _lib.call("mi_op_set_quad_channel", ctx.handle, ch, len(terms), host_ptr(coef), host_ptr(theta),
-                          host_ptr(T), host_ptr(qh), host_ptr(Qh))
-
-            quad(0, mass_terms(sd))
-            t1 = stiffness_terms(sd, float(sig[0]))
+            # c0 = M_s, c1 = D K_s (+ a c1 M_s at the zero iterate): the M_s and K_s stencils are
+            # generated by quadrature on the device once per (geometry data, device) and combined here
+            Ms, Ks = mapped_stencils(ctx, sd)
+            _lib.call("mi_op_set_channel_stencil", ctx.handle, 0, dptr(Ms))
+            c1s = float(sig[0]) * Ks
             if react != 0.0:
-                t1 += [(react, sd.measure(), [(0, 0)] * d)]
-            quad(1, t1)
+                c1s.add_(Ms, alpha=react)
+            _lib.call("mi_op_set_channel_stencil", ctx.handle, 1, dptr(c1s))
+            torch.cuda.current_stream(ctx.device).synchronize()
         else:
             c0 = np.array([1.0])
             b0 = pack([Mb])
@@ -214,13 +206,41 @@ class KroneckerOperator:
     __call__ = matvec
 
 
+def mapped_stencils(ctx, sd):
+    """(M_s, K_s) stencils ((2p+1)^d x N_s device tensors) of a mapped geometry, generated once by
+    mi_op_set_quad_channel (through ``ctx``'s channel 0, which the caller overwrites) and cached on
+    the MappedSpatialData object per device (the reference assembles M_s, K_s once per _Workspace,
+    solver.py:167-175)."""
+    from .geometry import mass_terms, quad_tables, stiffness_terms
+    cache = sd.__dict__.setdefault("_stencils", {})
+    key = str(ctx.device)
+    if key not in cache:
+        p, d = ctx.p, ctx.d
+        nmax = max(ctx.n[:-1] + [ctx.n3g])
+        qh = np.asarray(sd.q, dtype=np.int32)
+        Qh = np.asarray([r[0].size for r in sd.rules], dtype=np.int32)
+        nsten = (2 * p + 1) ** d
+        out = []
+        for terms in (mass_terms(sd), stiffness_terms(sd, 1.0)):
+            coef = np.asarray([t[0] for t in terms], float)
+            theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
+            T = quad_tables(sd, [t[2] for t in terms], p, nmax)
+            _lib.call("mi_op_set_quad_channel", ctx.handle, 0, len(terms), host_ptr(coef), host_ptr(theta),
+                      host_ptr(T), host_ptr(qh), host_ptr(Qh))
+            buf = ctx.empty(nsten * ctx.ns)
+            _lib.call("mi_op_get_channel_stencil", ctx.handle, 0, dptr(buf))
+            out.append(buf)
+        torch.cuda.current_stream(ctx.device).synchronize()
+        cache[key] = tuple(out)
+    return cache[key]
+
+
 class SpatialMassOperator:
     """(I_t (x) M_s) x on the device for a mapped geometry: one channel, identity time band, M_s
     assembled by quadrature (the PCG operator of solve_w_system, linalg.py:502-547, whose M_s is
     SpatialQuadratureData.mass on mapped geometries, solver.py:173-175)."""
 
     def __init__(self, space_time, spatial_data, device=0, context=None):
-        from .geometry import mass_terms, quad_tables
         st, sd = space_time, spatial_data
         self.ctx = context if context is not None else DeviceContext(st, device)
         ctx = self.ctx
@@ -230,15 +250,10 @@ class SpatialMassOperator:
         bands = np.zeros((1, ctx.nt, 2 * pt + 1))
         bands[0, :, pt] = 1.0
         _lib.call("mi_op_set_time_bands", ctx.handle, host_ptr(np.ascontiguousarray(bands)))
-        terms = mass_terms(sd)
-        coef = np.asarray([t[0] for t in terms], float)
-        theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
-        T = quad_tables(sd, [t[2] for t in terms], p, max(ctx.n))
-        qh = np.asarray(sd.q, dtype=np.int32)
-        Qh = np.asarray([r[0].size for r in sd.rules], dtype=np.int32)
-        _lib.call("mi_op_set_quad_channel", ctx.handle, 0, 1, host_ptr(coef), host_ptr(theta), host_ptr(T),
-                  host_ptr(qh), host_ptr(Qh))
+        Ms, _ = mapped_stencils(ctx, sd)
+        _lib.call("mi_op_set_channel_stencil", ctx.handle, 0, dptr(Ms))
         _lib.call("mi_op_clear_reaction", ctx.handle)
+        torch.cuda.current_stream(ctx.device).synchronize()
 
     def apply_device(self, x, y):
         self.ctx.bind_stream()

@@ -1,0 +1,106 @@
+"""BASELINE cfg 5 shape on one GPU: the prolate-ellipsoid shell slab (geometry.prolate_shell_geometry,
+our construction: the reference has no such geometry), p = 3.
+
+  apply: z = P^-1 (A x) on the mapped geometry (Galerkin terms + zero-iterate reaction; M_s and K_s
+         assembled by Gauss quadrature on the device), DoF/s and per-kernel ms;
+  solve: the relaxed fixed-point solve (Galerkin: Spline Upwind on mapped geometries is not built)
+         with S1-S2 source stand-ins (S1 on the phi = 0 face for t < 0.05, S2 on the quadrant
+         x < 0.5, z > 0 for 0.3 <= t < 0.35).
+
+Isotropic D = 1e-3 (the reference's scalar D); cfg 5's fibre-aligned sigma_l / sigma_t and its low-rank
+coefficients are not in the reference and not used here.
+
+    python tools/solve_mapped.py --ne 64 --ne-t 256 --solve-ne 24 --solve-ne-t 64
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2311_17500_b200 as mb  # noqa: E402
+from paper_2311_17500_b200.geometry import MappedSpatialData, prolate_shell_geometry  # noqa: E402
+
+RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
+
+
+def apply_rate(ne, ne_t, p, steps):
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
+    geo = prolate_shell_geometry()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sd = MappedSpatialData(st.spatial, geo)
+    op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, spatial_data=sd)
+    P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1e-3, RM["a"] * RM["c1"], spatial_data=sd, context=op.ctx)
+    x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, st.num_dof)).cuda()
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    op.apply_device(x, y)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    for _ in range(2):
+        op.apply_device(x, y)
+        P.apply_device(y, z)
+    torch.cuda.synchronize()
+    op.ctx.read_profile(reset=True)
+    op.ctx.profiling(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        op.apply_device(x, y)
+        P.apply_device(y, z)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    prof = {k: round(v[0] / steps, 3) for k, v in op.ctx.read_profile(reset=True).items() if v[1]}
+    return {"mesh": [ne] * 3 + [ne_t], "p": p, "N": st.num_dof, "ms_per_apply": ms,
+            "dof_per_s": st.num_dof / (ms * 1e-3), "kernel_ms": prof, "setup_s": setup,
+            "detj_range": [float(np.abs(sd.detj).min()), float(np.abs(sd.detj).max())]}
+
+
+def s1s2_source():
+    def host(x, t):
+        s1 = (x[:, 1] < 0.05) * (t < 0.05)
+        s2 = (x[:, 0] < 0.5) * (x[:, 2] > 0.0) * (t >= 0.3) * (t < 0.35)
+        return 1.0 * s1 + 1.0 * s2
+
+    def dev(x, t):
+        s1 = (x[:, 1] < 0.05) & (t < 0.05)
+        s2 = (x[:, 0] < 0.5) & (x[:, 2] > 0.0) & (t >= 0.3) & (t < 0.35)
+        return s1.to(x.dtype) + s2.to(x.dtype)
+
+    return mb.DeviceSource(host, dev)
+
+
+def solve(ne, ne_t, p, max_it):
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
+    prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s1s2_source(), D=1e-3)
+    cfg = mb.FixedPointConfig(stabilization="off", linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = mb.fixed_point_solve(prob, cfg)
+    torch.cuda.synchronize()
+    return {"mesh": [ne] * 3 + [ne_t], "p": p, "N": st.num_dof, "wall_seconds": time.perf_counter() - t0,
+            "sweeps": res.iterations, "converged": res.converged, "gmres_per_sweep": res.gmres_iterations,
+            "avg_pcg": res.avg_pcg, "phase_seconds": {k: round(v, 3) for k, v in res.phase_seconds.items()},
+            "u_max": float(np.abs(res.u).max())}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ne", type=int, default=64)
+    ap.add_argument("--ne-t", type=int, default=256)
+    ap.add_argument("--p", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--solve-ne", type=int, default=24)
+    ap.add_argument("--solve-ne-t", type=int, default=64)
+    ap.add_argument("--max-it", type=int, default=60)
+    a = ap.parse_args()
+    out = {"geometry": "prolate shell slab, quarter sector (radii 1/1/2, wall 0.2), degree-3 map, 8^3 elements",
+           "apply": apply_rate(a.ne, a.ne_t, a.p, a.steps)}
+    if a.solve_ne > 0:
+        out["solve_galerkin"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it)
+    print(json.dumps(out))
