@@ -560,6 +560,18 @@ def run_ours(args):
             except Exception as exc:   # keep the headline line even if an extra fails
                 line["fixed_point_cfg%d" % c] = {"error": repr(exc)[:300]}
             torch.cuda.empty_cache()
+        # BASELINE cfg 5 shape on one GPU: mapped prolate-shell geometry (our construction), p = 3,
+        # 64^3 x 256: the mapped apply rate and a Galerkin S1-S2 solve at 32^3 x 64
+        spec = importlib.util.spec_from_file_location("solve_mapped", os.path.join(ROOT, "tools", "solve_mapped.py"))
+        solve_mapped = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(solve_mapped)
+        try:
+            line["mapped_cfg5"] = {"geometry": "prolate shell slab, quarter sector (our construction, SURVEY App. B)",
+                                   "apply": solve_mapped.apply_rate(64, 256, 3, 5),
+                                   "solve_galerkin": solve_mapped.solve(32, 64, 3, 60)}
+        except Exception as exc:
+            line["mapped_cfg5"] = {"error": repr(exc)[:300]}
+        torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sec, sample, _ = cpu_sample_rate(3, 1, SAMPLE["ne"], SAMPLE["ne_t"])
         line["cpu_baseline"] = {"value": rate, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",
