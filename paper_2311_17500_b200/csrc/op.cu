@@ -198,6 +198,95 @@ __global__ void build_quad_channel(double* __restrict__ out, const double* __res
   out[(long long)s * g.ns + i] = v;
 }
 
+// Sum-factorised form of build_quad_channel for d = 3: one block per point i, the term's Gauss-weight
+// window theta[k3][k2][k1] (KW^3) staged in shared memory, then contracted one direction at a time
+// (k1 -> a1, k2 -> a2, k3 -> a3): ~KW^3 W + KW^2 W^2 + KW W^3 multiply-adds per term instead of
+// W^3 KW^3.
+template <int P, int KW>
+__global__ void __launch_bounds__(256) build_quad_channel_sf(double* __restrict__ out, const double* __restrict__ coef,
+                                                            const double* __restrict__ theta,
+                                                            const double* __restrict__ T, int nterms, int nmax,
+                                                            QuadSpec qs, Dims g) {
+  constexpr int W = 2 * P + 1, S = W * W * W;
+  extern __shared__ double smq[];
+  double* th = smq;                                  // [KW^3] Gauss-weight window
+  double* a1s = th + KW * KW * KW;                   // [KW][KW][W]
+  double* a2s = a1s + KW * KW * W;                   // [KW][W][W]
+  double (*h)[W * KW] = reinterpret_cast<double (*)[W * KW]>(a2s + KW * W * W);   // [3][W * KW]
+  const long long i = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2)) + g.z_lo;
+  const int ii[3] = {i1, i2, i3};
+  const int k0[3] = {(i1 - P) * qs.q[0], (i2 - P) * qs.q[1], (i3 - P) * qs.q[2]};
+  const int kw[3] = {(P + 1) * qs.q[0], (P + 1) * qs.q[1], (P + 1) * qs.q[2]};
+  double acc[(S + 255) / 256];
+#pragma unroll
+  for (int r = 0; r < (S + 255) / 256; ++r) acc[r] = 0.0;
+  for (int t = 0; t < nterms; ++t) {
+    __syncthreads();                                 // previous term's stages are done with th / h
+    for (int e = tid; e < KW * KW * KW; e += 256) {
+      const int b1 = e % KW, b2 = (e / KW) % KW, b3 = e / (KW * KW);
+      const int k1 = k0[0] + b1, k2 = k0[1] + b2, k3 = k0[2] + b3;
+      const bool ok = b1 < kw[0] && b2 < kw[1] && b3 < kw[2] && k1 >= 0 && k1 < qs.Q[0] && k2 >= 0 &&
+                      k2 < qs.Q[1] && k3 >= 0 && k3 < qs.Q[2];
+      th[e] = ok ? __ldg(theta + (long long)t * qs.nq + ((long long)k3 * qs.Q[1] + k2) * qs.Q[0] + k1) : 0.0;
+    }
+    for (int e = tid; e < 3 * W * KW; e += 256) {
+      const int l = e / (W * KW), r = e % (W * KW), a = r / KW, b = r % KW;
+      h[l][r] = b < qs.kw ? __ldg(T + ((((long long)t * 3 + l) * nmax + ii[l]) * W + a) * qs.kw + b) : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < KW * KW * W; e += 256) {    // a1s[b3][b2][a1] = sum_b1 h1[a1][b1] th[b3][b2][b1]
+      const int a1 = e % W, b23 = e / W;
+      const double* tr = th + b23 * KW;
+      const double* hr = h[0] + a1 * KW;
+      double v = 0.0;
+#pragma unroll
+      for (int b = 0; b < KW; ++b) v = fma(hr[b], tr[b], v);
+      a1s[e] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < KW * W * W; e += 256) {     // a2s[b3][a2][a1] = sum_b2 h2[a2][b2] a1s[b3][b2][a1]
+      const int a1 = e % W, a2 = (e / W) % W, b3 = e / (W * W);
+      const double* hr = h[1] + a2 * KW;
+      double v = 0.0;
+#pragma unroll
+      for (int b = 0; b < KW; ++b) v = fma(hr[b], a1s[(b3 * KW + b) * W + a1], v);
+      a2s[e] = v;
+    }
+    __syncthreads();
+    const double ct = __ldg(coef + t);
+#pragma unroll
+    for (int r = 0; r < (S + 255) / 256; ++r) {       // S[a3][a2][a1] += coef sum_b3 h3[a3][b3] a2s[b3][a2][a1]
+      const int s = tid + 256 * r;
+      if (s < S) {
+        const int a12 = s % (W * W), a3 = s / (W * W);
+        const double* hr = h[2] + a3 * KW;
+        double v = 0.0;
+#pragma unroll
+        for (int b = 0; b < KW; ++b) v = fma(hr[b], a2s[b * W * W + a12], v);
+        acc[r] = fma(ct, v, acc[r]);
+      }
+    }
+  }
+  const int nn[3] = {g.n1, g.n2, g.n3g};
+#pragma unroll
+  for (int r = 0; r < (S + 255) / 256; ++r) {
+    const int s = tid + 256 * r;
+    if (s < S) {
+      const int a1 = s % W, a2 = (s / W) % W, a3 = s / (W * W);
+      const int aa[3] = {a1, a2, a3};
+      bool inside = true;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const int j = ii[l] + aa[l] - P;
+        inside = inside && j >= 0 && j < nn[l];
+      }
+      out[(long long)s * g.ns + i] = inside ? acc[r] : 0.0;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- apply
 // W_c[t, i] = sum_s S_c[s, i] x[t, i + off(s)], channels in groups of CG,
 // TC time slices per thread.
@@ -375,14 +464,31 @@ int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
   DeviceBuf dc, dth, dT;
   int rc;
   if ((rc = dalloc(dc, nterms)) || (rc = dalloc(dth, (size_t)nterms * qs.nq)) || (rc = dalloc(dT, nT))) return rc;
-  MI_CUDA(cudaMemcpyAsync(dc.p, coef, sizeof(double) * nterms, cudaMemcpyHostToDevice, c->stream));
-  MI_CUDA(cudaMemcpyAsync(dth.p, theta, sizeof(double) * nterms * qs.nq, cudaMemcpyHostToDevice, c->stream));
-  MI_CUDA(cudaMemcpyAsync(dT.p, T, sizeof(double) * nT, cudaMemcpyHostToDevice, c->stream));
+  // host or device arrays (unified addressing picks the copy direction)
+  MI_CUDA(cudaMemcpyAsync(dc.p, coef, sizeof(double) * nterms, cudaMemcpyDefault, c->stream));
+  MI_CUDA(cudaMemcpyAsync(dth.p, theta, sizeof(double) * nterms * qs.nq, cudaMemcpyDefault, c->stream));
+  MI_CUDA(cudaMemcpyAsync(dT.p, T, sizeof(double) * nT, cudaMemcpyDefault, c->stream));
   Dims g = dims_of(c);
-  dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
   double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
-  MI_DISPATCH_DP(c->d, c->p, (build_quad_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dc.p, dth.p, dT.p, nterms,
-                                                                                      nmax, qs, g)));
+  const bool sf = c->d == 3 && ((c->p == 3 && kw <= 16) || (c->p == 2 && kw <= 9) || (c->p == 1 && kw <= 4));
+  if (sf) {
+    // sum-factorised generator (d = 3, q = p + 1)
+#define MI_QSF(PV, KWV)                                                                                   \
+  if (c->p == PV) {                                                                                     \
+    constexpr int Wv = 2 * PV + 1;                                                                      \
+    constexpr size_t sm = (size_t)(KWV * KWV * KWV + KWV * KWV * Wv + KWV * Wv * Wv + 3 * Wv * KWV) * 8; \
+    MI_CUDA(cudaFuncSetAttribute(build_quad_channel_sf<PV, KWV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)sm));                                                             \
+    build_quad_channel_sf<PV, KWV><<<(unsigned)c->ns, 256, sm, c->stream>>>(out, dc.p, dth.p, dT.p, nterms, nmax, \
+                                                                            qs, g);                     \
+  }
+    MI_QSF(3, 16) MI_QSF(2, 9) MI_QSF(1, 4)
+#undef MI_QSF
+  } else {
+    dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
+    MI_DISPATCH_DP(c->d, c->p, (build_quad_channel<D_, P_><<<grid, 128, 0, c->stream>>>(out, dc.p, dth.p, dT.p, nterms,
+                                                                                        nmax, qs, g)));
+  }
   MI_CHECK_LAUNCH("build_quad_channel");
   c->frag_dirty = true;
   MI_CUDA(cudaStreamSynchronize(c->stream));

@@ -44,11 +44,11 @@ class _Workspace:
         if self.indicator is not None and problem.source is not None:
             # one host evaluation of the source feeds both the load vector and the indicator's
             # device-resident copy
-            self.grid = self.indicator._grid = GaussGrid(st, problem.geometry)
+            self.grid = self.indicator._grid = GaussGrid(st, problem.geometry, mapped=self.sd)
             self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid,
                                      chunks=self.indicator.source_chunks(problem.source))
         else:
-            self.grid = GaussGrid(st, problem.geometry)
+            self.grid = GaussGrid(st, problem.geometry, mapped=self.sd)
             self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid, device=device)
         self.pc_ctx = DeviceContext(st, device)
         self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.D,

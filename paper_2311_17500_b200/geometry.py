@@ -44,14 +44,31 @@ class GeometryMap:
         self.affine_scales = affine_scales
         self._grid = cp.reshape(tuple(s.dimension for s in reversed(self.spaces)) + (self.dim,))
 
-    def grid_data(self, axes, order=1):
+    def grid_data(self, axes, order=1, device=None):
         """x (grid + (d,)) and, for order >= 1, jac (grid + (d, d)) with jac[..., c, a] = dF_c/deta_a;
-        grid axes in C order (direction d first), like geometry.py:135-186."""
+        grid axes in C order (direction d first), like geometry.py:135-186.  With a CUDA ``device``
+        the tensor contractions run there and torch tensors are returned."""
         if order > 1:
             raise NotImplementedError("Hessians are not needed on the device path")
         d = self.dim
         tabs = [[basis_table(s, np.asarray(ax, float), o) for o in range(order + 1)]
                 for s, ax in zip(self.spaces, axes)]
+        if device is not None:
+            import torch
+            tabs = [[torch.from_numpy(t).to(device) for t in tl] for tl in tabs]
+            grid0 = torch.from_numpy(np.ascontiguousarray(self._grid)).to(device)
+
+            def tabulate(orders):
+                val = grid0
+                for l in range(d):
+                    ax = d - 1 - l
+                    val = torch.movedim(torch.tensordot(tabs[l][orders[l]], val, dims=([1], [ax])), 0, ax)
+                return val
+
+            out = {"x": tabulate([0] * d)}
+            if order >= 1:
+                out["jac"] = torch.stack([tabulate([1 if l == a else 0 for l in range(d)]) for a in range(d)], dim=-1)
+            return out
 
         def tabulate(orders):
             val = self._grid
@@ -114,7 +131,9 @@ def is_mapped(geometry):
 class MappedSpatialData:
     """Quadrature data of a mapped geometry on the solution mesh (assembly.py:137-219)."""
 
-    def __init__(self, spatial_spaces, geometry):
+    def __init__(self, spatial_spaces, geometry, device="auto"):
+        """``device``: where the map is evaluated and the Jacobians inverted ("auto": the current
+        CUDA device if there is one; None: host numpy).  Results are host arrays either way."""
         self.spaces = tuple(spatial_spaces)
         d = len(self.spaces)
         if geometry.dim != d:
@@ -122,9 +141,25 @@ class MappedSpatialData:
         self.geo = geometry
         self.q = [s.degree + 1 for s in self.spaces]
         self.rules = [gauss_rule(s.breakpoints, s.degree + 1) for s in self.spaces]   # (points, weights)
-        data = geometry.grid_data([r[0] for r in self.rules], order=1)
-        self.xgrid = data["x"]
-        self.jinv, self.detj = jacobian_inverse_and_det(data["jac"])
+        if device == "auto":
+            import torch
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        if device is not None:
+            import torch
+            data = geometry.grid_data([r[0] for r in self.rules], order=1, device=device)
+            jac = data["jac"]
+            det = torch.linalg.det(jac)
+            scale = torch.prod(torch.linalg.norm(jac, dim=-2), dim=-1)
+            if bool(torch.any(det.abs() < SINGULAR_REL_TOL * torch.clamp(scale, min=1e-300)).item()):
+                raise GeometryError("singular Jacobian encountered during pull-back")
+            self.xgrid = data["x"].cpu().numpy()
+            self.jinv = torch.linalg.inv(jac).cpu().numpy()
+            self.detj = det.cpu().numpy()
+            del data, jac, det, scale
+        else:
+            data = geometry.grid_data([r[0] for r in self.rules], order=1)
+            self.xgrid = data["x"]
+            self.jinv, self.detj = jacobian_inverse_and_det(data["jac"])
         w = np.ones(())
         for l in reversed(range(d)):
             w = np.multiply.outer(w, self.rules[l][1])

@@ -208,11 +208,13 @@ def _mode(A, X, axis):
 class GaussGrid:
     """Default Gauss rules (q = p+1) of every direction with basis tables."""
 
-    def __init__(self, st, geometry):
+    def __init__(self, st, geometry, mapped=None):
         from .geometry import MappedSpatialData, is_mapped
         self.st = st
         # mapped geometries: parametric rules, physical points and |det J| from the map
-        self.mapped = MappedSpatialData(st.spatial, geometry) if is_mapped(geometry) else None
+        if mapped is None and is_mapped(geometry):
+            mapped = MappedSpatialData(st.spatial, geometry)
+        self.mapped = mapped
         if self.mapped is None:
             self.L, self.off = box_of(geometry)
         else:
