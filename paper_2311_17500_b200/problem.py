@@ -198,7 +198,7 @@ class ResidualIndicator:
 def _mode(A, X, axis):
     if not isinstance(X, np.ndarray):                 # torch tensor (device load vector)
         import torch
-        At = torch.as_tensor(A, dtype=X.dtype, device=X.device)
+        At = torch.tensor(A, dtype=X.dtype, device=X.device)    # copies (A may be a read-only table)
         return torch.movedim(torch.tensordot(At, X, dims=([1], [axis])), 0, axis)
     t = np.moveaxis(X, axis, 0)
     out = (A @ t.reshape(t.shape[0], -1)).reshape((A.shape[0],) + t.shape[1:])

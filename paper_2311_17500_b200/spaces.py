@@ -97,7 +97,27 @@ def greville(space):
     return (csum[i + p + 1] - csum[i + 1]) / p
 
 
+_TABLES = {}
+_TABLES_MAX = 512
+
+
 def basis_table(space, x, order=0):
+    """Dense (len(x), dimension) table of the order-th derivative of every basis (memoised: the
+    fixed-point driver re-evaluates the same 1D tables every sweep; the result is read-only)."""
+    u = np.asarray(space.knots, float)
+    xa = np.atleast_1d(np.asarray(x, float))
+    key = (u.tobytes(), int(space.degree), xa.tobytes(), int(order))
+    hit = _TABLES.get(key)
+    if hit is None:
+        hit = _basis_table(space, xa, order)
+        hit.setflags(write=False)
+        if len(_TABLES) >= _TABLES_MAX:
+            _TABLES.pop(next(iter(_TABLES)))
+        _TABLES[key] = hit
+    return hit
+
+
+def _basis_table(space, x, order=0):
     """Dense (len(x), dimension) table of the order-th derivative of every basis.
 
     Vectorised bottom-up recursion over degrees on all points at once, with
