@@ -119,6 +119,12 @@ int mi_op_clear_reaction(mi_ctx* ctx);
  * (reaction_mass with spatial_data, assembly.py:320-326); NULL = box.
  * Call after mi_op_set_reaction. */
 int mi_op_set_reaction_weight(mi_ctx* ctx, const double* jw);
+/* Stored-coefficient mode of the reaction: the iterate is frozen for a
+ * whole solve, so C_r times the spatial quadrature weight is evaluated once
+ * at every space-time Gauss point (next apply after a change) and each
+ * apply interpolates only x.  mode -1: when it fits in 40% of the free
+ * device memory (default), 0: never, 1: always. */
+int mi_op_set_reaction_store(mi_ctx* ctx, int mode);
 /* Time-sharded slabs: the reaction tables cover local time elements whose
  * full-basis function ft maps to local row ft + row_offset (default -1). */
 int mi_op_set_reaction_rows(mi_ctx* ctx, int row_offset);

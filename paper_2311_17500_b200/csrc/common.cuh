@@ -102,6 +102,9 @@ struct mi_ctx {
   int rx_q[4] = {1, 1, 1, 1}, rx_p[4] = {0, 0, 0, 0}, rx_nel[4] = {1, 1, 1, 1}, rx_E[4] = {1, 1, 1, 1};
   mi::DeviceBuf rx_jw;          // mapped geometry: |det J| on the spatial Gauss grid (Q_d .. Q_1); empty = box
   bool rx_mapped = false;
+  mi::DeviceBuf rx_cw;          // stored C_r x spatial weight at every Gauss point (reaction.cu RX_STORED)
+  bool rx_cw_ok = false, rx_cw_dirty = true;
+  int rx_store_mode = -1;       // -1 auto (fits in 40% of free memory), 0 off, 1 on
 
   // ---- preconditioner
   bool pc_ready = false;

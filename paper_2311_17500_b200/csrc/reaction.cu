@@ -40,7 +40,15 @@ struct RxArgs {
   long long ns;
   double c1, a, c2;
   const double* jw;    // mapped geometry: |det J| at the spatial Gauss points, C order (Q_3, Q_2, Q_1); null: box
+  double* cw;          // stored weighted coefficient C_r w_x (RX_PRE writes it, RX_STORED reads it)
 };
+
+// Kernel modes.  RX_FUSED interpolates u, w and x and evaluates C_r on the fly every apply.  The
+// iterate is frozen for a whole GMRES solve, so when the Gauss-point coefficients fit in memory
+// RX_PRE evaluates c_w = C_r x (spatial weight) once per operator build and RX_STORED applies M_R
+// with it: one interpolated field instead of three, and the time stage reads c_w (coalesced: the
+// store is laid out in the order each thread consumes its own points) instead of forming C_r.
+enum RxMode { RX_FUSED = 0, RX_PRE = 1, RX_STORED = 2 };
 
 // R5: time-streamed sum factorisation.  The block still owns a 2^d tile of
 // spatial elements and sweeps all time elements, but the spatial stages now
@@ -86,9 +94,11 @@ struct RxTile {
   static constexpr int MINB = (D == 3 && P == 2) ? 640 / NTH : 512 / NTH;
 };
 
-template <int D, int P, int PT>
+template <int D, int P, int PT, int MODE>
 __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reaction_tile(RxArgs r) {
   using G = RxTile<D, P>;
+  constexpr int NF = MODE == RX_FUSED ? 3 : (MODE == RX_PRE ? 2 : 1);   // interpolated fields
+  constexpr int NIN = NF * G::LS, NPRE = (NIN + G::NTH - 1) / G::NTH;
   constexpr int E = G::E, QE = G::QE, L = G::L, Q = G::Q;
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
   constexpr int LS = G::LS, KI = G::KI, KP = G::KP, QL = G::QL, NT = G::NT, MT = G::MT;
@@ -167,23 +177,23 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     return ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
   };
   // input slice items of this thread: (fld, s) -> global spatial index (-1: padding)
-  long long gsp[G::NPRE];
+  long long gsp[NPRE];
 #pragma unroll
-  for (int m = 0; m < G::NPRE; ++m) {
+  for (int m = 0; m < NPRE; ++m) {
     const int i = tid + NTH * m;
     const int s = i % LS;
     bool ok;
     const long long gs = spatial(s / (L1 * L2), (s / L1) % L2, s % L1, ok);
-    gsp[m] = (i < G::NIN && ok) ? gs : -1;
+    gsp[m] = (i < NIN && ok) ? gs : -1;
   }
-  double pre[G::NPRE];
+  double pre[NPRE];
   auto prefetch = [&](int ft) {
     const int ct = ft + r.rowoff;
     const bool vt = ct >= 0 && ct < r.ntc;
 #pragma unroll
-    for (int m = 0; m < G::NPRE; ++m) {
+    for (int m = 0; m < NPRE; ++m) {
       const int f = (tid + NTH * m) / LS;
-      const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
+      const double* src = MODE == RX_STORED ? r.x : (f == 0 ? r.u : (f == 1 ? r.w : r.x));
       pre[m] = (vt && gsp[m] >= 0) ? __ldg(src + (long long)ct * ns + gsp[m]) : 0.0;
     }
   };
@@ -213,13 +223,13 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
   const double rc1 = r.c1, rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;
 
   // window slot of time function f is f % PW (compile-time below: the slice loop is unrolled by PW)
-  double X[MT][PW][3][2], Y[MT][PW][2];
+  double X[MT][PW][NF][2], Y[MT][PW][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
     for (int a = 0; a < PW; ++a) {
 #pragma unroll
-      for (int f = 0; f < 3; ++f) X[mi][a][f][0] = X[mi][a][f][1] = 0.0;
+      for (int f = 0; f < NF; ++f) X[mi][a][f][0] = X[mi][a][f][1] = 0.0;
       Y[mi][a][0] = Y[mi][a][1] = 0.0;
     }
 
@@ -237,6 +247,14 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     }
   };
 
+  // c_w store layout: [tile][time element][g][line][q_last], valid Gauss points only (QL x Q per slice)
+  const long long tile_id = ((long long)(k[2] / E) * ((r.nel[1] + E - 1) / E) + k[1] / E) * ((r.nel[0] + E - 1) / E) +
+                            k[0] / E;
+  auto cw_valid = [&](int mi, int e) -> bool { return 8 * (warp + NW * mi) + fr < QL && 2 * fk + e < Q; };
+  auto cw_index = [&](int et, int g, int mi, int e) -> long long {
+    return ((tile_id * r.nel[3] + et) * QT + g) * (long long)(QL * Q) + (8 * (warp + NW * mi) + fr) * Q + 2 * fk + e;
+  };
+  [[maybe_unused]] double cwp[QT][MT][2];
   const int nfull = r.nel[3] + PT;                   // full-basis time functions
   const int jmax = nfull + PT;
   auto step = [&](auto phc, int j) {
@@ -244,12 +262,12 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     const int et = j - PT;                           // time element (0 <= et < nel_t); z-projection of function et
     const int fp = j - PT - 1;                       // function whose y / x projections run in this iteration
     const bool has_in = j < nfull;
-    [[maybe_unused]] const bool has_fp = fp >= 0 && fp < nfull;
+    [[maybe_unused]] const bool has_fp = MODE != RX_PRE && fp >= 0 && fp < nfull;
     if constexpr (D == 1) __syncthreads();           // sIn is read by the last stage directly
     if (has_in) {
 #pragma unroll
-      for (int m = 0; m < G::NPRE; ++m)
-        if (tid + NTH * m < G::NIN) sIn[tid + NTH * m] = pre[m];
+      for (int m = 0; m < NPRE; ++m)
+        if (tid + NTH * m < NIN) sIn[tid + NTH * m] = pre[m];
     }
     if (tid < NBT) sBt[(j & 1) * 32 + tid] = btp;
     if constexpr (D >= 2) {
@@ -262,11 +280,21 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     __syncthreads();                                 // B1
     if (j + 1 < nfull) prefetch(j + 1);
     prefetch_bt(et + 1);
+    if constexpr (MODE == RX_STORED) {               // this step's c_w, consumed by its time stage
+      if (et >= 0 && et < r.nel[3]) {
+#pragma unroll
+        for (int g = 0; g < QT; ++g)
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) cwp[g][mi][e] = cw_valid(mi, e) ? __ldcs(r.cw + cw_index(et, g, mi, e)) : 0.0;
+      }
+    }
     const double* fin = sIn;
     if constexpr (D >= 2) {
       // phase 2: x interpolation of slice j: lines (fld, j3, j2), K = j1, N = q1 -> sA [fld][j3][j2][q1]
       if (has_in) {
-        constexpr int NL = 3 * L3 * L2;
+        constexpr int NL = NF * L3 * L2;
         for (int mt = warp; mt < (NL + 7) / 8; mt += NW) {
           const int line = mt * 8 + fr;
           double c0 = 0.0, c1 = 0.0;
@@ -302,7 +330,7 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     if constexpr (D == 3) {
       // phase 3: y interpolation of slice j: lines (fld, j3, q1), K = j2, N = q2 -> sB [fld][j3][q2][q1]
       if (has_in) {
-        constexpr int NL = 3 * L3 * Q1;
+        constexpr int NL = NF * L3 * Q1;
         for (int mt = warp; mt < (NL + 7) / 8; mt += NW) {
           const int line = mt * 8 + fr;
           const int q1 = line % Q1, fj3 = line / Q1;
@@ -329,14 +357,15 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
         if (t < NT) {
           const int line = 8 * t + fr;
 #pragma unroll
-          for (int f = 0; f < 3; ++f) {
+          for (int f = 0; f < NF; ++f) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
             for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, fin[(f * L + 4 * ks + fk) * QL + line], bI[D - 1][ks]);
-            const double sc0 = f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]);
-            const double sc1 = f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]);
-            X[mi][PH][f][0] = f == 0 ? c0 : c0 * sc0;
-            X[mi][PH][f][1] = f == 0 ? c1 : c1 * sc1;
+            // fused: (u, c2 w, w_x x); pre: (u, c2 w); stored: (x) -- the weight is in c_w
+            const double sc0 = MODE == RX_STORED ? 1.0 : (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]));
+            const double sc1 = MODE == RX_STORED ? 1.0 : (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]));
+            X[mi][PH][f][0] = c0 * sc0;
+            X[mi][PH][f][1] = c1 * sc1;
           }
         }
       }
@@ -353,26 +382,42 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            double uu = 0.0, ww = 0.0, xx = 0.0;
+            if constexpr (MODE == RX_STORED) {
+              double xx = 0.0;
 #pragma unroll
-            for (int a = 0; a < PW; ++a) {
-              const double ba = bt[g * PW + a];
-              uu = fma(ba, X[mi][(S0 + a) % PW][0][e], uu);
-              ww = fma(ba, X[mi][(S0 + a) % PW][1][e], ww);
-              xx = fma(ba, X[mi][(S0 + a) % PW][2][e], xx);
+              for (int a = 0; a < PW; ++a) xx = fma(bt[g * PW + a], X[mi][(S0 + a) % PW][0][e], xx);
+              const double v = cwp[g][mi][e] * xx;
+#pragma unroll
+              for (int a = 0; a < PW; ++a)
+                Y[mi][(S0 + a) % PW][e] = fma(bt[QT * PW + g * PW + a], v, Y[mi][(S0 + a) % PW][e]);
+            } else {
+              double uu = 0.0, ww = 0.0;
+              [[maybe_unused]] double xx = 0.0;
+#pragma unroll
+              for (int a = 0; a < PW; ++a) {
+                const double ba = bt[g * PW + a];
+                uu = fma(ba, X[mi][(S0 + a) % PW][0][e], uu);
+                ww = fma(ba, X[mi][(S0 + a) % PW][1][e], ww);
+                if constexpr (MODE == RX_FUSED) xx = fma(ba, X[mi][(S0 + a) % PW][NF - 1][e], xx);
+              }
+              // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
+              const double cr = fma(uu, fma(rc1, uu, rk1), ww + rk0);
+              if constexpr (MODE == RX_PRE) {
+                if (cw_valid(mi, e)) r.cw[cw_index(et, g, mi, e)] = cr * wsp[mi][e];
+              } else {
+                const double v = cr * xx;
+#pragma unroll
+                for (int a = 0; a < PW; ++a)
+                  Y[mi][(S0 + a) % PW][e] = fma(bt[QT * PW + g * PW + a], v, Y[mi][(S0 + a) % PW][e]);
+              }
             }
-            // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
-            const double cr = fma(uu, fma(rc1, uu, rk1), ww + rk0);
-            const double v = cr * xx;
-#pragma unroll
-            for (int a = 0; a < PW; ++a)
-              Y[mi][(S0 + a) % PW][e] = fma(bt[QT * PW + g * PW + a], v, Y[mi][(S0 + a) % PW][e]);
           }
       }
     }
-    // ... and the last-direction projection of the completed function et (quad shuffles -> A fragments)
+    // ... and the last-direction projection of the completed function et (quad shuffles -> A fragments);
+    // RX_PRE projects nothing back
 #pragma unroll
-    for (int mi = 0; mi < MT; ++mi) {
+    for (int mi = 0; mi < (MODE == RX_PRE ? 0 : MT); ++mi) {
       const int t = warp + NW * mi;
       if (t < NT) {                                  // warp-uniform
         const int line = 8 * t + fr;
@@ -408,18 +453,18 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     step(std::integral_constant<int, PT>{}, j);
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi) {
-      double xs[3][2], ys[2];
+      double xs[NF][2], ys[2];
 #pragma unroll
-      for (int f = 0; f < 3; ++f) xs[f][0] = X[mi][0][f][0], xs[f][1] = X[mi][0][f][1];
+      for (int f = 0; f < NF; ++f) xs[f][0] = X[mi][0][f][0], xs[f][1] = X[mi][0][f][1];
       ys[0] = Y[mi][0][0], ys[1] = Y[mi][0][1];
 #pragma unroll
       for (int a = 0; a < PW - 1; ++a) {
 #pragma unroll
-        for (int f = 0; f < 3; ++f) X[mi][a][f][0] = X[mi][a + 1][f][0], X[mi][a][f][1] = X[mi][a + 1][f][1];
+        for (int f = 0; f < NF; ++f) X[mi][a][f][0] = X[mi][a + 1][f][0], X[mi][a][f][1] = X[mi][a + 1][f][1];
         Y[mi][a][0] = Y[mi][a + 1][0], Y[mi][a][1] = Y[mi][a + 1][1];
       }
 #pragma unroll
-      for (int f = 0; f < 3; ++f) X[mi][PW - 1][f][0] = xs[f][0], X[mi][PW - 1][f][1] = xs[f][1];
+      for (int f = 0; f < NF; ++f) X[mi][PW - 1][f][0] = xs[f][0], X[mi][PW - 1][f][1] = xs[f][1];
       Y[mi][PW - 1][0] = ys[0], Y[mi][PW - 1][1] = ys[1];
     }
   }
@@ -450,20 +495,9 @@ __global__ void add_owned_planes(double* __restrict__ y, const double* __restric
   if (i < ns && t < nt) y[(long long)t * ns + i] += yin[(long long)t * ns_in + off + i];
 }
 
-int reaction_apply(mi_ctx* c, const double* x, double* y) {
-  // the reaction runs on the input frame (owned + halo planes): element contributions to the owned
-  // planes need the iterate and x on every function of the elements touching them
-  const bool slab = c->ns_in != c->ns;
-  if (slab) {
-    int rc;
-    if ((rc = dalloc(c->y_in, (size_t)c->N_in))) return rc;
-    MI_CUDA(cudaMemsetAsync(c->y_in.p, 0, sizeof(double) * c->N_in, c->stream));
-  }
-  RxArgs r{};
+static void fill_args(mi_ctx* c, RxArgs& r) {
   r.u = c->u_it.p;
   r.w = c->w_it.p;
-  r.x = x;
-  r.y = slab ? c->y_in.p : y;
   for (int l = 0; l < 4; ++l) {
     r.B[l] = c->rx_B.p + c->rx_Boff[l];
     r.Wq[l] = c->rx_W.p + c->rx_Woff[l];
@@ -479,12 +513,18 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   r.a = c->a;
   r.c2 = c->c2;
   r.jw = c->rx_mapped ? c->rx_jw.p : nullptr;
+  r.cw = c->rx_cw_ok ? c->rx_cw.p : nullptr;
+}
+
+// all colour classes of one kernel mode
+template <int MODE>
+static int reaction_launch(mi_ctx* c, RxArgs r) {
   MI_RX_DISPATCH(c->d, c->p, c->pt, {
     using G = RxTile<D_, P_>;
     constexpr size_t smem = G::SMEM;
     static bool attr = false;
     if (!attr) {
-      MI_CUDA(cudaFuncSetAttribute(reaction_tile<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      MI_CUDA(cudaFuncSetAttribute(reaction_tile<D_, P_, PT_, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       attr = true;
     }
@@ -506,10 +546,79 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
         nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
       }
       if (nb == 0) continue;
-      reaction_tile<D_, P_, PT_><<<(unsigned)nb, G::NTH, smem, c->stream>>>(r);
+      reaction_tile<D_, P_, PT_, MODE><<<(unsigned)nb, G::NTH, smem, c->stream>>>(r);
       MI_CHECK_LAUNCH("reaction_tile");
     }
   });
+  return MI_OK;
+}
+
+// bytes of the stored weighted coefficient c_w for this context (0: dims unsupported)
+static size_t reaction_store_bytes(const mi_ctx* c) {
+  size_t out = 0;
+  auto one = [&](auto dv, auto pv) {
+    constexpr int D_ = decltype(dv)::value, P_ = decltype(pv)::value;
+    using G = RxTile<D_, P_>;
+    size_t tiles = 1;
+    for (int l = 0; l < D_; ++l) tiles *= (size_t)((c->rx_nel[l] + G::E - 1) / G::E);
+    out = tiles * c->rx_nel[3] * (P_ + 1) * (size_t)(G::QL * G::Q) * sizeof(double);
+  };
+  if (c->p == c->pt) {
+    if (c->d == 3 && c->p == 3) one(std::integral_constant<int, 3>{}, std::integral_constant<int, 3>{});
+    if (c->d == 3 && c->p == 2) one(std::integral_constant<int, 3>{}, std::integral_constant<int, 2>{});
+    if (c->d == 3 && c->p == 1) one(std::integral_constant<int, 3>{}, std::integral_constant<int, 1>{});
+    if (c->d == 2 && c->p == 3) one(std::integral_constant<int, 2>{}, std::integral_constant<int, 3>{});
+    if (c->d == 2 && c->p == 2) one(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{});
+    if (c->d == 2 && c->p == 1) one(std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
+    if (c->d == 1 && c->p == 3) one(std::integral_constant<int, 1>{}, std::integral_constant<int, 3>{});
+    if (c->d == 1 && c->p == 2) one(std::integral_constant<int, 1>{}, std::integral_constant<int, 2>{});
+    if (c->d == 1 && c->p == 1) one(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
+  }
+  return out;
+}
+
+// evaluate c_w once for the current iterate when it fits (store mode: -1 auto = at most 40% of the
+// free device memory, 0 never, 1 always)
+static int reaction_prepare_store(mi_ctx* c) {
+  c->rx_cw_ok = false;
+  if (c->rx_store_mode == 0) return MI_OK;
+  const size_t bytes = reaction_store_bytes(c);
+  if (bytes == 0) return MI_OK;
+  if (c->rx_store_mode < 0 && c->rx_cw.n * sizeof(double) < bytes) {
+    size_t free_b = 0, total_b = 0;
+    MI_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (bytes > free_b / 10 * 4) return MI_OK;
+  }
+  int rc;
+  if ((rc = dalloc(c->rx_cw, bytes / sizeof(double)))) return rc;
+  RxArgs r{};
+  fill_args(c, r);
+  r.cw = c->rx_cw.p;
+  if ((rc = reaction_launch<RX_PRE>(c, r))) return rc;
+  c->rx_cw_ok = true;
+  return MI_OK;
+}
+
+int reaction_apply(mi_ctx* c, const double* x, double* y) {
+  if (c->rx_cw_dirty) {
+    int rc = reaction_prepare_store(c);
+    if (rc) return rc;
+    c->rx_cw_dirty = false;
+  }
+  // the reaction runs on the input frame (owned + halo planes): element contributions to the owned
+  // planes need the iterate and x on every function of the elements touching them
+  const bool slab = c->ns_in != c->ns;
+  if (slab) {
+    int rc;
+    if ((rc = dalloc(c->y_in, (size_t)c->N_in))) return rc;
+    MI_CUDA(cudaMemsetAsync(c->y_in.p, 0, sizeof(double) * c->N_in, c->stream));
+  }
+  RxArgs r{};
+  fill_args(c, r);
+  r.x = x;
+  r.y = slab ? c->y_in.p : y;
+  int rc = c->rx_cw_ok ? reaction_launch<RX_STORED>(c, r) : reaction_launch<RX_FUSED>(c, r);
+  if (rc) return rc;
   if (slab) {
     dim3 g((unsigned)((c->ns + 255) / 256), c->nt);
     add_owned_planes<<<g, 256, 0, c->stream>>>(y, c->y_in.p, c->ns, c->ns_in,
@@ -572,6 +681,7 @@ int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, d
   for (int l = 0; l < 4; ++l)
     MI_REQUIRE(c->rx_q[l] == ((l == 3 || l < c->d) ? c->p + 1 : 1), MI_ERR_ARG, "reaction: need q = p + 1");
   c->reaction_on = true;
+  c->rx_cw_dirty = true;
   return MI_OK;
 }
 
@@ -588,12 +698,22 @@ int mi_op_set_reaction_weight(mi_ctx* c, const double* jw) {
   if ((rc = dalloc(c->rx_jw, nq))) return rc;
   MI_CUDA(cudaMemcpy(c->rx_jw.p, jw, sizeof(double) * nq, cudaMemcpyHostToDevice));
   c->rx_mapped = true;
+  c->rx_cw_dirty = true;
+  return MI_OK;
+}
+
+int mi_op_set_reaction_store(mi_ctx* c, int mode) {
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  MI_REQUIRE(mode >= -1 && mode <= 1, MI_ERR_ARG, "store mode must be -1, 0 or 1");
+  c->rx_store_mode = mode;
+  c->rx_cw_dirty = true;
   return MI_OK;
 }
 
 int mi_op_set_reaction_rows(mi_ctx* c, int row_offset) {
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   c->rx_rowoff = row_offset;
+  c->rx_cw_dirty = true;
   return MI_OK;
 }
 

@@ -82,7 +82,9 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
         minus = torch.full((1,), -1.0, dtype=torch.float64, device=dev)
         r = torch.empty_like(b)
         ops.comb(tmp.view(1, -1), 1, minus, b, r)
-    V = torch.empty((m + 1, n), dtype=torch.float64, device=dev)
+    # the basis grows on demand (doubling, up to m + 1 vectors): memory follows the iterations used,
+    # not the HBM-sized bound, so later allocations (e.g. the reaction's stored coefficient) still fit
+    V = torch.empty((min(m, 32) + 1, n), dtype=torch.float64, device=dev)
     apply_P(r, V[0])
     ops.dots(V[0].view(1, -1), 1, V[0], nrm)
     red(nrm)
@@ -99,6 +101,10 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
     k_done = None
     w = torch.empty_like(b)
     for j in range(m):
+        if j + 1 >= V.shape[0]:
+            grown = torch.empty((min(m + 1, 2 * V.shape[0]), n), dtype=torch.float64, device=dev)
+            grown[:V.shape[0]].copy_(V)
+            V = grown
         apply_A(V[j], tmp)
         apply_P(tmp, w)
         k = j + 1

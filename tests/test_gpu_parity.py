@@ -91,12 +91,17 @@ def test_gmres_known_answers_device():
 
 
 @pytest.mark.parametrize("name", CASES)
-def test_operator_general_iterate_reaction(name):
-    """Variant B: M_R (q=p+1 Gauss, Rogers-McCulloch linearisation) at u, w != 0."""
+@pytest.mark.parametrize("store", [0, 1])
+def test_operator_general_iterate_reaction(name, store):
+    """Variant B: M_R (q=p+1 Gauss, Rogers-McCulloch linearisation) at u, w != 0, with C_r formed
+    in every apply (store 0) and stored once per operator build (store 1)."""
+    from paper_2311_17500_b200 import _lib
     g = load(name)
     _, op, _ = product_objects(g, u=g["u"], w=g["w"])
     assert not op.zero_iterate
+    _lib.call("mi_op_set_reaction_store", op.ctx.handle, store)
     assert rel(op.matvec(g["x"]), g["y_b"]) < 1e-12
+    assert rel(op.matvec(g["x"]), g["y_b"]) < 1e-12         # a second apply reuses the stored c_w
     # the reaction part alone: A_b x - (A_a x - a c1 M_t M_s x) = M_R x
     _, op_sep, _ = product_objects(g, with_su=False, u=g["u"], w=g["w"])
     _, op_sep0, _ = product_objects(g, with_su=False)

@@ -30,6 +30,9 @@ def one(lib, ne, ne_t, reps, p=3):
     u = torch.from_numpy(rng.uniform(0, 1, N)).to(dev)
     w = torch.from_numpy(rng.uniform(0, 0.1, N)).to(dev)
     set_reaction(op.ctx, st, 1.0, RM, u, w, None)
+    if os.environ.get("RX_STORE") is not None:
+        from paper_2311_17500_b200 import _lib as LL
+        LL.call("mi_op_set_reaction_store", op.ctx.handle, int(os.environ["RX_STORE"]))
     del u, w
     x = torch.from_numpy(rng.uniform(-1, 1, N)).to(dev)
     y = torch.empty_like(x)
