@@ -100,7 +100,14 @@ def lowrank_factorize(values, tol):
     indicators through the Gram matrix, see below)."""
     if not 0.0 < tol < 1.0:
         raise ValueError("tolerance must lie in (0, 1)")
-    th = np.asarray(getattr(values, "values", values), float)
+    is_torch = type(values).__module__.startswith("torch")   # (a tensor's .values is a method)
+    th = values if is_torch else getattr(values, "values", values)
+    if type(th).__module__.startswith("torch"):
+        lr = _lowrank_device(th, tol)
+        if lr is not None:
+            return lr
+        th = th.cpu().numpy()
+    th = np.asarray(th, float)
     nrm = np.linalg.norm(th)
     nt, ns = th.shape
     if nrm == 0.0:
@@ -125,6 +132,30 @@ def lowrank_factorize(values, tol):
 
 
 GRAM_MIN_SIZE = 2_000_000
+
+
+def _lowrank_device(th, tol):
+    """The Gram path of lowrank_factorize with the indicator on the device: Theta Theta^T and the
+    spatial factors Theta^T W / s by cuBLAS DGEMM, the N_t x N_t eigendecomposition and the rank decision
+    on the host.  None when the full SVD must decide (small / not wide / tail at the cut)."""
+    import torch
+    nt, ns = th.shape
+    if not (nt * ns > GRAM_MIN_SIZE and ns >= 8 * nt):
+        return None
+    nrm = float(torch.linalg.norm(th).item())
+    if nrm == 0.0:
+        return None
+    lam, W = np.linalg.eigh((th @ th.T).cpu().numpy())
+    lam, W = np.clip(lam[::-1], 0.0, None), W[:, ::-1]
+    tails2 = np.append(np.cumsum(lam[::-1])[::-1], 0.0)
+    cut2 = (tol * nrm) ** 2
+    if np.min(np.abs(tails2 - cut2)) <= 1e-8 * nrm ** 2:
+        return None
+    rank = max(int(np.argmax(tails2 <= cut2)), 1)
+    s = np.sqrt(lam[:rank])
+    Wr = np.ascontiguousarray(W[:, :rank])
+    V = (th.T @ torch.from_numpy(Wr).to(th.device)).cpu().numpy() / s
+    return LowRankIndicator(th, rank, Wr, V, s[:rank].copy(), tol)
 
 
 def hat_values(nodes, x):

@@ -70,8 +70,17 @@ class _Workspace:
                                  lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd)
 
 
+def _host_indicator(ind):
+    """SolveResult carries a numpy indicator (the driver may hold it on the device)."""
+    v = getattr(ind, "values", None)
+    if torch.is_tensor(v):
+        ind.values = v.cpu().numpy()
+    return ind
+
+
 def _indicator_values(ind):
-    return np.asarray(getattr(ind, "values", ind), float)
+    v = ind if torch.is_tensor(ind) else getattr(ind, "values", ind)
+    return v if torch.is_tensor(v) else np.asarray(v, float)
 
 
 class _Phases:
@@ -136,12 +145,16 @@ def fixed_point_solve(problem, config=None, device=0):
                 if config.indicator_override is not None:
                     fresh = config.indicator_override(problem, u.cpu().numpy(), w.cpu().numpy())
                 else:
-                    fresh = ws.indicator.compute(u, w)
+                    fresh = ws.indicator.compute(u, w, on_device=True)
                 ph.stop("indicator")
                 if indicator is not None and alpha < 1.0:
                     prev = _indicator_values(indicator)
                     fv = _indicator_values(fresh)
-                    drift = float(np.max(np.abs(fv - prev)))
+                    if torch.is_tensor(fv) or torch.is_tensor(prev):
+                        fv, prev = (torch.as_tensor(v, device=dev) for v in (fv, prev))
+                        drift = float((fv - prev).abs().max().item())
+                    else:
+                        drift = float(np.max(np.abs(fv - prev)))
                     fresh.values = alpha * fv + (1.0 - alpha) * prev
                     if (config.indicator_freeze_tol > 0.0 and k > galerkin_sweeps + 1
                             and drift * alpha <= config.indicator_freeze_tol):
@@ -179,8 +192,8 @@ def fixed_point_solve(problem, config=None, device=0):
         u, w = u_new, w_new
         if inc <= config.tolerance:
             return SolveResult(u.cpu().numpy(), w.cpu().numpy(), k, increments, True, gmres_iters, pcg_iters,
-                               _time.perf_counter() - t0, indicator, ph.sec)
+                               _time.perf_counter() - t0, _host_indicator(indicator), ph.sec)
     result = SolveResult(u.cpu().numpy(), w.cpu().numpy(), galerkin_sweeps + config.max_iterations, increments,
-                         False, gmres_iters, pcg_iters, _time.perf_counter() - t0, indicator, ph.sec)
+                         False, gmres_iters, pcg_iters, _time.perf_counter() - t0, _host_indicator(indicator), ph.sec)
     raise FixedPointDiverged("fixed point did not reach %.2e in %d iterations"
                              % (config.tolerance, config.max_iterations), result)

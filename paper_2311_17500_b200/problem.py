@@ -181,14 +181,21 @@ class ResidualIndicator:
     """N_t x N_s indicator values with the Greville grids (stabilization.py:177-193)."""
 
     def __init__(self, values, time_greville, spatial_grevilles, spatial_shape):
-        self.values = np.asarray(values, float)
+        # numpy, or a CUDA tensor when the driver keeps the indicator on the device
+        self.values = values if _is_tensor(values) else np.asarray(values, float)
         self.time_greville = np.asarray(time_greville, float)
         self.spatial_grevilles = [np.asarray(g, float) for g in spatial_grevilles]
         self.spatial_shape = tuple(spatial_shape)
 
     @property
     def max(self):
+        if _is_tensor(self.values):
+            return float(self.values.max().item()) if self.values.numel() else 0.0
         return float(self.values.max(initial=0.0))
+
+
+def _is_tensor(v):
+    return type(v).__module__.startswith("torch")
 
 
 # --------------------------------------------------------------------------

@@ -131,8 +131,9 @@ class DeviceIndicator:
         _lib.call("mi_window_max", self.ctx.handle, dptr(src), dptr(dst), int(outer), int(n_in), len(wins),
                   int(inner), host_ptr(w0), host_ptr(w1))
 
-    def compute(self, u, w):
-        """ResidualIndicator for the state (u, w) (numpy or device tensors of length N)."""
+    def compute(self, u, w, on_device=False):
+        """ResidualIndicator for the state (u, w) (numpy or device tensors of length N).  With
+        ``on_device`` its values stay a CUDA tensor (the driver relaxes and factorises them there)."""
         ctx, st, d = self.ctx, self.st, self.d
         ctx.bind_stream()
         ud = ctx.to_device(u)
@@ -174,7 +175,7 @@ class DeviceIndicator:
         if denom > 0.0:
             theta = ctx.empty(numer.numel())
             _lib.call("mi_theta_ratio", ctx.handle, dptr(numer), dptr(theta), int(numer.numel()), denom)
-            values = theta.cpu().numpy().reshape(nt, st.num_space)
+            values = theta.view(nt, st.num_space) if on_device else theta.cpu().numpy().reshape(nt, st.num_space)
         else:
             # stabilization.py:317-333 (zero denominator)
             nh = numer.cpu().numpy().reshape(nt, st.num_space)
