@@ -125,7 +125,7 @@ int mi_op_set_reaction_weight(mi_ctx* ctx, const double* jw);
  * apply interpolates only x.  mode -1: when it fits in 40% of the free
  * device memory (default), 0: never, 1: always. */
 int mi_op_set_reaction_store(mi_ctx* ctx, int mode);
-/* Time-sharded slabs: the reaction tables cover local time elements whose
+/* Time slabs (KroneckerOperator(time_rows=...)): the reaction tables cover local time elements whose
  * full-basis function ft maps to local row ft + row_offset (default -1). */
 int mi_op_set_reaction_rows(mi_ctx* ctx, int row_offset);
 
@@ -145,7 +145,7 @@ int mi_pc_setup(mi_ctx* ctx, const double* U, const double* lam, double cm, doub
                 const double* g, const double* glow, double sigma);
 /* z = P^-1 r  (r, z device; may alias) */
 int mi_pc_apply(mi_ctx* ctx, const double* r, double* z);
-/* Stages for the time-sharded preconditioner: spatial transforms
+/* Split preconditioner stages (a caller distributing the columns itself): spatial transforms
  * of nrows local time rows (inverse=0: U^T, inverse=1: U), and the time
  * stage (Q^T, block-arrowhead solve, Q) in place on a time-major (N_t x
  * ncols) block of spatial eigen-columns [col0, col0+ncols) after the

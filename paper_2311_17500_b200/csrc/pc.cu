@@ -31,7 +31,7 @@ __global__ void arrowhead_solve(double* __restrict__ Y, const double* __restrict
                                 const double* __restrict__ gl, double sigma, double cm, double react,
                                 int n1, int n2, int nt, long long ns, long long col0) {
   // Y is (nt x ns) with ns = number of columns handled; column j is global
-  // spatial eigen-index col0 + j (time-sharded runs handle a column range).
+  // spatial eigen-index col0 + j (a caller may hand in a column range).
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= ns) return;
   const long long sg = s + col0;
@@ -209,7 +209,7 @@ static int pc_spatial(mi_ctx* c, const double* in, double* out, long long nrows,
 
 // time stage on a (nt x ncols) column block (time-major): Q^T, arrowhead, Q.  In place.  Column j is
 // the spatial eigen-index col0 + j of the grid (n1, n2c, *) whose direction-2 indices start at y_lo
-// (unsharded and time-sharded: n2c = n_2, y_lo = 0; z-sharded y-slabs: n2c = owned y range).
+// (unsharded / column ranges: n2c = n_2, y_lo = 0; z-sharded y-slabs: n2c = owned y range).
 static int pc_time(mi_ctx* c, double* y, long long ncols, long long col0, int y_lo = 0, int n2c = -1) {
   cudaStream_t st = c->stream;
   const int nt = c->nt;

@@ -9,7 +9,7 @@ Hessenberg column and the Givens rotations are handled on the host (one
 small device->host copy per iteration, needed for the stopping test).
 
 The core loop (:func:`gmres_core`) is written against a small vector-ops
-interface plus an optional ``allreduce`` hook, so the time-sharded solve
+interface plus an optional ``allreduce`` hook, so the space-sharded solve
 (sharded.py) runs the identical recurrence on local slabs with NCCL
 allreduces of the dot products.
 """
