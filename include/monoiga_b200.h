@@ -160,6 +160,11 @@ int mi_pc_apply_time(mi_ctx* ctx, double* y, long long ncols, long long col0);
  * i_2 in [y_lo, y_hi). */
 int mi_pc_mode(mi_ctx* ctx, int l, int inverse, const double* in, double* out, long long outer, long long inner);
 int mi_pc_apply_time_yslab(mi_ctx* ctx, double* y, int y_lo, int y_hi);
+/* Number of symmetric modes hs of direction l when its eigenbasis is an
+ * exactly mirrored even/odd basis (uniform knots: factors._centro_eigh) and
+ * the spatial transforms run as two half-size products (mode_fold.cuh);
+ * 0 when the dense n_l x n_l product is used.  Same P^-1 either way. */
+int mi_pc_fold(mi_ctx* ctx, int l);
 
 /* ---------------------------------------------------------------------
  * Recovery-variable solve ((W_t + b d_e M_t) (x) M_s) w = g  (replaces

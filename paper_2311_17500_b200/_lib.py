@@ -45,6 +45,7 @@ _SIGS = {
     "mi_pc_apply_time": ([_vp, _vp, _c_ll, _c_ll], _c_int),
     "mi_pc_apply_time_yslab": ([_vp, _vp, _c_int, _c_int], _c_int),
     "mi_pc_mode": ([_vp, _c_int, _c_int, _vp, _vp, _c_ll, _c_ll], _c_int),
+    "mi_pc_fold": ([_vp, _c_int], _c_int),
     "mi_ws_setup": ([_vp, _vp, _vp, _vp], _c_int),
     "mi_ws_time": ([_vp, _vp, _vp], _c_int),
     "mi_ws_mass": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),

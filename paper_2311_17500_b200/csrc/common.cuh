@@ -109,6 +109,7 @@ struct mi_ctx {
   // ---- preconditioner
   bool pc_ready = false;
   mi::DeviceBuf Us[3], UsT[3];  // per direction n_l x n_l (U and U^T)
+  int fold_hs[3] = {0, 0, 0};   // > 0: U_l is an exactly mirrored even/odd basis (mode_fold.cuh), hs symmetric modes first
   mi::DeviceBuf lam[3];         // per direction eigenvalues (already scaled by sigma_l)
   mi::DeviceBuf Q, QT;          // time basis nt x nt and transpose
   mi::DeviceBuf pen_diag, pen_off, pen_g, pen_glow;  // (nt-1)

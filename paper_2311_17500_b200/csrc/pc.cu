@@ -11,7 +11,10 @@
 // reference materialises H_int as an (N_t-1) x N_s complex array).
 #include "common.cuh"
 #include "gemm.cuh"
+#include "mode_fold.cuh"
 #include "mode_resident.cuh"
+
+#include <cstdlib>
 #include "tstage.cuh"
 
 #ifndef MI_TSTAGE
@@ -98,6 +101,38 @@ static cudaError_t mode_contig(const double* Bm, const double* in, double* out, 
   return launch_panel_n<false>(g, n, 1, st);
 }
 
+// Spatial transform of direction l (forward U_l^T, inverse U_l) along a mode of extent n_l that is
+// contiguous (inner == 1: `outer` rows) or strided.  Even/odd bases take the folded kernel.
+static cudaError_t spatial_mode(mi_ctx* c, int l, bool inverse, const double* in, double* out, long long inner,
+                                long long outer) {
+  const int n = c->n[l];
+  cudaError_t err;
+  if (c->fold_hs[l] > 0) {
+    const bool done = inner == 1
+        ? launch_mode_fold<true>(c->Us[l].p, in, out, n, inverse, 1, outer, num_sms(), c->stream, &err)
+        : launch_mode_fold<false>(c->Us[l].p, in, out, n, inverse, inner, outer, num_sms(), c->stream, &err);
+    if (done) return err;
+  }
+  if (inner == 1) return mode_contig(inverse ? c->UsT[l].p : c->Us[l].p, in, out, n, outer, c->stream);
+  return mode_strided(inverse ? c->Us[l].p : c->UsT[l].p, in, out, n, inner, outer, c->stream);
+}
+
+// hs (> 0) if the n x n row-major U is EXACTLY an even/odd basis with the symmetric modes first
+// (U[n-1-k][m] = U[k][m] for m < hs, = -U[k][m] and U[n/2][m] = 0 (n odd) for m >= hs), else 0
+static int exact_fold(const std::vector<double>& u, int n) {
+  const int h = n / 2, hs = n - h;
+  if (n < 4) return 0;
+  for (int k = 0; k < h; ++k)
+    for (int m = 0; m < n; ++m) {
+      const double a = u[(size_t)k * n + m], b = u[(size_t)(n - 1 - k) * n + m];
+      if (m < hs ? (a != b) : (a != -b)) return 0;
+    }
+  if (n & 1)
+    for (int m = hs; m < n; ++m)
+      if (u[(size_t)h * n + m] != 0.0) return 0;
+  return hs;
+}
+
 }  // namespace mi
 
 using namespace mi;
@@ -127,6 +162,7 @@ int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double
     } else {
       u[0] = ut[0] = 1.0;
     }
+    c->fold_hs[l] = (l < c->d && std::getenv("MI_NO_FOLD") == nullptr) ? exact_fold(u, nl) : 0;
     MI_CUDA(cudaMemcpy(c->Us[l].p, u.data(), sizeof(double) * nl * nl, cudaMemcpyHostToDevice));
     MI_CUDA(cudaMemcpy(c->UsT[l].p, ut.data(), sizeof(double) * nl * nl, cudaMemcpyHostToDevice));
     MI_CUDA(cudaMemcpy(c->lam[l].p, lm.data(), sizeof(double) * nl, cudaMemcpyHostToDevice));
@@ -196,11 +232,11 @@ static int pc_spatial(mi_ctx* c, const double* in, double* out, long long nrows,
     double* o = dst();
     ProfScope ps(c, PROF_PC_SPATIAL);
     if (l == 0) {
-      MI_CUDA(mode_contig(inverse ? c->UsT[0].p : c->Us[0].p, cur, o, n1, N / n1, st));
+      MI_CUDA(spatial_mode(c, 0, inverse, cur, o, 1, N / n1));
     } else if (l == 1) {
-      MI_CUDA(mode_strided(inverse ? c->Us[1].p : c->UsT[1].p, cur, o, n2, n1, N / ((long long)n1 * n2), st));
+      MI_CUDA(spatial_mode(c, 1, inverse, cur, o, n1, N / ((long long)n1 * n2)));
     } else {
-      MI_CUDA(mode_strided(inverse ? c->Us[2].p : c->UsT[2].p, cur, o, n3, (long long)n1 * n2, nrows, st));
+      MI_CUDA(spatial_mode(c, 2, inverse, cur, o, (long long)n1 * n2, nrows));
     }
     cur = o;
   }
@@ -278,18 +314,18 @@ int mi_pc_apply_time_yslab(mi_ctx* c, double* y, int y_lo, int y_hi) {
   return pc_time(c, y, ncols, 0, y_lo, y_hi - y_lo);
 }
 
+int mi_pc_fold(mi_ctx* c, int l) {
+  if (c == nullptr || !c->pc_ready || l < 0 || l > 2) return 0;
+  return c->fold_hs[l];
+}
+
 int mi_pc_mode(mi_ctx* c, int l, int inverse, const double* in, double* out, long long outer, long long inner) {
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   MI_REQUIRE(l >= 0 && l < c->d, MI_ERR_ARG, "direction out of range");
   MI_REQUIRE(outer >= 1 && inner >= 1 && in != out, MI_ERR_ARG, "bad mode-product shape or aliasing");
-  const int n = c->n[l];
   ProfScope ps(c, PROF_PC_SPATIAL);
   // forward applies U_l^T, inverse U_l (pc_spatial's convention)
-  if (inner == 1) {
-    MI_CUDA(mode_contig(inverse ? c->UsT[l].p : c->Us[l].p, in, out, n, outer, c->stream));
-  } else {
-    MI_CUDA(mode_strided(inverse ? c->Us[l].p : c->UsT[l].p, in, out, n, inner, outer, c->stream));
-  }
+  MI_CUDA(spatial_mode(c, l, inverse != 0, in, out, inner, outer));
   return MI_OK;
 }
 

@@ -262,6 +262,46 @@ def _hat_triple(space, length):
 # Fast diagonalisation
 # --------------------------------------------------------------------------
 
+def _centro_eigh(K, M):
+    """eigh(K, M) of a centrosymmetric pencil (J K J = K, J M J = M, J the index reversal: uniform
+    open knot vectors) as two half-size problems on the even and odd subspaces.  The hs = n - n/2
+    symmetric eigenvectors come first, then the h = n/2 skew ones, every pair of mirrored rows
+    EXACTLY equal (or opposite): the device then applies U_l^T / U_l as two half-size products
+    (csrc/mode_fold.cuh).  Returns None when the pencil is not centrosymmetric to rounding."""
+    n = K.shape[0]
+    if n < 4:
+        return None
+    for A in (K, M):
+        if np.max(np.abs(A - A[::-1, ::-1])) > 1e-13 * np.max(np.abs(A)):
+            return None
+    h = n // 2
+    hs = n - h
+    r = 1.0 / np.sqrt(2.0)
+    Ps = np.zeros((n, hs))
+    Pa = np.zeros((n, h))
+    for k in range(h):
+        Ps[k, k] = Ps[n - 1 - k, k] = r
+        Pa[k, k], Pa[n - 1 - k, k] = r, -r
+    if n % 2:
+        Ps[h, h] = 1.0
+    out_l, out_v = [], []
+    for P in (Ps, Pa):
+        Kb, Mb = P.T @ K @ P, P.T @ M @ P
+        lam, V = sla.eigh(0.5 * (Kb + Kb.T), 0.5 * (Mb + Mb.T))
+        out_l.append(lam)
+        out_v.append(V)
+    U = np.zeros((n, n))
+    top = out_v[0][:h] * r
+    U[:h, :hs] = top
+    U[n - 1 - np.arange(h), :hs] = top
+    if n % 2:
+        U[h, :hs] = out_v[0][h]
+    top = out_v[1] * r
+    U[:h, hs:] = top
+    U[n - 1 - np.arange(h), hs:] = -top
+    return np.concatenate(out_l), U
+
+
 def spatial_eigs(st, lengths=None):
     """eigh(K_l, M_l) per direction with the box separable weights.
 
@@ -276,8 +316,10 @@ def spatial_eigs(st, lengths=None):
     out = []
     for l, s in enumerate(st.spatial):
         M, K, _ = univariate_factors(s)
+        Kl, Ml = (cm / L[l] ** 2) * K, cm * M
         try:
-            lam, U = sla.eigh((cm / L[l] ** 2) * K, cm * M)
+            split = _centro_eigh(Kl, Ml)
+            lam, U = split if split is not None else sla.eigh(Kl, Ml)
         except sla.LinAlgError as exc:
             raise DecompositionError("generalized eigendecomposition failed: %s" % exc) from exc
         out.append((U, lam))
