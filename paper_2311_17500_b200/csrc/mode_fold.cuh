@@ -18,40 +18,63 @@
 // fold is applied to the operand fragments as they are read from shared
 // memory (one add per fragment, reused by every tile of its block); the
 // unfold happens in registers at the store (the lane holding g_s[k] also
-// holds g_a[k]).  Structure otherwise as mode_resident.cuh: one 256-thread
-// block per SM, both half factors resident in shared memory as DMMA
-// fragments, full-K data panels double-buffered by cp.async.
+// holds g_a[k]).
+//
+// One block per SM, warp-specialised over a ring of three panel buffers:
+// 4 producer warps load tile j+2 (cp.async, completion on the buffer's
+// mbarrier) and store tile j (coalesced rows) while 8 consumer warps run the
+// DMMAs of tile j+1.  Each consumer warp owns 8 columns (rows) of the panel
+// and writes its results back over them in place, so the store of a tile
+// needs no staging copy and overlaps the next tile's tensor-core work.  Both
+// half factors stay resident in shared memory as DMMA fragments.
+// (Loads, stores and DMMAs serialised in one warp set measured additive:
+// 2.4 + 2.5 + 4.3 ms for the six cfg-4 transforms.)
 #pragma once
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
 
+#ifndef MI_MF_NPW
+#define MI_MF_NPW 8
+#endif
+
 namespace mi {
 
 template <int TH>
 struct ModeFold {
+  static constexpr int NCW = 8, NPW = MI_MF_NPW;    // consumer / producer warps
+  static constexpr int NTH = 32 * (NCW + NPW);
+  static constexpr int NPT = 32 * NPW;              // producer threads
+  static constexpr int NB = 3;                      // panel ring
   static constexpr int KS = 2 * TH;                 // k-steps per half block: K padded to 8 * TH >= hs
-  static constexpr int KP = 16 * TH;                // panel depth: both halves (>= n)
+  static constexpr int KP = 16 * TH < 104 ? 16 * TH : 104;   // panel depth: n <= KP
   static constexpr int FH = TH * KS * 32;           // fragments of one half factor (doubles)
-  static constexpr int BLD = 68;                    // COLS panel row stride (conflict-free B reads)
+  static constexpr int BLD = 68;                    // COLS panel row stride (= 4 mod 16: conflict-free B reads)
   static constexpr int ALD = (KP % 16 == 4 || KP % 16 == 12) ? KP : KP + ((4 - KP % 16) + 16) % 16;
-  static constexpr size_t SMEM_COLS = (size_t)(2 * FH + 2 * KP * BLD) * 8;
-  static constexpr size_t SMEM_ROWS = (size_t)(2 * FH + 2 * 64 * ALD) * 8;
+  static constexpr int PCOLS = KP * BLD, PROWS = 64 * ALD;   // panel sizes (doubles)
+  static constexpr size_t SMEM_COLS = (size_t)(2 * FH + NB * PCOLS) * 8 + 64;
+  static constexpr size_t SMEM_ROWS = (size_t)(2 * FH + NB * PROWS) * 8 + 64;
   static_assert(SMEM_COLS <= 227 * 1024 && SMEM_ROWS <= 227 * 1024, "folded mode product exceeds shared memory");
 };
 
 // U: n x n row-major eigenvector matrix (columns = modes, symmetric first).  INV = false applies
 // U^T (into mode space), INV = true applies U.  ROWS: the mode is the contiguous index
 // (out[r][.] from in[r][.], `outer` rows); COLS: out[o][.][c] from in[o][.][c] (stride `inner`).
+// Tiles: 64 flattened columns (COLS) or 64 rows (ROWS).
 template <int TH, bool ROWS, bool INV>
-__global__ void __launch_bounds__(256, 1) mode_fold(const double* __restrict__ U, const double* __restrict__ in,
-                                                     double* __restrict__ out, int n, long long inner,
-                                                     long long outer) {
+__global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* __restrict__ U,
+                                                                   const double* __restrict__ in,
+                                                                   double* __restrict__ out, int n,
+                                                                   long long inner, long long outer) {
   using G = ModeFold<TH>;
-  constexpr int KS = G::KS, KP = G::KP;
-  extern __shared__ double smem[];
+  constexpr int KS = G::KS, NB = G::NB;
+  constexpr int PS = ROWS ? G::PROWS : G::PCOLS;    // panel size
+  constexpr int LD = ROWS ? G::ALD : G::BLD;        // panel row stride
+  extern __shared__ __align__(16) double smem[];
   double* frag = smem;                               // [half][TH][KS][32]
-  double* pan = smem + 2 * G::FH;                    // [2][panel]
+  double* pan = smem + 2 * G::FH;                    // [NB][panel]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(pan + NB * PS);   // [NB]
+  unsigned long long* done = full + NB;                                              // [NB] computed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, t4 = lane & 3;
   const int h = n >> 1, hs = n - h;
@@ -60,7 +83,7 @@ __global__ void __launch_bounds__(256, 1) mode_fold(const double* __restrict__ U
   // (size_0 = hs, size_1 = h).  Tile index i / k-step ks select
   //   COLS fwd : A[m = 8 i + q][k = 4 ks + t]      COLS inv : A[k = 8 i + q][m = 4 ks + t]
   //   ROWS fwd : B[k = 4 ks + t][m = 8 i + q]      ROWS inv : B[m = 4 ks + t][k = 8 i + q]
-  for (int e = tid; e < 2 * G::FH; e += 256) {
+  for (int e = tid; e < 2 * G::FH; e += G::NTH) {
     const int l = e & 31, ks = (e >> 5) % KS, i = ((e >> 5) / KS) % TH, b = (e >> 5) / (KS * TH);
     const int q = l >> 2, t = l & 3;
     const int r8 = 8 * i + q, c4 = 4 * ks + t;
@@ -68,179 +91,152 @@ __global__ void __launch_bounds__(256, 1) mode_fold(const double* __restrict__ U
     const int sz = b == 0 ? hs : h;
     frag[e] = (m < sz && k < sz) ? __ldg(U + (long long)k * n + b * hs + m) : 0.0;
   }
-  const double* fs = frag;
-  const double* fa = frag + G::FH;
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], G::NPT);                   // one cp.async-completion arrival per producer thread
+      mbar_init(&done[b], 32 * G::NCW);              // every consumer thread arrives after its write-back
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
   const long long total = ROWS ? outer : outer * inner;
   const long long ntiles = (total + 63) / 64;
-  if constexpr (!ROWS) {
-    const int lc = tid & 63, lk = tid >> 6;
-    auto load = [&](long long tile, int buf) {
-      const long long g = tile * 64 + lc;
-      const bool okc = g < total;
-      long long base = 0;
-      if (okc) {
-        const long long o = g / inner;
-        base = o * n * inner + (g - o * inner);
-      }
-      double* dst = pan + buf * KP * G::BLD + lc;
-#pragma unroll 4
-      for (int m = 0; m < KP / 4; ++m) {
-        const int k = lk + 4 * m;
-        const bool v = okc && k < n;
-        cp_async8(dst + k * G::BLD, v ? in + base + (long long)k * inner : in, v);
-      }
-      cp_async_commit();
+  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp >= G::NCW) {
+    // ================= producers: loads of tile j + 2, stores of tile j =================
+    const int p = tid - 32 * G::NCW;
+    // COLS: thread -> column c = p & 63, rows (p >> 6) + 2 m; ROWS: flat element stride
+    auto col_base = [&](long long tile, int c, bool& ok) -> long long {
+      const long long g = tile * 64 + c;
+      ok = g < total;
+      if (!ok) return 0;
+      const long long o = g / inner;
+      return o * n * inner + (g - o * inner);
     };
-    long long tile = blockIdx.x;
-    if (tile < ntiles) load(tile, 0);
-    __syncthreads();
-    const int col = 8 * warp + gq;
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-      const int buf = it & 1;
-      const long long next = tile + gridDim.x;
-      if (next < ntiles) {
-        load(next, buf ^ 1);
-        cp_async_wait<1>();
+    auto load = [&](long long j) {
+      const int b = (int)(j % NB);
+      const long long tile = blockIdx.x + j * gridDim.x;
+      double* dst = pan + b * PS;
+      if constexpr (!ROWS) {
+        const int c = p & 63;
+        bool ok;
+        const long long base = col_base(tile, c, ok);
+        if (ok)
+          for (int r = p >> 6; r < n; r += G::NPT / 64) cp_async8(dst + r * LD + c, in + base + (long long)r * inner, true);
       } else {
-        cp_async_wait<0>();
+        const long long r0 = tile * 64;
+        const int nrow = (int)(total - r0 < 64 ? total - r0 : 64);
+        const double* src = in + r0 * n;
+        for (int e = p; e < nrow * n; e += G::NPT) {
+          const int r = e / n, k = e - r * n;
+          cp_async8(dst + r * LD + k, src + e, true);
+        }
       }
-      __syncthreads();
-      const double* bs = pan + buf * KP * G::BLD;
+      cp_async_mbar_arrive_noinc(&full[b]);
+    };
+    auto store = [&](long long j) {
+      const int b = (int)(j % NB);
+      const long long tile = blockIdx.x + j * gridDim.x;
+      const double* sp = pan + b * PS;
+      if constexpr (!ROWS) {
+        const int c = p & 63;
+        bool ok;
+        const long long base = col_base(tile, c, ok);
+        if (ok)
+          for (int r = p >> 6; r < n; r += G::NPT / 64) out[base + (long long)r * inner] = sp[r * LD + c];
+      } else {
+        const long long r0 = tile * 64;
+        const int nrow = (int)(total - r0 < 64 ? total - r0 : 64);
+        double* dst = out + r0 * n;
+        for (int e = p; e < nrow * n; e += G::NPT) {
+          const int r = e / n, k = e - r * n;
+          dst[e] = sp[r * LD + k];
+        }
+      }
+    };
+    if (nloc > 0) load(0);
+    if (nloc > 1) load(1);
+    for (long long j = 0; j < nloc; ++j) {
+      // buffer (j + 2) % NB held tile j - 1, stored by every producer in the previous iteration
+      asm volatile("bar.sync 1, %0;\n" ::"n"(G::NPT) : "memory");
+      if (j + 2 < nloc) load(j + 2);
+      mbar_wait(&done[j % NB], (unsigned)((j / NB) & 1));
+      store(j);
+    }
+  } else {
+    // ================= consumers: DMMAs of tile j, results written over the panel =================
+    const int own = 8 * warp + gq;                   // COLS: column; ROWS: row of this lane's operand
+    for (long long j = 0; j < nloc; ++j) {
+      const int b = (int)(j % NB);
+      mbar_wait(&full[b], (unsigned)((j / NB) & 1));
+      double* P = pan + b * PS;
       double as_[TH][2], aa_[TH][2];
 #pragma unroll
       for (int i = 0; i < TH; ++i) as_[i][0] = as_[i][1] = aa_[i][0] = aa_[i][1] = 0.0;
+      // operand element v(k): COLS panel row k of column `own`; ROWS row `own`, column k
+      const double* src = ROWS ? P + own * LD : P + own;
+      constexpr int ST = ROWS ? 1 : LD;
 #pragma unroll 2
       for (int ks = 0; ks < KS; ++ks) {
         const int k = 4 * ks + t4;
-        double bsym, bskw;
+        double vs, va;
         if constexpr (!INV) {
-          const double xk = bs[k * G::BLD + col];
-          const double xr = bs[(k < h ? n - 1 - k : k) * G::BLD + col];
-          bsym = k < h ? xk + xr : ((odd && k == h) ? xk : 0.0);
-          bskw = k < h ? xk - xr : 0.0;
+          const double xk = src[k * ST];
+          const double xr = src[(k < h ? n - 1 - k : k) * ST];
+          vs = k < h ? xk + xr : ((odd && k == h) ? xk : 0.0);
+          va = k < h ? xk - xr : 0.0;
         } else {
-          bsym = k < hs ? bs[k * G::BLD + col] : 0.0;
-          bskw = k < h ? bs[(hs + k) * G::BLD + col] : 0.0;
+          vs = k < hs ? src[k * ST] : 0.0;
+          va = k < h ? src[(hs + k) * ST] : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < TH; ++i) {
-          dmma(as_[i][0], as_[i][1], fs[(i * KS + ks) * 32 + lane], bsym);
-          dmma(aa_[i][0], aa_[i][1], fa[(i * KS + ks) * 32 + lane], bskw);
+          if constexpr (!ROWS) {
+            dmma(as_[i][0], as_[i][1], frag[(i * KS + ks) * 32 + lane], vs);
+            dmma(aa_[i][0], aa_[i][1], frag[G::FH + (i * KS + ks) * 32 + lane], va);
+          } else {
+            dmma(as_[i][0], as_[i][1], vs, frag[(i * KS + ks) * 32 + lane]);
+            dmma(aa_[i][0], aa_[i][1], va, frag[G::FH + (i * KS + ks) * 32 + lane]);
+          }
         }
       }
-      long long ob[2];
+      __syncwarp();                                  // every lane's operand reads precede the write-back
+      // this lane's results: index r = 8 i + gq (COLS: panel row, columns 8 warp + 2 t4 + e) or
+      // r = 8 i + 2 t4 + e (ROWS: panel column of row 8 warp + gq)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const long long g = tile * 64 + 8 * warp + 2 * t4 + e;
-        ob[e] = -1;
-        if (g < total) {
-          const long long o = g / inner;
-          ob[e] = o * n * inner + (g - o * inner);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < TH; ++i) {
-        const int r = 8 * i + gq;
+      for (int i = 0; i < TH; ++i)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (ob[e] < 0) continue;
-          double* o = out + ob[e];
+          const int r = ROWS ? 8 * i + 2 * t4 + e : 8 * i + gq;
+          double* d = ROWS ? P + (8 * warp + gq) * LD : P + 8 * warp + 2 * t4 + e;
           if constexpr (!INV) {
-            if (r < hs) o[(long long)r * inner] = as_[i][e];
-            if (r < h) o[(long long)(hs + r) * inner] = aa_[i][e];
+            if (r < hs) d[r * ST] = as_[i][e];
+            if (r < h) d[(hs + r) * ST] = aa_[i][e];
           } else {
             if (r < h) {
-              o[(long long)r * inner] = as_[i][e] + aa_[i][e];
-              o[(long long)(n - 1 - r) * inner] = as_[i][e] - aa_[i][e];
+              d[r * ST] = as_[i][e] + aa_[i][e];
+              d[(n - 1 - r) * ST] = as_[i][e] - aa_[i][e];
             } else if (odd && r == h) {
-              o[(long long)r * inner] = as_[i][e];
+              d[r * ST] = as_[i][e];
             }
           }
         }
-      }
-      __syncthreads();
-    }
-  } else {
-    auto load = [&](long long tile, int buf) {
-      double* dst = pan + buf * 64 * G::ALD;
-      for (int e = tid; e < 64 * KP; e += 256) {
-        const int r = e / KP, k = e - r * KP;
-        const long long row = tile * 64 + r;
-        const bool v = row < total && k < n;
-        cp_async8(dst + r * G::ALD + k, v ? in + row * n + k : in, v);
-      }
-      cp_async_commit();
-    };
-    long long tile = blockIdx.x;
-    if (tile < ntiles) load(tile, 0);
-    __syncthreads();
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-      const int buf = it & 1;
-      const long long next = tile + gridDim.x;
-      if (next < ntiles) {
-        load(next, buf ^ 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* arow = pan + buf * 64 * G::ALD + (8 * warp + gq) * G::ALD;
-      double as_[TH][2], aa_[TH][2];
-#pragma unroll
-      for (int j = 0; j < TH; ++j) as_[j][0] = as_[j][1] = aa_[j][0] = aa_[j][1] = 0.0;
-#pragma unroll 2
-      for (int ks = 0; ks < KS; ++ks) {
-        const int k = 4 * ks + t4;
-        double asym, askw;
-        if constexpr (!INV) {
-          const double xk = arow[k];
-          const double xr = arow[k < h ? n - 1 - k : k];
-          asym = k < h ? xk + xr : ((odd && k == h) ? xk : 0.0);
-          askw = k < h ? xk - xr : 0.0;
-        } else {
-          asym = k < hs ? arow[k] : 0.0;
-          askw = k < h ? arow[hs + k] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < TH; ++j) {
-          dmma(as_[j][0], as_[j][1], asym, fs[(j * KS + ks) * 32 + lane]);
-          dmma(aa_[j][0], aa_[j][1], askw, fa[(j * KS + ks) * 32 + lane]);
-        }
-      }
-      const long long row = tile * 64 + 8 * warp + gq;
-      if (row < total) {
-        double* dst = out + row * n;
-#pragma unroll
-        for (int j = 0; j < TH; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = 8 * j + 2 * t4 + e;
-            if constexpr (!INV) {
-              if (c < hs) dst[c] = as_[j][e];
-              if (c < h) dst[hs + c] = aa_[j][e];
-            } else {
-              if (c < h) {
-                dst[c] = as_[j][e] + aa_[j][e];
-                dst[n - 1 - c] = as_[j][e] - aa_[j][e];
-              } else if (odd && c == h) {
-                dst[c] = as_[j][e];
-              }
-            }
-          }
-      }
-      __syncthreads();
+      mbar_arrive(&done[b]);
     }
   }
 }
 
-// Launch for hs = n - n/2 <= 8 * TH; returns false (nothing launched) outside the instantiated range.
+// Launch for hs = n - n/2 <= 8 * TH and n <= KP; returns false (nothing launched) outside the
+// instantiated range.
 template <bool ROWS>
 inline bool launch_mode_fold(const double* U, const double* in, double* out, int n, bool inverse, long long inner,
                              long long outer, int nsm, cudaStream_t st, cudaError_t* err) {
   const int hs = n - n / 2;
 #define MI_MF(THV)                                                                                       \
-  if (hs <= 8 * THV) {                                                                                   \
+  if (hs <= 8 * THV && n <= ModeFold<THV>::KP) {                                                         \
     constexpr size_t sm = ROWS ? ModeFold<THV>::SMEM_ROWS : ModeFold<THV>::SMEM_COLS;                    \
+    constexpr int nth = ModeFold<THV>::NTH;                                                              \
     static bool attr = false;                                                                            \
     if (!attr) {                                                                                         \
       cudaFuncSetAttribute(mode_fold<THV, ROWS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
@@ -251,9 +247,9 @@ inline bool launch_mode_fold(const double* U, const double* in, double* out, int
     const long long ntiles = (total + 63) / 64;                                                          \
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);                                                 \
     if (inverse)                                                                                         \
-      mode_fold<THV, ROWS, true><<<grid > 0 ? grid : 1, 256, sm, st>>>(U, in, out, n, inner, outer);     \
+      mode_fold<THV, ROWS, true><<<grid > 0 ? grid : 1, nth, sm, st>>>(U, in, out, n, inner, outer);     \
     else                                                                                                 \
-      mode_fold<THV, ROWS, false><<<grid > 0 ? grid : 1, 256, sm, st>>>(U, in, out, n, inner, outer);    \
+      mode_fold<THV, ROWS, false><<<grid > 0 ? grid : 1, nth, sm, st>>>(U, in, out, n, inner, outer);    \
     *err = cudaGetLastError();                                                                           \
     return true;                                                                                         \
   }
