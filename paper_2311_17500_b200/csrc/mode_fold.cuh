@@ -28,7 +28,10 @@
 // needs no staging copy and overlaps the next tile's tensor-core work.  Both
 // half factors stay resident in shared memory as DMMA fragments.
 // (Loads, stores and DMMAs serialised in one warp set measured additive:
-// 2.4 + 2.5 + 4.3 ms for the six cfg-4 transforms.)
+// 2.4 + 2.5 + 4.3 ms for the six cfg-4 transforms.)  Contiguous-mode tiles are
+// one contiguous HBM range: ONE bulk copy (TMA engine) in and one out, driven by a single
+// producer thread.  (Strided tiles with 16-byte cp.async per column pair, each panel row shifted
+// by the parity of its HBM start, measured slower than 8-byte copies: 7.4 vs 4.5 ms producer-only.)
 #pragma once
 #include <cuda_runtime.h>
 
@@ -51,7 +54,9 @@ struct ModeFold {
   static constexpr int FH = TH * KS * 32;           // fragments of one half factor (doubles)
   static constexpr int BLD = 68;                    // COLS panel row stride (= 4 mod 16: conflict-free B reads)
   static constexpr int ALD = (KP % 16 == 4 || KP % 16 == 12) ? KP : KP + ((4 - KP % 16) + 16) % 16;
-  static constexpr int PCOLS = KP * BLD, PROWS = 64 * ALD;   // panel sizes (doubles)
+  // panel sizes (doubles).  ROWS tiles are contiguous in HBM and move as ONE bulk copy each way, so
+  // their panel is dense (row stride n)
+  static constexpr int PCOLS = KP * BLD, PROWS = 64 * KP;
   static constexpr size_t SMEM_COLS = (size_t)(2 * FH + NB * PCOLS) * 8 + 64;
   static constexpr size_t SMEM_ROWS = (size_t)(2 * FH + NB * PROWS) * 8 + 64;
   static_assert(SMEM_COLS <= 227 * 1024 && SMEM_ROWS <= 227 * 1024, "folded mode product exceeds shared memory");
@@ -69,7 +74,7 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
   using G = ModeFold<TH>;
   constexpr int KS = G::KS, NB = G::NB;
   constexpr int PS = ROWS ? G::PROWS : G::PCOLS;    // panel size
-  constexpr int LD = ROWS ? G::ALD : G::BLD;        // panel row stride
+  const int LD = ROWS ? n : G::BLD;                 // panel row stride
   extern __shared__ __align__(16) double smem[];
   double* frag = smem;                               // [half][TH][KS][32]
   double* pan = smem + 2 * G::FH;                    // [NB][panel]
@@ -93,7 +98,7 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
   }
   if (tid == 0) {
     for (int b = 0; b < NB; ++b) {
-      mbar_init(&full[b], G::NPT);                   // one cp.async-completion arrival per producer thread
+      mbar_init(&full[b], ROWS ? 1 : G::NPT);        // COLS: one cp.async-completion arrival per producer thread
       mbar_init(&done[b], 32 * G::NCW);              // every consumer thread arrives after its write-back
     }
     mbar_fence_init();
@@ -124,16 +129,17 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
         const long long base = col_base(tile, c, ok);
         if (ok)
           for (int r = p >> 6; r < n; r += G::NPT / 64) cp_async8(dst + r * LD + c, in + base + (long long)r * inner, true);
+        cp_async_mbar_arrive_noinc(&full[b]);
       } else {
+        // one thread: the tile's nel = nrow * n doubles start 16-byte aligned (tile * 64 * n is even); an
+        // odd tail element is copied by hand before the arrive
         const long long r0 = tile * 64;
-        const int nrow = (int)(total - r0 < 64 ? total - r0 : 64);
+        const int nel = (int)(total - r0 < 64 ? total - r0 : 64) * n, nb = nel & ~1;
         const double* src = in + r0 * n;
-        for (int e = p; e < nrow * n; e += G::NPT) {
-          const int r = e / n, k = e - r * n;
-          cp_async8(dst + r * LD + k, src + e, true);
-        }
+        if (nel & 1) dst[nel - 1] = src[nel - 1];
+        mbar_expect_tx(&full[b], (unsigned)nb * 8);
+        if (nb) bulk_g2s(dst, src, (unsigned)nb * 8, &full[b]);
       }
-      cp_async_mbar_arrive_noinc(&full[b]);
     };
     auto store = [&](long long j) {
       const int b = (int)(j % NB);
@@ -147,26 +153,31 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
           for (int r = p >> 6; r < n; r += G::NPT / 64) out[base + (long long)r * inner] = sp[r * LD + c];
       } else {
         const long long r0 = tile * 64;
-        const int nrow = (int)(total - r0 < 64 ? total - r0 : 64);
+        const int nel = (int)(total - r0 < 64 ? total - r0 : 64) * n, nb = nel & ~1;
         double* dst = out + r0 * n;
-        for (int e = p; e < nrow * n; e += G::NPT) {
-          const int r = e / n, k = e - r * n;
-          dst[e] = sp[r * LD + k];
-        }
+        if (nel & 1) dst[nel - 1] = sp[nel - 1];
+        if (nb) bulk_s2g(dst, sp, (unsigned)nb * 8);
+        bulk_commit();
       }
     };
+    if (ROWS && p != 0) return;                      // ROWS: one thread drives the bulk copies
     if (nloc > 0) load(0);
     if (nloc > 1) load(1);
     for (long long j = 0; j < nloc; ++j) {
       // buffer (j + 2) % NB held tile j - 1, stored by every producer in the previous iteration
-      asm volatile("bar.sync 1, %0;\n" ::"n"(G::NPT) : "memory");
+      if constexpr (ROWS)
+        bulk_wait_read0();                           // the bulk store of tile j - 1 has read its buffer
+      else
+        asm volatile("bar.sync 1, %0;\n" ::"n"(G::NPT) : "memory");
       if (j + 2 < nloc) load(j + 2);
       mbar_wait(&done[j % NB], (unsigned)((j / NB) & 1));
       store(j);
     }
+    if constexpr (ROWS) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // before the block's smem goes away
   } else {
     // ================= consumers: DMMAs of tile j, results written over the panel =================
     const int own = 8 * warp + gq;                   // COLS: column; ROWS: row of this lane's operand
+    const int ksn = (hs + 3) >> 2;
     for (long long j = 0; j < nloc; ++j) {
       const int b = (int)(j % NB);
       mbar_wait(&full[b], (unsigned)((j / NB) & 1));
@@ -178,7 +189,7 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
       const double* src = ROWS ? P + own * LD : P + own;
       constexpr int ST = ROWS ? 1 : LD;
 #pragma unroll 2
-      for (int ks = 0; ks < KS; ++ks) {
+      for (int ks = 0; ks < ksn; ++ks) {            // K = hs (>= h) padded to 4, not to 8 * TH
         const int k = 4 * ks + t4;
         double vs, va;
         if constexpr (!INV) {
@@ -222,6 +233,7 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
             }
           }
         }
+      if constexpr (ROWS) fence_proxy_async_smem();   // the write-back is read by the bulk store (async proxy)
       mbar_arrive(&done[b]);
     }
   }

@@ -107,7 +107,8 @@ static cudaError_t spatial_mode(mi_ctx* c, int l, bool inverse, const double* in
                                 long long outer) {
   const int n = c->n[l];
   cudaError_t err;
-  if (c->fold_hs[l] > 0) {
+  // the contiguous mode moves each tile as one bulk copy: 16-byte-aligned buffers only
+  if (c->fold_hs[l] > 0 && (inner != 1 || ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0)) {
     const bool done = inner == 1
         ? launch_mode_fold<true>(c->Us[l].p, in, out, n, inverse, 1, outer, num_sms(), c->stream, &err)
         : launch_mode_fold<false>(c->Us[l].p, in, out, n, inverse, inner, outer, num_sms(), c->stream, &err);

@@ -82,4 +82,16 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(void* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(b) : "memory");
 }
 
+// 1D bulk copy shared -> global (TMA engine), bulk-group completion
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(src);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// this thread's committed bulk stores have finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// order this thread's generic-proxy shared-memory writes before later async-proxy (bulk copy) accesses
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 }  // namespace mi

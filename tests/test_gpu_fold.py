@@ -30,10 +30,14 @@ def _pc(st, fold):
             os.environ["MI_NO_FOLD"] = old
 
 
-# (d, p, ne, ne_t): n = ne + p spatial functions; hs = n - n // 2 covers every instantiated half
-# size (1, 2, 3, 5, 7 tiles of 8), odd and even n, and one size past the folded range (dense fallback)
+# (d, p, ne, ne_t): n = ne + p spatial functions (ne may differ per direction); hs = n - n // 2
+# covers every instantiated half size (1, 2, 3, 5, 7 tiles of 8), odd and even n, one size past
+# the folded range (dense fallback), contiguous-mode tiles with an odd element count (n odd, odd
+# row count in the last tile), and strided modes whose HBM parity flips at a slab boundary (n even,
+# inner extent odd)
 SHAPES = [(1, 2, 30, 10), (2, 3, 40, 6), (3, 1, 6, 4), (3, 2, 13, 6), (3, 3, 20, 8), (3, 2, 64, 4),
-          (3, 3, 96, 2), (2, 2, 120, 4)]
+          (3, 3, 96, 2), (2, 2, 120, 4), (1, 2, 31, 4), (2, 2, 11, 4), (2, 3, (20, 13), 5),
+          (3, 2, (11, 14, 9), 3)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -41,11 +45,12 @@ def test_folded_transforms_match_dense(shape):
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200 import _lib
     d, p, ne, ne_t = shape
-    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(d)], mb.SplineSpace.uniform(p, ne_t))
+    ne = (ne,) * d if np.isscalar(ne) else ne
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, e) for e in ne], mb.SplineSpace.uniform(p, ne_t))
     Pf, Pd = _pc(st, True), _pc(st, False)
-    n = ne + p
-    hs = n - n // 2
     for l in range(d):
+        n = ne[l] + p
+        hs = n - n // 2
         assert _lib.load().mi_pc_fold(Pf.ctx.handle, l) == hs   # past 56 the launch falls back to dense
         assert _lib.load().mi_pc_fold(Pd.ctx.handle, l) == 0
     r = np.random.default_rng(3).uniform(-1, 1, Pf.shape[0])
