@@ -20,6 +20,10 @@
 
 #include <type_traits>
 
+#ifndef MI_RX_NOCW
+#define MI_RX_NOCW 0   // timing ablation only (wrong results): the stored mode skips its coefficient reads
+#endif
+
 namespace mi {
 
 struct RxArgs {
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
       btp = tid < QT * PW ? bv : bv * __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
     }
   };
-  // x-projection outputs of this thread: line 8 warp + fr, j1 = 2 fk + e (old y prefetched a phase early)
+  // x-projection outputs of this thread: line 8 warp + fr, j1 = 2 fk + e
   const int xline = 8 * warp + fr;
   long long yidx[2];
 #pragma unroll
@@ -215,7 +219,6 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     if (xline < NLX) gs = spatial(D >= 2 ? xline / L2 : 0, D >= 2 ? xline % L2 : 0, 2 * fk + e, ok);
     yidx[e] = ok ? gs : -1;
   }
-  double yold[2] = {0.0, 0.0};
   auto yrow = [&](int ft) -> long long {           // row offset of time function ft, -1 if constrained / foreign
     const int ct = ft + r.rowoff;
     return (ct >= 0 && ct < r.ntc) ? (long long)ct * ns : -1;
@@ -241,8 +244,10 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
       for (int ks = 0; ks < KP; ++ks) dmma(c0, c1, xb[xline * Q1 + 4 * ks + fk], bP[0][ks]);
       const long long row = yrow(ft);
       if (row >= 0) {
-        if (yidx[0] >= 0) r.y[row + yidx[0]] = yold[0] + c0;
-        if (yidx[1] >= 0) r.y[row + yidx[1]] = yold[1] + c1;
+        // fire-and-forget reduction (no old-y round trip): within one colour launch every y entry has
+        // exactly one writer, and the launches are stream-ordered, so the sums stay deterministic
+        if (yidx[0] >= 0) atomicAdd(r.y + row + yidx[0], c0);
+        if (yidx[1] >= 0) atomicAdd(r.y + row + yidx[1], c1);
       }
     }
   };
@@ -270,13 +275,6 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
         if (tid + NTH * m < NIN) sIn[tid + NTH * m] = pre[m];
     }
     if (tid < NBT) sBt[(j & 1) * 32 + tid] = btp;
-    if constexpr (D >= 2) {
-      if (has_fp) {
-        const long long row = yrow(fp);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) yold[e] = (row >= 0 && yidx[e] >= 0) ? r.y[row + yidx[e]] : 0.0;
-      }
-    }
     __syncthreads();                                 // B1
     if (j + 1 < nfull) prefetch(j + 1);
     prefetch_bt(et + 1);
@@ -287,7 +285,8 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) cwp[g][mi][e] = cw_valid(mi, e) ? __ldcs(r.cw + cw_index(et, g, mi, e)) : 0.0;
+            for (int e = 0; e < 2; ++e)
+              cwp[g][mi][e] = MI_RX_NOCW ? 1.0 : (cw_valid(mi, e) ? __ldcs(r.cw + cw_index(et, g, mi, e)) : 0.0);
       }
     }
     const double* fin = sIn;
@@ -434,8 +433,8 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
           if constexpr (D == 1) {
             const long long row = yrow(et);
             if (row >= 0) {
-              if (yidx[0] >= 0) r.y[row + yidx[0]] += c0;
-              if (yidx[1] >= 0) r.y[row + yidx[1]] += c1;
+              if (yidx[0] >= 0) atomicAdd(r.y + row + yidx[0], c0);
+              if (yidx[1] >= 0) atomicAdd(r.y + row + yidx[1], c1);
             }
           } else {
             if (n0 < L) sC[n0 * QL + line] = c0;

@@ -19,6 +19,13 @@
 #include "ptx.cuh"
 #include <cuda.h>
 
+#ifndef MI_STEN_B1
+#define MI_STEN_B1 1
+#endif
+#ifndef MI_STEN_B2
+#define MI_STEN_B2 4
+#endif
+
 namespace mi {
 
 template <int D, int P>
@@ -29,12 +36,14 @@ struct DmmaSten {
   // a k-step's 4 points span at most one stencil-row boundary (W >= 4 for p >= 2)
   static constexpr int KS = (S + 3) / 4;            // k-steps per point
   static constexpr int KH = (KS + 1) / 2;           // k-steps per warp (2 warps / point)
-  // point block of one CTA: a 2x2x2 cube in 3D.  (A 1x1x6 column has halo rows of exactly the
-  // stencil width, so every k-step reads 4 consecutive halo points and the A loads are bank-conflict
-  // free; it was measured 0.7 ms SLOWER at cfg 4: 33% more blocks, each paying the start-up.)
-  static constexpr int B1 = D == 3 ? 2 : (D == 2 ? 4 : 8);
-  static constexpr int B2 = D == 3 ? 2 : (D == 2 ? 2 : 1);
-  static constexpr int B3 = D == 3 ? 2 : 1;
+  // point block of one CTA: 1 x 4 x 2 points in 3D.  With B1 = 1 the halo rows are exactly the stencil
+  // width, so k-steps that cross an x-row read consecutive halo points (no shared-memory bank
+  // conflicts; only plane crossings still conflict), with the same 8 points per block as the 2x2x2 cube
+  // it replaced (cfg 4: 38.68 -> 38.27 ms).  (A 1x1x6 column was 0.7 ms SLOWER: 33% more blocks, each
+  // paying the start-up.)
+  static constexpr int B1 = D == 3 ? MI_STEN_B1 : (D == 2 ? 4 : 8);
+  static constexpr int B2 = D == 3 ? MI_STEN_B2 : (D == 2 ? 2 : 1);
+  static constexpr int B3 = D == 3 ? 8 / (MI_STEN_B1 * MI_STEN_B2) : 1;
   static constexpr int PPB = B1 * B2 * B3;          // points per block
   static constexpr int H1 = B1 + 2 * P;
   static constexpr int H2 = D >= 2 ? B2 + 2 * P : 1;
