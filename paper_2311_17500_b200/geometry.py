@@ -45,13 +45,15 @@ class GeometryMap:
         self._grid = cp.reshape(tuple(s.dimension for s in reversed(self.spaces)) + (self.dim,))
 
     def grid_data(self, axes, order=1, device=None):
-        """x (grid + (d,)) and, for order >= 1, jac (grid + (d, d)) with jac[..., c, a] = dF_c/deta_a;
-        grid axes in C order (direction d first), like geometry.py:135-186.  With a CUDA ``device``
+        """x (grid + (d,)) and, for order >= 1, jac (grid + (d, d)) with jac[..., c, a] = dF_c/deta_a,
+        for order 2 (host only) hess (grid + (d, d, d)); grid axes in C order (direction d first),
+        like geometry.py:135-186.  With a CUDA ``device``
         the tensor contractions run there and torch tensors are returned."""
-        if order > 1:
-            raise NotImplementedError("Hessians are not needed on the device path")
+        if order > 2 or (order == 2 and device is not None):
+            raise NotImplementedError("Hessians are evaluated on the host only (residual indicator)")
         d = self.dim
-        tabs = [[basis_table(s, np.asarray(ax, float), o) for o in range(order + 1)]
+        tabs = [[basis_table(s, np.asarray(ax, float), o) if o <= s.degree else
+                 np.zeros((np.asarray(ax).size, s.dimension)) for o in range(order + 1)]
                 for s, ax in zip(self.spaces, axes)]
         if device is not None:
             import torch
@@ -85,6 +87,16 @@ class GeometryMap:
                 orders[a] = 1
                 jac[..., a] = tabulate(orders)
             out["jac"] = jac
+        if order >= 2:
+            # hess[..., a, b, c] = d^2 F_c / deta_a deta_b (geometry.py:176-184)
+            hess = np.empty(out["x"].shape[:-1] + (d, d, d))
+            for a in range(d):
+                for b in range(a, d):
+                    orders = [0] * d
+                    orders[a] += 1
+                    orders[b] += 1
+                    hess[..., a, b, :] = hess[..., b, a, :] = tabulate(orders)
+            out["hess"] = hess
         return out
 
 

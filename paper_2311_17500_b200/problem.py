@@ -372,25 +372,55 @@ def window_elements(space, i):
     return first, last + 1
 
 
+def _mapped_laplacian(problem, g, u):
+    """D times the physical Laplacian of u at the Gauss grid of a mapped geometry, pulled back with
+    the inverse Jacobian and the map's Hessians (stabilization.py:273-295):
+    lap = sum_ab (J^-1 J^-T)_ab (d_ab u - sum_c H_abc g_c), g_c = sum_i (J^-1)_ic d_i u."""
+    st, d = problem.space, g.d
+    geo_data = g.mapped.geo.grid_data([r[0] for r in g.mapped.rules], order=2)
+    jinv, hess = g.mapped.jinv, geo_data["hess"]
+    firsts = []
+    for a in range(d):
+        orders = [0] * d
+        orders[a] = 1
+        firsts.append(g.field(u, orders, 0))
+    grad_eta = np.stack(firsts, axis=-1)                        # (Q_t, Q_s..., d)
+    grad_phys = np.einsum("...ic,t...i->t...c", jinv, grad_eta)
+    lap = np.zeros(grad_eta.shape[:-1])
+    for a in range(d):
+        for b in range(d):
+            orders = [0] * d
+            orders[a] += 1
+            orders[b] += 1
+            second = g.field(u, orders, 0) if max(orders) <= min(2, st.spatial[a].degree, st.spatial[b].degree) \
+                else np.zeros_like(lap)
+            corr = np.einsum("...c,t...c->t...", hess[..., a, b, :], grad_phys)
+            metric = np.einsum("...k,...k->...", jinv[..., a, :], jinv[..., b, :])
+            lap += metric[None] * (second - corr)
+    return problem.D * lap
+
+
 def compute_theta(problem, u, w, grid=None):
-    """Residual indicator (stabilization.py:235-339) on a box geometry."""
+    """Residual indicator (stabilization.py:235-339) on a box or (host numpy, map Hessians) a mapped
+    geometry."""
     st = problem.space
     g = grid if grid is not None else GaussGrid(st, problem.geometry)
-    if g.mapped is not None:
-        raise NotImplementedError("the residual indicator on mapped geometries (map Hessians) is not built")
     d, T = g.d, g.T
     zero = [0] * d
     u_val = g.field(u, zero, 0)
     u_dtau = g.field(u, zero, 1)
     w_val = g.field(w, zero, 0)
-    lap = np.zeros_like(u_val)
-    Dv = problem.diffusion()
-    for a in range(d):
-        if st.spatial[a].degree < 2:
-            continue
-        orders = [0] * d
-        orders[a] = 2
-        lap += (Dv[a] / g.L[a] ** 2) * g.field(u, orders, 0)   # affine: metric diag(1/L^2), no Hessian term
+    if g.mapped is not None:
+        lap = _mapped_laplacian(problem, g, u)
+    else:
+        lap = np.zeros_like(u_val)
+        Dv = problem.diffusion()
+        for a in range(d):
+            if st.spatial[a].degree < 2:
+                continue
+            orders = [0] * d
+            orders[a] = 2
+            lap += (Dv[a] / g.L[a] ** 2) * g.field(u, orders, 0)   # affine: metric diag(1/L^2), no Hessian term
     res = (problem.C_m * (u_dtau / T) - lap
            + problem.c1 * u_val * (u_val - problem.a) * (u_val - 1.0) + problem.c2 * u_val * w_val)
     if problem.source is not None:

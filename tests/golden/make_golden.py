@@ -277,3 +277,55 @@ def mapped_cases():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "mapped":
     mapped_cases()
+
+
+def mapped_su_cases():
+    """Spline Upwind on mapped geometries (the reference's own SU-vs-Galerkin setting, acceptance
+    criterion 7, is the ellipse annulus): the residual indicator with the mapped Laplacian (map
+    Hessians), the SU Kronecker terms (SpatialQuadratureData on cells split at the spatial Greville
+    abscissae, p+2 points, |det J|-weighted), the operator with them, and a full SU fixed-point
+    solve."""
+    from monoiga.solver import fixed_point_solve
+    from monoiga.stabilization import compute_theta
+    out = {}
+    geos = {"annulus": builtin_geometry("ellipse_annulus", final_time=1.0), "warped": warped_cube_geometry()}
+    cases = [("s2d", "annulus", 2, (8, 3), 4, 1e-3, 51), ("s2d_p3", "annulus", 3, (6, 4), 5, 1e-3, 52),
+             ("s3d_p2", "warped", 2, (3, 3, 4), 3, 1e-2, 53), ("s3d_p3", "warped", 3, (2, 2, 3), 3, 1e-2, 54)]
+    for name, gkey, p, nes, ne_t, D, seed in cases:
+        rng = np.random.default_rng(seed)
+        geo = geos[gkey]
+        st = SpaceTimeSpace([SplineSpace.uniform(p, n) for n in nes], SplineSpace.uniform(p, ne_t))
+        N, nt, ns = st.num_dof, st.num_time, st.num_space
+        u = rng.uniform(0, 1, N)
+        w = rng.uniform(0, 0.1, N)
+        x = rng.uniform(-1, 1, N)
+        prob = MonodomainProblem(geo, st, source=smooth_source, D=D)
+        ind = compute_theta(prob, u, w)
+        tau = compute_tau(st.time)
+        # the operator from a random indicator (rank > 1 at tol 0.3)
+        thr = rng.random((nt, ns))
+        ind_r = ResidualIndicator(thr, st.time_greville(), [s.greville() for s in st.spatial], st.spatial_shape)
+        lr = lowrank_factorize(ind_r, 0.3)
+        stab = assemble_stabilization(tau, lr, st, geo, 1.0)
+        sd = SpatialQuadratureData(st.spatial, geo)
+        M_s, K_s = sd.mass(), sd.stiffness()
+        W_t, M_t = time_matrices(st, 1.0)
+        react = RM["a"] * RM["c1"]
+        op = KroneckerOperator(nt, ns, [(1.0, W_t, M_s), (D, M_t, K_s), (react, M_t, M_s)] + stab.terms())
+        rec = {"geo": gkey, "p": p, "ne": np.array(nes), "ne_t": ne_t, "D": D, "u": u, "w": w, "x": x,
+               "theta": ind.values, "theta_r": thr, "su_rank": lr.rank, "y": op.matvec(x)}
+        for r in range(lr.rank):
+            rec["ss%d" % r] = stab.space_mats[r].toarray()
+        out.update({name + "_" + k: v for k, v in rec.items()})
+        print(name, "N=%d R=%d theta max %.3f" % (N, lr.rank, ind.values.max()))
+    st = SpaceTimeSpace([SplineSpace.uniform(2, 8), SplineSpace.uniform(2, 3)], SplineSpace.uniform(2, 8))
+    prob = MonodomainProblem(geos["annulus"], st, source=smooth_source, D=1e-3)
+    res = fixed_point_solve(prob, FixedPointConfig(stabilization="spline_upwind", linear_solver="iterative"))
+    out.update(fp_u=res.u, fp_w=res.w, fp_it=res.iterations, fp_gm=np.array(res.gmres_iterations),
+               fp_pcg=np.array(res.pcg_iterations), fp_inc=np.array(res.increments))
+    print("fp SU annulus sweeps", res.iterations, "gmres", res.gmres_iterations, "pcg", res.pcg_iterations[:6])
+    np.savez_compressed(os.path.join(HERE, "mapped_su.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "mapped_su":
+    mapped_su_cases()
