@@ -90,6 +90,14 @@ int mi_op_set_su_channel(mi_ctx* ctx, int c, const double* theta, const double* 
  * q[l] Gauss points per element, Q[l] in total (direction 1 first). */
 int mi_op_set_quad_channel(mi_ctx* ctx, int c, int nterms, const double* coef, const double* theta,
                            const double* T, const int* q, const int* Q);
+/* The same with an explicit window per basis function (the Spline Upwind
+ * factors on mapped geometries, stabilization.py:469-488, integrate on cells
+ * split at the spatial Greville abscissae with p+2 points, so the number of
+ * Gauss points per element varies): function i of direction l covers the
+ * Gauss points kstart[l][i] .. kstart[l][i] + kw[l] - 1 of that direction
+ * (kstart: host d x nmax ints), and T's last index is relative to kstart. */
+int mi_op_set_quad_channel_k(mi_ctx* ctx, int c, int nterms, const double* coef, const double* theta,
+                             const double* T, const int* kstart, const int* kw, const int* Q);
 /* Device-to-device copy of channel c's stencil ((2p+1)^d x N_s, point
  * fastest) in / out: a caller reuses generated spatial factors across
  * operator rebuilds (the reference keeps M_s, K_s in its _Workspace,

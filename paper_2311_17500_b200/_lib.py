@@ -36,6 +36,7 @@ _SIGS = {
     "mi_op_set_reaction_weight": ([_vp, _vp], _c_int),
     "mi_op_set_reaction_store": ([_vp, _c_int], _c_int),
     "mi_op_set_quad_channel": ([_vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp], _c_int),
+    "mi_op_set_quad_channel_k": ([_vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_set_channel_stencil": ([_vp, _c_int, _vp], _c_int),
     "mi_op_get_channel_stencil": ([_vp, _c_int, _vp], _c_int),
     "mi_op_set_reaction_rows": ([_vp, _c_int], _c_int),

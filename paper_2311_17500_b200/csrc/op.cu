@@ -140,6 +140,10 @@ struct QuadSpec {
   int q[3], Q[3];       // Gauss points per element / in total, per direction (1 beyond d)
   int kw;               // window length (max over directions) = row stride of the T tables
   long long nq;         // Q_1 Q_2 Q_3
+  int kwl[3];           // window length per direction
+  const int* kst;       // device [3][nmax]: first Gauss point of function i's window (null: (i - p) q)
+  int nmax;
+  __device__ int k0(int l, int i, int P) const { return kst ? kst[l * nmax + i] : (i - P) * q[l]; }
 };
 
 template <int D, int P>
@@ -164,8 +168,9 @@ __global__ void build_quad_channel(double* __restrict__ out, const double* __res
   }
   double v = 0.0;
   if (inside) {
-    const int kw1 = (P + 1) * qs.q[0];
-    const int kw2 = D >= 2 ? (P + 1) * qs.q[1] : 1, kw3 = D >= 3 ? (P + 1) * qs.q[2] : 1;
+    const int kw1 = qs.kwl[0];
+    const int kw2 = D >= 2 ? qs.kwl[1] : 1, kw3 = D >= 3 ? qs.kwl[2] : 1;
+    const int s1 = qs.k0(0, i1, P), s2 = D >= 2 ? qs.k0(1, i2, P) : 0, s3 = D >= 3 ? qs.k0(2, i3, P) : 0;
     for (int t = 0; t < nterms; ++t) {
       const double* th = theta + (long long)t * qs.nq;
       const double* h[3];
@@ -173,19 +178,19 @@ __global__ void build_quad_channel(double* __restrict__ out, const double* __res
       for (int l = 0; l < D; ++l) h[l] = T + ((((long long)t * D + l) * nmax + ii[l]) * W + aa[l]) * qs.kw;
       double vt = 0.0;
       for (int b3 = 0; b3 < kw3; ++b3) {
-        const int k3 = D >= 3 ? (i3 - P) * qs.q[2] + b3 : 0;
+        const int k3 = D >= 3 ? s3 + b3 : 0;
         if (k3 < 0 || k3 >= qs.Q[2]) continue;
         const double h3 = D >= 3 ? h[2][b3] : 1.0;
         if (h3 == 0.0) continue;
         for (int b2 = 0; b2 < kw2; ++b2) {
-          const int k2 = D >= 2 ? (i2 - P) * qs.q[1] + b2 : 0;
+          const int k2 = D >= 2 ? s2 + b2 : 0;
           if (k2 < 0 || k2 >= qs.Q[1]) continue;
           const double h23 = h3 * (D >= 2 ? h[1][b2] : 1.0);
           if (h23 == 0.0) continue;
           const double* tr = th + ((long long)k3 * qs.Q[1] + k2) * qs.Q[0];
           double acc = 0.0;
           for (int b1 = 0; b1 < kw1; ++b1) {
-            const int k1 = (i1 - P) * qs.q[0] + b1;
+            const int k1 = s1 + b1;
             if (k1 < 0 || k1 >= qs.Q[0]) continue;
             acc += tr[k1] * h[0][b1];
           }
@@ -217,8 +222,8 @@ __global__ void __launch_bounds__(256) build_quad_channel_sf(double* __restrict_
   const int tid = threadIdx.x;
   const int i1 = (int)(i % g.n1), i2 = (int)((i / g.n1) % g.n2), i3 = (int)(i / ((long long)g.n1 * g.n2)) + g.z_lo;
   const int ii[3] = {i1, i2, i3};
-  const int k0[3] = {(i1 - P) * qs.q[0], (i2 - P) * qs.q[1], (i3 - P) * qs.q[2]};
-  const int kw[3] = {(P + 1) * qs.q[0], (P + 1) * qs.q[1], (P + 1) * qs.q[2]};
+  const int k0[3] = {qs.k0(0, i1, P), qs.k0(1, i2, P), qs.k0(2, i3, P)};
+  const int kw[3] = {qs.kwl[0], qs.kwl[1], qs.kwl[2]};
   double acc[(S + 255) / 256];
 #pragma unroll
   for (int r = 0; r < (S + 255) / 256; ++r) acc[r] = 0.0;
@@ -443,19 +448,21 @@ int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H
   return MI_OK;
 }
 
-int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta,
-                           const double* T, const int* q, const int* Q) {
+static int quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta, const double* T,
+                        const int* q, const int* kstart, const int* kwin, const int* Q) {
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
-  MI_REQUIRE(nterms >= 1 && coef && theta && T && q && Q, MI_ERR_ARG, "bad quadrature channel arguments");
+  MI_REQUIRE(nterms >= 1 && coef && theta && T && Q && (q || (kstart && kwin)), MI_ERR_ARG,
+             "bad quadrature channel arguments");
   QuadSpec qs{};
   qs.nq = 1;
   int kw = 1;
   for (int l = 0; l < 3; ++l) {
-    qs.q[l] = l < c->d ? q[l] : 1;
+    qs.q[l] = l < c->d && q ? q[l] : 1;
     qs.Q[l] = l < c->d ? Q[l] : 1;
-    MI_REQUIRE(qs.q[l] >= 1 && qs.Q[l] >= 1, MI_ERR_ARG, "quadrature sizes must be positive");
-    if (l < c->d) kw = max(kw, (c->p + 1) * qs.q[l]);
+    qs.kwl[l] = l < c->d ? (q ? (c->p + 1) * q[l] : kwin[l]) : 1;
+    MI_REQUIRE(qs.q[l] >= 1 && qs.Q[l] >= 1 && qs.kwl[l] >= 1, MI_ERR_ARG, "quadrature sizes must be positive");
+    kw = max(kw, qs.kwl[l]);
     qs.nq *= qs.Q[l];
   }
   qs.kw = kw;
@@ -464,17 +471,28 @@ int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
   DeviceBuf dc, dth, dT;
   int rc;
   if ((rc = dalloc(dc, nterms)) || (rc = dalloc(dth, (size_t)nterms * qs.nq)) || (rc = dalloc(dT, nT))) return rc;
+  qs.nmax = nmax;
+  int* dks = nullptr;
+  if (kstart) {
+    std::vector<int> ks((size_t)3 * nmax, 0);
+    for (int l = 0; l < c->d; ++l)
+      for (int i = 0; i < nmax; ++i) ks[(size_t)l * nmax + i] = kstart[(size_t)l * nmax + i];
+    MI_CUDA(cudaMalloc(&dks, sizeof(int) * ks.size()));
+    MI_CUDA(cudaMemcpyAsync(dks, ks.data(), sizeof(int) * ks.size(), cudaMemcpyHostToDevice, c->stream));
+    qs.kst = dks;
+  }
   // host or device arrays (unified addressing picks the copy direction)
   MI_CUDA(cudaMemcpyAsync(dc.p, coef, sizeof(double) * nterms, cudaMemcpyDefault, c->stream));
   MI_CUDA(cudaMemcpyAsync(dth.p, theta, sizeof(double) * nterms * qs.nq, cudaMemcpyDefault, c->stream));
   MI_CUDA(cudaMemcpyAsync(dT.p, T, sizeof(double) * nT, cudaMemcpyDefault, c->stream));
   Dims g = dims_of(c);
   double* out = c->stencil.p + (size_t)ch * c->nsten * c->ns;
-  const bool sf = c->d == 3 && ((c->p == 3 && kw <= 16) || (c->p == 2 && kw <= 9) || (c->p == 1 && kw <= 4));
+  const bool sf = c->d == 3 && ((c->p == 3 && kw <= 25) || (c->p == 2 && kw <= 24) || (c->p == 1 && kw <= 6));
   if (sf) {
-    // sum-factorised generator (d = 3, q = p + 1)
+    // sum-factorised generator (d = 3): q = p + 1 windows, or the refined (Greville-split, p + 2 point)
+    // rules of the mapped Spline Upwind factors
 #define MI_QSF(PV, KWV)                                                                                   \
-  if (c->p == PV) {                                                                                     \
+  if (c->p == PV && kw <= KWV) {                                                                        \
     constexpr int Wv = 2 * PV + 1;                                                                      \
     constexpr size_t sm = (size_t)(KWV * KWV * KWV + KWV * KWV * Wv + KWV * Wv * Wv + 3 * Wv * KWV) * 8; \
     MI_CUDA(cudaFuncSetAttribute(build_quad_channel_sf<PV, KWV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -482,7 +500,7 @@ int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
     build_quad_channel_sf<PV, KWV><<<(unsigned)c->ns, 256, sm, c->stream>>>(out, dc.p, dth.p, dT.p, nterms, nmax, \
                                                                             qs, g);                     \
   }
-    MI_QSF(3, 16) MI_QSF(2, 9) MI_QSF(1, 4)
+    MI_QSF(3, 16) else MI_QSF(3, 25) else MI_QSF(2, 9) else MI_QSF(2, 24) else MI_QSF(1, 4) else MI_QSF(1, 6)
 #undef MI_QSF
   } else {
     dim3 grid((unsigned)((c->ns + 127) / 128), c->nsten);
@@ -495,7 +513,18 @@ int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
   dfree(dc);
   dfree(dth);
   dfree(dT);
+  if (dks) cudaFree(dks);
   return MI_OK;
+}
+
+int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta,
+                           const double* T, const int* q, const int* Q) {
+  return quad_channel(c, ch, nterms, coef, theta, T, q, nullptr, nullptr, Q);
+}
+
+int mi_op_set_quad_channel_k(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta,
+                             const double* T, const int* kstart, const int* kw, const int* Q) {
+  return quad_channel(c, ch, nterms, coef, theta, T, nullptr, kstart, kw, Q);
 }
 
 int mi_op_set_channel_stencil(mi_ctx* c, int ch, const double* sten) {

@@ -35,13 +35,16 @@ class _Workspace:
             raise NotImplementedError("the direct (host LU) linear solver is not part of the device path")
         # mapped geometries: quadrature M_s / K_s, |det J| reaction, separable-weight P^-1 (solver.py:167-202)
         self.sd = MappedSpatialData(st.spatial, problem.geometry) if is_mapped(problem.geometry) else None
-        if self.sd is not None and config.stabilization == "spline_upwind":
-            raise NotImplementedError("Spline Upwind on mapped geometries is not built (the residual indicator "
-                                      "needs the map's Hessians)")
         self.L = None if self.sd is not None else box_of(problem.geometry)[0]
         self.device = device
-        self.indicator = DeviceIndicator(problem, device) if config.stabilization == "spline_upwind" else None
-        if self.indicator is not None and problem.source is not None:
+        self.indicator = None
+        if config.stabilization == "spline_upwind":
+            self.indicator = (DeviceIndicator(problem, device) if self.sd is None else
+                              MappedIndicator(problem, GaussGrid(st, problem.geometry, mapped=self.sd)))
+        if self.indicator is not None and self.sd is not None:
+            self.grid = self.indicator.grid
+            self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid, device=device)
+        elif self.indicator is not None and problem.source is not None:
             # one host evaluation of the source feeds both the load vector and the indicator's
             # device-resident copy
             self.grid = self.indicator._grid = GaussGrid(st, problem.geometry, mapped=self.sd)
@@ -68,6 +71,20 @@ class _Workspace:
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
                                  problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
                                  lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd)
+
+
+class MappedIndicator:
+    """Residual indicator on a mapped geometry: problem.compute_theta with the pulled-back Laplacian
+    (map Hessians, stabilization.py:273-295), host numpy on the Gauss grid (the device indicator
+    kernel, csrc/theta.cu, covers boxes)."""
+
+    def __init__(self, problem, grid):
+        self.problem, self.grid = problem, grid
+
+    def compute(self, u, w, on_device=True):
+        from .problem import compute_theta
+        host = [v.cpu().numpy() if torch.is_tensor(v) else np.asarray(v, float) for v in (u, w)]
+        return compute_theta(self.problem, host[0], host[1], grid=self.grid)
 
 
 def _host_indicator(ind):
@@ -117,9 +134,15 @@ def fixed_point_solve(problem, config=None, device=0):
         if config.indicator_override is not None:
             frozen_indicator = config.indicator_override(problem, pre.u, pre.w)
         else:
-            frozen_indicator = DeviceIndicator(problem, device).compute(pre.u, pre.w)
+            from .geometry import is_mapped
+            if is_mapped(problem.geometry):
+                from .problem import compute_theta
+                frozen_indicator = compute_theta(problem, pre.u, pre.w)
+            else:
+                frozen_indicator = DeviceIndicator(problem, device).compute(pre.u, pre.w)
+        from .geometry import is_mapped
         frozen_stab = Stabilization(st, _indicator_values(frozen_indicator), config.lowrank_tol, problem.C_m,
-                                    lengths=box_of(problem.geometry)[0])
+                                    lengths=None if is_mapped(problem.geometry) else box_of(problem.geometry)[0])
 
     ph.start()
     ws = _Workspace(problem, config, device)

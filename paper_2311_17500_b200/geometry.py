@@ -57,7 +57,7 @@ class GeometryMap:
                 for s, ax in zip(self.spaces, axes)]
         if device is not None:
             import torch
-            tabs = [[torch.from_numpy(t).to(device) for t in tl] for tl in tabs]
+            tabs = [[torch.from_numpy(np.array(t)).to(device) for t in tl] for tl in tabs]
             grid0 = torch.from_numpy(np.ascontiguousarray(self._grid)).to(device)
 
             def tabulate(orders):
@@ -312,3 +312,80 @@ def prolate_shell_geometry(final_time=1.0, radii=(1.0, 1.0, 2.0), thickness=0.2,
     geo = interpolate_map(spaces, shell)
     geo.final_time = float(final_time)
     return geo
+
+
+class MappedSUData:
+    """Quadrature data of the Spline Upwind spatial factors S^s_r on a mapped geometry
+    (assemble_stabilization, stabilization.py:469-488: SpatialQuadratureData with p+2 Gauss points on
+    cells split at the spatial Greville abscissae, assembly.py:137-203, weight w |det J| times the
+    multilinear profile theta_r of LowRankIndicator.space_profile, stabilization.py:383-398).
+
+    The refined rule has a variable number of Gauss points per element, so every basis function i
+    of direction l gets an explicit window kst[l][i] .. kst[l][i] + kw[l] - 1 of that direction's
+    points (mi_op_set_quad_channel_k)."""
+
+    def __init__(self, spatial_spaces, geometry, device="auto"):
+        from .factors import hat_values
+        from .spaces import cells_with, greville
+        self.spaces = tuple(spatial_spaces)
+        d = len(self.spaces)
+        self.grev = [greville(s) for s in self.spaces]
+        self.rules = [gauss_rule(cells_with(s, g), s.degree + 2) for s, g in zip(self.spaces, self.grev)]
+        axes = [r[0] for r in self.rules]
+        if device == "auto":
+            import torch
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        if device is not None:
+            import torch
+            jac = geometry.grid_data(axes, order=1, device=device)["jac"]
+            det = torch.linalg.det(jac).abs().cpu().numpy()
+            del jac
+        else:
+            det = np.abs(np.linalg.det(geometry.grid_data(axes, order=1)["jac"]))
+        w = np.ones(())
+        for l in reversed(range(d)):
+            w = np.multiply.outer(w, self.rules[l][1])
+        self.measure = w * det                              # (Q_d, ..., Q_1)
+        self.Q = [r[0].size for r in self.rules]
+        self.kst, self.kend = [], []
+        for s, (x, _) in zip(self.spaces, self.rules):
+            p, u = s.degree, np.asarray(s.knots, float)
+            i = np.arange(s.dimension)
+            self.kst.append(np.searchsorted(x, u[i]).astype(np.int32))
+            self.kend.append(np.searchsorted(x, u[i + p + 1]).astype(np.int32))
+        self.kw = [int(np.max(b - a)) for a, b in zip(self.kst, self.kend)]
+        self.hats = [hat_values(g, x) for g, (x, _) in zip(self.grev, self.rules)]
+
+    def tables(self, p, nmax):
+        """T[0, l, i, a, b] = B_i(x_k) B_j(x_k), j = i + a - p, k = kst[l][i] + b (one mass term)."""
+        d = len(self.spaces)
+        kw = max(self.kw)
+        T = np.zeros((1, d, nmax, 2 * p + 1, kw))
+        for l, s in enumerate(self.spaces):
+            n, x = s.dimension, self.rules[l][0]
+            B = basis_table(s, x, 0)
+            i = np.arange(n)[:, None, None]
+            a = np.arange(2 * p + 1)[None, :, None]
+            b = np.arange(kw)[None, None, :]
+            j = i + a - p
+            k = self.kst[l][:, None, None] + b
+            ok = (j >= 0) & (j < n) & (k < self.kend[l][:, None, None])
+            jj, kk = np.where(ok, j, 0), np.where(ok, k, 0)
+            T[0, l, :n] = np.where(ok, B[kk, np.broadcast_to(i, ok.shape)] * B[kk, jj], 0.0)
+        return np.ascontiguousarray(T)
+
+    def kstart(self, nmax):
+        ks = np.zeros((len(self.spaces), nmax), dtype=np.int32)
+        for l, k in enumerate(self.kst):
+            ks[l, :k.size] = k
+        return ks
+
+    def weight(self, theta_r):
+        """w |det J| times the multilinear interpolant of theta_r (flat N_s, direction 1 fastest) on
+        the Greville grid, at the refined Gauss grid (C order, direction d first)."""
+        d = len(self.spaces)
+        prof = np.asarray(theta_r, float).reshape(tuple(s.dimension for s in reversed(self.spaces)))
+        for l in range(d):
+            ax = d - 1 - l
+            prof = np.moveaxis(np.tensordot(self.hats[l], prof, axes=(1, ax)), 0, ax)
+        return self.measure * prof

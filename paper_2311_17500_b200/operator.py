@@ -83,8 +83,6 @@ class KroneckerOperator:
         if sd is not None:
             if z_planes is not None or time_rows is not None:
                 raise NotImplementedError("mapped geometries are not sharded")
-            if stabilization is not None and stabilization.rank:
-                raise NotImplementedError("Spline Upwind on mapped geometries is not built")
             if np.atleast_1d(np.asarray(diffusion, float)).size != 1:
                 raise ValueError("mapped geometries take a scalar diffusion (the reference's D)")
         st = space_time
@@ -166,7 +164,19 @@ class KroneckerOperator:
             c1 = np.asarray(coefs, float)
             b1 = pack(rows)
             _lib.call("mi_op_set_kron_channel", ctx.handle, 1, len(rows), host_ptr(c1), host_ptr(b1))
-        for r in range(R):
+        if R and sd is not None:
+            # mapped geometry: S^s_r by quadrature on the Greville-split rule, weight w |det J| theta_r
+            su = mapped_su_data(sd)
+            T = su.tables(p, nmax)
+            ks = np.ascontiguousarray(su.kstart(nmax))
+            kw = np.asarray(su.kw, dtype=np.int32)
+            Qh = np.asarray(su.Q, dtype=np.int32)
+            one = np.ones(1)
+            for r in range(R):
+                wr = np.ascontiguousarray(su.weight(stab.theta[r]))
+                _lib.call("mi_op_set_quad_channel_k", ctx.handle, 2 + r, 1, host_ptr(one), host_ptr(wr), host_ptr(T),
+                          host_ptr(ks), host_ptr(kw), host_ptr(Qh))
+        for r in range(R if sd is None else 0):
             th = np.ascontiguousarray(stab.theta[r])
             H = np.ascontiguousarray(stab.H)
             _lib.call("mi_op_set_su_channel", ctx.handle, 2 + r, host_ptr(th), host_ptr(H), stab.ko)
@@ -204,6 +214,15 @@ class KroneckerOperator:
         return yd.cpu().numpy()
 
     __call__ = matvec
+
+
+def mapped_su_data(sd):
+    """geometry.MappedSUData of a MappedSpatialData's spaces and map, built once and cached on it."""
+    from .geometry import MappedSUData
+    cache = sd.__dict__
+    if "_su" not in cache:
+        cache["_su"] = MappedSUData(sd.spaces, sd.geo)
+    return cache["_su"]
 
 
 def mapped_stencils(ctx, sd):
