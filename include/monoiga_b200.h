@@ -231,6 +231,16 @@ int mi_theta_setup(mi_ctx* ctx, const int* nel, const double* B0, const double* 
 int mi_theta_elements(mi_ctx* ctx, const double* u, const double* w, const double* src, int et0, int et1,
                       double* emax, double* maxes);
 /* out[o][i][r] = max over e in [w0[i], w1[i]) of in[o][e][r]   (w0, w1 host) */
+/* Mapped geometries: the residual indicator's element maxima from
+ * precomputed Gauss-point fields of time elements [et0, et1)
+ * (stabilization.py:235-295 with the pulled-back Laplacian):
+ * fields = [u, u_tau, w, d_i u (i < d), d_ab u (a = b first, then a < b)]
+ * x rows x G_s, coef = [cg_i, cm_ab] x G_s (see theta.py MappedDeviceIndicator),
+ * src = NULL or f at the same points; G[l] = nel[l] q spatial Gauss points.
+ * emax / maxes as mi_theta_elements. */
+int mi_theta_mapped_elements(mi_ctx* ctx, const double* fields, const double* coef, const double* src, int et0,
+                             int et1, const int* G, int q, int qt, const int* nel, double D, double cmT, double c1,
+                             double a, double c2, double* emax, double* maxes);
 int mi_window_max(mi_ctx* ctx, const double* in, double* out, long long outer, int n_in, int n_out,
                   long long inner, const int* w0, const int* w1);
 /* theta = min(numer / denom, 1)   (denom > 0) */

@@ -61,6 +61,7 @@ _SIGS = {
     "mi_cgs_pass": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp, _vp], _c_int),
     "mi_theta_setup": ([_vp, _vp, _vp, _vp, _vp, _vp, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_dbl], _c_int),
     "mi_theta_elements": ([_vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _vp], _c_int),
+    "mi_theta_mapped_elements": ([_vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _vp, _vp], _c_int),
     "mi_window_max": ([_vp, _vp, _vp, _c_ll, _c_int, _c_int, _c_ll, _vp, _vp], _c_int),
     "mi_theta_ratio": ([_vp, _vp, _vp, _c_ll, _c_dbl], _c_int),
 }

@@ -337,6 +337,51 @@ __global__ void theta_ratio_kernel(const double* __restrict__ numer, double* __r
     theta[i] = fmin(numer[i] / denom, 1.0);
 }
 
+// Mapped geometries (stabilization.py:273-295): the strong residual at the Gauss points of time
+// elements [et0, et1) from precomputed Gauss-point fields (rows = time Gauss points of the chunk,
+// G_s spatial Gauss points per row):
+//   fields[f][row][s], f = u, u_tau, w, d_i u (i < d), d_ab u (aa first, then a < b)
+//   coef[c][s],        c = cg_i (i < d), cm_ab (same order as the second derivatives)
+// with  lap = sum_i cg_i d_i u + sum_ab cm_ab d_ab u  (cm_ab = (J^-1 J^-T)_ab, doubled for a != b;
+// cg_i = -sum_ab (J^-1 J^-T)_ab sum_c H_abc (J^-1)_ic), so
+//   res = C_m u_tau / T - D lap + c1 u (u - a)(u - 1) + c2 u w - f.
+// |res| goes to its element's maximum (bit-pattern atomicMax of non-negative doubles: exact and order
+// independent, as theta_elements), max|u| and max|u_tau| to the denominator maxima.
+__global__ void mapped_residual_kernel(const double* __restrict__ fields, const double* __restrict__ coef,
+                                       const double* __restrict__ src, double* __restrict__ emax,
+                                       unsigned long long* __restrict__ maxes, int d, int rows, long long gs,
+                                       int G1, int G2, int q, int qt, int et0, int E1, int E2, int E3,
+                                       double D, double cmT, double c1, double a, double c2) {
+  const int nd2 = d * (d + 1) / 2;
+  const long long total = (long long)rows * gs;
+  double umax = 0.0, utmax = 0.0;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long sp = idx % gs;
+    const int row = (int)(idx / gs);
+    const double u = fields[idx], ut = fields[total + idx], w = fields[2 * total + idx];
+    double lap = 0.0;
+    for (int i = 0; i < d; ++i) lap = fma(coef[i * gs + sp], fields[(3 + i) * total + idx], lap);
+    for (int k = 0; k < nd2; ++k) lap = fma(coef[(d + k) * gs + sp], fields[(3 + d + k) * total + idx], lap);
+    double res = cmT * ut - D * lap + c1 * u * (u - a) * (u - 1.0) + c2 * u * w;
+    if (src) res -= src[idx];
+    const int g1 = (int)(sp % G1), g2 = (int)((sp / G1) % G2), g3 = (int)(sp / ((long long)G1 * G2));
+    const long long el = (((long long)(et0 + row / qt) * E3 + g3 / q) * E2 + g2 / q) * E1 + g1 / q;
+    atomicMax(reinterpret_cast<unsigned long long*>(emax) + el, dbits(fabs(res)));
+    umax = fmax(umax, fabs(u));
+    utmax = fmax(utmax, fabs(ut));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    utmax = fmax(utmax, __shfl_xor_sync(0xffffffffu, utmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&maxes[0], dbits(umax));
+    atomicMax(&maxes[1], dbits(utmax));
+  }
+}
+
 #define MI_TH_CASE(dv, pv, ptv, ...)                                 \
   case ((dv) * 8 + (pv)) * 8 + (ptv): {                              \
     constexpr int D_ = (dv), P_ = (pv), PT_ = (ptv);                 \
@@ -446,6 +491,31 @@ int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double*
     theta_elements<D_, P_, PT_><<<(unsigned)nb, 256, G::SMEM, c->stream>>>(r);
     MI_CHECK_LAUNCH("theta_elements");
   });
+  return MI_OK;
+}
+
+int mi_theta_mapped_elements(mi_ctx* c, const double* fields, const double* coef, const double* src, int et0,
+                             int et1, const int* G, int q, int qt, const int* nel, double D, double cmT, double c1,
+                             double a, double c2, double* emax, double* maxes) {
+  MI_REQUIRE(c && fields && coef && G && nel && emax && maxes, MI_ERR_ARG, "NULL argument to mi_theta_mapped_elements");
+  MI_REQUIRE(0 <= et0 && et0 <= et1 && q >= 1 && qt >= 1, MI_ERR_ARG, "bad element range or rule");
+  if (et0 == et1) return MI_OK;
+  const int d = c->d;
+  long long gs = 1;
+  int Gl[3] = {1, 1, 1}, El[3] = {1, 1, 1};
+  for (int l = 0; l < d; ++l) {
+    Gl[l] = G[l];
+    El[l] = nel[l];
+    MI_REQUIRE(G[l] == nel[l] * q, MI_ERR_ARG, "Gauss grid does not match the element count");
+    gs *= G[l];
+  }
+  const int rows = (et1 - et0) * qt;
+  const long long total = (long long)rows * gs;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  mapped_residual_kernel<<<grid, 256, 0, c->stream>>>(fields, coef, src, emax,
+                                                     reinterpret_cast<unsigned long long*>(maxes), d, rows, gs,
+                                                     Gl[0], Gl[1], q, qt, et0, El[0], El[1], El[2], D, cmT, c1, a, c2);
+  MI_CHECK_LAUNCH("mapped_residual_kernel");
   return MI_OK;
 }
 

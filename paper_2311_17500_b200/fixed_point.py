@@ -21,7 +21,7 @@ from .krylov import gmres
 from .operator import KroneckerOperator, Stabilization
 from .precond import FastDiagPreconditioner
 from .problem import FixedPointConfig, FixedPointDiverged, GaussGrid, SolveResult, box_of, load_vector
-from .theta import DeviceIndicator
+from .theta import DeviceIndicator, MappedDeviceIndicator
 from .wsolve import RecoverySolver
 
 
@@ -40,9 +40,10 @@ class _Workspace:
         self.indicator = None
         if config.stabilization == "spline_upwind":
             self.indicator = (DeviceIndicator(problem, device) if self.sd is None else
-                              MappedIndicator(problem, GaussGrid(st, problem.geometry, mapped=self.sd)))
+                              MappedDeviceIndicator(problem, device,
+                                                    grid=GaussGrid(st, problem.geometry, mapped=self.sd)))
         if self.indicator is not None and self.sd is not None:
-            self.grid = self.indicator.grid
+            self.grid = self.indicator._grid
             self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid, device=device)
         elif self.indicator is not None and problem.source is not None:
             # one host evaluation of the source feeds both the load vector and the indicator's
@@ -71,20 +72,6 @@ class _Workspace:
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
                                  problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
                                  lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd)
-
-
-class MappedIndicator:
-    """Residual indicator on a mapped geometry: problem.compute_theta with the pulled-back Laplacian
-    (map Hessians, stabilization.py:273-295), host numpy on the Gauss grid (the device indicator
-    kernel, csrc/theta.cu, covers boxes)."""
-
-    def __init__(self, problem, grid):
-        self.problem, self.grid = problem, grid
-
-    def compute(self, u, w, on_device=True):
-        from .problem import compute_theta
-        host = [v.cpu().numpy() if torch.is_tensor(v) else np.asarray(v, float) for v in (u, w)]
-        return compute_theta(self.problem, host[0], host[1], grid=self.grid)
 
 
 def _host_indicator(ind):
@@ -135,11 +122,8 @@ def fixed_point_solve(problem, config=None, device=0):
             frozen_indicator = config.indicator_override(problem, pre.u, pre.w)
         else:
             from .geometry import is_mapped
-            if is_mapped(problem.geometry):
-                from .problem import compute_theta
-                frozen_indicator = compute_theta(problem, pre.u, pre.w)
-            else:
-                frozen_indicator = DeviceIndicator(problem, device).compute(pre.u, pre.w)
+            cls = MappedDeviceIndicator if is_mapped(problem.geometry) else DeviceIndicator
+            frozen_indicator = cls(problem, device).compute(pre.u, pre.w)
         from .geometry import is_mapped
         frozen_stab = Stabilization(st, _indicator_values(frozen_indicator), config.lowrank_tol, problem.C_m,
                                     lengths=None if is_mapped(problem.geometry) else box_of(problem.geometry)[0])

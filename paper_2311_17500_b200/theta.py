@@ -154,6 +154,13 @@ class DeviceIndicator:
             for et0, et1, fd in self._source_chunks(source, nel_t):
                 _lib.call("mi_theta_elements", ctx.handle, dptr(ud), dptr(wd), dptr(fd), et0, et1, dptr(emax),
                           dptr(maxes))
+        return self._finish(emax, maxes, on_device)
+
+    def _finish(self, emax, maxes, on_device):
+        """Window maxima of the element maxima and the clamped ratio (stabilization.py:297-339)."""
+        ctx, st, d = self.ctx, self.st, self.d
+        nel_t = self.nel[d]
+        nes = int(np.prod(self.nel[:d]))
         umax, utmax = (float(v) for v in maxes.cpu().numpy())
         denom = float(self.problem.C_m) * (umax / self.T + utmax / self.T)
         # window maxima: time (over elements -> functions), then x, y, z
@@ -191,3 +198,118 @@ class DeviceIndicator:
 
     def close(self):
         self.ctx.close()
+
+
+class MappedDeviceIndicator(DeviceIndicator):
+    """compute_theta on a mapped geometry (stabilization.py:235-339 with the pulled-back Laplacian,
+    273-295).  Per chunk of time elements the Gauss-point fields u, u_tau, w, the first and second
+    parametric derivatives of u are interpolated by tensor mode products with the 1D basis tables
+    (plain dense GEMMs: cuBLAS through torch.tensordot), then ``mapped_residual_kernel``
+    (csrc/theta.cu) forms the residual with the per-point metric / Hessian coefficients and the
+    Rogers-McCulloch current and reduces it to element maxima; the window maxima and the ratio
+    are the box path's kernels."""
+
+    def __init__(self, problem, device=0, context=None, grid=None, chunk_points=1 << 24, cache_bytes=None):
+        st = problem.space
+        self.problem, self.st, self.d = problem, st, len(st.spatial)
+        self.ctx = context if context is not None else DeviceContext(st, device)
+        self.T = float(problem.final_time)
+        self._grid = grid if grid is not None else GaussGrid(st, problem.geometry)
+        g, d = self._grid, self.d
+        sd = g.mapped
+        if sd is None:
+            raise ValueError("MappedDeviceIndicator needs a mapped geometry")
+        dev = self.ctx.device
+        self.tB = [torch.tensor(np.asarray(t), device=dev) for t in g.tB]
+        self.sB = [[torch.tensor(np.asarray(t), device=dev) for t in tl] for tl in g.sB]
+        # per spatial Gauss point: cg_i = -sum_ab m_ab sum_c H_abc (J^-1)_ic, cm_ab = m_ab (x2 off-diagonal)
+        hess = sd.geo.grid_data([r[0] for r in sd.rules], order=2)["hess"]
+        jinv = sd.jinv
+        metric = np.einsum("...ak,...bk->...ab", jinv, jinv)
+        hj = np.einsum("...abc,...ic->...abi", hess, jinv)
+        coef = [-np.einsum("...ab,...abi->...i", metric, hj)[..., i] for i in range(d)]
+        self.pairs = [(a, a) for a in range(d)] + [(a, b) for a in range(d) for b in range(a + 1, d)]
+        coef += [metric[..., a, b] * (1.0 if a == b else 2.0) for a, b in self.pairs]
+        self.coef = torch.tensor(np.ascontiguousarray(np.stack([c.reshape(-1) for c in coef])), device=dev)
+        self.G = np.asarray([x.size for x in g.sx], dtype=np.int32)
+        self.q = st.spatial[0].degree + 1
+        if any(s.degree + 1 != self.q for s in st.spatial):
+            raise ValueError("mapped residual indicator: equal spatial degrees required")
+        self.nel = [s.breakpoints.size - 1 for s in st.spatial] + [st.time.breakpoints.size - 1]
+        self.chunk_points = int(chunk_points)
+        if cache_bytes is None:
+            cache_bytes = torch.cuda.mem_get_info(dev)[0] // 8
+        self.cache_bytes = int(cache_bytes)
+        self._src_cache = None
+        self.win_t = [window_elements(st.time, c) for c in range(st.num_time)]
+        self.win_s = [[window_elements(s, i) for i in range(s.dimension)] for s in st.spatial]
+
+    def _fields(self, U, W, et0, et1):
+        """(3 + d + d(d+1)/2, rows, G_s) Gauss-point fields of time elements [et0, et1)."""
+        st, d = self.st, self.d
+        qt = st.time.degree + 1
+        r0, r1 = et0 * qt, et1 * qt
+        shape = tuple(s.dimension for s in reversed(st.spatial))
+        memo = {}
+
+        def spatial(X, key, orders):
+            out = X
+            for l in range(d):
+                k = key + tuple(orders[:l + 1])
+                if k not in memo:
+                    o = orders[l]
+                    if o >= len(self.sB[l]):                # derivative order above the degree: zero
+                        memo[k] = None
+                    elif out is None:
+                        memo[k] = None
+                    else:
+                        ax = 1 + (d - 1 - l)
+                        memo[k] = torch.movedim(torch.tensordot(self.sB[l][o], out, dims=([1], [ax])), 0, ax)
+                out = memo[k]
+            return out
+
+        Ut = (self.tB[0][r0:r1] @ U).reshape((r1 - r0,) + shape)
+        Utt = (self.tB[1][r0:r1] @ U).reshape((r1 - r0,) + shape)
+        Wt = (self.tB[0][r0:r1] @ W).reshape((r1 - r0,) + shape)
+        zero = [0] * d
+        outs = [spatial(Ut, ("u",), zero), spatial(Utt, ("ut",), zero), spatial(Wt, ("w",), zero)]
+        for i in range(d):
+            o = [0] * d
+            o[i] = 1
+            outs.append(spatial(Ut, ("u",), o))
+        for a, b in self.pairs:
+            o = [0] * d
+            o[a] += 1
+            o[b] += 1
+            outs.append(spatial(Ut, ("u",), o))
+        ref = outs[0]
+        return torch.stack([v.reshape(r1 - r0, -1) if v is not None else torch.zeros_like(ref).reshape(r1 - r0, -1)
+                            for v in outs]).contiguous()
+
+    def compute(self, u, w, on_device=False):
+        ctx, st, d = self.ctx, self.st, self.d
+        ctx.bind_stream()
+        ud, wd = ctx.to_device(u), ctx.to_device(w)
+        if ud.numel() != ctx.N or wd.numel() != ctx.N:
+            raise ValueError("dimension mismatch: state of size %d for a space of size %d" % (ud.numel(), ctx.N))
+        U, W = ud.view(st.num_time, -1), wd.view(st.num_time, -1)
+        nel_t = self.nel[d]
+        emax = torch.zeros(nel_t * int(np.prod(self.nel[:d])), dtype=torch.float64, device=ctx.device)
+        maxes = torch.zeros(2, dtype=torch.float64, device=ctx.device)
+        qt = st.time.degree + 1
+        nel = np.asarray(self.nel[:d], dtype=np.int32)
+        pr = self.problem
+        source = pr.source
+        if source is not None:
+            chunks = self._source_chunks(source, nel_t)
+        else:
+            step = max(1, self.chunk_points // (qt * int(np.prod(self.G))))
+            chunks = ((e0, min(nel_t, e0 + step), None) for e0 in range(0, nel_t, step))
+        for et0, et1, fd in chunks:
+            F = self._fields(U, W, et0, et1)
+            _lib.call("mi_theta_mapped_elements", ctx.handle, dptr(F), dptr(self.coef),
+                      dptr(fd) if fd is not None else None, int(et0), int(et1), host_ptr(self.G), self.q, qt,
+                      host_ptr(nel), float(pr.D), float(pr.C_m) / self.T, float(pr.c1), float(pr.a), float(pr.c2),
+                      dptr(emax), dptr(maxes))
+            del F
+        return self._finish(emax, maxes, on_device)
