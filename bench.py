@@ -568,7 +568,8 @@ def run_ours(args):
         try:
             line["mapped_cfg5"] = {"geometry": "prolate shell slab, quarter sector (our construction, SURVEY App. B)",
                                    "apply": solve_mapped.apply_rate(64, 256, 3, 5),
-                                   "solve_galerkin": solve_mapped.solve(32, 64, 3, 60)}
+                                   "solve_galerkin": solve_mapped.solve(32, 64, 3, 60),
+                                   "solve_su": solve_mapped.solve(32, 64, 3, 60, "spline_upwind")}
         except Exception as exc:
             line["mapped_cfg5"] = {"error": repr(exc)[:300]}
         torch.cuda.empty_cache()

@@ -3,8 +3,8 @@ our construction: the reference has no such geometry), p = 3.
 
   apply: z = P^-1 (A x) on the mapped geometry (Galerkin terms + zero-iterate reaction; M_s and K_s
          assembled by Gauss quadrature on the device), DoF/s and per-kernel ms;
-  solve: the relaxed fixed-point solve (Galerkin: Spline Upwind on mapped geometries is not built)
-         with S1-S2 source stand-ins (S1 on the phi = 0 face for t < 0.05, S2 on the quadrant
+  solve: the relaxed fixed-point solve (Galerkin, and with --su Spline Upwind: mapped SU stencils and
+         the device mapped residual indicator) with S1-S2 source stand-ins (S1 on the phi = 0 face for t < 0.05, S2 on the quadrant
          x < 0.5, z > 0 for 0.3 <= t < 0.35).
 
 Isotropic D = 1e-3 (the reference's scalar D); cfg 5's fibre-aligned sigma_l / sigma_t and its low-rank
@@ -75,10 +75,10 @@ def s1s2_source():
     return mb.DeviceSource(host, dev)
 
 
-def solve(ne, ne_t, p, max_it):
+def solve(ne, ne_t, p, max_it, stab="off"):
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
     prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s1s2_source(), D=1e-3)
-    cfg = mb.FixedPointConfig(stabilization="off", linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it)
+    cfg = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = mb.fixed_point_solve(prob, cfg)
@@ -86,7 +86,7 @@ def solve(ne, ne_t, p, max_it):
     return {"mesh": [ne] * 3 + [ne_t], "p": p, "N": st.num_dof, "wall_seconds": time.perf_counter() - t0,
             "sweeps": res.iterations, "converged": res.converged, "gmres_per_sweep": res.gmres_iterations,
             "avg_pcg": res.avg_pcg, "phase_seconds": {k: round(v, 3) for k, v in res.phase_seconds.items()},
-            "u_max": float(np.abs(res.u).max())}
+            "stabilization": stab, "u_max": float(np.abs(res.u).max())}
 
 
 if __name__ == "__main__":
@@ -98,9 +98,14 @@ if __name__ == "__main__":
     ap.add_argument("--solve-ne", type=int, default=24)
     ap.add_argument("--solve-ne-t", type=int, default=64)
     ap.add_argument("--max-it", type=int, default=60)
+    ap.add_argument("--su", action="store_true", help="also run the Spline Upwind solve")
+    ap.add_argument("--no-apply", action="store_true")
     a = ap.parse_args()
-    out = {"geometry": "prolate shell slab, quarter sector (radii 1/1/2, wall 0.2), degree-3 map, 8^3 elements",
-           "apply": apply_rate(a.ne, a.ne_t, a.p, a.steps)}
+    out = {"geometry": "prolate shell slab, quarter sector (radii 1/1/2, wall 0.2), degree-3 map, 8^3 elements"}
+    if not a.no_apply:
+        out["apply"] = apply_rate(a.ne, a.ne_t, a.p, a.steps)
     if a.solve_ne > 0:
         out["solve_galerkin"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it)
+        if a.su:
+            out["solve_su"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it, "spline_upwind")
     print(json.dumps(out))
