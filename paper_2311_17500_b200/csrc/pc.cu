@@ -190,7 +190,7 @@ int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double
   MI_CUDA(cudaMemcpy(c->pen_partner, partner, sizeof(int) * m, cudaMemcpyHostToDevice));
   c->tq_mb = MI_TSTAGE ? tstage_mb(nt) : 0;
   if (c->tq_mb > 0) {
-    c->tq_ksp = 2 * (((nt + 3) / 4 + 1) / 2);
+    c->tq_ksp = MI_TS_KC * (((nt + 3) / 4 + MI_TS_KC - 1) / MI_TS_KC);
     std::vector<double> f;
     build_tstage_frags(Q, nt, c->tq_mb, c->tq_ksp, f);
     if ((rc = dalloc(c->tq_frag, f.size()))) return rc;

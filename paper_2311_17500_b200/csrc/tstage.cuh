@@ -30,6 +30,12 @@
 #ifndef MI_TS_WM
 #define MI_TS_WM 4
 #endif
+#ifndef MI_TS_KC
+#define MI_TS_KC 2
+#endif
+#ifndef MI_TS_NST
+#define MI_TS_NST 4
+#endif
 
 namespace mi {
 
@@ -46,8 +52,8 @@ struct TStageArgs {
 
 template <int MB, int NC, int WM>
 struct TStage {
-  static constexpr int KC = 2;                      // k-steps per ring stage (= 8 tile rows)
-  static constexpr int NST = 4;                     // ring stages
+  static constexpr int KC = MI_TS_KC;               // k-steps per ring stage (2 = 8 tile rows)
+  static constexpr int NST = MI_TS_NST;             // ring stages
   static constexpr int NP = NC / 16;                // column pairs of 8-column blocks
   static constexpr int MH = (MB + WM - 1) / WM;     // row blocks per warp (rows split in WM groups)
   static constexpr int WARPS = WM * NP;
@@ -121,7 +127,8 @@ __global__ void __launch_bounds__(TStage<MB, NC, WM>::THREADS, 1) time_stage_fus
     for (int k = 0; k < nchk; ++k) {
       const int f = f0 + k;
       if (tid == 0) produce(f + G::NST - 1);
-      if (wait_rows && k < G::RCH) mbar_wait(&ybar[k], 0);
+      if (wait_rows)                                 // tile rows [4 KC k, 4 KC (k + 1)) have landed
+        for (int j = (4 * G::KC * k) / 8; j < G::RCH && j < (4 * G::KC * (k + 1) + 7) / 8; ++j) mbar_wait(&ybar[j], 0);
       mbar_wait(&full[f % G::NST], (unsigned)((f / G::NST) & 1));
       const double* st = ring + (f % G::NST) * G::STAGE + (h * G::MH) * 32 + lane;
 #pragma unroll
