@@ -238,7 +238,14 @@ def run_sharded(args):
     rank, world, local = dist_env()
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29577")
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    # MI_DIST_BACKEND=gloo: functional runs of several ranks on fewer GPUs (collectives staged through
+    # host memory; never a timing configuration)
+    backend = os.environ.get("MI_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     d, p = CFG["d"], CFG["p"]
@@ -286,9 +293,11 @@ def run_sharded(args):
         for k, v in c.read_profile(reset=True).items():
             a, b = prof.get(k, (0.0, 0))
             prof[k] = (a + v[0], b + v[1])
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    zsq = torch.tensor([float((z * z).sum())], dtype=torch.float64, device=t.device)
+    dist.all_reduce(zsq)                             # |P^-1 A x| over all ranks (sanity vs other N)
     value = N * args.steps / (ms_max * 1e-3)
     # e2e: pinned host slab -> device -> sharded A, P^-1 -> pinned host slab
     xh = x.cpu().pin_memory()
@@ -304,7 +313,7 @@ def run_sharded(args):
         zh.copy_(z, non_blocking=True)
     e1.record()
     torch.cuda.synchronize(dev)
-    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=t.device)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     dom = max(prof, key=lambda k: prof[k][0])
     nsten = (2 * p + 1) ** d
@@ -322,13 +331,14 @@ def run_sharded(args):
         "config": {"workload": CFG["name"], "d": d, "p": p, "mesh": [args.ne] * 3 + [args.ne_t], "dofs": N,
                    "su_rank": stab.rank,
                    "parallelism": "z-sharded x%d (p-plane halo + 2 all-to-all per step)" % world,
-                   "planes_per_rank": L.nz, "setup_s": t_setup,
+                   "planes_per_rank": L.nz, "setup_s": t_setup, "backend": backend,
                    "l2": "inputs > 126 MB L2 per rank (no flush needed)"},
         "e2e": {"value": N * e2s / (float(te.item()) * 1e-3), "unit": "DoF/s",
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                 "path": "ShardedOperator + ShardedPreconditioner from pinned host slabs (all ranks)"},
         "roofline": roof,
         "kernel_ms_per_step_rank0": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "z_norm": float(zsq.item()) ** 0.5,
         "gpu_launches": sum(v[1] for v in prof.values()),
         "clocks": clk.summary(),
     }

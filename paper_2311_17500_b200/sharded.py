@@ -92,6 +92,21 @@ class ZSlabLayout:
         return x_global.reshape(self.nt, self.n3, self.plane)[:, self.z_lo:self.z_hi].reshape(-1)
 
 
+def _staged(t, group=None):
+    """CUDA tensors under a gloo group are exchanged through host copies (functional runs of several
+    ranks on one GPU; NCCL moves device memory directly)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def _all_to_all(out, inp, out_splits, in_splits, group=None):
+    if _staged(inp, group):
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+
+
 def exchange_halo(L, x_own, x_in, group=None):
     """x_in = [h_lo planes from the left | owned planes | h_hi planes from the right], all time rows."""
     nt, P = L.nt, L.plane
@@ -102,14 +117,15 @@ def exchange_halo(L, x_own, x_in, group=None):
         return x_in
     ops, recv = [], []
     h = L.halo
+    dev = "cpu" if _staged(x_own, group) else x_own.device
     if L.rank > 0:
-        snd = xo[:, :h].contiguous()                   # my first planes = the left neighbour's upper halo
-        rcv = torch.empty(nt, L.h_lo, P, dtype=x_own.dtype, device=x_own.device)
+        snd = xo[:, :h].contiguous().to(dev)           # my first planes = the left neighbour's upper halo
+        rcv = torch.empty(nt, L.h_lo, P, dtype=x_own.dtype, device=dev)
         ops += [dist.P2POp(dist.isend, snd, L.rank - 1, group), dist.P2POp(dist.irecv, rcv, L.rank - 1, group)]
         recv.append((rcv, 0))
     if L.rank < L.world - 1:
-        snd_r = xo[:, L.nz - h:].contiguous()
-        rcv_r = torch.empty(nt, L.h_hi, P, dtype=x_own.dtype, device=x_own.device)
+        snd_r = xo[:, L.nz - h:].contiguous().to(dev)
+        rcv_r = torch.empty(nt, L.h_hi, P, dtype=x_own.dtype, device=dev)
         ops += [dist.P2POp(dist.isend, snd_r, L.rank + 1, group), dist.P2POp(dist.irecv, rcv_r, L.rank + 1, group)]
         recv.append((rcv_r, L.h_lo + L.nz))
     for r in dist.batch_isend_irecv(ops):
@@ -160,7 +176,7 @@ class ShardedPreconditioner:
             self.send[off:off + n].view(L.nt, L.nz, y1 - y0, L.n1).copy_(S[:, :, y0:y1])
             off += n
         if L.world > 1:
-            dist.all_to_all_single(self.blk2, self.send, self.split_blk, self.split_own, group=self.group)
+            _all_to_all(self.blk2, self.send, self.split_blk, self.split_own, group=self.group)
         else:
             self.blk2.copy_(self.send)
         B = self.blk.view(L.nt, L.n3, L.ny, L.n1)
@@ -182,7 +198,7 @@ class ShardedPreconditioner:
             self.blk2[off:off + n].view(L.nt, z1 - z0, L.ny, L.n1).copy_(B[:, z0:z1])
             off += n
         if L.world > 1:
-            dist.all_to_all_single(self.send, self.blk2, self.split_own, self.split_blk, group=self.group)
+            _all_to_all(self.send, self.blk2, self.split_own, self.split_blk, group=self.group)
         else:
             self.send.copy_(self.blk2)
         S = s_own.view(L.nt, L.nz, L.n2, L.n1)
@@ -212,7 +228,12 @@ class ShardedPreconditioner:
 
 def allreduce_sum(group=None):
     def red(t):
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        if _staged(t, group):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return red
 
 
