@@ -55,7 +55,10 @@ def grid_data(geo_spaces, ctrl, axes):
 class QuadData:
     """assembly.py:137-219 on the solution spaces (q = p+1 Gauss per element)."""
 
-    def __init__(self, spaces, geo_spaces, ctrl):
+    def __init__(self, spaces, geo_spaces, ctrl, fibre=None):
+        """``fibre = (sigma_l, sigma_t, direction)``: the transversely isotropic conductivity of BASELINE
+        cfg 5 (an extension: the reference's D is a scalar), D = sigma_t I + (sigma_l - sigma_t) f f^T
+        with f the unit tangent of map direction ``direction``; the stiffness metric is J^-1 D J^-T."""
         d = len(spaces)
         self.spaces = spaces
         self.rules = [Rule.on(s) for s in spaces]
@@ -68,12 +71,20 @@ class QuadData:
         self.x, jac = grid_data(geo_spaces, ctrl, [r.points for r in self.rules])
         self.detj = np.linalg.det(jac)
         self.jinv = np.linalg.inv(jac)
+        self.G = None
+        if fibre is not None:
+            sl, st_, k = fibre
+            f = jac[..., :, k] / np.linalg.norm(jac[..., :, k], axis=-1, keepdims=True)
+            D = st_ * np.eye(d) + (sl - st_) * f[..., :, None] * f[..., None, :]
+            self.G = self.jinv @ D @ np.swapaxes(self.jinv, -1, -2)
 
     def _ckron(self, deriv=None):
         d = len(self.spaces)
         return kron_list([self.c1[l] if l == deriv else self.c0[l] for l in reversed(range(d))])
 
     def metric(self, a, b):
+        if self.G is not None:
+            return self.G[..., a, b]
         return np.einsum("...k,...k->...", self.jinv[..., a, :], self.jinv[..., b, :])
 
     def mass(self):

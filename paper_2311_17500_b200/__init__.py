@@ -29,6 +29,7 @@ from .errors import (ConsistencyError, DecompositionError, ExtensionError, NonCo
 from .problem import (BoxGeometry, DeviceSource, FixedPointConfig, FixedPointDiverged, MonodomainProblem, ResidualIndicator,
                       SolveResult, compute_theta)
 from .spaces import SpaceTimeSpace, SplineSpace
+from .geometry import FibreConductivity, GeometryMap, MappedSpatialData, load_geometry, save_geometry
 
 __version__ = "0.1.0"
 
@@ -38,7 +39,8 @@ __all__ = [
     "gmres", "DeviceContext", "ConsistencyError", "DecompositionError", "ExtensionError",
     "NonConvergenceError", "StabilizationError", "BoxGeometry", "FixedPointConfig", "FixedPointDiverged",
     "MonodomainProblem", "ResidualIndicator", "SolveResult", "compute_theta", "fixed_point_solve",
-    "RecoverySolver", "ApplyStream",
+    "RecoverySolver", "ApplyStream", "GeometryMap", "MappedSpatialData", "FibreConductivity", "load_geometry",
+    "save_geometry",
 ]
 
 

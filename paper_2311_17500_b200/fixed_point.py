@@ -34,7 +34,13 @@ class _Workspace:
         if config.linear_solver == "direct":
             raise NotImplementedError("the direct (host LU) linear solver is not part of the device path")
         # mapped geometries: quadrature M_s / K_s, |det J| reaction, separable-weight P^-1 (solver.py:167-202)
-        self.sd = MappedSpatialData(st.spatial, problem.geometry) if is_mapped(problem.geometry) else None
+        from .geometry import is_fibre
+        fibre = problem.D if is_fibre(problem.D) else None
+        if fibre is not None and config.stabilization == "spline_upwind":
+            raise NotImplementedError("the residual indicator with a fibre conductivity (div(D grad u) with a "
+                                      "varying D) is not built; use Galerkin")
+        self.sd = (MappedSpatialData(st.spatial, problem.geometry, conductivity=fibre)
+                   if is_mapped(problem.geometry) else None)
         self.L = None if self.sd is not None else box_of(problem.geometry)[0]
         self.device = device
         self.indicator = None
@@ -55,7 +61,7 @@ class _Workspace:
             self.grid = GaussGrid(st, problem.geometry, mapped=self.sd)
             self.f_vec = load_vector(st, problem.geometry, problem.source, self.grid, device=device)
         self.pc_ctx = DeviceContext(st, device)
-        self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.D,
+        self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.scalar_D(),
                                                     problem.a * problem.c1, lengths=self.L, context=self.pc_ctx,
                                                     spatial_data=self.sd)
         # M_t (x) M_s for g = b (M_t (x) M_s) u  (C_m = D = 0, unit reaction: channel c1 = M_t (x) M_s)
@@ -69,7 +75,7 @@ class _Workspace:
         # allocations), so a sweep rebuilds tables, not allocations
         if getattr(self, "op_ctx", None) is None:
             self.op_ctx = DeviceContext(problem.space, self.device)
-        return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.D,
+        return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.scalar_D(),
                                  problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
                                  lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd)
 

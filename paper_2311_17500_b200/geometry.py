@@ -140,10 +140,39 @@ def is_mapped(geometry):
     return isinstance(geometry, GeometryMap) and geometry.affine_scales is None
 
 
-class MappedSpatialData:
-    """Quadrature data of a mapped geometry on the solution mesh (assembly.py:137-219)."""
+class FibreConductivity:
+    """Transversely isotropic conductivity D(x) = sigma_t I + (sigma_l - sigma_t) f f^T with the fibre
+    f(x) the unit physical tangent of map direction ``direction`` (BASELINE cfg 5: fibre-aligned
+    sigma_l = 1e-3, sigma_t = 3e-4).  An extension: the reference takes a scalar D (solver.py:66-101,
+    assembly.py:205-219); with this object the pulled-back stiffness metric becomes J^-1 D J^-T."""
 
-    def __init__(self, spatial_spaces, geometry, device="auto"):
+    def __init__(self, sigma_l, sigma_t, direction=0):
+        if sigma_l < 0 or sigma_t < 0:
+            raise ValueError("conductivities must be nonnegative")
+        self.sigma_l, self.sigma_t, self.direction = float(sigma_l), float(sigma_t), int(direction)
+
+    def tensor(self, jac):
+        """D on a grid of Jacobians jac[..., c, a] = dF_c / deta_a: grid + (d, d) (numpy or torch)."""
+        f = jac[..., :, self.direction]
+        d = jac.shape[-1]
+        if isinstance(jac, np.ndarray):
+            f = f / np.linalg.norm(f, axis=-1, keepdims=True)
+            return self.sigma_t * np.eye(d) + (self.sigma_l - self.sigma_t) * (f[..., :, None] * f[..., None, :])
+        import torch
+        f = f / torch.linalg.norm(f, dim=-1, keepdim=True)
+        eye = torch.eye(d, dtype=jac.dtype, device=jac.device)
+        return self.sigma_t * eye + (self.sigma_l - self.sigma_t) * (f[..., :, None] * f[..., None, :])
+
+
+def is_fibre(D):
+    return isinstance(D, FibreConductivity)
+
+
+class MappedSpatialData:
+    """Quadrature data of a mapped geometry on the solution mesh (assembly.py:137-219).  With a
+    ``conductivity`` (FibreConductivity) the stiffness metric is J^-1 D J^-T instead of J^-1 J^-T."""
+
+    def __init__(self, spatial_spaces, geometry, device="auto", conductivity=None):
         """``device``: where the map is evaluated and the Jacobians inverted ("auto": the current
         CUDA device if there is one; None: host numpy).  Results are host arrays either way."""
         self.spaces = tuple(spatial_spaces)
@@ -165,25 +194,35 @@ class MappedSpatialData:
             if bool(torch.any(det.abs() < SINGULAR_REL_TOL * torch.clamp(scale, min=1e-300)).item()):
                 raise GeometryError("singular Jacobian encountered during pull-back")
             self.xgrid = data["x"].cpu().numpy()
-            self.jinv = torch.linalg.inv(jac).cpu().numpy()
+            jinv = torch.linalg.inv(jac)
+            self._G = None
+            if conductivity is not None:
+                self._G = (jinv @ conductivity.tensor(jac) @ jinv.transpose(-1, -2)).cpu().numpy()
+            self.jinv = jinv.cpu().numpy()
             self.detj = det.cpu().numpy()
-            del data, jac, det, scale
+            del data, jac, det, scale, jinv
         else:
             data = geometry.grid_data([r[0] for r in self.rules], order=1)
             self.xgrid = data["x"]
             self.jinv, self.detj = jacobian_inverse_and_det(data["jac"])
+            self._G = None
+            if conductivity is not None:
+                self._G = self.jinv @ conductivity.tensor(data["jac"]) @ np.swapaxes(self.jinv, -1, -2)
         w = np.ones(())
         for l in reversed(range(d)):
             w = np.multiply.outer(w, self.rules[l][1])
         self.wgrid = w                                        # (Q_d, ..., Q_1)
         self.grid_shape = self.wgrid.shape
+        self.conductivity = conductivity
 
     def measure(self):
         """w |det J| on the grid."""
         return self.wgrid * np.abs(self.detj)
 
     def metric(self, a, b):
-        """(J^-1 J^-T)_{ab} on the grid."""
+        """(J^-1 J^-T)_{ab} on the grid ((J^-1 D J^-T)_{ab} with a conductivity)."""
+        if self._G is not None:
+            return self._G[..., a, b]
         return np.einsum("...k,...k->...", self.jinv[..., a, :], self.jinv[..., b, :])
 
     def metric_diag(self, direction):

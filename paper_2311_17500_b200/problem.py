@@ -98,11 +98,17 @@ class MonodomainProblem:
                 raise ValueError("%s must be nonnegative" % name)
         # D: scalar (the reference) or one value per spatial direction (anisotropic diagonal sigma,
         # the oracle extension of SURVEY Appendix B)
-        Dv = np.atleast_1d(np.asarray(self.D, float))
-        if np.any(Dv < 0):
-            raise ValueError("D must be nonnegative")
-        if Dv.size not in (1, len(self.space.spatial)):
-            raise ValueError("D must be a scalar or one value per spatial direction")
+        # or a geometry.FibreConductivity on mapped geometries (BASELINE cfg 5 extension)
+        from .geometry import is_fibre, is_mapped
+        if is_fibre(self.D):
+            if not is_mapped(self.geometry):
+                raise ValueError("a fibre conductivity needs a mapped geometry")
+        else:
+            Dv = np.atleast_1d(np.asarray(self.D, float))
+            if np.any(Dv < 0):
+                raise ValueError("D must be nonnegative")
+            if Dv.size not in (1, len(self.space.spatial)):
+                raise ValueError("D must be a scalar or one value per spatial direction")
         if self.geometry.final_time <= 0:
             raise ValueError("final time must be positive")
         if self.geometry.dim != len(self.space.spatial):
@@ -111,6 +117,11 @@ class MonodomainProblem:
     @property
     def final_time(self):
         return self.geometry.final_time
+
+    def scalar_D(self):
+        """The scalar multiplying K_s: D itself, or 1 when a FibreConductivity is folded into K_s."""
+        from .geometry import is_fibre
+        return 1.0 if is_fibre(self.D) else self.D
 
     def diffusion(self):
         """Per-direction diffusion coefficients (length d)."""

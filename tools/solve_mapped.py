@@ -7,8 +7,10 @@ our construction: the reference has no such geometry), p = 3.
          the device mapped residual indicator) with S1-S2 source stand-ins (S1 on the phi = 0 face for t < 0.05, S2 on the quadrant
          x < 0.5, z > 0 for 0.3 <= t < 0.35).
 
-Isotropic D = 1e-3 (the reference's scalar D); cfg 5's fibre-aligned sigma_l / sigma_t and its low-rank
-coefficients are not in the reference and not used here.
+Conductivity: cfg 5's fibre-aligned sigma_l = 1e-3 / sigma_t = 3e-4 (geometry.FibreConductivity, fibres
+along the azimuth; an extension of the reference's scalar D) for the apply and the Galerkin solve; the
+Spline Upwind solve uses the scalar D = 1e-3.  cfg 5's low-rank coefficient approximation is not used:
+the exact pulled-back coefficients are integrated by quadrature.
 
     python tools/solve_mapped.py --ne 64 --ne-t 256 --solve-ne 24 --solve-ne-t 64
 """
@@ -23,7 +25,12 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2311_17500_b200 as mb  # noqa: E402
-from paper_2311_17500_b200.geometry import MappedSpatialData, prolate_shell_geometry  # noqa: E402
+from paper_2311_17500_b200.geometry import (FibreConductivity, MappedSpatialData,  # noqa: E402
+                                            prolate_shell_geometry)
+
+# BASELINE cfg 5 conductivity: sigma_l = 1e-3 along the fibres, sigma_t = 3e-4 across; fibres along the
+# shell's azimuth (map direction 1).  An extension of the reference's scalar D (geometry.FibreConductivity).
+FIBRE = FibreConductivity(1e-3, 3e-4, direction=0)
 
 RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
 
@@ -33,9 +40,9 @@ def apply_rate(ne, ne_t, p, steps):
     geo = prolate_shell_geometry()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sd = MappedSpatialData(st.spatial, geo)
-    op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, spatial_data=sd)
-    P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1e-3, RM["a"] * RM["c1"], spatial_data=sd, context=op.ctx)
+    sd = MappedSpatialData(st.spatial, geo, conductivity=FIBRE)
+    op = mb.KroneckerOperator(st, 1.0, 1.0, 1.0, RM, spatial_data=sd)
+    P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1.0, RM["a"] * RM["c1"], spatial_data=sd, context=op.ctx)
     x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, st.num_dof)).cuda()
     y, z = torch.empty_like(x), torch.empty_like(x)
     op.apply_device(x, y)
@@ -77,7 +84,10 @@ def s1s2_source():
 
 def solve(ne, ne_t, p, max_it, stab="off"):
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
-    prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s1s2_source(), D=1e-3)
+    # Galerkin: the fibre conductivity; Spline Upwind: scalar D = sigma_l (its residual indicator with a
+    # varying conductivity tensor is not built)
+    prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s1s2_source(),
+                                D=FIBRE if stab == "off" else 1e-3)
     cfg = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -86,7 +96,8 @@ def solve(ne, ne_t, p, max_it, stab="off"):
     return {"mesh": [ne] * 3 + [ne_t], "p": p, "N": st.num_dof, "wall_seconds": time.perf_counter() - t0,
             "sweeps": res.iterations, "converged": res.converged, "gmres_per_sweep": res.gmres_iterations,
             "avg_pcg": res.avg_pcg, "phase_seconds": {k: round(v, 3) for k, v in res.phase_seconds.items()},
-            "stabilization": stab, "u_max": float(np.abs(res.u).max())}
+            "stabilization": stab, "conductivity": "fibre 1e-3 / 3e-4" if stab == "off" else "scalar 1e-3",
+            "u_max": float(np.abs(res.u).max())}
 
 
 if __name__ == "__main__":
