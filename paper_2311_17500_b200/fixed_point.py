@@ -39,7 +39,8 @@ class _Workspace:
         if fibre is not None and config.stabilization == "spline_upwind":
             raise NotImplementedError("the residual indicator with a fibre conductivity (div(D grad u) with a "
                                       "varying D) is not built; use Galerkin")
-        self.sd = (MappedSpatialData(st.spatial, problem.geometry, conductivity=fibre)
+        self.sd = (MappedSpatialData(st.spatial, problem.geometry, conductivity=fibre,
+                                     coefficient_rank=config.coefficient_rank, coefficient_tol=config.coefficient_tol)
                    if is_mapped(problem.geometry) else None)
         self.L = None if self.sd is not None else box_of(problem.geometry)[0]
         self.device = device

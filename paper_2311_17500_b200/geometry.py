@@ -172,9 +172,14 @@ class MappedSpatialData:
     """Quadrature data of a mapped geometry on the solution mesh (assembly.py:137-219).  With a
     ``conductivity`` (FibreConductivity) the stiffness metric is J^-1 D J^-T instead of J^-1 J^-T."""
 
-    def __init__(self, spatial_spaces, geometry, device="auto", conductivity=None):
+    def __init__(self, spatial_spaces, geometry, device="auto", conductivity=None, coefficient_rank=None,
+                 coefficient_tol=1e-6):
         """``device``: where the map is evaluated and the Jacobians inverted ("auto": the current
-        CUDA device if there is one; None: host numpy).  Results are host arrays either way."""
+        CUDA device if there is one; None: host numpy).  Results are host arrays either way.
+        ``coefficient_rank``: if given, M_s and K_s (and the reaction's |det J|) use canonical rank
+        <= coefficient_rank approximations of the coefficients (LowRankCoefficients, BASELINE cfg 5)
+        instead of the exact pulled-back values; ``coefficient_tol`` is the relative error at which
+        the rank search stops."""
         self.spaces = tuple(spatial_spaces)
         d = len(self.spaces)
         if geometry.dim != d:
@@ -214,6 +219,9 @@ class MappedSpatialData:
         self.wgrid = w                                        # (Q_d, ..., Q_1)
         self.grid_shape = self.wgrid.shape
         self.conductivity = conductivity
+        self.lowrank = None
+        if coefficient_rank is not None:
+            self.lowrank = LowRankCoefficients(self, coefficient_rank, coefficient_tol, device=device)
 
     def measure(self):
         """w |det J| on the grid."""
@@ -312,6 +320,170 @@ def separable_weights(sd):
         other = tuple(x for x in range(d) if x != axis)
         stiff.append(ratio.mean(axis=other) if other else ratio)
     return mass, stiff
+
+
+def _khatri_rao(A, B):
+    """Column-wise Kronecker product: (I, r), (J, r) -> (I*J, r), row i*J + j."""
+    return (A[:, None, :] * B[None, :, :]).reshape(-1, A.shape[1])
+
+
+def _leading_vectors(G, r, gen):
+    """r leading eigenvectors of the symmetric Gram matrix G (the HOSVD start of CP-ALS); columns past
+    G's size are seeded random."""
+    import torch
+    _, V = torch.linalg.eigh(G)
+    k = min(r, G.shape[0])
+    A = V[:, -k:].flip(-1)
+    if k < r:
+        extra = torch.rand((G.shape[0], r - k), generator=gen, dtype=G.dtype).to(G.device)
+        A = torch.cat([A, extra], dim=1)
+    return A.contiguous()
+
+
+def cp_als(X, rank, max_iter=500, rtol=1e-13):
+    """Canonical polyadic approximation X ~ sum_r prod_k A_k[:, r] of a 1-, 2- or 3-way torch f64
+    array (axis k of X <-> factor k).  1-way: X itself (rank 1); 2-way: truncated SVD (optimal);
+    3-way: alternating least squares from the HOSVD start, column norms balanced each sweep, stopped
+    when the squared residual changes by less than ``rtol`` relative.  Returns (factors, rel_err) with
+    rel_err = ||X - X_r|| / ||X|| evaluated explicitly.  (The low-rank coefficient approximation of
+    BASELINE cfg 5 has no counterpart in the reference.)"""
+    import torch
+    nd = X.dim()
+    if float(torch.linalg.norm(X)) == 0.0:
+        return [torch.zeros((n, 1), dtype=X.dtype, device=X.device) for n in X.shape], 0.0
+    if nd == 1:
+        return [X[:, None].clone()], 0.0
+    if nd == 2:
+        U, S, Vh = torch.linalg.svd(X, full_matrices=False)
+        r = min(rank, S.numel())
+        A = [U[:, :r] * S[:r], Vh[:r].T.contiguous()]
+    elif nd == 3:
+        Q0, Q1, Q2 = X.shape
+        gen = torch.Generator().manual_seed(0)
+        X0 = X.reshape(Q0, Q1 * Q2)
+        X2 = X.reshape(Q0 * Q1, Q2)
+        A = [_leading_vectors(X0 @ X0.T, rank, gen),
+             _leading_vectors(torch.einsum("ijk,ilk->jl", X, X), rank, gen),
+             _leading_vectors(X2.T @ X2, rank, gen)]
+        nx2 = float((X * X).sum())
+        prev = None
+        for _ in range(max_iter):
+            G = [a.T @ a for a in A]
+            A[0] = (X0 @ _khatri_rao(A[1], A[2])) @ torch.linalg.pinv(G[1] * G[2], hermitian=True)
+            G[0] = A[0].T @ A[0]
+            T = (X2 @ A[2]).reshape(Q0, Q1, -1)
+            A[1] = torch.einsum("ijr,ir->jr", T, A[0]) @ torch.linalg.pinv(G[0] * G[2], hermitian=True)
+            G[1] = A[1].T @ A[1]
+            V = G[0] * G[1]
+            M = X2.T @ _khatri_rao(A[0], A[1])
+            A[2] = M @ torch.linalg.pinv(V, hermitian=True)
+            res2 = max(nx2 - 2.0 * float((M * A[2]).sum()) + float((V * (A[2].T @ A[2])).sum()), 0.0)
+            nrm = [torch.linalg.norm(a, dim=0) for a in A]
+            g = (nrm[0] * nrm[1] * nrm[2]).clamp_min(1e-300) ** (1.0 / 3.0)
+            A = [a * (g / n.clamp_min(1e-300)) for a, n in zip(A, nrm)]
+            if prev is not None and abs(prev - res2) <= rtol * max(prev, 1e-30 * nx2):
+                break
+            prev = res2
+    else:
+        raise ValueError("cp_als takes 1-, 2- or 3-way arrays")
+    err = float(torch.linalg.norm(X - cp_reconstruct(A)) / torch.linalg.norm(X).clamp_min(1e-300))
+    return A, err
+
+
+def cp_reconstruct(A):
+    """sum_r prod_k A_k[:, r] as a dense array (axis k <-> A[k])."""
+    import torch
+    if len(A) == 1:
+        return A[0].sum(dim=1)
+    if len(A) == 2:
+        return A[0] @ A[1].T
+    return torch.einsum("ir,jr,kr->ijk", A[0], A[1], A[2])
+
+
+class LowRankCoefficients:
+    """Canonical rank <= ``max_rank`` approximations of the pulled-back geometry and conductivity
+    coefficients on the Gauss grid (BASELINE cfg 5: "geometry and conductivity coefficients low-rank
+    approximated (canonical rank <= 8)"; absent in the reference, whose SpatialQuadratureData integrates
+    the exact coefficients, assembly.py:197-219):
+
+    * ``"mass"``: |det J|,
+    * ``(a, b)``, a <= b: |det J| (J^-1 D J^-T)_ab (D = I, or the FibreConductivity tensor).
+
+    Each field c is approximated by c ~ sum_r prod_l g_{l,r}(xi_l) with the smallest rank whose
+    relative error on the grid is <= ``tol`` (capped at ``max_rank``).  Then every quadrature term of
+    M_s / K_s is a sum of Kronecker products of 1D weighted matrices
+    F_{l,r}[i, j] = sum_k w_k g_{l,r}(xi_k) B^(o)_i(xi_k) B^(o')_j(xi_k), so the device builds the
+    stencils with the Kronecker generator (mi_op_set_kron_channel) instead of tensor quadrature."""
+
+    def __init__(self, sd, max_rank=8, tol=1e-6, device="auto"):
+        import torch
+        if max_rank < 1:
+            raise ValueError("max_rank must be >= 1")
+        if device == "auto":
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        dev = torch.device("cpu") if device is None else torch.device(device)
+        d = len(sd.spaces)
+        self.d, self.max_rank, self.tol = d, int(max_rank), float(tol)
+        detj = np.abs(sd.detj)
+        fields = {"mass": detj}
+        for a in range(d):
+            for b in range(a, d):
+                fields[(a, b)] = detj * sd.metric(a, b)
+        self.factors, self.rank, self.error = {}, {}, {}
+        for key, f in fields.items():
+            X = torch.as_tensor(np.ascontiguousarray(f), dtype=torch.float64, device=dev)
+            for r in range(1, self.max_rank + 1):
+                A, err = cp_als(X, r)
+                if err <= self.tol:
+                    break
+            # factor of direction l = array axis d-1-l
+            self.factors[key] = [A[d - 1 - l].cpu().numpy() for l in range(d)]
+            self.rank[key] = A[0].shape[1]
+            self.error[key] = err
+            del X
+
+    def reconstruct(self, key):
+        """The rank-r field on the grid (Q_d, ..., Q_1)."""
+        import torch
+        A = [torch.as_tensor(self.factors[key][self.d - 1 - k]) for k in range(self.d)]
+        return cp_reconstruct(A).numpy()
+
+    def stiffness_key(self, a, b):
+        return (min(a, b), max(a, b))
+
+    def kron_terms(self, sd, kind, p, nmax):
+        """(coef, bands) of mi_op_set_kron_channel for ``kind`` "mass" (M_s) or "stiffness" (K_s, the
+        test function carrying the derivative in direction a, the trial function in b, as
+        stiffness_terms)."""
+        from .spaces import to_band
+        d = self.d
+        if kind == "mass":
+            terms = [("mass", [(0, 0)] * d)]
+        elif kind == "stiffness":
+            terms = [(self.stiffness_key(a, b), [(1 if l == a else 0, 1 if l == b else 0) for l in range(d)])
+                     for a in range(d) for b in range(d)]
+        else:
+            raise ValueError("kind must be 'mass' or 'stiffness'")
+        rows = []
+        for key, orders in terms:
+            g = self.factors[key]
+            for r in range(g[0].shape[1]):
+                row = []
+                for l in range(d):
+                    oi, oj = orders[l]
+                    w = sd.rules[l][1] * g[l][:, r]
+                    F = (sd.tables(l, oi) * w[:, None]).T @ sd.tables(l, oj)
+                    row.append(to_band(F, p))
+                rows.append(row)
+        bands = np.zeros((len(rows), d, nmax, 2 * p + 1))
+        for t, row in enumerate(rows):
+            for l in range(d):
+                bands[t, l, :row[l].shape[0]] = row[l]
+        return np.ones(len(rows)), np.ascontiguousarray(bands)
+
+    def summary(self):
+        return {("%s" % (k,)).replace(" ", ""): {"rank": self.rank[k], "rel_err": self.error[k]}
+                for k in self.factors}
 
 
 def interpolate_map(spaces, fn):

@@ -185,7 +185,8 @@ class KroneckerOperator:
             set_reaction(ctx, st, final_time, consts, u, w, None if sd is not None else L,
                          time_rows=self.time_rows, zslab=ctx.zslab)
             if sd is not None:
-                jw = np.ascontiguousarray(np.abs(sd.detj))
+                jw = np.abs(sd.detj) if sd.lowrank is None else sd.lowrank.reconstruct("mass")
+                jw = np.ascontiguousarray(jw)
                 _lib.call("mi_op_set_reaction_weight", ctx.handle, host_ptr(jw))
         else:
             _lib.call("mi_op_clear_reaction", ctx.handle)    # a reused context may carry one
@@ -240,12 +241,17 @@ def mapped_stencils(ctx, sd):
         Qh = np.asarray([r[0].size for r in sd.rules], dtype=np.int32)
         nsten = (2 * p + 1) ** d
         out = []
-        for terms in (mass_terms(sd), stiffness_terms(sd, 1.0)):
-            coef = np.asarray([t[0] for t in terms], float)
-            theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
-            T = quad_tables(sd, [t[2] for t in terms], p, nmax)
-            _lib.call("mi_op_set_quad_channel", ctx.handle, 0, len(terms), host_ptr(coef), host_ptr(theta),
-                      host_ptr(T), host_ptr(qh), host_ptr(Qh))
+        for kind, terms in (("mass", mass_terms(sd)), ("stiffness", stiffness_terms(sd, 1.0))):
+            if sd.lowrank is not None:
+                # low-rank coefficients: a sum of Kronecker products of 1D weighted factors
+                coef, bands = sd.lowrank.kron_terms(sd, kind, p, nmax)
+                _lib.call("mi_op_set_kron_channel", ctx.handle, 0, len(coef), host_ptr(coef), host_ptr(bands))
+            else:
+                coef = np.asarray([t[0] for t in terms], float)
+                theta = np.ascontiguousarray(np.stack([t[1] for t in terms]))
+                T = quad_tables(sd, [t[2] for t in terms], p, nmax)
+                _lib.call("mi_op_set_quad_channel", ctx.handle, 0, len(terms), host_ptr(coef), host_ptr(theta),
+                          host_ptr(T), host_ptr(qh), host_ptr(Qh))
             buf = ctx.empty(nsten * ctx.ns)
             _lib.call("mi_op_get_channel_stencil", ctx.handle, 0, dptr(buf))
             out.append(buf)

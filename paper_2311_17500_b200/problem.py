@@ -150,6 +150,11 @@ class FixedPointConfig:
     evolve_recovery: bool = True
     indicator_override: object = None
     verbose: bool = False
+    # extension (BASELINE cfg 5; not in the reference): canonical rank <= coefficient_rank approximations
+    # of the mapped geometry / conductivity coefficients in M_s, K_s (geometry.LowRankCoefficients);
+    # None keeps the exact pulled-back coefficients of the reference
+    coefficient_rank: object = None
+    coefficient_tol: float = 1e-6
 
     def __post_init__(self):
         if not 0.0 < self.relaxation <= 1.0:
@@ -162,6 +167,8 @@ class FixedPointConfig:
             raise ValueError("unknown indicator update %r" % self.indicator_update)
         if self.linear_solver not in ("auto", "direct", "iterative"):
             raise ValueError("unknown linear solver %r" % self.linear_solver)
+        if self.coefficient_rank is not None and int(self.coefficient_rank) < 1:
+            raise ValueError("coefficient_rank must be >= 1")
 
 
 @dataclass

@@ -2,15 +2,17 @@
 our construction: the reference has no such geometry), p = 3.
 
   apply: z = P^-1 (A x) on the mapped geometry (Galerkin terms + zero-iterate reaction; M_s and K_s
-         assembled by Gauss quadrature on the device), DoF/s and per-kernel ms;
+         from the low-rank coefficients as Kronecker sums, or with --rank 0 by Gauss quadrature of the
+         exact coefficients on the device), DoF/s and per-kernel ms;
   solve: the relaxed fixed-point solve (Galerkin, and with --su Spline Upwind: mapped SU stencils and
          the device mapped residual indicator) with S1-S2 source stand-ins (S1 on the phi = 0 face for t < 0.05, S2 on the quadrant
          x < 0.5, z > 0 for 0.3 <= t < 0.35).
 
 Conductivity: cfg 5's fibre-aligned sigma_l = 1e-3 / sigma_t = 3e-4 (geometry.FibreConductivity, fibres
 along the azimuth; an extension of the reference's scalar D) for the apply and the Galerkin solve; the
-Spline Upwind solve uses the scalar D = 1e-3.  cfg 5's low-rank coefficient approximation is not used:
-the exact pulled-back coefficients are integrated by quadrature.
+Spline Upwind solve uses the scalar D = 1e-3.  Coefficients: cfg 5's canonical rank <= 8 approximation
+of |det J| and |det J| J^-1 D J^-T (geometry.LowRankCoefficients, --rank 8, the default); --rank 0
+integrates the exact pulled-back coefficients (the reference's SpatialQuadratureData).
 
     python tools/solve_mapped.py --ne 64 --ne-t 256 --solve-ne 24 --solve-ne-t 64
 """
@@ -35,12 +37,12 @@ FIBRE = FibreConductivity(1e-3, 3e-4, direction=0)
 RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
 
 
-def apply_rate(ne, ne_t, p, steps):
+def apply_rate(ne, ne_t, p, steps, rank=8):
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
     geo = prolate_shell_geometry()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sd = MappedSpatialData(st.spatial, geo, conductivity=FIBRE)
+    sd = MappedSpatialData(st.spatial, geo, conductivity=FIBRE, coefficient_rank=rank or None)
     op = mb.KroneckerOperator(st, 1.0, 1.0, 1.0, RM, spatial_data=sd)
     P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1.0, RM["a"] * RM["c1"], spatial_data=sd, context=op.ctx)
     x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, st.num_dof)).cuda()
@@ -65,7 +67,14 @@ def apply_rate(ne, ne_t, p, steps):
     prof = {k: round(v[0] / steps, 3) for k, v in op.ctx.read_profile(reset=True).items() if v[1]}
     return {"mesh": [ne] * 3 + [ne_t], "p": p, "N": st.num_dof, "ms_per_apply": ms,
             "dof_per_s": st.num_dof / (ms * 1e-3), "kernel_ms": prof, "setup_s": setup,
-            "detj_range": [float(np.abs(sd.detj).min()), float(np.abs(sd.detj).max())]}
+            "detj_range": [float(np.abs(sd.detj).min()), float(np.abs(sd.detj).max())],
+            "coefficients": coefficient_summary(sd)}
+
+
+def coefficient_summary(sd):
+    if sd is None or sd.lowrank is None:
+        return "exact pulled-back coefficients (Gauss quadrature)"
+    return {"max_rank": sd.lowrank.max_rank, "tol": sd.lowrank.tol, "fields": sd.lowrank.summary()}
 
 
 def s1s2_source():
@@ -82,13 +91,14 @@ def s1s2_source():
     return mb.DeviceSource(host, dev)
 
 
-def solve(ne, ne_t, p, max_it, stab="off"):
+def solve(ne, ne_t, p, max_it, stab="off", rank=8):
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
     # Galerkin: the fibre conductivity; Spline Upwind: scalar D = sigma_l (its residual indicator with a
     # varying conductivity tensor is not built)
     prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s1s2_source(),
                                 D=FIBRE if stab == "off" else 1e-3)
-    cfg = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it)
+    cfg = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it,
+                              coefficient_rank=rank or None)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = mb.fixed_point_solve(prob, cfg)
@@ -97,7 +107,8 @@ def solve(ne, ne_t, p, max_it, stab="off"):
             "sweeps": res.iterations, "converged": res.converged, "gmres_per_sweep": res.gmres_iterations,
             "avg_pcg": res.avg_pcg, "phase_seconds": {k: round(v, 3) for k, v in res.phase_seconds.items()},
             "stabilization": stab, "conductivity": "fibre 1e-3 / 3e-4" if stab == "off" else "scalar 1e-3",
-            "u_max": float(np.abs(res.u).max())}
+            "u_max": float(np.abs(res.u).max()),
+            "coefficients": "canonical rank <= %d" % rank if rank else "exact"}
 
 
 if __name__ == "__main__":
@@ -111,12 +122,13 @@ if __name__ == "__main__":
     ap.add_argument("--max-it", type=int, default=60)
     ap.add_argument("--su", action="store_true", help="also run the Spline Upwind solve")
     ap.add_argument("--no-apply", action="store_true")
+    ap.add_argument("--rank", type=int, default=8, help="canonical rank cap of the coefficients (0: exact)")
     a = ap.parse_args()
     out = {"geometry": "prolate shell slab, quarter sector (radii 1/1/2, wall 0.2), degree-3 map, 8^3 elements"}
     if not a.no_apply:
-        out["apply"] = apply_rate(a.ne, a.ne_t, a.p, a.steps)
+        out["apply"] = apply_rate(a.ne, a.ne_t, a.p, a.steps, a.rank)
     if a.solve_ne > 0:
-        out["solve_galerkin"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it)
+        out["solve_galerkin"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it, rank=a.rank)
         if a.su:
-            out["solve_su"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it, "spline_upwind")
+            out["solve_su"] = solve(a.solve_ne, a.solve_ne_t, a.p, a.max_it, "spline_upwind", rank=a.rank)
     print(json.dumps(out))
