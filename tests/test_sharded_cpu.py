@@ -1,5 +1,5 @@
 """Space-sharded orchestration (z-plane halo exchange, all-to-all transposes to
-y-slabs, allreduce'd GMRES) on CPU with the gloo backend, world_size 2-4.
+y-slabs, allreduce'd GMRES) on CPU with the gloo backend, world_size 2-8.
 
 The product orchestration (paper_2311_17500_b200/sharded.py) runs unchanged;
 the local slab operations are supplied by a numpy reference backend built on
@@ -169,12 +169,16 @@ def _gather(g, res, key_index, world):
     return out.ravel()
 
 
-CASES = [(2, "case_3d_p2_front"), (2, "case_3d_p3"), (3, "synthetic"), (4, "synthetic")]
+# "synthetic8": the BASELINE's largest rank count (8 z slabs of 2 planes, 8 y-column ranges of 1)
+CASES = [(2, "case_3d_p2_front"), (2, "case_3d_p3"), (3, "synthetic"), (4, "synthetic"), (8, "synthetic8")]
 
 
 @pytest.mark.parametrize("world,CASE", CASES)
 def test_space_sharded_apply_and_gmres_gloo(world, CASE):
-    g = synthetic_case() if CASE == "synthetic" else load(CASE)
+    if CASE == "synthetic8":
+        g = synthetic_case(ne=(3, 6, 14))
+    else:
+        g = synthetic_case() if CASE == "synthetic" else load(CASE)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
