@@ -611,7 +611,11 @@ static int dmma_prepare(mi_ctx* c) {
 // y = sum_c T_c (x) along time of the time-innermost W buffer (HBM-bound)
 static int launch_time_filter(mi_ctx* c, double* y) {
   MI_REQUIRE(c->nchan <= 64, MI_ERR_ARG, "too many channels for the time filter");
-  if (TFilterCfg::smem(c->pt, c->nchan) <= 232448 && c->pt <= TFilterCfg::PX) {
+#ifndef MI_TF_FRAG
+#define MI_TF_FRAG 1
+#endif
+  const bool frag = MI_TF_FRAG && TFilterCfg::smem(c->pt, c->nchan, true) <= 232448;
+  if (TFilterCfg::smem(c->pt, c->nchan, frag) <= 232448 && c->pt <= TFilterCfg::PX) {
     // tensor-core filter: persistent blocks, one time block of 56 rows each
     static int nsm = 0;
     if (nsm == 0) {
@@ -622,15 +626,19 @@ static int launch_time_filter(mi_ctx* c, double* y) {
     }
     const int ntb = (c->nt + TFilterCfg::TR - 1) / TFilterCfg::TR;
     const int grid = ntb * std::max(1, nsm / ntb);
-    const size_t sm = TFilterCfg::smem(c->pt, c->nchan);
+    const size_t sm = TFilterCfg::smem(c->pt, c->nchan, frag);
 #define MI_TFD(PTV)                                                                                            \
   case PTV: {                                                                                                  \
     static bool attr = false;                                                                                  \
     if (!attr) {                                                                                               \
-      MI_CUDA(cudaFuncSetAttribute(time_filter_dmma<PTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448)); \
+      MI_CUDA(cudaFuncSetAttribute(time_filter_dmma<PTV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448)); \
+      MI_CUDA(cudaFuncSetAttribute(time_filter_dmma<PTV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448)); \
       attr = true;                                                                                             \
     }                                                                                                          \
-    time_filter_dmma<PTV><<<grid, 256, sm, c->stream>>>(c->tmap_w, c->tband.p, y, c->nchan, c->nt, c->ns, ntb, 0); \
+    if (frag)                                                                                                  \
+      time_filter_dmma<PTV, true><<<grid, 256, sm, c->stream>>>(c->tmap_w, c->tband.p, y, c->nchan, c->nt, c->ns, ntb, 0); \
+    else                                                                                                       \
+      time_filter_dmma<PTV, false><<<grid, 256, sm, c->stream>>>(c->tmap_w, c->tband.p, y, c->nchan, c->nt, c->ns, ntb, 0); \
   } break;
     switch (c->pt) {
       MI_TFD(1) MI_TFD(2) MI_TFD(3) MI_TFD(4)
