@@ -86,8 +86,17 @@ struct RxTile {
   static constexpr int ev(int n) { return (n + 1) & ~1; }                        // 16-byte aligned buffers
   static constexpr int SIN = ev(3 * B4::LS);
   static constexpr int SA = D >= 2 ? ev(3 * B4::L3 * B4::L2 * B4::Q1) : 2;
-  static constexpr int SB = D >= 3 ? ev(3 * B4::L3 * B4::Q2 * B4::Q1) : 2;
-  static constexpr int SC = D >= 2 ? ev(B4::L * QL) : 2;
+  // bank-conflict padding (d = 3, 8 Gauss points per direction, i.e. p = 3): the y-interpolation
+  // output rows (q2 stride BS1 = 4 mod 8) and planes (j3 stride BJ = 8 mod 16), and the last-direction
+  // projection output (j stride CS = 4 mod 8), so that the DMMA accumulator stores (lanes 2 fk, fr) and
+  // the A-fragment reads (lanes fk, fr) each touch every bank pair exactly twice.  ncu before: 47% of
+  // the kernel's shared wavefronts were conflict replays.
+  static constexpr bool PADB = D == 3 && Q1 % 8 == 0;
+  static constexpr int BS1 = PADB ? Q1 + 4 : Q1;
+  static constexpr int BJ = PADB ? Q2 * BS1 + ((8 - (Q2 * BS1) % 16) + 16) % 16 : Q2 * Q1;
+  static constexpr int CS = PADB ? QL + 4 : QL;
+  static constexpr int SB = D >= 3 ? ev(3 * B4::L3 * BJ) : 2;
+  static constexpr int SC = D >= 2 ? ev(B4::L * CS) : 2;
   static constexpr int SD = D >= 3 ? ev(B4::L3 * B4::L2 * B4::Q1) : 2;
   static constexpr int NIN = 3 * B4::LS;                                          // input items per slice
   static constexpr int NPRE = (NIN + NTH - 1) / NTH;
@@ -107,6 +116,7 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
   constexpr int LS = G::LS, KI = G::KI, KP = G::KP, QL = G::QL, NT = G::NT, MT = G::MT;
   constexpr int NW = G::NW, NTH = G::NTH;
+  constexpr int BS1 = G::BS1, BJ = G::BJ, CS = G::CS;
   constexpr int PW = PT + 1, QT = PT + 1;
   constexpr int NBT = 2 * QT * PW;                  // time basis (interpolation) + weighted (projection)
   constexpr int NLX = L3 * L2;                      // x-projection lines (j3, j2)
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
             const int q1 = line % Q1, j3 = line / Q1;
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < KP; ++ks) dmma(c0, c1, sC[(j3 * Q2 + 4 * ks + fk) * Q1 + q1], bP[1][ks]);
+            for (int ks = 0; ks < KP; ++ks) dmma(c0, c1, sC[j3 * CS + (4 * ks + fk) * Q1 + q1], bP[1][ks]);
             const int n0 = 2 * fk;
             if (line < NL) {
               if (n0 < L2) sD[(j3 * L2 + n0) * Q1 + q1] = c0;
@@ -338,8 +348,8 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
           for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, sA[(fj3 * L2 + 4 * ks + fk) * Q1 + q1], bI[1][ks]);
           const int n0 = 2 * fk;
           if (line < NL) {
-            if (n0 < Q2) sB[(fj3 * Q2 + n0) * Q1 + q1] = c0;
-            if (n0 + 1 < Q2) sB[(fj3 * Q2 + n0 + 1) * Q1 + q1] = c1;
+            if (n0 < Q2) sB[fj3 * BJ + n0 * BS1 + q1] = c0;
+            if (n0 + 1 < Q2) sB[fj3 * BJ + (n0 + 1) * BS1 + q1] = c1;
           }
         }
       }
@@ -355,11 +365,14 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
         const int t = warp + NW * mi;
         if (t < NT) {
           const int line = 8 * t + fr;
+          // sB (d = 3) holds (q2, q1) rows at stride BS1 and j3 planes at stride BJ
+          const int loff = D == 3 ? (line / Q1) * BS1 + line % Q1 : line;
+          constexpr int FS = D == 3 ? BJ : QL;
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, fin[(f * L + 4 * ks + fk) * QL + line], bI[D - 1][ks]);
+            for (int ks = 0; ks < KI; ++ks) dmma(c0, c1, fin[(f * L + 4 * ks + fk) * FS + loff], bI[D - 1][ks]);
             // fused: (u, c2 w, w_x x); pre: (u, c2 w); stored: (x) -- the weight is in c_w
             const double sc0 = MODE == RX_STORED ? 1.0 : (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]));
             const double sc1 = MODE == RX_STORED ? 1.0 : (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]));
@@ -437,8 +450,8 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
               if (yidx[1] >= 0) atomicAdd(r.y + row + yidx[1], c1);
             }
           } else {
-            if (n0 < L) sC[n0 * QL + line] = c0;
-            if (n0 + 1 < L) sC[(n0 + 1) * QL + line] = c1;
+            if (n0 < L) sC[n0 * CS + line] = c0;
+            if (n0 + 1 < L) sC[(n0 + 1) * CS + line] = c1;
           }
         }
       }
