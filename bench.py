@@ -12,9 +12,10 @@ L2 flush is needed between steps.
 Arms:
   (default)          this package's CUDA path, device-resident vectors ("value"),
                      plus "e2e" through the public API from pinned host memory.
-  --impl reference   the reference algorithm on the host CPU: the oracle port
-                     (oracle/, a restatement of the reference pinned against
-                     its golden vectors) at a bounded sample of the workload.
+  --impl reference   the reference's own CPU path on the host: the unmodified
+                     reference installed under baseline/_ref (else the pinned
+                     oracle port) on a bounded sample of the workload (the
+                     reference cannot assemble the cfg-4 SU operator).
 
 Multi-GPU (torchrun, N > 1): the space-sharded apply of the SAME workload
 (strong scaling): each rank owns n_3/G z planes for all time rows; a step is
@@ -71,16 +72,69 @@ def front_indicator_np(tg, g1, ns):
 
 
 # ---------------------------------------------------------------- CPU arm
+def workload_config(world=1):
+    """The workload both arms report (BASELINE configs[3]); identical dicts so the driver can match them."""
+    ne, ne_t, p = CFG["ne"], CFG["ne_t"], CFG["p"]
+    n = ne + p
+    return {"workload": CFG["name"], "d": CFG["d"], "p": p, "mesh": [ne] * 3 + [ne_t],
+            "dofs": n ** 3 * (ne_t + p - 1), "su_rank": 6, "su_tol": CFG["su_tol"],
+            "reaction": "zero-iterate a*c1 M_t x M_s", "sigma": CFG["sigma"],
+            "l2": "inputs 1.5 GB > 126 MB L2 (no flush needed)",
+            "parallelism": "single GPU" if world == 1 else "z-sharded x%d" % world}
+
+
+def _reference_module():
+    """The unmodified reference installed under baseline/_ref (pip --target), else None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "monoiga")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import monoiga  # noqa: F401
+        return path
+    except Exception:
+        return None
+
+
 def cpu_sample_rate(steps, warmup, ne, ne_t):
-    """Reference algorithm (oracle port) on the host: DoF/s of P^-1 (A x)."""
-    from oracle import problem as oprob
-    from oracle.splines import make_space_time
-    st = make_space_time(CFG["d"], CFG["p"], ne, ne_t)
-    th = oprob.front_indicator(st)
-    su, lr, _ = oprob.su_from_indicator(st, th, CFG["su_tol"])
-    op = oprob.operator_terms(st, 1.0, 1.0, CFG["sigma"], RM, su_terms=su)
-    pc = oprob.preconditioner(st, 1.0, 1.0, CFG["sigma"], RM)
-    x = np.random.default_rng(0).uniform(-1, 1, st.num_dof)
+    """The reference's own CPU path on the host: DoF/s of P^-1 (A x) on a bounded sample of the
+    workload (same d, p, physics, SU indicator and tolerance; smaller mesh).  Runs the unmodified
+    reference from baseline/_ref when installed (kind "reference"), else the pinned oracle port."""
+    d, p = CFG["d"], CFG["p"]
+    x = None
+    if _reference_module() is not None:
+        from monoiga.assembly import KroneckerOperator, SpatialQuadratureData, spatial_operators, time_matrices
+        from monoiga.bspline import SplineSpace, SpaceTimeSpace
+        from monoiga.geometry import builtin_geometry
+        from monoiga.linalg import FastDiagPreconditioner
+        from monoiga.stabilization import ResidualIndicator, assemble_stabilization, compute_tau, lowrank_factorize
+        st = SpaceTimeSpace([SplineSpace.uniform(p, ne) for _ in range(d)], SplineSpace.uniform(p, ne_t))
+        geo = builtin_geometry("unit_cube", final_time=1.0)
+        W_t, M_t = time_matrices(st, 1.0)
+        M_s, K_s = spatial_operators(st.spatial, geo)
+        th = front_indicator_np(st.time_greville(), st.spatial[0].greville(), st.num_space)
+        ind = ResidualIndicator(th, st.time_greville(), [s.greville() for s in st.spatial], st.spatial_shape)
+        lr = lowrank_factorize(ind, CFG["su_tol"])
+        stab = assemble_stabilization(compute_tau(st.time), lr, st, geo, 1.0)
+        react = RM["a"] * RM["c1"]
+        op = KroneckerOperator(st.num_time, st.num_space, [(1.0, W_t, M_s), (CFG["sigma"], M_t, K_s),
+                                                           (react, M_t, M_s)] + stab.terms())
+        pc = FastDiagPreconditioner.build(st, 1.0, 1.0, CFG["sigma"], react,
+                                          spatial_data=SpatialQuadratureData(st.spatial, geo))
+        kind, what, rank, N = "reference", "the unmodified reference (baseline/_ref monoiga: KroneckerOperator." \
+            "matvec + FastDiagPreconditioner.apply)", lr.rank, st.num_dof
+    else:
+        from oracle import problem as oprob
+        from oracle.splines import make_space_time
+        st = make_space_time(d, p, ne, ne_t)
+        th = oprob.front_indicator(st)
+        su, lr, _ = oprob.su_from_indicator(st, th, CFG["su_tol"])
+        op = oprob.operator_terms(st, 1.0, 1.0, CFG["sigma"], RM, su_terms=su)
+        pc = oprob.preconditioner(st, 1.0, 1.0, CFG["sigma"], RM)
+        kind, what, rank, N = "port", "oracle port of the reference (CSR Kronecker matvec + complex FD apply)", \
+            lr.rank, st.num_dof
+    x = np.random.default_rng(0).uniform(-1, 1, N)
     for _ in range(warmup):
         pc.apply(op.matvec(x))
     ts = []
@@ -89,9 +143,23 @@ def cpu_sample_rate(steps, warmup, ne, ne_t):
         pc.apply(op.matvec(x))
         ts.append(time.perf_counter() - t0)
     tot = sum(ts)
-    sample = ("oracle port of the reference (CSR Kronecker matvec + complex FD apply), d=3 p=3 %d^3 x %d "
-              "elements (N=%d, SU rank %d), %d timed applies" % (ne, ne_t, st.num_dof, lr.rank, steps))
-    return st.num_dof * steps / tot, tot / steps, sample, st.num_dof
+    sample = ("%s, d=3 p=3 %d^3 x %d elements (N=%d, SU rank %d, the seeded front indicator at tol %.1f), %d "
+              "timed applies; numpy/OpenBLAS threads = all %d host cores, scipy.sparse SpMM single-threaded "
+              "(the reference's design); the full cfg-4 operator with SU cannot be assembled by the reference "
+              "(SURVEY 8c)" % (what, ne, ne_t, N, rank, CFG["su_tol"], steps, os.cpu_count()))
+    return N * steps / tot, tot / steps, sample, N, kind
+
+
+def reference_full_size():
+    """Full-size reference CPU timings from tools/ref_cpu.py (run on the same box type), if recorded."""
+    path = os.path.join(ROOT, "profiles", "r02_ref_cpu.json")
+    try:
+        with open(path) as fh:
+            out = json.load(fh)
+        out["source"] = "profiles/r02_ref_cpu.json (tools/ref_cpu.py on a B200 box host; not re-run by bench.py)"
+        return out
+    except Exception:
+        return None
 
 
 def run_reference(args):
@@ -99,16 +167,18 @@ def run_reference(args):
     if rank != 0:
         return
     cores = os.cpu_count()
-    rate, sec, sample, n = cpu_sample_rate(args.steps, max(args.warmup, 1), SAMPLE["ne"], SAMPLE["ne_t"])
+    rate, sec, sample, n, kind = cpu_sample_rate(args.steps, max(args.warmup, 1), SAMPLE["ne"], SAMPLE["ne_t"])
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "DoF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": {"workload": CFG["name"] + " (bounded CPU sample)", "d": 3, "p": 3,
-                   "sample_mesh": [SAMPLE["ne"]] * 3 + [SAMPLE["ne_t"]], "dofs": n},
-        "cpu_baseline": {"value": rate, "unit": "DoF/s", "cores": cores, "kind": "port", "sample": sample},
+        "config": workload_config(1),
+        "cpu_baseline": {"value": rate, "unit": "DoF/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": rate, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    full = reference_full_size()
+    if full is not None:
+        line["reference_full_size"] = full
     print(json.dumps(line), flush=True)
 
 
@@ -162,23 +232,31 @@ class ClockSampler:
 
 
 def fp64_peak_tflops(torch, dev):
-    """Measured FP64 tensor-core throughput (cuBLAS DGEMM 4096^3, best of 5)."""
-    n = 4096
+    """Measured FP64 tensor-core peak: max(cuBLAS DGEMM 8192^3 best of 10, the library's DMMA
+    microbenchmark mi_diag_fp64_peak).  Returns (peak, details)."""
+    import ctypes
+    from paper_2311_17500_b200 import _lib
+    n = 8192
     a = torch.randn(n, n, dtype=torch.float64, device=dev)
     b = torch.randn(n, n, dtype=torch.float64, device=dev)
-    for _ in range(2):
-        a @ b
+    c = a @ b
     torch.cuda.synchronize(dev)
     best = 1e30
-    for _ in range(5):
+    for _ in range(10):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        a @ b
+        torch.matmul(a, b, out=c)
         e1.record()
         torch.cuda.synchronize(dev)
         best = min(best, e0.elapsed_time(e1))
-    del a, b
-    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    del a, b, c
+    dgemm = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    det = {"dgemm_8192": dgemm}
+    for kind, name in ((0, "dmma_micro"), (1, "dfma_micro"), (2, "dmma_dfma_mixed_micro")):
+        tf = ctypes.c_double()
+        _lib.call("mi_diag_fp64_peak", dev.index, kind, ctypes.byref(tf), None)
+        det[name] = tf.value
+    return max(dgemm, det["dmma_micro"]), det
 
 
 def measured_peaks():
@@ -218,6 +296,32 @@ def measure_solve(torch, mb, dev):
     out = {"config": "cfg3 3D p=2 64^3x128 (N=%d), sigma=diag(1e-3,4e-4,4e-4), SU rank %d" % (st.num_dof, stab.rank),
            "seconds": e0.elapsed_time(e1) * 1e-3, "iterations": it, "final_rel_residual": hist[-1],
            "n_gpus": 1}
+    op.ctx.close()
+    return out
+
+
+def measure_gmres_cfg2(torch, mb, dev):
+    """The cfg-2 sweep-1 system (2D p=3 128^2 x 256, N=4.4M: Galerkin + zero-iterate reaction + SU with
+    the front indicator at tol 0.1), gmres(tol=1e-8, max_iter=300) from a seeded N(0,1) rhs: the solve
+    tools/ref_cpu.py times with the reference (tests/test_gpu_fullsize.py checks its iteration count
+    and solution against the reference's own).  Device time with CUDA events, 1 GPU."""
+    from paper_2311_17500_b200.spaces import greville
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(3, 128) for _ in range(2)], mb.SplineSpace.uniform(3, 256))
+    theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
+    stab = mb.Stabilization(st, theta, 0.1, 1.0)
+    op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-3, RM, stabilization=stab, device=dev.index)
+    P = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, 1e-3, RM["a"] * RM["c1"], context=op.ctx)
+    b = torch.from_numpy(np.random.default_rng(2).standard_normal(st.num_dof)).to(dev)
+    mb.gmres(op, b, precond=P, tol=1e-2, max_iter=5)      # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    xs, it, hist = mb.gmres(op, b, precond=P, tol=1e-8, max_iter=300)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    out = {"config": "cfg2 sweep-1 system 2D p=3 128^2x256 (N=%d), SU rank %d, rhs N(0,1) seed 2" % (st.num_dof,
+                                                                                                   stab.rank),
+           "seconds": e0.elapsed_time(e1) * 1e-3, "iterations": it, "final_rel_residual": hist[-1], "n_gpus": 1}
     op.ctx.close()
     return out
 
@@ -317,10 +421,13 @@ def run_sharded(args):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     dom = max(prof, key=lambda k: prof[k][0])
     nsten = (2 * p + 1) ** d
-    F_dom = 2.0 * sop.backend.op.nchan * nsten * L.n_own if dom == "op_stencil" else None
-    peak64 = fp64_peak_tflops(torch, dev)
+    # algorithmic flops of the stencil kernel: SU ranks x 2 (2p+1)^d + the 8 banded spatial mode
+    # products of the separable terms (the kernel executes the Galerkin channels as stencils)
+    F_dom = (2.0 * stab.rank * nsten + 8 * 2 * (2 * p + 1)) * L.n_own if dom == "op_stencil" else None
+    peak64, peak_det = fp64_peak_tflops(torch, dev)
     roof = {"kernel": dom, "bound": "tensor", "unit": "TFLOP/s", "peak": peak64,
-            "peak_source": "FP64 cuBLAS DGEMM 4096^3 measured live (rank %d)" % rank,
+            "peak_source": "max(cuBLAS DGEMM 8192^3, DMMA microbenchmark) measured live (rank %d)" % rank,
+            "peak_details": peak_det,
             "achieved": (F_dom / (prof[dom][0] / args.steps * 1e-3) / 1e12) if F_dom else None,
             "traffic": None}
     roof["frac"] = roof["achieved"] / peak64 if roof["achieved"] else None
@@ -328,11 +435,9 @@ def run_sharded(args):
         "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded x ~ U[-1,1])",
-        "config": {"workload": CFG["name"], "d": d, "p": p, "mesh": [args.ne] * 3 + [args.ne_t], "dofs": N,
-                   "su_rank": stab.rank,
-                   "parallelism": "z-sharded x%d (p-plane halo + 2 all-to-all per step)" % world,
-                   "planes_per_rank": L.nz, "setup_s": t_setup, "backend": backend,
-                   "l2": "inputs > 126 MB L2 per rank (no flush needed)"},
+        "config": workload_config(world),
+        "sharding": {"planes_per_rank": L.nz, "exchange": "p-plane halo + 2 all-to-all per step",
+                     "backend": backend, "setup_s": t_setup},
         "e2e": {"value": N * e2s / (float(te.item()) * 1e-3), "unit": "DoF/s",
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                 "path": "ShardedOperator + ShardedPreconditioner from pinned host slabs (all ranks)"},
@@ -408,7 +513,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize(dev)
-    peak64 = fp64_peak_tflops(torch, dev)
+    peak64, peak_det = fp64_peak_tflops(torch, dev)
     ctx.read_profile(reset=True)
     ctx.profiling(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -466,8 +571,8 @@ def run_ours(args):
 
     serial(1)
     pipelined(2)
-    e2_serial = timed(serial, max(1, min(args.steps, 5)))
-    e2e_value = timed(pipelined, args.steps)
+    e2e_value = timed(serial, args.steps)
+    e2_streamed = timed(pipelined, args.steps)
     del pipe
     y = torch.empty_like(x)
     z = torch.empty_like(x)
@@ -476,25 +581,36 @@ def run_ours(args):
     dom = max(prof, key=lambda k: prof[k][0])
     dom_ms = prof[dom][0] / args.steps
     nsten = (2 * p + 1) ** d
-    F_dom = {"op_stencil": 2.0 * op.nchan * nsten * N,
+    R = stab.rank
+    # algorithmic flops per DoF: the stencil kernel does the spatial part of every channel:
+    # R SU stencils (2 (2p+1)^d each) + the 8 banded spatial mode products of the separable terms; it
+    # EXECUTES the two Galerkin channels as full stencils too (they fill the DMMA N = 8 tile)
+    F_alg = {"op_stencil": (2.0 * R * nsten + 8 * 2 * (2 * p + 1)) * N,
              "pc_spatial": 2.0 * 2 * sum(n for n in ctx.n) * N,
-             "pc_time": 2.0 * 2 * ctx.nt * N,
+             "pc_time": (4.0 * ctx.nt + 20) * N,
              "pc_arrowhead": 20.0 * N}.get(dom)
+    F_exec = 2.0 * op.nchan * nsten * N if dom == "op_stencil" else F_alg
     peaks = measured_peaks()
     roof = {"kernel": dom, "bound": "tensor", "unit": "TFLOP/s", "peak": peak64,
-            "peak_source": "FP64 cuBLAS DGEMM 4096^3 measured live in this run (FP64 DMMA/DFMA pipes)",
-            "achieved": (F_dom / (dom_ms * 1e-3) / 1e12) if F_dom else None,
-            "flops_per_step": F_dom, "ms_per_step": dom_ms, "traffic": None}
+            "peak_source": "max(cuBLAS DGEMM 8192^3 best of 10, DMMA m8n8k4 microbenchmark) measured live in this "
+                           "run (MEASURED_PEAKS.json has no FP64 entry)",
+            "peak_details": peak_det,
+            "achieved": (F_alg / (dom_ms * 1e-3) / 1e12) if F_alg else None,
+            "flops_per_step": F_alg, "flops_basis": "algorithmic (SURVEY 8d)", "ms_per_step": dom_ms,
+            "executed_flops_per_step": F_exec,
+            "executed_tflops": (F_exec / (dom_ms * 1e-3) / 1e12) if F_exec else None, "traffic": None}
     roof["frac"] = roof["achieved"] / peak64 if roof["achieved"] else None
-    try:  # DRAM traffic of the same kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_stencil_ncu.json")) as fh:
-            cap = json.load(fh)
-        if dom == "op_stencil" and str(N) in cap["command"].replace(",", ""):
-            roof["traffic"] = cap["traffic_bytes"]
-            roof["traffic_source"] = "profiles/r01_stencil_ncu.json (dram__bytes_read.sum + dram__bytes_write.sum)"
-    except Exception:
-        pass
-    R = stab.rank
+    roof["executed_frac"] = roof["executed_tflops"] / peak64 if roof["executed_tflops"] else None
+    for cap_name in ("r02_stencil_ncu.json", "r01_stencil_ncu.json"):
+        try:  # DRAM traffic of the same kernel from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", cap_name)) as fh:
+                cap = json.load(fh)
+            if dom == "op_stencil" and str(N) in cap["command"].replace(",", ""):
+                roof["traffic"] = cap["traffic_bytes"]
+                roof["traffic_source"] = "profiles/%s (dram__bytes_read.sum + dram__bytes_write.sum)" % cap_name
+                break
+        except Exception:
+            pass
     F_sep = 10 * 2 * (2 * p + 1)
     F_su = R * (2 * (2 * p + 1) + 2 * nsten)
     F_pc = 4 * ctx.nt + 4 * sum(ctx.n) + 40
@@ -509,54 +625,65 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded x ~ U[-1,1])",
-        "config": {"workload": CFG["name"], "d": d, "p": p, "mesh": [args.ne] * 3 + [args.ne_t], "dofs": N,
-                   "su_rank": R, "channels": op.nchan, "reaction": "zero-iterate a*c1 M_t x M_s",
-                   "l2": "inputs 1.5 GB > 126 MB L2 (no flush needed)",
-                   "parallelism": "replicas" if world > 1 else "single GPU", "setup_s": t_setup},
+        "config": workload_config(world),
+        "channels": op.nchan, "setup_s": t_setup,
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
-                "path": "ApplyStream(KroneckerOperator, FastDiagPreconditioner): pinned host x_k -> device -> "
-                        "A, P^-1 -> pinned host z_k, copy-in / apply / copy-out on three streams",
-                "serial_value": e2_serial,
-                "serial_path": "KroneckerOperator.matvec + FastDiagPreconditioner.apply per call, one stream"},
+                "path": "the reference-facing calls KroneckerOperator.matvec + FastDiagPreconditioner.apply per "
+                        "vector (each step: pinned host x -> device, A, P^-1, device -> pinned host z; one "
+                        "stream, dependent like a GMRES iteration)",
+                "streamed_value": e2_streamed,
+                "streamed_path": "ApplyStream over independent vectors: copy-in of k+1 / apply of k / copy-out "
+                                 "of k-1 on three streams (not usable inside one GMRES solve)"},
         "roofline": roof,
         "apply_roofline": apply_roof,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    # ---- variant B: the same apply at a general iterate (reaction mass M_R with the
-    #      Rogers-McCulloch linearisation at q=p+1 Gauss points), u ~ U[0,1], w ~ U[0,0.1]
+    del op, P, x, y, z, xhs, zhs
+    ctx.close()
+    torch.cuda.empty_cache()
+    # ---- variant B: the apply at a general iterate, on an operator built there as the reference's
+    #      _Workspace.operator does (solver.py:219-236: the M_R correction replaces the a*c1 term),
+    #      u ~ U[0,1], w ~ U[0,0.1] (seed 1)
     extras = not args.skip_extras and world == 1
     if extras:
         rng = np.random.default_rng(1)
         u = torch.from_numpy(rng.uniform(0, 1, N)).to(dev)
         w = torch.from_numpy(rng.uniform(0, 0.1, N)).to(dev)
-        from paper_2311_17500_b200.reaction import set_reaction
-        set_reaction(ctx, st, 1.0, RM, u, w, None)
+        opb = mb.KroneckerOperator(st, 1.0, 1.0, CFG["sigma"], RM, u=u, w=w, stabilization=stab, device=local)
+        Pb = mb.FastDiagPreconditioner.build(st, 1.0, 1.0, CFG["sigma"], RM["a"] * RM["c1"], context=opb.ctx)
         del u, w
+        x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).to(dev)
+        y = torch.empty_like(x)
+        z = torch.empty_like(x)
+        cb = opb.ctx
         for _ in range(2):
-            step()
+            opb.apply_device(x, y)
+            Pb.apply_device(y, z)
         torch.cuda.synchronize(dev)
-        ctx.read_profile(reset=True)
-        ctx.profiling(True)
+        cb.read_profile(reset=True)
+        cb.profiling(True)
         e0.record()
         nb = 3
         for _ in range(nb):
-            step()
+            opb.apply_device(x, y)
+            Pb.apply_device(y, z)
         e1.record()
         torch.cuda.synchronize(dev)
-        pb = ctx.read_profile(reset=True)
-        ctx.profiling(False)
-        _lib_clear(ctx)
+        pb = cb.read_profile(reset=True)
+        cb.profiling(False)
         line["variant_b"] = {"value": N * nb / (e0.elapsed_time(e1) * 1e-3), "unit": "DoF/s",
                              "ms_per_step": e0.elapsed_time(e1) / nb,
                              "kernel_ms_per_step": {k: v[0] / nb for k, v in pb.items() if v[1]},
-                             "note": "A x with M_R at u~U[0,1], w~U[0,0.1] (seed 1), then P^-1"}
-    del op, P, x, y, z, xhs, zhs
-    ctx.close()
-    torch.cuda.empty_cache()
+                             "note": "P^-1 A x with A built at u~U[0,1], w~U[0,0.1] (seed 1): Galerkin + SU + M_R "
+                                     "(q=p+1 Gauss, Rogers-McCulloch linearisation), no a*c1 term"}
+        del opb, Pb, x, y, z
+        cb.close()
+        torch.cuda.empty_cache()
     if extras:
         line["solve"] = measure_solve(torch, mb, dev)
+        line["gmres_cfg2"] = measure_gmres_cfg2(torch, mb, dev)
         line["fixed_point_cfg1"] = measure_fixed_point_cfg1(torch, mb, dev)
         # full relaxed fixed-point solves (SU every sweep, GMRES rtol 1e-8) on BASELINE cfgs 2 and 3:
         # BASELINE's "solve time" at 1 GPU (source-pulse stimulus stand-ins)
@@ -586,9 +713,12 @@ def run_ours(args):
             line["mapped_cfg5"] = {"error": repr(exc)[:300]}
         torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, sec, sample, _ = cpu_sample_rate(3, 1, SAMPLE["ne"], SAMPLE["ne_t"])
-        line["cpu_baseline"] = {"value": rate, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",
+        rate, sec, sample, _, kind = cpu_sample_rate(3, 1, SAMPLE["ne"], SAMPLE["ne_t"])
+        line["cpu_baseline"] = {"value": rate, "unit": "DoF/s", "cores": os.cpu_count(), "kind": kind,
                                 "sample": sample}
+        full = reference_full_size()
+        if full is not None:
+            line["reference_full_size"] = full
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -33,6 +33,11 @@ typedef struct mi_ctx mi_ctx;
 int mi_version(void);
 const char* mi_last_error(void);
 
+/* Measurement diagnostic (no reference counterpart): FP64 throughput on `device` of a DMMA-only
+ * (kind 0, mma.sync m8n8k4 f64), DFMA-only (kind 1) or mixed DMMA+DFMA (kind 2) kernel, 8 blocks of
+ * 256 threads per SM.  bench.py takes max(cuBLAS DGEMM, kind 0) as the FP64 tensor peak. */
+int mi_diag_fp64_peak(int device, int kind, double* tflops, double* ms);
+
 /* Context for one space-time tensor shape on one device.
  * Replaces the dimension bookkeeping of SpaceTimeSpace (bspline.py:311-420):
  * d spatial directions with n[0..d-1] = n_1..n_d functions, N_t = nt

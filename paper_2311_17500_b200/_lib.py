@@ -20,6 +20,7 @@ _ip = ctypes.POINTER(ctypes.c_int)
 _SIGS = {
     "mi_version": ([], _c_int),
     "mi_last_error": ([], ctypes.c_char_p),
+    "mi_diag_fp64_peak": ([_c_int, _c_int, _vp, _vp], _c_int),
     "mi_ctx_create": ([_c_int, _c_int, _vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
     "mi_ctx_destroy": ([_vp], _c_int),
     "mi_ctx_set_stream": ([_vp, _vp], _c_int),

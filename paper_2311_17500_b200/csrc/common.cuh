@@ -51,6 +51,15 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// Makes the context's device current for one C-ABI call and restores the caller's device on return
+// (every mi_* entry point that takes a context opens with MI_DEVICE_GUARD).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+#define MI_DEVICE_GUARD(ctx) ::mi::DeviceGuard _mi_dev_guard((ctx) ? (ctx)->device : -1)
+
 struct DeviceBuf {
   double* p = nullptr;
   size_t n = 0;

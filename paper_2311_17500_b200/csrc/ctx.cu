@@ -64,17 +64,30 @@ ProfScope::~ProfScope() {
   }
 }
 
+DeviceGuard::DeviceGuard(int dev) {
+  if (dev < 0) return;
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  if (cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+}
+
+DeviceGuard::~DeviceGuard() {
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
 }  // namespace mi
 
 extern "C" {
 
 int mi_prof_enable(mi_ctx* c, int on) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   c->prof_on = on != 0;
   return MI_OK;
 }
 
 int mi_prof_read(mi_ctx* c, double* ms, long long* launches, int reset) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   MI_CUDA(cudaStreamSynchronize(c->stream));
   for (auto& r : c->prof_events) {
@@ -106,7 +119,10 @@ int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx
   MI_REQUIRE(p >= 1 && p <= MI_MAX_P, MI_ERR_ARG, "spatial degree must be in [1, 4]");
   MI_REQUIRE(pt >= 1 && pt <= MI_MAX_P, MI_ERR_ARG, "time degree must be in [1, 4]");
   MI_REQUIRE(nt >= 2, MI_ERR_ARG, "N_t must be >= 2");
-  MI_CUDA(cudaSetDevice(device));
+  int ndev = 0;
+  MI_CUDA(cudaGetDeviceCount(&ndev));
+  MI_REQUIRE(device >= 0 && device < ndev, MI_ERR_ARG, "device ordinal out of range");
+  mi::DeviceGuard guard(device);
   mi_ctx* c = new mi_ctx();
   c->device = device;
   c->d = d;
@@ -141,6 +157,7 @@ int mi_ctx_create(int device, int d, const int* n, int nt, int p, int pt, mi_ctx
 }
 
 int mi_ctx_set_zslab(mi_ctx* c, int z_lo, int n3g, int hz_lo, int hz_hi) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   MI_REQUIRE(!c->op_ready, MI_ERR_STATE, "mi_ctx_set_zslab must precede mi_op_setup");
   MI_REQUIRE(c->d == 3, MI_ERR_ARG, "z-slab contexts need d = 3");
@@ -157,8 +174,8 @@ int mi_ctx_set_zslab(mi_ctx* c, int z_lo, int n3g, int hz_lo, int hz_hi) {
 }
 
 int mi_ctx_destroy(mi_ctx* c) {
+  MI_DEVICE_GUARD(c);
   if (!c) return MI_OK;
-  cudaSetDevice(c->device);
   mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->frag, &c->xt, &c->afr, &c->u_it, &c->w_it, &c->rx_B,
                            &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
                            &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->tq_frag, &c->y_in, &c->rx_jw, &c->rx_cw,
@@ -186,6 +203,7 @@ int mi_ctx_destroy(mi_ctx* c) {
 }
 
 int mi_ctx_set_stream(mi_ctx* c, void* stream) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   c->stream = static_cast<cudaStream_t>(stream);
   return MI_OK;

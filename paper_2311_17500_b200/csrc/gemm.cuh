@@ -110,7 +110,7 @@ static __global__ void __launch_bounds__(256) dgemm_dmma(GemmArgs g) {
 
 // Launch helper: returns cudaError_t of the launch.
 static inline cudaError_t launch_dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
-  static bool attr = false;
+  MI_DEV_FLAG(attr);
   if (!attr) {
     cudaFuncSetAttribute(dgemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
     attr = true;
@@ -210,7 +210,7 @@ inline cudaError_t launch_panel(const GemmArgs& g, int batch, cudaStream_t st) {
   constexpr int BN = ALONG_N ? 64 : 8 * TILES;
   constexpr int BLD = BN + ((BN % 16 == 0) ? 4 : (BN % 16 == 8 ? 12 : 4));
   constexpr int SM = 2 * (BM * (KC + 8) + KC * BLD) * 8;
-  static bool attr = false;
+  MI_DEV_FLAG(attr);
   if (!attr) {
     cudaFuncSetAttribute(dgemm_panel<TILES, ALONG_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
     attr = true;

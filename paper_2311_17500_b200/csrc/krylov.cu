@@ -100,6 +100,7 @@ using namespace mi;
 extern "C" {
 
 int mi_dots(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* w, double* h) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_dots");
   if (k == 0) return MI_OK;
   int rc;
@@ -115,6 +116,7 @@ int mi_dots(mi_ctx* c, long long n, int k, const double* V, long long ldv, const
 }
 
 int mi_sub_combination(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* h, double* w) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_sub_combination");
   if (k == 0) return MI_OK;
   ProfScope ps(c, PROF_KRYLOV);
@@ -125,6 +127,7 @@ int mi_sub_combination(mi_ctx* c, long long n, int k, const double* V, long long
 
 int mi_combination(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* y,
                    const double* x0, double* out) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_combination");
   ProfScope ps(c, PROF_KRYLOV);
   comb<<<grid_for(n), 256, sizeof(double) * (k > 0 ? k : 1), c->stream>>>(V, ldv, y, k, x0, out, n);
@@ -133,6 +136,7 @@ int mi_combination(mi_ctx* c, long long n, int k, const double* V, long long ldv
 }
 
 int mi_scale_inv(mi_ctx* c, long long n, const double* x, const double* hnorm, double* out) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   ProfScope ps(c, PROF_KRYLOV);
   scale_div<<<grid_for(n), 256, 0, c->stream>>>(x, hnorm, out, n, 0);
@@ -141,6 +145,7 @@ int mi_scale_inv(mi_ctx* c, long long n, const double* x, const double* hnorm, d
 }
 
 int mi_normalize(mi_ctx* c, long long n, const double* x, const double* nrm2, double* out) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   ProfScope ps(c, PROF_KRYLOV);
   scale_div<<<grid_for(n), 256, 0, c->stream>>>(x, nrm2, out, n, 1);
@@ -150,6 +155,7 @@ int mi_normalize(mi_ctx* c, long long n, const double* x, const double* nrm2, do
 
 int mi_cgs_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* h_in, double* w,
                 double* h_out) {
+  MI_DEVICE_GUARD(c);
   int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
   if (rc) return rc;
   return mi_dots(c, n, k, V, ldv, w, h_out);

@@ -249,7 +249,7 @@ inline bool launch_mode_fold(const double* U, const double* in, double* out, int
   if (hs <= 8 * THV && n <= ModeFold<THV>::KP) {                                                         \
     constexpr size_t sm = ROWS ? ModeFold<THV>::SMEM_ROWS : ModeFold<THV>::SMEM_COLS;                    \
     constexpr int nth = ModeFold<THV>::NTH;                                                              \
-    static bool attr = false;                                                                            \
+    MI_DEV_FLAG(attr);                                                                            \
     if (!attr) {                                                                                         \
       cudaFuncSetAttribute(mode_fold<THV, ROWS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
       cudaFuncSetAttribute(mode_fold<THV, ROWS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \

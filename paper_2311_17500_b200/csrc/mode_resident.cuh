@@ -175,7 +175,7 @@ inline bool launch_mode_resident(const double* A, const double* in, double* out,
 #define MI_MR(TNV)                                                                                       \
   if (n <= 8 * TNV) {                                                                                    \
     constexpr size_t sm = ROWS ? ModeRes<TNV>::SMEM_ROWS : ModeRes<TNV>::SMEM_COLS;                      \
-    static bool attr = false;                                                                            \
+    MI_DEV_FLAG(attr);                                                                            \
     if (!attr) {                                                                                         \
       cudaFuncSetAttribute(mode_resident<TNV, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
       attr = true;                                                                                       \

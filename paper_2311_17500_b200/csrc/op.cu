@@ -374,9 +374,9 @@ using namespace mi;
 extern "C" {
 
 int mi_op_setup(mi_ctx* c, int nchan) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   MI_REQUIRE(nchan >= 1 && nchan <= MI_MAX_CHAN, MI_ERR_ARG, "nchan must be in [1, 64]");
-  MI_CUDA(cudaSetDevice(c->device));
   c->nchan = nchan;
   int rc;
   if ((rc = dalloc(c->tband, (size_t)nchan * c->nt * (2 * c->pt + 1)))) return rc;
@@ -393,6 +393,7 @@ int mi_op_setup(mi_ctx* c, int nchan) {
 }
 
 int mi_op_set_time_bands(mi_ctx* c, const double* bands) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_CUDA(cudaMemcpyAsync(c->tband.p, bands, sizeof(double) * c->nchan * c->nt * (2 * c->pt + 1),
                           cudaMemcpyHostToDevice, c->stream));
@@ -402,6 +403,7 @@ int mi_op_set_time_bands(mi_ctx* c, const double* bands) {
 }
 
 int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* bands) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(nterms >= 1, MI_ERR_ARG, "nterms must be >= 1");
@@ -425,6 +427,7 @@ int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
 }
 
 int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H, int ko) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(ko >= 0 && ko <= 8, MI_ERR_ARG, "ko out of range");
@@ -519,15 +522,18 @@ static int quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const
 
 int mi_op_set_quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta,
                            const double* T, const int* q, const int* Q) {
+  MI_DEVICE_GUARD(c);
   return quad_channel(c, ch, nterms, coef, theta, T, q, nullptr, nullptr, Q);
 }
 
 int mi_op_set_quad_channel_k(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta,
                              const double* T, const int* kstart, const int* kw, const int* Q) {
+  MI_DEVICE_GUARD(c);
   return quad_channel(c, ch, nterms, coef, theta, T, nullptr, kstart, kw, Q);
 }
 
 int mi_op_set_channel_stencil(mi_ctx* c, int ch, const double* sten) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan && sten != nullptr, MI_ERR_ARG, "channel out of range");
   MI_CUDA(cudaMemcpyAsync(c->stencil.p + (size_t)ch * c->nsten * c->ns, sten, sizeof(double) * c->nsten * c->ns,
@@ -537,6 +543,7 @@ int mi_op_set_channel_stencil(mi_ctx* c, int ch, const double* sten) {
 }
 
 int mi_op_get_channel_stencil(mi_ctx* c, int ch, double* sten) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(ch >= 0 && ch < c->nchan && sten != nullptr, MI_ERR_ARG, "channel out of range");
   MI_CUDA(cudaMemcpyAsync(sten, c->stencil.p + (size_t)ch * c->nsten * c->ns, sizeof(double) * c->nsten * c->ns,
@@ -617,19 +624,13 @@ static int launch_time_filter(mi_ctx* c, double* y) {
   const bool frag = MI_TF_FRAG && TFilterCfg::smem(c->pt, c->nchan, true) <= 232448;
   if (TFilterCfg::smem(c->pt, c->nchan, frag) <= 232448 && c->pt <= TFilterCfg::PX) {
     // tensor-core filter: persistent blocks, one time block of 56 rows each
-    static int nsm = 0;
-    if (nsm == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      if (nsm <= 0) nsm = 148;
-    }
+    const int nsm = mi::num_sms();
     const int ntb = (c->nt + TFilterCfg::TR - 1) / TFilterCfg::TR;
     const int grid = ntb * std::max(1, nsm / ntb);
     const size_t sm = TFilterCfg::smem(c->pt, c->nchan, frag);
 #define MI_TFD(PTV)                                                                                            \
   case PTV: {                                                                                                  \
-    static bool attr = false;                                                                                  \
+    MI_DEV_FLAG(attr);                                                                                  \
     if (!attr) {                                                                                               \
       MI_CUDA(cudaFuncSetAttribute(time_filter_dmma<PTV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448)); \
       MI_CUDA(cudaFuncSetAttribute(time_filter_dmma<PTV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448)); \
@@ -703,6 +704,7 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
 }
 
 int mi_op_apply(mi_ctx* c, const double* x, double* y) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
   MI_REQUIRE(x != y, MI_ERR_ARG, "x and y must not alias");
   if (c->use_dmma) {

@@ -72,16 +72,7 @@ __global__ void arrowhead_solve(double* __restrict__ Y, const double* __restrict
   Y[(long long)m * ns + s] = xl;
 }
 
-static int num_sms() {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
-  return nsm;
-}
+using mi::num_sms;
 
 static cudaError_t mode_strided(const double* A, const double* in, double* out, int n, long long inner,
                                 long long outer, cudaStream_t st) {
@@ -143,8 +134,8 @@ extern "C" {
 int mi_pc_setup(mi_ctx* c, const double* U, const double* lam, double cm, double react, const double* Q,
                 const double* diag, const double* off, const int* partner, const double* g,
                 const double* glow, double sigma) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
-  MI_CUDA(cudaSetDevice(c->device));
   const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
   int rc;
   for (int l = 0; l < 3; ++l) {
@@ -286,6 +277,7 @@ using namespace mi;
 extern "C" {
 
 int mi_pc_apply(mi_ctx* c, const double* r, double* z) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   int rc;
   // forward spatial into pc_t1 (scratch t2 used internally), time stage in place, inverse into z
@@ -296,6 +288,7 @@ int mi_pc_apply(mi_ctx* c, const double* r, double* z) {
 }
 
 int mi_pc_apply_spatial(mi_ctx* c, const double* in, double* out, long long nrows, int inverse) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   MI_REQUIRE(nrows >= 1 && nrows <= c->nt, MI_ERR_ARG, "nrows out of range");
   MI_REQUIRE(in != out, MI_ERR_ARG, "in and out must not alias");
@@ -303,12 +296,14 @@ int mi_pc_apply_spatial(mi_ctx* c, const double* in, double* out, long long nrow
 }
 
 int mi_pc_apply_time(mi_ctx* c, double* y, long long ncols, long long col0) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   MI_REQUIRE(ncols >= 1 && col0 >= 0 && col0 + ncols <= c->ns, MI_ERR_ARG, "column range out of range");
   return pc_time(c, y, ncols, col0);
 }
 
 int mi_pc_apply_time_yslab(mi_ctx* c, double* y, int y_lo, int y_hi) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   MI_REQUIRE(c->d == 3 && 0 <= y_lo && y_lo < y_hi && y_hi <= c->n[1], MI_ERR_ARG, "y range out of range");
   const long long ncols = (long long)c->n[0] * (y_hi - y_lo) * c->n[2];
@@ -316,11 +311,13 @@ int mi_pc_apply_time_yslab(mi_ctx* c, double* y, int y_lo, int y_hi) {
 }
 
 int mi_pc_fold(mi_ctx* c, int l) {
+  MI_DEVICE_GUARD(c);
   if (c == nullptr || !c->pc_ready || l < 0 || l > 2) return 0;
   return c->fold_hs[l];
 }
 
 int mi_pc_mode(mi_ctx* c, int l, int inverse, const double* in, double* out, long long outer, long long inner) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
   MI_REQUIRE(l >= 0 && l < c->d, MI_ERR_ARG, "direction out of range");
   MI_REQUIRE(outer >= 1 && inner >= 1 && in != out, MI_ERR_ARG, "bad mode-product shape or aliasing");

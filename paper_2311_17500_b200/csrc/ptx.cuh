@@ -4,6 +4,28 @@
 
 namespace mi {
 
+// ---- per-device host caches (one process may drive several GPUs: ADVICE r01)
+constexpr int MAX_DEV = 64;
+inline int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= MAX_DEV ? 0 : d;
+}
+inline int num_sms() {
+  static int cache[MAX_DEV] = {};
+  const int d = cur_dev();
+  if (cache[d] <= 0) {
+    cudaDeviceGetAttribute(&cache[d], cudaDevAttrMultiProcessorCount, d);
+    if (cache[d] <= 0) cache[d] = 148;
+  }
+  return cache[d];
+}
+// `name` is a bool& flag private to the enclosing function (or template instance) and the current device:
+// kernel attributes such as the dynamic shared-memory limit are per device.
+#define MI_DEV_FLAG(name)                                     \
+  static bool name##_per_dev[::mi::MAX_DEV] = {};             \
+  bool& name = name##_per_dev[::mi::cur_dev()]
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int n = valid ? 8 : 0;

@@ -534,7 +534,7 @@ static int reaction_launch(mi_ctx* c, RxArgs r) {
   MI_RX_DISPATCH(c->d, c->p, c->pt, {
     using G = RxTile<D_, P_>;
     constexpr size_t smem = G::SMEM;
-    static bool attr = false;
+    MI_DEV_FLAG(attr);
     if (!attr) {
       MI_CUDA(cudaFuncSetAttribute(reaction_tile<D_, P_, PT_, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
@@ -648,6 +648,7 @@ extern "C" {
 
 int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, double a, double c2,
                        const int* q, const int* nel, const double* B, const double* Wq) {
+  MI_DEVICE_GUARD(c);
   if (c) c->rx_mapped = false;    // a mapped weight is re-attached by mi_op_set_reaction_weight
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_REQUIRE(u && w && q && nel && B && Wq, MI_ERR_ARG, "NULL argument to mi_op_set_reaction");
@@ -698,6 +699,7 @@ int mi_op_set_reaction(mi_ctx* c, const double* u, const double* w, double c1, d
 }
 
 int mi_op_set_reaction_weight(mi_ctx* c, const double* jw) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   if (jw == nullptr) {
     c->rx_mapped = false;
@@ -715,6 +717,7 @@ int mi_op_set_reaction_weight(mi_ctx* c, const double* jw) {
 }
 
 int mi_op_set_reaction_store(mi_ctx* c, int mode) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   MI_REQUIRE(mode >= -1 && mode <= 1, MI_ERR_ARG, "store mode must be -1, 0 or 1");
   c->rx_store_mode = mode;
@@ -723,6 +726,7 @@ int mi_op_set_reaction_store(mi_ctx* c, int mode) {
 }
 
 int mi_op_set_reaction_rows(mi_ctx* c, int row_offset) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   c->rx_rowoff = row_offset;
   c->rx_cw_dirty = true;
@@ -730,6 +734,7 @@ int mi_op_set_reaction_rows(mi_ctx* c, int row_offset) {
 }
 
 int mi_op_clear_reaction(mi_ctx* c) {
+  MI_DEVICE_GUARD(c);
   if (c) c->reaction_on = false;
   return MI_OK;
 }

@@ -407,10 +407,10 @@ extern "C" {
 
 int mi_theta_setup(mi_ctx* c, const int* nel, const double* B0, const double* B1, const double* lengths,
                    const double* diffusion, double final_time, double C_m, double c1, double a, double c2) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && nel && B0 && B1 && lengths && diffusion, MI_ERR_ARG, "NULL argument to mi_theta_setup");
   MI_REQUIRE(final_time > 0.0, MI_ERR_ARG, "final time must be positive");
   MI_REQUIRE(c->p == c->pt && c->p <= 3, MI_ERR_ARG, "residual indicator: need p = p_t <= 3");
-  MI_CUDA(cudaSetDevice(c->device));
   size_t tot = 0;
   for (int l = 0; l < 4; ++l) {
     const bool present = l == 3 || l < c->d;
@@ -447,6 +447,7 @@ int mi_theta_setup(mi_ctx* c, const int* nel, const double* B0, const double* B1
 
 int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double* src, int et0, int et1,
                       double* emax, double* maxes) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->th_ready, MI_ERR_STATE, "mi_theta_setup must be called first");
   MI_REQUIRE(u && w && emax && maxes, MI_ERR_ARG, "NULL argument to mi_theta_elements");
   MI_REQUIRE(0 <= et0 && et0 <= et1 && et1 <= c->th_nel[3], MI_ERR_ARG, "time element range out of bounds");
@@ -482,7 +483,7 @@ int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double*
   for (int l = 0; l < c->d; ++l) nb *= (c->th_nel[l] + 1) / 2;
   MI_TH_DISPATCH(c->d, c->p, c->pt, {
     using G = ThTile<D_, P_>;
-    static bool attr = false;
+    MI_DEV_FLAG(attr);
     if (!attr) {
       MI_CUDA(cudaFuncSetAttribute(theta_elements<D_, P_, PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)G::SMEM));
@@ -497,6 +498,7 @@ int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double*
 int mi_theta_mapped_elements(mi_ctx* c, const double* fields, const double* coef, const double* src, int et0,
                              int et1, const int* G, int q, int qt, const int* nel, double D, double cmT, double c1,
                              double a, double c2, double* emax, double* maxes) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && fields && coef && G && nel && emax && maxes, MI_ERR_ARG, "NULL argument to mi_theta_mapped_elements");
   MI_REQUIRE(0 <= et0 && et0 <= et1 && q >= 1 && qt >= 1, MI_ERR_ARG, "bad element range or rule");
   if (et0 == et1) return MI_OK;
@@ -521,6 +523,7 @@ int mi_theta_mapped_elements(mi_ctx* c, const double* fields, const double* coef
 
 int mi_window_max(mi_ctx* c, const double* in, double* out, long long outer, int n_in, int n_out, long long inner,
                   const int* w0, const int* w1) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && in && out && w0 && w1 && in != out, MI_ERR_ARG, "bad arguments to mi_window_max");
   MI_REQUIRE(outer >= 0 && n_in > 0 && n_out >= 0 && inner >= 0, MI_ERR_ARG, "bad shape in mi_window_max");
   for (int i = 0; i < n_out; ++i)
@@ -544,6 +547,7 @@ int mi_window_max(mi_ctx* c, const double* in, double* out, long long outer, int
 }
 
 int mi_theta_ratio(mi_ctx* c, const double* numer, double* theta, long long n, double denom) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && numer && theta && n >= 0, MI_ERR_ARG, "bad arguments to mi_theta_ratio");
   MI_REQUIRE(denom > 0.0, MI_ERR_ARG, "denominator must be positive");
   if (n == 0) return MI_OK;

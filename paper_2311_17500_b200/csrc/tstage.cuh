@@ -256,7 +256,7 @@ template <int MB, int NC, int WM>
 inline cudaError_t launch_tstage_t(const TStageArgs& a, cudaStream_t st) {
   using G = TStage<MB, NC, WM>;
   static_assert(G::SMEM <= 232448, "tile does not fit in shared memory");
-  static bool attr = false;
+  MI_DEV_FLAG(attr);
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(time_stage_fused<MB, NC, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)G::SMEM);

@@ -99,8 +99,8 @@ using namespace mi;
 extern "C" {
 
 int mi_ws_setup(mi_ctx* c, const double* Kinv, const double* Mmat, const double* Minv) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
-  MI_CUDA(cudaSetDevice(c->device));
   const int nmax = max(c->n[0], max(c->n[1], c->n[2]));
   int rc;
   if ((rc = dalloc(c->ws_Kinv, (size_t)c->nt * c->nt))) return rc;
@@ -133,6 +133,7 @@ int mi_ws_setup(mi_ctx* c, const double* Kinv, const double* Mmat, const double*
 
 /* out = (K_t^{-1} (x) I) in */
 int mi_ws_time(mi_ctx* c, const double* in, double* out) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->ws_ready, MI_ERR_STATE, "w-solve not set up");
   MI_REQUIRE(in != out, MI_ERR_ARG, "in and out must not alias");
   GemmArgs g{c->ws_Kinv.p, in, out, c->nt, (int)c->ns, c->nt, c->nt, c->ns, c->ns, 0, 0, 0};
@@ -142,6 +143,7 @@ int mi_ws_time(mi_ctx* c, const double* in, double* out) {
 
 /* out = (I (x) kron_l M_l) in  (inverse != 0: kron_l M_l^{-1}) on nrows time rows */
 int mi_ws_mass(mi_ctx* c, const double* in, double* out, long long nrows, int inverse) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->ws_ready, MI_ERR_STATE, "w-solve not set up");
   MI_REQUIRE(in != out, MI_ERR_ARG, "in and out must not alias");
   double* A[3] = {nullptr, inverse ? c->ws_Mi[1].p : c->ws_M[1].p, inverse ? c->ws_Mi[2].p : c->ws_M[2].p};
@@ -150,6 +152,7 @@ int mi_ws_mass(mi_ctx* c, const double* in, double* out, long long nrows, int in
 
 /* out[r] = <a[r, :], b[r, :]> for r < nrows (device) */
 int mi_rowdots(mi_ctx* c, long long nrows, long long ncols, const double* a, const double* b, double* out) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && nrows >= 0, MI_ERR_ARG, "bad arguments to mi_rowdots");
   if (nrows == 0) return MI_OK;
   rowdots_kernel<<<(unsigned)nrows, 256, 0, c->stream>>>(a, b, out, ncols);
@@ -160,6 +163,7 @@ int mi_rowdots(mi_ctx* c, long long nrows, long long ncols, const double* a, con
 /* y[r, :] += sign * alpha[r] * x[r, :] */
 int mi_row_axpy(mi_ctx* c, long long nrows, long long ncols, const double* alpha, double sign, const double* x,
                 double* y) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   const long long total = nrows * ncols;
   const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
@@ -170,6 +174,7 @@ int mi_row_axpy(mi_ctx* c, long long nrows, long long ncols, const double* alpha
 
 /* p[r, :] = z[r, :] + beta[r] * p[r, :] */
 int mi_row_xpby(mi_ctx* c, long long nrows, long long ncols, const double* beta, const double* z, double* p) {
+  MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   const long long total = nrows * ncols;
   const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);

@@ -69,10 +69,6 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
     n = b.numel()
     red = allreduce if allreduce is not None else (lambda t: None)
     tmp = torch.empty_like(b)
-    scal = torch.zeros(8 + 2 * (m + 1), dtype=torch.float64, device=dev)
-    nrm = scal[0:1]
-    h1 = scal[8:8 + m + 1]
-    h2 = scal[8 + m + 1:8 + 2 * (m + 1)]
     if x0 is None:
         xs = torch.zeros_like(b)
         r = b
@@ -82,9 +78,13 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
         minus = torch.full((1,), -1.0, dtype=torch.float64, device=dev)
         r = torch.empty_like(b)
         ops.comb(tmp.view(1, -1), 1, minus, b, r)
-    # the basis grows on demand (doubling, up to m + 1 vectors): memory follows the iterations used,
-    # not the HBM-sized bound, so later allocations (e.g. the reaction's stored coefficient) still fit
-    V = torch.empty((min(m, 32) + 1, n), dtype=torch.float64, device=dev)
+    # The basis, the Hessenberg matrix and the dot-product scratch grow on demand (doubling, up to m + 1
+    # vectors): memory follows the iterations used, not max_iter, so the reference's default
+    # max_iter = n (linalg.py:381-382) costs nothing up front.  Running out of HBM raises MemoryError.
+    cap = min(m, 32)
+    V = torch.empty((cap + 1, n), dtype=torch.float64, device=dev)
+    scal = torch.zeros(8 + 2 * (cap + 1), dtype=torch.float64, device=dev)
+    nrm = scal[0:1]
     apply_P(r, V[0])
     ops.dots(V[0].view(1, -1), 1, V[0], nrm)
     red(nrm)
@@ -94,17 +94,32 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
             _write_log(log_path, [0.0])
         return xs, 0, [0.0]
     ops.normalize(V[0], nrm, V[0])
-    H = np.zeros((m + 1, m))
-    cs, sn, gv = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+    H = np.zeros((cap + 1, cap))
+    cs, sn, gv = np.zeros(cap), np.zeros(cap), np.zeros(cap + 1)
     gv[0] = beta
     history = [1.0]
     k_done = None
     w = torch.empty_like(b)
     for j in range(m):
         if j + 1 >= V.shape[0]:
-            grown = torch.empty((min(m + 1, 2 * V.shape[0]), n), dtype=torch.float64, device=dev)
+            new_cap = min(m, 2 * cap)
+            try:
+                grown = torch.empty((new_cap + 1, n), dtype=torch.float64, device=dev)
+            except torch.cuda.OutOfMemoryError as exc:
+                raise MemoryError("GMRES basis of %d vectors of %d DoFs does not fit in device memory "
+                                  "(iteration %d; pass a smaller max_iter)" % (new_cap + 1, n, j)) from exc
             grown[:V.shape[0]].copy_(V)
             V = grown
+            Hn = np.zeros((new_cap + 1, new_cap))
+            Hn[:cap + 1, :cap] = H
+            H = Hn
+            cs, sn = np.resize(cs, new_cap), np.resize(sn, new_cap)
+            gv = np.concatenate([gv, np.zeros(new_cap - cap)])
+            scal = torch.zeros(8 + 2 * (new_cap + 1), dtype=torch.float64, device=dev)
+            nrm = scal[0:1]
+            cap = new_cap
+        h1 = scal[8:8 + cap + 1]
+        h2 = scal[8 + cap + 1:8 + 2 * (cap + 1)]
         apply_A(V[j], tmp)
         apply_P(tmp, w)
         k = j + 1
@@ -117,7 +132,7 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
         ops.dots(w.view(1, -1), 1, w, nrm)
         red(nrm)
         host = scal.cpu().numpy()
-        hv = host[8:8 + k] + host[8 + m + 1:8 + m + 1 + k]
+        hv = host[8:8 + k] + host[8 + cap + 1:8 + cap + 1 + k]
         hnorm = float(np.sqrt(host[0]))
         H[:k, j] = hv
         H[k, j] = hnorm
@@ -154,14 +169,6 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
     return xout, k_done, history
 
 
-def default_max_iter(n, device, reserve_vectors=8, fraction=0.6):
-    """Unrestarted GMRES keeps max_iter+1 basis vectors; the reference's
-    default max_iter = n (linalg.py:381-382) is replaced by the HBM bound."""
-    free, _ = torch.cuda.mem_get_info(device)
-    cap = int(fraction * free // (8 * n)) - reserve_vectors
-    return max(1, min(n, cap, 1000))
-
-
 def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None):
     """Returns ``(x, iterations, residual_history)`` like linalg.py:367-447.
 
@@ -181,7 +188,7 @@ def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None
     if n != op.shape[0]:
         raise ValueError("dimension mismatch: operator of size %d applied to vector of size %d"
                          % (op.shape[0], n))
-    m = default_max_iter(n, ctx.device) if max_iter is None else int(max_iter)
+    m = n if max_iter is None else int(max_iter)  # reference default (linalg.py:381-382)
 
     def P(src, dst):
         if precond is None:

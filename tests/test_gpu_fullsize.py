@@ -1,0 +1,196 @@
+"""GPU parity at the BASELINE sizes (cfg 2: N = 4.4 M, cfg 3: 37 M, cfg 4: 188 M).
+
+Two kinds of evidence, both through the C ABI on the full-size vectors the benchmarks use:
+
+1. Reference outputs.  ``tests/golden/make_fullsize.py`` ran the unmodified reference at these sizes
+   (what it can assemble: the whole sweep-1 system with Spline Upwind at cfg 2, the separable system at
+   cfgs 3/4, the FD preconditioner everywhere, and GMRES at cfg 2) and stored size-independent
+   summaries of its output vectors: a sample of entries, the 2-norm of every time row and the dot
+   product of every time row with a seeded probe vector.  The device vectors must reproduce all three
+   to 1e-12 (applies) / 1e-10 (GMRES solution), with equal GMRES iteration counts.
+2. The pinned oracle on sampled rows (``oracle/rows.py``: the reference's own quadratures restricted
+   to one row's support, pinned against the reference's assembled products in
+   tests/test_oracle_golden.py) for what the reference cannot assemble at these sizes: the Spline
+   Upwind terms at cfgs 3/4 and the reaction mass M_R (variant B) at every size, in both the stored
+   and the fused reaction modes.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from cases import GOLDEN
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+RM = {"c1": 0.26, "a": 0.13, "c2": 0.1}
+CFG = {2: dict(d=2, p=3, ne=128, ne_t=256, sigma=1e-3),
+       3: dict(d=3, p=2, ne=64, ne_t=128, sigma=(1e-3, 4e-4, 4e-4)),
+       4: dict(d=3, p=3, ne=96, ne_t=192, sigma=1e-3)}
+NROWS = 1000
+
+
+def fixture(cfg):
+    path = os.path.join(GOLDEN, "fullsize_cfg%d.npz" % cfg)
+    z = np.load(path)
+    return {k: z[k] for k in z.files}
+
+
+def check_summary(g, key, v, tol, probe):
+    """Device vector v (CUDA tensor) vs the reference's summaries of the same vector."""
+    import torch
+    nt = int(g["nt"])
+    V = v.view(nt, -1)
+    vals = v[torch.from_numpy(g["idx"]).to(v.device)].cpu().numpy()
+    ref = g[key + "_val"]
+    assert np.linalg.norm(vals - ref) <= tol * np.linalg.norm(ref), key
+    assert np.abs(vals - ref).max() <= tol * np.abs(ref).max(), key
+    rn = torch.linalg.norm(V, dim=1).cpu().numpy()
+    np.testing.assert_allclose(rn, g[key + "_rownorm"], rtol=tol, atol=0, err_msg=key)
+    P = probe.view(nt, -1)
+    rd = (V * P).sum(dim=1).cpu().numpy()
+    bound = tol * g[key + "_rownorm"] * torch.linalg.norm(P, dim=1).cpu().numpy()
+    assert np.all(np.abs(rd - g[key + "_rowdot"]) <= bound), key
+
+
+class Setup:
+    """Device and oracle objects of one BASELINE config (built once per module)."""
+
+    def __init__(self, cfg):
+        import torch
+        import paper_2311_17500_b200 as mb
+        from oracle import problem as oprob
+        from oracle import stab as ostab
+        from oracle.splines import make_space_time
+        c = CFG[cfg]
+        self.cfg, self.c = cfg, c
+        self.g = fixture(cfg)
+        d, p = c["d"], c["p"]
+        self.st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, c["ne"]) for _ in range(d)],
+                                    mb.SplineSpace.uniform(p, c["ne_t"]))
+        self.N = self.st.num_dof
+        assert self.N == int(self.g["N"])
+        self.ost = make_space_time(d, p, c["ne"], c["ne_t"])
+        self.theta = oprob.front_indicator(self.ost)
+        self.dev = torch.device("cuda", 0)
+        self.x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, self.N)).to(self.dev)
+        self.probe = torch.from_numpy(np.random.default_rng(7).standard_normal(self.N)).to(self.dev)
+        rng = np.random.default_rng(4)
+        self.rows = np.sort(rng.choice(self.g["idx"], NROWS, replace=False))
+        self.mb = mb
+        self.tau = ostab.compute_tau(self.ost.time)
+        self.lr = ostab.lowrank_factorize(ostab.indicator_for(self.ost, self.theta), 0.1)
+
+    def operator(self, su, u=None, w=None):
+        mb = self.mb
+        stab = mb.Stabilization(self.st, self.theta, 0.1, 1.0) if su else None
+        if su:
+            assert stab.rank == self.lr.rank
+        return mb.KroneckerOperator(self.st, 1.0, 1.0, self.c["sigma"], RM, u=u, w=w, stabilization=stab)
+
+    def precond(self, op):
+        return self.mb.FastDiagPreconditioner.build(self.st, 1.0, 1.0, self.c["sigma"], RM["a"] * RM["c1"],
+                                                    context=op.ctx)
+
+    def apply(self, obj, v):
+        import torch
+        out = torch.empty_like(v)
+        obj.apply_device(v, out)
+        return out
+
+    def mass_rows(self, v_host, rows):
+        """(a c1 M_t (x) M_s) v at rows (oracle row form of the Kronecker term)."""
+        from oracle import assembly as asm
+        from oracle import rows as orows
+        _, Mt = asm.time_factors(self.ost, 1.0)
+        Ms = [asm.mass_stiff_adv(s)[0] for s in self.ost.spatial]
+        return orows.kron_rows(self.ost, [(RM["a"] * RM["c1"], Mt, Ms)], v_host, rows)
+
+
+@pytest.fixture(scope="module", params=[2, 3, 4])
+def setup(request):
+    import torch
+    if not os.path.exists(os.path.join(GOLDEN, "fullsize_cfg%d.npz" % request.param)):
+        pytest.skip("fixture not generated")
+    s = Setup(request.param)
+    yield s
+    del s
+    torch.cuda.empty_cache()
+
+
+def test_operator_and_preconditioner_vs_reference(setup):
+    """A x (cfg 2: with the SU terms; cfgs 3/4: separable + zero-iterate reaction), P^-1 x and
+    P^-1 A x against the reference's own full-size outputs."""
+    s = setup
+    op = s.operator(su=(s.cfg == 2))
+    P = s.precond(op)
+    y = s.apply(op, s.x)
+    check_summary(s.g, "y_a", y, 1e-12, s.probe)
+    check_summary(s.g, "z_pc", s.apply(P, s.x), 1e-12, s.probe)
+    check_summary(s.g, "z_pca", s.apply(P, y), 1e-12, s.probe)
+    op.ctx.close()
+
+
+def test_spline_upwind_rows_vs_oracle(setup):
+    """SU terms at the full size on sampled rows: (A_SU - A_sep) x vs oracle/rows.su_rows."""
+    from oracle import rows as orows
+    s = setup
+    if s.cfg == 2:
+        pytest.skip("cfg 2 checks the SU operator against the reference itself")
+    op = s.operator(su=True)
+    y = s.apply(op, s.x)
+    got = y[s.rows].cpu().numpy()
+    op.ctx.close()
+    pos = np.searchsorted(s.g["idx"], s.rows)
+    y_sep = s.g["y_a_val"][pos]
+    ref = orows.su_rows(s.ost, s.tau, s.lr, 1.0, s.x.cpu().numpy(), s.rows)
+    assert np.abs((got - y_sep) - ref).max() <= 1e-12 * np.abs(got).max()
+    assert np.linalg.norm((got - y_sep) - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_reaction_rows_vs_oracle(setup):
+    """Variant B (M_R at u ~ U[0,1], w ~ U[0,0.1], seed 1) on sampled rows, in the stored mode (c_w formed
+    once per build, where it fits: cfgs 2, 3) and the fused mode (C_r formed every apply):
+    A_b x - A_a x + a c1 (M_t (x) M_s) x = M_R x vs oracle/rows.reaction_rows."""
+    import torch
+    from oracle import rows as orows
+    from paper_2311_17500_b200 import _lib
+    s = setup
+    rng = np.random.default_rng(1)
+    u = rng.uniform(0, 1, s.N)
+    w = rng.uniform(0, 0.1, s.N)
+    xh = s.x.cpu().numpy()
+    ref = orows.reaction_rows(s.ost, 1.0, RM, u, w, xh, s.rows) - s.mass_rows(xh, s.rows)
+    op0 = s.operator(su=False)
+    y0 = s.apply(op0, s.x)[s.rows].cpu().numpy()
+    op0.ctx.close()
+    ud, wd = torch.from_numpy(u).to(s.dev), torch.from_numpy(w).to(s.dev)
+    del u, w
+    opb = s.operator(su=False, u=ud, w=wd)
+    del ud, wd
+    modes = [0, 1] if s.cfg in (2, 3) else [0]
+    for mode in modes:
+        _lib.call("mi_op_set_reaction_store", opb.ctx.handle, mode)
+        yb = s.apply(opb, s.x)[s.rows].cpu().numpy()
+        got = yb - y0
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(yb).max(), mode
+        assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(ref), mode
+    opb.ctx.close()
+
+
+def test_gmres_vs_reference(setup):
+    """cfg 2: the sweep-1 system (Galerkin + zero-iterate reaction + SU), gmres(tol=1e-8,
+    max_iter=300) from a seeded N(0,1) rhs: equal iteration count, equal history, x to 1e-10."""
+    import torch
+    s = setup
+    if s.cfg != 2:
+        pytest.skip("the reference's GMRES runs at cfg 2 (dense H and CSR SU beyond)")
+    op = s.operator(su=True)
+    P = s.precond(op)
+    b = torch.from_numpy(np.random.default_rng(2).standard_normal(s.N)).to(s.dev)
+    x, it, hist = s.mb.gmres(op, b, precond=P, tol=1e-8, max_iter=300)
+    assert it == int(s.g["gm_it"])
+    np.testing.assert_allclose(hist, s.g["gm_hist"], rtol=1e-6, atol=1e-14)
+    check_summary(s.g, "gm_x", x, 1e-10, s.probe)
+    op.ctx.close()
