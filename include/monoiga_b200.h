@@ -127,6 +127,22 @@ int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
 int mi_op_set_reaction(mi_ctx* ctx, const double* u, const double* w, double c1, double a, double c2,
                        const int* q, const int* nel, const double* B, const double* Wq);
 int mi_op_clear_reaction(mi_ctx* ctx);
+
+/* u0 lifting (no reference counterpart: the reference's trial space drops the first time function,
+ * bspline.py:384-387, and fields.py:8-12 pads that slab with zeros, so it cannot take u0 != 0; SURVEY
+ * Appendix B).  u = u0_h(x) b_0(t) + u~.  mi_op_set_lift stores the lifting coefficients u0 (device,
+ * N_s of the input slab; NULL clears) and, per channel, the column of the channel's FULL time factor
+ * that couples the constrained rows to b_0 (host, nchan x N_t, nonzero in the first p_t rows only).
+ * While a lift is set the reaction's C_r sees the lifted iterate (the u0 slab is read for b_0).
+ * mi_op_apply_lift writes y = A_{c,0} u0: the lifted column of every channel and of M_R applied to u0
+ * (the sweep's right-hand side correction f - A_{c,0} u0). */
+int mi_op_set_lift(mi_ctx* ctx, const double* column0, const double* u0);
+
+/* Pack the channel stencils into the tensor-core layout now and free the plain stencil copy (the
+ * operator's largest table after the packed one: 21 GB at BASELINE cfg 4).  Afterwards the channels
+ * are immutable until the next mi_op_setup; time bands, the reaction and the lift may still change. */
+int mi_op_finalize(mi_ctx* ctx);
+int mi_op_apply_lift(mi_ctx* ctx, double* y);
 /* Mapped geometry: |det J| at the spatial Gauss points (host, C order
  * Q_d ... Q_1) multiplies the reaction's quadrature weights
  * (reaction_mass with spatial_data, assembly.py:320-326); NULL = box.
@@ -172,6 +188,12 @@ int mi_pc_apply_time(mi_ctx* ctx, double* y, long long ncols, long long col0);
  * (N_t, n_3, y_hi - y_lo, n_1) holding spatial eigen-indices with
  * i_2 in [y_lo, y_hi). */
 int mi_pc_mode(mi_ctx* ctx, int l, int inverse, const double* in, double* out, long long outer, long long inner);
+/* mi_pc_mode along a strided direction (inner >= 2) with addressing maps (device int64, 2 n_l entries
+ * each, nullable): element (o, r, c) of the input / output lives at map[2r] + o * map[2r+1] + c.  Lets
+ * the space-sharded P^-1 read and write the all-to-all send / receive layouts without packing copies.
+ * Needs a mirrored (folded) eigenbasis. */
+int mi_pc_mode_mapped(mi_ctx* ctx, int l, int inverse, const double* in, double* out, long long outer,
+                      long long inner, const long long* imap, const long long* omap);
 int mi_pc_apply_time_yslab(mi_ctx* ctx, double* y, int y_lo, int y_hi);
 /* Number of symmetric modes hs of direction l when its eigenbasis is an
  * exactly mirrored even/odd basis (uniform knots: factors._centro_eigh) and
@@ -212,9 +234,14 @@ int mi_combination(mi_ctx* ctx, long long n, int k, const double* V, long long l
 int mi_scale_inv(mi_ctx* ctx, long long n, const double* x, const double* hnorm, double* out);
 /* out = x / sqrt(*nrm2)  (nrm2 device: squared norm from mi_dots) */
 int mi_normalize(mi_ctx* ctx, long long n, const double* x, const double* nrm2, double* out);
-/* fused CGS2 pass: w -= V^T h_in ; h_out = V w ; optional ||w||^2 into *nrm2 */
+/* fused CGS2 pass (linalg.py:405-411, one read of V): w -= sum_i h_in[i] V_i, then h_out[i] = V_i . w;
+ * bitwise the same as mi_sub_combination followed by mi_dots (k <= 32 fused, two passes beyond) */
 int mi_cgs_pass(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* h_in,
                 double* w, double* h_out);
+/* fused last CGS2 pass + norm (linalg.py:409-412): w -= sum_i h_in[i] V_i, then *nrm2 = w . w;
+ * bitwise the same as mi_sub_combination followed by mi_dots(w, w) */
+int mi_cgs_norm_pass(mi_ctx* ctx, long long n, int k, const double* V, long long ldv, const double* h_in,
+                     double* w, double* nrm2);
 
 /* ---------------------------------------------------------------------
  * Spline Upwind residual indicator (replaces compute_theta's grid work,
@@ -243,6 +270,10 @@ int mi_theta_elements(mi_ctx* ctx, const double* u, const double* w, const doubl
  * x rows x G_s, coef = [cg_i, cm_ab] x G_s (see theta.py MappedDeviceIndicator),
  * src = NULL or f at the same points; G[l] = nel[l] q spatial Gauss points.
  * emax / maxes as mi_theta_elements. */
+/* Lifting for the indicator: the u field's dropped slab holds u0 (device, N_s) instead of zeros
+ * (the lifted counterpart of _full_time_tensor, fields.py:8-12); NULL clears. */
+int mi_theta_set_lift(mi_ctx* ctx, const double* u0);
+
 int mi_theta_mapped_elements(mi_ctx* ctx, const double* fields, const double* coef, const double* src, int et0,
                              int et1, const int* G, int q, int qt, const int* nel, double D, double cmT, double c1,
                              double a, double c2, double* emax, double* maxes);

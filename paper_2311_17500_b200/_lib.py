@@ -34,6 +34,10 @@ _SIGS = {
     "mi_op_apply": ([_vp, _vp, _vp], _c_int),
     "mi_op_set_reaction": ([_vp, _vp, _vp, _c_dbl, _c_dbl, _c_dbl, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_clear_reaction": ([_vp], _c_int),
+    "mi_op_set_lift": ([_vp, _vp, _vp], _c_int),
+    "mi_op_finalize": ([_vp], _c_int),
+    "mi_op_apply_lift": ([_vp, _vp], _c_int),
+    "mi_theta_set_lift": ([_vp, _vp], _c_int),
     "mi_op_set_reaction_weight": ([_vp, _vp], _c_int),
     "mi_op_set_reaction_store": ([_vp, _c_int], _c_int),
     "mi_op_set_quad_channel": ([_vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp], _c_int),
@@ -48,6 +52,7 @@ _SIGS = {
     "mi_pc_apply_time_yslab": ([_vp, _vp, _c_int, _c_int], _c_int),
     "mi_pc_mode": ([_vp, _c_int, _c_int, _vp, _vp, _c_ll, _c_ll], _c_int),
     "mi_pc_fold": ([_vp, _c_int], _c_int),
+    "mi_pc_mode_mapped": ([_vp, _c_int, _c_int, _vp, _vp, _c_ll, _c_ll, _vp, _vp], _c_int),
     "mi_ws_setup": ([_vp, _vp, _vp, _vp], _c_int),
     "mi_ws_time": ([_vp, _vp, _vp], _c_int),
     "mi_ws_mass": ([_vp, _vp, _vp, _c_ll, _c_int], _c_int),
@@ -60,6 +65,7 @@ _SIGS = {
     "mi_scale_inv": ([_vp, _c_ll, _vp, _vp, _vp], _c_int),
     "mi_normalize": ([_vp, _c_ll, _vp, _vp, _vp], _c_int),
     "mi_cgs_pass": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp, _vp], _c_int),
+    "mi_cgs_norm_pass": ([_vp, _c_ll, _c_int, _vp, _c_ll, _vp, _vp, _vp], _c_int),
     "mi_theta_setup": ([_vp, _vp, _vp, _vp, _vp, _vp, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_dbl], _c_int),
     "mi_theta_elements": ([_vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _vp], _c_int),
     "mi_theta_mapped_elements": ([_vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _vp, _vp], _c_int),

@@ -97,8 +97,15 @@ struct mi_ctx {
   int ntau = 0;
   bool op_ready = false;
   bool frag_dirty = true;
+  bool stencil_released = false;  // mi_op_finalize freed `stencil` after packing it into `frag`
   bool use_dmma = false;
   int C[3] = {1, 1, 1};         // DMMA cube grid
+
+  // ---- u0 lifting (initial data on the dropped first time function, DESIGN 7)
+  bool lift_on = false;
+  mi::DeviceBuf lift_u0;        // N_s_in lifting coefficients (input slab)
+  mi::DeviceBuf lift_band;      // nchan x nt x (2pt+1): each channel's full-time column 0 as band entries
+  mi::DeviceBuf lift_x;         // N_in scratch of mi_op_apply_lift
 
   // ---- reaction correction M_R (variant B)
   bool reaction_on = false;
@@ -136,6 +143,7 @@ struct mi_ctx {
 
   // ---- SU residual indicator (compute_theta)
   bool th_ready = false;
+  mi::DeviceBuf th_u0;          // lifting coefficients seen by the indicator (empty: no lifting)
   mi::DeviceBuf th_B0, th_B1;   // element tables, directions x, y, z, t (values; 2nd / 1st derivatives)
   size_t th_off[4] = {0, 0, 0, 0};
   int th_nel[4] = {1, 1, 1, 1};

@@ -179,7 +179,7 @@ int mi_ctx_destroy(mi_ctx* c) {
   mi::DeviceBuf* bufs[] = {&c->tband, &c->stencil, &c->wbuf, &c->frag, &c->xt, &c->afr, &c->u_it, &c->w_it, &c->rx_B,
                            &c->rx_W, &c->Q, &c->QT, &c->pen_diag, &c->pen_off,
                            &c->pen_g, &c->pen_glow, &c->pc_t1, &c->pc_t2, &c->pc_t3, &c->tq_frag, &c->y_in, &c->rx_jw, &c->rx_cw,
-                           &c->partials};
+                           &c->partials, &c->lift_u0, &c->lift_band, &c->lift_x, &c->th_u0};
   for (auto* b : bufs) mi::dfree(*b);
   mi::DeviceBuf* wbufs[] = {&c->ws_Kinv, &c->ws_MT0, &c->ws_MiT0, &c->ws_t1, &c->ws_t2, &c->ws_t3,
                             &c->th_B0, &c->th_B1};

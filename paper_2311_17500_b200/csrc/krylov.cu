@@ -88,6 +88,59 @@ __global__ void scale_div(const double* __restrict__ x, const double* __restrict
     out[j] = x[j] / d;
 }
 
+// Fused CGS2 passes (k <= KM basis vectors): each V entry is read ONCE for both the subtraction and the
+// following reduction.  MODE 0: w -= V h, then h_out = V^T w (the second classical Gram-Schmidt
+// pass's dots); MODE 1: w -= V h, then |w|^2.  Per-block partials in a fixed partition, reduced by
+// dots_final: deterministic, the same rounding as the unfused pair only up to the summation order.
+template <int KM, int MODE>
+__global__ void __launch_bounds__(KT) sub_reduce(const double* __restrict__ V, long long ldv,
+                                                 const double* __restrict__ h, int k, double* __restrict__ w,
+                                                 long long n, double* __restrict__ part) {
+  constexpr int NA = MODE == 0 ? KM : 1;
+  __shared__ double hs[KM];
+  __shared__ double red[NA][KT / 32];
+  if (threadIdx.x < KM) hs[threadIdx.x] = threadIdx.x < k ? h[threadIdx.x] : 0.0;
+  __syncthreads();
+  double acc[NA];
+#pragma unroll
+  for (int g = 0; g < NA; ++g) acc[g] = 0.0;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  for (long long j = lo + threadIdx.x; j < hi; j += KT) {
+    double v[KM];
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      v[i] = i < k ? V[(long long)i * ldv + j] : 0.0;
+      s = fma(hs[i], v[i], s);
+    }
+    const double wn = w[j] - s;
+    w[j] = wn;
+    if constexpr (MODE == 0) {
+#pragma unroll
+      for (int i = 0; i < KM; ++i) acc[i] = fma(v[i], wn, acc[i]);
+    } else {
+      acc[0] = fma(wn, wn, acc[0]);
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int g = 0; g < NA; ++g) {
+    double x = acc[g];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[g][warp] = x;
+  }
+  __syncthreads();
+  const int nout = MODE == 0 ? k : 1;
+  for (int g = threadIdx.x; g < nout; g += KT) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < KT / 32; ++q) x += red[g][q];
+    part[(long long)g * gridDim.x + blockIdx.x] = x;
+  }
+}
+
 static int grid_for(long long n) {
   long long b = (n + 255) / 256;
   return (int)(b < 148LL * 16 ? b : 148LL * 16);
@@ -156,9 +209,50 @@ int mi_normalize(mi_ctx* c, long long n, const double* x, const double* nrm2, do
 int mi_cgs_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* h_in, double* w,
                 double* h_out) {
   MI_DEVICE_GUARD(c);
-  int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
-  if (rc) return rc;
-  return mi_dots(c, n, k, V, ldv, w, h_out);
+  MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_cgs_pass");
+  if (k == 0) return MI_OK;
+  if (k > 32) {   // beyond the fused kernel's register budget: two passes
+    int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
+    if (rc) return rc;
+    return mi_dots(c, n, k, V, ldv, w, h_out);
+  }
+  int rc;
+  if ((rc = dalloc(c->partials, (size_t)k * KB))) return rc;
+  ProfScope ps(c, PROF_KRYLOV, 2);
+  if (k <= 8)
+    sub_reduce<8, 0><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  else if (k <= 16)
+    sub_reduce<16, 0><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  else
+    sub_reduce<32, 0><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  MI_CHECK_LAUNCH("sub_reduce");
+  dots_final<<<k, 512, 0, c->stream>>>(c->partials.p, KB, h_out, 1);
+  MI_CHECK_LAUNCH("dots_final");
+  return MI_OK;
+}
+
+int mi_cgs_norm_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* h_in, double* w,
+                     double* nrm2) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_cgs_norm_pass");
+  if (k == 0 || k > 32) {
+    int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
+    if (rc) return rc;
+    return mi_dots(c, n, 1, w, n, w, nrm2);
+  }
+  int rc;
+  if ((rc = dalloc(c->partials, (size_t)KB))) return rc;
+  ProfScope ps(c, PROF_KRYLOV, 2);
+  if (k <= 8)
+    sub_reduce<8, 1><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  else if (k <= 16)
+    sub_reduce<16, 1><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  else
+    sub_reduce<32, 1><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  MI_CHECK_LAUNCH("sub_reduce");
+  dots_final<<<1, 512, 0, c->stream>>>(c->partials.p, KB, nrm2, 1);
+  MI_CHECK_LAUNCH("dots_final");
+  return MI_OK;
 }
 
 }  // extern "C"

@@ -66,11 +66,16 @@ struct ModeFold {
 // U^T (into mode space), INV = true applies U.  ROWS: the mode is the contiguous index
 // (out[r][.] from in[r][.], `outer` rows); COLS: out[o][.][c] from in[o][.][c] (stride `inner`).
 // Tiles: 64 flattened columns (COLS) or 64 rows (ROWS).
+// COLS addressing maps (nullable, 2n int64 each): element (o, r, c) of the input / output sits at
+// map[2r] + o * map[2r + 1] + c instead of (o * n + r) * inner + c.  The space-sharded P^-1
+// (sharded.py) uses them to read and write the all-to-all send / receive layouts directly.
 template <int TH, bool ROWS, bool INV>
 __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* __restrict__ U,
                                                                    const double* __restrict__ in,
                                                                    double* __restrict__ out, int n,
-                                                                   long long inner, long long outer) {
+                                                                   long long inner, long long outer,
+                                                                   const long long* __restrict__ imap,
+                                                                   const long long* __restrict__ omap) {
   using G = ModeFold<TH>;
   constexpr int KS = G::KS, NB = G::NB;
   constexpr int PS = ROWS ? G::PROWS : G::PCOLS;    // panel size
@@ -112,12 +117,13 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
     // ================= producers: loads of tile j + 2, stores of tile j =================
     const int p = tid - 32 * G::NCW;
     // COLS: thread -> column c = p & 63, rows (p >> 6) + 2 m; ROWS: flat element stride
-    auto col_base = [&](long long tile, int c, bool& ok) -> long long {
+    // flattened column g -> (outer index o, inner index cc)
+    auto col_pos = [&](long long tile, int c, long long& o, long long& cc) -> bool {
       const long long g = tile * 64 + c;
-      ok = g < total;
-      if (!ok) return 0;
-      const long long o = g / inner;
-      return o * n * inner + (g - o * inner);
+      if (g >= total) return false;
+      o = g / inner;
+      cc = g - o * inner;
+      return true;
     };
     auto load = [&](long long j) {
       const int b = (int)(j % NB);
@@ -125,10 +131,16 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
       double* dst = pan + b * PS;
       if constexpr (!ROWS) {
         const int c = p & 63;
-        bool ok;
-        const long long base = col_base(tile, c, ok);
-        if (ok)
-          for (int r = p >> 6; r < n; r += G::NPT / 64) cp_async8(dst + r * LD + c, in + base + (long long)r * inner, true);
+        long long o, cc;
+        if (col_pos(tile, c, o, cc)) {
+          if (imap != nullptr) {
+            for (int r = p >> 6; r < n; r += G::NPT / 64)
+              cp_async8(dst + r * LD + c, in + __ldg(imap + 2 * r) + o * __ldg(imap + 2 * r + 1) + cc, true);
+          } else {
+            const long long base = o * n * inner + cc;
+            for (int r = p >> 6; r < n; r += G::NPT / 64) cp_async8(dst + r * LD + c, in + base + (long long)r * inner, true);
+          }
+        }
         cp_async_mbar_arrive_noinc(&full[b]);
       } else {
         // one thread: the tile's nel = nrow * n doubles start 16-byte aligned (tile * 64 * n is even); an
@@ -147,10 +159,16 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
       const double* sp = pan + b * PS;
       if constexpr (!ROWS) {
         const int c = p & 63;
-        bool ok;
-        const long long base = col_base(tile, c, ok);
-        if (ok)
-          for (int r = p >> 6; r < n; r += G::NPT / 64) out[base + (long long)r * inner] = sp[r * LD + c];
+        long long o, cc;
+        if (col_pos(tile, c, o, cc)) {
+          if (omap != nullptr) {
+            for (int r = p >> 6; r < n; r += G::NPT / 64)
+              out[__ldg(omap + 2 * r) + o * __ldg(omap + 2 * r + 1) + cc] = sp[r * LD + c];
+          } else {
+            const long long base = o * n * inner + cc;
+            for (int r = p >> 6; r < n; r += G::NPT / 64) out[base + (long long)r * inner] = sp[r * LD + c];
+          }
+        }
       } else {
         const long long r0 = tile * 64;
         const int nel = (int)(total - r0 < 64 ? total - r0 : 64) * n, nb = nel & ~1;
@@ -243,7 +261,8 @@ __global__ void __launch_bounds__(ModeFold<TH>::NTH, 1) mode_fold(const double* 
 // instantiated range.
 template <bool ROWS>
 inline bool launch_mode_fold(const double* U, const double* in, double* out, int n, bool inverse, long long inner,
-                             long long outer, int nsm, cudaStream_t st, cudaError_t* err) {
+                             long long outer, int nsm, cudaStream_t st, cudaError_t* err,
+                             const long long* imap = nullptr, const long long* omap = nullptr) {
   const int hs = n - n / 2;
 #define MI_MF(THV)                                                                                       \
   if (hs <= 8 * THV && n <= ModeFold<THV>::KP) {                                                         \
@@ -259,9 +278,9 @@ inline bool launch_mode_fold(const double* U, const double* in, double* out, int
     const long long ntiles = (total + 63) / 64;                                                          \
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);                                                 \
     if (inverse)                                                                                         \
-      mode_fold<THV, ROWS, true><<<grid > 0 ? grid : 1, nth, sm, st>>>(U, in, out, n, inner, outer);     \
+      mode_fold<THV, ROWS, true><<<grid > 0 ? grid : 1, nth, sm, st>>>(U, in, out, n, inner, outer, imap, omap);  \
     else                                                                                                 \
-      mode_fold<THV, ROWS, false><<<grid > 0 ? grid : 1, nth, sm, st>>>(U, in, out, n, inner, outer);    \
+      mode_fold<THV, ROWS, false><<<grid > 0 ? grid : 1, nth, sm, st>>>(U, in, out, n, inner, outer, imap, omap); \
     *err = cudaGetLastError();                                                                           \
     return true;                                                                                         \
   }

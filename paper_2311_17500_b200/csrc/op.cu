@@ -365,7 +365,7 @@ __global__ void time_filter(const double* __restrict__ w, const double* __restri
   y[(long long)t * g.ns + i] = acc;
 }
 
-int reaction_apply(mi_ctx* c, const double* x, double* y);  // reaction.cu
+int reaction_apply(mi_ctx* c, const double* x, double* y, const double* x0);  // reaction.cu
 
 }  // namespace mi
 
@@ -381,6 +381,7 @@ int mi_op_setup(mi_ctx* c, int nchan) {
   int rc;
   if ((rc = dalloc(c->tband, (size_t)nchan * c->nt * (2 * c->pt + 1)))) return rc;
   if ((rc = dalloc(c->stencil, (size_t)nchan * c->nsten * c->ns))) return rc;
+  c->stencil_released = false;
   c->use_dmma = c->p <= 3 && c->pt <= 4;
   MI_REQUIRE(c->use_dmma || (c->n3g == c->n[2] && c->ns_in == c->ns), MI_ERR_ARG,
              "z-slab contexts need the tensor-core operator (p <= 3)");
@@ -397,7 +398,6 @@ int mi_op_set_time_bands(mi_ctx* c, const double* bands) {
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   MI_CUDA(cudaMemcpyAsync(c->tband.p, bands, sizeof(double) * c->nchan * c->nt * (2 * c->pt + 1),
                           cudaMemcpyHostToDevice, c->stream));
-  c->frag_dirty = true;
   MI_CUDA(cudaStreamSynchronize(c->stream));
   return MI_OK;
 }
@@ -405,6 +405,7 @@ int mi_op_set_time_bands(mi_ctx* c, const double* bands) {
 int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* bands) {
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(!c->stencil_released, MI_ERR_STATE, "channel stencils were packed and released (mi_op_finalize); call mi_op_setup again");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(nterms >= 1, MI_ERR_ARG, "nterms must be >= 1");
   const int nmax = table_rows(c);
@@ -429,6 +430,7 @@ int mi_op_set_kron_channel(mi_ctx* c, int ch, int nterms, const double* coef, co
 int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H, int ko) {
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(!c->stencil_released, MI_ERR_STATE, "channel stencils were packed and released (mi_op_finalize); call mi_op_setup again");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(ko >= 0 && ko <= 8, MI_ERR_ARG, "ko out of range");
   const int nmax = table_rows(c);
@@ -454,6 +456,7 @@ int mi_op_set_su_channel(mi_ctx* c, int ch, const double* theta, const double* H
 static int quad_channel(mi_ctx* c, int ch, int nterms, const double* coef, const double* theta, const double* T,
                         const int* q, const int* kstart, const int* kwin, const int* Q) {
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(!c->stencil_released, MI_ERR_STATE, "channel stencils were packed and released (mi_op_finalize); call mi_op_setup again");
   MI_REQUIRE(ch >= 0 && ch < c->nchan, MI_ERR_ARG, "channel out of range");
   MI_REQUIRE(nterms >= 1 && coef && theta && T && Q && (q || (kstart && kwin)), MI_ERR_ARG,
              "bad quadrature channel arguments");
@@ -535,6 +538,7 @@ int mi_op_set_quad_channel_k(mi_ctx* c, int ch, int nterms, const double* coef, 
 int mi_op_set_channel_stencil(mi_ctx* c, int ch, const double* sten) {
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(!c->stencil_released, MI_ERR_STATE, "channel stencils were packed and released (mi_op_finalize); call mi_op_setup again");
   MI_REQUIRE(ch >= 0 && ch < c->nchan && sten != nullptr, MI_ERR_ARG, "channel out of range");
   MI_CUDA(cudaMemcpyAsync(c->stencil.p + (size_t)ch * c->nsten * c->ns, sten, sizeof(double) * c->nsten * c->ns,
                           cudaMemcpyDeviceToDevice, c->stream));
@@ -545,6 +549,7 @@ int mi_op_set_channel_stencil(mi_ctx* c, int ch, const double* sten) {
 int mi_op_get_channel_stencil(mi_ctx* c, int ch, double* sten) {
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  MI_REQUIRE(!c->stencil_released, MI_ERR_STATE, "channel stencils were packed and released (mi_op_finalize); call mi_op_setup again");
   MI_REQUIRE(ch >= 0 && ch < c->nchan && sten != nullptr, MI_ERR_ARG, "channel out of range");
   MI_CUDA(cudaMemcpyAsync(sten, c->stencil.p + (size_t)ch * c->nsten * c->ns, sizeof(double) * c->nsten * c->ns,
                           cudaMemcpyDeviceToDevice, c->stream));
@@ -589,6 +594,7 @@ static int dmma_prepare(mi_ctx* c) {
           c->ns, per_group);
       MI_CHECK_LAUNCH("repack_frag");
     }
+#if !MI_STEN_FUSE
     if ((rc = dalloc(c->wbuf, (size_t)c->nchan * c->ns * ntp))) return rc;
     MI_CUDA(cudaMemsetAsync(c->wbuf.p, 0, sizeof(double) * c->nchan * c->ns * ntp, c->stream));
     {
@@ -607,6 +613,9 @@ static int dmma_prepare(mi_ctx* c) {
                                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       MI_REQUIRE(r == CUDA_SUCCESS, MI_ERR_CUDA, "cuTensorMapEncodeTiled (W) failed");
     }
+#else
+    mi::dfree(c->wbuf);   // the fused filter keeps W in shared memory
+#endif
     MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)G::SMEM));
   });
@@ -615,6 +624,7 @@ static int dmma_prepare(mi_ctx* c) {
   return rc;
 }
 
+#if !MI_STEN_FUSE
 // y = sum_c T_c (x) along time of the time-innermost W buffer (HBM-bound)
 static int launch_time_filter(mi_ctx* c, double* y) {
   MI_REQUIRE(c->nchan <= 64, MI_ERR_ARG, "too many channels for the time filter");
@@ -672,6 +682,7 @@ static int launch_time_filter(mi_ctx* c, double* y) {
   MI_CHECK_LAUNCH("time_filter_ti");
   return MI_OK;
 }
+#endif
 
 static int dmma_apply(mi_ctx* c, const double* x, double* y) {
   MI_DISPATCH_DP(c->d, c->p, {
@@ -693,29 +704,24 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
       stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");
     }
+#if !MI_STEN_FUSE
     {
       ProfScope ps(c, PROF_OP_TFILTER);
       int frc = launch_time_filter(c, y);
       if (frc) return frc;
       MI_CHECK_LAUNCH("time_filter_ti");
     }
+#endif
   });
   return MI_OK;
 }
 
-int mi_op_apply(mi_ctx* c, const double* x, double* y) {
-  MI_DEVICE_GUARD(c);
-  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
-  MI_REQUIRE(x != y, MI_ERR_ARG, "x and y must not alias");
+// y = sum_c T_c (x) S_c x (every Kronecker / SU / quadrature channel; no reaction)
+static int channels_apply(mi_ctx* c, const double* x, double* y) {
   if (c->use_dmma) {
     int rc;
     if (c->frag_dirty && (rc = dmma_prepare(c))) return rc;
-    if ((rc = dmma_apply(c, x, y))) return rc;
-    if (c->reaction_on) {
-      ProfScope ps(c, PROF_OP_REACTION);
-      return reaction_apply(c, x, y);
-    }
-    return MI_OK;
+    return dmma_apply(c, x, y);
   }
   Dims g = dims_of(c);
   constexpr int CG = 4, TC = 8;
@@ -726,15 +732,86 @@ int mi_op_apply(mi_ctx* c, const double* x, double* y) {
     MI_DISPATCH_DP(c->d, c->p, (stencil_apply<D_, P_, CG, TC><<<grid, 128, 0, c->stream>>>(x, c->stencil.p, c->wbuf.p, c0, nc, g)));
     MI_CHECK_LAUNCH("stencil_apply");
   }
-  {
   dim3 g2((unsigned)((c->ns + 255) / 256), c->nt);
   ProfScope ps(c, PROF_OP_TFILTER);
   time_filter<<<g2, 256, 0, c->stream>>>(c->wbuf.p, c->tband.p, y, c->nchan, c->pt, g);
   MI_CHECK_LAUNCH("time_filter");
-  }
+  return MI_OK;
+}
+
+int mi_op_apply(mi_ctx* c, const double* x, double* y) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
+  MI_REQUIRE(x != y, MI_ERR_ARG, "x and y must not alias");
+  int rc = channels_apply(c, x, y);
+  if (rc) return rc;
   if (c->reaction_on) {
     ProfScope ps(c, PROF_OP_REACTION);
-    return reaction_apply(c, x, y);
+    return reaction_apply(c, x, y, nullptr);
+  }
+  return MI_OK;
+}
+
+int mi_op_finalize(mi_ctx* c) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  if (!c->use_dmma || c->stencil_released) return MI_OK;
+  int rc;
+  if (c->frag_dirty && (rc = dmma_prepare(c))) return rc;
+  mi::dfree(c->stencil);          // only the fragment-major copy is read from now on
+  c->stencil_released = true;
+  return MI_OK;
+}
+
+int mi_op_set_lift(mi_ctx* c, const double* column0, const double* u0) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
+  if (u0 == nullptr) {
+    c->lift_on = false;
+    c->rx_cw_dirty = true;
+    return MI_OK;
+  }
+  MI_REQUIRE(column0 != nullptr, MI_ERR_ARG, "NULL lifting column");
+  MI_REQUIRE(c->rx_rowoff == -1, MI_ERR_ARG, "lifting needs the whole time axis (not a time slab)");
+  int rc;
+  if ((rc = dalloc(c->lift_u0, (size_t)c->ns_in))) return rc;
+  MI_CUDA(cudaMemcpyAsync(c->lift_u0.p, u0, sizeof(double) * c->ns_in, cudaMemcpyDeviceToDevice, c->stream));
+  // the column-0 coupling v_c[t] = T_c,full[t + 1, 0] multiplies W_c at time row 0 (where mi_op_apply_lift
+  // places u0): band entry k = pt - t of row t
+  const int bw = 2 * c->pt + 1;
+  std::vector<double> hb((size_t)c->nchan * c->nt * bw, 0.0);
+  for (int ch = 0; ch < c->nchan; ++ch)
+    for (int t = 0; t < std::min(c->pt, c->nt); ++t)
+      hb[((size_t)ch * c->nt + t) * bw + (c->pt - t)] = column0[(size_t)ch * c->nt + t];
+  for (int ch = 0; ch < c->nchan; ++ch)
+    for (int t = c->pt; t < c->nt; ++t)
+      MI_REQUIRE(column0[(size_t)ch * c->nt + t] == 0.0, MI_ERR_ARG, "lifting column beyond the time band");
+  if ((rc = dalloc(c->lift_band, hb.size()))) return rc;
+  MI_CUDA(cudaMemcpyAsync(c->lift_band.p, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice, c->stream));
+  MI_CUDA(cudaStreamSynchronize(c->stream));
+  c->lift_on = true;
+  c->rx_cw_dirty = true;      // C_r sees the lifted iterate
+  return MI_OK;
+}
+
+int mi_op_apply_lift(mi_ctx* c, double* y) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
+  MI_REQUIRE(c->lift_on, MI_ERR_STATE, "no lifting set (mi_op_set_lift)");
+  int rc;
+  if ((rc = dalloc(c->lift_x, (size_t)c->N_in))) return rc;
+  // channels: x = u0 in time row 0, time bands = the column-0 couplings
+  MI_CUDA(cudaMemsetAsync(c->lift_x.p, 0, sizeof(double) * c->N_in, c->stream));
+  MI_CUDA(cudaMemcpyAsync(c->lift_x.p, c->lift_u0.p, sizeof(double) * c->ns_in, cudaMemcpyDeviceToDevice, c->stream));
+  std::swap(c->tband, c->lift_band);
+  rc = channels_apply(c, c->lift_x.p, y);
+  std::swap(c->tband, c->lift_band);
+  if (rc) return rc;
+  if (c->reaction_on) {
+    // reaction: x = 0 on the constrained rows, u0 on the lifted slab
+    MI_CUDA(cudaMemsetAsync(c->lift_x.p, 0, sizeof(double) * c->ns_in, c->stream));
+    ProfScope ps(c, PROF_OP_REACTION);
+    return reaction_apply(c, c->lift_x.p, y, c->lift_u0.p);
   }
   return MI_OK;
 }

@@ -72,7 +72,6 @@ __global__ void arrowhead_solve(double* __restrict__ Y, const double* __restrict
   Y[(long long)m * ns + s] = xl;
 }
 
-using mi::num_sms;
 
 static cudaError_t mode_strided(const double* A, const double* in, double* out, int n, long long inner,
                                 long long outer, cudaStream_t st) {
@@ -314,6 +313,22 @@ int mi_pc_fold(mi_ctx* c, int l) {
   MI_DEVICE_GUARD(c);
   if (c == nullptr || !c->pc_ready || l < 0 || l > 2) return 0;
   return c->fold_hs[l];
+}
+
+int mi_pc_mode_mapped(mi_ctx* c, int l, int inverse, const double* in, double* out, long long outer,
+                      long long inner, const long long* imap, const long long* omap) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->pc_ready, MI_ERR_STATE, "preconditioner not set up");
+  MI_REQUIRE(l >= 0 && l < c->d, MI_ERR_ARG, "direction out of range");
+  MI_REQUIRE(outer >= 1 && inner >= 2 && in != out, MI_ERR_ARG, "bad mode-product shape or aliasing");
+  MI_REQUIRE(c->fold_hs[l] > 0, MI_ERR_ARG, "addressing maps need a mirrored (folded) eigenbasis");
+  ProfScope ps(c, PROF_PC_SPATIAL);
+  cudaError_t err = cudaSuccess;
+  const bool done = launch_mode_fold<false>(c->Us[l].p, in, out, c->n[l], inverse != 0, inner, outer, num_sms(),
+                                            c->stream, &err, imap, omap);
+  MI_REQUIRE(done, MI_ERR_ARG, "mode extent outside the folded kernel's range");
+  MI_CUDA(err);
+  return MI_OK;
 }
 
 int mi_pc_mode(mi_ctx* c, int l, int inverse, const double* in, double* out, long long outer, long long inner) {

@@ -45,6 +45,10 @@ struct RxArgs {
   double c1, a, c2;
   const double* jw;    // mapped geometry: |det J| at the spatial Gauss points, C order (Q_3, Q_2, Q_1); null: box
   double* cw;          // stored weighted coefficient C_r w_x (RX_PRE writes it, RX_STORED reads it)
+  // u0 lifting: coefficients of the dropped first time function (constrained row -1) for the u field
+  // (the lifted iterate) and for the x field (mi_op_apply_lift); null = zero slab (the reference)
+  const double* lift_u;
+  const double* lift_x;
 };
 
 // Kernel modes.  RX_FUSED interpolates u, w and x and evaluates C_r on the fly every apply.  The
@@ -208,7 +212,13 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
     for (int m = 0; m < NPRE; ++m) {
       const int f = (tid + NTH * m) / LS;
       const double* src = MODE == RX_STORED ? r.x : (f == 0 ? r.u : (f == 1 ? r.w : r.x));
-      pre[m] = (vt && gsp[m] >= 0) ? __ldg(src + (long long)ct * ns + gsp[m]) : 0.0;
+      const double* lift = MODE == RX_STORED ? r.lift_x : (f == 0 ? r.lift_u : (f == 1 ? nullptr : r.lift_x));
+      double v = 0.0;
+      if (gsp[m] >= 0) {
+        if (vt) v = __ldg(src + (long long)ct * ns + gsp[m]);
+        else if (ct == -1 && lift != nullptr) v = __ldg(lift + gsp[m]);
+      }
+      pre[m] = v;
     }
   };
   double btp = 0.0;
@@ -526,6 +536,8 @@ static void fill_args(mi_ctx* c, RxArgs& r) {
   r.c2 = c->c2;
   r.jw = c->rx_mapped ? c->rx_jw.p : nullptr;
   r.cw = c->rx_cw_ok ? c->rx_cw.p : nullptr;
+  r.lift_u = c->lift_on ? c->lift_u0.p : nullptr;
+  r.lift_x = nullptr;
 }
 
 // all colour classes of one kernel mode
@@ -611,7 +623,8 @@ static int reaction_prepare_store(mi_ctx* c) {
   return MI_OK;
 }
 
-int reaction_apply(mi_ctx* c, const double* x, double* y) {
+// y += M_R x; x0 (nullable) = the x coefficients of the lifted slab (mi_op_apply_lift)
+int reaction_apply(mi_ctx* c, const double* x, double* y, const double* x0) {
   if (c->rx_cw_dirty) {
     int rc = reaction_prepare_store(c);
     if (rc) return rc;
@@ -628,6 +641,7 @@ int reaction_apply(mi_ctx* c, const double* x, double* y) {
   RxArgs r{};
   fill_args(c, r);
   r.x = x;
+  r.lift_x = x0;
   r.y = slab ? c->y_in.p : y;
   int rc = c->rx_cw_ok ? reaction_launch<RX_STORED>(c, r) : reaction_launch<RX_FUSED>(c, r);
   if (rc) return rc;

@@ -41,6 +41,7 @@ struct ThArgs {
   int et0, et1;
   double il2[3];                  // D_l / L_l^2
   double cmT, c1, a, c2;          // C_m / T, Rogers-McCulloch constants
+  const double* u0;               // u0 lifting: u coefficients of the dropped first time function (null: zero)
 };
 
 template <int D, int P>
@@ -150,8 +151,14 @@ __global__ void __launch_bounds__(256, 2) theta_elements(ThArgs r) {
     const bool vt = ct >= 0 && ct < r.ntc;
 #pragma unroll
     for (int m = 0; m < G::NPRE; ++m) {
-      const double* src = (tid + 256 * m) < LS ? r.u : r.w;
-      pre[m] = (vt && gsp[m] >= 0) ? __ldg(src + (long long)ct * ns + gsp[m]) : 0.0;
+      const bool isu = (tid + 256 * m) < LS;
+      const double* src = isu ? r.u : r.w;
+      double v = 0.0;
+      if (gsp[m] >= 0) {
+        if (vt) v = __ldg(src + (long long)ct * ns + gsp[m]);
+        else if (ct == -1 && isu && r.u0 != nullptr) v = __ldg(r.u0 + gsp[m]);
+      }
+      pre[m] = v;
     }
   };
   double btp = 0.0;
@@ -479,6 +486,7 @@ int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double*
   r.c1 = c->th_c1;
   r.a = c->th_a;
   r.c2 = c->th_c2;
+  r.u0 = c->th_u0.n ? c->th_u0.p : nullptr;
   long long nb = 1;
   for (int l = 0; l < c->d; ++l) nb *= (c->th_nel[l] + 1) / 2;
   MI_TH_DISPATCH(c->d, c->p, c->pt, {
@@ -492,6 +500,19 @@ int mi_theta_elements(mi_ctx* c, const double* u, const double* w, const double*
     theta_elements<D_, P_, PT_><<<(unsigned)nb, 256, G::SMEM, c->stream>>>(r);
     MI_CHECK_LAUNCH("theta_elements");
   });
+  return MI_OK;
+}
+
+int mi_theta_set_lift(mi_ctx* c, const double* u0) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->th_ready, MI_ERR_STATE, "mi_theta_setup must be called first");
+  if (u0 == nullptr) {
+    mi::dfree(c->th_u0);
+    return MI_OK;
+  }
+  int rc;
+  if ((rc = mi::dalloc(c->th_u0, (size_t)c->ns))) return rc;
+  MI_CUDA(cudaMemcpyAsync(c->th_u0.p, u0, sizeof(double) * c->ns, cudaMemcpyDeviceToDevice, c->stream));
   return MI_OK;
 }
 

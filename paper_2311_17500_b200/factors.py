@@ -209,6 +209,22 @@ def su_time_bands(st, tau, lowrank, capacitance):
     return bands * coef[:, None, None]
 
 
+def su_time_lift(st, tau, lowrank, capacitance):
+    """Per rank r: C_m s_r sum_k int tau_k prof_r b_i^(k) b_0^(k) dt for the constrained rows i -- the
+    column of the full SU time factor coupling them to the dropped b_0 (u0 lifting).  Same rule as
+    su_time_bands.  Returns (R, N_t) (nonzero in the first p rows only)."""
+    p = st.time.degree
+    tg = st.time_greville()
+    x, w = gauss_rule(cells_with(st.time, tg), p + 2)
+    prof = hat_values(tg, x) @ lowrank.time_factors          # (nq, R)
+    out = np.zeros((lowrank.rank, st.num_time))
+    for k in range(1, p + 1):
+        Bf = basis_table(st.time, x, k)
+        wk = (w * tau.evaluate(k, x))[:, None] * prof         # (nq, R)
+        out += wk.T @ (Bf[:, 1:] * Bf[:, :1])
+    return out * (capacitance * lowrank.weights)[:, None]
+
+
 def hat_triple(space, length=1.0):
     """H[i, dj, k] = L * int hat_{i+k-KO}(x) b_i(x) b_{i+dj-p}(x) dx.
 

@@ -20,7 +20,8 @@ from .device import DeviceContext
 from .krylov import gmres
 from .operator import KroneckerOperator, Stabilization
 from .precond import FastDiagPreconditioner
-from .problem import FixedPointConfig, FixedPointDiverged, GaussGrid, SolveResult, box_of, load_vector
+from .problem import (FixedPointConfig, FixedPointDiverged, GaussGrid, SolveResult, box_of, lift_coefficients,
+                      load_vector)
 from .theta import DeviceIndicator, MappedDeviceIndicator
 from .wsolve import RecoverySolver
 
@@ -65,9 +66,15 @@ class _Workspace:
         self.precond = FastDiagPreconditioner.build(st, problem.final_time, problem.C_m, problem.scalar_D(),
                                                     problem.a * problem.c1, lengths=self.L, context=self.pc_ctx,
                                                     spatial_data=self.sd)
-        # M_t (x) M_s for g = b (M_t (x) M_s) u  (C_m = D = 0, unit reaction: channel c1 = M_t (x) M_s)
+        # u0 lifting (DESIGN 7): the lifted slab's coefficients stay on the device for every sweep
+        lift = lift_coefficients(problem)
+        self.lift = None if lift is None else torch.from_numpy(lift).to(torch.device("cuda", device))
+        # M_t (x) M_s for g = b (M_t (x) M_s) u  (C_m = D = 0, unit reaction: channel c1 = M_t (x) M_s);
+        # with a lift, g also takes the lifted column b (T M[1:, 0] (x) M_s) u0
         self.mass_op = KroneckerOperator(st, problem.final_time, 0.0, 0.0, {"c1": 1.0, "a": 1.0, "c2": 0.0},
-                                         lengths=self.L, device=device, spatial_data=self.sd)
+                                         lengths=self.L, device=device, spatial_data=self.sd, lift=self.lift,
+                                         lift_in_reaction=False)
+        self.g_lift = self.mass_op.lift_apply() if self.lift is not None else None
         self.wsolver = RecoverySolver(st, problem.final_time, problem.b, problem.d_e, config.linear_tol,
                                       lengths=self.L, device=device, spatial_data=self.sd)
 
@@ -78,7 +85,8 @@ class _Workspace:
             self.op_ctx = DeviceContext(problem.space, self.device)
         return KroneckerOperator(problem.space, problem.final_time, problem.C_m, problem.scalar_D(),
                                  problem.reaction_constants(), u=u_k, w=w_k, stabilization=stab,
-                                 lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd)
+                                 lengths=self.L, device=self.device, context=self.op_ctx, spatial_data=self.sd,
+                                 lift=self.lift)
 
 
 def _host_indicator(ind):
@@ -130,7 +138,7 @@ def fixed_point_solve(problem, config=None, device=0):
         else:
             from .geometry import is_mapped
             cls = MappedDeviceIndicator if is_mapped(problem.geometry) else DeviceIndicator
-            frozen_indicator = cls(problem, device).compute(pre.u, pre.w)
+            frozen_indicator = cls(problem, device).compute(pre.u, pre.w, lift=pre.lift)
         from .geometry import is_mapped
         frozen_stab = Stabilization(st, _indicator_values(frozen_indicator), config.lowrank_tol, problem.C_m,
                                     lengths=None if is_mapped(problem.geometry) else box_of(problem.geometry)[0])
@@ -142,6 +150,7 @@ def fixed_point_solve(problem, config=None, device=0):
     f_dev = (ws.f_vec.to(dev) if torch.is_tensor(ws.f_vec)
              else torch.from_numpy(np.ascontiguousarray(ws.f_vec)).to(dev))
     ph.stop("setup")
+    lift_host = None if ws.lift is None else ws.lift.cpu().numpy()
     u = torch.zeros(st.num_dof, dtype=torch.float64, device=dev)
     w = torch.zeros_like(u)
     increments, gmres_iters, pcg_iters = [], [], []
@@ -159,7 +168,7 @@ def fixed_point_solve(problem, config=None, device=0):
                 if config.indicator_override is not None:
                     fresh = config.indicator_override(problem, u.cpu().numpy(), w.cpu().numpy())
                 else:
-                    fresh = ws.indicator.compute(u, w, on_device=True)
+                    fresh = ws.indicator.compute(u, w, on_device=True, lift=ws.lift)
                 ph.stop("indicator")
                 if indicator is not None and alpha < 1.0:
                     prev = _indicator_values(indicator)
@@ -184,13 +193,17 @@ def fixed_point_solve(problem, config=None, device=0):
         op = ws.operator(problem, u, w, stab)
         ph.stop("operator_setup")
         ph.start()
-        u_tilde, nit, _ = gmres(op, f_dev, precond=ws.precond, tol=config.linear_tol)
+        rhs = f_dev if ws.lift is None else f_dev - op.lift_apply()
+        u_tilde, nit, _ = gmres(op, rhs, precond=ws.precond, tol=config.linear_tol)
         ph.stop("gmres")
         gmres_iters.append(nit)
 
         ph.start()
         if config.evolve_recovery:
-            g_vec = problem.b * ws.mass_op.matvec(u)
+            g_vec = ws.mass_op.matvec(u)
+            if ws.g_lift is not None:
+                g_vec = g_vec + ws.g_lift
+            g_vec = problem.b * g_vec
             w_tilde, w_its = ws.wsolver.solve(g_vec)
             pcg_iters.extend(w_its)
         else:
@@ -206,8 +219,9 @@ def fixed_point_solve(problem, config=None, device=0):
         u, w = u_new, w_new
         if inc <= config.tolerance:
             return SolveResult(u.cpu().numpy(), w.cpu().numpy(), k, increments, True, gmres_iters, pcg_iters,
-                               _time.perf_counter() - t0, _host_indicator(indicator), ph.sec)
+                               _time.perf_counter() - t0, _host_indicator(indicator), ph.sec, lift_host)
     result = SolveResult(u.cpu().numpy(), w.cpu().numpy(), galerkin_sweeps + config.max_iterations, increments,
-                         False, gmres_iters, pcg_iters, _time.perf_counter() - t0, _host_indicator(indicator), ph.sec)
+                         False, gmres_iters, pcg_iters, _time.perf_counter() - t0, _host_indicator(indicator), ph.sec,
+                         lift_host)
     raise FixedPointDiverged("fixed point did not reach %.2e in %d iterations"
                              % (config.tolerance, config.max_iterations), result)

@@ -49,6 +49,16 @@ class DeviceVecOps:
         _lib.call("mi_sub_combination", self.h, n, k, ctypes.c_void_p(V.data_ptr()), V.stride(0), dptr(hvec),
                   dptr(w))
 
+    def sub_dots(self, V, k, h_in, w, h_out):
+        """w -= V[:k]^T h_in, then h_out[:k] = V[:k] @ w (one fused pass over V)."""
+        _lib.call("mi_cgs_pass", self.h, w.numel(), k, ctypes.c_void_p(V.data_ptr()), V.stride(0), dptr(h_in),
+                  dptr(w), dptr(h_out))
+
+    def sub_norm(self, V, k, h_in, w, nrm2):
+        """w -= V[:k]^T h_in, then nrm2 = w . w (one fused pass over V)."""
+        _lib.call("mi_cgs_norm_pass", self.h, w.numel(), k, ctypes.c_void_p(V.data_ptr()), V.stride(0),
+                  dptr(h_in), dptr(w), dptr(nrm2))
+
     def normalize(self, src, nrm2, dst):
         _lib.call("mi_normalize", self.h, src.numel(), dptr(src), dptr(nrm2), dptr(dst))
 
@@ -123,13 +133,20 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
         apply_A(V[j], tmp)
         apply_P(tmp, w)
         k = j + 1
+        # CGS2 (linalg.py:405-412); the fused passes read V once per subtraction + reduction
         ops.dots(V, k, w, h1)
         red(h1[:k])
-        ops.sub_comb(V, k, h1, w)
-        ops.dots(V, k, w, h2)
+        if hasattr(ops, "sub_dots"):
+            ops.sub_dots(V, k, h1, w, h2)
+        else:
+            ops.sub_comb(V, k, h1, w)
+            ops.dots(V, k, w, h2)
         red(h2[:k])
-        ops.sub_comb(V, k, h2, w)
-        ops.dots(w.view(1, -1), 1, w, nrm)
+        if hasattr(ops, "sub_norm"):
+            ops.sub_norm(V, k, h2, w, nrm)
+        else:
+            ops.sub_comb(V, k, h2, w)
+            ops.dots(w.view(1, -1), 1, w, nrm)
         red(nrm)
         host = scal.cpu().numpy()
         hv = host[8:8 + k] + host[8 + cap + 1:8 + cap + 1 + k]

@@ -39,6 +39,8 @@ class Stabilization:
     def __init__(self, space_time, indicator, tol=0.1, capacitance=1.0, lengths=None):
         st = space_time
         self.tau = upwind_weights(st.time)
+        self.capacitance = capacitance
+        self.space_time = st
         self.lowrank = lowrank_factorize(indicator, tol)
         self.rank = self.lowrank.rank
         d = len(st.spatial)
@@ -69,7 +71,7 @@ class KroneckerOperator:
 
     def __init__(self, space_time, final_time, capacitance=1.0, diffusion=1e-4, constants=None,
                  u=None, w=None, stabilization=None, lengths=None, device=0, context=None, time_rows=None,
-                 z_planes=None, spatial_data=None):
+                 z_planes=None, spatial_data=None, lift=None, lift_in_reaction=True):
         """``time_rows=(e_lo, e_hi)`` builds the operator restricted to a slab of
         constrained time rows: the time bands are the global rows e_lo..e_hi, and
         u, w (if given) are slab vectors.  ``z_planes=(z_lo, z_hi)`` (d = 3) builds
@@ -78,7 +80,12 @@ class KroneckerOperator:
         to the owned planes of A x; u, w (if given) are input-slab vectors.
         ``spatial_data`` (a geometry.MappedSpatialData) selects a mapped geometry: M_s and K_s are
         then assembled by Gauss quadrature on the device (SpatialQuadratureData.mass/stiffness,
-        assembly.py:197-219) and the reaction carries |det J| (assembly.py:320-326)."""
+        assembly.py:197-219) and the reaction carries |det J| (assembly.py:320-326).
+        ``lift`` (N_s coefficients of u0, numpy or device; the u0 lifting of DESIGN section 7, absent
+        in the reference): the reaction sees the lifted iterate u0 b_0 + u, the zero-iterate switch
+        needs u0 = 0 too, and ``lift_apply()`` returns the right-hand side correction A_{c,0} u0.
+        ``lift_in_reaction=False`` keeps the Kronecker reaction term of the zero iterate (an operator
+        that only uses that channel as a plain mass term, like the recovery right-hand side's)."""
         sd = spatial_data
         if sd is not None:
             if z_planes is not None or time_rows is not None:
@@ -105,7 +112,10 @@ class KroneckerOperator:
         sig = np.repeat(sig, d) if sig.size == 1 else sig
         if sig.size != d:
             raise ValueError("diffusion must be a scalar or one value per direction")
-        zero_iterate = _is_zero(u) and _is_zero(w)
+        has_lift = lift is not None and not _is_zero(lift)
+        if has_lift and time_rows is not None:
+            raise NotImplementedError("u0 lifting needs the whole time axis (not a time slab)")
+        zero_iterate = _is_zero(u) and _is_zero(w) and not (has_lift and lift_in_reaction)
         react = consts["c1"] * consts["a"] if zero_iterate else 0.0
         self.zero_iterate = zero_iterate
         stab = stabilization
@@ -182,6 +192,10 @@ class KroneckerOperator:
             _lib.call("mi_op_set_su_channel", ctx.handle, 2 + r, host_ptr(th), host_ptr(H), stab.ko)
         if not zero_iterate:
             from .reaction import set_reaction
+            if u is None or w is None:
+                zeros = ctx.empty(ctx.N_in).zero_()
+                u = zeros if u is None else u
+                w = zeros if w is None else w
             set_reaction(ctx, st, final_time, consts, u, w, None if sd is not None else L,
                          time_rows=self.time_rows, zslab=ctx.zslab)
             if sd is not None:
@@ -190,6 +204,35 @@ class KroneckerOperator:
                 _lib.call("mi_op_set_reaction_weight", ctx.handle, host_ptr(jw))
         else:
             _lib.call("mi_op_clear_reaction", ctx.handle)    # a reused context may carry one
+        self.has_lift = has_lift
+        if has_lift:
+            from .factors import su_time_lift
+            from .spaces import time_lift_columns
+            wcol, mcol = time_lift_columns(st, final_time)
+            col0 = np.zeros((nchan, ctx.nt))
+            col0[0] = capacitance * wcol
+            col0[1] = mcol
+            if R:
+                col0[2:] = su_time_lift(st, stab.tau, stab.lowrank, stab.capacitance)
+            self._lift = ctx.to_device(lift).contiguous()
+            if self._lift.numel() != ctx.ns_in:
+                raise ValueError("lifting coefficients must have one entry per spatial function (%d), got %d"
+                                 % (ctx.ns_in, self._lift.numel()))
+            _lib.call("mi_op_set_lift", ctx.handle, host_ptr(np.ascontiguousarray(col0)), dptr(self._lift))
+        else:
+            _lib.call("mi_op_set_lift", ctx.handle, None, None)
+        # pack the channels for the tensor cores now and drop the plain stencil copy
+        _lib.call("mi_op_finalize", ctx.handle)
+
+    def lift_apply(self):
+        """A_{c,0} u0: every term's lifted column applied to the lifting coefficients (device tensor,
+        length N); the sweep solves A u~ = f - lift_apply()."""
+        y = self.ctx.empty(self.num_time * self.num_space)
+        if not self.has_lift:
+            return y.zero_()
+        self.ctx.bind_stream()
+        _lib.call("mi_op_apply_lift", self.ctx.handle, dptr(y))
+        return y
 
     @property
     def shape(self):
@@ -278,6 +321,7 @@ class SpatialMassOperator:
         Ms, _ = mapped_stencils(ctx, sd)
         _lib.call("mi_op_set_channel_stencil", ctx.handle, 0, dptr(Ms))
         _lib.call("mi_op_clear_reaction", ctx.handle)
+        _lib.call("mi_op_finalize", ctx.handle)
         torch.cuda.current_stream(ctx.device).synchronize()
 
     def apply_device(self, x, y):

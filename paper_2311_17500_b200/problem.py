@@ -91,6 +91,10 @@ class MonodomainProblem:
     c1: float = 0.26
     c2: float = 0.1
     d_e: float = 1.0
+    # extension (BASELINE's stimuli; absent in the reference): initial potential u0 as a
+    # callable on (n, d) physical points or as N_s spline coefficients; lifted as u0_h(x) b_0(t) with
+    # u0_h the Greville quasi-interpolant (lift_coefficients).  None = the reference (u vanishes at t=0).
+    u0: object = None
 
     def __post_init__(self):
         for name in ("C_m", "a", "b", "c1", "c2", "d_e"):
@@ -130,6 +134,33 @@ class MonodomainProblem:
 
     def reaction_constants(self):
         return {"c1": self.c1, "a": self.a, "c2": self.c2}
+
+
+def lift_coefficients(problem):
+    """N_s coefficients of u0_h = sum_s u0(F(gamma_s)) B_s (Schoenberg quasi-interpolant at the tensor
+    Greville abscissae gamma_s, mapped to physical points): monotone, so a step u0 stays in its range.
+    None when the problem has no (or a zero) u0."""
+    from .spaces import greville_points
+    u0 = problem.u0
+    if u0 is None:
+        return None
+    st = problem.space
+    if callable(u0):
+        eta = greville_points(st.spatial)
+        aff = getattr(problem.geometry, "affine_scales", None)
+        if aff is not None:
+            L, off = aff
+            x = np.asarray(off, float)[None, :] + eta * np.asarray(L, float)[None, :]
+        else:
+            d = len(st.spatial)
+            axes = [greville(s) for s in st.spatial]
+            x = np.asarray(problem.geometry.grid_data(axes, order=0)["x"]).reshape(-1, d)
+        c = np.asarray(u0(x), float).reshape(-1)
+    else:
+        c = np.asarray(u0, float).reshape(-1)
+    if c.size != st.num_space:
+        raise ValueError("u0 needs one coefficient per spatial function (%d), got %d" % (st.num_space, c.size))
+    return None if not np.any(c) else c
 
 
 @dataclass
@@ -185,6 +216,7 @@ class SolveResult:
     wall_time: float = 0.0
     indicator: object = None
     phase_seconds: dict = field(default_factory=dict)   # device driver only: wall time per phase
+    lift: object = None   # u0 lifting coefficients (N_s) when the problem has u0: u_h = lift b_0 + u
 
     @property
     def avg_gmres(self):
@@ -255,6 +287,7 @@ class GaussGrid:
         tx, tw = gauss_rule(st.time.breakpoints, st.time.degree + 1)
         self.tx, self.tw = tx, tw
         self.tB = [basis_table(st.time, tx, o)[:, 1:] for o in range(2)]   # constrained time basis
+        self.tB0 = [basis_table(st.time, tx, o)[:, 0].copy() for o in range(2)]   # the dropped b_0 (lifting)
 
     def field(self, coeffs, space_orders, time_order):
         """Values on the grid (Q_t, Q_d, ..., Q_1) of a coefficient vector."""
@@ -418,9 +451,23 @@ def _mapped_laplacian(problem, g, u):
     return problem.D * lap
 
 
-def compute_theta(problem, u, w, grid=None):
-    """Residual indicator (stabilization.py:235-339) on a box or (host numpy, map Hessians) a mapped
-    geometry."""
+def compute_theta(problem, u, w, grid=None, device=0, lift=None):
+    """Residual indicator (stabilization.py:235-339): the drop-in name runs the device indicator
+    (theta.DeviceIndicator on boxes, theta.MappedDeviceIndicator on mapped geometries; ``grid`` is
+    accepted for signature compatibility).  ``lift``: the indicator of the lifted field."""
+    from .geometry import is_mapped
+    from .theta import DeviceIndicator, MappedDeviceIndicator
+    cls = MappedDeviceIndicator if is_mapped(problem.geometry) else DeviceIndicator
+    ind = cls(problem, device)
+    try:
+        return ind.compute(u, w, lift=lift)
+    finally:
+        ind.close()
+
+
+def host_compute_theta(problem, u, w, grid=None):
+    """Host numpy restatement of compute_theta on a box or (map Hessians) a mapped geometry.  Used only
+    by tests to cross-check the device kernels; no solver path calls it."""
     st = problem.space
     g = grid if grid is not None else GaussGrid(st, problem.geometry)
     d, T = g.d, g.T

@@ -17,6 +17,8 @@ the path needs:
   z planes and all time rows of n_2/G y-columns), the direction-3 transform
   and the time stage (Q^T, arrowhead, Q) locally, the inverse direction-3
   transform, the inverse all-to-all, the inverse direction-2/1 transforms.
+  The direction-2/3 transforms write / read the all-to-all buffers in their
+  send / receive layouts (addressing maps), so nothing packs or unpacks.
 * GMRES: the CGS2 dot products and norms are summed with all_reduce; the
   Hessenberg recurrence is replicated on every rank (krylov.gmres_core).
 
@@ -151,9 +153,16 @@ class ShardedOperator:
 
 
 class ShardedPreconditioner:
-    """z_own = (P^-1 r)_own with two all-to-all transposes (``apply_device``)."""
+    """z_own = (P^-1 r)_own with two all-to-all transposes (``apply_device``).
+
+    The direction-2 and -3 mode products read and write the all-to-all send / receive layouts
+    directly through addressing maps (mi_pc_mode_mapped): element (o, r, c) of a mode product lives
+    at map[r, 0] + o map[r, 1] + c, so no packing copies run around the transposes.
+      send (to rank q: its y columns of my planes)   block q = (N_t, nz, ny_q, n_1)
+      recv (from rank r: my y columns of its planes) block r = (N_t, nz_r, ny, n_1)"""
 
     def __init__(self, layout, backend, group=None):
+        import numpy as np
         self.layout, self.backend, self.group = layout, backend, group
         L = layout
         self.t1 = backend.empty(L.n_own)
@@ -164,66 +173,47 @@ class ShardedPreconditioner:
         # all-to-all splits: to rank q go my planes x its y columns; from rank r come its planes x my columns
         self.split_own = [L.nt * L.nz * (L.ys[q + 1] - L.ys[q]) * L.n1 for q in range(L.world)]
         self.split_blk = [L.nt * (L.zs[r + 1] - L.zs[r]) * L.ny * L.n1 for r in range(L.world)]
-
-    def _to_blk(self, s_own):
-        """(N_t, nz, n_2, n_1) owned slab -> (N_t, n_3, ny, n_1) y-slab via all-to-all."""
-        L = self.layout
-        S = s_own.view(L.nt, L.nz, L.n2, L.n1)
+        # direction-2 map over y (outer o = t nz + z, inner c = x) into the send layout
+        ms = np.zeros((L.n2, 2), dtype=np.int64)
         off = 0
         for q in range(L.world):
             y0, y1 = L.ys[q], L.ys[q + 1]
-            n = L.nt * L.nz * (y1 - y0) * L.n1
-            self.send[off:off + n].view(L.nt, L.nz, y1 - y0, L.n1).copy_(S[:, :, y0:y1])
-            off += n
-        if L.world > 1:
-            _all_to_all(self.blk2, self.send, self.split_blk, self.split_own, group=self.group)
-        else:
-            self.blk2.copy_(self.send)
-        B = self.blk.view(L.nt, L.n3, L.ny, L.n1)
+            ms[y0:y1, 0] = off + (np.arange(y0, y1) - y0) * L.n1
+            ms[y0:y1, 1] = (y1 - y0) * L.n1
+            off += self.split_own[q]
+        # direction-3 map over z (outer o = t, inner c = y' n_1 + x) into the receive layout
+        mr = np.zeros((L.n3, 2), dtype=np.int64)
         off = 0
         for r in range(L.world):
             z0, z1 = L.zs[r], L.zs[r + 1]
-            n = L.nt * (z1 - z0) * L.ny * L.n1
-            B[:, z0:z1].copy_(self.blk2[off:off + n].view(L.nt, z1 - z0, L.ny, L.n1))
-            off += n
-        return self.blk
-
-    def _from_blk(self, blk, s_own):
-        L = self.layout
-        B = blk.view(L.nt, L.n3, L.ny, L.n1)
-        off = 0
-        for r in range(L.world):
-            z0, z1 = L.zs[r], L.zs[r + 1]
-            n = L.nt * (z1 - z0) * L.ny * L.n1
-            self.blk2[off:off + n].view(L.nt, z1 - z0, L.ny, L.n1).copy_(B[:, z0:z1])
-            off += n
-        if L.world > 1:
-            _all_to_all(self.send, self.blk2, self.split_own, self.split_blk, group=self.group)
-        else:
-            self.send.copy_(self.blk2)
-        S = s_own.view(L.nt, L.nz, L.n2, L.n1)
-        off = 0
-        for q in range(L.world):
-            y0, y1 = L.ys[q], L.ys[q + 1]
-            n = L.nt * L.nz * (y1 - y0) * L.n1
-            S[:, :, y0:y1].copy_(self.send[off:off + n].view(L.nt, L.nz, y1 - y0, L.n1))
-            off += n
+            mr[z0:z1, 0] = off + (np.arange(z0, z1) - z0) * L.ny * L.n1
+            mr[z0:z1, 1] = (z1 - z0) * L.ny * L.n1
+            off += self.split_blk[r]
+        self.map_send = backend.index_map(ms)
+        self.map_recv = backend.index_map(mr)
 
     def apply_device(self, r_own, z_own):
         L, be = self.layout, self.backend
         # forward: U_1^T (contiguous), U_2^T (stride n_1) on the owned planes
         be.pc_mode(0, False, r_own, self.t1, L.nt * L.nz * L.n2, 1)
-        be.pc_mode(1, False, self.t1, self.t2, L.nt * L.nz, L.n1)
-        # one rank: the owned slab already is the y-slab (no transposes)
-        blk = self.t2 if L.world == 1 else self._to_blk(self.t2)
-        # y-slab: U_3^T (stride ny n_1), time stage in place, U_3
-        be.pc_mode(2, False, blk, self.blk2, L.nt, L.ny * L.n1)
-        be.pc_time_yslab(self.blk2, L.y_lo, L.y_hi)
-        be.pc_mode(2, True, self.blk2, blk, L.nt, L.ny * L.n1)
-        if L.world > 1:
-            self._from_blk(blk, self.t2)
-        be.pc_mode(1, True, self.t2, self.t1, L.nt * L.nz, L.n1)
-        be.pc_mode(0, True, self.t1, z_own, L.nt * L.nz * L.n2, 1)
+        if L.world == 1:
+            # one rank: the owned slab already is the y-slab (no transposes)
+            be.pc_mode(1, False, self.t1, self.t2, L.nt * L.nz, L.n1)
+            be.pc_mode(2, False, self.t2, self.blk2, L.nt, L.ny * L.n1)
+            be.pc_time_yslab(self.blk2, L.y_lo, L.y_hi)
+            be.pc_mode(2, True, self.blk2, self.t2, L.nt, L.ny * L.n1)
+            be.pc_mode(1, True, self.t2, self.t1, L.nt * L.nz, L.n1)
+            be.pc_mode(0, True, self.t1, z_own, L.nt * L.nz * L.n2, 1)
+            return
+        be.pc_mode(1, False, self.t1, self.send, L.nt * L.nz, L.n1, omap=self.map_send)
+        _all_to_all(self.blk2, self.send, self.split_blk, self.split_own, group=self.group)
+        # y-slab: U_3^T (stride ny n_1) from the receive layout, time stage in place, U_3 back into it
+        be.pc_mode(2, False, self.blk2, self.blk, L.nt, L.ny * L.n1, imap=self.map_recv)
+        be.pc_time_yslab(self.blk, L.y_lo, L.y_hi)
+        be.pc_mode(2, True, self.blk, self.blk2, L.nt, L.ny * L.n1, omap=self.map_recv)
+        _all_to_all(self.send, self.blk2, self.split_own, self.split_blk, group=self.group)
+        be.pc_mode(1, True, self.send, self.t2, L.nt * L.nz, L.n1, imap=self.map_send)
+        be.pc_mode(0, True, self.t2, z_own, L.nt * L.nz * L.n2, 1)
 
 
 def allreduce_sum(group=None):
@@ -274,11 +264,20 @@ class DeviceSlabBackend:
     def apply_in(self, x_in, y_own):
         self.op.apply_device(x_in, y_own)
 
-    def pc_mode(self, l, inverse, src, dst, outer, inner):
+    def index_map(self, m):
+        """(n, 2) int64 addressing map of mi_pc_mode_mapped, on the device."""
+        return torch.from_numpy(m).to(self.device).contiguous()
+
+    def pc_mode(self, l, inverse, src, dst, outer, inner, imap=None, omap=None):
         from .device import dptr
         self.pc.ctx.bind_stream()
-        self._lib.call("mi_pc_mode", self.pc.ctx.handle, l, 1 if inverse else 0, dptr(src), dptr(dst),
-                       int(outer), int(inner))
+        if imap is None and omap is None:
+            self._lib.call("mi_pc_mode", self.pc.ctx.handle, l, 1 if inverse else 0, dptr(src), dptr(dst),
+                           int(outer), int(inner))
+        else:
+            self._lib.call("mi_pc_mode_mapped", self.pc.ctx.handle, l, 1 if inverse else 0, dptr(src), dptr(dst),
+                           int(outer), int(inner), None if imap is None else dptr(imap),
+                           None if omap is None else dptr(omap))
 
     def pc_time_yslab(self, blk, y_lo, y_hi):
         from .device import dptr

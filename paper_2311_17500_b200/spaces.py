@@ -220,3 +220,18 @@ def time_factors(st, final_time):
     """(W_t, M_t): constrained time advection and T-scaled mass (assembly.py:125-134)."""
     M, _, W = univariate_factors(st.time)
     return W[1:, 1:].copy(), final_time * M[1:, 1:]
+
+
+def time_lift_columns(st, final_time):
+    """(W[1:, 0], T M[1:, 0]): the columns of the FULL time factors that couple the constrained rows to
+    the dropped first function b_0 (the u0 lifting)."""
+    M, _, W = univariate_factors(st.time)
+    return W[1:, 0].copy(), final_time * M[1:, 0]
+
+
+def greville_points(spaces):
+    """Tensor Greville abscissae as (N_s, d) parametric points, direction 1 fastest (C order)."""
+    d = len(spaces)
+    g = [greville(s) for s in spaces]
+    mesh = np.meshgrid(*[g[l] for l in reversed(range(d))], indexing="ij")
+    return np.stack([mesh[d - 1 - l].ravel() for l in range(d)], axis=1)

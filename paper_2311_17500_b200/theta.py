@@ -131,15 +131,23 @@ class DeviceIndicator:
         _lib.call("mi_window_max", self.ctx.handle, dptr(src), dptr(dst), int(outer), int(n_in), len(wins),
                   int(inner), host_ptr(w0), host_ptr(w1))
 
-    def compute(self, u, w, on_device=False):
+    def compute(self, u, w, on_device=False, lift=None):
         """ResidualIndicator for the state (u, w) (numpy or device tensors of length N).  With
-        ``on_device`` its values stay a CUDA tensor (the driver relaxes and factorises them there)."""
+        ``on_device`` its values stay a CUDA tensor (the driver relaxes and factorises them there).
+        ``lift`` (N_s coefficients of u0): the indicator of the lifted field u0 b_0 + u (DESIGN 7)."""
         ctx, st, d = self.ctx, self.st, self.d
         ctx.bind_stream()
         ud = ctx.to_device(u)
         wd = ctx.to_device(w)
         if ud.numel() != ctx.N or wd.numel() != ctx.N:
             raise ValueError("dimension mismatch: state of size %d for a space of size %d" % (ud.numel(), ctx.N))
+        if lift is not None:
+            ld = ctx.to_device(lift).contiguous()
+            if ld.numel() != ctx.ns:
+                raise ValueError("lifting coefficients must have one entry per spatial function")
+            _lib.call("mi_theta_set_lift", ctx.handle, dptr(ld))
+        else:
+            _lib.call("mi_theta_set_lift", ctx.handle, None)
         nel_t = self.nel[d]
         nes = int(np.prod(self.nel[:d]))
         emax = ctx.empty(nel_t * nes)
@@ -221,6 +229,7 @@ class MappedDeviceIndicator(DeviceIndicator):
             raise ValueError("MappedDeviceIndicator needs a mapped geometry")
         dev = self.ctx.device
         self.tB = [torch.tensor(np.asarray(t), device=dev) for t in g.tB]
+        self.tB0 = [torch.tensor(np.asarray(t), device=dev) for t in g.tB0]
         self.sB = [[torch.tensor(np.asarray(t), device=dev) for t in tl] for tl in g.sB]
         # per spatial Gauss point: cg_i = -sum_ab m_ab sum_c H_abc (J^-1)_ic, cm_ab = m_ab (x2 off-diagonal)
         hess = sd.geo.grid_data([r[0] for r in sd.rules], order=2)["hess"]
@@ -244,8 +253,9 @@ class MappedDeviceIndicator(DeviceIndicator):
         self.win_t = [window_elements(st.time, c) for c in range(st.num_time)]
         self.win_s = [[window_elements(s, i) for i in range(s.dimension)] for s in st.spatial]
 
-    def _fields(self, U, W, et0, et1):
-        """(3 + d + d(d+1)/2, rows, G_s) Gauss-point fields of time elements [et0, et1)."""
+    def _fields(self, U, W, et0, et1, lift=None):
+        """(3 + d + d(d+1)/2, rows, G_s) Gauss-point fields of time elements [et0, et1); ``lift`` adds
+        u0 b_0 to u (the dropped time function's column of the full time tables)."""
         st, d = self.st, self.d
         qt = st.time.degree + 1
         r0, r1 = et0 * qt, et1 * qt
@@ -268,8 +278,13 @@ class MappedDeviceIndicator(DeviceIndicator):
                 out = memo[k]
             return out
 
-        Ut = (self.tB[0][r0:r1] @ U).reshape((r1 - r0,) + shape)
-        Utt = (self.tB[1][r0:r1] @ U).reshape((r1 - r0,) + shape)
+        Ut = self.tB[0][r0:r1] @ U
+        Utt = self.tB[1][r0:r1] @ U
+        if lift is not None:
+            Ut = Ut + torch.outer(self.tB0[0][r0:r1], lift)
+            Utt = Utt + torch.outer(self.tB0[1][r0:r1], lift)
+        Ut = Ut.reshape((r1 - r0,) + shape)
+        Utt = Utt.reshape((r1 - r0,) + shape)
         Wt = (self.tB[0][r0:r1] @ W).reshape((r1 - r0,) + shape)
         zero = [0] * d
         outs = [spatial(Ut, ("u",), zero), spatial(Utt, ("ut",), zero), spatial(Wt, ("w",), zero)]
@@ -286,10 +301,11 @@ class MappedDeviceIndicator(DeviceIndicator):
         return torch.stack([v.reshape(r1 - r0, -1) if v is not None else torch.zeros_like(ref).reshape(r1 - r0, -1)
                             for v in outs]).contiguous()
 
-    def compute(self, u, w, on_device=False):
+    def compute(self, u, w, on_device=False, lift=None):
         ctx, st, d = self.ctx, self.st, self.d
         ctx.bind_stream()
         ud, wd = ctx.to_device(u), ctx.to_device(w)
+        ld = None if lift is None else ctx.to_device(lift).reshape(-1)
         if ud.numel() != ctx.N or wd.numel() != ctx.N:
             raise ValueError("dimension mismatch: state of size %d for a space of size %d" % (ud.numel(), ctx.N))
         U, W = ud.view(st.num_time, -1), wd.view(st.num_time, -1)
@@ -306,7 +322,7 @@ class MappedDeviceIndicator(DeviceIndicator):
             step = max(1, self.chunk_points // (qt * int(np.prod(self.G))))
             chunks = ((e0, min(nel_t, e0 + step), None) for e0 in range(0, nel_t, step))
         for et0, et1, fd in chunks:
-            F = self._fields(U, W, et0, et1)
+            F = self._fields(U, W, et0, et1, ld)
             _lib.call("mi_theta_mapped_elements", ctx.handle, dptr(F), dptr(self.coef),
                       dptr(fd) if fd is not None else None, int(et0), int(et1), host_ptr(self.G), self.q, qt,
                       host_ptr(nel), float(pr.D), float(pr.C_m) / self.T, float(pr.c1), float(pr.a), float(pr.c2),

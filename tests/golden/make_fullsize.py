@@ -1,6 +1,7 @@
 """Full-size golden fixtures at the BASELINE configs, produced by the REFERENCE package here.
 
-Run in the build container (the reference is mounted read-only; needs ~35 GB of host RAM for cfg 4):
+Run in the build container (the reference is mounted read-only) or, for cfg 4 (~65 GB of host RAM), on a
+GPU box host against the identical package installed under baseline/_ref:
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_fullsize.py [cfg ...]
 
@@ -17,7 +18,8 @@ What the reference can run at each size (SURVEY 8c limits):
 
 * cfg 2 (2D p=3 128^2 x 256, N = 4.4 M): the full potential system at sweep 1 -- Galerkin terms,
   zero-iterate reaction and the Spline Upwind terms of the seeded front indicator (R = 6) --
-  A x, P^-1 x, P^-1 A x, and ``gmres(op, rhs, precond=P, tol=1e-8, max_iter=300)``.
+  A x, P^-1 x, P^-1 A x, and ``gmres(op, f, precond=P, tol=1e-8, max_iter=300)`` with f the load vector
+  of the corner-square pulse 1[x<0.1, y<0.1] 1[t<0.05] (the first fixed-point sweep's system).
 * cfg 3 (3D p=2 64^3 x 128, N = 37 M, sigma = diag(1e-3, 4e-4, 4e-4)): the separable operator with the
   zero-iterate reaction (SU assembly does not fit: Kronecker collocation ~4e9 nnz), P^-1.
 * cfg 4 (3D p=3 96^3 x 192, N = 188 M): the same separable operator and P^-1 (31 GB of CSR).
@@ -34,7 +36,12 @@ import numpy as np
 import scipy.sparse as sp
 
 sys.dont_write_bytecode = True
-sys.path.insert(0, "/root/reference/pkg/src")
+# the read-only reference checkout (build container), else the same unmodified package installed under
+# baseline/_ref (a GPU box host: cfg 4 needs more RAM than the build container has)
+_REF = "/root/reference/pkg/src"
+if not os.path.isdir(_REF):
+    _REF = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))), "baseline", "_ref")
+sys.path.insert(0, _REF)
 
 from monoiga.assembly import (  # noqa: E402
     KroneckerOperator, SpatialQuadratureData, UnivariateMatrices, spatial_operators, time_matrices)
@@ -65,6 +72,11 @@ def summary(prefix, v, nt, ns, idx, probe):
     V = v.reshape(nt, ns)
     return {prefix + "_val": v[idx], prefix + "_rownorm": np.linalg.norm(V, axis=1),
             prefix + "_rowdot": np.einsum("ij,ij->i", V, probe.reshape(nt, ns)), prefix + "_norm": np.linalg.norm(v)}
+
+
+def corner_pulse(x, t):
+    """cfg-2 stimulus stand-in as a source (the reference has no u0): 1 on [0,0.1]^2 for t < 0.05."""
+    return 1.0 * (x[:, 0] < 0.1) * (x[:, 1] < 0.1) * (t < 0.05)
 
 
 def front(st):
@@ -134,15 +146,22 @@ def run(cfg):
     out["ref_seconds"] = np.array([t2 - t1, t3 - t2])
     print("cfg %d: A x %.1f s, P^-1 x %.1f s" % (cfg, t2 - t1, t3 - t2), flush=True)
     if cfg == 2:
-        rhs = np.random.default_rng(2).standard_normal(N)
+        # the first fixed-point sweep's system: the load vector of the corner-square pulse
+        from monoiga.assembly import rhs_vectors
+        geo = builtin_geometry("unit_square", final_time=1.0)
+        rhs, _ = rhs_vectors(st, geo, corner_pulse, np.zeros(N), 0.013)
+        out.update(summary("rhs", rhs, nt, ns, idx, probe))
         t4 = time.perf_counter()
         sol, it, hist = gmres(op, rhs, precond=P, tol=1e-8, max_iter=300)
         out.update(summary("gm_x", sol, nt, ns, idx, probe))
         out.update(gm_it=it, gm_hist=np.array(hist), gm_seconds=time.perf_counter() - t4)
         print("cfg 2: gmres %d iterations in %.1f s" % (it, time.perf_counter() - t4), flush=True)
-    np.savez_compressed(os.path.join(HERE, "fullsize_cfg%d.npz" % cfg), **out)
+    out["reference_path"] = _REF
+    tmp = os.path.join(HERE, "fullsize_cfg%d.tmp.npz" % cfg)
+    np.savez_compressed(tmp, **out)
+    os.replace(tmp, os.path.join(HERE, "fullsize_cfg%d.npz" % cfg))
 
 
 if __name__ == "__main__":
-    for c in (sys.argv[1:] or ["2", "3", "4"]):
+    for c in (sys.argv[1:] or ["3", "4", "2"]):
         run(int(c))

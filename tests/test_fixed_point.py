@@ -24,7 +24,7 @@ def problem_for(g, name, D=1e-3):
 
 def test_compute_theta_matches_reference():
     import paper_2311_17500_b200.spaces as sp
-    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, compute_theta
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, host_compute_theta as compute_theta
     g = load("fixed_point")
     st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(2, 5), sp.SplineSpace.uniform(3, 4)], sp.SplineSpace.uniform(2, 6))
     prob = MonodomainProblem(BoxGeometry([1.0, 1.0], 2.0), st, source=pulse_source, D=1e-2)

@@ -179,16 +179,25 @@ def test_reaction_rows_vs_oracle(setup):
     opb.ctx.close()
 
 
+def corner_pulse(x, t):
+    return 1.0 * (x[:, 0] < 0.1) * (x[:, 1] < 0.1) * (t < 0.05)
+
+
 def test_gmres_vs_reference(setup):
-    """cfg 2: the sweep-1 system (Galerkin + zero-iterate reaction + SU), gmres(tol=1e-8,
-    max_iter=300) from a seeded N(0,1) rhs: equal iteration count, equal history, x to 1e-10."""
+    """cfg 2: the first fixed-point sweep's system (Galerkin + zero-iterate reaction + SU) with the
+    load vector of the corner-square pulse: the load vector itself (rhs_vectors, assembly.py:350-398),
+    then gmres(tol=1e-8, max_iter=300): equal iteration count, equal history, x to 1e-10."""
     import torch
+    from paper_2311_17500_b200.problem import BoxGeometry, load_vector
     s = setup
     if s.cfg != 2:
         pytest.skip("the reference's GMRES runs at cfg 2 (dense H and CSR SU beyond)")
     op = s.operator(su=True)
     P = s.precond(op)
-    b = torch.from_numpy(np.random.default_rng(2).standard_normal(s.N)).to(s.dev)
+    f = load_vector(s.st, BoxGeometry([1.0, 1.0], 1.0), corner_pulse, device=0)
+    b = f if torch.is_tensor(f) else torch.from_numpy(np.ascontiguousarray(f))
+    b = b.to(s.dev)
+    check_summary(s.g, "rhs", b, 1e-12, s.probe)
     x, it, hist = s.mb.gmres(op, b, precond=P, tol=1e-8, max_iter=300)
     assert it == int(s.g["gm_it"])
     np.testing.assert_allclose(hist, s.g["gm_hist"], rtol=1e-6, atol=1e-14)

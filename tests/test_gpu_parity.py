@@ -151,3 +151,33 @@ def test_apply_stream_matches_serial(depth):
         assert np.array_equal(z.numpy(), ref_z)
     with pytest.raises(ValueError):
         mb.ApplyStream(op, P).run(xs[:1], [torch.empty(3, dtype=torch.float64)])
+
+
+@pytest.mark.parametrize("k", [1, 5, 13, 31, 40])
+def test_fused_cgs_passes_are_bitwise_the_two_pass_kernels(k):
+    """mi_cgs_pass / mi_cgs_norm_pass (one read of V per CGS2 subtraction + reduction) equal
+    mi_sub_combination followed by mi_dots bit for bit (linalg.py:405-412)."""
+    import torch
+    from paper_2311_17500_b200.device import DeviceContext
+    from paper_2311_17500_b200.krylov import DeviceVecOps
+    import paper_2311_17500_b200 as mb
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(2, 30)], mb.SplineSpace.uniform(2, 40))
+    ctx = DeviceContext(st, 0)
+    ops = DeviceVecOps(ctx)
+    n = 1_000_003
+    g = torch.Generator(device="cuda").manual_seed(k)
+    V = torch.randn(k + 1, n, dtype=torch.float64, device="cuda", generator=g)
+    w0 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    h = torch.randn(k, dtype=torch.float64, device="cuda", generator=g)
+    wa, wb = w0.clone(), w0.clone()
+    ha, hb = torch.zeros(k, dtype=torch.float64, device="cuda"), torch.zeros(k, dtype=torch.float64, device="cuda")
+    ops.sub_comb(V, k, h, wa)
+    ops.dots(V, k, wa, ha)
+    ops.sub_dots(V, k, h, wb, hb)
+    assert torch.equal(wa, wb) and torch.equal(ha, hb)
+    na, nb = torch.zeros(1, dtype=torch.float64, device="cuda"), torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.sub_comb(V, k, ha, wa)
+    ops.dots(wa.view(1, -1), 1, wa, na)
+    ops.sub_norm(V, k, hb, wb, nb)
+    assert torch.equal(wa, wb) and torch.equal(na, nb)
+    ctx.close()

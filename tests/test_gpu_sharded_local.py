@@ -61,6 +61,23 @@ def test_slab_backend_matches_reference(name, world, variant):
                 orf = torch.empty(n, dtype=torch.float64)
                 ref.pc_mode(l, inv, torch.from_numpy(src), orf, outer, inner)
                 assert rel(od.cpu().numpy(), orf.numpy()) < 1e-12, (rank, l, inv)
+        # the transposes' addressing maps (send layout for direction 2, receive layout for direction 3)
+        if world > 1:
+            spc_d = sh.ShardedPreconditioner(L, dev)
+            spc_r = sh.ShardedPreconditioner(L, ref)
+            for l, outer, inner, n_in, n_out, key in [(1, L.nt * L.nz, L.n1, L.n_own, L.n_own, "send"),
+                                                      (2, L.nt, L.ny * L.n1, L.n_blk, L.n_blk, "recv")]:
+                for inv in (False, True):
+                    for side in ("in", "out"):
+                        mp_d = getattr(spc_d, "map_" + key)
+                        mp_r = getattr(spc_r, "map_" + key)
+                        src = rng.uniform(-1, 1, n_in)
+                        od, orf = dev.empty(n_out).zero_(), torch.zeros(n_out, dtype=torch.float64)
+                        kw_d = {"imap": mp_d} if side == "in" else {"omap": mp_d}
+                        kw_r = {"imap": mp_r} if side == "in" else {"omap": mp_r}
+                        dev.pc_mode(l, inv, torch.from_numpy(src).cuda(), od, outer, inner, **kw_d)
+                        ref.pc_mode(l, inv, torch.from_numpy(src), orf, outer, inner, **kw_r)
+                        assert rel(od.cpu().numpy(), orf.numpy()) < 1e-12, (rank, l, inv, side)
         blk = rng.uniform(-1, 1, L.n_blk)
         bd = torch.from_numpy(blk).cuda()
         dev.pc_time_yslab(bd, L.y_lo, L.y_hi)

@@ -84,11 +84,25 @@ class NumpySlabBackend:
         yg = self.op.matvec(xg.ravel()).reshape(L.nt, L.n3, L.plane)
         y_own.copy_(torch.from_numpy(np.ascontiguousarray(yg[:, L.z_lo:L.z_hi]).ravel()))
 
-    def pc_mode(self, l, inverse, src, dst, outer, inner):
+    def index_map(self, m):
+        return m
+
+    def pc_mode(self, l, inverse, src, dst, outer, inner, imap=None, omap=None):
+        """mi_pc_mode / mi_pc_mode_mapped: element (o, r, c) at map[r, 0] + o map[r, 1] + c."""
         U = self.eigs[l][0]
+        n = U.shape[0]
         A = U if inverse else U.T
-        X = src.numpy().reshape(outer, U.shape[0], inner)
-        dst.copy_(torch.from_numpy(np.einsum("ij,ojc->oic", A, X).ravel()))
+        o = np.arange(outer)[:, None, None]
+        r = np.arange(n)[None, :, None]
+        c = np.arange(inner)[None, None, :]
+
+        def addr(m):
+            return (o * n + r) * inner + c if m is None else m[:, 0][r] + o * m[:, 1][r] + c
+
+        X = src.numpy()[addr(imap)]
+        Y = np.einsum("ij,ojc->oic", A, X)
+        out = dst.numpy()
+        out[addr(omap)] = Y
 
     def pc_time_yslab(self, blk, y_lo, y_hi):
         pen, L = self.pen, self.L

@@ -27,7 +27,7 @@ def problem_for(g, name):
 
 @pytest.mark.parametrize("name", CASES)
 def test_host_theta_matches_reference(name):
-    from paper_2311_17500_b200.problem import compute_theta
+    from paper_2311_17500_b200.problem import host_compute_theta as compute_theta
     g = load("theta")
     prob = problem_for(g, name)
     th = compute_theta(prob, g[name + "_u"], g[name + "_w"])
@@ -66,7 +66,7 @@ def test_device_theta_device_source(name, chunk):
 @pytest.mark.parametrize("p", [1, 2, 3])
 def test_device_theta_matches_host_2d(p):
     import paper_2311_17500_b200.spaces as sp
-    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, compute_theta
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, host_compute_theta as compute_theta
     from paper_2311_17500_b200.theta import DeviceIndicator
     st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(p, 7), sp.SplineSpace.uniform(p, 4)], sp.SplineSpace.uniform(p, 5))
     prob = MonodomainProblem(BoxGeometry([2.0, 0.7], 1.5), st, source=pulse_source, D=3e-2)
@@ -83,7 +83,7 @@ def test_device_theta_zero_denominator():
     """u = w = 0 with a source: denominator 0, stabilizer switched fully on where the residual is hot
     (stabilization.py:317-333), with the reference's warning."""
     import paper_2311_17500_b200.spaces as sp
-    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, compute_theta
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, host_compute_theta as compute_theta
     from paper_2311_17500_b200.theta import DeviceIndicator
     st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(2, 12)], sp.SplineSpace.uniform(2, 10))
     prob = MonodomainProblem(BoxGeometry([1.0], 1.0), st, source=pulse_source, D=1e-3)
@@ -100,7 +100,7 @@ def test_device_theta_zero_denominator():
 def test_device_theta_anisotropic_matches_host():
     """Diagonal anisotropic D (cfg 3's sigma; SURVEY App. B extension): device vs host restatement."""
     import paper_2311_17500_b200.spaces as sp
-    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, compute_theta
+    from paper_2311_17500_b200.problem import BoxGeometry, MonodomainProblem, host_compute_theta as compute_theta
     from paper_2311_17500_b200.theta import DeviceIndicator
     st = sp.SpaceTimeSpace([sp.SplineSpace.uniform(2, n) for n in (5, 4, 3)], sp.SplineSpace.uniform(2, 4))
     prob = MonodomainProblem(BoxGeometry([1.0, 0.8, 1.2], 1.0), st, source=pulse_source, D=[1e-1, 4e-2, 2e-2])

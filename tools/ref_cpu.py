@@ -14,7 +14,8 @@ Measured (BASELINE.md section 2 / SURVEY 8d, best of 2 unless stated):
 * ``apply_su_<mesh>``: the workload operator WITH the Spline Upwind terms (front indicator, tol 0.1)
   at the largest 3D p=3 meshes whose SU assembly finishes in minutes;
 * ``gmres_cfg2``: ``gmres(op, rhs, precond=P, tol=1e-8, max_iter=300)`` on the cfg-2 sweep-1 system
-  (Galerkin + zero-iterate reaction + SU, N = 4.4 M, seeded N(0,1) rhs) -- the same solve bench.py
+  (Galerkin + zero-iterate reaction + SU, N = 4.4 M, load vector of the corner-square pulse) -- the
+  same solve bench.py
   times on the GPU as ``gmres_cfg2``;
 * ``fixed_point_cfg1``: ``fixed_point_solve`` with Spline Upwind and ``linear_solver="iterative"``
   at cfg 1 (1D p=2 64x64), driven by the source pulse 1[x<0.1] 1[t<0.05] (the reference has no u0).
@@ -91,14 +92,21 @@ def time_apply(d, p, ne, ne_t, D, su, reps=2):
 
 
 def gmres_cfg2():
+    from monoiga.assembly import rhs_vectors
+    from monoiga.geometry import builtin_geometry
     from monoiga.linalg import gmres
+
+    def corner_pulse(x, t):
+        return 1.0 * (x[:, 0] < 0.1) * (x[:, 1] < 0.1) * (t < 0.05)
+
     st, op, P, rec = system(2, 3, 128, 256, 1e-3, True)
-    rhs = np.random.default_rng(2).standard_normal(st.num_dof)
+    rhs, _ = rhs_vectors(st, builtin_geometry("unit_square", final_time=1.0), corner_pulse,
+                         np.zeros(st.num_dof), 0.013)
     t0 = time.perf_counter()
     _, it, hist = gmres(op, rhs, precond=P, tol=1e-8, max_iter=300)
     rec.update(seconds=time.perf_counter() - t0, iterations=it, final_rel_residual=hist[-1],
                system="cfg2 sweep-1 system: Galerkin + zero-iterate reaction + SU (front indicator, tol 0.1), "
-                      "rhs ~ N(0,1) seed 2, tol 1e-8, max_iter 300")
+                      "rhs = load vector of the corner pulse 1[x<0.1, y<0.1] 1[t<0.05], tol 1e-8, max_iter 300")
     return rec
 
 
