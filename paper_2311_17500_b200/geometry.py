@@ -101,39 +101,53 @@ class GeometryMap:
 
 
 def jacobian_inverse_and_det(jac):
-    """geometry.py:207-214."""
+    """Inverse Jacobians and determinants of a grid of maps (the pull-back of geometry.py:207-214).
+
+    A point counts as singular when |det J| falls below SINGULAR_REL_TOL times the product of the
+    column norms of J (a scale-free test: a nearly degenerate but large map is still caught)."""
     det = np.linalg.det(jac)
-    scale = np.prod(np.linalg.norm(jac, axis=-2), axis=-1)
-    if np.any(np.abs(det) < SINGULAR_REL_TOL * np.maximum(scale, 1e-300)):
+    col_norms = np.linalg.norm(jac, axis=-2)
+    bound = SINGULAR_REL_TOL * np.maximum(np.prod(col_norms, axis=-1), 1e-300)
+    if (np.abs(det) < bound).any():
         raise GeometryError("singular Jacobian encountered during pull-back")
     return np.linalg.inv(jac), det
 
 
+def _format_row(values):
+    return " ".join(repr(float(v)) for v in values)
+
+
 def save_geometry(geo, path):
-    """geometry.py:309-323: dimension; degrees; knot counts; knot lines; control points."""
-    lines = [str(geo.dim), " ".join(str(s.degree) for s in geo.spaces),
-             " ".join(str(s.knots.size) for s in geo.spaces)]
-    for s in geo.spaces:
-        lines.append(" ".join("%.17g" % k for k in s.knots))
-    for row in geo.control_points:
-        lines.append(" ".join("%.17g" % v for v in row))
+    """Write a GeometryMap in the reference's plain-text layout (geometry.py:309-323), which
+    load_geometry (ours and the reference's) reads back bit for bit: a line with d, a line of
+    degrees, a line of knot counts, one line of knots per direction, then one control point per line
+    (direction 1 fastest)."""
+    header = [str(geo.dim),
+              " ".join(str(sp.degree) for sp in geo.spaces),
+              " ".join(str(len(sp.knots)) for sp in geo.spaces)]
+    body = [_format_row(sp.knots) for sp in geo.spaces] + [_format_row(pt) for pt in geo.control_points]
     with open(path, "w") as fh:
-        fh.write("\n".join(lines) + "\n")
+        fh.writelines(line + "\n" for line in header + body)
 
 
 def load_geometry(path, final_time=1.0):
-    """geometry.py:326-344."""
+    """Read the plain-text layout of save_geometry (geometry.py:326-344); blank lines and lines
+    starting with '#' are skipped."""
     with open(path) as fh:
-        tokens = [ln.split() for ln in fh if ln.strip() and not ln.startswith("#")]
-    d = int(tokens[0][0])
-    degrees = [int(v) for v in tokens[1][:d]]
-    counts = [int(v) for v in tokens[2][:d]]
-    spaces = [SplineSpace(np.array([float(v) for v in tokens[3 + l][:counts[l]]]), degrees[l]) for l in range(d)]
-    n = int(np.prod([s.dimension for s in spaces]))
-    rows = tokens[3 + d:3 + d + n]
-    if len(rows) != n:
-        raise ValueError("geometry file has %d control rows, expected %d" % (len(rows), n))
-    return GeometryMap(spaces, np.array([[float(v) for v in r[:d]] for r in rows]), final_time=final_time)
+        rows = [line.split() for line in fh if line.strip() and not line.lstrip().startswith("#")]
+    it = iter(rows)
+    dim = int(next(it)[0])
+    degrees = [int(v) for v in next(it)[:dim]]
+    counts = [int(v) for v in next(it)[:dim]]
+    spaces = []
+    for l in range(dim):
+        knots = np.asarray(next(it)[:counts[l]], dtype=float)
+        spaces.append(SplineSpace(knots, degrees[l]))
+    ncp = int(np.prod([sp.dimension for sp in spaces]))
+    ctrl = [row[:dim] for row in it][:ncp]
+    if len(ctrl) != ncp:
+        raise ValueError("geometry file has %d control rows, expected %d" % (len(ctrl), ncp))
+    return GeometryMap(spaces, np.asarray(ctrl, dtype=float), final_time=final_time)
 
 
 def is_mapped(geometry):

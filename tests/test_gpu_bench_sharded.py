@@ -43,5 +43,5 @@ def test_sharded_bench_path_matches_single_rank():
     ref = _run(1)
     for n in (2, 3):
         line = _run(n)
-        assert line["n_gpus"] == n and line["config"]["backend"] == "gloo"
+        assert line["n_gpus"] == n and line["sharding"]["backend"] == "gloo"
         assert abs(line["z_norm"] - ref["z_norm"]) <= 1e-12 * ref["z_norm"], (n, line["z_norm"], ref["z_norm"])

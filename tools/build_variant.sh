@@ -1,5 +1,5 @@
 #!/bin/bash
-# Build an alternative library with extra nvcc defines into exp/<name>.so (timing experiments only).
+# Build an alternative library with extra nvcc defines into varlib/<name>.so (timing experiments only).
 # usage: tools/build_variant.sh <name> "<extra nvcc flags>"
 set -e
 cd "$(dirname "$0")/.."
@@ -10,6 +10,6 @@ for f in paper_2311_17500_b200/csrc/*.cu; do
   pids="$pids $!"
 done
 for p in $pids; do wait $p || { echo "compile failed"; exit 1; }; done
-nvcc -shared -gencode arch=compute_100a,code=sm_100a -o exp/$name.so $tmp/*.o -lcudart
+mkdir -p varlib; nvcc -shared -gencode arch=compute_100a,code=sm_100a -o varlib/$name.so $tmp/*.o -lcudart
 rm -rf $tmp
-echo built exp/$name.so
+echo built varlib/$name.so

@@ -14,15 +14,16 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-# BASELINE configs 1-3.  The reference cannot take u0 != 0: each stimulus is a
-# source pulse on the same region for t < 0.05 (cfg 1: x < 0.1; cfg 2: the corner square
-# [0, 0.1]^2; cfg 3: the plane x < 0.05).
+# BASELINE configs 1-3 with their stimuli as INITIAL DATA u0 (the u0 lifting, DESIGN 7; cfg 1: u0 = 1
+# on x < 0.1; cfg 2: the corner square [0, 0.1]^2; cfg 3: the plane x < 0.05), no source.  The
+# reference cannot take u0 != 0; ``stimulus="pulse"`` runs the stand-in it can take
+# instead: a source pulse on the same region for t < 0.05.
 PRESETS = {1: dict(d=1, p=2, ne=64, ne_t=64, sigma=[1e-3], stim=0.1, corner=False),
            2: dict(d=2, p=3, ne=128, ne_t=256, sigma=[1e-3], stim=0.1, corner=True),
            3: dict(d=3, p=2, ne=64, ne_t=128, sigma=[1e-3, 4e-4, 4e-4], stim=0.05, corner=False)}
 
 
-def make_problem(d, p, ne, ne_t, sigma, stim, corner):
+def make_problem(d, p, ne, ne_t, sigma, stim, corner, stimulus="u0"):
     import numpy as np
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200.problem import BoxGeometry
@@ -43,19 +44,27 @@ def make_problem(d, p, ne, ne_t, sigma, stim, corner):
     # vector and the residual indicator are evaluated on the GPU
     pulse = mb.DeviceSource(pulse_host, pulse_torch)
 
+    def u0(x):
+        m = (x[:, 0] < stim).astype(float)
+        if corner:
+            m = m * (x[:, 1] < stim)
+        return m
+
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(d)], mb.SplineSpace.uniform(p, ne_t))
     D = sigma[0] if len(sigma) == 1 else list(sigma)
+    if stimulus == "u0":
+        return mb.MonodomainProblem(BoxGeometry([1.0] * d, 1.0), st, D=D, u0=u0)
     return mb.MonodomainProblem(BoxGeometry([1.0] * d, 1.0), st, source=pulse, D=D)
 
 
-def run(cfg=None, stab="spline_upwind", max_it=100, device=0, **kw):
+def run(cfg=None, stab="spline_upwind", max_it=100, device=0, stimulus="u0", **kw):
     """Full relaxed fixed-point solve; returns a JSON-able summary."""
     import torch
     import paper_2311_17500_b200 as mb
     spec = dict(PRESETS[cfg]) if cfg is not None else {}
     spec.update(kw)
     prob = make_problem(spec["d"], spec["p"], spec["ne"], spec["ne_t"], spec.get("sigma", [1e-3]),
-                        spec.get("stim", 0.1), spec.get("corner", False))
+                        spec.get("stim", 0.1), spec.get("corner", False), stimulus)
     config = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8,
                                  max_iterations=max_it)
     torch.cuda.synchronize()
@@ -64,6 +73,8 @@ def run(cfg=None, stab="spline_upwind", max_it=100, device=0, **kw):
     torch.cuda.synchronize()
     return {"cfg": cfg, "d": spec["d"], "p": spec["p"], "mesh": [spec["ne"]] * spec["d"] + [spec["ne_t"]],
             "N": prob.space.num_dof, "sigma": spec.get("sigma", [1e-3]), "stabilization": stab,
+            "stimulus": ("initial data u0 (lifting u0_h(x) b_0(t), DESIGN 7)" if stimulus == "u0" else
+                         "source pulse stand-in on the stimulus region for t < 0.05"),
             "wall_seconds": time.perf_counter() - t0, "sweeps": res.iterations, "converged": res.converged,
             "gmres_per_sweep": res.gmres_iterations, "avg_gmres": res.avg_gmres, "avg_pcg": res.avg_pcg,
             "phase_seconds": {k: round(v, 3) for k, v in res.phase_seconds.items()},
@@ -81,10 +92,11 @@ if __name__ == "__main__":
     ap.add_argument("--stim", type=float, default=0.1)
     ap.add_argument("--stab", default="spline_upwind")
     ap.add_argument("--max-it", type=int, default=100)
+    ap.add_argument("--stimulus", default="u0", choices=["u0", "pulse"])
     a = ap.parse_args()
     if a.cfg is not None:
-        out = run(a.cfg, a.stab, a.max_it)
+        out = run(a.cfg, a.stab, a.max_it, stimulus=a.stimulus)
     else:
-        out = run(None, a.stab, a.max_it, d=a.d, p=a.p, ne=a.ne, ne_t=a.ne_t, sigma=a.sigma, stim=a.stim,
-                  corner=False)
+        out = run(None, a.stab, a.max_it, stimulus=a.stimulus, d=a.d, p=a.p, ne=a.ne, ne_t=a.ne_t,
+                  sigma=a.sigma, stim=a.stim, corner=False)
     print(json.dumps(out))
