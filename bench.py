@@ -454,10 +454,48 @@ def run_sharded(args):
         "gpu_launches": sum(v[1] for v in prof.values()),
         "clocks": clk.summary(),
     }
+    del sop, spc, be, x, y, z
+    torch.cuda.empty_cache()
+    if not args.skip_extras:
+        try:
+            line["solve"] = sharded_solve_cfg3(torch, dist, mb, sh, rank, world, local, dev)
+        except Exception as exc:   # keep the headline line even if the extra fails
+            line["solve"] = {"error": repr(exc)[:300]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def sharded_solve_cfg3(torch, dist, mb, sh, rank, world, local, dev):
+    """BASELINE's "solve time at 1/2/4/8 GPUs" for cfg 3 (3D p=2 64^3 x 128, N = 37.1 M, anisotropic
+    sigma, SU front indicator, zero-iterate reaction): the z-sharded GMRES (tol 1e-8, seeded N(0,1)
+    rhs, the same system measure_solve times on one GPU), device time max over ranks."""
+    from paper_2311_17500_b200.spaces import greville
+    d, p, ne, ne_t = 3, 2, 64, 128
+    sigma = (1e-3, 4e-4, 4e-4)
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(d)], mb.SplineSpace.uniform(p, ne_t))
+    theta = front_indicator_np(st.time_greville(), greville(st.spatial[0]), st.num_space)
+    stab = mb.Stabilization(st, theta, 0.1, 1.0)
+    del theta
+    L = sh.ZSlabLayout(st.num_time, [s.dimension for s in st.spatial], p, rank, world)
+    be = sh.DeviceSlabBackend(L, st, 1.0, 1.0, sigma, RM, stabilization=stab, device=local)
+    sop, spc = sh.ShardedOperator(L, be), sh.ShardedPreconditioner(L, be)
+    b = torch.from_numpy(np.ascontiguousarray(L.own_slice(np.random.default_rng(2).standard_normal(st.num_dof))))
+    b = b.to(dev)
+    sh.sharded_gmres(sop, spc, be.vec_ops, b, tol=1e-2, max_iter=3)     # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record()
+    _, it, hist = sh.sharded_gmres(sop, spc, be.vec_ops, b, tol=1e-8, max_iter=200)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"config": "cfg3 3D p=2 64^3x128 (N=%d), sigma=diag(1e-3,4e-4,4e-4), SU rank %d, z-sharded x%d"
+                      % (st.num_dof, stab.rank, world),
+            "seconds": float(t.item()), "iterations": it, "final_rel_residual": hist[-1], "n_gpus": world}
 
 
 def measure_fixed_point_cfg1(torch, mb, dev, stimulus="u0"):

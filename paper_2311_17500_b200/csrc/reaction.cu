@@ -21,6 +21,9 @@
 
 #include <type_traits>
 
+#ifndef MI_RX_BAL
+#define MI_RX_BAL 1    // projection tiles on the warps with the fewest interpolation tiles (phase balance)
+#endif
 #ifndef MI_RX_NOCW
 #define MI_RX_NOCW 0   // timing ablation only (wrong results): the stored mode skips its coefficient reads
 #endif
@@ -230,8 +233,12 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
       btp = tid < QT * PW ? bv : bv * __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
     }
   };
-  // x-projection outputs of this thread: line 8 warp + fr, j1 = 2 fk + e
-  const int xline = 8 * warp + fr;
+  // projection tiles run on the warps in reverse order (pwarp): the interpolation tiles of the same
+  // phase fill the low warps first, so the phase's slowest warp does one tile fewer (d = 3, p = 3:
+  // x-interpolation 10 tiles + y-projection 5 tiles over 8 warps -> at most 2 per warp, was 3)
+  const int pwarp = MI_RX_BAL ? NW - 1 - warp : warp;
+  // x-projection outputs of this thread: line 8 pwarp + fr, j1 = 2 fk + e
+  const int xline = 8 * pwarp + fr;
   long long yidx[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
 
   // x projection of function ft: lines (j3, j2), K = q1, N = j1 -> y (from sC for D = 2, sD for D = 3)
   auto xproj = [&](int ft, const double* xb) {
-    if (warp < (NLX + 7) / 8) {
+    if (pwarp < (NLX + 7) / 8) {
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KP; ++ks) dmma(c0, c1, xb[xline * Q1 + 4 * ks + fk], bP[0][ks]);
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
       if (has_fp) {
         if constexpr (D == 3) {
           constexpr int NL = L3 * Q1;
-          for (int mt = warp; mt < (NL + 7) / 8; mt += NW) {
+          for (int mt = pwarp; mt < (NL + 7) / 8; mt += NW) {
             const int line = mt * 8 + fr;
             const int q1 = line % Q1, j3 = line / Q1;
             double c0 = 0.0, c1 = 0.0;

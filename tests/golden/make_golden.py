@@ -200,6 +200,33 @@ def theta_cases():
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fixed_point":
     fixed_point_cases()
 
+
+def fixed_point_3d_cases():
+    """3D box fixed-point solves with Spline Upwind (p = 2 and 3, ~2-3k DoFs, GMRES iterative):
+    the 3D counterparts of fixed_point_cases, compared sweep for sweep on the device."""
+    from monoiga.solver import fixed_point_solve
+    from monoiga.assembly import rhs_vectors
+    out = {}
+    cases = [("fp_3d_p2_su", 3, 2, (6, 5, 4), 8, "spline_upwind", 1e-2),
+             ("fp_3d_p3_su", 3, 3, (4, 3, 3), 6, "spline_upwind", 1e-2),
+             ("fp_3d_p2_off", 3, 2, (6, 5, 4), 8, "off", 1e-2)]
+    for name, d, p, nes, ne_t, stab, D in cases:
+        st = SpaceTimeSpace([SplineSpace.uniform(p, n) for n in nes], SplineSpace.uniform(p, ne_t))
+        geo = builtin_geometry("unit_cube", final_time=1.0)
+        prob = MonodomainProblem(geo, st, source=pulse_source, D=D)
+        res = fixed_point_solve(prob, FixedPointConfig(stabilization=stab, linear_solver="iterative"))
+        fv, _ = rhs_vectors(st, geo, pulse_source, np.zeros(st.num_dof), prob.b)
+        out.update({name + "_u": res.u, name + "_w": res.w, name + "_it": res.iterations,
+                    name + "_inc": np.array(res.increments), name + "_gm": np.array(res.gmres_iterations),
+                    name + "_pcg": np.array(res.pcg_iterations), name + "_d": d, name + "_p": p,
+                    name + "_ne": np.array(nes), name + "_ne_t": ne_t, name + "_D": D, name + "_f": fv})
+        print(name, "N", st.num_dof, "sweeps", res.iterations, "gmres", res.gmres_iterations[:5], flush=True)
+    np.savez_compressed(os.path.join(HERE, "fixed_point_3d.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fixed_point_3d":
+    fixed_point_3d_cases()
+
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "theta":
     theta_cases()
 

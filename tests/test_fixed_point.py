@@ -101,3 +101,30 @@ def test_fixed_point_solve_device_source(name):
     for key in ("u", "w"):
         ref = g[name + "_" + key]
         assert np.linalg.norm(getattr(res, key) - ref) / np.linalg.norm(ref) < 1e-10, key
+
+
+SWEEPS_3D = ["fp_3d_p2_su", "fp_3d_p3_su", "fp_3d_p2_off"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SWEEPS_3D)
+def test_fixed_point_solve_3d_matches_reference(name):
+    """3D boxes (p = 2, 3; Spline Upwind and Galerkin): the device driver vs the reference's own
+    fixed_point_solve, sweep for sweep (tests/golden/make_golden.py fixed_point_3d)."""
+    import os
+    from cases import GOLDEN
+    from paper_2311_17500_b200.fixed_point import fixed_point_solve
+    from paper_2311_17500_b200.problem import FixedPointConfig
+    if not os.path.exists(os.path.join(GOLDEN, "fixed_point_3d.npz")):
+        pytest.skip("fixture not generated")
+    g = load("fixed_point_3d")
+    prob = problem_for(g, name, D=float(g[name + "_D"]))
+    stab = "off" if name.endswith("off") else "spline_upwind"
+    res = fixed_point_solve(prob, FixedPointConfig(stabilization=stab, linear_solver="iterative"))
+    assert res.iterations == int(g[name + "_it"])
+    assert res.gmres_iterations == [int(v) for v in g[name + "_gm"]]
+    assert res.pcg_iterations == [int(v) for v in g[name + "_pcg"]]
+    for key in ("u", "w"):
+        ref = g[name + "_" + key]
+        assert np.linalg.norm(getattr(res, key) - ref) / np.linalg.norm(ref) < 1e-10, key
+    np.testing.assert_allclose(res.increments, g[name + "_inc"], rtol=1e-8)

@@ -209,3 +209,25 @@ def test_lifted_fixed_point_matches_oracle(name, d, p, nes, ne_t, D, u0, stab):
     assert rel(res.u, ref["u"]) < 1e-10
     assert rel(res.w, ref["w"]) < 1e-10
     np.testing.assert_allclose(res.increments, ref["increments"], rtol=1e-8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,p", [(1, 2), (2, 3), (3, 2)])
+def test_recovery_solver_matches_solve_w_system(d, p):
+    """wsolve.RecoverySolver (device) vs the restatement of solve_w_system + pcg +
+    KroneckerMassPreconditioner (linalg.py:176-203, 450-547): w to 1e-12 and equal PCG counts."""
+    import paper_2311_17500_b200 as mb
+    from oracle import assembly as asm
+    from oracle import lifting
+    from oracle.splines import make_space_time
+    from paper_2311_17500_b200.wsolve import RecoverySolver
+    nes = {1: (13,), 2: (6, 5), 3: (4, 3, 5)}[d]
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, n) for n in nes], mb.SplineSpace.uniform(p, 7))
+    ost = make_space_time(d, p, nes, 7)
+    g = np.random.default_rng(d).standard_normal(st.num_dof)
+    w, its = RecoverySolver(st, 1.3, 0.013, 1.0, 1e-8).solve(g)
+    Wt, Mt = asm.time_factors(ost, 1.3)
+    Ms, _ = asm.box_spatial(ost.spatial)
+    wr, itr = lifting.solve_w(ost, Wt, Mt, Ms, 0.013, 1.0, g, 1e-8)
+    assert list(its) == list(itr)
+    assert rel(w, wr) < 1e-12
