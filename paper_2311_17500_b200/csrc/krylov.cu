@@ -9,6 +9,11 @@ namespace mi {
 constexpr int KB = 592;   // 4 x 148 SMs
 constexpr int KT = 256;
 constexpr int KG = 8;     // vectors per pass
+constexpr int KU = 4;     // elements per thread per loop trip (independent loads in flight)
+
+// Every reduction below walks its block's chunk [lo, hi) in the same order -- thread t takes
+// j = lo + t + u KT for u < KU, then advances by KU KT -- so the fused and the two-pass kernels sum
+// in the same order and agree bit for bit.
 
 template <int G>
 __global__ void __launch_bounds__(KT) dots_partial(const double* __restrict__ V, long long ldv,
@@ -20,11 +25,21 @@ __global__ void __launch_bounds__(KT) dots_partial(const double* __restrict__ V,
   for (int g = 0; g < G; ++g) acc[g] = 0.0;
   const long long chunk = (n + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-  for (long long i = lo + threadIdx.x; i < hi; i += KT) {
-    const double wi = w[i];
+  for (long long b = lo + threadIdx.x; b < hi; b += KU * KT) {
+    double wv[KU], vv[KU][G];
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (k0 + g < k) acc[g] = fma(V[(long long)(k0 + g) * ldv + i], wi, acc[g]);
+    for (int u = 0; u < KU; ++u) {
+      const long long i = b + (long long)u * KT;
+      const bool ok = i < hi;
+      wv[u] = ok ? w[i] : 0.0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) vv[u][g] = (ok && k0 + g < k) ? V[(long long)(k0 + g) * ldv + i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < KU; ++u)
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (b + (long long)u * KT < hi && k0 + g < k) acc[g] = fma(vv[u][g], wv[u], acc[g]);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -84,8 +99,15 @@ __global__ void comb(const double* __restrict__ V, long long ldv, const double* 
 __global__ void scale_div(const double* __restrict__ x, const double* __restrict__ s, double* __restrict__ out,
                           long long n, int take_sqrt) {
   const double d = take_sqrt ? sqrt(*s) : *s;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
-    out[j] = x[j] / d;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < n; b += KU * stride) {
+    double v[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) v[u] = b + u * stride < n ? x[b + u * stride] : 0.0;
+#pragma unroll
+    for (int u = 0; u < KU; ++u)
+      if (b + u * stride < n) out[b + u * stride] = v[u] / d;
+  }
 }
 
 // Fused CGS2 passes (k <= KM basis vectors): each V entry is read ONCE for both the subtraction and the
@@ -106,21 +128,32 @@ __global__ void __launch_bounds__(KT) sub_reduce(const double* __restrict__ V, l
   for (int g = 0; g < NA; ++g) acc[g] = 0.0;
   const long long chunk = (n + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-  for (long long j = lo + threadIdx.x; j < hi; j += KT) {
-    double v[KM];
-    double s = 0.0;
+  for (long long b = lo + threadIdx.x; b < hi; b += KU * KT) {
+    double wn[KU];
 #pragma unroll
-    for (int i = 0; i < KM; ++i) {
-      v[i] = i < k ? V[(long long)i * ldv + j] : 0.0;
-      s = fma(hs[i], v[i], s);
+    for (int u = 0; u < KU; ++u) {
+      const long long j = b + (long long)u * KT;
+      double sacc = 0.0;
+      if (j < hi) {
+#pragma unroll 8
+        for (int i = 0; i < KM; ++i)
+          if (i < k) sacc = fma(hs[i], V[(long long)i * ldv + j], sacc);
+        wn[u] = w[j] - sacc;
+        w[j] = wn[u];
+      }
     }
-    const double wn = w[j] - s;
-    w[j] = wn;
-    if constexpr (MODE == 0) {
 #pragma unroll
-      for (int i = 0; i < KM; ++i) acc[i] = fma(v[i], wn, acc[i]);
-    } else {
-      acc[0] = fma(wn, wn, acc[0]);
+    for (int u = 0; u < KU; ++u) {
+      const long long j = b + (long long)u * KT;
+      if (j < hi) {
+        if constexpr (MODE == 0) {
+#pragma unroll
+          for (int i = 0; i < KM; ++i)
+            if (i < k) acc[i] = fma(V[(long long)i * ldv + j], wn[u], acc[i]);   // second read: L1
+        } else {
+          acc[0] = fma(wn[u], wn[u], acc[0]);
+        }
+      }
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -594,7 +594,6 @@ static int dmma_prepare(mi_ctx* c) {
           c->ns, per_group);
       MI_CHECK_LAUNCH("repack_frag");
     }
-#if !MI_STEN_FUSE
     if ((rc = dalloc(c->wbuf, (size_t)c->nchan * c->ns * ntp))) return rc;
     MI_CUDA(cudaMemsetAsync(c->wbuf.p, 0, sizeof(double) * c->nchan * c->ns * ntp, c->stream));
     {
@@ -613,9 +612,6 @@ static int dmma_prepare(mi_ctx* c) {
                                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       MI_REQUIRE(r == CUDA_SUCCESS, MI_ERR_CUDA, "cuTensorMapEncodeTiled (W) failed");
     }
-#else
-    mi::dfree(c->wbuf);   // the fused filter keeps W in shared memory
-#endif
     MI_CUDA(cudaFuncSetAttribute(stencil_dmma<D_, P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)G::SMEM));
   });
@@ -624,7 +620,6 @@ static int dmma_prepare(mi_ctx* c) {
   return rc;
 }
 
-#if !MI_STEN_FUSE
 // y = sum_c T_c (x) along time of the time-innermost W buffer (HBM-bound)
 static int launch_time_filter(mi_ctx* c, double* y) {
   MI_REQUIRE(c->nchan <= 64, MI_ERR_ARG, "too many channels for the time filter");
@@ -682,7 +677,6 @@ static int launch_time_filter(mi_ctx* c, double* y) {
   MI_CHECK_LAUNCH("time_filter_ti");
   return MI_OK;
 }
-#endif
 
 static int dmma_apply(mi_ctx* c, const double* x, double* y) {
   MI_DISPATCH_DP(c->d, c->p, {
@@ -704,14 +698,12 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
       stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");
     }
-#if !MI_STEN_FUSE
     {
       ProfScope ps(c, PROF_OP_TFILTER);
       int frc = launch_time_filter(c, y);
       if (frc) return frc;
       MI_CHECK_LAUNCH("time_filter_ti");
     }
-#endif
   });
   return MI_OK;
 }

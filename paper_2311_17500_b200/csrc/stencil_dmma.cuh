@@ -12,11 +12,12 @@
 // per point into registers (fragment-major storage, coalesced 256 B per
 // k-step) and reused for all N_t time slices.  A block owns 8 points
 // (2x2x2 for d=3) and sweeps time in chunks of TT=16 with a cp.async
-// double-buffered halo tile; two warps per point split K.  The banded time
-// filter runs in the same kernel (MI_STEN_FUSE, the default): W rows stay in
-// a 3-chunk shared-memory ring and y is written directly, so W never touches
-// HBM.  With MI_STEN_FUSE=0 (timing ablation) W is written to HBM and a
-// separate time-filter kernel (tfilter.cuh) forms y.
+// double-buffered halo tile; two warps per point split K.  W is written
+// time-innermost and the banded time filter is a separate kernel
+// (tfilter.cuh).  (Fusing the filter into this kernel with a 3-chunk W ring in
+// shared memory measured 65.6 ms against 38.4 + 3.65 ms: with one 229 KB block
+// per SM nothing overlaps the filter phase, whose band loads sit on its
+// critical path; profiles/r02_optimisation_log.md S1.)
 #pragma once
 #include "common.cuh"
 #include "ptx.cuh"
@@ -27,9 +28,6 @@
 #endif
 #ifndef MI_STEN_B2
 #define MI_STEN_B2 4
-#endif
-#ifndef MI_STEN_FUSE
-#define MI_STEN_FUSE 1
 #endif
 
 namespace mi {
@@ -60,9 +58,7 @@ struct DmmaSten {
   static constexpr int TSTR = TT + 4;               // smem stride per halo point (= 4 mod 16)
   static constexpr int PTMAX = 4;
   static constexpr int BW = 2 * PTMAX + 1;
-  // W partial rows: fused filter -- a ring of 3 chunks (the filtered chunk and its two neighbours);
-  // unfused -- this chunk + the previous one
-  static constexpr int WL = (MI_STEN_FUSE ? 3 : 2) * TT;
+  static constexpr int WL = 2 * TT;                 // W partial rows: this chunk + the previous one
   static constexpr int PSTR = 8 * WL + 4;           // point stride in the W buffer (= 4 mod 16)
   static constexpr int THREADS = 64 * PPB;          // two warps per point
   static constexpr int FK = 8 * 16;                 // filter K: 8 channels x 16 time taps
@@ -86,7 +82,7 @@ struct DmmaSten {
 
 struct DmmaArgs {
   const double* xt;     // time-innermost copy of x: xt[i * ntp + t]
-  double* wout;         // unfused ablation only: W_c of all channels, time-innermost (nchan, ns, ntp)
+  double* wout;         // W_c of all channels, time-innermost (nchan, ns, ntp): the time filter is a separate kernel
   const double* frag;   // fragment-major coefficients of this channel group
   const double* band;   // time bands (nchan_total, nt, 2pt+1)
   double* y;
@@ -206,54 +202,15 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
   const int kl = lane & 3, mrow = lane >> 2;
   double* wmine = Wp + (half * G::PPB + pt) * G::PSTR + 2 * kl * G::WL;   // channels 2kl, 2kl+1
 
-  // banded time filter of one finished chunk (fused path): thread -> (point q, row r, channel pair cp);
-  // y[t, i] (+)= sum_c sum_k band_c[t, k] W_c[t - pt + k, i] with W from the ring (both K-halves), the
-  // 4 channel pairs reduced by quad shuffles.  Ring rows outside [0, nt) meet zero band entries.
-  auto filter = [&](int tf0) {
-    const int q = tid >> 6, r = (tid >> 2) & 15, cp = tid & 3;
-    const int t = tf0 + r;
-    const int q1 = o1 + q % G::B1, q2 = o2 + (q / G::B1) % G::B2, q3 = o3 + q / (G::B1 * G::B2);
-    const bool ok = t < a.nt && q1 < a.n1 && q2 < a.n2 && q3 < a.n3;
-    double acc = 0.0;
-    if (ok) {
-      const int bw = 2 * a.pt + 1;
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = 2 * cp + cc;
-        if (c < a.nc) {
-          const double* bnd = a.band + ((long long)(a.c0 + c) * a.nt + t) * bw;
-          const double* w0 = Wp + q * G::PSTR + c * G::WL;
-          const double* w1 = w0 + G::PPB * G::PSTR;
-#pragma unroll
-          for (int k = 0; k <= 2 * G::PTMAX; ++k) {
-            if (k < bw) {
-              const int ri = ((t + k - a.pt) % G::WL + G::WL) % G::WL;
-              acc = fma(__ldg(bnd + k), w0[ri] + w1[ri], acc);
-            }
-          }
-        }
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (ok && cp == 0) {
-      double* dst = a.y + (long long)t * a.ns + ((long long)q3 * a.n2 + q2) * a.n1 + q1;
-      *dst = a.accumulate ? *dst + acc : acc;
-    }
-  };
-
   const int nchunks = (a.nt + G::TT - 1) / G::TT;
   load_chunk(0, 0);
   for (int ch = 0; ch < nchunks; ++ch) {
     const int t0 = ch * G::TT;
     if (t0 < a.nt) mbar_wait(&bars[ch & 1], (ch >> 1) & 1);   // X(ch) landed (k-th use of buffer -> parity k&1)
-    // other X buffer free; unfused: W rows of chunk ch-1 complete; fused: the filter of chunk ch-2 no
-    // longer reads the ring slot chunk ch overwrites
-    __syncthreads();
+    __syncthreads();                  // other buffer free; W rows of chunk ch-1 complete
     if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
-    if constexpr (!MI_STEN_FUSE) {
-      if (ch >= 1) write_w(t0 - G::TT);             // W of chunk ch-1 to HBM
-    }
+    // ---- W of chunk ch-1 to HBM (its partials were completed before the barrier)
+    if (ch >= 1) write_w(t0 - G::TT);
     // ---- DMMA sweep of chunk ch into this half's W partial rows
     {
       double acc[G::MT][2];
@@ -281,17 +238,10 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
         wmine[G::WL + r] = acc[m][1];
       }
     }
-    if constexpr (MI_STEN_FUSE) {
-      __syncthreads();                              // W of chunk ch complete
-      if (ch >= 1) filter(t0 - G::TT);              // chunk ch-1 (its neighbours ch-2 and ch are in the ring)
-    }
   }
-  if constexpr (MI_STEN_FUSE) {
-    filter((nchunks - 1) * G::TT);                  // the last chunk (rows past it meet zero band entries)
-  } else {
-    __syncthreads();
-    write_w((nchunks - 1) * G::TT);                 // W of the last chunk
-  }
+  // W of the last chunk
+  __syncthreads();
+  write_w((nchunks - 1) * G::TT);
 }
 
 // y[t, i] (+)= sum_c sum_k band_c[t, k] W_c[t - pt + k, i] with W time-innermost

@@ -71,7 +71,7 @@ class KroneckerOperator:
 
     def __init__(self, space_time, final_time, capacitance=1.0, diffusion=1e-4, constants=None,
                  u=None, w=None, stabilization=None, lengths=None, device=0, context=None, time_rows=None,
-                 z_planes=None, spatial_data=None, lift=None, lift_in_reaction=True):
+                 z_planes=None, spatial_data=None, lift=None, lift_in_reaction=True, iterate_is_zero=None):
         """``time_rows=(e_lo, e_hi)`` builds the operator restricted to a slab of
         constrained time rows: the time bands are the global rows e_lo..e_hi, and
         u, w (if given) are slab vectors.  ``z_planes=(z_lo, z_hi)`` (d = 3) builds
@@ -85,7 +85,9 @@ class KroneckerOperator:
         in the reference): the reaction sees the lifted iterate u0 b_0 + u, the zero-iterate switch
         needs u0 = 0 too, and ``lift_apply()`` returns the right-hand side correction A_{c,0} u0.
         ``lift_in_reaction=False`` keeps the Kronecker reaction term of the zero iterate (an operator
-        that only uses that channel as a plain mass term, like the recovery right-hand side's)."""
+        that only uses that channel as a plain mass term, like the recovery right-hand side's).
+        ``iterate_is_zero`` overrides the zero-iterate test (solver.py:220) with a decision taken
+        elsewhere -- the sharded driver takes it over the GLOBAL iterate, not this rank's slab."""
         sd = spatial_data
         if sd is not None:
             if z_planes is not None or time_rows is not None:
@@ -115,7 +117,8 @@ class KroneckerOperator:
         has_lift = lift is not None and not _is_zero(lift)
         if has_lift and time_rows is not None:
             raise NotImplementedError("u0 lifting needs the whole time axis (not a time slab)")
-        zero_iterate = _is_zero(u) and _is_zero(w) and not (has_lift and lift_in_reaction)
+        zero_iterate = (_is_zero(u) and _is_zero(w)) if iterate_is_zero is None else bool(iterate_is_zero)
+        zero_iterate = zero_iterate and not (has_lift and lift_in_reaction)
         react = consts["c1"] * consts["a"] if zero_iterate else 0.0
         self.zero_iterate = zero_iterate
         stab = stabilization

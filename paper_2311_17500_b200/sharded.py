@@ -242,7 +242,11 @@ class DeviceSlabBackend:
     (libmonoiga_b200).  ``u``, ``w`` (variant B) are input-slab vectors."""
 
     def __init__(self, layout, space_time, final_time, capacitance, diffusion, constants,
-                 stabilization=None, u=None, w=None, device=0):
+                 stabilization=None, u=None, w=None, device=0, precond=None, op_context=None, lift=None,
+                 iterate_is_zero=None):
+        """``precond`` / ``op_context``: reuse a preconditioner and an operator context (the sharded
+        fixed-point driver rebuilds only the operator's tables every sweep); ``lift``: u0 lifting
+        coefficients of the input slab; ``iterate_is_zero``: the global zero-iterate decision."""
         from . import _lib
         from .operator import KroneckerOperator
         from .precond import FastDiagPreconditioner
@@ -252,9 +256,10 @@ class DeviceSlabBackend:
         L = layout
         self.op = KroneckerOperator(space_time, final_time, capacitance, diffusion, constants,
                                     u=u, w=w, stabilization=stabilization, device=device,
-                                    z_planes=(L.z_lo, L.z_hi))
-        self.pc = FastDiagPreconditioner.build(space_time, final_time, capacitance, diffusion,
-                                               constants["a"] * constants["c1"], device=device)
+                                    z_planes=(L.z_lo, L.z_hi), context=op_context, lift=lift,
+                                    iterate_is_zero=iterate_is_zero)
+        self.pc = precond if precond is not None else FastDiagPreconditioner.build(
+            space_time, final_time, capacitance, diffusion, constants["a"] * constants["c1"], device=device)
         self.device = self.op.ctx.device
         self.vec_ops = DeviceVecOps(self.op.ctx)
 
@@ -283,3 +288,160 @@ class DeviceSlabBackend:
         from .device import dptr
         self.pc.ctx.bind_stream()
         self._lib.call("mi_pc_apply_time_yslab", self.pc.ctx.handle, dptr(blk), int(y_lo), int(y_hi))
+
+
+# --------------------------------------------------------------------------
+# Sharded fixed-point driver
+# --------------------------------------------------------------------------
+
+def gather_slabs(L, own, group=None):
+    """The global (N_t, n_3, n_2 n_1) vector from every rank's owned z slab (all-gather, padded to the
+    largest slab)."""
+    world = L.world
+    if world == 1:
+        return own.clone()
+    nmax = max(L.nt * (L.zs[r + 1] - L.zs[r]) * L.plane for r in range(world))
+    dev = "cpu" if _staged(own, group) else own.device
+    buf = torch.zeros(nmax, dtype=own.dtype, device=dev)
+    buf[:own.numel()].copy_(own)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    full = torch.empty(L.nt, L.n3, L.plane, dtype=own.dtype, device=own.device)
+    for r in range(world):
+        z0, z1 = L.zs[r], L.zs[r + 1]
+        n = L.nt * (z1 - z0) * L.plane
+        full[:, z0:z1].copy_(parts[r][:n].view(L.nt, z1 - z0, L.plane))
+    return full.view(-1)
+
+
+def input_slab(L, full):
+    """This rank's operator input slab (owned planes + halo planes) of a global vector."""
+    v = full.view(L.nt, L.n3, L.plane)[:, L.z_lo - L.h_lo:L.z_hi + L.h_hi]
+    return v.contiguous().view(-1)
+
+
+def own_slab(L, full):
+    return full.view(L.nt, L.n3, L.plane)[:, L.z_lo:L.z_hi].contiguous().view(-1)
+
+
+def sharded_fixed_point_solve(problem, config=None, group=None, device=0):
+    """fixed_point_solve (solver.py:239-386) with its hot path sharded over the ranks of ``group``.
+
+    The potential solve of every sweep -- the z-slab operator (p-plane halo exchange), P^-1 with its
+    two all-to-all transposes and GMRES with all-reduced CGS2 dots -- runs on each rank's z slab.  The
+    per-sweep setup that needs the global iterate (the residual indicator, its low-rank split and the
+    stencil tables, solver.py:291-324) and the recovery solve (a banded time solve and spatial mass
+    solves, linalg.py:502-547) run replicated on every rank from all-gathered iterates; the load
+    vector and the lifting are computed once.  Box geometries, d = 3, every-sweep or no indicator.
+    Returns the same SolveResult on every rank (u, w gathered)."""
+    import time as _time
+
+    import numpy as np
+
+    from .krylov import DeviceVecOps
+    from .operator import KroneckerOperator, Stabilization
+    from .precond import FastDiagPreconditioner
+    from .problem import FixedPointConfig, FixedPointDiverged, SolveResult, box_of, lift_coefficients, load_vector
+    from .theta import DeviceIndicator
+    from .wsolve import RecoverySolver
+    from .device import DeviceContext
+
+    if config is None:
+        config = FixedPointConfig()
+    st = problem.space
+    if len(st.spatial) != 3:
+        raise ValueError("the sharded driver needs d = 3")
+    if config.stabilization == "spline_upwind" and config.indicator_update != "every_sweep":
+        raise NotImplementedError("the sharded driver recomputes the indicator every sweep")
+    if config.linear_solver == "direct":
+        raise NotImplementedError("the direct (host LU) linear solver is not part of the device path")
+    t0 = _time.perf_counter()
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", device)
+    p = st.spatial[0].degree
+    L = ZSlabLayout(st.num_time, [s.dimension for s in st.spatial], p, rank, world)
+    Lb, _ = box_of(problem.geometry)
+    T, consts = problem.final_time, problem.reaction_constants()
+    D = problem.D if np.atleast_1d(problem.D).size > 1 else problem.scalar_D()
+    # replicated, once: load vector, lifting, recovery solver and its mass operator, indicator
+    f = load_vector(st, problem.geometry, problem.source, device=device)
+    f = (f if torch.is_tensor(f) else torch.from_numpy(np.ascontiguousarray(f))).to(dev)
+    f_own = own_slab(L, f)
+    lift_np = lift_coefficients(problem)
+    lift = None if lift_np is None else torch.from_numpy(lift_np).to(dev)
+    lift_in = None
+    if lift is not None:
+        lift_in = lift.view(L.n3, L.plane)[L.z_lo - L.h_lo:L.z_hi + L.h_hi].contiguous().view(-1)
+    mass_op = KroneckerOperator(st, T, 0.0, 0.0, {"c1": 1.0, "a": 1.0, "c2": 0.0}, lengths=Lb, device=device,
+                                lift=lift, lift_in_reaction=False)
+    g_lift = mass_op.lift_apply() if lift is not None else None
+    wsolver = RecoverySolver(st, T, problem.b, problem.d_e, config.linear_tol, lengths=Lb, device=device)
+    indicator = DeviceIndicator(problem, device) if config.stabilization == "spline_upwind" else None
+    # sharded, once: the preconditioner; the operator context is reused by every sweep
+    pc = FastDiagPreconditioner.build(st, T, problem.C_m, D, problem.a * problem.c1, lengths=Lb, device=device)
+    op_ctx = DeviceContext(st, device, zslab=(L.z_lo, L.z_hi, L.h_lo, L.h_hi))
+    def allmax(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if _staged(f_own, group) else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return float(t.item())
+
+    u_own = torch.zeros(L.n_own, dtype=torch.float64, device=dev)
+    w_own = torch.zeros_like(u_own)
+    increments, gmres_iters, pcg_iters = [], [], []
+    ind_vals = None
+    frozen_stab = None
+    alpha = config.relaxation
+    for k in range(1, config.max_iterations + 1):
+        u_full = gather_slabs(L, u_own, group)
+        w_full = gather_slabs(L, w_own, group)
+        zero = allmax(float(u_own.abs().max().item()) + float(w_own.abs().max().item())) == 0.0
+        stab = None
+        if indicator is not None:
+            if frozen_stab is not None:
+                stab = frozen_stab
+            else:
+                fresh = indicator.compute(u_full, w_full, on_device=True, lift=lift).values
+                fresh = torch.as_tensor(fresh, device=dev)
+                freeze = False
+                if ind_vals is not None and alpha < 1.0:
+                    drift = float((fresh - ind_vals).abs().max().item())
+                    fresh = alpha * fresh + (1.0 - alpha) * ind_vals
+                    if config.indicator_freeze_tol > 0.0 and k > 1 and drift * alpha <= config.indicator_freeze_tol:
+                        freeze = True
+                ind_vals = fresh
+                stab = Stabilization(st, ind_vals, config.lowrank_tol, problem.C_m, lengths=Lb)
+                if freeze:
+                    frozen_stab = stab
+        be = DeviceSlabBackend(L, st, T, problem.C_m, D, consts, stabilization=stab,
+                               u=None if zero else input_slab(L, u_full), w=None if zero else input_slab(L, w_full),
+                               device=device, precond=pc, op_context=op_ctx, lift=lift_in, iterate_is_zero=zero)
+        sop, spc = ShardedOperator(L, be, group), ShardedPreconditioner(L, be, group)
+        rhs = f_own if lift is None else f_own - be.op.lift_apply()
+        u_t, nit, _ = sharded_gmres(sop, spc, be.vec_ops, rhs, tol=config.linear_tol, max_iter=st.num_dof,
+                                    group=group)
+        gmres_iters.append(nit)
+        if config.evolve_recovery:
+            g_full = mass_op.matvec(u_full)
+            if g_lift is not None:
+                g_full = g_full + g_lift
+            w_t_full, w_its = wsolver.solve(problem.b * g_full)
+            pcg_iters.extend(w_its)
+            w_t = own_slab(L, w_t_full)
+        else:
+            w_t = w_own
+        u_new = alpha * u_t + (1.0 - alpha) * u_own
+        w_new = alpha * w_t + (1.0 - alpha) * w_own
+        inc = allmax(float((u_new - u_own).abs().max().item()))
+        increments.append(inc)
+        u_own, w_own = u_new, w_new
+        if inc <= config.tolerance:
+            u_full = gather_slabs(L, u_own, group).cpu().numpy()
+            w_full = gather_slabs(L, w_own, group).cpu().numpy()
+            return SolveResult(u_full, w_full, k, increments, True, gmres_iters, pcg_iters,
+                               _time.perf_counter() - t0, None, {}, lift_np)
+    result = SolveResult(gather_slabs(L, u_own, group).cpu().numpy(), gather_slabs(L, w_own, group).cpu().numpy(),
+                         config.max_iterations, increments, False, gmres_iters, pcg_iters,
+                         _time.perf_counter() - t0, None, {}, lift_np)
+    raise FixedPointDiverged("fixed point did not reach %.2e in %d iterations"
+                             % (config.tolerance, config.max_iterations), result)
