@@ -179,3 +179,68 @@ def kron_rows(st, terms, x, rows):
             acc += c * float(blk)
         out[m] = acc
     return out
+
+
+def mapped_rows(st, geo_spaces, ctrl, terms, x, rows, fibre=None):
+    """Rows of the mapped-geometry operator sum_k c_k T_k (x) S_k with S_k the pulled-back quadrature
+    mass ('mass': w |det J| B_i B_j) or stiffness ('stiffness': w |det J| grad B_i . J^-1 G J^-T grad B_j,
+    G = I or the fibre tensor) of SpatialQuadratureData (assembly.py:137-219, q = p+1 Gauss), evaluated
+    on the support of each row's function only.  ``terms`` = [(c_k, T_k, kind_k)]; ``fibre`` as
+    oracle.mapped.QuadData.  The map is evaluated with oracle.mapped.grid_data (geometry.py:135-186)."""
+    from .mapped import grid_data
+    d = st.d
+    X = np.asarray(x, float).reshape(st.num_time, st.num_space)
+    rules = [Rule.on(s) for s in st.spatial]
+    sshape = st.spatial_shape
+    out = np.zeros(len(rows))
+    for m, row in enumerate(rows):
+        it, isp = _split(st, row)
+        loc = [_local_1d(s, isp[l], rules[l]) for l, s in enumerate(st.spatial)]
+        idx = [loc[l][2] for l in reversed(range(d))]
+        flat = np.ravel_multi_index(np.ix_(*idx), sshape).ravel()
+        pts = [loc[l][0] for l in range(d)]
+        xg, jac = grid_data(geo_spaces, ctrl, pts)             # (Q_d..Q_1, d), (.., d, d)
+        detj = np.abs(np.linalg.det(jac))
+        jinv = np.linalg.inv(jac)
+        if fibre is not None:
+            sl, stv, kdir = fibre
+            f = jac[..., :, kdir] / np.linalg.norm(jac[..., :, kdir], axis=-1, keepdims=True)
+            Dm = stv * np.eye(d) + (sl - stv) * f[..., :, None] * f[..., None, :]
+            metric = jinv @ Dm @ np.swapaxes(jinv, -1, -2)
+        else:
+            metric = jinv @ np.swapaxes(jinv, -1, -2)
+        w = np.ones(())
+        for l in reversed(range(d)):
+            w = np.multiply.outer(w, loc[l][1])
+        w = w * detj
+        # B_i and its parametric gradient at the local grid; the trial field and its gradient from the
+        # local coefficient block of (T_k X)[i_t]
+        bi = [loc[l][4] for l in range(d)]
+        dsp = [st.spatial[l].colloc(pts[l], 1).toarray() for l in range(d)]
+        dbi = [dsp[l][:, isp[l]] for l in range(d)]
+        dmat = [dsp[l][:, loc[l][2]] for l in range(d)]
+
+        def outer(vecs):
+            g = np.ones(())
+            for l in reversed(range(d)):
+                g = np.multiply.outer(g, vecs[l])
+            return g
+
+        Bi = outer(bi)
+        gBi = [outer([dbi[l] if l == a else bi[l] for l in range(d)]) for a in range(d)]
+        acc = 0.0
+        for c, T, kind in terms:
+            trow = sp.csr_matrix(T).getrow(it)
+            Z = (trow.data @ X[trow.indices][:, flat]).reshape(tuple(len(ix) for ix in idx))
+            if kind == "mass":
+                zq = _field(Z, [loc[l][3] for l in reversed(range(d))])
+                acc += c * np.sum(w * Bi * zq)
+            else:
+                gz = [_field(Z, [(dmat[l] if l == a else loc[l][3]) for l in reversed(range(d))]) for a in range(d)]
+                val = 0.0
+                for a in range(d):
+                    for b in range(d):
+                        val = val + np.sum(w * metric[..., a, b] * gBi[a] * gz[b])
+                acc += c * val
+        out[m] = acc
+    return out

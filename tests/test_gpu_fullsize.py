@@ -205,3 +205,41 @@ def test_gmres_vs_reference(setup):
     # relative at the 1e-8 end, 3.4e-10 absolute)
     np.testing.assert_allclose(hist, s.g["gm_hist"], rtol=1e-3, atol=1e-12)
     op.ctx.close()
+
+
+def test_mapped_cfg5_shape_rows_vs_oracle(tmp_path):
+    """BASELINE cfg-5 shape (p = 3, 64^3 x 256, N = 77.6 M) on the prolate-shell map with cfg 5's fibre
+    conductivity: the device mapped operator (quadrature stencils of the exact pulled-back coefficients,
+    zero-iterate reaction) on 1000 sampled rows vs oracle/rows.mapped_rows (the reference's
+    SpatialQuadratureData integrals restricted to each row's support, pinned on the reference's annulus
+    and warped cube in tests/test_oracle_golden.py)."""
+    import torch
+    import paper_2311_17500_b200 as mb
+    from oracle import assembly as asm
+    from oracle import rows as orows
+    from oracle.mapped import read_geometry
+    from oracle.splines import make_space_time
+    from paper_2311_17500_b200.geometry import (FibreConductivity, MappedSpatialData, prolate_shell_geometry,
+                                                save_geometry)
+    p, ne, ne_t = 3, 64, 256
+    geo = prolate_shell_geometry()
+    path = str(tmp_path / "shell.txt")
+    save_geometry(geo, path)
+    gs, ctrl = read_geometry(path)
+    st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
+    fib = (1e-3, 3e-4, 0)
+    sd = MappedSpatialData(st.spatial, geo, conductivity=FibreConductivity(*fib))
+    op = mb.KroneckerOperator(st, 1.0, 1.0, 1.0, RM, spatial_data=sd)
+    N = st.num_dof
+    x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).cuda()
+    y = torch.empty_like(x)
+    op.apply_device(x, y)
+    rows = np.sort(np.random.default_rng(9).choice(N, NROWS, replace=False))
+    got = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    op.ctx.close()
+    ost = make_space_time(3, p, ne, ne_t)
+    Wt, Mt = asm.time_factors(ost, 1.0)
+    terms = [(1.0, Wt, "mass"), (1.0, Mt, "stiffness"), (RM["a"] * RM["c1"], Mt, "mass")]
+    ref = orows.mapped_rows(ost, gs, ctrl, terms, x.cpu().numpy(), rows, fibre=fib)
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(got).max()
+    assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(ref)
