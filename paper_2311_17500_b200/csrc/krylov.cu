@@ -6,17 +6,23 @@
 
 namespace mi {
 
-constexpr int KB = 592;   // 4 x 148 SMs
+#ifndef MI_KRY_KB
+#define MI_KRY_KB 296
+#endif
+#ifndef MI_KRY_KU
+#define MI_KRY_KU 1
+#endif
+constexpr int KB = MI_KRY_KB;   // reduction blocks: 2 x 148 SMs, one wave at <= 128 registers
 constexpr int KT = 256;
 constexpr int KG = 8;     // vectors per pass
-constexpr int KU = 4;     // elements per thread per loop trip (independent loads in flight)
+constexpr int KU = MI_KRY_KU;   // elements per thread per loop trip (independent loads in flight)
 
 // Every reduction below walks its block's chunk [lo, hi) in the same order -- thread t takes
 // j = lo + t + u KT for u < KU, then advances by KU KT -- so the fused and the two-pass kernels sum
 // in the same order and agree bit for bit.
 
 template <int G>
-__global__ void __launch_bounds__(KT) dots_partial(const double* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(KT, 2) dots_partial(const double* __restrict__ V, long long ldv,
                                                    const double* __restrict__ w, long long n, int k0,
                                                    int k, double* __restrict__ part) {
   __shared__ double red[G][KT / 32];
@@ -115,7 +121,7 @@ __global__ void scale_div(const double* __restrict__ x, const double* __restrict
 // pass's dots); MODE 1: w -= V h, then |w|^2.  Per-block partials in a fixed partition, reduced by
 // dots_final: deterministic, the same rounding as the unfused pair only up to the summation order.
 template <int KM, int MODE>
-__global__ void __launch_bounds__(KT) sub_reduce(const double* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(KT, 2) sub_reduce(const double* __restrict__ V, long long ldv,
                                                  const double* __restrict__ h, int k, double* __restrict__ w,
                                                  long long n, double* __restrict__ part) {
   constexpr int NA = MODE == 0 ? KM : 1;

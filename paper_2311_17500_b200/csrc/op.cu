@@ -695,7 +695,9 @@ static int dmma_apply(mi_ctx* c, const double* x, double* y) {
       DmmaArgs a{c->xt.p, c->wbuf.p, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
                  gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns, c->hz_lo};
       ProfScope ps(c, PROF_OP_STENCIL);
-      stencil_dmma<D_, P_><<<(unsigned)ncubes, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
+      // persistent: one CTA per SM (the kernel is sized for 1 CTA / SM), each sweeping cubes b, b + grid, ...
+      const long long grid = MI_STEN_PERSIST ? std::min<long long>(ncubes, mi::num_sms()) : ncubes;
+      stencil_dmma<D_, P_><<<(unsigned)grid, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");
     }
     {

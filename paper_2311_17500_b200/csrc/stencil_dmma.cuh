@@ -29,6 +29,9 @@
 #ifndef MI_STEN_B2
 #define MI_STEN_B2 4
 #endif
+#ifndef MI_STEN_PERSIST
+#define MI_STEN_PERSIST 1   // persistent CTAs with cross-cube prefetch (stencil_dmma)
+#endif
 
 namespace mi {
 
@@ -146,21 +149,14 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pt = warp >> 1, half = warp & 1;
-  const int cube = blockIdx.x;
-  const int c1 = cube % a.C1, c2 = (cube / a.C1) % a.C2, c3 = cube / (a.C1 * a.C2);
-  const int o1 = c1 * G::B1, o2 = c2 * G::B2, o3 = c3 * G::B3;
+  const int ncubes = a.C1 * a.C2 * a.C3;
+  // Persistent CTAs (MI_STEN_PERSIST): block b sweeps cubes b, b + grid, ...  The first halo tile of the
+  // next cube is loaded by TMA during the current cube's last chunk and the next cube's coefficient
+  // fragments are prefetched into L2 during its sweep, so a cube's start-up (fragment loads, first
+  // tile) no longer runs with the tensor cores idle.  Without persistence: one cube per block.
+  const int cstep = MI_STEN_PERSIST ? (int)gridDim.x : ncubes;
 
   for (int e = tid; e < 2 * G::PPB * G::PSTR; e += G::THREADS) Wp[e] = 0.0;
-
-  double breg[G::KH];
-  {
-    const double* f = a.frag + ((long long)cube * G::PPB + pt) * G::KS * 32 + lane;
-#pragma unroll
-    for (int j = 0; j < G::KH; ++j) {
-      const int ks = half * G::KH + j;
-      breg[j] = ks < G::KS ? __ldg(f + ks * 32) : 0.0;
-    }
-  }
 
   // ---- async loads of chunk t0: halo tile (16 B copies) + band rows of the
   // halo tile of chunk t0 by ONE TMA bulk-tensor copy: box (TSTR time rows, H1, H2, H3) of the
@@ -172,76 +168,111 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
     mbar_fence_init();
   }
   __syncthreads();
-  auto load_chunk = [&](int buf, int t0) {
+  auto origin = [&](int cube, int& o1, int& o2, int& o3) {
+    const int c1 = cube % a.C1, c2 = (cube / a.C1) % a.C2, c3 = cube / (a.C1 * a.C2);
+    o1 = c1 * G::B1;
+    o2 = c2 * G::B2;
+    o3 = c3 * G::B3;
+  };
+  auto load_chunk = [&](int cube, int buf, int t0) {
     if (tid == 0 && t0 < a.nt) {
+      int q1, q2, q3;
+      origin(cube, q1, q2, q3);
       mbar_expect_tx(&bars[buf], TILE_BYTES);
-      tma_load_4d(Xs + buf * G::HS * G::TSTR, &tmap, &bars[buf], t0, o1 - P, D >= 2 ? o2 - P : 0,
-                  D >= 3 ? o3 - P + a.zoff : 0);
+      tma_load_4d(Xs + buf * G::HS * G::TSTR, &tmap, &bars[buf], t0, q1 - P, D >= 2 ? q2 - P : 0,
+                  D >= 3 ? q3 - P + a.zoff : 0);
     }
   };
-
-  // write-out of W of a finished chunk (both K-halves summed) to the time-innermost layout:
-  // thread -> (row pair rp, point q, channel c); 8 consecutive threads write 16 consecutive rows (128 B)
-  auto write_w = [&](int tc0) {
-    const int rp = tid & 7, q = (tid >> 3) % G::PPB, c = tid / (8 * G::PPB);
-    const int q1 = o1 + q % G::B1, q2 = o2 + (q / G::B1) % G::B2, q3 = o3 + q / (G::B1 * G::B2);
-    if (c >= a.nc || q1 >= a.n1 || q2 >= a.n2 || q3 >= a.n3) return;
-    const long long gi = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
-    const double* w0 = Wp + q * G::PSTR + c * G::WL;
-    const double* w1 = w0 + G::PPB * G::PSTR;
-    const int t = tc0 + 2 * rp;                      // tc0 is a multiple of TT; ntp a multiple of TT
-    const int r = t % G::WL;
-    double2 v;
-    v.x = w0[r] + w1[r];
-    v.y = w0[r + 1] + w1[r + 1];
-    *reinterpret_cast<double2*>(a.wout + ((long long)(a.c0 + c) * a.ns + gi) * a.ntp + t) = v;
-  };
-
-
+  constexpr long long FRAG_CUBE = (long long)G::PPB * G::KS * 32;   // doubles of one cube's fragments
   const int base = ((pt / (G::B1 * G::B2)) * G::H2 + (pt / G::B1) % G::B2) * G::H1 + pt % G::B1;
   const int kl = lane & 3, mrow = lane >> 2;
   double* wmine = Wp + (half * G::PPB + pt) * G::PSTR + 2 * kl * G::WL;   // channels 2kl, 2kl+1
-
   const int nchunks = (a.nt + G::TT - 1) / G::TT;
-  load_chunk(0, 0);
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int t0 = ch * G::TT;
-    if (t0 < a.nt) mbar_wait(&bars[ch & 1], (ch >> 1) & 1);   // X(ch) landed (k-th use of buffer -> parity k&1)
-    __syncthreads();                  // other buffer free; W rows of chunk ch-1 complete
-    if (ch + 1 < nchunks) load_chunk((ch + 1) & 1, t0 + G::TT);
-    // ---- W of chunk ch-1 to HBM (its partials were completed before the barrier)
-    if (ch >= 1) write_w(t0 - G::TT);
-    // ---- DMMA sweep of chunk ch into this half's W partial rows
+  int gc = 0;                                        // chunks consumed by this block: buffer gc & 1, phase (gc >> 1) & 1
+
+  if (blockIdx.x < ncubes) load_chunk(blockIdx.x, 0, 0);
+  for (int cube = blockIdx.x; cube < ncubes; cube += cstep) {
+    int o1, o2, o3;
+    origin(cube, o1, o2, o3);
+    const int next = cube + cstep;
+    double breg[G::KH];
     {
-      double acc[G::MT][2];
+      const double* f = a.frag + ((long long)cube * G::PPB + pt) * G::KS * 32 + lane;
 #pragma unroll
-      for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-      if (t0 < a.nt) {
-        const double* X = Xs + (ch & 1) * G::HS * G::TSTR + (base + kl) * G::TSTR + mrow;
-        // the last chunk skips M-tiles that lie wholly past nt (warp-uniform)
-        if (t0 + 8 * (G::MT - 1) < a.nt) {
-          if (half == 0)
-            dmma_sweep<G, 0, G::MT>(X, kl, breg, acc);
-          else
-            dmma_sweep<G, 1, G::MT>(X, kl, breg, acc);
-        } else {
-          if (half == 0)
-            dmma_sweep<G, 0, 1>(X, kl, breg, acc);
-          else
-            dmma_sweep<G, 1, 1>(X, kl, breg, acc);
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < G::MT; ++m) {
-        const int r = (t0 + m * 8 + mrow) % G::WL;
-        wmine[r] = acc[m][0];
-        wmine[G::WL + r] = acc[m][1];
+      for (int j = 0; j < G::KH; ++j) {
+        const int ks = half * G::KH + j;
+        breg[j] = ks < G::KS ? __ldg(f + ks * 32) : 0.0;
       }
     }
+    // the next cube's fragments into L2 while this one sweeps (one bulk prefetch per 16 KB piece)
+    if (MI_STEN_PERSIST && next < ncubes && warp == 0) {
+      const char* nf = reinterpret_cast<const char*>(a.frag + (long long)next * FRAG_CUBE);
+      constexpr long long BYTES = FRAG_CUBE * 8;
+      for (long long off = (long long)lane * 16384; off < BYTES; off += 32LL * 16384) {
+        const unsigned sz = (unsigned)(BYTES - off < 16384 ? BYTES - off : 16384);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(nf + off), "r"(sz) : "memory");
+      }
+    }
+
+    // write-out of W of a finished chunk (both K-halves summed) to the time-innermost layout:
+    // thread -> (row pair rp, point q, channel c); 8 consecutive threads write 16 consecutive rows (128 B)
+    auto write_w = [&](int tc0) {
+      const int rp = tid & 7, q = (tid >> 3) % G::PPB, c = tid / (8 * G::PPB);
+      const int q1 = o1 + q % G::B1, q2 = o2 + (q / G::B1) % G::B2, q3 = o3 + q / (G::B1 * G::B2);
+      if (c >= a.nc || q1 >= a.n1 || q2 >= a.n2 || q3 >= a.n3) return;
+      const long long gi = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
+      const double* w0 = Wp + q * G::PSTR + c * G::WL;
+      const double* w1 = w0 + G::PPB * G::PSTR;
+      const int t = tc0 + 2 * rp;                    // tc0 is a multiple of TT; ntp a multiple of TT
+      const int r = t % G::WL;
+      double2 v;
+      v.x = w0[r] + w1[r];
+      v.y = w0[r + 1] + w1[r + 1];
+      *reinterpret_cast<double2*>(a.wout + ((long long)(a.c0 + c) * a.ns + gi) * a.ntp + t) = v;
+    };
+
+    for (int ch = 0; ch < nchunks; ++ch, ++gc) {
+      const int t0 = ch * G::TT;
+      if (t0 < a.nt) mbar_wait(&bars[gc & 1], (gc >> 1) & 1);   // X(ch) landed (k-th use of buffer -> parity k&1)
+      __syncthreads();                // other buffer free; W rows of chunk ch-1 complete
+      if (ch + 1 < nchunks)
+        load_chunk(cube, (gc + 1) & 1, t0 + G::TT);
+      else if (next < ncubes)
+        load_chunk(next, (gc + 1) & 1, 0);           // the next cube's first tile
+      // ---- W of chunk ch-1 to HBM (its partials were completed before the barrier)
+      if (ch >= 1) write_w(t0 - G::TT);
+      // ---- DMMA sweep of chunk ch into this half's W partial rows
+      {
+        double acc[G::MT][2];
+#pragma unroll
+        for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+        if (t0 < a.nt) {
+          const double* X = Xs + (gc & 1) * G::HS * G::TSTR + (base + kl) * G::TSTR + mrow;
+          // the last chunk skips M-tiles that lie wholly past nt (warp-uniform)
+          if (t0 + 8 * (G::MT - 1) < a.nt) {
+            if (half == 0)
+              dmma_sweep<G, 0, G::MT>(X, kl, breg, acc);
+            else
+              dmma_sweep<G, 1, G::MT>(X, kl, breg, acc);
+          } else {
+            if (half == 0)
+              dmma_sweep<G, 0, 1>(X, kl, breg, acc);
+            else
+              dmma_sweep<G, 1, 1>(X, kl, breg, acc);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < G::MT; ++m) {
+          const int r = (t0 + m * 8 + mrow) % G::WL;
+          wmine[r] = acc[m][0];
+          wmine[G::WL + r] = acc[m][1];
+        }
+      }
+    }
+    // W of the last chunk
+    __syncthreads();
+    write_w((nchunks - 1) * G::TT);
   }
-  // W of the last chunk
-  __syncthreads();
-  write_w((nchunks - 1) * G::TT);
 }
 
 // y[t, i] (+)= sum_c sum_k band_c[t, k] W_c[t - pt + k, i] with W time-innermost
