@@ -32,6 +32,9 @@
 #ifndef MI_STEN_PERSIST
 #define MI_STEN_PERSIST 1   // persistent CTAs with cross-cube prefetch (stencil_dmma)
 #endif
+#ifndef MI_STEN_L2PF
+#define MI_STEN_L2PF 1      // persistent CTAs also prefetch the next cube's fragments into L2
+#endif
 
 namespace mi {
 
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
       }
     }
     // the next cube's fragments into L2 while this one sweeps (one bulk prefetch per 16 KB piece)
-    if (MI_STEN_PERSIST && next < ncubes && warp == 0) {
+    if (MI_STEN_PERSIST && MI_STEN_L2PF && next < ncubes && warp == 0) {
       const char* nf = reinterpret_cast<const char*>(a.frag + (long long)next * FRAG_CUBE);
       constexpr long long BYTES = FRAG_CUBE * 8;
       for (long long off = (long long)lane * 16384; off < BYTES; off += 32LL * 16384) {

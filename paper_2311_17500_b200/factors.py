@@ -125,13 +125,39 @@ def lowrank_factorize(values, tol):
             s = np.sqrt(lam[:rank])          # > 0: tails2[rank-1] > cut2 >= tails2[rank]
             V = (th.T @ W[:, :rank]) / s
             return LowRankIndicator(th, rank, np.ascontiguousarray(W[:, :rank]), V, s[:rank].copy(), tol)
-    U, s, Vt = np.linalg.svd(th, full_matrices=False)
+    with _single_thread_blas(th.size < 1 << 20):
+        U, s, Vt = np.linalg.svd(th, full_matrices=False)
     tails = np.sqrt(np.append(np.cumsum((s ** 2)[::-1])[::-1], 0.0))
     rank = max(int(np.argmax(tails <= tol * nrm)), 1)
     return LowRankIndicator(th, rank, U[:, :rank], Vt[:rank].T.copy(), s[:rank].copy(), tol)
 
 
 GRAM_MIN_SIZE = 2_000_000
+
+
+class _single_thread_blas:
+    """Small dense LAPACK calls (N_t x N_s indicators of small problems, the N_t x N_t pencil) run on one
+    BLAS thread: a many-threaded OpenBLAS spends far longer waking its pool than computing them
+    (measured 28 ms per 65 x 66 SVD on a 16-core GPU host inside the fixed-point driver)."""
+
+    def __init__(self, on):
+        self.on = on
+        self.ctx = None
+
+    def __enter__(self):
+        if self.on:
+            try:
+                from threadpoolctl import threadpool_limits
+                self.ctx = threadpool_limits(limits=1, user_api="blas")
+                self.ctx.__enter__()
+            except Exception:      # threadpoolctl is optional: then nothing is limited
+                self.ctx = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+        return False
 
 
 def _lowrank_device(th, tol):
@@ -405,7 +431,9 @@ class RealTimePencil:
         Q[:-1, :-1] = Ui
         Q[:-1, -1] = t
         Q[-1, -1] = rho
-        if np.linalg.cond(Q) > cond_limit:
+        with _single_thread_blas(True):
+            condq = np.linalg.cond(Q)
+        if condq > cond_limit:
             raise DecompositionError("temporal pencil eigenvectors ill-conditioned")
         # 2x2 block partition of the quasi-triangular T (skew => block diagonal)
         m = n - 1

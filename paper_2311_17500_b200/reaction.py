@@ -14,19 +14,34 @@ from .device import dptr, host_ptr
 from .spaces import basis_table, gauss_rule
 
 
+_ELEMENT_TABLES = {}
+
+
 def element_tables(space, q, scale):
-    """(B, W): B[e, g, a] = value of function e + a at Gauss point g of element e."""
+    """(B, W): B[e, g, a] = value of function e + a at Gauss point g of element e (memoised: the
+    fixed-point driver rebuilds the reaction every sweep on the same spaces; the result is read-only)."""
+    key = (np.asarray(space.knots, float).tobytes(), int(space.degree), int(q), float(scale))
+    hit = _ELEMENT_TABLES.get(key)
+    if hit is not None:
+        return hit
     bp = space.breakpoints
     ne = bp.size - 1
     x, w = gauss_rule(bp, q)
     T = basis_table(space, x, 0)
     p = space.degree
-    B = np.zeros((ne, q, p + 1))
-    for e in range(ne):
-        B[e] = T[e * q:(e + 1) * q, e:e + p + 1]
-        # open uniform knots: element e carries functions e..e+p
-        assert np.allclose(T[e * q:(e + 1) * q].sum(axis=1), 1.0)
-    return B, (w * scale).reshape(ne, q)
+    # open uniform knots: element e carries functions e..e+p (the partition of unity checks it)
+    rows = np.arange(ne * q).reshape(ne, q)
+    cols = np.arange(ne)[:, None, None] + np.arange(p + 1)[None, None, :]
+    B = T[rows[:, :, None], cols]
+    if not np.allclose(B.sum(axis=2), 1.0):
+        raise ValueError("element tables need an open knot vector with simple interior knots")
+    out = (B, (w * scale).reshape(ne, q))
+    for a in out:
+        a.setflags(write=False)
+    if len(_ELEMENT_TABLES) > 64:
+        _ELEMENT_TABLES.pop(next(iter(_ELEMENT_TABLES)))
+    _ELEMENT_TABLES[key] = out
+    return out
 
 
 def set_reaction(ctx, st, final_time, consts, u, w, lengths, time_rows=None, zslab=None):

@@ -27,7 +27,12 @@ def one(lib):
     out = torch.zeros(33, dtype=torch.float64, device="cuda")
     res = []
     for k in (8, 16, 32):
+        def two_pass():
+            ops.sub_comb(V, k, h, w)
+            ops.dots(V, k, w, out)
+
         for name, fn, nbytes in (("dots", lambda: ops.dots(V, k, w, out), (k + 1) * 8 * n),
+                                 ("sub+dots", two_pass, (2 * k + 3) * 8 * n),
                                  ("cgs_pass", lambda: ops.sub_dots(V, k, h, w, out), (k + 2) * 8 * n),
                                  ("cgs_norm", lambda: ops.sub_norm(V, k, h, w, out), (k + 2) * 8 * n)):
             fn()
