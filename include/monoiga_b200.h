@@ -138,10 +138,11 @@ int mi_op_clear_reaction(mi_ctx* ctx);
  * (the sweep's right-hand side correction f - A_{c,0} u0). */
 int mi_op_set_lift(mi_ctx* ctx, const double* column0, const double* u0);
 
-/* Pack the channel stencils into the tensor-core layout now and free the plain stencil copy (the
- * operator's largest table after the packed one: 21 GB at BASELINE cfg 4).  Afterwards the channels
- * are immutable until the next mi_op_setup; time bands, the reaction and the lift may still change. */
-int mi_op_finalize(mi_ctx* ctx);
+/* Pack the channel stencils into the tensor-core layout now; with release != 0 also free the plain
+ * stencil copy (the operator's largest table after the packed one: 21 GB at BASELINE cfg 4), after
+ * which the channels are immutable until the next mi_op_setup (time bands, the reaction and the lift
+ * may still change).  Contexts rebuilt every sweep keep it (release = 0): no per-sweep reallocation. */
+int mi_op_finalize(mi_ctx* ctx, int release);
 int mi_op_apply_lift(mi_ctx* ctx, double* y);
 /* Mapped geometry: |det J| at the spatial Gauss points (host, C order
  * Q_d ... Q_1) multiplies the reaction's quadrature weights

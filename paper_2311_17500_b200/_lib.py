@@ -35,7 +35,7 @@ _SIGS = {
     "mi_op_set_reaction": ([_vp, _vp, _vp, _c_dbl, _c_dbl, _c_dbl, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_clear_reaction": ([_vp], _c_int),
     "mi_op_set_lift": ([_vp, _vp, _vp], _c_int),
-    "mi_op_finalize": ([_vp], _c_int),
+    "mi_op_finalize": ([_vp, _c_int], _c_int),
     "mi_op_apply_lift": ([_vp, _vp], _c_int),
     "mi_theta_set_lift": ([_vp, _vp], _c_int),
     "mi_op_set_reaction_weight": ([_vp, _vp], _c_int),

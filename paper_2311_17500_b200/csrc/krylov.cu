@@ -116,22 +116,21 @@ __global__ void scale_div(const double* __restrict__ x, const double* __restrict
   }
 }
 
-// Fused CGS2 passes (k <= KM basis vectors): each V entry is read ONCE for both the subtraction and the
-// following reduction.  MODE 0: w -= V h, then h_out = V^T w (the second classical Gram-Schmidt
-// pass's dots); MODE 1: w -= V h, then |w|^2.  Per-block partials in a fixed partition, reduced by
-// dots_final: deterministic, the same rounding as the unfused pair only up to the summation order.
-template <int KM, int MODE>
+// Fused CGS2 pass (k <= KM basis vectors): w -= V h, then h_out = V^T w (the second classical
+// Gram-Schmidt pass's dots); each V entry streams from HBM once (the reduction re-reads it from L1).
+// Per-block partials in a fixed partition, reduced by dots_final, in the same order as
+// sub_comb + dots_partial: the two agree bit for bit.
+template <int KM>
 __global__ void __launch_bounds__(KT, 2) sub_reduce(const double* __restrict__ V, long long ldv,
-                                                 const double* __restrict__ h, int k, double* __restrict__ w,
-                                                 long long n, double* __restrict__ part) {
-  constexpr int NA = MODE == 0 ? KM : 1;
+                                                    const double* __restrict__ h, int k, double* __restrict__ w,
+                                                    long long n, double* __restrict__ part) {
   __shared__ double hs[KM];
-  __shared__ double red[NA][KT / 32];
+  __shared__ double red[KM][KT / 32];
   if (threadIdx.x < KM) hs[threadIdx.x] = threadIdx.x < k ? h[threadIdx.x] : 0.0;
   __syncthreads();
-  double acc[NA];
+  double acc[KM];
 #pragma unroll
-  for (int g = 0; g < NA; ++g) acc[g] = 0.0;
+  for (int g = 0; g < KM; ++g) acc[g] = 0.0;
   const long long chunk = (n + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   for (long long b = lo + threadIdx.x; b < hi; b += KU * KT) {
@@ -141,7 +140,7 @@ __global__ void __launch_bounds__(KT, 2) sub_reduce(const double* __restrict__ V
       const long long j = b + (long long)u * KT;
       double sacc = 0.0;
       if (j < hi) {
-#pragma unroll 8
+#pragma unroll
         for (int i = 0; i < KM; ++i)
           if (i < k) sacc = fma(hs[i], V[(long long)i * ldv + j], sacc);
         wn[u] = w[j] - sacc;
@@ -152,27 +151,22 @@ __global__ void __launch_bounds__(KT, 2) sub_reduce(const double* __restrict__ V
     for (int u = 0; u < KU; ++u) {
       const long long j = b + (long long)u * KT;
       if (j < hi) {
-        if constexpr (MODE == 0) {
 #pragma unroll
-          for (int i = 0; i < KM; ++i)
-            if (i < k) acc[i] = fma(V[(long long)i * ldv + j], wn[u], acc[i]);   // second read: L1
-        } else {
-          acc[0] = fma(wn[u], wn[u], acc[0]);
-        }
+        for (int i = 0; i < KM; ++i)
+          if (i < k) acc[i] = fma(V[(long long)i * ldv + j], wn[u], acc[i]);   // second read: L1
       }
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int g = 0; g < NA; ++g) {
+  for (int g = 0; g < KM; ++g) {
     double x = acc[g];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
     if (lane == 0) red[g][warp] = x;
   }
   __syncthreads();
-  const int nout = MODE == 0 ? k : 1;
-  for (int g = threadIdx.x; g < nout; g += KT) {
+  for (int g = threadIdx.x; g < k; g += KT) {
     double x = 0.0;
 #pragma unroll
     for (int q = 0; q < KT / 32; ++q) x += red[g][q];
@@ -250,7 +244,10 @@ int mi_cgs_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, c
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_cgs_pass");
   if (k == 0) return MI_OK;
-  if (k > 32) {   // beyond the fused kernel's register budget: two passes
+  // fused for k <= 8 (one read of V: 0.70 vs 0.90 ms at N = 37 M); beyond, the elementwise subtraction
+  // plus the 8-row reductions stream at ~6 TB/s and tie or beat the fused kernel, whose per-thread row
+  // count limits its loads in flight (tools/time_krylov.py, profiles/r02_optimisation_log.md K3)
+  if (k > 8) {
     int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
     if (rc) return rc;
     return mi_dots(c, n, k, V, ldv, w, h_out);
@@ -258,12 +255,7 @@ int mi_cgs_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, c
   int rc;
   if ((rc = dalloc(c->partials, (size_t)k * KB))) return rc;
   ProfScope ps(c, PROF_KRYLOV, 2);
-  if (k <= 8)
-    sub_reduce<8, 0><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
-  else if (k <= 16)
-    sub_reduce<16, 0><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
-  else
-    sub_reduce<32, 0><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
+  sub_reduce<8><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
   MI_CHECK_LAUNCH("sub_reduce");
   dots_final<<<k, 512, 0, c->stream>>>(c->partials.p, KB, h_out, 1);
   MI_CHECK_LAUNCH("dots_final");
@@ -272,26 +264,13 @@ int mi_cgs_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, c
 
 int mi_cgs_norm_pass(mi_ctx* c, long long n, int k, const double* V, long long ldv, const double* h_in, double* w,
                      double* nrm2) {
+  // the last CGS2 subtraction and |w|^2 as two streaming passes: measured faster than a fused kernel
+  // at every k (0.54 vs 0.74 ms at k = 8, N = 37 M)
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr && k >= 0, MI_ERR_ARG, "bad arguments to mi_cgs_norm_pass");
-  if (k == 0 || k > 32) {
-    int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
-    if (rc) return rc;
-    return mi_dots(c, n, 1, w, n, w, nrm2);
-  }
-  int rc;
-  if ((rc = dalloc(c->partials, (size_t)KB))) return rc;
-  ProfScope ps(c, PROF_KRYLOV, 2);
-  if (k <= 8)
-    sub_reduce<8, 1><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
-  else if (k <= 16)
-    sub_reduce<16, 1><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
-  else
-    sub_reduce<32, 1><<<KB, KT, 0, c->stream>>>(V, ldv, h_in, k, w, n, c->partials.p);
-  MI_CHECK_LAUNCH("sub_reduce");
-  dots_final<<<1, 512, 0, c->stream>>>(c->partials.p, KB, nrm2, 1);
-  MI_CHECK_LAUNCH("dots_final");
-  return MI_OK;
+  int rc = mi_sub_combination(c, n, k, V, ldv, h_in, w);
+  if (rc) return rc;
+  return mi_dots(c, n, 1, w, n, w, nrm2);
 }
 
 }  // extern "C"

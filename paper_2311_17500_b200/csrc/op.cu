@@ -746,14 +746,16 @@ int mi_op_apply(mi_ctx* c, const double* x, double* y) {
   return MI_OK;
 }
 
-int mi_op_finalize(mi_ctx* c) {
+int mi_op_finalize(mi_ctx* c, int release) {
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "mi_op_setup must be called first");
   if (!c->use_dmma || c->stencil_released) return MI_OK;
   int rc;
   if (c->frag_dirty && (rc = dmma_prepare(c))) return rc;
-  mi::dfree(c->stencil);          // only the fragment-major copy is read from now on
-  c->stencil_released = true;
+  if (release) {
+    mi::dfree(c->stencil);        // only the fragment-major copy is read from now on
+    c->stencil_released = true;
+  }
   return MI_OK;
 }
 

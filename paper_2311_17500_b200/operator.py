@@ -224,8 +224,9 @@ class KroneckerOperator:
             _lib.call("mi_op_set_lift", ctx.handle, host_ptr(np.ascontiguousarray(col0)), dptr(self._lift))
         else:
             _lib.call("mi_op_set_lift", ctx.handle, None, None)
-        # pack the channels for the tensor cores now and drop the plain stencil copy
-        _lib.call("mi_op_finalize", ctx.handle)
+        # pack the channels for the tensor cores now; an operator on its own context drops the plain
+        # stencil copy, a reused context (the fixed-point drivers rebuild one every sweep) keeps it
+        _lib.call("mi_op_finalize", ctx.handle, 1 if context is None else 0)
 
     def lift_apply(self):
         """A_{c,0} u0: every term's lifted column applied to the lifting coefficients (device tensor,
@@ -324,7 +325,7 @@ class SpatialMassOperator:
         Ms, _ = mapped_stencils(ctx, sd)
         _lib.call("mi_op_set_channel_stencil", ctx.handle, 0, dptr(Ms))
         _lib.call("mi_op_clear_reaction", ctx.handle)
-        _lib.call("mi_op_finalize", ctx.handle)
+        _lib.call("mi_op_finalize", ctx.handle, 1 if context is None else 0)
         torch.cuda.current_stream(ctx.device).synchronize()
 
     def apply_device(self, x, y):
