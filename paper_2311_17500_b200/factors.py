@@ -15,6 +15,7 @@ All tables are <= O(n^2) with n <= a few hundred.
 import numpy as np
 import scipy.linalg as sla
 
+from ._blas import single_thread_blas as _single_thread_blas
 from .errors import DecompositionError, StabilizationError
 from .spaces import (SplineSpace, basis_table, cells_with, gauss_rule, greville,
                      time_factors, to_band, univariate_factors)
@@ -135,29 +136,7 @@ def lowrank_factorize(values, tol):
 GRAM_MIN_SIZE = 2_000_000
 
 
-class _single_thread_blas:
-    """Small dense LAPACK calls (N_t x N_s indicators of small problems, the N_t x N_t pencil) run on one
-    BLAS thread: a many-threaded OpenBLAS spends far longer waking its pool than computing them
-    (measured 28 ms per 65 x 66 SVD on a 16-core GPU host inside the fixed-point driver)."""
 
-    def __init__(self, on):
-        self.on = on
-        self.ctx = None
-
-    def __enter__(self):
-        if self.on:
-            try:
-                from threadpoolctl import threadpool_limits
-                self.ctx = threadpool_limits(limits=1, user_api="blas")
-                self.ctx.__enter__()
-            except Exception:      # threadpoolctl is optional: then nothing is limited
-                self.ctx = None
-        return self
-
-    def __exit__(self, *exc):
-        if self.ctx is not None:
-            self.ctx.__exit__(*exc)
-        return False
 
 
 def _lowrank_device(th, tol):
@@ -360,8 +339,9 @@ def spatial_eigs(st, lengths=None):
         M, K, _ = univariate_factors(s)
         Kl, Ml = (cm / L[l] ** 2) * K, cm * M
         try:
-            split = _centro_eigh(Kl, Ml)
-            lam, U = split if split is not None else sla.eigh(Kl, Ml)
+            with _single_thread_blas():
+                split = _centro_eigh(Kl, Ml)
+                lam, U = split if split is not None else sla.eigh(Kl, Ml)
         except sla.LinAlgError as exc:
             raise DecompositionError("generalized eigendecomposition failed: %s" % exc) from exc
         out.append((U, lam))
@@ -491,4 +471,5 @@ class RealTimePencil:
 
 def time_pencil(st, final_time):
     Wt, Mt = time_factors(st, final_time)
-    return RealTimePencil(Wt, Mt)
+    with _single_thread_blas():
+        return RealTimePencil(Wt, Mt)

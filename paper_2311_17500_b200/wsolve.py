@@ -15,6 +15,7 @@ import scipy.linalg as sla
 import torch
 
 from . import _lib
+from ._blas import single_thread_blas
 from .device import DeviceContext, dptr, host_ptr
 from .errors import DecompositionError, NonConvergenceError
 from .spaces import time_factors, univariate_factors
@@ -35,10 +36,12 @@ class RecoverySolver:
         Wt, Mt = time_factors(st, final_time)
         Kt = Wt + recovery_rate * equilibrium_rate * Mt
         try:
-            lu = sla.lu_factor(Kt)
+            with single_thread_blas():
+                lu = sla.lu_factor(Kt)
         except sla.LinAlgError as exc:  # pragma: no cover - singular K_t
             raise DecompositionError("temporal recovery matrix is singular: %s" % exc) from exc
-        Kinv = np.ascontiguousarray(sla.lu_solve(lu, np.eye(Kt.shape[0])))
+        with single_thread_blas():
+            Kinv = np.ascontiguousarray(sla.lu_solve(lu, np.eye(Kt.shape[0])))
         nmax = max(ctx.n)
         M = np.zeros((d, nmax, nmax))
         Minv = np.zeros((d, nmax, nmax))
