@@ -757,8 +757,8 @@ def run_ours(args):
         spec.loader.exec_module(solve_mapped)
         try:
             line["mapped_cfg5"] = {"geometry": "prolate shell slab, quarter sector (our construction, SURVEY App. B)",
-                                   "conductivity": "apply and Galerkin solve: fibre-aligned sigma_l 1e-3 / sigma_t 3e-4 "
-                                                   "(fibres along the azimuth); SU solve: scalar 1e-3",
+                                   "conductivity": "fibre-aligned sigma_l 1e-3 / sigma_t 3e-4 (fibres along the "
+                                                   "azimuth) in the apply and both solves",
                                    "apply": solve_mapped.apply_rate(64, 256, 3, 5),
                                    "solve_galerkin": solve_mapped.solve(32, 64, 3, 60),
                                    "solve_su": solve_mapped.solve(32, 64, 3, 60, "spline_upwind")}

@@ -37,9 +37,6 @@ class _Workspace:
         # mapped geometries: quadrature M_s / K_s, |det J| reaction, separable-weight P^-1 (solver.py:167-202)
         from .geometry import is_fibre
         fibre = problem.D if is_fibre(problem.D) else None
-        if fibre is not None and config.stabilization == "spline_upwind":
-            raise NotImplementedError("the residual indicator with a fibre conductivity (div(D grad u) with a "
-                                      "varying D) is not built; use Galerkin")
         self.sd = (MappedSpatialData(st.spatial, problem.geometry, conductivity=fibre,
                                      coefficient_rank=config.coefficient_rank, coefficient_tol=config.coefficient_tol)
                    if is_mapped(problem.geometry) else None)

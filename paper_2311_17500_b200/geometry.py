@@ -178,6 +178,28 @@ class FibreConductivity:
         return self.sigma_t * eye + (self.sigma_l - self.sigma_t) * (f[..., :, None] * f[..., None, :])
 
 
+    def diffusion_coefficients(self, jac, hess, jinv):
+        """(MD, divD) for the strong residual's div(D grad u) on a grid of Gauss points (host numpy):
+        div(D grad u) = sum_ab MD_ab (d_ab u - sum_e H_abe g_e) + sum_d divD_d g_d with g = J^-T grad_eta u,
+        MD = J^-1 D J^-T (the stiffness metric) and divD_d = sum_c d(D_cd)/dx_c
+        = (sigma_l - sigma_t) ((div f) f_d + ((f . grad) f)_d), the fibre's physical derivatives from
+        the map Hessian: d_a f = (d_a J_k - f (f . d_a J_k)) / |J_k|, df/dx_c = sum_a J^-1[a, c] d_a f.
+        (The extension of stabilization.py:273-295 -- whose D is a scalar -- to the cfg-5 fibres.)"""
+        k = self.direction
+        Jk = jac[..., :, k]
+        nrm = np.linalg.norm(Jk, axis=-1, keepdims=True)
+        f = Jk / nrm
+        D = self.sigma_t * np.eye(jac.shape[-1]) + (self.sigma_l - self.sigma_t) * (f[..., :, None] * f[..., None, :])
+        MD = np.einsum("...ac,...cd,...bd->...ab", jinv, D, jinv)
+        dJk = hess[..., :, k, :]                                        # [a, c] = d_a d_k x_c
+        da_f = (dJk - f[..., None, :] * np.einsum("...ac,...c->...a", dJk, f)[..., :, None]) / nrm[..., None]
+        dfdx = np.einsum("...ac,...ad->...cd", jinv, da_f)             # [c, d] = d f_d / d x_c
+        divf = np.einsum("...cc->...", dfdx)
+        fgradf = np.einsum("...c,...cd->...d", f, dfdx)
+        divD = (self.sigma_l - self.sigma_t) * (divf[..., None] * f + fgradf)
+        return MD, divD
+
+
 def is_fibre(D):
     return isinstance(D, FibreConductivity)
 

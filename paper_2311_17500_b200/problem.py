@@ -424,12 +424,17 @@ def window_elements(space, i):
 
 
 def _mapped_laplacian(problem, g, u):
-    """D times the physical Laplacian of u at the Gauss grid of a mapped geometry, pulled back with
-    the inverse Jacobian and the map's Hessians (stabilization.py:273-295):
-    lap = sum_ab (J^-1 J^-T)_ab (d_ab u - sum_c H_abc g_c), g_c = sum_i (J^-1)_ic d_i u."""
+    """div(D grad u) at the Gauss grid of a mapped geometry, pulled back with the inverse Jacobian and
+    the map's Hessians (stabilization.py:273-295): D lap u = D sum_ab (J^-1 J^-T)_ab (d_ab u -
+    sum_c H_abc g_c), g_c = sum_i (J^-1)_ic d_i u; with a FibreConductivity the metric is J^-1 D J^-T
+    and div D adds sum_d (div D)_d g_d (FibreConductivity.diffusion_coefficients)."""
+    from .geometry import is_fibre
     st, d = problem.space, g.d
     geo_data = g.mapped.geo.grid_data([r[0] for r in g.mapped.rules], order=2)
     jinv, hess = g.mapped.jinv, geo_data["hess"]
+    fibre = is_fibre(problem.D)
+    if fibre:
+        MD, divD = problem.D.diffusion_coefficients(geo_data["jac"], hess, jinv)
     firsts = []
     for a in range(d):
         orders = [0] * d
@@ -446,8 +451,10 @@ def _mapped_laplacian(problem, g, u):
             second = g.field(u, orders, 0) if max(orders) <= min(2, st.spatial[a].degree, st.spatial[b].degree) \
                 else np.zeros_like(lap)
             corr = np.einsum("...c,t...c->t...", hess[..., a, b, :], grad_phys)
-            metric = np.einsum("...k,...k->...", jinv[..., a, :], jinv[..., b, :])
+            metric = MD[..., a, b] if fibre else np.einsum("...k,...k->...", jinv[..., a, :], jinv[..., b, :])
             lap += metric[None] * (second - corr)
+    if fibre:
+        return lap + np.einsum("...d,t...d->t...", divD, grad_phys)
     return problem.D * lap
 
 

@@ -232,11 +232,21 @@ class MappedDeviceIndicator(DeviceIndicator):
         self.tB0 = [torch.tensor(np.asarray(t), device=dev) for t in g.tB0]
         self.sB = [[torch.tensor(np.asarray(t), device=dev) for t in tl] for tl in g.sB]
         # per spatial Gauss point: cg_i = -sum_ab m_ab sum_c H_abc (J^-1)_ic, cm_ab = m_ab (x2 off-diagonal)
-        hess = sd.geo.grid_data([r[0] for r in sd.rules], order=2)["hess"]
+        gdat = sd.geo.grid_data([r[0] for r in sd.rules], order=2)
+        hess = gdat["hess"]
         jinv = sd.jinv
-        metric = np.einsum("...ak,...bk->...ab", jinv, jinv)
         hj = np.einsum("...abc,...ic->...abi", hess, jinv)
-        coef = [-np.einsum("...ab,...abi->...i", metric, hj)[..., i] for i in range(d)]
+        from .geometry import is_fibre
+        if is_fibre(problem.D):
+            # div(D grad u) with the fibre tensor: the metric J^-1 D J^-T and the first-order term of div D
+            metric, divD = problem.D.diffusion_coefficients(gdat["jac"], hess, jinv)
+            coef = [(-np.einsum("...ab,...abi->...i", metric, hj) + np.einsum("...d,...id->...i", divD, jinv))[..., i]
+                    for i in range(d)]
+            self.diff = 1.0
+        else:
+            metric = np.einsum("...ak,...bk->...ab", jinv, jinv)
+            coef = [-np.einsum("...ab,...abi->...i", metric, hj)[..., i] for i in range(d)]
+            self.diff = float(problem.D)
         self.pairs = [(a, a) for a in range(d)] + [(a, b) for a in range(d) for b in range(a + 1, d)]
         coef += [metric[..., a, b] * (1.0 if a == b else 2.0) for a, b in self.pairs]
         self.coef = torch.tensor(np.ascontiguousarray(np.stack([c.reshape(-1) for c in coef])), device=dev)
@@ -325,7 +335,7 @@ class MappedDeviceIndicator(DeviceIndicator):
             F = self._fields(U, W, et0, et1, ld)
             _lib.call("mi_theta_mapped_elements", ctx.handle, dptr(F), dptr(self.coef),
                       dptr(fd) if fd is not None else None, int(et0), int(et1), host_ptr(self.G), self.q, qt,
-                      host_ptr(nel), float(pr.D), float(pr.C_m) / self.T, float(pr.c1), float(pr.a), float(pr.c2),
+                      host_ptr(nel), self.diff, float(pr.C_m) / self.T, float(pr.c1), float(pr.a), float(pr.c2),
                       dptr(emax), dptr(maxes))
             del F
         return self._finish(emax, maxes, on_device)

@@ -10,8 +10,8 @@ our construction: the reference has no such geometry), p = 3.
          0.3 <= t < 0.35 (not expressible as initial data).
 
 Conductivity: cfg 5's fibre-aligned sigma_l = 1e-3 / sigma_t = 3e-4 (geometry.FibreConductivity, fibres
-along the azimuth; an extension of the reference's scalar D) for the apply and the Galerkin solve; the
-Spline Upwind solve uses the scalar D = 1e-3.  Coefficients: cfg 5's canonical rank <= 8 approximation
+along the azimuth; an extension of the reference's scalar D) for the apply and both solves (the Spline
+Upwind indicator takes div(D grad u) with the varying fibre tensor).  Coefficients: cfg 5's canonical rank <= 8 approximation
 of |det J| and |det J| J^-1 D J^-T (geometry.LowRankCoefficients, --rank 8, the default); --rank 0
 integrates the exact pulled-back coefficients (the reference's SpatialQuadratureData).
 
@@ -98,10 +98,9 @@ def s2_source():
 
 def solve(ne, ne_t, p, max_it, stab="off", rank=8):
     st = mb.SpaceTimeSpace([mb.SplineSpace.uniform(p, ne) for _ in range(3)], mb.SplineSpace.uniform(p, ne_t))
-    # Galerkin: the fibre conductivity; Spline Upwind: scalar D = sigma_l (its residual indicator with a
-    # varying conductivity tensor is not built)
-    prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s2_source(),
-                                D=FIBRE if stab == "off" else 1e-3, u0=s1_initial)
+    # both with cfg 5's fibre conductivity (the SU residual indicator takes div(D grad u) with the
+    # fibre tensor varying along the map, FibreConductivity.diffusion_coefficients)
+    prob = mb.MonodomainProblem(prolate_shell_geometry(), st, source=s2_source(), D=FIBRE, u0=s1_initial)
     cfg = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8, max_iterations=max_it,
                               coefficient_rank=rank or None)
     torch.cuda.synchronize()
@@ -111,7 +110,7 @@ def solve(ne, ne_t, p, max_it, stab="off", rank=8):
     return {"mesh": [ne] * 3 + [ne_t], "p": p, "N": st.num_dof, "wall_seconds": time.perf_counter() - t0,
             "sweeps": res.iterations, "converged": res.converged, "gmres_per_sweep": res.gmres_iterations,
             "avg_pcg": res.avg_pcg, "phase_seconds": {k: round(v, 3) for k, v in res.phase_seconds.items()},
-            "stabilization": stab, "conductivity": "fibre 1e-3 / 3e-4" if stab == "off" else "scalar 1e-3",
+            "stabilization": stab, "conductivity": "fibre 1e-3 / 3e-4",
             "stimulus": "S1 u0 on the phi=0 face (lifting) + S2 source pulse on a quadrant at t=0.3",
             "u_max": float(np.abs(res.u).max()),
             "coefficients": "canonical rank <= %d" % rank if rank else "exact"}
