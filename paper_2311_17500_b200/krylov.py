@@ -69,11 +69,10 @@ class DeviceVecOps:
                   dptr(x0) if x0 is not None else ctypes.c_void_p(0), dptr(out))
 
 
-def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=None, n_global=None, apply_PA=None):
+def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=None, n_global=None):
     """CGS2 GMRES on (local) vectors; see module docstring.
 
-    apply_A(src, dst), apply_P(src, dst): device applies on local vectors; apply_PA(src, dst) (optional)
-    does both in one call (a replayed CUDA graph for small problems).
+    apply_A(src, dst), apply_P(src, dst): device applies on local vectors.
     allreduce(t): in-place sum over ranks of a small tensor (None = 1 rank).
     Returns (x_local, iterations, history).
     """
@@ -132,11 +131,8 @@ def gmres_core(apply_A, apply_P, ops, b, x0, tol, m, allreduce=None, log_path=No
             cap = new_cap
         h1 = scal[8:8 + cap + 1]
         h2 = scal[8 + cap + 1:8 + 2 * (cap + 1)]
-        if apply_PA is not None:
-            apply_PA(V[j], w)
-        else:
-            apply_A(V[j], tmp)
-            apply_P(tmp, w)
+        apply_A(V[j], tmp)
+        apply_P(tmp, w)
         k = j + 1
         # CGS2 (linalg.py:405-412); the fused passes read V once per subtraction + reduction
         ops.dots(V, k, w, h1)
@@ -220,43 +216,6 @@ def gmres(op, rhs, precond=None, tol=1e-8, max_iter=None, x0=None, log_path=None
             precond.apply_device(src, dst)
 
     x0d = None if x0 is None else ctx.to_device(x0)
-    PA = _graph_apply(op, precond, ctx, b) if precond is not None and n <= GRAPH_MAX_N else None
-    x, it, hist = gmres_core(op.apply_device, P, DeviceVecOps(ctx), b, x0d, tol, m, log_path=log_path,
-                             apply_PA=PA)
+    x, it, hist = gmres_core(op.apply_device, P, DeviceVecOps(ctx), b, x0d, tol, m, log_path=log_path)
     return (x.cpu().numpy() if as_numpy else x), it, hist
 
-
-# Below this size one P^-1 A apply is a few microseconds of kernel time per launch, and the launches
-# and their host calls dominate a GMRES iteration: the pair is captured once per solve as a CUDA graph
-# and replayed (BASELINE cfg 1: N = 4,290).
-GRAPH_MAX_N = 1 << 20
-
-
-def _graph_apply(op, precond, ctx, like):
-    """z = P^-1 (A v) as a replayed CUDA graph over fixed buffers; None if capture fails (the plain
-    calls are then used).  One eager apply first runs every lazy setup step outside the capture."""
-    vin, tmp, out = torch.empty_like(like), torch.empty_like(like), torch.empty_like(like)
-    vin.zero_()
-    op.apply_device(vin, tmp)
-    precond.apply_device(tmp, out)
-    torch.cuda.synchronize(like.device)
-    g = torch.cuda.CUDAGraph()
-    try:
-        with torch.cuda.graph(g):
-            op.apply_device(vin, tmp)
-            precond.apply_device(tmp, out)
-    except Exception:
-        return None
-    finally:
-        ctx.bind_stream()            # back on the caller's stream
-        pctx = getattr(precond, "ctx", None)
-        if pctx is not None:
-            pctx.bind_stream()
-
-    def apply(src, dst):
-        vin.copy_(src)
-        g.replay()
-        dst.copy_(out)
-
-    apply.graph = g                  # keeps the graph (and its buffers) alive with the closure
-    return apply
