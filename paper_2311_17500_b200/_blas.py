@@ -19,15 +19,30 @@ class single_thread_blas:
 
     def __enter__(self):
         if self.on:
-            try:
-                from threadpoolctl import threadpool_limits
-                self.ctx = threadpool_limits(limits=1, user_api="blas")
-                self.ctx.__enter__()
-            except Exception:      # threadpoolctl is optional: then nothing is limited
-                self.ctx = None
+            ctl = _controller()
+            if ctl is not None:
+                try:
+                    self.ctx = ctl.limit(limits=1, user_api="blas")
+                    self.ctx.__enter__()
+                except Exception:
+                    self.ctx = None
         return self
 
     def __exit__(self, *exc):
         if self.ctx is not None:
             self.ctx.__exit__(*exc)
         return False
+
+
+_CONTROLLER = []
+
+
+def _controller():
+    """One threadpoolctl controller per process (building one scans every loaded library: ~1 ms)."""
+    if not _CONTROLLER:
+        try:
+            from threadpoolctl import ThreadpoolController
+            _CONTROLLER.append(ThreadpoolController())
+        except Exception:      # threadpoolctl is optional: then nothing is limited
+            _CONTROLLER.append(None)
+    return _CONTROLLER[0]
