@@ -614,7 +614,8 @@ def run_ours(args):
 
     def serial(nsteps):
         for k in range(nsteps):
-            zhs[k % 2].copy_(P.apply(op.matvec(xhs[k % 2].to(dev, non_blocking=True))), non_blocking=True)
+            # the host vector streams in z-plane chunks under the stencil (mi_op_apply_from_host)
+            zhs[k % 2].copy_(P.apply(op.matvec_from_host(xhs[k % 2])), non_blocking=True)
 
     pipe = mb.ApplyStream(op, P, depth=2)
 
@@ -680,9 +681,9 @@ def run_ours(args):
         "config": workload_config(world),
         "channels": op.nchan, "setup_s": t_setup,
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
-                "path": "the reference-facing calls KroneckerOperator.matvec + FastDiagPreconditioner.apply per "
-                        "vector (each step: pinned host x -> device, A, P^-1, device -> pinned host z; one "
-                        "stream, dependent like a GMRES iteration)",
+                "path": "per vector, the public calls KroneckerOperator.matvec_from_host (pinned host x, its H2D "
+                        "copy streamed in z-plane chunks under the stencil) + FastDiagPreconditioner.apply, then "
+                        "device -> pinned host z; dependent like a GMRES iteration (no overlap across steps)",
                 "streamed_value": e2_streamed,
                 "streamed_path": "ApplyStream over independent vectors: copy-in of k+1 / apply of k / copy-out "
                                  "of k-1 on three streams (not usable inside one GMRES solve)"},

@@ -111,6 +111,11 @@ int mi_op_set_channel_stencil(mi_ctx* ctx, int c, const double* stencil);
 int mi_op_get_channel_stencil(mi_ctx* ctx, int c, double* stencil);
 /* y = A x   (x, y device, length N, must not alias) */
 int mi_op_apply(mi_ctx* ctx, const double* x, double* y);
+/* y = A x for x in PINNED HOST memory (x_dev: a device buffer of N for the copy): the host-to-device copy
+ * of x runs on the context's copy stream in nparts z-plane chunks, and the stencil over the cube layers
+ * of chunk p runs while chunk p+1 is still on its way (d = 3 tensor-core operator; otherwise one copy
+ * then mi_op_apply).  The reference-facing KroneckerOperator.matvec path for host input. */
+int mi_op_apply_from_host(mi_ctx* ctx, const double* x_host, double* x_dev, double* y, int nparts);
 
 /* Reaction correction y += M_R x (added by every subsequent mi_op_apply),
  * M_R = int int C_r B_i B_j with the Rogers-McCulloch linearisation

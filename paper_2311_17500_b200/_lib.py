@@ -32,6 +32,7 @@ _SIGS = {
     "mi_op_set_kron_channel": ([_vp, _c_int, _c_int, _vp, _vp], _c_int),
     "mi_op_set_su_channel": ([_vp, _c_int, _vp, _vp, _c_int], _c_int),
     "mi_op_apply": ([_vp, _vp, _vp], _c_int),
+    "mi_op_apply_from_host": ([_vp, _vp, _vp, _vp, _c_int], _c_int),
     "mi_op_set_reaction": ([_vp, _vp, _vp, _c_dbl, _c_dbl, _c_dbl, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_clear_reaction": ([_vp], _c_int),
     "mi_op_set_lift": ([_vp, _vp, _vp], _c_int),

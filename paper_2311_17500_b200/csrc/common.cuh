@@ -162,4 +162,8 @@ struct mi_ctx {
 
   // ---- Krylov scratch
   mi::DeviceBuf partials;       // reduction partials
+
+  // ---- host-input apply (mi_op_apply_from_host): H2D copy stream and per-chunk events
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_events;
 };

@@ -198,6 +198,8 @@ int mi_ctx_destroy(mi_ctx* c) {
     cudaEventDestroy(r.b);
   }
   for (auto e : c->prof_pool) cudaEventDestroy(e);
+  for (auto e : c->copy_events) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
   return MI_OK;
 }

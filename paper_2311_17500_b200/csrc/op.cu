@@ -678,36 +678,49 @@ static int launch_time_filter(mi_ctx* c, double* y) {
   return MI_OK;
 }
 
-static int dmma_apply(mi_ctx* c, const double* x, double* y) {
+// The DMMA operator in stages: transpose spatial points [s_lo, s_hi) of x into xt, run the stencil over
+// cubes [cube_lo, cube_hi) (z-slowest numbering), then the time filter over everything.  dmma_apply runs
+// them once over the whole domain; mi_op_apply_from_host interleaves them with the H2D copy of x.
+static int dmma_transpose(mi_ctx* c, const double* x, long long s_lo, long long s_hi) {
+  const int ntp = ((c->nt + 15) / 16) * 16;          // = DmmaSten<.,.>::TT multiple (TT = 16)
+  if (s_hi <= s_lo) return MI_OK;
+  ProfScope ps(c, PROF_OP_STENCIL);
+  dim3 tg((unsigned)((s_hi - s_lo + 31) / 32), (ntp + 31) / 32);
+  transpose_time_inner<<<tg, dim3(32, 8), 0, c->stream>>>(x + s_lo, c->xt.p + s_lo * ntp, c->nt, ntp, s_hi - s_lo,
+                                                          c->ns_in);
+  MI_CHECK_LAUNCH("transpose_time_inner");
+  return MI_OK;
+}
+
+static int dmma_stencil(mi_ctx* c, double* y, int cube_lo, int cube_hi) {
   MI_DISPATCH_DP(c->d, c->p, {
     using G = DmmaSten<D_, P_>;
+    static_assert(G::TT == 16, "dmma_transpose pads time to multiples of 16");
     const long long ncubes = (long long)c->C[0] * c->C[1] * c->C[2];
     const long long per_group = ncubes * G::PPB * G::KS * 32;
     const int ngroups = (c->nchan + 7) / 8;
     const int ntp = ((c->nt + G::TT - 1) / G::TT) * G::TT;
-    {
-      ProfScope ps(c, PROF_OP_STENCIL);
-      dim3 tg((unsigned)((c->ns_in + 31) / 32), (ntp + 31) / 32);
-      transpose_time_inner<<<tg, dim3(32, 8), 0, c->stream>>>(x, c->xt.p, c->nt, ntp, c->ns_in);
-      MI_CHECK_LAUNCH("transpose_time_inner");
-    }
-    for (int gi = 0; gi < ngroups; ++gi) {
+    for (int gi = 0; gi < ngroups && cube_hi > cube_lo; ++gi) {
       DmmaArgs a{c->xt.p, c->wbuf.p, c->frag.p + gi * per_group, c->tband.p, y, gi * 8, min(8, c->nchan - gi * 8), c->pt,
-                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns, c->hz_lo};
+                 gi > 0 ? 1 : 0, c->n[0], c->n[1], c->n[2], c->nt, ntp, c->C[0], c->C[1], c->C[2], c->ns, c->hz_lo,
+                 cube_lo, cube_hi};
       ProfScope ps(c, PROF_OP_STENCIL);
       // persistent: one CTA per SM (the kernel is sized for 1 CTA / SM), each sweeping cubes b, b + grid, ...
-      const long long grid = MI_STEN_PERSIST ? std::min<long long>(ncubes, mi::num_sms()) : ncubes;
+      const long long nc = cube_hi - cube_lo;
+      const long long grid = MI_STEN_PERSIST ? std::min<long long>(nc, mi::num_sms()) : nc;
       stencil_dmma<D_, P_><<<(unsigned)grid, G::THREADS, G::SMEM, c->stream>>>(a, c->tmap_xt);
       MI_CHECK_LAUNCH("stencil_dmma");
     }
-    {
-      ProfScope ps(c, PROF_OP_TFILTER);
-      int frc = launch_time_filter(c, y);
-      if (frc) return frc;
-      MI_CHECK_LAUNCH("time_filter_ti");
-    }
   });
   return MI_OK;
+}
+
+static int dmma_apply(mi_ctx* c, const double* x, double* y) {
+  int rc;
+  if ((rc = dmma_transpose(c, x, 0, c->ns_in))) return rc;
+  if ((rc = dmma_stencil(c, y, 0, c->C[0] * c->C[1] * c->C[2]))) return rc;
+  ProfScope ps(c, PROF_OP_TFILTER);
+  return launch_time_filter(c, y);
 }
 
 // y = sum_c T_c (x) S_c x (every Kronecker / SU / quadrature channel; no reaction)
@@ -742,6 +755,58 @@ int mi_op_apply(mi_ctx* c, const double* x, double* y) {
   if (c->reaction_on) {
     ProfScope ps(c, PROF_OP_REACTION);
     return reaction_apply(c, x, y, nullptr);
+  }
+  return MI_OK;
+}
+
+int mi_op_apply_from_host(mi_ctx* c, const double* x_host, double* x_dev, double* y, int nparts) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c && c->op_ready, MI_ERR_STATE, "operator not set up");
+  MI_REQUIRE(x_host && x_dev && y && x_dev != y, MI_ERR_ARG, "bad pointers to mi_op_apply_from_host");
+  const long long plane = (long long)c->n[0] * c->n[1];
+  if (!c->use_dmma || c->d != 3 || c->ns_in != c->ns || nparts <= 1) {
+    MI_CUDA(cudaMemcpyAsync(x_dev, x_host, sizeof(double) * c->N, cudaMemcpyHostToDevice, c->stream));
+    return mi_op_apply(c, x_dev, y);
+  }
+  int rc;
+  if (c->frag_dirty && (rc = dmma_prepare(c))) return rc;
+  if (!c->copy_stream) MI_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  while ((int)c->copy_events.size() < nparts + 1) {
+    cudaEvent_t e;
+    MI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->copy_events.push_back(e);
+  }
+  // part p: the stencil over cube layers [cz_p, cz_{p+1}) (cube z size B3 = 2 planes); H2D chunk p holds
+  // planes [b_p, b_{p+1}) with b_p = cz_p B3 + p_s (the stencil of part p reads up to p_s planes past its
+  // layers).  Chunk p+1 copies while part p's stencil runs.
+  const int C3 = c->C[2], B3 = (int)((c->n[2] + C3 - 1) / C3);
+  nparts = std::min(nparts, C3);
+  std::vector<int> cz(nparts + 1), b(nparts + 1);
+  for (int q = 0; q <= nparts; ++q) cz[q] = (int)((long long)q * C3 / nparts);
+  for (int q = 0; q <= nparts; ++q) b[q] = q == 0 ? 0 : (q == nparts ? c->n[2] : std::min(c->n[2], cz[q] * B3 + c->p));
+  // x_dev is free once the compute stream reaches this point
+  MI_CUDA(cudaEventRecord(c->copy_events[nparts], c->stream));
+  MI_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_events[nparts], 0));
+  for (int q = 0; q < nparts; ++q) {
+    const long long o = b[q] * plane, w = (long long)(b[q + 1] - b[q]) * plane;
+    if (w > 0)
+      MI_CUDA(cudaMemcpy2DAsync(x_dev + o, sizeof(double) * c->ns, x_host + o, sizeof(double) * c->ns,
+                                sizeof(double) * w, c->nt, cudaMemcpyHostToDevice, c->copy_stream));
+    MI_CUDA(cudaEventRecord(c->copy_events[q], c->copy_stream));
+  }
+  const int cubes_per_layer = c->C[0] * c->C[1];
+  for (int q = 0; q < nparts; ++q) {
+    MI_CUDA(cudaStreamWaitEvent(c->stream, c->copy_events[q], 0));
+    if ((rc = dmma_transpose(c, x_dev, b[q] * plane, b[q + 1] * plane))) return rc;
+    if ((rc = dmma_stencil(c, y, cz[q] * cubes_per_layer, cz[q + 1] * cubes_per_layer))) return rc;
+  }
+  {
+    ProfScope ps(c, PROF_OP_TFILTER);
+    if ((rc = launch_time_filter(c, y))) return rc;
+  }
+  if (c->reaction_on) {
+    ProfScope ps(c, PROF_OP_REACTION);
+    return reaction_apply(c, x_dev, y, nullptr);
   }
   return MI_OK;
 }

@@ -98,18 +98,21 @@ struct DmmaArgs {
   int C1, C2, C3;       // cube grid
   long long ns;
   int zoff;             // halo planes below the owned ones in xt (z-slab contexts; 0 unsharded)
+  int cube_lo, cube_hi; // cubes of this launch (a z range: cubes are numbered z-slowest)
 };
 
-// x (nt, ns) -> xt (ns, ntp), zero padded in time; 32x32 smem tiles.
+// x (nt, ns) -> xt (ns, ntp), zero padded in time; 32x32 smem tiles.  Columns [0, ns) of x and rows
+// [0, ns) of xt, both given already offset to the first spatial index of the range; x_ld = x's row
+// stride (the full N_s when a range of spatial points is transposed).
 __global__ void transpose_time_inner(const double* __restrict__ x, double* __restrict__ xt, int nt, int ntp,
-                                     long long ns) {
+                                     long long ns, long long x_ld) {
   __shared__ double tile[32][33];
   const long long s0 = (long long)blockIdx.x * 32;
   const int t0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int t = t0 + r;
     const long long s = s0 + threadIdx.x;
-    tile[r][threadIdx.x] = (t < nt && s < ns) ? x[(long long)t * ns + s] : 0.0;
+    tile[r][threadIdx.x] = (t < nt && s < ns) ? x[(long long)t * x_ld + s] : 0.0;
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -152,12 +155,12 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pt = warp >> 1, half = warp & 1;
-  const int ncubes = a.C1 * a.C2 * a.C3;
+  const int ncubes = a.cube_hi;                      // this launch sweeps cubes [cube_lo, cube_hi)
   // Persistent CTAs (MI_STEN_PERSIST): block b sweeps cubes b, b + grid, ...  The first halo tile of the
   // next cube is loaded by TMA during the current cube's last chunk and the next cube's coefficient
   // fragments are prefetched into L2 during its sweep, so a cube's start-up (fragment loads, first
   // tile) no longer runs with the tensor cores idle.  Without persistence: one cube per block.
-  const int cstep = MI_STEN_PERSIST ? (int)gridDim.x : ncubes;
+  const int cstep = MI_STEN_PERSIST ? (int)gridDim.x : ncubes - a.cube_lo;
 
   for (int e = tid; e < 2 * G::PPB * G::PSTR; e += G::THREADS) Wp[e] = 0.0;
 
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
   const int nchunks = (a.nt + G::TT - 1) / G::TT;
   int gc = 0;                                        // chunks consumed by this block: buffer gc & 1, phase (gc >> 1) & 1
 
-  if (blockIdx.x < ncubes) load_chunk(blockIdx.x, 0, 0);
-  for (int cube = blockIdx.x; cube < ncubes; cube += cstep) {
+  if (a.cube_lo + (int)blockIdx.x < ncubes) load_chunk(a.cube_lo + blockIdx.x, 0, 0);
+  for (int cube = a.cube_lo + blockIdx.x; cube < ncubes; cube += cstep) {
     int o1, o2, o3;
     origin(cube, o1, o2, o3);
     const int next = cube + cstep;

@@ -10,6 +10,8 @@ reaction mass otherwise (assembly.py:287-347).  Each Kronecker term is one
 device "channel" (see csrc/op.cu).
 """
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -247,6 +249,28 @@ class KroneckerOperator:
         """y = A x for contiguous fp64 CUDA tensors of length N (no checks)."""
         self.ctx.bind_stream()
         _lib.call("mi_op_apply", self.ctx.handle, dptr(x), dptr(y))
+
+    def matvec_from_host(self, x_host, nparts=4, out=None):
+        """A x for x in PINNED host memory (a CPU torch tensor): the host-to-device copy streams in
+        ``nparts`` z-plane chunks while the stencil of the chunks already on the device runs
+        (mi_op_apply_from_host).  Returns the device result (``out`` if given)."""
+        if not (isinstance(x_host, torch.Tensor) and x_host.device.type == "cpu"):
+            raise TypeError("matvec_from_host needs a CPU torch tensor (pinned for an asynchronous copy)")
+        n, n_in = self.shape
+        if x_host.numel() != n_in:
+            raise ValueError("dimension mismatch: operator of size %d applied to vector of size %d"
+                             % (n_in, x_host.numel()))
+        xh = x_host.contiguous()
+        if not xh.is_pinned():
+            xh = xh.pin_memory()
+        if getattr(self, "_xdev", None) is None or self._xdev.numel() != n_in:
+            self._xdev = self.ctx.empty(n_in)
+        y = self.ctx.empty(n) if out is None else out
+        self.ctx.bind_stream()
+        _lib.call("mi_op_apply_from_host", self.ctx.handle, ctypes.c_void_p(xh.data_ptr()), dptr(self._xdev),
+                  dptr(y), int(nparts))
+        self._xh_keep = xh           # the copy is asynchronous: keep the host buffer alive until reuse
+        return y
 
     def matvec(self, x):
         n, n_in = self.shape

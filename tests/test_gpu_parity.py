@@ -181,3 +181,19 @@ def test_fused_cgs_passes_are_bitwise_the_two_pass_kernels(k):
     ops.sub_norm(V, k, hb, wb, nb)
     assert torch.equal(wa, wb) and torch.equal(na, nb)
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["case_3d_p3", "case_3d_p2_front", "case_2d_p2"])
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_matvec_from_host_is_bitwise_matvec(name, nparts):
+    """KroneckerOperator.matvec_from_host (H2D in z-plane chunks under the stencil of the chunks already
+    copied, mi_op_apply_from_host) == matvec of the device vector, bit for bit, with and without M_R."""
+    import torch
+    g = load(name)
+    for u, w in ((None, None), (g["u"], g["w"])):
+        _, op, _ = product_objects(g, u=u, w=w)
+        xh = torch.from_numpy(g["x"]).pin_memory()
+        y = op.matvec_from_host(xh, nparts=nparts)
+        ref = op.matvec(xh.cuda())
+        assert torch.equal(y, ref)
+        assert rel(y.cpu().numpy(), g["y_a"] if u is None else g["y_b"]) < 1e-12
