@@ -250,7 +250,7 @@ class KroneckerOperator:
         self.ctx.bind_stream()
         _lib.call("mi_op_apply", self.ctx.handle, dptr(x), dptr(y))
 
-    def matvec_from_host(self, x_host, nparts=4, out=None):
+    def matvec_from_host(self, x_host, nparts=16, out=None):
         """A x for x in PINNED host memory (a CPU torch tensor): the host-to-device copy streams in
         ``nparts`` z-plane chunks while the stencil of the chunks already on the device runs
         (mi_op_apply_from_host).  Returns the device result (``out`` if given)."""
