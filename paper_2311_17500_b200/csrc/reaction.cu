@@ -19,6 +19,7 @@
 #include "dispatch.cuh"
 #include "ptx.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 #ifndef MI_RX_BAL
@@ -517,6 +518,21 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
       return MI_ERR_ARG;                                                         \
   }
 
+}  // namespace mi
+
+#include "reaction_ws.cuh"
+
+namespace mi {
+
+// the warp-specialised kernel serves the fused mode at d = 3, p = p_t = 3 (MI_RX_WS=0: reaction_tile)
+static bool use_reaction_ws(const mi_ctx* c) {
+  static const bool on = [] {
+    const char* e = std::getenv("MI_RX_WS");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on && c->d == 3 && c->p == 3 && c->pt == 3;
+}
+
 // y[t, owned planes] += y_in[t, same planes of the input slab] (z-slab contexts)
 __global__ void add_owned_planes(double* __restrict__ y, const double* __restrict__ yin, long long ns,
                                  long long ns_in, long long off, int nt) {
@@ -651,7 +667,8 @@ int reaction_apply(mi_ctx* c, const double* x, double* y, const double* x0) {
   r.x = x;
   r.lift_x = x0;
   r.y = slab ? c->y_in.p : y;
-  int rc = c->rx_cw_ok ? reaction_launch<RX_STORED>(c, r) : reaction_launch<RX_FUSED>(c, r);
+  int rc = c->rx_cw_ok ? reaction_launch<RX_STORED>(c, r)
+                        : (use_reaction_ws(c) ? reaction_ws_launch(c, r) : reaction_launch<RX_FUSED>(c, r));
   if (rc) return rc;
   if (slab) {
     dim3 g((unsigned)((c->ns + 255) / 256), c->nt);

@@ -1,0 +1,449 @@
+// Warp-specialised fused reaction kernel for d = 3, p = p_t = 3 (BASELINE cfg 4 / cfg 5 shapes):
+// y += M_R x with C_r evaluated on the fly (reference reaction_mass, assembly.py:287-347; the
+// algorithm is reaction_tile's, reaction.cu: time-streamed sum factorisation, q = p+1 Gauss rule).
+//
+// reaction_tile runs every stage on every warp with three block barriers per time slice; its ncu
+// source page (gpurun rx12) puts 53% of the warp time into the x / y stages and their barriers,
+// where almost no FP64 work issues, and the register window caps residency at 16 warps per SM.
+// Here one 384-thread block per SM owns a 2 x 4 x 2 element tile (16 elements, 8 x 16 x 8 spatial
+// Gauss points) and splits into
+//   * 8 CONSUMER warps: z interpolation of the entering slice (DMMA, accumulators = the window in
+//     registers, 4 Gauss points per thread), the per-point time stage (DFMA) and the z projection
+//     of the finished function (DMMA, A fragments by quad shuffles);
+//   * 4 PRODUCER warps: global loads, x and y interpolation of slice j + 1 and the y and x
+//     projections of function j - p_t - 1 (DMMA through shared memory), the reductions into y.
+// The two sides meet only on mbarriers (double-buffered y-interpolation output sB and z-projection
+// output sC), so the consumers never stop at a block barrier; the producers synchronise among
+// themselves on a named barrier.  Colour classes (3 x 2 x 3 = 18 launches) give every y entry one
+// writer per launch, as in reaction_tile: deterministic sums.
+#pragma once
+
+namespace mi {
+
+struct RxWS {
+  static constexpr int P = 3, QE = 4, PW = 4, QT = 4, NF = 3;
+  static constexpr int E1 = 2, E2 = 4, E3 = 2;
+  static constexpr int L1 = E1 + P, L2 = E2 + P, L3 = E3 + P;          // 5, 7, 5 functions
+  static constexpr int Q1 = E1 * QE, Q2 = E2 * QE, Q3 = E3 * QE;       // 8, 16, 8 Gauss points
+  static constexpr int RC1 = (L1 + E1 - 1) / E1, RC2 = (L2 + E2 - 1) / E2, RC3 = (L3 + E3 - 1) / E3;   // 3, 2, 3
+  static constexpr int LS = L1 * L2 * L3, NIN = NF * LS;              // 175, 525
+  static constexpr int NCW = 8, NPW = 4, NCT = 32 * NCW, NPT = 32 * NPW, NTH = NCT + NPT;
+  static constexpr int QL = Q1 * Q2;                                    // 128 (q2, q1) lines of the z stage
+  static constexpr int MT = QL / 8 / NCW;                               // 2 line tiles per consumer warp
+  static constexpr int NPRE = (NIN + NPT - 1) / NPT;                    // 5 input items per producer thread
+  // shared-memory strides (doubles), chosen so every DMMA operand load / accumulator store touches each
+  // bank pair exactly twice: sIn rows 6 (5 functions), sB q2 rows 12, sB planes = 8 mod 16, sC rows = 4
+  // mod 8, sD rows 12
+  static constexpr int IS1 = 6, BS1 = Q1 + 4, BJ = Q2 * BS1 + 8, CS = QL + 4, DS1 = 12;
+  static constexpr int SIN = NF * L3 * L2 * IS1;                        // 630
+  static constexpr int SA = NF * L3 * L2 * Q1;                          // 840
+  static constexpr int SB = NF * L3 * BJ;                               // 3000 (x2 buffers)
+  static constexpr int SC = L3 * CS;                                    // 660  (x2 buffers)
+  static constexpr int SD = L3 * L2 * DS1 + 76;                         // 420 + over-read pad
+  static constexpr int SBT = NCW * 64;                                  // per consumer warp [2][32] time tables
+  static constexpr int NDBL = SIN + SA + 2 * SB + 2 * SC + SD + SBT;
+  static constexpr size_t SMEM = (size_t)NDBL * 8 + 8 * 8;              // + 8 mbarriers
+  static_assert(BJ % 16 == 8 && CS % 8 == 4 && NDBL % 2 == 0, "padding");
+  static_assert(MT * NCW * 8 == QL, "consumer tiling");
+};
+
+__device__ __forceinline__ void rxws_bar_producers() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(RxWS::NPT) : "memory");
+}
+
+__global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
+  using G = RxWS;
+  constexpr int P = G::P, QE = G::QE, PW = G::PW, QT = G::QT, NF = G::NF, PT = G::P;
+  constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2, Q3 = G::Q3;
+  constexpr int BS1 = G::BS1, BJ = G::BJ, CS = G::CS, IS1 = G::IS1, DS1 = G::DS1, MT = G::MT;
+  extern __shared__ __align__(16) double sm[];
+  double* sIn = sm;                 // [fld][j3][j2][IS1]
+  double* sA = sIn + G::SIN;        // x-interpolation out [fld][j3][j2][q1]
+  double* sB = sA + G::SA;          // [2] y-interpolation out [fld][j3] planes of (q2 rows BS1) + q1
+  double* sC = sB + 2 * G::SB;      // [2] z-projection out [j3][CS: (q2, q1)]
+  double* sD = sC + 2 * G::SC;      // y-projection out [j3][j2][DS1]
+  double* sBt = sD + G::SD;         // [warp][2][32] time tables
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sBt + G::SBT);
+  unsigned long long *fullB = bars, *emptyB = bars + 2, *fullC = bars + 4, *emptyC = bars + 6;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  // A-fragment loads run unpredicated over padded rows / k columns: whatever they read is finite (the
+  // buffers start zeroed and only ever hold finite data) and meets a zero B entry or a discarded row
+  for (int i = tid; i < G::NDBL; i += G::NTH) sm[i] = 0.0;
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&fullB[b], G::NPT);
+      mbar_init(&emptyB[b], G::NCT);
+      mbar_init(&fullC[b], G::NCT);
+      mbar_init(&emptyC[b], G::NPT);
+    }
+    mbar_fence_init();
+  }
+  int k[3], ne[3];
+  {
+    constexpr int EL[3] = {G::E1, G::E2, G::E3}, RCL[3] = {G::RC1, G::RC2, G::RC3};
+    int b = blockIdx.x;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const int m = b % r.ncol[l];
+      b /= r.ncol[l];
+      k[l] = (m * RCL[l] + r.color[l]) * EL[l];
+      ne[l] = min(EL[l], r.nel[l] - k[l]);
+    }
+  }
+  // local function j, local Gauss point q of direction l (0 outside the tile / the element's support)
+  auto basis = [&](int l, int j, int q) -> double {
+    const int Ll = l == 1 ? L2 : L1, Ql = l == 1 ? Q2 : Q1;       // L1 = L3, Q1 = Q3
+    const int le = q / QE, gq = q % QE, aa = j - le;
+    if (q >= Ql || j >= Ll || le >= ne[l] || aa < 0 || aa > P) return 0.0;
+    return __ldg(r.B[l] + ((long long)(k[l] + le) * QE + gq) * (P + 1) + aa);
+  };
+  auto wgt = [&](int l, int q) -> double {
+    const int le = q / QE;
+    return le < ne[l] ? __ldg(r.Wq[l] + (long long)(k[l] + le) * QE + q % QE) : 0.0;
+  };
+  const int nelt = r.nel[3];
+  const int nfull = nelt + PT;                       // full-basis time functions
+  __syncthreads();
+
+  if (warp < G::NCW) {
+    // =========================== consumers ===========================
+    double bI[2], bP[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      bI[ks] = basis(2, 4 * ks + fk, fr);
+      bP[ks] = basis(2, fr, 4 * ks + fk);
+    }
+    // the thread's Gauss points: line tile t = warp + 8 mi (q2 = t, q1 = fr), q3 = 2 fk + e.  The spatial
+    // weight is folded into the x field and c2 into the w field as the slice enters the window.
+    double wsp[MT][2];
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int q2 = warp + G::NCW * mi, q3 = 2 * fk + e;
+        double v = wgt(2, q3) * wgt(0, fr) * wgt(1, q2);
+        if (r.jw != nullptr && v != 0.0) {
+          const long long G1 = (long long)r.nel[0] * QE, G2 = (long long)r.nel[1] * QE;
+          v *= __ldg(r.jw + ((long long)(k[2] * QE + q3) * G2 + k[1] * QE + q2) * G1 + k[0] * QE + fr);
+        }
+        wsp[mi][e] = v;
+      }
+    const double rc1 = r.c1, rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;
+    double X[MT][PW][NF][2], Y[MT][PW][2];
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+      for (int a = 0; a < PW; ++a) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) X[mi][a][f][0] = X[mi][a][f][1] = 0.0;
+        Y[mi][a][0] = Y[mi][a][1] = 0.0;
+      }
+    double* myBt = sBt + warp * 64;
+    double btp = 0.0;
+    auto prefetch_bt = [&](int et) {
+      if (et >= 0 && et < nelt) {
+        const int ga = lane & 15;
+        const double bv = __ldg(r.B[3] + (long long)et * QT * PW + ga);
+        btp = lane < 16 ? bv : bv * __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
+      }
+    };
+    for (int j = 0; j < nfull + PT; ++j) {
+      const int et = j - PT;                         // time element; the function completed by it
+      myBt[(j & 1) * 32 + lane] = btp;
+      __syncwarp();
+      prefetch_bt(et + 1);
+      if (j < nfull) {
+        // z interpolation of slice j -> window slot PT
+        const int bb = j & 1;
+        mbar_wait(&fullB[bb], (unsigned)((j >> 1) & 1));
+        const double* fin = sB + bb * G::SB + fk * BJ + fr;
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          const int q2 = warp + G::NCW * mi;
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, fin[(f * L3 + 4 * ks) * BJ + q2 * BS1], bI[ks]);
+            X[mi][PT][f][0] = c0 * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]));
+            X[mi][PT][f][1] = c1 * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]));
+          }
+        }
+        mbar_arrive(&emptyB[bb]);
+      }
+      if (et >= 0) {
+        // time element et on the thread's own points (window slots a = functions et + a)
+        if (et < nelt) {
+          const double* bt = myBt + (j & 1) * 32;
+#pragma unroll
+          for (int g = 0; g < QT; ++g) {
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                double uu = 0.0, ww = 0.0, xx = 0.0;
+#pragma unroll
+                for (int a = 0; a < PW; ++a) {
+                  const double ba = bt[g * PW + a];
+                  uu = fma(ba, X[mi][a][0][e], uu);
+                  ww = fma(ba, X[mi][a][1][e], ww);
+                  xx = fma(ba, X[mi][a][2][e], xx);
+                }
+                // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
+                const double v = fma(uu, fma(rc1, uu, rk1), ww + rk0) * xx;
+#pragma unroll
+                for (int a = 0; a < PW; ++a) Y[mi][a][e] = fma(bt[QT * PW + g * PW + a], v, Y[mi][a][e]);
+              }
+          }
+        }
+        // z projection of the completed function et (slot 0): A fragments by quad shuffles
+        double c[MT][2];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          c[mi][0] = c[mi][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int cc = 4 * ks + fk, src = (lane & ~3) | (cc >> 1);
+            const double v0 = __shfl_sync(0xffffffffu, Y[mi][0][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, Y[mi][0][1], src);
+            dmma(c[mi][0], c[mi][1], (cc & 1) ? v1 : v0, bP[ks]);
+          }
+          Y[mi][0][0] = Y[mi][0][1] = 0.0;
+        }
+        const int cb = et & 1;
+        if (et >= 2) mbar_wait(&emptyC[cb], (unsigned)(((et >> 1) - 1) & 1));
+        double* out = sC + cb * G::SC;
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          const int line = 8 * (warp + G::NCW * mi) + fr, n0 = 2 * fk;
+          if (n0 < L3) out[n0 * CS + line] = c[mi][0];
+          if (n0 + 1 < L3) out[(n0 + 1) * CS + line] = c[mi][1];
+        }
+        mbar_arrive(&fullC[cb]);
+      }
+      // rotate both windows: slot a <- slot a + 1, the projected (zeroed) slot becomes the entering one
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) {
+        double xs[NF][2], ys[2];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) xs[f][0] = X[mi][0][f][0], xs[f][1] = X[mi][0][f][1];
+        ys[0] = Y[mi][0][0], ys[1] = Y[mi][0][1];
+#pragma unroll
+        for (int a = 0; a < PW - 1; ++a) {
+#pragma unroll
+          for (int f = 0; f < NF; ++f) X[mi][a][f][0] = X[mi][a + 1][f][0], X[mi][a][f][1] = X[mi][a + 1][f][1];
+          Y[mi][a][0] = Y[mi][a + 1][0], Y[mi][a][1] = Y[mi][a + 1][1];
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) X[mi][PW - 1][f][0] = xs[f][0], X[mi][PW - 1][f][1] = xs[f][1];
+        Y[mi][PW - 1][0] = ys[0], Y[mi][PW - 1][1] = ys[1];
+      }
+    }
+  } else {
+    // =========================== producers ===========================
+    const int p = tid - G::NCT, pw = warp - G::NCW;
+    double bIx[2], bIy[2][2], bPy[4], bPx[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      bIx[ks] = basis(0, 4 * ks + fk, fr);
+      bPx[ks] = basis(0, fr, 4 * ks + fk);
+#pragma unroll
+      for (int n2 = 0; n2 < 2; ++n2) bIy[n2][ks] = basis(1, 4 * ks + fk, 8 * n2 + fr);
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) bPy[ks] = basis(1, fr, 4 * ks + fk);
+    const long long ns = r.ns;
+    auto spatial = [&](int j3, int j2, int j1, bool& ok) -> long long {
+      const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
+      ok = g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
+      return ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+    };
+    // input slice items of this thread: (fld, j3, j2, j1) -> global spatial index (-1: padding)
+    long long gsp[G::NPRE];
+    int sidx[G::NPRE];
+#pragma unroll
+    for (int m = 0; m < G::NPRE; ++m) {
+      const int i = p + G::NPT * m;
+      const int f = i / G::LS, s = i % G::LS;
+      const int j3 = s / (L1 * L2), j2 = (s / L1) % L2, j1 = s % L1;
+      bool ok;
+      const long long gs = spatial(j3, j2, j1, ok);
+      gsp[m] = (i < G::NIN && ok) ? gs : -1;
+      sidx[m] = i < G::NIN ? ((f * L3 + j3) * L2 + j2) * IS1 + j1 : -1;
+    }
+    double pre[G::NPRE];
+    auto prefetch = [&](int ft) {
+      const int ct = ft + r.rowoff;
+      const bool vt = ct >= 0 && ct < r.ntc;
+#pragma unroll
+      for (int m = 0; m < G::NPRE; ++m) {
+        const int f = (p + G::NPT * m) / G::LS;
+        const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
+        const double* lift = f == 0 ? r.lift_u : (f == 1 ? nullptr : r.lift_x);
+        double v = 0.0;
+        if (gsp[m] >= 0) {
+          if (vt) v = __ldg(src + (long long)ct * ns + gsp[m]);
+          else if (ct == -1 && lift != nullptr) v = __ldg(lift + gsp[m]);
+        }
+        pre[m] = v;
+      }
+    };
+    // x-projection outputs of this thread: line tiles mt = pw + 4 u, xline = 8 mt + fr = (j3, j2), j1 = 2 fk + e
+    long long yidx[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int xline = 8 * (pw + G::NPW * u) + fr, j1 = 2 * fk + e;
+        bool ok = false;
+        long long gs = 0;
+        if (xline < L3 * L2 && j1 < L1) gs = spatial(xline / L2, xline % L2, j1, ok);
+        yidx[u][e] = ok ? gs : -1;
+      }
+    prefetch(0);
+    for (int i = 0; i <= nfull + PT; ++i) {
+      const bool has_in = i < nfull;
+      const int fq = i - PT - 1;                     // function whose y / x projections run now
+      const bool has_fq = fq >= 0 && fq < nfull;
+      if (has_in) {
+#pragma unroll
+        for (int m = 0; m < G::NPRE; ++m)
+          if (sidx[m] >= 0) sIn[sidx[m]] = pre[m];
+      }
+      rxws_bar_producers();
+      if (i + 1 < nfull) prefetch(i + 1);
+      if (has_in) {
+        // x interpolation of slice i: lines (fld, j3, j2), K = j1, N = q1 -> sA
+        constexpr int NL = NF * L3 * L2, NMT = (NL + 7) / 8;    // 105 lines, 14 tiles
+        double c[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          c[u][0] = c[u][1] = 0.0;
+          const int mt = pw + G::NPW * u;
+          if (mt < NMT) {
+            const int line = mt * 8 + fr;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) dmma(c[u][0], c[u][1], sIn[line * IS1 + 4 * ks + fk], bIx[ks]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int line = (pw + G::NPW * u) * 8 + fr;
+          if (line < NL) *reinterpret_cast<double2*>(sA + line * Q1 + 2 * fk) = make_double2(c[u][0], c[u][1]);
+        }
+      }
+      rxws_bar_producers();
+      if (has_in) {
+        // y interpolation of slice i: lines (fld j3, q1), K = j2, N = q2 (two N tiles) -> sB[i & 1]
+        const int bb = i & 1;
+        constexpr int NMT = NF * L3;                 // 15 line tiles (one (fld, j3) plane each)
+        double c[4][2][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int n2 = 0; n2 < 2; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
+          const int mt = pw + G::NPW * u;
+          if (mt < NMT) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const double av = sA[(mt * L2 + 4 * ks + fk) * Q1 + fr];
+#pragma unroll
+              for (int n2 = 0; n2 < 2; ++n2) dmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
+            }
+          }
+        }
+        if (i >= 2) mbar_wait(&emptyB[bb], (unsigned)(((i >> 1) - 1) & 1));
+        double* out = sB + bb * G::SB;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int mt = pw + G::NPW * u;
+          if (mt < NMT) {
+#pragma unroll
+            for (int n2 = 0; n2 < 2; ++n2) {
+              const int n0 = 8 * n2 + 2 * fk;
+              out[mt * BJ + n0 * BS1 + fr] = c[u][n2][0];
+              out[mt * BJ + (n0 + 1) * BS1 + fr] = c[u][n2][1];
+            }
+          }
+        }
+        mbar_arrive(&fullB[bb]);
+      }
+      if (has_fq) {
+        // y projection of function fq: lines (j3, q1), K = q2, N = j2: sC[fq & 1] -> sD
+        const int cb = fq & 1;
+        mbar_wait(&fullC[cb], (unsigned)((fq >> 1) & 1));
+        const double* in = sC + cb * G::SC;
+        double c[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          c[u][0] = c[u][1] = 0.0;
+          const int mt = pw + G::NPW * u;            // = j3
+          if (mt < L3) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) dmma(c[u][0], c[u][1], in[mt * CS + (4 * ks + fk) * Q1 + fr], bPy[ks]);
+          }
+        }
+        mbar_arrive(&emptyC[cb]);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int mt = pw + G::NPW * u, n0 = 2 * fk;
+          if (mt < L3) {
+            if (n0 < L2) sD[(mt * L2 + n0) * DS1 + fr] = c[u][0];
+            if (n0 + 1 < L2) sD[(mt * L2 + n0 + 1) * DS1 + fr] = c[u][1];
+          }
+        }
+      }
+      rxws_bar_producers();
+      if (has_fq) {
+        // x projection of function fq: lines (j3, j2), K = q1, N = j1 -> y (fire-and-forget reductions:
+        // one writer per y entry per colour launch, stream-ordered launches: deterministic)
+        const int ct = fq + r.rowoff;
+        const long long row = (ct >= 0 && ct < r.ntc) ? (long long)ct * ns : -1;
+        constexpr int NMT = (L3 * L2 + 7) / 8;       // 35 lines, 5 tiles
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int mt = pw + G::NPW * u;
+          if (mt < NMT) {
+            const int xline = 8 * mt + fr;
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, sD[xline * DS1 + 4 * ks + fk], bPx[ks]);
+            if (row >= 0) {
+              if (yidx[u][0] >= 0) atomicAdd(r.y + row + yidx[u][0], c0);
+              if (yidx[u][1] >= 0) atomicAdd(r.y + row + yidx[u][1], c1);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// all colour classes of the warp-specialised kernel (d = 3, p = p_t = 3, fused mode)
+static int reaction_ws_launch(mi_ctx* c, RxArgs r) {
+  using G = RxWS;
+  MI_DEV_FLAG(attr);
+  if (!attr) {
+    MI_CUDA(cudaFuncSetAttribute(reaction_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    attr = true;
+  }
+  const int EL[3] = {G::E1, G::E2, G::E3}, RCL[3] = {G::RC1, G::RC2, G::RC3};
+  for (int col = 0; col < G::RC1 * G::RC2 * G::RC3; ++col) {
+    int cc = col;
+    long long nb = 1;
+    for (int l = 0; l < 3; ++l) {
+      r.color[l] = cc % RCL[l];
+      cc /= RCL[l];
+      const int ntile = (c->rx_nel[l] + EL[l] - 1) / EL[l];
+      r.ncol[l] = (ntile - r.color[l] + RCL[l] - 1) / RCL[l];
+      nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
+    }
+    if (nb == 0) continue;
+    reaction_ws<<<(unsigned)nb, G::NTH, G::SMEM, c->stream>>>(r);
+    MI_CHECK_LAUNCH("reaction_ws");
+  }
+  return MI_OK;
+}
+
+}  // namespace mi
