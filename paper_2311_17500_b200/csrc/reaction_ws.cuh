@@ -41,11 +41,25 @@ struct RxWS {
   static constexpr int SC = L3 * CS;                                    // 660  (x2 buffers)
   static constexpr int SD = L3 * L2 * DS1 + 76;                         // 420 + over-read pad
   static constexpr int SBT = NCW * 64;                                  // per consumer warp [2][32] time tables
-  static constexpr int NDBL = SIN + SA + 2 * SB + 2 * SC + SD + SBT;
+  static constexpr int NDBL = 2 * SIN + SA + 2 * SB + 2 * SC + SD + SBT;
   static constexpr size_t SMEM = (size_t)NDBL * 8 + 8 * 8;              // + 8 mbarriers
   static_assert(BJ % 16 == 8 && CS % 8 == 4 && NDBL % 2 == 0, "padding");
   static_assert(MT * NCW * 8 == QL, "consumer tiling");
 };
+
+#ifndef MI_RXWS_REGC
+#define MI_RXWS_REGC 208   // consumer registers after the split (256 x REGC + 128 x REGP <= 384 x 168)
+#endif
+#ifndef MI_RXWS_REGP
+#define MI_RXWS_REGP 88
+#endif
+#ifndef MI_RXWS_UNROLL
+#define MI_RXWS_UNROLL 1   // consumer slice loop unrolled by p_t + 1 (compile-time window slots, no rotation copies)
+#endif
+template <int N>
+__device__ __forceinline__ void rxws_reg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void rxws_reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void rxws_bar_producers() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(RxWS::NPT) : "memory");
@@ -57,8 +71,8 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2, Q3 = G::Q3;
   constexpr int BS1 = G::BS1, BJ = G::BJ, CS = G::CS, IS1 = G::IS1, DS1 = G::DS1, MT = G::MT;
   extern __shared__ __align__(16) double sm[];
-  double* sIn = sm;                 // [fld][j3][j2][IS1]
-  double* sA = sIn + G::SIN;        // x-interpolation out [fld][j3][j2][q1]
+  double* sIn = sm;                 // [2][fld][j3][j2][IS1]
+  double* sA = sIn + 2 * G::SIN;    // x-interpolation out [fld][j3][j2][q1]
   double* sB = sA + G::SA;          // [2] y-interpolation out [fld][j3] planes of (q2 rows BS1) + q1
   double* sC = sB + 2 * G::SB;      // [2] z-projection out [j3][CS: (q2, q1)]
   double* sD = sC + 2 * G::SC;      // y-projection out [j3][j2][DS1]
@@ -108,6 +122,7 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
 
   if (warp < G::NCW) {
     // =========================== consumers ===========================
+    rxws_reg_inc<MI_RXWS_REGC>();                    // the producers' released registers: window + ILP-4 time stage
     double bI[2], bP[2];
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
@@ -140,89 +155,129 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         Y[mi][a][0] = Y[mi][a][1] = 0.0;
       }
     double* myBt = sBt + warp * 64;
-    double btp = 0.0;
+    // time tables of element et: lanes 0-15 the basis values (interpolation), lanes 16-31 the same
+    // times the Gauss weight (projection).  The loads are consumed one step later (no stall on them).
+    double btb = 0.0, btw = 1.0;
     auto prefetch_bt = [&](int et) {
       if (et >= 0 && et < nelt) {
         const int ga = lane & 15;
-        const double bv = __ldg(r.B[3] + (long long)et * QT * PW + ga);
-        btp = lane < 16 ? bv : bv * __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
+        btb = __ldg(r.B[3] + (long long)et * QT * PW + ga);
+        if (lane >= 16) btw = __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
       }
     };
-    for (int j = 0; j < nfull + PT; ++j) {
+    // One slice step with compile-time window slots: the entering slice j goes to slot PH, function
+    // et + a sits in slot (S0 + a) % PW with S0 = (PH + 1) % PW.
+    auto step = [&](auto phc, int j) {
+      constexpr int PH = decltype(phc)::value, S0 = (PH + 1) % PW;
       const int et = j - PT;                         // time element; the function completed by it
-      myBt[(j & 1) * 32 + lane] = btp;
+      myBt[(j & 1) * 32 + lane] = btb * btw;
       __syncwarp();
       prefetch_bt(et + 1);
       if (j < nfull) {
-        // z interpolation of slice j -> window slot PT
+        // z interpolation of slice j -> window slot PH
         const int bb = j & 1;
         mbar_wait(&fullB[bb], (unsigned)((j >> 1) & 1));
         const double* fin = sB + bb * G::SB + fk * BJ + fr;
+        double c[MT][NF][2];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi) {
-          const int q2 = warp + G::NCW * mi;
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+          for (int f = 0; f < NF; ++f) c[mi][f][0] = c[mi][f][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+              dmma(c[mi][f][0], c[mi][f][1], fin[(f * L3 + 4 * ks) * BJ + (warp + G::NCW * mi) * BS1], bI[ks]);
+        mbar_arrive(&emptyB[bb]);
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, fin[(f * L3 + 4 * ks) * BJ + q2 * BS1], bI[ks]);
-            X[mi][PT][f][0] = c0 * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]));
-            X[mi][PT][f][1] = c1 * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]));
+            X[mi][PH][f][0] = c[mi][f][0] * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]));
+            X[mi][PH][f][1] = c[mi][f][1] * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]));
           }
-        }
-        mbar_arrive(&emptyB[bb]);
       }
-      if (et >= 0) {
-        // time element et on the thread's own points (window slots a = functions et + a)
-        if (et < nelt) {
-          const double* bt = myBt + (j & 1) * 32;
+      if (et < 0) return;
+      // time element et on the thread's own four points, all chains interleaved
+      if (et < nelt) {
+        const double* bt = myBt + (j & 1) * 32;
 #pragma unroll
-          for (int g = 0; g < QT; ++g) {
+        for (int g = 0; g < QT; ++g) {
+          double uu[MT][2], ww[MT][2], xx[MT][2];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) uu[mi][e] = ww[mi][e] = xx[mi][e] = 0.0;
+#pragma unroll
+          for (int a = 0; a < PW; ++a) {
+            const double ba = bt[g * PW + a];
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                double uu = 0.0, ww = 0.0, xx = 0.0;
-#pragma unroll
-                for (int a = 0; a < PW; ++a) {
-                  const double ba = bt[g * PW + a];
-                  uu = fma(ba, X[mi][a][0][e], uu);
-                  ww = fma(ba, X[mi][a][1][e], ww);
-                  xx = fma(ba, X[mi][a][2][e], xx);
-                }
-                // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
-                const double v = fma(uu, fma(rc1, uu, rk1), ww + rk0) * xx;
-#pragma unroll
-                for (int a = 0; a < PW; ++a) Y[mi][a][e] = fma(bt[QT * PW + g * PW + a], v, Y[mi][a][e]);
+                uu[mi][e] = fma(ba, X[mi][(S0 + a) % PW][0][e], uu[mi][e]);
+                ww[mi][e] = fma(ba, X[mi][(S0 + a) % PW][1][e], ww[mi][e]);
+                xx[mi][e] = fma(ba, X[mi][(S0 + a) % PW][2][e], xx[mi][e]);
               }
           }
-        }
-        // z projection of the completed function et (slot 0): A fragments by quad shuffles
-        double c[MT][2];
+          // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
+          double v[MT][2];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi) {
-          c[mi][0] = c[mi][1] = 0.0;
+          for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const int cc = 4 * ks + fk, src = (lane & ~3) | (cc >> 1);
-            const double v0 = __shfl_sync(0xffffffffu, Y[mi][0][0], src);
-            const double v1 = __shfl_sync(0xffffffffu, Y[mi][0][1], src);
-            dmma(c[mi][0], c[mi][1], (cc & 1) ? v1 : v0, bP[ks]);
+            for (int e = 0; e < 2; ++e)
+              v[mi][e] = fma(uu[mi][e], fma(rc1, uu[mi][e], rk1), ww[mi][e] + rk0) * xx[mi][e];
+#pragma unroll
+          for (int a = 0; a < PW; ++a) {
+            const double bw = bt[QT * PW + g * PW + a];
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) Y[mi][(S0 + a) % PW][e] = fma(bw, v[mi][e], Y[mi][(S0 + a) % PW][e]);
           }
-          Y[mi][0][0] = Y[mi][0][1] = 0.0;
         }
-        const int cb = et & 1;
-        if (et >= 2) mbar_wait(&emptyC[cb], (unsigned)(((et >> 1) - 1) & 1));
-        double* out = sC + cb * G::SC;
+      }
+      // z projection of the completed function et (slot S0): A fragments by quad shuffles
+      double c[MT][2];
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) c[mi][0] = c[mi][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi) {
-          const int line = 8 * (warp + G::NCW * mi) + fr, n0 = 2 * fk;
-          if (n0 < L3) out[n0 * CS + line] = c[mi][0];
-          if (n0 + 1 < L3) out[(n0 + 1) * CS + line] = c[mi][1];
+          const int cc = 4 * ks + fk, src = (lane & ~3) | (cc >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, Y[mi][S0][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, Y[mi][S0][1], src);
+          dmma(c[mi][0], c[mi][1], (cc & 1) ? v1 : v0, bP[ks]);
         }
-        mbar_arrive(&fullC[cb]);
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) Y[mi][S0][0] = Y[mi][S0][1] = 0.0;
+      const int cb = et & 1;
+      if (et >= 2) mbar_wait(&emptyC[cb], (unsigned)(((et >> 1) - 1) & 1));
+      double* out = sC + cb * G::SC;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) {
+        const int line = 8 * (warp + G::NCW * mi) + fr, n0 = 2 * fk;
+        if (n0 < L3) out[n0 * CS + line] = c[mi][0];
+        if (n0 + 1 < L3) out[(n0 + 1) * CS + line] = c[mi][1];
       }
-      // rotate both windows: slot a <- slot a + 1, the projected (zeroed) slot becomes the entering one
+      mbar_arrive(&fullC[cb]);
+    };
+    const int nsteps = nfull + PT;
+#if MI_RXWS_UNROLL
+    for (int j0 = 0; j0 < nsteps; j0 += PW) {
+      step(std::integral_constant<int, 0>{}, j0);
+      if (j0 + 1 < nsteps) step(std::integral_constant<int, 1>{}, j0 + 1);
+      if (j0 + 2 < nsteps) step(std::integral_constant<int, 2>{}, j0 + 2);
+      if (j0 + 3 < nsteps) step(std::integral_constant<int, 3>{}, j0 + 3);
+    }
+#else
+    // one copy of the step with fixed slots (entering slice -> slot PT, function et -> slot 0) and a
+    // cyclic rotation of both windows after it
+    for (int j = 0; j < nsteps; ++j) {
+      step(std::integral_constant<int, PT>{}, j);
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi) {
         double xs[NF][2], ys[2];
@@ -240,8 +295,10 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         Y[mi][PW - 1][0] = ys[0], Y[mi][PW - 1][1] = ys[1];
       }
     }
+#endif
   } else {
     // =========================== producers ===========================
+    rxws_reg_dec<MI_RXWS_REGP>();
     const int p = tid - G::NCT, pw = warp - G::NCW;
     double bIx[2], bIy[2][2], bPy[4], bPx[2];
 #pragma unroll
@@ -254,66 +311,78 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) bPy[ks] = basis(1, fr, 4 * ks + fk);
     const long long ns = r.ns;
-    auto spatial = [&](int j3, int j2, int j1, bool& ok) -> long long {
+    // spatial indices fit in 32 bits (the launcher checks N_s < 2^31)
+    auto spatial = [&](int j3, int j2, int j1, bool& ok) -> int {
       const int g1 = k[0] + j1, g2 = k[1] + j2, g3 = k[2] + j3;
       ok = g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
-      return ((long long)g3 * r.n[1] + g2) * r.n[0] + g1;
+      return (g3 * r.n[1] + g2) * r.n[0] + g1;
     };
     // input slice items of this thread: (fld, j3, j2, j1) -> global spatial index (-1: padding)
-    long long gsp[G::NPRE];
-    int sidx[G::NPRE];
+    int gsp[G::NPRE], sidx[G::NPRE];
 #pragma unroll
     for (int m = 0; m < G::NPRE; ++m) {
       const int i = p + G::NPT * m;
       const int f = i / G::LS, s = i % G::LS;
       const int j3 = s / (L1 * L2), j2 = (s / L1) % L2, j1 = s % L1;
       bool ok;
-      const long long gs = spatial(j3, j2, j1, ok);
+      const int gs = spatial(j3, j2, j1, ok);
       gsp[m] = (i < G::NIN && ok) ? gs : -1;
       sidx[m] = i < G::NIN ? ((f * L3 + j3) * L2 + j2) * IS1 + j1 : -1;
     }
-    double pre[G::NPRE];
-    auto prefetch = [&](int ft) {
+    // field of every item (2 bits each); the slice is copied asynchronously (cp.async, zero fill for
+    // padding / constrained rows) straight into the double-buffered sIn: no register staging, and no
+    // global-load scoreboard in front of the x-interpolation DMMAs
+    int fcode = 0;
+#pragma unroll
+    for (int m = 0; m < G::NPRE; ++m) fcode |= ((p + G::NPT * m) / G::LS) << (2 * m);
+    auto issue = [&](int ft) {
       const int ct = ft + r.rowoff;
       const bool vt = ct >= 0 && ct < r.ntc;
+      double* dst = sIn + (ft & 1) * G::SIN;
 #pragma unroll
       for (int m = 0; m < G::NPRE; ++m) {
-        const int f = (p + G::NPT * m) / G::LS;
-        const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
-        const double* lift = f == 0 ? r.lift_u : (f == 1 ? nullptr : r.lift_x);
-        double v = 0.0;
-        if (gsp[m] >= 0) {
-          if (vt) v = __ldg(src + (long long)ct * ns + gsp[m]);
-          else if (ct == -1 && lift != nullptr) v = __ldg(lift + gsp[m]);
+        if (sidx[m] >= 0) {
+          const int f = (fcode >> (2 * m)) & 3;
+          const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
+          const double* lift = f == 0 ? r.lift_u : (f == 1 ? nullptr : r.lift_x);
+          const double* sp = r.u;
+          bool valid = false;
+          if (gsp[m] >= 0) {
+            if (vt) {
+              sp = src + (long long)ct * ns + gsp[m];
+              valid = true;
+            } else if (ct == -1 && lift != nullptr) {
+              sp = lift + gsp[m];
+              valid = true;
+            }
+          }
+          cp_async8(dst + sidx[m], sp, valid);
         }
-        pre[m] = v;
       }
+      cp_async_commit();
     };
     // x-projection outputs of this thread: line tiles mt = pw + 4 u, xline = 8 mt + fr = (j3, j2), j1 = 2 fk + e
-    long long yidx[2][2];
+    int yidx[2][2];
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int xline = 8 * (pw + G::NPW * u) + fr, j1 = 2 * fk + e;
         bool ok = false;
-        long long gs = 0;
+        int gs = 0;
         if (xline < L3 * L2 && j1 < L1) gs = spatial(xline / L2, xline % L2, j1, ok);
         yidx[u][e] = ok ? gs : -1;
       }
-    prefetch(0);
+    issue(0);
     for (int i = 0; i <= nfull + PT; ++i) {
       const bool has_in = i < nfull;
       const int fq = i - PT - 1;                     // function whose y / x projections run now
       const bool has_fq = fq >= 0 && fq < nfull;
+      cp_async_wait<0>();                            // this thread's copies of slice i have landed ...
+      rxws_bar_producers();                          // ... and everyone's; the other sIn buffer is free
+      if (i + 1 < nfull) issue(i + 1);
       if (has_in) {
-#pragma unroll
-        for (int m = 0; m < G::NPRE; ++m)
-          if (sidx[m] >= 0) sIn[sidx[m]] = pre[m];
-      }
-      rxws_bar_producers();
-      if (i + 1 < nfull) prefetch(i + 1);
-      if (has_in) {
+        const double* sI = sIn + (i & 1) * G::SIN;
         // x interpolation of slice i: lines (fld, j3, j2), K = j1, N = q1 -> sA
         constexpr int NL = NF * L3 * L2, NMT = (NL + 7) / 8;    // 105 lines, 14 tiles
         double c[4][2];
@@ -324,7 +393,7 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
           if (mt < NMT) {
             const int line = mt * 8 + fr;
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) dmma(c[u][0], c[u][1], sIn[line * IS1 + 4 * ks + fk], bIx[ks]);
+            for (int ks = 0; ks < 2; ++ks) dmma(c[u][0], c[u][1], sI[line * IS1 + 4 * ks + fk], bIx[ks]);
           }
         }
 #pragma unroll
@@ -338,32 +407,35 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         // y interpolation of slice i: lines (fld j3, q1), K = j2, N = q2 (two N tiles) -> sB[i & 1]
         const int bb = i & 1;
         constexpr int NMT = NF * L3;                 // 15 line tiles (one (fld, j3) plane each)
-        double c[4][2][2];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-          for (int n2 = 0; n2 < 2; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
-          const int mt = pw + G::NPW * u;
-          if (mt < NMT) {
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const double av = sA[(mt * L2 + 4 * ks + fk) * Q1 + fr];
-#pragma unroll
-              for (int n2 = 0; n2 < 2; ++n2) dmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
-            }
-          }
-        }
-        if (i >= 2) mbar_wait(&emptyB[bb], (unsigned)(((i >> 1) - 1) & 1));
         double* out = sB + bb * G::SB;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int mt = pw + G::NPW * u;
-          if (mt < NMT) {
+        for (int h = 0; h < 2; ++h) {               // two line tiles at a time (register budget)
+          double c[2][2][2];
 #pragma unroll
-            for (int n2 = 0; n2 < 2; ++n2) {
-              const int n0 = 8 * n2 + 2 * fk;
-              out[mt * BJ + n0 * BS1 + fr] = c[u][n2][0];
-              out[mt * BJ + (n0 + 1) * BS1 + fr] = c[u][n2][1];
+          for (int u = 0; u < 2; ++u) {
+#pragma unroll
+            for (int n2 = 0; n2 < 2; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
+            const int mt = pw + G::NPW * (2 * h + u);
+            if (mt < NMT) {
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) {
+                const double av = sA[(mt * L2 + 4 * ks + fk) * Q1 + fr];
+#pragma unroll
+                for (int n2 = 0; n2 < 2; ++n2) dmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
+              }
+            }
+          }
+          if (h == 0 && i >= 2) mbar_wait(&emptyB[bb], (unsigned)(((i >> 1) - 1) & 1));
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int mt = pw + G::NPW * (2 * h + u);
+            if (mt < NMT) {
+#pragma unroll
+              for (int n2 = 0; n2 < 2; ++n2) {
+                const int n0 = 8 * n2 + 2 * fk;
+                out[mt * BJ + n0 * BS1 + fr] = c[u][n2][0];
+                out[mt * BJ + (n0 + 1) * BS1 + fr] = c[u][n2][1];
+              }
             }
           }
         }
