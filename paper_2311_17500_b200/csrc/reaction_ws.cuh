@@ -30,7 +30,6 @@ struct RxWS {
   static constexpr int NCW = 8, NPW = 4, NCT = 32 * NCW, NPT = 32 * NPW, NTH = NCT + NPT;
   static constexpr int QL = Q1 * Q2;                                    // 128 (q2, q1) lines of the z stage
   static constexpr int MT = QL / 8 / NCW;                               // 2 line tiles per consumer warp
-  static constexpr int NPRE = (NIN + NPT - 1) / NPT;                    // 5 input items per producer thread
   // shared-memory strides (doubles), chosen so every DMMA operand load / accumulator store touches each
   // bank pair exactly twice: sIn rows 6 (5 functions), sB q2 rows 12, sB planes = 8 mod 16, sC rows = 4
   // mod 8, sD rows 12
@@ -317,46 +316,59 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
       ok = g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
       return (g3 * r.n[1] + g2) * r.n[0] + g1;
     };
-    // input slice items of this thread: (fld, j3, j2, j1) -> global spatial index (-1: padding)
-    int gsp[G::NPRE], sidx[G::NPRE];
+    // Input slice items of this thread: spatial positions s = p + 128 h (h = 0, 1; s < LS) of all three
+    // fields.  The slice is copied asynchronously (cp.async, zero fill for padding / constrained rows)
+    // straight into the double-buffered sIn: no register staging, and no global-load scoreboard in
+    // front of the x-interpolation DMMAs.
+    int gsp[2];                                      // global spatial index (-1: outside the domain, -2: no item)
+    unsigned sdst[2];                                // shared address of the field-0 copy in buffer 0
 #pragma unroll
-    for (int m = 0; m < G::NPRE; ++m) {
-      const int i = p + G::NPT * m;
-      const int f = i / G::LS, s = i % G::LS;
-      const int j3 = s / (L1 * L2), j2 = (s / L1) % L2, j1 = s % L1;
+    for (int h = 0; h < 2; ++h) {
+      const int sp = p + G::NPT * h;
+      const int j3 = sp / (L1 * L2), j2 = (sp / L1) % L2, j1 = sp % L1;
       bool ok;
       const int gs = spatial(j3, j2, j1, ok);
-      gsp[m] = (i < G::NIN && ok) ? gs : -1;
-      sidx[m] = i < G::NIN ? ((f * L3 + j3) * L2 + j2) * IS1 + j1 : -1;
+      gsp[h] = sp < G::LS ? (ok ? gs : -1) : -2;
+      sdst[h] = (unsigned)__cvta_generic_to_shared(sIn + (sp < G::LS ? (j3 * L2 + j2) * IS1 + j1 : 0));
     }
-    // field of every item (2 bits each); the slice is copied asynchronously (cp.async, zero fill for
-    // padding / constrained rows) straight into the double-buffered sIn: no register staging, and no
-    // global-load scoreboard in front of the x-interpolation DMMAs
-    int fcode = 0;
-#pragma unroll
-    for (int m = 0; m < G::NPRE; ++m) fcode |= ((p + G::NPT * m) / G::LS) << (2 * m);
+    auto put = [&](unsigned dst, const double* src, bool valid) {   // one double: async copy, or a zero
+      if (valid)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+      else
+        asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0) : "memory");
+    };
     auto issue = [&](int ft) {
       const int ct = ft + r.rowoff;
-      const bool vt = ct >= 0 && ct < r.ntc;
-      double* dst = sIn + (ft & 1) * G::SIN;
+      const unsigned boff = (unsigned)((ft & 1) * G::SIN * 8);
+      constexpr unsigned FO = L3 * L2 * IS1 * 8;     // field stride in sIn (bytes)
+      if (ct >= 0 && ct < r.ntc) {
+        const long long off = (long long)ct * ns;
+        const double *ru = r.u + off, *rw = r.w + off, *rx = r.x + off;
 #pragma unroll
-      for (int m = 0; m < G::NPRE; ++m) {
-        if (sidx[m] >= 0) {
-          const int f = (fcode >> (2 * m)) & 3;
-          const double* src = f == 0 ? r.u : (f == 1 ? r.w : r.x);
-          const double* lift = f == 0 ? r.lift_u : (f == 1 ? nullptr : r.lift_x);
-          const double* sp = r.u;
-          bool valid = false;
-          if (gsp[m] >= 0) {
-            if (vt) {
-              sp = src + (long long)ct * ns + gsp[m];
-              valid = true;
-            } else if (ct == -1 && lift != nullptr) {
-              sp = lift + gsp[m];
-              valid = true;
-            }
+        for (int h = 0; h < 2; ++h) {
+          if (gsp[h] != -2) {
+            const bool v = gsp[h] >= 0;
+            const int g = v ? gsp[h] : 0;
+            const unsigned d = sdst[h] + boff;
+            put(d, ru + g, v);
+            put(d + FO, rw + g, v);
+            put(d + 2 * FO, rx + g, v);
           }
-          cp_async8(dst + sidx[m], sp, valid);
+        }
+      } else {
+        // the lifted slab (row -1: u and x from the lift, if set) or a row outside this context: zeros
+        const double* lu = ct == -1 ? r.lift_u : nullptr;
+        const double* lx = ct == -1 ? r.lift_x : nullptr;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (gsp[h] != -2) {
+            const bool v = gsp[h] >= 0;
+            const int g = v ? gsp[h] : 0;
+            const unsigned d = sdst[h] + boff;
+            put(d, lu + g, v && lu != nullptr);
+            put(d + FO, nullptr, false);
+            put(d + 2 * FO, lx + g, v && lx != nullptr);
+          }
         }
       }
       cp_async_commit();
