@@ -122,12 +122,12 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
   if (warp < G::NCW) {
     // =========================== consumers ===========================
     rxws_reg_inc<MI_RXWS_REGC>();                    // the producers' released registers: window + ILP-4 time stage
-    double bI[2], bP[2];
+    double bP[2];
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      bI[ks] = basis(2, 4 * ks + fk, fr);
-      bP[ks] = basis(2, fr, 4 * ks + fk);
-    }
+    for (int ks = 0; ks < 2; ++ks) bP[ks] = basis(2, fr, 4 * ks + fk);
+    // z interpolation operands: functions 1..4 as the DMMA B fragment, function 0 at this thread's two points
+    const double bI1 = basis(2, 1 + fk, fr);
+    const double bI0[2] = {basis(2, 0, 2 * fk), basis(2, 0, 2 * fk + 1)};
     // the thread's Gauss points: line tile t = warp + 8 mi (q2 = t, q1 = fr), q3 = 2 fk + e.  The spatial
     // weight is folded into the x field and c2 into the w field as the slice enters the window.
     double wsp[MT][2];
@@ -176,26 +176,29 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         // z interpolation of slice j -> window slot PH
         const int bb = j & 1;
         mbar_wait(&fullB[bb], (unsigned)((j >> 1) & 1));
-        const double* fin = sB + bb * G::SB + fk * BJ + fr;
-        double c[MT][NF][2];
+        // K = 5 functions: j3 = 1..4 in ONE DMMA (k = fk), j3 = 0 as a rank-1 update on the CUDA cores
+        // (it only reaches the first element's Gauss points, q3 < 4: bI0 is zero elsewhere) instead of
+        // a second, 3/4 empty k-step
+        const double* fin = sB + bb * G::SB + fr;
+        double c[MT][NF][2], a0[MT][NF];
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-          for (int f = 0; f < NF; ++f) c[mi][f][0] = c[mi][f][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-          for (int mi = 0; mi < MT; ++mi)
-#pragma unroll
-            for (int f = 0; f < NF; ++f)
-              dmma(c[mi][f][0], c[mi][f][1], fin[(f * L3 + 4 * ks) * BJ + (warp + G::NCW * mi) * BS1], bI[ks]);
+          for (int f = 0; f < NF; ++f) {
+            const double* fp = fin + f * L3 * BJ + (warp + G::NCW * mi) * BS1;
+            c[mi][f][0] = c[mi][f][1] = 0.0;
+            a0[mi][f] = fp[0];
+            dmma(c[mi][f][0], c[mi][f][1], fp[(1 + fk) * BJ], bI1);
+          }
         mbar_arrive(&emptyB[bb]);
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            X[mi][PH][f][0] = c[mi][f][0] * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][0]));
-            X[mi][PH][f][1] = c[mi][f][1] * (f == 0 ? 1.0 : (f == 1 ? rc2 : wsp[mi][1]));
+            const double c0 = fma(a0[mi][f], bI0[0], c[mi][f][0]), c1 = fma(a0[mi][f], bI0[1], c[mi][f][1]);
+            // (u, c2 w + c1 a, w_x x): the constant of C_r rides on the w field (the time basis sums to 1)
+            X[mi][PH][f][0] = f == 0 ? c0 : (f == 1 ? fma(c0, rc2, rk0) : c0 * wsp[mi][0]);
+            X[mi][PH][f][1] = f == 0 ? c1 : (f == 1 ? fma(c1, rc2, rk0) : c1 * wsp[mi][1]);
           }
       }
       if (et < 0) return;
@@ -221,13 +224,13 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
                 xx[mi][e] = fma(ba, X[mi][(S0 + a) % PW][2][e], xx[mi][e]);
               }
           }
-          // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + c1 a + c2 w
+          // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + (c1 a + c2 w)
           double v[MT][2];
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
-              v[mi][e] = fma(uu[mi][e], fma(rc1, uu[mi][e], rk1), ww[mi][e] + rk0) * xx[mi][e];
+              v[mi][e] = fma(uu[mi][e], fma(rc1, uu[mi][e], rk1), ww[mi][e]) * xx[mi][e];
 #pragma unroll
           for (int a = 0; a < PW; ++a) {
             const double bw = bt[QT * PW + g * PW + a];
