@@ -530,7 +530,7 @@ static bool use_reaction_ws(const mi_ctx* c) {
     const char* e = std::getenv("MI_RX_WS");
     return e == nullptr || e[0] != '0';
   }();
-  return on && c->d == 3 && c->p == 3 && c->pt == 3 && c->ns_in < (1LL << 31);
+  return on && c->d == 3 && c->p == 3 && c->pt == 3 && c->ns_in < (1LL << 31) && c->c1 >= 0.0;
 }
 
 // y[t, owned planes] += y_in[t, same planes of the input slab] (z-slab contexts)

@@ -52,6 +52,12 @@ struct RxWS {
 #ifndef MI_RXWS_REGP
 #define MI_RXWS_REGP 88
 #endif
+#ifndef MI_RXWS_ABL
+#define MI_RXWS_ABL 0      // timing ablations (wrong results): 1 no time stage, 2 no producer DMMAs, 4 no z stages
+#endif
+#ifndef MI_RXWS_SKEW
+#define MI_RXWS_SKEW 0
+#endif
 #ifndef MI_RXWS_UNROLL
 #define MI_RXWS_UNROLL 1   // consumer slice loop unrolled by p_t + 1 (compile-time window slots, no rotation copies)
 #endif
@@ -60,6 +66,12 @@ __device__ __forceinline__ void rxws_reg_inc() { asm volatile("setmaxnreg.inc.sy
 template <int N>
 __device__ __forceinline__ void rxws_reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N)); }
 
+__device__ __forceinline__ void rxws_pdmma(double& c0, double& c1, double a, double b) {
+  if (MI_RXWS_ABL & 2) { c0 += a; c1 += b; } else dmma(c0, c1, a, b);
+}
+__device__ __forceinline__ void rxws_cdmma(double& c0, double& c1, double a, double b) {
+  if (MI_RXWS_ABL & 4) { c0 += a; c1 += b; } else dmma(c0, c1, a, b);
+}
 __device__ __forceinline__ void rxws_bar_producers() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(RxWS::NPT) : "memory");
 }
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         }
         wsp[mi][e] = v;
       }
-    const double rc1 = r.c1, rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;
+    const double rsq = sqrt(r.c1), rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;   // c1 >= 0 (launcher)
     double X[MT][PW][NF][2], Y[MT][PW][2];
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi)
@@ -158,53 +170,76 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
     // times the Gauss weight (projection).  The loads are consumed one step later (no stall on them).
     double btb = 0.0, btw = 1.0;
     auto prefetch_bt = [&](int et) {
+      btb = 0.0;                                     // no such element: all-zero tables (the step adds nothing)
       if (et >= 0 && et < nelt) {
         const int ga = lane & 15;
         btb = __ldg(r.B[3] + (long long)et * QT * PW + ga);
         if (lane >= 16) btw = __ldg(r.Wq[3] + (long long)et * QT + ga / PW);
       }
     };
-    // One slice step with compile-time window slots: the entering slice j goes to slot PH, function
-    // et + a sits in slot (S0 + a) % PW with S0 = (PH + 1) % PW.
+    // One software-pipelined slice step with compile-time window slots (PH = j % PW).  Three mutually
+    // independent pieces share ONE basic block, so the DMMA / shuffle / shared-memory latencies of the
+    // z stages hide behind the DFMA stream of the time stage of the same warp:
+    //   * z interpolation of the entering slice j (its accumulators reach window slot PH only at the
+    //     end of the step: the slot still holds function j - PW, the first one of this step's element);
+    //   * the time stage of element et = j - PW (functions et + a in slot (PH + a) % PW);
+    //   * the z projection of function fz = et - 1, completed by the previous step (its Y slot, copied
+    //     out first, is the one this step starts to fill for function et + PT).
+    // Steps without a valid element run the time stage on all-zero tables (no branch), steps without an
+    // entering slice interpolate stale (finite) data into a slot nothing reads.
     auto step = [&](auto phc, int j) {
-      constexpr int PH = decltype(phc)::value, S0 = (PH + 1) % PW;
-      const int et = j - PT;                         // time element; the function completed by it
-      myBt[(j & 1) * 32 + lane] = btb * btw;
+      constexpr int PH = decltype(phc)::value, SZ = (PH + PW - 1) % PW;
+      const int et = j - PW, fz = et - 1;
+      const bool has_in = j < nfull, has_fz = fz >= 0;     // fz < nfull by the loop bound
+      const int bb = j & 1, cb = fz & 1;
+      myBt[bb * 32 + lane] = btb * btw;
       __syncwarp();
       prefetch_bt(et + 1);
-      if (j < nfull) {
-        // z interpolation of slice j -> window slot PH
-        const int bb = j & 1;
-        mbar_wait(&fullB[bb], (unsigned)((j >> 1) & 1));
-        // K = 5 functions: j3 = 1..4 in ONE DMMA (k = fk), j3 = 0 as a rank-1 update on the CUDA cores
-        // (it only reaches the first element's Gauss points, q3 < 4: bI0 is zero elsewhere) instead of
-        // a second, 3/4 empty k-step
-        const double* fin = sB + bb * G::SB + fr;
-        double c[MT][NF][2], a0[MT][NF];
+      if (has_in) mbar_wait(&fullB[bb], (unsigned)((j >> 1) & 1));
+      if (fz >= 2) mbar_wait(&emptyC[cb], (unsigned)(((fz >> 1) - 1) & 1));
+      // ---- z interpolation of slice j: functions 1..4 in ONE DMMA (k = fk), function 0 as a rank-1
+      // update on the CUDA cores (it only reaches the first element's Gauss points: bI0 is zero elsewhere)
+      const double* fin = sB + bb * G::SB + fr;
+      double zc[MT][NF][2], a0[MT][NF], za[MT][NF];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi)
+      for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-          for (int f = 0; f < NF; ++f) {
-            const double* fp = fin + f * L3 * BJ + (warp + G::NCW * mi) * BS1;
-            c[mi][f][0] = c[mi][f][1] = 0.0;
-            a0[mi][f] = fp[0];
-            dmma(c[mi][f][0], c[mi][f][1], fp[(1 + fk) * BJ], bI1);
-          }
-        mbar_arrive(&emptyB[bb]);
+        for (int f = 0; f < NF; ++f) {
+          const double* fp = fin + f * L3 * BJ + (warp + G::NCW * mi) * BS1;
+          a0[mi][f] = fp[0];
+          za[mi][f] = fp[(1 + fk) * BJ];
+        }
+      const double* bt = myBt + bb * 32;
+      double btv[2 * QT * PW];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi)
+      for (int i = 0; i < 2 * QT * PW; ++i) btv[i] = bt[i];
+      if (has_in) mbar_arrive(&emptyB[bb]);
+      // ---- z projection operands of function fz (slot SZ), and the slot's fresh start
+      double yz[MT][2], zp[MT][2];
 #pragma unroll
-          for (int f = 0; f < NF; ++f) {
-            const double c0 = fma(a0[mi][f], bI0[0], c[mi][f][0]), c1 = fma(a0[mi][f], bI0[1], c[mi][f][1]);
-            // (u, c2 w + c1 a, w_x x): the constant of C_r rides on the w field (the time basis sums to 1)
-            X[mi][PH][f][0] = f == 0 ? c0 : (f == 1 ? fma(c0, rc2, rk0) : c0 * wsp[mi][0]);
-            X[mi][PH][f][1] = f == 0 ? c1 : (f == 1 ? fma(c1, rc2, rk0) : c1 * wsp[mi][1]);
-          }
+      for (int mi = 0; mi < MT; ++mi) {
+        yz[mi][0] = Y[mi][SZ][0], yz[mi][1] = Y[mi][SZ][1];
+        Y[mi][SZ][0] = Y[mi][SZ][1] = 0.0;
+        zp[mi][0] = zp[mi][1] = 0.0;
       }
-      if (et < 0) return;
-      // time element et on the thread's own four points, all chains interleaved
-      if (et < nelt) {
-        const double* bt = myBt + (j & 1) * 32;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          zc[mi][f][0] = zc[mi][f][1] = 0.0;
+          rxws_cdmma(zc[mi][f][0], zc[mi][f][1], za[mi][f], bI1);
+        }
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          const int cc = 4 * ks + fk, src = (lane & ~3) | (cc >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, yz[mi][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, yz[mi][1], src);
+          rxws_cdmma(zp[mi][0], zp[mi][1], (cc & 1) ? v1 : v0, bP[ks]);
+        }
+      // ---- time element et on the thread's own four points, all chains interleaved
+      if (!(MI_RXWS_ABL & 1)) {
 #pragma unroll
         for (int g = 0; g < QT; ++g) {
           double uu[MT][2], ww[MT][2], xx[MT][2];
@@ -214,98 +249,73 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
             for (int e = 0; e < 2; ++e) uu[mi][e] = ww[mi][e] = xx[mi][e] = 0.0;
 #pragma unroll
           for (int a = 0; a < PW; ++a) {
-            const double ba = bt[g * PW + a];
+            const double ba = btv[g * PW + a];
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                uu[mi][e] = fma(ba, X[mi][(S0 + a) % PW][0][e], uu[mi][e]);
-                ww[mi][e] = fma(ba, X[mi][(S0 + a) % PW][1][e], ww[mi][e]);
-                xx[mi][e] = fma(ba, X[mi][(S0 + a) % PW][2][e], xx[mi][e]);
+                uu[mi][e] = fma(ba, X[mi][(PH + a) % PW][0][e], uu[mi][e]);
+                ww[mi][e] = fma(ba, X[mi][(PH + a) % PW][1][e], ww[mi][e]);
+                xx[mi][e] = fma(ba, X[mi][(PH + a) % PW][2][e], xx[mi][e]);
               }
           }
-          // C_r = c1 (u - a)(u - 1) + c2 w = u (c1 u - c1 (1 + a)) + (c1 a + c2 w)
-          double v[MT][2];
+          double v[MT][2];                           // C_r x w_x = (u'^2 + p) x'
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
-              v[mi][e] = fma(uu[mi][e], fma(rc1, uu[mi][e], rk1), ww[mi][e]) * xx[mi][e];
+            for (int e = 0; e < 2; ++e) v[mi][e] = fma(uu[mi][e], uu[mi][e], ww[mi][e]) * xx[mi][e];
 #pragma unroll
           for (int a = 0; a < PW; ++a) {
-            const double bw = bt[QT * PW + g * PW + a];
+            const double bw = btv[QT * PW + g * PW + a];
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) Y[mi][(S0 + a) % PW][e] = fma(bw, v[mi][e], Y[mi][(S0 + a) % PW][e]);
+              for (int e = 0; e < 2; ++e) Y[mi][(PH + a) % PW][e] = fma(bw, v[mi][e], Y[mi][(PH + a) % PW][e]);
           }
         }
       }
-      // z projection of the completed function et (slot S0): A fragments by quad shuffles
-      double c[MT][2];
+      // ---- the entering slice reaches its window slot as (sqrt(c1) u, p, w_x x) with
+      // p = c2 w - c1 (1 + a) u + c1 a, so that C_r = c1 (u - a)(u - 1) + c2 w = (sqrt(c1) u)^2 + p is ONE
+      // fused multiply-add per Gauss point; p is linear in the coefficients, and its constant rides
+      // along because the time basis sums to 1
 #pragma unroll
-      for (int mi = 0; mi < MT; ++mi) c[mi][0] = c[mi][1] = 0.0;
+      for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
+        for (int e = 0; e < 2; ++e) {
+          const double cu = fma(a0[mi][0], bI0[e], zc[mi][0][e]), cw = fma(a0[mi][1], bI0[e], zc[mi][1][e]),
+                       cx = fma(a0[mi][2], bI0[e], zc[mi][2][e]);
+          X[mi][PH][0][e] = cu * rsq;
+          X[mi][PH][1][e] = fma(cu, rk1, fma(cw, rc2, rk0));
+          X[mi][PH][2][e] = cx * wsp[mi][e];
+        }
+      // ---- projected function fz to the producers
+      if (has_fz) {
+        double* out = sC + cb * G::SC;
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi) {
-          const int cc = 4 * ks + fk, src = (lane & ~3) | (cc >> 1);
-          const double v0 = __shfl_sync(0xffffffffu, Y[mi][S0][0], src);
-          const double v1 = __shfl_sync(0xffffffffu, Y[mi][S0][1], src);
-          dmma(c[mi][0], c[mi][1], (cc & 1) ? v1 : v0, bP[ks]);
+          const int line = 8 * (warp + G::NCW * mi) + fr, n0 = 2 * fk;
+          if (n0 < L3) out[n0 * CS + line] = zp[mi][0];
+          if (n0 + 1 < L3) out[(n0 + 1) * CS + line] = zp[mi][1];
         }
-#pragma unroll
-      for (int mi = 0; mi < MT; ++mi) Y[mi][S0][0] = Y[mi][S0][1] = 0.0;
-      const int cb = et & 1;
-      if (et >= 2) mbar_wait(&emptyC[cb], (unsigned)(((et >> 1) - 1) & 1));
-      double* out = sC + cb * G::SC;
-#pragma unroll
-      for (int mi = 0; mi < MT; ++mi) {
-        const int line = 8 * (warp + G::NCW * mi) + fr, n0 = 2 * fk;
-        if (n0 < L3) out[n0 * CS + line] = c[mi][0];
-        if (n0 + 1 < L3) out[(n0 + 1) * CS + line] = c[mi][1];
+        mbar_arrive(&fullC[cb]);
       }
-      mbar_arrive(&fullC[cb]);
     };
-    const int nsteps = nfull + PT;
-#if MI_RXWS_UNROLL
+    const int nsteps = nfull + PW + 1;               // the last step projects function nfull - 1
     for (int j0 = 0; j0 < nsteps; j0 += PW) {
       step(std::integral_constant<int, 0>{}, j0);
       if (j0 + 1 < nsteps) step(std::integral_constant<int, 1>{}, j0 + 1);
       if (j0 + 2 < nsteps) step(std::integral_constant<int, 2>{}, j0 + 2);
       if (j0 + 3 < nsteps) step(std::integral_constant<int, 3>{}, j0 + 3);
     }
-#else
-    // one copy of the step with fixed slots (entering slice -> slot PT, function et -> slot 0) and a
-    // cyclic rotation of both windows after it
-    for (int j = 0; j < nsteps; ++j) {
-      step(std::integral_constant<int, PT>{}, j);
-#pragma unroll
-      for (int mi = 0; mi < MT; ++mi) {
-        double xs[NF][2], ys[2];
-#pragma unroll
-        for (int f = 0; f < NF; ++f) xs[f][0] = X[mi][0][f][0], xs[f][1] = X[mi][0][f][1];
-        ys[0] = Y[mi][0][0], ys[1] = Y[mi][0][1];
-#pragma unroll
-        for (int a = 0; a < PW - 1; ++a) {
-#pragma unroll
-          for (int f = 0; f < NF; ++f) X[mi][a][f][0] = X[mi][a + 1][f][0], X[mi][a][f][1] = X[mi][a + 1][f][1];
-          Y[mi][a][0] = Y[mi][a + 1][0], Y[mi][a][1] = Y[mi][a + 1][1];
-        }
-#pragma unroll
-        for (int f = 0; f < NF; ++f) X[mi][PW - 1][f][0] = xs[f][0], X[mi][PW - 1][f][1] = xs[f][1];
-        Y[mi][PW - 1][0] = ys[0], Y[mi][PW - 1][1] = ys[1];
-      }
-    }
-#endif
   } else {
     // =========================== producers ===========================
     rxws_reg_dec<MI_RXWS_REGP>();
     const int p = tid - G::NCT, pw = warp - G::NCW;
-    double bIx[2], bIy[2][2], bPy[4], bPx[2];
+    double bIy[2][2], bPy[4], bPx[2];
+    const double bIx1 = basis(0, 1 + fk, fr);
+    const double bIx0[2] = {basis(0, 0, 2 * fk), basis(0, 0, 2 * fk + 1)};
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
-      bIx[ks] = basis(0, 4 * ks + fk, fr);
       bPx[ks] = basis(0, fr, 4 * ks + fk);
 #pragma unroll
       for (int n2 = 0; n2 < 2; ++n2) bIy[n2][ks] = basis(1, 4 * ks + fk, 8 * n2 + fr);
@@ -389,9 +399,10 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         yidx[u][e] = ok ? gs : -1;
       }
     issue(0);
-    for (int i = 0; i <= nfull + PT; ++i) {
+    for (int i = 0; i <= nfull + PW + 1; ++i) {
       const bool has_in = i < nfull;
-      const int fq = i - PT - 1;                     // function whose y / x projections run now
+      const int fq = i - PW - 2;                     // function whose y / x projections run now (its z
+                                                     // projection ended with consumer step i - 1)
       const bool has_fq = fq >= 0 && fq < nfull;
       cp_async_wait<0>();                            // this thread's copies of slice i have landed ...
       rxws_bar_producers();                          // ... and everyone's; the other sIn buffer is free
@@ -400,21 +411,25 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
         const double* sI = sIn + (i & 1) * G::SIN;
         // x interpolation of slice i: lines (fld, j3, j2), K = j1, N = q1 -> sA
         constexpr int NL = NF * L3 * L2, NMT = (NL + 7) / 8;    // 105 lines, 14 tiles
-        double c[4][2];
+        // functions 1..4 in ONE DMMA, function 0 (first element's Gauss points only) as a rank-1 update
+        double c[4][2], a0[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           c[u][0] = c[u][1] = 0.0;
+          a0[u] = 0.0;
           const int mt = pw + G::NPW * u;
           if (mt < NMT) {
-            const int line = mt * 8 + fr;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) dmma(c[u][0], c[u][1], sI[line * IS1 + 4 * ks + fk], bIx[ks]);
+            const double* row = sI + (mt * 8 + fr) * IS1;
+            a0[u] = row[0];
+            rxws_pdmma(c[u][0], c[u][1], row[1 + fk], bIx1);
           }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int line = (pw + G::NPW * u) * 8 + fr;
-          if (line < NL) *reinterpret_cast<double2*>(sA + line * Q1 + 2 * fk) = make_double2(c[u][0], c[u][1]);
+          if (line < NL)
+            *reinterpret_cast<double2*>(sA + line * Q1 + 2 * fk) =
+                make_double2(fma(a0[u], bIx0[0], c[u][0]), fma(a0[u], bIx0[1], c[u][1]));
         }
       }
       rxws_bar_producers();
@@ -436,7 +451,7 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
               for (int ks = 0; ks < 2; ++ks) {
                 const double av = sA[(mt * L2 + 4 * ks + fk) * Q1 + fr];
 #pragma unroll
-                for (int n2 = 0; n2 < 2; ++n2) dmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
+                for (int n2 = 0; n2 < 2; ++n2) rxws_pdmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
               }
             }
           }
@@ -468,7 +483,7 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
           const int mt = pw + G::NPW * u;            // = j3
           if (mt < L3) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) dmma(c[u][0], c[u][1], in[mt * CS + (4 * ks + fk) * Q1 + fr], bPy[ks]);
+            for (int ks = 0; ks < 4; ++ks) rxws_pdmma(c[u][0], c[u][1], in[mt * CS + (4 * ks + fk) * Q1 + fr], bPy[ks]);
           }
         }
         mbar_arrive(&emptyC[cb]);
@@ -495,7 +510,7 @@ __global__ void __launch_bounds__(RxWS::NTH, 1) reaction_ws(RxArgs r) {
             const int xline = 8 * mt + fr;
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, sD[xline * DS1 + 4 * ks + fk], bPx[ks]);
+            for (int ks = 0; ks < 2; ++ks) rxws_pdmma(c0, c1, sD[xline * DS1 + 4 * ks + fk], bPx[ks]);
             if (row >= 0) {
               if (yidx[u][0] >= 0) atomicAdd(r.y + row + yidx[u][0], c0);
               if (yidx[u][1] >= 0) atomicAdd(r.y + row + yidx[u][1], c1);
