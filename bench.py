@@ -731,6 +731,14 @@ def run_ours(args):
                              "kernel_ms_per_step": {k: v[0] / nb for k, v in pb.items() if v[1]},
                              "note": "P^-1 A x with A built at u~U[0,1], w~U[0,0.1] (seed 1): Galerkin + SU + M_R "
                                      "(q=p+1 Gauss, Rogers-McCulloch linearisation), no a*c1 term"}
+        if "op_reaction" in pb and pb["op_reaction"][1]:
+            # F_MR = 13,952 flop/DoF (sum-factorised, matrix-free, q = p+1) against the FP64 peak
+            rx_ms = pb["op_reaction"][0] / nb
+            rx_tf = 13952.0 * N / (rx_ms * 1e-3) / 1e12
+            line["variant_b"]["reaction_roofline"] = {
+                "kernel": "reaction_ws (warp-specialised, d=3 p=3 fused mode)", "bound": "tensor",
+                "flops_per_dof": 13952, "ms": rx_ms, "achieved": rx_tf, "unit": "TFLOP/s",
+                "peak": line["roofline"]["peak"], "frac": rx_tf / line["roofline"]["peak"]}
         del opb, Pb, x, y, z
         cb.close()
         torch.cuda.empty_cache()

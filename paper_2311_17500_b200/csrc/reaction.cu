@@ -14,7 +14,9 @@
 //
 // History (cfg 4, 96^3 x 192, p = 3): warp per element 1259 ms, line ops
 // 1123, block tile sweep 813, DMMA stages 615, time-streamed 281, pipelined
-// projections 229 (profiles/r01_optimisation_log.md).
+// projections 229 (profiles/r01_optimisation_log.md), reaction_tile 202; the
+// fused mode at d = 3, p = 3 now runs the warp-specialised reaction_ws
+// (reaction_ws.cuh, 112.8 ms; profiles/r02_optimisation_log.md R15-R22).
 #include "common.cuh"
 #include "dispatch.cuh"
 #include "ptx.cuh"
