@@ -160,6 +160,11 @@ int mi_op_set_reaction_weight(mi_ctx* ctx, const double* jw);
  * apply interpolates only x.  mode -1: when it fits in 40% of the free
  * device memory (default), 0: never, 1: always. */
 int mi_op_set_reaction_store(mi_ctx* ctx, int mode);
+/* Kernel of the fused (non-stored) reaction: -1 auto (the warp-specialised
+ * reaction_ws at d = 3, p = p_t = 3, c1 >= 0; reaction_tile otherwise),
+ * 0 reaction_tile, 1 reaction_ws.  Both evaluate reaction_mass's quadrature
+ * (assembly.py:287-347); the switch exists for parity tests and timing. */
+int mi_op_set_reaction_kernel(mi_ctx* ctx, int kernel);
 /* Time slabs (KroneckerOperator(time_rows=...)): the reaction tables cover local time elements whose
  * full-basis function ft maps to local row ft + row_offset (default -1). */
 int mi_op_set_reaction_rows(mi_ctx* ctx, int row_offset);

@@ -41,6 +41,7 @@ _SIGS = {
     "mi_theta_set_lift": ([_vp, _vp], _c_int),
     "mi_op_set_reaction_weight": ([_vp, _vp], _c_int),
     "mi_op_set_reaction_store": ([_vp, _c_int], _c_int),
+    "mi_op_set_reaction_kernel": ([_vp, _c_int], _c_int),
     "mi_op_set_quad_channel": ([_vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_set_quad_channel_k": ([_vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp], _c_int),
     "mi_op_set_channel_stencil": ([_vp, _c_int, _vp], _c_int),

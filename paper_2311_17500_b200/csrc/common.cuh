@@ -121,6 +121,7 @@ struct mi_ctx {
   mi::DeviceBuf rx_cw;          // stored C_r x spatial weight at every Gauss point (reaction.cu RX_STORED)
   bool rx_cw_ok = false, rx_cw_dirty = true;
   int rx_store_mode = -1;       // -1 auto (fits in 40% of free memory), 0 off, 1 on
+  int rx_kernel = -1;           // fused mode: -1 auto (reaction_ws where it applies), 0 reaction_tile, 1 reaction_ws
 
   // ---- preconditioner
   bool pc_ready = false;

@@ -532,7 +532,8 @@ static bool use_reaction_ws(const mi_ctx* c) {
     const char* e = std::getenv("MI_RX_WS");
     return e == nullptr || e[0] != '0';
   }();
-  return on && c->d == 3 && c->p == 3 && c->pt == 3 && c->ns_in < (1LL << 31) && c->c1 >= 0.0;
+  const bool can = c->d == 3 && c->p == 3 && c->pt == 3 && c->ns_in < (1LL << 31) && c->c1 >= 0.0;
+  return can && (c->rx_kernel == 1 || (c->rx_kernel < 0 && on));
 }
 
 // y[t, owned planes] += y_in[t, same planes of the input slab] (z-slab contexts)
@@ -763,6 +764,16 @@ int mi_op_set_reaction_store(mi_ctx* c, int mode) {
   MI_REQUIRE(mode >= -1 && mode <= 1, MI_ERR_ARG, "store mode must be -1, 0 or 1");
   c->rx_store_mode = mode;
   c->rx_cw_dirty = true;
+  return MI_OK;
+}
+
+int mi_op_set_reaction_kernel(mi_ctx* c, int kernel) {
+  MI_DEVICE_GUARD(c);
+  MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
+  MI_REQUIRE(kernel >= -1 && kernel <= 1, MI_ERR_ARG, "kernel must be -1 (auto), 0 (reaction_tile) or 1 (reaction_ws)");
+  MI_REQUIRE(kernel != 1 || (c->d == 3 && c->p == 3 && c->pt == 3), MI_ERR_ARG,
+             "reaction_ws serves d = 3, p = p_t = 3 only");
+  c->rx_kernel = kernel;
   return MI_OK;
 }
 
