@@ -32,6 +32,10 @@
 #ifndef MI_STEN_PERSIST
 #define MI_STEN_PERSIST 1   // persistent CTAs with cross-cube prefetch (stencil_dmma)
 #endif
+#ifndef MI_STEN_DECOUPLED
+#define MI_STEN_DECOUPLED 1 // no block barrier in the chunk loop: the two warps of a point meet on a named barrier,
+                            // the halo buffers are recycled by whichever warp finishes a chunk last
+#endif
 #ifndef MI_STEN_L2PF
 #define MI_STEN_L2PF 1      // persistent CTAs also prefetch the next cube's fragments into L2
 #endif
@@ -70,7 +74,8 @@ struct DmmaSten {
   static constexpr int FK = 8 * 16;                 // filter K: 8 channels x 16 time taps
   static constexpr size_t SMEM = (size_t)2 * HS * TSTR * 8       // X halo [buf][h][t]
                                  + (size_t)2 * PPB * PSTR * 8     // W partials [half][pt][ch*WL + row]
-                                 + 16;                            // TMA mbarriers
+                                 + 16                             // TMA mbarriers
+                                 + 16;                            // buffer-release counters
   // halo offset of stencil point s (0 beyond S)
   static constexpr __host__ __device__ int offs(int s) {
     return s >= S ? 0 : ((D >= 3 ? s / (W * W) : 0) * H2 + (D >= 2 ? (s / W) % W : 0)) * H1 + s % W;
@@ -196,6 +201,116 @@ __global__ void __launch_bounds__(DmmaSten<D, P>::THREADS, 1) stencil_dmma(DmmaA
   const int nchunks = (a.nt + G::TT - 1) / G::TT;
   int gc = 0;                                        // chunks consumed by this block: buffer gc & 1, phase (gc >> 1) & 1
 
+#if MI_STEN_DECOUPLED
+  {
+    // ---- decoupled sweep.  The block's chunk sequence g = 0, 1, ... runs over its cubes (nchunks
+    // chunks each); chunk g lives in halo buffer g & 1 and in W ring half g & 1.  No block barrier:
+    //   * a warp that has finished the sweep of chunk g bumps cnt[g & 1]; the LAST of the block's warps
+    //     to do so re-arms the buffer with the TMA load of chunk g + 2 (nobody waits for a free buffer);
+    //   * the two warps of a point (the K halves) meet on a named barrier once per chunk, after which
+    //     the pair writes the point's 8 channels x 16 rows of W out.
+    // A warp that is done with chunk g starts on g + 1 at once, so the write-out, the barrier skew and
+    // the accumulator drains of some warps overlap the DMMA sweeps of the others.
+    int* cnt = reinterpret_cast<int*>(bars + 2);
+    constexpr int NWARP = G::THREADS / 32;
+    const int first = a.cube_lo + (int)blockIdx.x;
+    const int ncb = first < ncubes ? (ncubes - first + cstep - 1) / cstep : 0;     // cubes of this block
+    const long long gtot = (long long)ncb * nchunks;
+    auto load_g = [&](long long g) {                 // one thread: TMA load of chunk g into buffer g & 1
+      if (g < gtot) {
+        const int cube = first + (int)(g / nchunks) * cstep, t0 = (int)(g % nchunks) * G::TT;
+        int q1, q2, q3;
+        origin(cube, q1, q2, q3);
+        const int buf = (int)(g & 1);
+        mbar_expect_tx(&bars[buf], TILE_BYTES);
+        tma_load_4d(Xs + buf * G::HS * G::TSTR, &tmap, &bars[buf], t0, q1 - P, D >= 2 ? q2 - P : 0,
+                    D >= 3 ? q3 - P + a.zoff : 0);
+      }
+    };
+    if (tid == 0) {
+      cnt[0] = cnt[1] = 0;
+      load_g(0);
+      load_g(1);
+    }
+    __syncthreads();                                 // Wp zeroed, counters set
+    const int tp = half * 32 + lane;                 // thread of the point's warp pair
+    long long g = 0;
+    for (int ci = 0; ci < ncb; ++ci) {
+      const int cube = first + ci * cstep;
+      int o1, o2, o3;
+      origin(cube, o1, o2, o3);
+      double breg[G::KH];
+      {
+        const double* f = a.frag + ((long long)cube * G::PPB + pt) * G::KS * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < G::KH; ++j) {
+          const int ks = half * G::KH + j;
+          breg[j] = ks < G::KS ? __ldg(f + ks * 32) : 0.0;
+        }
+      }
+      if (MI_STEN_L2PF && ci + 1 < ncb && warp == 0) {
+        const char* nf = reinterpret_cast<const char*>(a.frag + (long long)(cube + cstep) * FRAG_CUBE);
+        constexpr long long BYTES = FRAG_CUBE * 8;
+        for (long long off = (long long)lane * 16384; off < BYTES; off += 32LL * 16384) {
+          const unsigned sz = (unsigned)(BYTES - off < 16384 ? BYTES - off : 16384);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(nf + off), "r"(sz) : "memory");
+        }
+      }
+      // this point's output position
+      const int q1 = o1 + pt % G::B1, q2 = o2 + (pt / G::B1) % G::B2, q3 = o3 + pt / (G::B1 * G::B2);
+      const bool pvalid = q1 < a.n1 && q2 < a.n2 && q3 < a.n3;
+      const long long gi = ((long long)q3 * a.n2 + q2) * a.n1 + q1;
+      for (int ch = 0; ch < nchunks; ++ch, ++g) {
+        const int t0 = ch * G::TT, buf = (int)(g & 1), rb = buf * G::TT;   // W ring half of this chunk
+        mbar_wait(&bars[buf], (unsigned)((g >> 1) & 1));                   // X(g) landed
+        double acc[G::MT][2];
+#pragma unroll
+        for (int m = 0; m < G::MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+        {
+          const double* X = Xs + buf * G::HS * G::TSTR + (base + kl) * G::TSTR + mrow;
+          if (t0 + 8 * (G::MT - 1) < a.nt) {
+            if (half == 0)
+              dmma_sweep<G, 0, G::MT>(X, kl, breg, acc);
+            else
+              dmma_sweep<G, 1, G::MT>(X, kl, breg, acc);
+          } else {
+            if (half == 0)
+              dmma_sweep<G, 0, 1>(X, kl, breg, acc);
+            else
+              dmma_sweep<G, 1, 1>(X, kl, breg, acc);
+          }
+        }
+        // the sweep's operand loads have returned (their DMMAs have issued): release the halo buffer
+        __syncwarp();
+        if (lane == 0) {
+          if (atomicAdd(&cnt[buf], 1) == NWARP - 1) {
+            cnt[buf] = 0;
+            load_g(g + 2);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < G::MT; ++m) {
+          wmine[rb + m * 8 + mrow] = acc[m][0];
+          wmine[G::WL + rb + m * 8 + mrow] = acc[m][1];
+        }
+        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + pt) : "memory");      // both K halves of this point are in
+        // W of this chunk: thread -> (row pair rp, channel c); 8 consecutive threads write 16 rows (128 B)
+        {
+          const int rp = tp & 7, c = tp >> 3;
+          if (c < a.nc && pvalid) {
+            const double* w0 = Wp + pt * G::PSTR + c * G::WL + rb + 2 * rp;
+            const double* w1 = w0 + G::PPB * G::PSTR;
+            double2 v;
+            v.x = w0[0] + w1[0];
+            v.y = w0[1] + w1[1];
+            *reinterpret_cast<double2*>(a.wout + ((long long)(a.c0 + c) * a.ns + gi) * a.ntp + t0 + 2 * rp) = v;
+          }
+        }
+      }
+    }
+    return;
+  }
+#endif
   if (a.cube_lo + (int)blockIdx.x < ncubes) load_chunk(a.cube_lo + blockIdx.x, 0, 0);
   for (int cube = a.cube_lo + blockIdx.x; cube < ncubes; cube += cstep) {
     int o1, o2, o3;
