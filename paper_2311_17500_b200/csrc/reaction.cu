@@ -526,13 +526,13 @@ __global__ void __launch_bounds__(RxTile<D, P>::NTH, RxTile<D, P>::MINB) reactio
 
 namespace mi {
 
-// the warp-specialised kernel serves the fused mode at d = 3, p = p_t = 3 (MI_RX_WS=0: reaction_tile)
+// the warp-specialised kernel serves the fused mode at d = 3, p = p_t in {2, 3} (MI_RX_WS=0: reaction_tile)
 static bool use_reaction_ws(const mi_ctx* c) {
   static const bool on = [] {
     const char* e = std::getenv("MI_RX_WS");
     return e == nullptr || e[0] != '0';
   }();
-  const bool can = c->d == 3 && c->p == 3 && c->pt == 3 && c->ns_in < (1LL << 31) && c->c1 >= 0.0;
+  const bool can = c->d == 3 && (c->p == 3 || c->p == 2) && c->pt == c->p && c->ns_in < (1LL << 31) && c->c1 >= 0.0;
   return can && (c->rx_kernel == 1 || (c->rx_kernel < 0 && on));
 }
 
@@ -671,7 +671,8 @@ int reaction_apply(mi_ctx* c, const double* x, double* y, const double* x0) {
   r.lift_x = x0;
   r.y = slab ? c->y_in.p : y;
   int rc = c->rx_cw_ok ? reaction_launch<RX_STORED>(c, r)
-                        : (use_reaction_ws(c) ? reaction_ws_launch(c, r) : reaction_launch<RX_FUSED>(c, r));
+                        : (use_reaction_ws(c) ? (c->p == 3 ? reaction_ws_launch<3>(c, r) : reaction_ws_launch<2>(c, r))
+                                              : reaction_launch<RX_FUSED>(c, r));
   if (rc) return rc;
   if (slab) {
     dim3 g((unsigned)((c->ns + 255) / 256), c->nt);
@@ -771,8 +772,8 @@ int mi_op_set_reaction_kernel(mi_ctx* c, int kernel) {
   MI_DEVICE_GUARD(c);
   MI_REQUIRE(c != nullptr, MI_ERR_ARG, "ctx is NULL");
   MI_REQUIRE(kernel >= -1 && kernel <= 1, MI_ERR_ARG, "kernel must be -1 (auto), 0 (reaction_tile) or 1 (reaction_ws)");
-  MI_REQUIRE(kernel != 1 || (c->d == 3 && c->p == 3 && c->pt == 3), MI_ERR_ARG,
-             "reaction_ws serves d = 3, p = p_t = 3 only");
+  MI_REQUIRE(kernel != 1 || (c->d == 3 && (c->p == 3 || c->p == 2) && c->pt == c->p), MI_ERR_ARG,
+             "reaction_ws serves d = 3, p = p_t in {2, 3} only");
   c->rx_kernel = kernel;
   return MI_OK;
 }

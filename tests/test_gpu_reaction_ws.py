@@ -1,4 +1,4 @@
-"""The warp-specialised fused reaction kernel (csrc/reaction_ws.cuh; d = 3, p = p_t = 3) against the
+"""The warp-specialised fused reaction kernel (csrc/reaction_ws.cuh; d = 3, p = p_t in {2, 3}) against the
 CPU oracle (reaction_mass's q = p+1 quadrature, assembly.py:287-347) and against reaction_tile, on
 meshes that leave partial 2 x 4 x 2 element tiles in every direction, with the u0 lifting, on time-row
 slabs and on a z slab (the sharded contexts)."""
@@ -21,6 +21,9 @@ def _spaces(nes, ne_t, p=3):
     return st, make_space_time(3, p, nes, ne_t)
 
 
+PS = pytest.mark.parametrize("p", [2, 3])
+
+
 def _mr(op, x, kernel):
     """M_R x alone: the operator with the reaction minus the same operator without it."""
     from paper_2311_17500_b200 import _lib
@@ -29,11 +32,12 @@ def _mr(op, x, kernel):
     return op.matvec(x)
 
 
+@pytest.mark.parametrize("p", [2, 3])
 @pytest.mark.parametrize("nes,ne_t", [((5, 7, 3), 6), ((2, 4, 2), 4), ((1, 1, 1), 1), ((9, 3, 5), 3)])
-def test_reaction_ws_matches_oracle_and_tile_kernel(nes, ne_t):
+def test_reaction_ws_matches_oracle_and_tile_kernel(nes, ne_t, p):
     import paper_2311_17500_b200 as mb
     from oracle import assembly as oasm
-    st, ost = _spaces(nes, ne_t)
+    st, ost = _spaces(nes, ne_t, p)
     T, D = 1.3, 2e-2
     rng = np.random.default_rng(sum(nes) + ne_t)
     N = st.num_dof
@@ -51,10 +55,11 @@ def test_reaction_ws_matches_oracle_and_tile_kernel(nes, ne_t):
     assert np.array_equal(_mr(op, x, 1), _mr(op, x, 1))
 
 
-def test_reaction_ws_with_lift_matches_tile_kernel():
+@PS
+def test_reaction_ws_with_lift_matches_tile_kernel(p):
     """The lifted slab (row -1) of u and of x (mi_op_apply_lift) enters through the producers' copies."""
     import paper_2311_17500_b200 as mb
-    st, _ = _spaces((5, 6, 3), 5)
+    st, _ = _spaces((5, 6, 3), 5, p)
     rng = np.random.default_rng(3)
     N, ns = st.num_dof, st.num_space
     u, w, x = rng.uniform(0, 1, N), rng.uniform(0, 0.1, N), rng.uniform(-1, 1, N)
@@ -70,11 +75,12 @@ def test_reaction_ws_with_lift_matches_tile_kernel():
     assert rel(out[1][1], out[0][1]) < 1e-13
 
 
-def test_reaction_ws_on_time_row_slabs():
+@PS
+def test_reaction_ws_on_time_row_slabs(p):
     """Time-row slabs (KroneckerOperator(time_rows=...)): rows outside the slab are zero slabs."""
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200 import _lib
-    st, _ = _spaces((4, 5, 3), 9)
+    st, _ = _spaces((4, 5, 3), 9, p)
     rng = np.random.default_rng(5)
     N, ns, nt = st.num_dof, st.num_space, st.num_time
     u, w, x = rng.uniform(0, 1, N), rng.uniform(0, 0.1, N), rng.uniform(-1, 1, N)
@@ -89,17 +95,17 @@ def test_reaction_ws_on_time_row_slabs():
     assert rel(ys[1], ys[0]) < 1e-13
 
 
-def test_reaction_ws_on_z_slab():
+@PS
+def test_reaction_ws_on_z_slab(p):
     """The z-slab operator of the space-sharded solve: the reaction runs on the input slab (owned planes
     + halos) and only the owned planes are kept."""
     import paper_2311_17500_b200 as mb
     from paper_2311_17500_b200 import _lib
-    st, _ = _spaces((4, 4, 9), 4)
+    st, _ = _spaces((4, 4, 9), 4, p)
     rng = np.random.default_rng(8)
     n1, n2, n3 = (s.dimension for s in st.spatial)
     nt = st.num_time
     z_lo, z_hi = 4, 8
-    p = 3
     h_lo, h_hi = min(p, z_lo), min(p, n3 - z_hi)
     nin = (z_hi + h_hi - (z_lo - h_lo)) * n1 * n2
     u, w, x = (rng.uniform(0, 1, nt * nin), rng.uniform(0, 0.1, nt * nin), rng.uniform(-1, 1, nt * nin))
