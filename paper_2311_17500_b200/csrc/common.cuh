@@ -120,6 +120,7 @@ struct mi_ctx {
   bool rx_mapped = false;
   mi::DeviceBuf rx_cw;          // stored C_r x spatial weight at every Gauss point (reaction.cu RX_STORED)
   bool rx_cw_ok = false, rx_cw_dirty = true;
+  bool rx_cw_ws = false;        // rx_cw is in reaction_ws's layout (else reaction_tile's)
   int rx_store_mode = -1;       // -1 auto (fits in 40% of free memory), 0 off, 1 on
   int rx_kernel = -1;           // fused mode: -1 auto (reaction_ws where it applies), 0 reaction_tile, 1 reaction_ws
 

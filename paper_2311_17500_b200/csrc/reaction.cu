@@ -536,6 +536,11 @@ static bool use_reaction_ws(const mi_ctx* c) {
   return can && (c->rx_kernel == 1 || (c->rx_kernel < 0 && on));
 }
 
+template <int MODE>
+static int reaction_ws_mode(mi_ctx* c, RxArgs r) {
+  return c->p == 3 ? reaction_ws_launch<3, MODE>(c, r) : reaction_ws_launch<2, MODE>(c, r);
+}
+
 // y[t, owned planes] += y_in[t, same planes of the input slab] (z-slab contexts)
 __global__ void add_owned_planes(double* __restrict__ y, const double* __restrict__ yin, long long ns,
                                  long long ns_in, long long off, int nt) {
@@ -607,6 +612,12 @@ static int reaction_launch(mi_ctx* c, RxArgs r) {
 // bytes of the stored weighted coefficient c_w for this context (0: dims unsupported)
 static size_t reaction_store_bytes(const mi_ctx* c) {
   size_t out = 0;
+  if (use_reaction_ws(c)) {
+    // reaction_ws: [tile (2 x 4 x 2 elements)][time element][g][8 E1 QE... valid Gauss points]
+    const size_t qe = (size_t)c->p + 1, e2 = MI_RXWS_E2(c->p);
+    size_t tiles = ((c->rx_nel[0] + 1) / 2) * (size_t)((c->rx_nel[1] + e2 - 1) / e2) * ((c->rx_nel[2] + 1) / 2);
+    return tiles * c->rx_nel[3] * qe * (2 * qe) * (e2 * qe) * (2 * qe) * sizeof(double);
+  }
   auto one = [&](auto dv, auto pv) {
     constexpr int D_ = decltype(dv)::value, P_ = decltype(pv)::value;
     using G = RxTile<D_, P_>;
@@ -645,7 +656,8 @@ static int reaction_prepare_store(mi_ctx* c) {
   RxArgs r{};
   fill_args(c, r);
   r.cw = c->rx_cw.p;
-  if ((rc = reaction_launch<RX_PRE>(c, r))) return rc;
+  c->rx_cw_ws = use_reaction_ws(c);
+  if ((rc = c->rx_cw_ws ? reaction_ws_mode<RX_PRE>(c, r) : reaction_launch<RX_PRE>(c, r))) return rc;
   c->rx_cw_ok = true;
   return MI_OK;
 }
@@ -670,9 +682,8 @@ int reaction_apply(mi_ctx* c, const double* x, double* y, const double* x0) {
   r.x = x;
   r.lift_x = x0;
   r.y = slab ? c->y_in.p : y;
-  int rc = c->rx_cw_ok ? reaction_launch<RX_STORED>(c, r)
-                        : (use_reaction_ws(c) ? (c->p == 3 ? reaction_ws_launch<3>(c, r) : reaction_ws_launch<2>(c, r))
-                                              : reaction_launch<RX_FUSED>(c, r));
+  int rc = c->rx_cw_ok ? (c->rx_cw_ws ? reaction_ws_mode<RX_STORED>(c, r) : reaction_launch<RX_STORED>(c, r))
+                        : (use_reaction_ws(c) ? reaction_ws_mode<RX_FUSED>(c, r) : reaction_launch<RX_FUSED>(c, r));
   if (rc) return rc;
   if (slab) {
     dim3 g((unsigned)((c->ns + 255) / 256), c->nt);
@@ -775,6 +786,7 @@ int mi_op_set_reaction_kernel(mi_ctx* c, int kernel) {
   MI_REQUIRE(kernel != 1 || (c->d == 3 && (c->p == 3 || c->p == 2) && c->pt == c->p), MI_ERR_ARG,
              "reaction_ws serves d = 3, p = p_t in {2, 3} only");
   c->rx_kernel = kernel;
+  c->rx_cw_dirty = true;          // the stored coefficient's layout follows the kernel
   return MI_OK;
 }
 

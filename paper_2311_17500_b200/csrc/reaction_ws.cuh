@@ -19,19 +19,26 @@
 // writer per launch, as in reaction_tile: deterministic sums.
 #pragma once
 
+#ifndef MI_RXWS_E2
+#define MI_RXWS_E2(p) ((p) == 2 ? 8 : 4)
+#endif
+
 namespace mi {
 
-template <int P_>
+// MODE: RX_FUSED interpolates u, w, x and forms C_r every apply; RX_PRE (u, w) evaluates the weighted
+// coefficient c_w = C_r w_x once per operator build into HBM; RX_STORED (x) applies M_R with it.
+template <int P_, int MODE_>
 struct RxWS {
-  static constexpr int P = P_, QE = P + 1, PW = P + 1, QT = P + 1, NF = 3;
-  static constexpr int E1 = 2, E2 = 4, E3 = 2;
+  static constexpr int P = P_, QE = P + 1, PW = P + 1, QT = P + 1;
+  static constexpr int MODE = MODE_, NF = MODE == RX_FUSED ? 3 : (MODE == RX_PRE ? 2 : 1);
+  static constexpr int E1 = 2, E2 = MI_RXWS_E2(P), E3 = 2;          // p = 2: a longer tile, more work per slice step
   static constexpr int L1 = E1 + P, L2 = E2 + P, L3 = E3 + P;          // p = 3: 5, 7, 5 functions
   static constexpr int Q1 = E1 * QE, Q2 = E2 * QE, Q3 = E3 * QE;       // p = 3: 8, 16, 8 Gauss points
   static constexpr int RC1 = (L1 + E1 - 1) / E1, RC2 = (L2 + E2 - 1) / E2, RC3 = (L3 + E3 - 1) / E3;   // 3, 2, 3
   static constexpr int LS = L1 * L2 * L3;                               // functions per slice and field
   static constexpr int QL = Q1 * Q2;                                    // (q2, q1) lines of the z stage
   static constexpr int NT = (QL + 7) / 8;                               // their 8-line tiles: 16 (p = 3), 9 (p = 2)
-  static constexpr int NCW = NT <= 9 ? NT : 8;                          // consumer warps
+  static constexpr int NCW = NT % 9 == 0 ? 9 : 8;                       // consumer warps
   static constexpr int MT = (NT + NCW - 1) / NCW;                       // line tiles per consumer warp
   static constexpr int NPW = 12 - NCW, NCT = 32 * NCW, NPT = 32 * NPW, NTH = NCT + NPT;
   static constexpr bool REGSPLIT = NCW % 4 == 0 && NPW % 4 == 0;       // setmaxnreg works on groups of 4 warps
@@ -45,6 +52,7 @@ struct RxWS {
   static_assert(R1 == 0 || R1 == 1, "x / z interpolation: one k-step plus at most one rank-1 update");
   static constexpr int KY = (L2 + 3) / 4, NY = (Q2 + 7) / 8;           // y interpolation k-steps / N tiles
   static constexpr int KZP = (Q3 + 3) / 4, KYP = (Q2 + 3) / 4, KXP = (Q1 + 3) / 4;   // projection k-steps
+  static constexpr int NYP = (L2 + 7) / 8;                              // N tiles of the y projection
   // shared-memory strides (doubles), chosen so the DMMA operand loads / accumulator stores of the
   // p = 3 shapes touch each bank pair exactly twice (p = 2 keeps dense rows: a few 3-way conflicts)
   static constexpr int IS1 = P == 3 ? 6 : L1;                           // sIn rows
@@ -58,8 +66,14 @@ struct RxWS {
   static constexpr int SC = L3 * CS;                                    // x2 buffers
   static constexpr int SD = L3 * L2 * DS1 + 96;                         // + over-read pad
   static constexpr int SBT = NCW * 64;                                  // per consumer warp [2][32] time tables
-  static constexpr int NDBL = 2 * SIN + SA + 2 * SB + 2 * SC + SD + SBT + (SIN + SD + SBT) % 2;
-  static constexpr size_t SMEM = (size_t)NDBL * 8 + 8 * 8;              // + 8 mbarriers
+  // RX_STORED: the c_w block of one (tile, time element), [g][line][q3], streams through a ring of
+  // NSW stages (one bulk copy per element, issued NSW - 1 elements ahead by a producer thread)
+  static constexpr int NSW = 4, CWB = QT * QL * Q3;
+  static constexpr int SW = MODE == RX_STORED ? NSW * CWB : 0;
+  static constexpr int NDBL0 = 2 * SIN + SA + 2 * SB + 2 * SC + SD + SBT;
+  static constexpr int NDBL = NDBL0 + NDBL0 % 2 + SW;                   // the ring starts 16-byte aligned
+  static constexpr size_t SMEM = (size_t)NDBL * 8 + (8 + 2 * NSW) * 8;  // + mbarriers
+  static_assert(CWB % 2 == 0 && SMEM <= 227 * 1024, "c_w ring");
   static_assert(BJ % 16 == 8 && CS % 8 == 4 && (2 * SIN) % 2 == 0 && SA % 2 == 0, "padding");
   // tiles of the producer stages
   static constexpr int XI_T = (NF * L3 * L2 + 7) / 8, YI_T = (NF * L3 * Q1 + 7) / 8;
@@ -94,9 +108,9 @@ __device__ __forceinline__ void rxws_bar_producers() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NPT) : "memory");
 }
 
-template <int P_>
-__global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
-  using G = RxWS<P_>;
+template <int P_, int MODE>
+__global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) {
+  using G = RxWS<P_, MODE>;
   constexpr int P = G::P, QE = G::QE, PW = G::PW, QT = G::QT, NF = G::NF, PT = G::P;
   constexpr int L1 = G::L1, L2 = G::L2, L3 = G::L3, Q1 = G::Q1, Q2 = G::Q2;
   constexpr int BS1 = G::BS1, BJ = G::BJ, CS = G::CS, IS1 = G::IS1, DS1 = G::DS1, MT = G::MT, R1 = G::R1;
@@ -109,6 +123,8 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
   double* sBt = sD + G::SD;         // [warp][2][32] time tables
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + G::NDBL);
   unsigned long long *fullB = bars, *emptyB = bars + 2, *fullC = bars + 4, *emptyC = bars + 6;
+  [[maybe_unused]] unsigned long long *fullW = bars + 8, *emptyW = bars + 8 + G::NSW;
+  [[maybe_unused]] double* sW = sm + (G::NDBL - G::SW);     // RX_STORED: c_w ring
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   // A-fragment loads run unpredicated over padded rows / k columns: whatever they read is finite (the
@@ -120,6 +136,12 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
       mbar_init(&emptyB[b], G::NCT);
       mbar_init(&fullC[b], G::NCT);
       mbar_init(&emptyC[b], G::NPT);
+    }
+    if constexpr (MODE == RX_STORED) {
+      for (int b = 0; b < G::NSW; ++b) {
+        mbar_init(&fullW[b], 1);
+        mbar_init(&emptyW[b], G::NCT);
+      }
     }
     mbar_fence_init();
   }
@@ -148,6 +170,12 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
   };
   const int nelt = r.nel[3];
   const int nfull = nelt + PT;                       // full-basis time functions
+  // c_w store: [tile][time element][g][line][q3], valid Gauss points only
+  [[maybe_unused]] long long cw_tile = 0;
+  if constexpr (MODE != RX_FUSED) {
+    const long long nt1 = (r.nel[0] + G::E1 - 1) / G::E1, nt2 = (r.nel[1] + G::E2 - 1) / G::E2;
+    cw_tile = (((long long)(k[2] / G::E3) * nt2 + k[1] / G::E2) * nt1 + k[0] / G::E1) * nelt;
+  }
   __syncthreads();
 
   if (warp < G::NCW) {
@@ -189,6 +217,12 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
         for (int f = 0; f < NF; ++f) X[mi][a][f][0] = X[mi][a][f][1] = 0.0;
         Y[mi][a][0] = Y[mi][a][1] = 0.0;
       }
+    // a thread's two points of a line tile are one aligned double2 of the c_w block
+    constexpr int Q3 = G::Q3;
+    [[maybe_unused]] const bool cw_lane = 2 * fk < Q3;
+    [[maybe_unused]] auto cw_ptr = [&](int et, int g, int mi) -> double* {
+      return r.cw + ((cw_tile + et) * QT + g) * (long long)(G::QL * Q3) + (8 * (warp + G::NCW * mi) + fr) * Q3 + 2 * fk;
+    };
     double* myBt = sBt + warp * 64;
     const double* sBme = sB + loff0 + fk * BJ;       // this lane's DMMA operand column of buffer 0, function R1
     // time tables of element et: lanes 0-15 the basis values (interpolation), lanes 16-31 the same
@@ -215,13 +249,34 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
     auto step = [&](auto phc, int j) {
       constexpr int PH = decltype(phc)::value, SZ = (PH + PW - 1) % PW;
       const int et = j - PW, fz = et - 1;
-      const bool has_in = j < nfull, has_fz = fz >= 0;     // fz < nfull by the loop bound
+      const bool has_in = j < nfull, has_fz = MODE != RX_PRE && fz >= 0;     // fz < nfull by the loop bound
       const int bb = j & 1, cb = fz & 1;
       myBt[bb * 32 + lane] = btb * btw;
       __syncwarp();
       prefetch_bt(et + 1);
       if (has_in) mbar_wait(&fullB[bb], (unsigned)((j >> 1) & 1));
-      if (fz >= 2) mbar_wait(&emptyC[cb], (unsigned)(((fz >> 1) - 1) & 1));
+      if (MODE != RX_PRE && fz >= 2) mbar_wait(&emptyC[cb], (unsigned)(((fz >> 1) - 1) & 1));
+      // ---- RX_STORED: this element's c_w from the ring
+      [[maybe_unused]] double2 cwl[QT][MT];
+      if constexpr (MODE == RX_STORED) {
+#pragma unroll
+        for (int g = 0; g < QT; ++g)
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) cwl[g][mi] = make_double2(0.0, 0.0);
+        if (et >= 0 && et < nelt) {
+          const int sw = et % G::NSW;
+          mbar_wait(&fullW[sw], (unsigned)((et / G::NSW) & 1));
+          if (cw_lane) {
+            const double* blk = sW + sw * G::CWB + (8 * warp + fr) * Q3 + 2 * fk;
+#pragma unroll
+            for (int g = 0; g < QT; ++g)
+#pragma unroll
+              for (int mi = 0; mi < MT; ++mi)
+                cwl[g][mi] = *reinterpret_cast<const double2*>(blk + g * (G::QL * Q3) + 8 * G::NCW * mi * Q3);
+          }
+          mbar_arrive(&emptyW[sw]);
+        }
+      }
       // ---- z interpolation of slice j
       const double* fin = sBme + bb * G::SB;
       double zc[MT][NF][2], a0[MT][NF], za[MT][NF];
@@ -253,7 +308,7 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
           rxws_cdmma(zc[mi][f][0], zc[mi][f][1], za[mi][f], bI1);
         }
 #pragma unroll
-      for (int ks = 0; ks < G::KZP; ++ks)
+      for (int ks = 0; ks < (MODE == RX_PRE ? 0 : G::KZP); ++ks)
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi) {
           const int cc = 4 * ks + fk, src = (lane & ~3) | ((cc >> 1) & 3);
@@ -265,35 +320,50 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
       if (!(MI_RXWS_ABL & 1)) {
 #pragma unroll
         for (int g = 0; g < QT; ++g) {
-          double uu[MT][2], ww[MT][2], xx[MT][2];
+          double acc[MT][NF][2];                     // fused: (u', p, x'); pre: (u', p); stored: (x)
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) uu[mi][e] = ww[mi][e] = xx[mi][e] = 0.0;
+            for (int f = 0; f < NF; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
 #pragma unroll
           for (int a = 0; a < PW; ++a) {
             const double ba = btv[0][g * PW + a];
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                uu[mi][e] = fma(ba, X[mi][(PH + a) % PW][0][e], uu[mi][e]);
-                ww[mi][e] = fma(ba, X[mi][(PH + a) % PW][1][e], ww[mi][e]);
-                xx[mi][e] = fma(ba, X[mi][(PH + a) % PW][2][e], xx[mi][e]);
-              }
+              for (int f = 0; f < NF; ++f)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) acc[mi][f][e] = fma(ba, X[mi][(PH + a) % PW][f][e], acc[mi][f][e]);
           }
-          double v[MT][2];                           // C_r x w_x = (u'^2 + p) x'
+          if constexpr (MODE == RX_PRE) {
+            // c_w = C_r w_x = (u'^2 + p) w_x at the thread's points of this (element, g)
+            if (et >= 0 && et < nelt && cw_lane) {
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi)
+              for (int mi = 0; mi < MT; ++mi)
+                *reinterpret_cast<double2*>(cw_ptr(et, g, mi)) =
+                    make_double2(fma(acc[mi][0][0], acc[mi][0][0], acc[mi][1][0]) * wsp[mi][0],
+                                 fma(acc[mi][0][1], acc[mi][0][1], acc[mi][1][1]) * wsp[mi][1]);
+            }
+          } else {
+            double v[MT][2];                         // C_r w_x x
 #pragma unroll
-            for (int e = 0; e < 2; ++e) v[mi][e] = fma(uu[mi][e], uu[mi][e], ww[mi][e]) * xx[mi][e];
+            for (int mi = 0; mi < MT; ++mi) {
+              if constexpr (MODE == RX_FUSED) {
+                v[mi][0] = fma(acc[mi][0][0], acc[mi][0][0], acc[mi][1][0]) * acc[mi][2][0];
+                v[mi][1] = fma(acc[mi][0][1], acc[mi][0][1], acc[mi][1][1]) * acc[mi][2][1];
+              } else {
+                v[mi][0] = cwl[g][mi].x * acc[mi][0][0];
+                v[mi][1] = cwl[g][mi].y * acc[mi][0][1];
+              }
+            }
 #pragma unroll
-          for (int a = 0; a < PW; ++a) {
-            const double bw = btv[1][g * PW + a];
+            for (int a = 0; a < PW; ++a) {
+              const double bw = btv[1][g * PW + a];
 #pragma unroll
-            for (int mi = 0; mi < MT; ++mi)
+              for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) Y[mi][(PH + a) % PW][e] = fma(bw, v[mi][e], Y[mi][(PH + a) % PW][e]);
+                for (int e = 0; e < 2; ++e) Y[mi][(PH + a) % PW][e] = fma(bw, v[mi][e], Y[mi][(PH + a) % PW][e]);
+            }
           }
         }
       }
@@ -305,12 +375,16 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
       for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const double cu = R1 ? fma(a0[mi][0], bI0[e], zc[mi][0][e]) : zc[mi][0][e],
-                       cw = R1 ? fma(a0[mi][1], bI0[e], zc[mi][1][e]) : zc[mi][1][e],
-                       cx = R1 ? fma(a0[mi][2], bI0[e], zc[mi][2][e]) : zc[mi][2][e];
-          X[mi][PH][0][e] = cu * rsq;
-          X[mi][PH][1][e] = fma(cu, rk1, fma(cw, rc2, rk0));
-          X[mi][PH][2][e] = cx * wsp[mi][e];
+          double cf[NF];
+#pragma unroll
+          for (int f = 0; f < NF; ++f) cf[f] = R1 ? fma(a0[mi][f], bI0[e], zc[mi][f][e]) : zc[mi][f][e];
+          if constexpr (MODE == RX_STORED) {
+            X[mi][PH][0][e] = cf[0];                 // x alone: the weight is in c_w
+          } else {
+            X[mi][PH][0][e] = cf[0] * rsq;
+            X[mi][PH][1][e] = fma(cf[0], rk1, fma(cf[1], rc2, rk0));
+            if constexpr (MODE == RX_FUSED) X[mi][PH][2][e] = cf[2] * wsp[mi][e];
+          }
         }
       // ---- projected function fz to the producers
       if (has_fz) {
@@ -337,7 +411,7 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
     if constexpr (G::REGSPLIT) rxws_reg_dec<MI_RXWS_REGP>();
     constexpr int NPW = G::NPW, NPT = G::NPT;
     const int p = tid - G::NCT, pw = warp - G::NCW;
-    double bIy[G::NY][G::KY], bPy[G::KYP], bPx[G::KXP];
+    double bIy[G::NY][G::KY], bPy[G::NYP][G::KYP], bPx[G::KXP];
     const double bIx1 = basis(0, R1 + fk, fr);
     const double bIx0[2] = {R1 ? basis(0, 0, 2 * fk) : 0.0, R1 ? basis(0, 0, 2 * fk + 1) : 0.0};
 #pragma unroll
@@ -347,7 +421,9 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
 #pragma unroll
       for (int n2 = 0; n2 < G::NY; ++n2) bIy[n2][ks] = basis(1, 4 * ks + fk, 8 * n2 + fr);
 #pragma unroll
-    for (int ks = 0; ks < G::KYP; ++ks) bPy[ks] = basis(1, fr, 4 * ks + fk);
+    for (int ks = 0; ks < G::KYP; ++ks)
+#pragma unroll
+      for (int n2 = 0; n2 < G::NYP; ++n2) bPy[n2][ks] = basis(1, 8 * n2 + fr, 4 * ks + fk);
     const long long ns = r.ns;
     // spatial indices fit in 32 bits (the launcher checks N_s < 2^31)
     auto spatial = [&](int j3, int j2, int j1, bool& ok) -> int {
@@ -380,33 +456,34 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
       const int ct = ft + r.rowoff;
       const unsigned boff = (unsigned)((ft & 1) * G::SIN * 8);
       constexpr unsigned FO = L3 * L2 * IS1 * 8;     // field stride in sIn (bytes)
+      // fields of this mode: fused (u, w, x), pre (u, w), stored (x)
+      const double* fld[3] = {MODE == RX_STORED ? r.x : r.u, r.w, r.x};
+      const double* lft[3] = {MODE == RX_STORED ? r.lift_x : r.lift_u, nullptr, r.lift_x};
       if (ct >= 0 && ct < r.ntc) {
         const long long off = (long long)ct * ns;
-        const double *ru = r.u + off, *rw = r.w + off, *rx = r.x + off;
 #pragma unroll
         for (int h = 0; h < G::NIT; ++h) {
           if (gsp[h] != -2) {
             const bool v = gsp[h] >= 0;
             const int g = v ? gsp[h] : 0;
             const unsigned d = sdst[h] + boff;
-            put(d, ru + g, v);
-            put(d + FO, rw + g, v);
-            put(d + 2 * FO, rx + g, v);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) put(d + f * FO, fld[f] + off + g, v);
           }
         }
       } else {
         // the lifted slab (row -1: u and x from the lift, if set) or a row outside this context: zeros
-        const double* lu = ct == -1 ? r.lift_u : nullptr;
-        const double* lx = ct == -1 ? r.lift_x : nullptr;
 #pragma unroll
         for (int h = 0; h < G::NIT; ++h) {
           if (gsp[h] != -2) {
             const bool v = gsp[h] >= 0;
             const int g = v ? gsp[h] : 0;
             const unsigned d = sdst[h] + boff;
-            put(d, lu + g, v && lu != nullptr);
-            put(d + FO, nullptr, false);
-            put(d + 2 * FO, lx + g, v && lx != nullptr);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              const double* l = ct == -1 ? lft[f] : nullptr;
+              put(d + f * FO, l + g, v && l != nullptr);
+            }
           }
         }
       }
@@ -425,11 +502,24 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
         yidx[u][e] = ok ? gs : -1;
       }
     issue(0);
+    [[maybe_unused]] int e_next = 0;                 // RX_STORED: next c_w block to request
     for (int i = 0; i <= nfull + PW + 1; ++i) {
+      if constexpr (MODE == RX_STORED) {
+        // c_w blocks NSW - 1 elements ahead of the consumers (who are on element i - 1 - PW); a stage is
+        // free once they have read element e - NSW, which they did steps ago
+        if (p == 0) {
+          for (; e_next < nelt && e_next <= i - PW + G::NSW - 2; ++e_next) {
+            const int sw = e_next % G::NSW, kuse = e_next / G::NSW;
+            if (kuse >= 1) mbar_wait(&emptyW[sw], (unsigned)((kuse - 1) & 1));
+            mbar_expect_tx(&fullW[sw], (unsigned)(G::CWB * 8));
+            bulk_g2s(sW + sw * G::CWB, r.cw + (cw_tile + e_next) * (long long)G::CWB, (unsigned)(G::CWB * 8), &fullW[sw]);
+          }
+        }
+      }
       const bool has_in = i < nfull;
       const int fq = i - PW - 2;                     // function whose y / x projections run now (its z
                                                      // projection ended with consumer step i - 1)
-      const bool has_fq = fq >= 0 && fq < nfull;
+      const bool has_fq = MODE != RX_PRE && fq >= 0 && fq < nfull;
       cp_async_wait<0>();                            // this thread's copies of slice i have landed ...
       rxws_bar_producers<NPT>();                     // ... and everyone's; the other sIn buffer is free
       if (i + 1 < nfull) issue(i + 1);
@@ -505,26 +595,34 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
         mbar_wait(&fullC[cb], (unsigned)((fq >> 1) & 1));
         const double* in = sC + cb * G::SC;
         constexpr int NL = L3 * Q1;
-        double c[G::YP_U][2];
+        double c[G::YP_U][G::NYP][2];
         int j3[G::YP_U], q1[G::YP_U];
 #pragma unroll
         for (int u = 0; u < G::YP_U; ++u) {
-          c[u][0] = c[u][1] = 0.0;
+#pragma unroll
+          for (int n2 = 0; n2 < G::NYP; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
           const int mt = pw + NPW * u, line = 8 * mt + fr;
           j3[u] = Q1 == 8 ? mt : line / Q1, q1[u] = Q1 == 8 ? fr : line % Q1;
           if (mt < G::YP_T) {
 #pragma unroll
-            for (int ks = 0; ks < G::KYP; ++ks)
-              rxws_pdmma(c[u][0], c[u][1], in[j3[u] * CS + (4 * ks + fk) * Q1 + q1[u]], bPy[ks]);
+            for (int ks = 0; ks < G::KYP; ++ks) {
+              const double av = in[j3[u] * CS + (4 * ks + fk) * Q1 + q1[u]];
+#pragma unroll
+              for (int n2 = 0; n2 < G::NYP; ++n2) rxws_pdmma(c[u][n2][0], c[u][n2][1], av, bPy[n2][ks]);
+            }
           }
         }
         mbar_arrive(&emptyC[cb]);
 #pragma unroll
         for (int u = 0; u < G::YP_U; ++u) {
-          const int line = 8 * (pw + NPW * u) + fr, n0 = 2 * fk;
+          const int line = 8 * (pw + NPW * u) + fr;
           if (line < NL) {
-            if (n0 < L2) sD[(j3[u] * L2 + n0) * DS1 + q1[u]] = c[u][0];
-            if (n0 + 1 < L2) sD[(j3[u] * L2 + n0 + 1) * DS1 + q1[u]] = c[u][1];
+#pragma unroll
+            for (int n2 = 0; n2 < G::NYP; ++n2) {
+              const int n0 = 8 * n2 + 2 * fk;
+              if (n0 < L2) sD[(j3[u] * L2 + n0) * DS1 + q1[u]] = c[u][n2][0];
+              if (n0 + 1 < L2) sD[(j3[u] * L2 + n0 + 1) * DS1 + q1[u]] = c[u][n2][1];
+            }
           }
         }
       }
@@ -554,12 +652,12 @@ __global__ void __launch_bounds__(RxWS<P_>::NTH, 1) reaction_ws(RxArgs r) {
 }
 
 // all colour classes of the warp-specialised kernel (d = 3, p = p_t, fused mode)
-template <int P_>
+template <int P_, int MODE>
 static int reaction_ws_launch(mi_ctx* c, RxArgs r) {
-  using G = RxWS<P_>;
+  using G = RxWS<P_, MODE>;
   MI_DEV_FLAG(attr);
   if (!attr) {
-    MI_CUDA(cudaFuncSetAttribute(reaction_ws<P_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    MI_CUDA(cudaFuncSetAttribute(reaction_ws<P_, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
     attr = true;
   }
   const int EL[3] = {G::E1, G::E2, G::E3}, RCL[3] = {G::RC1, G::RC2, G::RC3};
@@ -574,7 +672,7 @@ static int reaction_ws_launch(mi_ctx* c, RxArgs r) {
       nb *= r.ncol[l] > 0 ? r.ncol[l] : 0;
     }
     if (nb == 0) continue;
-    reaction_ws<P_><<<(unsigned)nb, G::NTH, G::SMEM, c->stream>>>(r);
+    reaction_ws<P_, MODE><<<(unsigned)nb, G::NTH, G::SMEM, c->stream>>>(r);
     MI_CHECK_LAUNCH("reaction_ws");
   }
   return MI_OK;

@@ -24,10 +24,11 @@ def _spaces(nes, ne_t, p=3):
 PS = pytest.mark.parametrize("p", [2, 3])
 
 
-def _mr(op, x, kernel):
-    """M_R x alone: the operator with the reaction minus the same operator without it."""
+def _mr(op, x, kernel, store=0):
+    """A x with the reaction evaluated by the given kernel (0 reaction_tile, 1 reaction_ws) in the fused
+    (store 0) or the stored-coefficient mode (store 1)."""
     from paper_2311_17500_b200 import _lib
-    _lib.call("mi_op_set_reaction_store", op.ctx.handle, 0)
+    _lib.call("mi_op_set_reaction_store", op.ctx.handle, store)
     _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
     return op.matvec(x)
 
@@ -51,6 +52,11 @@ def test_reaction_ws_matches_oracle_and_tile_kernel(nes, ne_t, p):
     assert rel(y_ws, y_ref) < 1e-12
     assert rel(y_tile, y_ref) < 1e-12
     assert rel(y_ws, y_tile) < 1e-13
+    # the stored-coefficient mode of both kernels (c_w written once by the kernel's own RX_PRE pass)
+    for kernel in (0, 1):
+        y_st = _mr(op, x, kernel, store=1) - y0
+        assert rel(y_st, y_ref) < 1e-12
+        assert rel(_mr(op, x, kernel, store=1) - y0, y_st) == 0.0      # a second apply reuses c_w
     # repeated applies are bitwise identical (one writer per entry per colour launch)
     assert np.array_equal(_mr(op, x, 1), _mr(op, x, 1))
 
@@ -66,13 +72,15 @@ def test_reaction_ws_with_lift_matches_tile_kernel(p):
     lift = rng.uniform(0, 1, ns)
     op = mb.KroneckerOperator(st, 0.9, 1.0, 1e-2, RM, u=u, w=w, lift=lift)
     from paper_2311_17500_b200 import _lib
-    _lib.call("mi_op_set_reaction_store", op.ctx.handle, 0)
     out = {}
-    for kernel in (0, 1):
-        _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
-        out[kernel] = (op.matvec(x), op.lift_apply().cpu().numpy())
-    assert rel(out[1][0], out[0][0]) < 1e-13
-    assert rel(out[1][1], out[0][1]) < 1e-13
+    for store in (0, 1):
+        _lib.call("mi_op_set_reaction_store", op.ctx.handle, store)
+        for kernel in (0, 1):
+            _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
+            out[store, kernel] = (op.matvec(x), op.lift_apply().cpu().numpy())
+    for key in ((0, 1), (1, 0), (1, 1)):
+        assert rel(out[key][0], out[0, 0][0]) < 1e-13
+        assert rel(out[key][1], out[0, 0][1]) < 1e-13
 
 
 @PS
@@ -87,12 +95,14 @@ def test_reaction_ws_on_time_row_slabs(p):
     r0, r1 = 3, 8
     sl = slice(r0 * ns, r1 * ns)
     op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-2, RM, u=u[sl], w=w[sl], time_rows=(r0, r1))
-    _lib.call("mi_op_set_reaction_store", op.ctx.handle, 0)
     ys = []
-    for kernel in (0, 1):
-        _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
-        ys.append(op.matvec(x[sl]))
-    assert rel(ys[1], ys[0]) < 1e-13
+    for store in (0, 1):
+        _lib.call("mi_op_set_reaction_store", op.ctx.handle, store)
+        for kernel in (0, 1):
+            _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
+            ys.append(op.matvec(x[sl]))
+    for y in ys[1:]:
+        assert rel(y, ys[0]) < 1e-13
 
 
 @PS
@@ -110,12 +120,14 @@ def test_reaction_ws_on_z_slab(p):
     nin = (z_hi + h_hi - (z_lo - h_lo)) * n1 * n2
     u, w, x = (rng.uniform(0, 1, nt * nin), rng.uniform(0, 0.1, nt * nin), rng.uniform(-1, 1, nt * nin))
     op = mb.KroneckerOperator(st, 1.0, 1.0, 1e-2, RM, u=u, w=w, z_planes=(z_lo, z_hi))
-    _lib.call("mi_op_set_reaction_store", op.ctx.handle, 0)
     ys = []
-    for kernel in (0, 1):
-        _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
-        ys.append(op.matvec(x))
-    assert rel(ys[1], ys[0]) < 1e-13
+    for store in (0, 1):
+        _lib.call("mi_op_set_reaction_store", op.ctx.handle, store)
+        for kernel in (0, 1):
+            _lib.call("mi_op_set_reaction_kernel", op.ctx.handle, kernel)
+            ys.append(op.matvec(x))
+    for y in ys[1:]:
+        assert rel(y, ys[0]) < 1e-13
 
 
 def test_reaction_kernel_selector_rejects_unsupported_shapes():
