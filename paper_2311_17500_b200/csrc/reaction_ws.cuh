@@ -19,6 +19,9 @@
 // writer per launch, as in reaction_tile: deterministic sums.
 #pragma once
 
+#ifndef MI_RXWS_ST6
+#define MI_RXWS_ST6 1
+#endif
 #ifndef MI_RXWS_E2
 #define MI_RXWS_E2(p) ((p) == 2 ? 8 : 4)
 #endif
@@ -38,7 +41,9 @@ struct RxWS {
   static constexpr int LS = L1 * L2 * L3;                               // functions per slice and field
   static constexpr int QL = Q1 * Q2;                                    // (q2, q1) lines of the z stage
   static constexpr int NT = (QL + 7) / 8;                               // their 8-line tiles: 16 (p = 3), 9 (p = 2)
-  static constexpr int NCW = NT % 9 == 0 ? 9 : 8;                       // consumer warps
+  // consumer warps (the rest of the 12 produce).  The stored mode's consumers have little to do per
+  // slice (one field, no C_r): p = 2 gives half of the warps to the producers there
+  static constexpr int NCW = NT % 9 == 0 ? ((MODE == RX_STORED && NT == 18 && MI_RXWS_ST6) ? 6 : 9) : 8;
   static constexpr int MT = (NT + NCW - 1) / NCW;                       // line tiles per consumer warp
   static constexpr int NPW = 12 - NCW, NCT = 32 * NCW, NPT = 32 * NPW, NTH = NCT + NPT;
   static constexpr bool REGSPLIT = NCW % 4 == 0 && NPW % 4 == 0;       // setmaxnreg works on groups of 4 warps
