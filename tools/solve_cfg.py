@@ -67,6 +67,7 @@ def run(cfg=None, stab="spline_upwind", max_it=100, device=0, stimulus="u0", **k
                         spec.get("stim", 0.1), spec.get("corner", False), stimulus)
     config = mb.FixedPointConfig(stabilization=stab, linear_solver="iterative", linear_tol=1e-8,
                                  max_iterations=max_it)
+    torch.cuda.empty_cache()      # earlier workloads of the process leave no cached blocks to fragment around
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = mb.fixed_point_solve(prob, config, device=device)
