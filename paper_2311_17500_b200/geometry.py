@@ -18,6 +18,23 @@ reference assembles N_s x N_s CSR matrices instead.
 
 import numpy as np
 
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _einsum(expr, *ops):
+    """np.einsum for per-Gauss-point small-tensor contractions over millions of points: numpy's c_einsum
+    is single-threaded there (0.2 s a call at 128^3 points), so on a CUDA machine the contraction runs
+    through torch on the device and comes back as numpy (setup data; the values agree to rounding)."""
+    import torch
+    if torch.cuda.is_available() and max(np.asarray(o).size for o in ops) >= (1 << 16):
+        dev = torch.device("cuda", torch.cuda.current_device())
+        out = torch.einsum(expr, *[torch.as_tensor(np.ascontiguousarray(o), device=dev) for o in ops])
+        return out.cpu().numpy()
+    return np.einsum(expr, *ops)         # host-only runs (the CPU test suite) and small arrays
+
+
 from .spaces import SplineSpace, basis_table, gauss_rule
 
 SINGULAR_REL_TOL = 1e-12
@@ -185,17 +202,24 @@ class FibreConductivity:
         = (sigma_l - sigma_t) ((div f) f_d + ((f . grad) f)_d), the fibre's physical derivatives from
         the map Hessian: d_a f = (d_a J_k - f (f . d_a J_k)) / |J_k|, df/dx_c = sum_a J^-1[a, c] d_a f.
         (The extension of stabilization.py:273-295 -- whose D is a scalar -- to the cfg-5 fibres.)"""
+        # numpy arrays (host restatement, tests) or torch tensors (the device indicator's setup: millions of
+        # Gauss points) -- the same formulas through either library
+        if _is_torch(jac):
+            import torch
+            es, eye = torch.einsum, torch.eye(jac.shape[-1], dtype=jac.dtype, device=jac.device)
+        else:
+            es, eye = _einsum, np.eye(jac.shape[-1])
         k = self.direction
         Jk = jac[..., :, k]
-        nrm = np.linalg.norm(Jk, axis=-1, keepdims=True)
+        nrm = (Jk * Jk).sum(-1)[..., None] ** 0.5
         f = Jk / nrm
-        D = self.sigma_t * np.eye(jac.shape[-1]) + (self.sigma_l - self.sigma_t) * (f[..., :, None] * f[..., None, :])
-        MD = np.einsum("...ac,...cd,...bd->...ab", jinv, D, jinv)
+        D = self.sigma_t * eye + (self.sigma_l - self.sigma_t) * (f[..., :, None] * f[..., None, :])
+        MD = es("...ac,...cd,...bd->...ab", jinv, D, jinv)
         dJk = hess[..., :, k, :]                                        # [a, c] = d_a d_k x_c
-        da_f = (dJk - f[..., None, :] * np.einsum("...ac,...c->...a", dJk, f)[..., :, None]) / nrm[..., None]
-        dfdx = np.einsum("...ac,...ad->...cd", jinv, da_f)             # [c, d] = d f_d / d x_c
-        divf = np.einsum("...cc->...", dfdx)
-        fgradf = np.einsum("...c,...cd->...d", f, dfdx)
+        da_f = (dJk - f[..., None, :] * es("...ac,...c->...a", dJk, f)[..., :, None]) / nrm[..., None]
+        dfdx = es("...ac,...ad->...cd", jinv, da_f)                    # [c, d] = d f_d / d x_c
+        divf = es("...cc->...", dfdx)
+        fgradf = es("...c,...cd->...d", f, dfdx)
         divD = (self.sigma_l - self.sigma_t) * (divf[..., None] * f + fgradf)
         return MD, divD
 

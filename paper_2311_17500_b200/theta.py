@@ -233,23 +233,26 @@ class MappedDeviceIndicator(DeviceIndicator):
         self.sB = [[torch.tensor(np.asarray(t), device=dev) for t in tl] for tl in g.sB]
         # per spatial Gauss point: cg_i = -sum_ab m_ab sum_c H_abc (J^-1)_ic, cm_ab = m_ab (x2 off-diagonal)
         gdat = sd.geo.grid_data([r[0] for r in sd.rules], order=2)
-        hess = gdat["hess"]
-        jinv = sd.jinv
-        hj = np.einsum("...abc,...ic->...abi", hess, jinv)
+        # (on the device: per-point 3 x 3 x 3 contractions over every spatial Gauss point)
         from .geometry import is_fibre
+        hess = torch.as_tensor(np.ascontiguousarray(gdat["hess"]), device=dev)
+        jinv = torch.as_tensor(np.ascontiguousarray(sd.jinv), device=dev)
+        hj = torch.einsum("...abc,...ic->...abi", hess, jinv)
         if is_fibre(problem.D):
             # div(D grad u) with the fibre tensor: the metric J^-1 D J^-T and the first-order term of div D
-            metric, divD = problem.D.diffusion_coefficients(gdat["jac"], hess, jinv)
-            coef = [(-np.einsum("...ab,...abi->...i", metric, hj) + np.einsum("...d,...id->...i", divD, jinv))[..., i]
-                    for i in range(d)]
+            jac = torch.as_tensor(np.ascontiguousarray(gdat["jac"]), device=dev)
+            metric, divD = problem.D.diffusion_coefficients(jac, hess, jinv)
+            cg = -torch.einsum("...ab,...abi->...i", metric, hj) + torch.einsum("...d,...id->...i", divD, jinv)
             self.diff = 1.0
         else:
-            metric = np.einsum("...ak,...bk->...ab", jinv, jinv)
-            coef = [-np.einsum("...ab,...abi->...i", metric, hj)[..., i] for i in range(d)]
+            metric = torch.einsum("...ak,...bk->...ab", jinv, jinv)
+            cg = -torch.einsum("...ab,...abi->...i", metric, hj)
             self.diff = float(problem.D)
         self.pairs = [(a, a) for a in range(d)] + [(a, b) for a in range(d) for b in range(a + 1, d)]
+        coef = [cg[..., i] for i in range(d)]
         coef += [metric[..., a, b] * (1.0 if a == b else 2.0) for a, b in self.pairs]
-        self.coef = torch.tensor(np.ascontiguousarray(np.stack([c.reshape(-1) for c in coef])), device=dev)
+        self.coef = torch.stack([c.reshape(-1) for c in coef]).contiguous()
+        del hess, jinv, hj, metric, cg
         self.G = np.asarray([x.size for x in g.sx], dtype=np.int32)
         self.q = st.spatial[0].degree + 1
         if any(s.degree + 1 != self.q for s in st.spatial):
