@@ -86,6 +86,13 @@ struct RxWS {
   static constexpr int XI_U = (XI_T + NPW - 1) / NPW, YI_U = (YI_T + NPW - 1) / NPW;
   static constexpr int YP_U = (YP_T + NPW - 1) / NPW, XP_U = (XP_T + NPW - 1) / NPW;
   static constexpr int NIT = (LS + NPT - 1) / NPT;                      // input positions per producer thread
+  // the unpredicated operand loads of padded rows / k columns stay inside the shared-memory carve-up
+  static_assert(SIN + (XI_T * 8 - 1) * IS1 + R1 + 3 < 2 * SIN + SA, "x interpolation over-read");
+  static_assert((((YI_T * 8 - 1) / Q1) * L2 + 4 * (KY - 1) + 3) * Q1 + Q1 - 1 < SA + SB, "y interpolation over-read");
+  static_assert(((NF - 1) * L3 + R1 + 3) * BJ + MIQ2 * BS1 * (MT - 1) + (Q2 - 1) * BS1 + Q1 - 1 < SB + SC,
+                "z interpolation over-read");
+  static_assert(((YP_T * 8 - 1) / Q1) * CS + (4 * (KYP - 1) + 3) * Q1 + Q1 - 1 < SC + SD, "y projection over-read");
+  static_assert((XP_T * 8 - 1) * DS1 + 4 * (KXP - 1) + 3 < SD, "x projection over-read");
 };
 
 #ifndef MI_RXWS_REGC
