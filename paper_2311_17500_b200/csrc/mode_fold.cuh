@@ -21,7 +21,7 @@
 // holds g_a[k]).
 //
 // One block per SM, warp-specialised over a ring of three panel buffers:
-// 4 producer warps load tile j+2 (cp.async, completion on the buffer's
+// 2 (n > 80) or 8 producer warps load tile j+2 (cp.async, completion on the buffer's
 // mbarrier) and store tile j (coalesced rows) while 8 consumer warps run the
 // DMMAs of tile j+1.  Each consumer warp owns 8 columns (rows) of the panel
 // and writes its results back over them in place, so the store of a tile
@@ -38,14 +38,17 @@
 #include "ptx.cuh"
 
 #ifndef MI_MF_NPW
-#define MI_MF_NPW 8
+#define MI_MF_NPW 0    // > 0: fixed number of producer warps (timing experiments)
 #endif
 
 namespace mi {
 
 template <int TH>
 struct ModeFold {
-  static constexpr int NCW = 8, NPW = MI_MF_NPW;    // consumer / producer warps
+  // consumer / producer warps.  The producers' 8-byte copies share the MIO queue with the consumers'
+  // operand loads: at n = 99 (TH = 7) two producer warps keep up and beat 4 / 8 / 12 (pc_spatial 5.57 /
+  // 5.70 / 5.94 / 6.91 ms at cfg 4); the shorter DMMA phase of smaller n needs the copies done faster
+  static constexpr int NCW = 8, NPW = MI_MF_NPW > 0 ? MI_MF_NPW : (TH >= 7 ? 2 : 8);
   static constexpr int NTH = 32 * (NCW + NPW);
   static constexpr int NPT = 32 * NPW;              // producer threads
   static constexpr int NB = 3;                      // panel ring
