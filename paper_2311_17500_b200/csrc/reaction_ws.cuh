@@ -83,9 +83,16 @@ struct RxWS {
   // tiles of the producer stages
   static constexpr int XI_T = (NF * L3 * L2 + 7) / 8, YI_T = (NF * L3 * Q1 + 7) / 8;
   static constexpr int YP_T = (L3 * Q1 + 7) / 8, XP_T = (L3 * L2 + 7) / 8;
-  static constexpr int XI_U = (XI_T + NPW - 1) / NPW, YI_U = (YI_T + NPW - 1) / NPW;
-  static constexpr int YP_U = (YP_T + NPW - 1) / NPW, XP_U = (XP_T + NPW - 1) / NPW;
-  static constexpr int NIT = (LS + NPT - 1) / NPT;                      // input positions per producer thread
+  // The producers split into an INTERPOLATION group (loads, x / y interpolation of the next slice) and a
+  // PROJECTION group (y / x projection of a finished function, the reductions into y), each with its own
+  // named barrier: their per-slice chains run side by side instead of one after the other (at p = 2 the
+  // chain, not the FP64 pipe, bounds the kernel).  RX_PRE has nothing to project.
+  static constexpr int NPP = MODE == RX_PRE ? 0 : (NPW >= 6 ? 3 : 1);
+  static constexpr int NPI = NPW - NPP, NIT_T = 32 * NPI, NPR_T = 32 * (NPP > 0 ? NPP : NPW);
+  static constexpr int NPJ = NPP > 0 ? NPP : NPW;                       // warps that project
+  static constexpr int XI_U = (XI_T + NPI - 1) / NPI, YI_U = (YI_T + NPI - 1) / NPI;
+  static constexpr int YP_U = (YP_T + NPJ - 1) / NPJ, XP_U = (XP_T + NPJ - 1) / NPJ;
+  static constexpr int NIT = (LS + NIT_T - 1) / NIT_T;                  // input positions per interpolation thread
   // the unpredicated operand loads of padded rows / k columns stay inside the shared-memory carve-up
   static_assert(SIN + (XI_T * 8 - 1) * IS1 + R1 + 3 < 2 * SIN + SA, "x interpolation over-read");
   static_assert((((YI_T * 8 - 1) / Q1) * L2 + 4 * (KY - 1) + 3) * Q1 + Q1 - 1 < SA + SB, "y interpolation over-read");
@@ -115,9 +122,9 @@ __device__ __forceinline__ void rxws_pdmma(double& c0, double& c1, double a, dou
 __device__ __forceinline__ void rxws_cdmma(double& c0, double& c1, double a, double b) {
   if (MI_RXWS_ABL & 4) { c0 += a; c1 += b; } else dmma(c0, c1, a, b);
 }
-template <int NPT>
-__device__ __forceinline__ void rxws_bar_producers() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(NPT) : "memory");
+template <int ID, int NT>
+__device__ __forceinline__ void rxws_bar_group() {
+  asm volatile("bar.sync %0, %1;\n" ::"n"(ID), "n"(NT) : "memory");
 }
 
 template <int P_, int MODE>
@@ -144,10 +151,10 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
   for (int i = tid; i < G::NDBL; i += G::NTH) sm[i] = 0.0;
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&fullB[b], G::NPT);
+      mbar_init(&fullB[b], G::NIT_T);
       mbar_init(&emptyB[b], G::NCT);
       mbar_init(&fullC[b], G::NCT);
-      mbar_init(&emptyC[b], G::NPT);
+      mbar_init(&emptyC[b], G::NPR_T);
     }
     if constexpr (MODE == RX_STORED) {
       for (int b = 0; b < G::NSW; ++b) {
@@ -421,21 +428,7 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
   } else {
     // =========================== producers ===========================
     if constexpr (G::REGSPLIT) rxws_reg_dec<MI_RXWS_REGP>();
-    constexpr int NPW = G::NPW, NPT = G::NPT;
-    const int p = tid - G::NCT, pw = warp - G::NCW;
-    double bIy[G::NY][G::KY], bPy[G::NYP][G::KYP], bPx[G::KXP];
-    const double bIx1 = basis(0, R1 + fk, fr);
-    const double bIx0[2] = {R1 ? basis(0, 0, 2 * fk) : 0.0, R1 ? basis(0, 0, 2 * fk + 1) : 0.0};
-#pragma unroll
-    for (int ks = 0; ks < G::KXP; ++ks) bPx[ks] = basis(0, fr, 4 * ks + fk);
-#pragma unroll
-    for (int ks = 0; ks < G::KY; ++ks)
-#pragma unroll
-      for (int n2 = 0; n2 < G::NY; ++n2) bIy[n2][ks] = basis(1, 4 * ks + fk, 8 * n2 + fr);
-#pragma unroll
-    for (int ks = 0; ks < G::KYP; ++ks)
-#pragma unroll
-      for (int n2 = 0; n2 < G::NYP; ++n2) bPy[n2][ks] = basis(1, 8 * n2 + fr, 4 * ks + fk);
+    const int pw = warp - G::NCW;
     const long long ns = r.ns;
     // spatial indices fit in 32 bits (the launcher checks N_s < 2^31)
     auto spatial = [&](int j3, int j2, int j1, bool& ok) -> int {
@@ -443,221 +436,244 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
       ok = g1 < r.n[0] && g2 < r.n[1] && g3 < r.n[2];
       return (g3 * r.n[1] + g2) * r.n[0] + g1;
     };
-    // Input slice items of this thread: spatial positions s = p + NPT h (s < LS) of all three fields.
-    // The slice is copied asynchronously (cp.async, zeros for padding / constrained rows) straight into
-    // the double-buffered sIn: no register staging, and no global-load scoreboard in front of the
-    // x-interpolation DMMAs.
-    int gsp[G::NIT];                                 // global spatial index (-1: outside the domain, -2: no item)
-    unsigned sdst[G::NIT];                           // shared address of the field-0 copy in buffer 0
+    if (pw < G::NPI) {
+      // ----------------- interpolation group: loads, x and y interpolation of slice i -----------------
+      constexpr int NPI = G::NPI, NT_ = G::NIT_T;
+      const int p = tid - G::NCT;
+      double bIy[G::NY][G::KY];
+      const double bIx1 = basis(0, R1 + fk, fr);
+      const double bIx0[2] = {R1 ? basis(0, 0, 2 * fk) : 0.0, R1 ? basis(0, 0, 2 * fk + 1) : 0.0};
 #pragma unroll
-    for (int h = 0; h < G::NIT; ++h) {
-      const int sp = p + NPT * h;
-      const int j3 = sp / (L1 * L2), j2 = (sp / L1) % L2, j1 = sp % L1;
-      bool ok;
-      const int gs = spatial(j3, j2, j1, ok);
-      gsp[h] = sp < G::LS ? (ok ? gs : -1) : -2;
-      sdst[h] = (unsigned)__cvta_generic_to_shared(sIn + (sp < G::LS ? (j3 * L2 + j2) * IS1 + j1 : 0));
-    }
-    auto put = [&](unsigned dst, const double* src, bool valid) {   // one double: async copy, or a zero
-      if (valid)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
-      else
-        asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0) : "memory");
-    };
-    auto issue = [&](int ft) {
-      const int ct = ft + r.rowoff;
-      const unsigned boff = (unsigned)((ft & 1) * G::SIN * 8);
-      constexpr unsigned FO = L3 * L2 * IS1 * 8;     // field stride in sIn (bytes)
-      // fields of this mode: fused (u, w, x), pre (u, w), stored (x)
-      const double* fld[3] = {MODE == RX_STORED ? r.x : r.u, r.w, r.x};
-      const double* lft[3] = {MODE == RX_STORED ? r.lift_x : r.lift_u, nullptr, r.lift_x};
-      if (ct >= 0 && ct < r.ntc) {
-        const long long off = (long long)ct * ns;
+      for (int ks = 0; ks < G::KY; ++ks)
 #pragma unroll
-        for (int h = 0; h < G::NIT; ++h) {
-          if (gsp[h] != -2) {
-            const bool v = gsp[h] >= 0;
-            const int g = v ? gsp[h] : 0;
-            const unsigned d = sdst[h] + boff;
+        for (int n2 = 0; n2 < G::NY; ++n2) bIy[n2][ks] = basis(1, 4 * ks + fk, 8 * n2 + fr);
+      // Input slice items of this thread: spatial positions s = p + NT_ h (s < LS) of all the mode's fields.
+      // The slice is copied asynchronously (cp.async, zeros for padding / constrained rows) straight into
+      // the double-buffered sIn: no register staging, and no global-load scoreboard in front of the
+      // x-interpolation DMMAs.
+      int gsp[G::NIT];                               // global spatial index (-1: outside the domain, -2: no item)
+      unsigned sdst[G::NIT];                         // shared address of the field-0 copy in buffer 0
 #pragma unroll
-            for (int f = 0; f < NF; ++f) put(d + f * FO, fld[f] + off + g, v);
-          }
-        }
-      } else {
-        // the lifted slab (row -1: u and x from the lift, if set) or a row outside this context: zeros
+      for (int h = 0; h < G::NIT; ++h) {
+        const int sp = p + NT_ * h;
+        const int j3 = sp / (L1 * L2), j2 = (sp / L1) % L2, j1 = sp % L1;
+        bool ok;
+        const int gs = spatial(j3, j2, j1, ok);
+        gsp[h] = sp < G::LS ? (ok ? gs : -1) : -2;
+        sdst[h] = (unsigned)__cvta_generic_to_shared(sIn + (sp < G::LS ? (j3 * L2 + j2) * IS1 + j1 : 0));
+      }
+      auto put = [&](unsigned dst, const double* src, bool valid) {   // one double: async copy, or a zero
+        if (valid)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+        else
+          asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0) : "memory");
+      };
+      auto issue = [&](int ft) {
+        const int ct = ft + r.rowoff;
+        const unsigned boff = (unsigned)((ft & 1) * G::SIN * 8);
+        constexpr unsigned FO = L3 * L2 * IS1 * 8;   // field stride in sIn (bytes)
+        // fields of this mode: fused (u, w, x), pre (u, w), stored (x)
+        const double* fld[3] = {MODE == RX_STORED ? r.x : r.u, r.w, r.x};
+        const double* lft[3] = {MODE == RX_STORED ? r.lift_x : r.lift_u, nullptr, r.lift_x};
+        if (ct >= 0 && ct < r.ntc) {
+          const long long off = (long long)ct * ns;
 #pragma unroll
-        for (int h = 0; h < G::NIT; ++h) {
-          if (gsp[h] != -2) {
-            const bool v = gsp[h] >= 0;
-            const int g = v ? gsp[h] : 0;
-            const unsigned d = sdst[h] + boff;
+          for (int h = 0; h < G::NIT; ++h) {
+            if (gsp[h] != -2) {
+              const bool v = gsp[h] >= 0;
+              const int g = v ? gsp[h] : 0;
+              const unsigned d = sdst[h] + boff;
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const double* l = ct == -1 ? lft[f] : nullptr;
-              put(d + f * FO, l + g, v && l != nullptr);
+              for (int f = 0; f < NF; ++f) put(d + f * FO, fld[f] + off + g, v);
             }
           }
-        }
-      }
-      cp_async_commit();
-    };
-    // x-projection outputs of this thread: line tiles mt = pw + NPW u, xline = 8 mt + fr = (j3, j2), j1 = 2 fk + e
-    int yidx[G::XP_U][2];
+        } else {
+          // the lifted slab (row -1: u and x from the lift, if set) or a row outside this context: zeros
 #pragma unroll
-    for (int u = 0; u < G::XP_U; ++u)
+          for (int h = 0; h < G::NIT; ++h) {
+            if (gsp[h] != -2) {
+              const bool v = gsp[h] >= 0;
+              const int g = v ? gsp[h] : 0;
+              const unsigned d = sdst[h] + boff;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int xline = 8 * (pw + NPW * u) + fr, j1 = 2 * fk + e;
-        bool ok = false;
-        int gs = 0;
-        if (xline < L3 * L2 && j1 < L1) gs = spatial(xline / L2, xline % L2, j1, ok);
-        yidx[u][e] = ok ? gs : -1;
-      }
-    issue(0);
-    [[maybe_unused]] int e_next = 0;                 // RX_STORED: next c_w block to request
-    for (int i = 0; i <= nfull + PW + 1; ++i) {
-      if constexpr (MODE == RX_STORED) {
-        // c_w blocks NSW - 1 elements ahead of the consumers (who are on element i - 1 - PW); a stage is
-        // free once they have read element e - NSW, which they did steps ago
-        if (p == 0) {
-          for (; e_next < nelt && e_next <= i - PW + G::NSW - 2; ++e_next) {
-            const int sw = e_next % G::NSW, kuse = e_next / G::NSW;
-            if (kuse >= 1) mbar_wait(&emptyW[sw], (unsigned)((kuse - 1) & 1));
-            mbar_expect_tx(&fullW[sw], (unsigned)(G::CWB * 8));
-            bulk_g2s(sW + sw * G::CWB, r.cw + (cw_tile + e_next) * (long long)G::CWB, (unsigned)(G::CWB * 8), &fullW[sw]);
-          }
-        }
-      }
-      const bool has_in = i < nfull;
-      const int fq = i - PW - 2;                     // function whose y / x projections run now (its z
-                                                     // projection ended with consumer step i - 1)
-      const bool has_fq = MODE != RX_PRE && fq >= 0 && fq < nfull;
-      cp_async_wait<0>();                            // this thread's copies of slice i have landed ...
-      rxws_bar_producers<NPT>();                     // ... and everyone's; the other sIn buffer is free
-      if (i + 1 < nfull) issue(i + 1);
-      if (has_in) {
-        const double* sI = sIn + (i & 1) * G::SIN;
-        // x interpolation of slice i: lines (fld, j3, j2), K = j1, N = q1 -> sA.  The last 4 functions in
-        // ONE DMMA, a leading one (first element's Gauss points only) as a rank-1 update
-        constexpr int NL = NF * L3 * L2;
-        double c[G::XI_U][2], a0[G::XI_U];
-#pragma unroll
-        for (int u = 0; u < G::XI_U; ++u) {
-          c[u][0] = c[u][1] = 0.0;
-          a0[u] = 0.0;
-          const int mt = pw + NPW * u;
-          if (mt < G::XI_T) {
-            const double* row = sI + (mt * 8 + fr) * IS1;
-            if (R1) a0[u] = row[0];
-            rxws_pdmma(c[u][0], c[u][1], row[R1 + fk], bIx1);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < G::XI_U; ++u) {
-          const int line = (pw + NPW * u) * 8 + fr;
-          if (line < NL && 2 * fk < Q1)
-            *reinterpret_cast<double2*>(sA + line * Q1 + 2 * fk) =
-                make_double2(fma(a0[u], bIx0[0], c[u][0]), fma(a0[u], bIx0[1], c[u][1]));
-        }
-      }
-      rxws_bar_producers<NPT>();
-      if (has_in) {
-        // y interpolation of slice i: lines (fld j3, q1), K = j2, N = q2 -> sB[i & 1]
-        const int bb = i & 1;
-        constexpr int NL = NF * L3 * Q1;
-        double* out = sB + bb * G::SB;
-#pragma unroll
-        for (int h = 0; h < (G::YI_U + 1) / 2; ++h) {   // two line tiles at a time (register budget)
-          double c[2][G::NY][2];
-          int fj3[2], q1[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-#pragma unroll
-            for (int n2 = 0; n2 < G::NY; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
-            const int mt = pw + NPW * (2 * h + u), line = mt * 8 + fr;
-            fj3[u] = Q1 == 8 ? mt : line / Q1, q1[u] = Q1 == 8 ? fr : line % Q1;
-            if (2 * h + u < G::YI_U && mt < G::YI_T) {
-#pragma unroll
-              for (int ks = 0; ks < G::KY; ++ks) {
-                const double av = sA[(fj3[u] * L2 + 4 * ks + fk) * Q1 + q1[u]];
-#pragma unroll
-                for (int n2 = 0; n2 < G::NY; ++n2) rxws_pdmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
+              for (int f = 0; f < NF; ++f) {
+                const double* l = ct == -1 ? lft[f] : nullptr;
+                put(d + f * FO, l + g, v && l != nullptr);
               }
             }
           }
-          if (h == 0 && i >= 2) mbar_wait(&emptyB[bb], (unsigned)(((i >> 1) - 1) & 1));
+        }
+        cp_async_commit();
+      };
+      issue(0);
+      [[maybe_unused]] int e_next = 0;               // RX_STORED: next c_w block to request
+      for (int i = 0; i < nfull; ++i) {
+        if constexpr (MODE == RX_STORED) {
+          // c_w blocks NSW - 1 elements ahead of the consumers (who are on element i - 1 - PW); a stage is
+          // free once they have read element e - NSW, which they did steps ago
+          if (p == 0) {
+            for (; e_next < nelt && e_next <= i - PW + G::NSW - 2; ++e_next) {
+              const int sw = e_next % G::NSW, kuse = e_next / G::NSW;
+              if (kuse >= 1) mbar_wait(&emptyW[sw], (unsigned)((kuse - 1) & 1));
+              mbar_expect_tx(&fullW[sw], (unsigned)(G::CWB * 8));
+              bulk_g2s(sW + sw * G::CWB, r.cw + (cw_tile + e_next) * (long long)G::CWB, (unsigned)(G::CWB * 8),
+                       &fullW[sw]);
+            }
+          }
+        }
+        cp_async_wait<0>();                          // this thread's copies of slice i have landed ...
+        rxws_bar_group<1, NT_>();                    // ... and everyone's; the other sIn buffer is free
+        if (i + 1 < nfull) issue(i + 1);
+        {
+          const double* sI = sIn + (i & 1) * G::SIN;
+          // x interpolation of slice i: lines (fld, j3, j2), K = j1, N = q1 -> sA.  The last 4 functions in
+          // ONE DMMA, a leading one (first element's Gauss points only) as a rank-1 update
+          constexpr int NL = NF * L3 * L2;
+          double c[G::XI_U][2], a0[G::XI_U];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int mt = pw + NPW * (2 * h + u), line = mt * 8 + fr;
-            if (2 * h + u < G::YI_U && line < NL) {
+          for (int u = 0; u < G::XI_U; ++u) {
+            c[u][0] = c[u][1] = 0.0;
+            a0[u] = 0.0;
+            const int mt = pw + NPI * u;
+            if (mt < G::XI_T) {
+              const double* row = sI + (mt * 8 + fr) * IS1;
+              if (R1) a0[u] = row[0];
+              rxws_pdmma(c[u][0], c[u][1], row[R1 + fk], bIx1);
+            }
+          }
 #pragma unroll
-              for (int n2 = 0; n2 < G::NY; ++n2) {
+          for (int u = 0; u < G::XI_U; ++u) {
+            const int line = (pw + NPI * u) * 8 + fr;
+            if (line < NL && 2 * fk < Q1)
+              *reinterpret_cast<double2*>(sA + line * Q1 + 2 * fk) =
+                  make_double2(fma(a0[u], bIx0[0], c[u][0]), fma(a0[u], bIx0[1], c[u][1]));
+          }
+        }
+        rxws_bar_group<1, NT_>();
+        {
+          // y interpolation of slice i: lines (fld j3, q1), K = j2, N = q2 -> sB[i & 1]
+          const int bb = i & 1;
+          constexpr int NL = NF * L3 * Q1;
+          double* out = sB + bb * G::SB;
+#pragma unroll
+          for (int h = 0; h < (G::YI_U + 1) / 2; ++h) {   // two line tiles at a time (register budget)
+            double c[2][G::NY][2];
+            int fj3[2], q1[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+#pragma unroll
+              for (int n2 = 0; n2 < G::NY; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
+              const int mt = pw + NPI * (2 * h + u), line = mt * 8 + fr;
+              fj3[u] = Q1 == 8 ? mt : line / Q1, q1[u] = Q1 == 8 ? fr : line % Q1;
+              if (2 * h + u < G::YI_U && mt < G::YI_T) {
+#pragma unroll
+                for (int ks = 0; ks < G::KY; ++ks) {
+                  const double av = sA[(fj3[u] * L2 + 4 * ks + fk) * Q1 + q1[u]];
+#pragma unroll
+                  for (int n2 = 0; n2 < G::NY; ++n2) rxws_pdmma(c[u][n2][0], c[u][n2][1], av, bIy[n2][ks]);
+                }
+              }
+            }
+            if (h == 0 && i >= 2) mbar_wait(&emptyB[bb], (unsigned)(((i >> 1) - 1) & 1));
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int mt = pw + NPI * (2 * h + u), line = mt * 8 + fr;
+              if (2 * h + u < G::YI_U && line < NL) {
+#pragma unroll
+                for (int n2 = 0; n2 < G::NY; ++n2) {
+                  const int n0 = 8 * n2 + 2 * fk;
+                  if (n0 < Q2) out[fj3[u] * BJ + n0 * BS1 + q1[u]] = c[u][n2][0];
+                  if (n0 + 1 < Q2) out[fj3[u] * BJ + (n0 + 1) * BS1 + q1[u]] = c[u][n2][1];
+                }
+              }
+            }
+          }
+          mbar_arrive(&fullB[bb]);
+        }
+      }
+    } else if constexpr (G::NPP > 0) {
+      // ----------------- projection group: y and x projection of function fq, reductions into y -----------------
+      constexpr int NPP = G::NPP, NT_ = G::NPR_T;
+      const int pp = pw - G::NPI;
+      double bPy[G::NYP][G::KYP], bPx[G::KXP];
+#pragma unroll
+      for (int ks = 0; ks < G::KXP; ++ks) bPx[ks] = basis(0, fr, 4 * ks + fk);
+#pragma unroll
+      for (int ks = 0; ks < G::KYP; ++ks)
+#pragma unroll
+        for (int n2 = 0; n2 < G::NYP; ++n2) bPy[n2][ks] = basis(1, 8 * n2 + fr, 4 * ks + fk);
+      // x-projection outputs of this thread: line tiles mt = pp + NPP u, xline = 8 mt + fr = (j3, j2), j1 = 2 fk + e
+      int yidx[G::XP_U][2];
+#pragma unroll
+      for (int u = 0; u < G::XP_U; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int xline = 8 * (pp + NPP * u) + fr, j1 = 2 * fk + e;
+          bool ok = false;
+          int gs = 0;
+          if (xline < L3 * L2 && j1 < L1) gs = spatial(xline / L2, xline % L2, j1, ok);
+          yidx[u][e] = ok ? gs : -1;
+        }
+      for (int fq = 0; fq < nfull; ++fq) {
+        {
+          // y projection of function fq: lines (j3, q1), K = q2, N = j2: sC[fq & 1] -> sD
+          const int cb = fq & 1;
+          mbar_wait(&fullC[cb], (unsigned)((fq >> 1) & 1));
+          const double* in = sC + cb * G::SC;
+          constexpr int NL = L3 * Q1;
+          double c[G::YP_U][G::NYP][2];
+          int j3[G::YP_U], q1[G::YP_U];
+#pragma unroll
+          for (int u = 0; u < G::YP_U; ++u) {
+#pragma unroll
+            for (int n2 = 0; n2 < G::NYP; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
+            const int mt = pp + NPP * u, line = 8 * mt + fr;
+            j3[u] = Q1 == 8 ? mt : line / Q1, q1[u] = Q1 == 8 ? fr : line % Q1;
+            if (mt < G::YP_T) {
+#pragma unroll
+              for (int ks = 0; ks < G::KYP; ++ks) {
+                const double av = in[j3[u] * CS + (4 * ks + fk) * Q1 + q1[u]];
+#pragma unroll
+                for (int n2 = 0; n2 < G::NYP; ++n2) rxws_pdmma(c[u][n2][0], c[u][n2][1], av, bPy[n2][ks]);
+              }
+            }
+          }
+          mbar_arrive(&emptyC[cb]);
+#pragma unroll
+          for (int u = 0; u < G::YP_U; ++u) {
+            const int line = 8 * (pp + NPP * u) + fr;
+            if (line < NL) {
+#pragma unroll
+              for (int n2 = 0; n2 < G::NYP; ++n2) {
                 const int n0 = 8 * n2 + 2 * fk;
-                if (n0 < Q2) out[fj3[u] * BJ + n0 * BS1 + q1[u]] = c[u][n2][0];
-                if (n0 + 1 < Q2) out[fj3[u] * BJ + (n0 + 1) * BS1 + q1[u]] = c[u][n2][1];
+                if (n0 < L2) sD[(j3[u] * L2 + n0) * DS1 + q1[u]] = c[u][n2][0];
+                if (n0 + 1 < L2) sD[(j3[u] * L2 + n0 + 1) * DS1 + q1[u]] = c[u][n2][1];
               }
             }
           }
         }
-        mbar_arrive(&fullB[bb]);
-      }
-      if (has_fq) {
-        // y projection of function fq: lines (j3, q1), K = q2, N = j2: sC[fq & 1] -> sD
-        const int cb = fq & 1;
-        mbar_wait(&fullC[cb], (unsigned)((fq >> 1) & 1));
-        const double* in = sC + cb * G::SC;
-        constexpr int NL = L3 * Q1;
-        double c[G::YP_U][G::NYP][2];
-        int j3[G::YP_U], q1[G::YP_U];
+        rxws_bar_group<2, NT_>();
+        {
+          // x projection of function fq: lines (j3, j2), K = q1, N = j1 -> y (fire-and-forget reductions:
+          // one writer per y entry per colour launch, stream-ordered launches: deterministic)
+          const int ct = fq + r.rowoff;
+          const long long row = (ct >= 0 && ct < r.ntc) ? (long long)ct * ns : -1;
 #pragma unroll
-        for (int u = 0; u < G::YP_U; ++u) {
+          for (int u = 0; u < G::XP_U; ++u) {
+            const int mt = pp + NPP * u;
+            if (mt < G::XP_T) {
+              const int xline = 8 * mt + fr;
+              double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int n2 = 0; n2 < G::NYP; ++n2) c[u][n2][0] = c[u][n2][1] = 0.0;
-          const int mt = pw + NPW * u, line = 8 * mt + fr;
-          j3[u] = Q1 == 8 ? mt : line / Q1, q1[u] = Q1 == 8 ? fr : line % Q1;
-          if (mt < G::YP_T) {
-#pragma unroll
-            for (int ks = 0; ks < G::KYP; ++ks) {
-              const double av = in[j3[u] * CS + (4 * ks + fk) * Q1 + q1[u]];
-#pragma unroll
-              for (int n2 = 0; n2 < G::NYP; ++n2) rxws_pdmma(c[u][n2][0], c[u][n2][1], av, bPy[n2][ks]);
+              for (int ks = 0; ks < G::KXP; ++ks) rxws_pdmma(c0, c1, sD[xline * DS1 + 4 * ks + fk], bPx[ks]);
+              if (row >= 0) {
+                if (yidx[u][0] >= 0) atomicAdd(r.y + row + yidx[u][0], c0);
+                if (yidx[u][1] >= 0) atomicAdd(r.y + row + yidx[u][1], c1);
+              }
             }
           }
         }
-        mbar_arrive(&emptyC[cb]);
-#pragma unroll
-        for (int u = 0; u < G::YP_U; ++u) {
-          const int line = 8 * (pw + NPW * u) + fr;
-          if (line < NL) {
-#pragma unroll
-            for (int n2 = 0; n2 < G::NYP; ++n2) {
-              const int n0 = 8 * n2 + 2 * fk;
-              if (n0 < L2) sD[(j3[u] * L2 + n0) * DS1 + q1[u]] = c[u][n2][0];
-              if (n0 + 1 < L2) sD[(j3[u] * L2 + n0 + 1) * DS1 + q1[u]] = c[u][n2][1];
-            }
-          }
-        }
-      }
-      rxws_bar_producers<NPT>();
-      if (has_fq) {
-        // x projection of function fq: lines (j3, j2), K = q1, N = j1 -> y (fire-and-forget reductions:
-        // one writer per y entry per colour launch, stream-ordered launches: deterministic)
-        const int ct = fq + r.rowoff;
-        const long long row = (ct >= 0 && ct < r.ntc) ? (long long)ct * ns : -1;
-#pragma unroll
-        for (int u = 0; u < G::XP_U; ++u) {
-          const int mt = pw + NPW * u;
-          if (mt < G::XP_T) {
-            const int xline = 8 * mt + fr;
-            double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < G::KXP; ++ks) rxws_pdmma(c0, c1, sD[xline * DS1 + 4 * ks + fk], bPx[ks]);
-            if (row >= 0) {
-              if (yidx[u][0] >= 0) atomicAdd(r.y + row + yidx[u][0], c0);
-              if (yidx[u][1] >= 0) atomicAdd(r.y + row + yidx[u][1], c1);
-            }
-          }
-        }
+        rxws_bar_group<2, NT_>();                    // sD is free for the next function
       }
     }
   }
