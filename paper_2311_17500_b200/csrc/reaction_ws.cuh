@@ -19,6 +19,9 @@
 // writer per launch, as in reaction_tile: deterministic sums.
 #pragma once
 
+#ifndef MI_RXWS_NPP
+#define MI_RXWS_NPP 0      // > 0: projection warps (timing experiments)
+#endif
 #ifndef MI_RXWS_ST6
 #define MI_RXWS_ST6 1
 #endif
@@ -87,7 +90,7 @@ struct RxWS {
   // PROJECTION group (y / x projection of a finished function, the reductions into y), each with its own
   // named barrier: their per-slice chains run side by side instead of one after the other (at p = 2 the
   // chain, not the FP64 pipe, bounds the kernel).  RX_PRE has nothing to project.
-  static constexpr int NPP = MODE == RX_PRE ? 0 : (NPW >= 6 ? 3 : 1);
+  static constexpr int NPP = MODE == RX_PRE ? 0 : (MI_RXWS_NPP > 0 ? MI_RXWS_NPP : (NPW >= 6 ? 2 : 1));
   static constexpr int NPI = NPW - NPP, NIT_T = 32 * NPI, NPR_T = 32 * (NPP > 0 ? NPP : NPW);
   static constexpr int NPJ = NPP > 0 ? NPP : NPW;                       // warps that project
   static constexpr int XI_U = (XI_T + NPI - 1) / NPI, YI_U = (YI_T + NPI - 1) / NPI;
