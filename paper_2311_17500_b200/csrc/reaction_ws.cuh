@@ -203,9 +203,12 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
   if (warp < G::NCW) {
     // =========================== consumers ===========================
     if constexpr (G::REGSPLIT) rxws_reg_inc<MI_RXWS_REGC>();   // the producers' released registers
-    double bP[G::KZP];
+    // z projection operand: B[k][n] = basis of function n at Gauss point q3 = 2 k + ks (the accumulator
+    // layout of the z interpolation: lane k of a quad owns q3 = 2 k and 2 k + 1)
+    static_assert(G::KZP <= 2, "z projection: two k-steps cover q3 = 2 k + ks < 8");
+    double bP[2];
 #pragma unroll
-    for (int ks = 0; ks < G::KZP; ++ks) bP[ks] = basis(2, fr, 4 * ks + fk);
+    for (int ks = 0; ks < 2; ++ks) bP[ks] = basis(2, fr, 2 * fk + ks);
     // z interpolation operands: the last 4 functions as the DMMA B fragment, a leading one (p = 3) at
     // this thread's two points
     const double bI1 = basis(2, R1 + fk, fr);
@@ -329,15 +332,12 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
           zc[mi][f][0] = zc[mi][f][1] = 0.0;
           rxws_cdmma(zc[mi][f][0], zc[mi][f][1], za[mi][f], bI1);
         }
+      // (the K order of this product is q3 = 2 k + ks: k-step ks takes every lane's OWN point e = ks, so
+      // the A fragments need no shuffles)
 #pragma unroll
-      for (int ks = 0; ks < (MODE == RX_PRE ? 0 : G::KZP); ++ks)
+      for (int ks = 0; ks < (MODE == RX_PRE ? 0 : 2); ++ks)
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi) {
-          const int cc = 4 * ks + fk, src = (lane & ~3) | ((cc >> 1) & 3);
-          const double v0 = __shfl_sync(0xffffffffu, yz[mi][0], src);
-          const double v1 = __shfl_sync(0xffffffffu, yz[mi][1], src);
-          rxws_cdmma(zp[mi][0], zp[mi][1], (cc & 1) ? v1 : v0, bP[ks]);
-        }
+        for (int mi = 0; mi < MT; ++mi) rxws_cdmma(zp[mi][0], zp[mi][1], yz[mi][ks], bP[ks]);
       // ---- time element et on the thread's own points, all chains interleaved
       if (!(MI_RXWS_ABL & 1)) {
 #pragma unroll
