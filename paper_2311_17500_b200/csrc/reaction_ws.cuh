@@ -106,10 +106,10 @@ struct RxWS {
 };
 
 #ifndef MI_RXWS_REGC
-#define MI_RXWS_REGC 208   // consumer registers after the split (256 x REGC + 128 x REGP <= 384 x 168)
+#define MI_RXWS_REGC 216   // consumer registers after the split (256 x REGC + 128 x REGP <= 384 x 168)
 #endif
 #ifndef MI_RXWS_REGP
-#define MI_RXWS_REGP 88
+#define MI_RXWS_REGP 72
 #endif
 #ifndef MI_RXWS_ABL
 #define MI_RXWS_ABL 0      // timing ablations (wrong results): 1 no time stage, 2 no producer DMMAs, 4 no z stages
