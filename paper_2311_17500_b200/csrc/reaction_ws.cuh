@@ -232,7 +232,6 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
         wsp[mi][e] = v;
       }
     }
-    const double rsq = sqrt(r.c1), rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;   // c1 >= 0 (launcher)
     double X[MT][PW][NF][2], Y[MT][PW][2];
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi)
@@ -389,25 +388,17 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
           }
         }
       }
-      // ---- the entering slice reaches its window slot as (sqrt(c1) u, p, w_x x) with
-      // p = c2 w - c1 (1 + a) u + c1 a, so that C_r = c1 (u - a)(u - 1) + c2 w = (sqrt(c1) u)^2 + p is ONE
-      // fused multiply-add per Gauss point; p is linear in the coefficients, and its constant rides
-      // along because the time basis sums to 1
+      // ---- the entering slice reaches its window slot: (sqrt(c1) u, p) arrive transformed by the
+      // producers; x takes its spatial weight here (stored mode: the weight is in c_w)
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double cf[NF];
+        for (int e = 0; e < 2; ++e)
 #pragma unroll
-          for (int f = 0; f < NF; ++f) cf[f] = R1 ? fma(a0[mi][f], bI0[e], zc[mi][f][e]) : zc[mi][f][e];
-          if constexpr (MODE == RX_STORED) {
-            X[mi][PH][0][e] = cf[0];                 // x alone: the weight is in c_w
-          } else {
-            X[mi][PH][0][e] = cf[0] * rsq;
-            X[mi][PH][1][e] = fma(cf[0], rk1, fma(cf[1], rc2, rk0));
-            if constexpr (MODE == RX_FUSED) X[mi][PH][2][e] = cf[2] * wsp[mi][e];
+          for (int f = 0; f < NF; ++f) {
+            const double cf = R1 ? fma(a0[mi][f], bI0[e], zc[mi][f][e]) : zc[mi][f][e];
+            X[mi][PH][f][e] = (MODE == RX_FUSED && f == 2) ? cf * wsp[mi][e] : cf;
           }
-        }
       // ---- projected function fz to the producers
       if (has_fz) {
         double* out = sC + cb * G::SC;
@@ -456,6 +447,7 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
       // x-interpolation DMMAs.
       int gsp[G::NIT];                               // global spatial index (-1: outside the domain, -2: no item)
       unsigned sdst[G::NIT];                         // shared address of the field-0 copy in buffer 0
+      int sof[G::NIT];                               // ... and its offset in sIn (doubles)
 #pragma unroll
       for (int h = 0; h < G::NIT; ++h) {
         const int sp = p + NT_ * h;
@@ -463,8 +455,15 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
         bool ok;
         const int gs = spatial(j3, j2, j1, ok);
         gsp[h] = sp < G::LS ? (ok ? gs : -1) : -2;
-        sdst[h] = (unsigned)__cvta_generic_to_shared(sIn + (sp < G::LS ? (j3 * L2 + j2) * IS1 + j1 : 0));
+        sof[h] = sp < G::LS ? (j3 * L2 + j2) * IS1 + j1 : 0;
+        sdst[h] = (unsigned)__cvta_generic_to_shared(sIn + sof[h]);
       }
+      // C_r = c1 (u - a)(u - 1) + c2 w = (sqrt(c1) u)^2 + p with p = c2 w - c1 (1 + a) u + c1 a LINEAR in
+      // the coefficients: every thread turns its own landed (u, w) items into (sqrt(c1) u, p) in place, so
+      // the consumers interpolate u' and p directly and form C_r with ONE fused multiply-add per Gauss
+      // point.  (The constant c1 a rides on the coefficients because the basis sums to 1 at every Gauss
+      // point in every direction; zero slabs and padding become p = c1 a, as C_r of u = w = 0 is.)
+      [[maybe_unused]] const double rsq = sqrt(r.c1), rk1 = -r.c1 * (1.0 + r.a), rk0 = r.c1 * r.a, rc2 = r.c2;
       auto put = [&](unsigned dst, const double* src, bool valid) {   // one double: async copy, or a zero
         if (valid)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
@@ -525,6 +524,17 @@ __global__ void __launch_bounds__(RxWS<P_, MODE>::NTH, 1) reaction_ws(RxArgs r) 
           }
         }
         cp_async_wait<0>();                          // this thread's copies of slice i have landed ...
+        if constexpr (MODE != RX_STORED) {
+          double* sI = sIn + (i & 1) * G::SIN;
+#pragma unroll
+          for (int h = 0; h < G::NIT; ++h) {
+            if (gsp[h] != -2) {
+              const double uv = sI[sof[h]], wv = sI[sof[h] + L3 * L2 * IS1];
+              sI[sof[h]] = uv * rsq;
+              sI[sof[h] + L3 * L2 * IS1] = fma(uv, rk1, fma(wv, rc2, rk0));
+            }
+          }
+        }
         rxws_bar_group<1, NT_>();                    // ... and everyone's; the other sIn buffer is free
         if (i + 1 < nfull) issue(i + 1);
         {
